@@ -1,0 +1,177 @@
+"""Cheetah coefficient packing for HE convolution -- oracle side (test infrastructure only).
+
+The paper states the property, not the formulas: Cheetah "encodes messages directly into
+the coefficients of the polynomials ... placed strategically within the polynomials such
+that one vector dot product is computed with a single polynomial multiplication. This
+strategy results in a sparse output with very few coefficients containing the actual
+result" (§2.3; §6.1). SPEC.md:626 adds "input at index
+c*HW + h*W + w; kernel mirrored". The formulas below are DESIGN.md reading R6/R7/R8; they are
+pinned by the end-to-end test decrypt(server(Enc(x))) = conv(x, K) mod 2^t.
+
+Geometry
+    Xe      effective input: zero-padded by `pad`, and for a 1x1 kernel with stride > 1
+            pre-decimated to Xe[c, i, j] = Xpad[c, i*stride, j*stride] (reading R7)
+    Hp, Wp  extent of Xe;  Ph, Pw = number of stride-1 window positions that must be covered
+    window  Cw channels x Hw rows x Ww cols per polynomial, Cw*Hw*Ww <= N
+    G       = ceil(C / Cw) channel groups;  S = nbh * nbw spatial blocks
+    O       = (Cw-1)*Hw*Ww + (kh-1)*Ww + (kw-1)
+
+    input poly (g, s), s = bh*nbw + bw, origin (h0, w0) = (bh*(Hw-kh+1), bw*(Ww-kw+1)):
+        coeff[c*Hw*Ww + i*Ww + j] = Xe[g*Cw + c, h0+i, w0+j]      (0 outside Xe)
+    kernel poly (m, g):
+        coeff[O - c*Hw*Ww - l*Ww - l'] = K[m, g*Cw + c, l, l']
+    output poly (m, s), designated coefficient O + i*Ww + j (0 <= i <= Hw-kh, 0 <= j <= Ww-kw)
+        = sum_{c,l,l'} Xe[c, h0+i+l, w0+j+l'] K[m, c, l, l']  = stride-1 output at (h0+i, w0+j)
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+
+@dataclass(frozen=True)
+class Plan:
+    C: int
+    H: int
+    W: int
+    M: int
+    kh: int
+    kw: int
+    stride: int
+    pad: int
+    OH: int
+    OW: int
+    decim: int
+    Hp: int
+    Wp: int
+    Cw: int
+    Hw: int
+    Ww: int
+    G: int
+    S: int
+    nbh: int
+    nbw: int
+    O: int
+
+
+def _geometry(C, H, W, kh, kw, stride, pad):
+    OH = (H + 2 * pad - kh) // stride + 1
+    OW = (W + 2 * pad - kw) // stride + 1
+    decim = 1 if (kh == 1 and kw == 1 and stride > 1) else 0
+    if decim:
+        Hp, Wp, Ph, Pw = OH, OW, OH, OW
+    else:
+        Hp, Wp = H + 2 * pad, W + 2 * pad
+        Ph, Pw = (OH - 1) * stride + 1, (OW - 1) * stride + 1
+    return OH, OW, decim, Hp, Wp, Ph, Pw
+
+
+def plan_conv(C, H, W, M, kh, kw, stride=1, pad=0, n=4096, L=2, Hw=None, Ww=None) -> Plan:
+    """Reading R6: enumerate Hw in [kh, Hp], Ww in [kw, Wp] with Hw*Ww <= N, take
+    Cw = min(C, N // (Hw*Ww)), and minimise the algorithmic bytes
+        8*L*N*(2*G*S + M*G + 2*M*S) + 8*N*M*S
+    tie-breaking on fewer M*G*S products, then larger Hw, then larger Ww.
+    An explicit (Hw, Ww) is validated and used instead."""
+    OH, OW, decim, Hp, Wp, Ph, Pw = _geometry(C, H, W, kh, kw, stride, pad)
+    if OH <= 0 or OW <= 0 or kh * kw > n:
+        raise ValueError("unsupported shape")
+    best = None
+    cands = [(Hw, Ww)] if Hw is not None else [(a, b) for a in range(kh, Hp + 1) for b in range(kw, Wp + 1)]
+    for a, b in cands:
+        if a < kh or b < kw or a * b > n:
+            continue
+        Cw = min(C, n // (a * b))
+        G = -(-C // Cw)
+        nbh = -(-Ph // (a - kh + 1))
+        nbw = -(-Pw // (b - kw + 1))
+        S = nbh * nbw
+        cost = 8 * L * n * (2 * G * S + M * G + 2 * M * S) + 8 * n * M * S
+        key = (cost, M * G * S, -a, -b)
+        if best is None or key < best[0]:
+            best = (key, a, b, Cw, G, S, nbh, nbw)
+    if best is None:
+        raise ValueError("unsupported shape: no window fits N")
+    _, a, b, Cw, G, S, nbh, nbw = best
+    O = (Cw - 1) * a * b + (kh - 1) * b + (kw - 1)
+    return Plan(C, H, W, M, kh, kw, stride, pad, OH, OW, decim, Hp, Wp, Cw, a, b, G, S, nbh, nbw, O)
+
+
+def effective_input(x: np.ndarray, p: Plan) -> np.ndarray:
+    """Zero-pad (and for decimated 1x1/stride>1 plans, subsample) the input share (C,H,W)."""
+    xp = np.zeros((p.C, p.H + 2 * p.pad, p.W + 2 * p.pad), dtype=np.uint64)
+    xp[:, p.pad:p.pad + p.H, p.pad:p.pad + p.W] = x
+    if p.decim:
+        xp = xp[:, ::p.stride, ::p.stride][:, :p.OH, :p.OW]
+    return np.ascontiguousarray(xp)
+
+
+def pack_input(x: np.ndarray, p: Plan, n: int) -> np.ndarray:
+    """Input share (C,H,W) -> polys [G*S][N] (index g*S+s)."""
+    xe = effective_input(x, p)
+    out = np.zeros((p.G * p.S, n), dtype=np.uint64)
+    for g in range(p.G):
+        for bh in range(p.nbh):
+            for bw in range(p.nbw):
+                s = bh * p.nbw + bw
+                h0, w0 = bh * (p.Hw - p.kh + 1), bw * (p.Ww - p.kw + 1)
+                for c in range(p.Cw):
+                    cc = g * p.Cw + c
+                    if cc >= p.C:
+                        break
+                    for i in range(p.Hw):
+                        if h0 + i >= p.Hp:
+                            break
+                        row = xe[cc, h0 + i, w0:min(w0 + p.Ww, p.Wp)]
+                        base = c * p.Hw * p.Ww + i * p.Ww
+                        out[g * p.S + s, base:base + row.size] = row
+    return out
+
+
+def kernel_polys(K: np.ndarray, p: Plan, n: int) -> np.ndarray:
+    """Kernel (M,C,kh,kw) values < 2^t -> raw mirrored plaintext polys [M][G][N] (not lifted)."""
+    out = np.zeros((p.M, p.G, n), dtype=np.uint64)
+    for m in range(p.M):
+        for g in range(p.G):
+            for c in range(p.Cw):
+                cc = g * p.Cw + c
+                if cc >= p.C:
+                    break
+                for l in range(p.kh):
+                    for l2 in range(p.kw):
+                        out[m, g, p.O - c * p.Hw * p.Ww - l * p.Ww - l2] = K[m, cc, l, l2]
+    return out
+
+
+def sparse(polys: np.ndarray):
+    """[M][G][N] -> (koff, kidx, kval) CSR over the M*G polys, nonzero coefficients only."""
+    MG = polys.shape[0] * polys.shape[1]
+    flat = polys.reshape(MG, -1)
+    koff = np.zeros(MG + 1, dtype=np.uint64)
+    idx, val = [], []
+    for r in range(MG):
+        nz = np.nonzero(flat[r])[0]
+        idx.append(nz.astype(np.uint32))
+        val.append(flat[r, nz])
+        koff[r + 1] = koff[r] + nz.size
+    kidx = np.concatenate(idx) if idx else np.zeros(0, np.uint32)
+    kval = np.concatenate(val) if val else np.zeros(0, np.uint64)
+    return koff, np.ascontiguousarray(kidx), np.ascontiguousarray(kval)
+
+
+def designated_map(p: Plan):
+    """Arrays (s_idx, coef_idx) of shape (OH, OW): output (oy, ox) of channel m is coefficient
+    coef_idx[oy, ox] of output poly (m, s_idx[oy, ox])."""
+    sh = 1 if p.decim else p.stride
+    oy, ox = np.meshgrid(np.arange(p.OH), np.arange(p.OW), indexing="ij")
+    py, px = oy * sh, ox * sh
+    bh, i = py // (p.Hw - p.kh + 1), py % (p.Hw - p.kh + 1)
+    bw, j = px // (p.Ww - p.kw + 1), px % (p.Ww - p.kw + 1)
+    return bh * p.nbw + bw, p.O + i * p.Ww + j
+
+
+def extract(polys: np.ndarray, p: Plan) -> np.ndarray:
+    """polys [M*S][N] (values mod t) -> y [M][OH][OW] at the designated coefficients."""
+    s_idx, coef = designated_map(p)
+    P = polys.reshape(p.M, p.S, -1)
+    return P[:, s_idx, coef]
