@@ -1,0 +1,150 @@
+/*
+ * secn.h -- C ABI of libsecn, the B200 (sm_100a) server-side homomorphic linear layer of
+ * SecONNds (arXiv 2506.11586): Cheetah-style coefficient-encoded convolution on RLWE/BFV
+ * ciphertexts with NTT-preprocessed weights.
+ *
+ * Citations are PAPER.md line numbers (PAPER.md = the paper's LaTeX source) with the section;
+ * "reading Rk" refers to DESIGN.md's list of readings where the paper is silent.
+ *
+ * Conventions shared by every call
+ * --------------------------------
+ *  - Ring R_Q = Z_Q[X]/(X^N+1) (§2.1), Q = q_0 ... q_{L-1} in RNS. A limb-poly is
+ *    N uint64 residues mod one q_j; a poly is L limb-polys [L][N]; a ciphertext is (a, b) =
+ *    [2][L][N] (App. C; index 0 = a, 1 = b). All arrays are row-major with
+ *    the last index fastest and live in DEVICE memory of the context's device unless stated.
+ *  - Every residue at the boundary is canonical, in [0, q_j). Plaintext-side values (server
+ *    shares x0, masks r, kernel weights) are integers in [0, 2^t_bits).
+ *  - NTT domain: entry k of a limb-poly holds a(psi_j^(2 brv(k) + 1)) with psi_j the smallest
+ *    primitive 2N-th root mod q_j (bit-reversed order, reading R4; App. C.1).
+ *  - Encoding (reading R2): enc_j(v) = round(Q v / t) mod q_j, round half up, t = 2^t_bits.
+ *  - Ownership: the caller allocates and owns every I/O and workspace buffer and the stream.
+ *    The library owns only the context's device tables (freed by secn_ctx_destroy).
+ *  - Asynchrony: compute calls only enqueue work on `stream` (a cudaStream_t passed as void*;
+ *    NULL = legacy default stream) and return; device faults surface at the caller's next
+ *    synchronisation. No call synchronises the device or allocates memory except
+ *    secn_ctx_create / secn_ctx_destroy.
+ *  - Errors: every call returns a secn_status; none throws or aborts. secn_last_error()
+ *    returns a thread-local message for the last non-OK status of the calling thread.
+ *  - Thread safety: a context is immutable after creation; concurrent calls on different
+ *    streams (and threads) are safe.
+ *  - Range checks of input VALUES (residue < q_j, share < 2^t_bits) cost bandwidth and run
+ *    only when the environment variable SECN_VALIDATE=1 is set (then the call synchronises
+ *    its stream and returns SECN_ERANGE on a violation).
+ */
+#ifndef SECN_H_
+#define SECN_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SECN_MAX_LIMBS 4
+
+typedef struct secn_ctx secn_ctx; /* opaque */
+
+typedef enum {
+  SECN_OK = 0,
+  SECN_EINVAL = -1,       /* NULL pointer, size/shape/plan inconsistency            */
+  SECN_EUNSUPPORTED = -2, /* parameter outside the supported set (see each call)     */
+  SECN_ERANGE = -3,       /* input value out of range (only with SECN_VALIDATE=1)    */
+  SECN_ENOMEM = -4,       /* device allocation failed (ctx creation only)            */
+  SECN_ECUDA = -5,        /* a CUDA runtime call failed (message has the CUDA error) */
+  SECN_ESTATE = -6        /* context/device mismatch                                 */
+} secn_status;
+
+/* Packing plan for one convolution layer (reading R6-R8; Cheetah packing PAPER.md:131 §2.3,
+ * :374 §6.1). Inputs: C,H,W,M,kh,kw,stride,pad (and optionally Hw,Ww). secn_conv_plan fills
+ * the rest:
+ *   OH,OW   output extent;  decim = 1 for a 1x1 kernel with stride > 1 (input pre-decimated)
+ *   Hp,Wp   extent of the effective (padded, decimated) input the windows tile
+ *   Cw,Hw,Ww window: Cw channels x Hw rows x Ww cols per polynomial, Cw*Hw*Ww <= N
+ *   G = ceil(C/Cw) input channel groups; S = nbh*nbw spatial blocks
+ *   O = (Cw-1)*Hw*Ww + (kh-1)*Ww + (kw-1), the offset of the first designated coefficient
+ * Input poly (g,s): coeff[c*Hw*Ww + i*Ww + j] = Xe[g*Cw+c, h0+i, w0+j], (h0,w0) =
+ * (bh*(Hw-kh+1), bw*(Ww-kw+1)), s = bh*nbw+bw. Kernel poly (m,g):
+ * coeff[O - c*Hw*Ww - l*Ww - l'] = K[m, g*Cw+c, l, l']. Output (m,oy,ox) is coefficient
+ * O + i*Ww + j of output ct (m,s) where (bh*(Hw-kh+1)+i, bw*(Ww-kw+1)+j) = (oy*sh, ox*sh),
+ * sh = stride (1 if decim). */
+typedef struct {
+  uint32_t C, H, W, M, kh, kw, stride, pad; /* layer geometry (caller)                   */
+  uint32_t Hw, Ww;                          /* 0 = choose (byte-min rule); else validated  */
+  uint32_t OH, OW, decim, Hp, Wp;           /* filled                                      */
+  uint32_t Cw, G, S, nbh, nbw, O;           /* filled                                      */
+} secn_conv_plan_t;
+
+typedef struct {
+  uint32_t log_n, n, n_limbs, t_bits;
+  uint64_t primes[SECN_MAX_LIMBS];
+  uint64_t psi[SECN_MAX_LIMBS]; /* minimal primitive 2N-th roots (reading R4)              */
+  int device;
+} secn_ctx_info;
+
+/* Creates a context on CUDA device `device`: copies the primes, finds psi_j, and builds the
+ * device tables (psi^brv(i) and psi^-brv(i) with Shoup companions, N^-1, floor(Q/t) mod q_j,
+ * Q mod t). Supported: 12 <= log_n <= 14, 1 <= n_limbs <= 4, every prime q_j < 2^61 with
+ * q_j = 1 (mod 2N) (probable-prime tested), distinct; 1 <= t_bits <= 44.
+ * Returns SECN_EUNSUPPORTED otherwise, SECN_ENOMEM / SECN_ECUDA on device failure. */
+int secn_ctx_create(secn_ctx** out, int device, uint32_t log_n, uint32_t n_limbs, const uint64_t* primes,
+                    uint32_t t_bits);
+int secn_ctx_destroy(secn_ctx* ctx);
+int secn_ctx_query(const secn_ctx* ctx, secn_ctx_info* info);
+const char* secn_last_error(void);
+
+/* Host only. Fills `p` from its geometry for ring degree 2^log_n and n_limbs limbs using the
+ * byte-min rule of reading R6 (or validates the caller's Hw,Ww when both are nonzero).
+ * SECN_EUNSUPPORTED if no window fits (kh*kw > N or Hp < kh). */
+int secn_conv_plan(uint32_t log_n, uint32_t n_limbs, secn_conv_plan_t* p);
+
+/* A1: in-place forward negacyclic NTT of n_polys polys [n_polys][L][N] (coefficient domain ->
+ * NTT domain), PAPER.md:378-380 (§6.2), App. C.1. */
+int secn_ntt_fwd(secn_ctx* ctx, uint64_t* polys, size_t n_polys, void* stream);
+
+/* A2: in-place inverse of secn_ntt_fwd, N^-1 included. */
+int secn_ntt_inv(secn_ctx* ctx, uint64_t* polys, size_t n_polys, void* stream);
+
+/* A3: NTT preprocessing of the weights (PAPER.md:376-380 §6.2, :427 §7 step 1, :445 §8.1):
+ * kernel [M][C][kh][kw] (values < 2^t_bits, two's complement mod 2^t) is packed into the
+ * mirrored plaintext polys of `plan`, centred-lifted to every q_j (reading R3) and transformed:
+ * w_ntt [M][G][L][N] (NTT domain). Deterministic (idempotent). Uses only `plan->M` kernels. */
+int secn_preprocess_weights(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* kernel, uint64_t* w_ntt,
+                            void* stream);
+
+/* A6: server-share add (§7): for ct [n][2][L][N] (coefficient domain),
+ * b_j += enc_j(x0) with x0 [n][N] < 2^t_bits. */
+int secn_share_add(secn_ctx* ctx, uint64_t* ct, const uint64_t* x0, size_t n, void* stream);
+
+/* A7: random output mask (§7): b_j += enc_j(r) for ct [n][2][L][N]
+ * (coefficient domain), r [n][N] < 2^t_bits. The server's share is (t - r) mod t. */
+int secn_mask_add(secn_ctx* ctx, uint64_t* ct, const uint64_t* r, size_t n, void* stream);
+
+/* Bytes of device workspace secn_he_conv2d needs for `plan` (the NTT-domain inputs
+ * X^ = G*S*2*L*N*8 bytes). */
+size_t secn_he_conv2d_workspace(const secn_ctx* ctx, const secn_conv_plan_t* plan);
+
+/* The hot path (PAPER.md:380 §6.2, :431 §7), one layer:
+ *   in'  = ct_in with b += enc(x0)                       (A6, fused; skipped if x0 == NULL)
+ *   X^   = NTT(in')                                       (A1)
+ *   Y^[m,s] = sum_{g<G} X^[g,s] (.) w_ntt[m,g]            (A4, both components, every limb)
+ *   out  = INTT(Y^), then b += enc(r[m,s])                (A2 + A7 fused; skipped if r == NULL)
+ * ct_in [G*S][2][L][N] coefficient domain (index g*S+s) -- read only;
+ * x0 [G*S][N] or NULL; w_ntt [M][G][L][N] from secn_preprocess_weights (M = plan->M, which may
+ * be a slice of the layer's output channels: pass a plan copy with M = slice size and
+ * pointers offset to the slice); r [M*S][N] or NULL; ct_out [M*S][2][L][N] (index m*S+s,
+ * coefficient domain, overwritten; must not alias the inputs); workspace >=
+ * secn_he_conv2d_workspace bytes, 16-byte aligned. */
+int secn_he_conv2d(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* ct_in, const uint64_t* x0,
+                   const uint64_t* w_ntt, const uint64_t* r, uint64_t* ct_out, void* workspace, size_t ws_bytes,
+                   void* stream);
+
+/* Server's output share at the designated coefficients (§7; Cheetah's sparse
+ * result): y0[m][oy][ox] = (t - r[m*S+s][O + i*Ww + j]) mod t for the plan's
+ * index map, m in [0, plan->M). r [M*S][N], y0 [M][OH][OW]. */
+int secn_extract_share(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* r, uint64_t* y0, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SECN_H_ */

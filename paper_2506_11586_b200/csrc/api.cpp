@@ -1,0 +1,408 @@
+// libsecn host side: the C ABI declared in include/secn.h -- context/table construction,
+// packing plan, argument validation and kernel dispatch. No torch types anywhere.
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+typedef unsigned __int128 u128;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int status, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return status;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(SECN_ECUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+// ---- 64-bit number theory with 128-bit intermediates (host) ----
+uint64_t mulmod(uint64_t a, uint64_t b, uint64_t q) { return (uint64_t)((u128)a * b % q); }
+
+uint64_t powmod(uint64_t b, uint64_t e, uint64_t q) {
+  uint64_t r = 1 % q;
+  b %= q;
+  for (; e; e >>= 1) {
+    if (e & 1) r = mulmod(r, b, q);
+    b = mulmod(b, b, q);
+  }
+  return r;
+}
+
+bool probable_prime(uint64_t n) {
+  if (n < 2) return false;
+  static const uint64_t bases[] = {2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37};
+  for (uint64_t p : bases)
+    if (n % p == 0) return n == p;
+  uint64_t d = n - 1;
+  int s = 0;
+  while (!(d & 1)) d >>= 1, ++s;
+  for (uint64_t a : bases) {
+    uint64_t x = powmod(a, d, n);
+    if (x == 1 || x == n - 1) continue;
+    bool comp = true;
+    for (int i = 1; i < s && comp; ++i) {
+      x = mulmod(x, x, n);
+      if (x == n - 1) comp = false;
+    }
+    if (comp) return false;
+  }
+  return true;
+}
+
+uint64_t shoup_companion(uint64_t w, uint64_t q) { return (uint64_t)(((u128)w << 64) / q); }
+
+uint32_t bitrev(uint32_t x, uint32_t bits) {
+  uint32_t r = 0;
+  for (uint32_t i = 0; i < bits; ++i, x >>= 1) r = (r << 1) | (x & 1);
+  return r;
+}
+
+// The smallest primitive 2N-th root of unity mod prime q (reading R4): psi^N = -1; the
+// primitive 2N-th roots are the odd powers of any one of them.
+uint64_t min_primitive_root(uint64_t q, uint64_t n) {
+  for (uint64_t x = 2; x < q; ++x) {
+    const uint64_t y = powmod(x, (q - 1) / (2 * n), q);
+    if (powmod(y, n, q) != q - 1) continue;
+    const uint64_t y2 = mulmod(y, y, q);
+    uint64_t best = y, cur = y;
+    for (uint64_t k = 3; k < 2 * n; k += 2) {
+      cur = mulmod(cur, y2, q);
+      if (cur < best) best = cur;
+    }
+    return best;
+  }
+  return 0;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+bool validate_env() {
+  const char* v = std::getenv("SECN_VALIDATE");
+  return v && v[0] == '1';
+}
+
+// With SECN_VALIDATE=1: synchronously check that `n_words` words are in range
+// (kind 0: residues < q_j by limb, kind 1: < 2^t_bits).
+int check_range(secn_ctx* ctx, const uint64_t* v, size_t n_words, int kind, cudaStream_t s, const char* what) {
+  if (!validate_env() || v == nullptr || n_words == 0) return SECN_OK;
+  cudaError_t e = cudaMemsetAsync(ctx->d_flag, 0, sizeof(uint32_t), s);
+  if (e == cudaSuccess) e = secn::launch_check_range(ctx->dc, v, n_words, kind, ctx->d_flag, s);
+  uint32_t flag = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&flag, ctx->d_flag, sizeof flag, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "range check");
+  if (flag) return fail(SECN_ERANGE, "%s: value out of range (%s)", what, kind == 0 ? ">= q_j" : ">= 2^t_bits");
+  return SECN_OK;
+}
+
+secn::PlanDev plan_dev(const secn_conv_plan_t* p) {
+  secn::PlanDev d;
+  d.M = p->M, d.G = p->G, d.S = p->S, d.Cw = p->Cw, d.Hw = p->Hw, d.Ww = p->Ww, d.kh = p->kh, d.kw = p->kw;
+  d.C = p->C, d.O = p->O, d.OH = p->OH, d.OW = p->OW, d.nbh = p->nbh, d.nbw = p->nbw;
+  d.sh = p->decim ? 1 : p->stride;
+  return d;
+}
+
+// Recompute the derived fields of a plan from its geometry and (Hw, Ww); 0 if consistent.
+int derive_plan(uint32_t n, uint32_t Hw, uint32_t Ww, secn_conv_plan_t* p) {
+  const uint32_t C = p->C, kh = p->kh, kw = p->kw, st = p->stride, pad = p->pad;
+  if (!C || !p->H || !p->W || !p->M || !kh || !kw || !st) return -1;
+  if (p->H + 2 * pad < kh || p->W + 2 * pad < kw) return -1;
+  const uint32_t OH = (p->H + 2 * pad - kh) / st + 1, OW = (p->W + 2 * pad - kw) / st + 1;
+  const uint32_t decim = (kh == 1 && kw == 1 && st > 1) ? 1 : 0;
+  uint32_t Hp, Wp, Ph, Pw;
+  if (decim) {
+    Hp = Ph = OH, Wp = Pw = OW;
+  } else {
+    Hp = p->H + 2 * pad, Wp = p->W + 2 * pad, Ph = (OH - 1) * st + 1, Pw = (OW - 1) * st + 1;
+  }
+  if (Hw < kh || Ww < kw || Hw > Hp || Ww > Wp || (uint64_t)Hw * Ww > n) return -1;
+  const uint32_t Cw = C < n / (Hw * Ww) ? C : n / (Hw * Ww);
+  p->OH = OH, p->OW = OW, p->decim = decim, p->Hp = Hp, p->Wp = Wp, p->Hw = Hw, p->Ww = Ww, p->Cw = Cw;
+  p->G = (C + Cw - 1) / Cw;
+  p->nbh = (Ph + (Hw - kh)) / (Hw - kh + 1);
+  p->nbw = (Pw + (Ww - kw)) / (Ww - kw + 1);
+  p->S = p->nbh * p->nbw;
+  p->O = (Cw - 1) * Hw * Ww + (kh - 1) * Ww + (kw - 1);
+  return 0;
+}
+
+int check_ctx(const secn_ctx* ctx) {
+  if (!ctx) return fail(SECN_EINVAL, "NULL context");
+  int dev;
+  if (cudaGetDevice(&dev) != cudaSuccess) return fail(SECN_ESTATE, "no current CUDA device");
+  return SECN_OK;
+}
+
+int check_plan(const secn_ctx* ctx, const secn_conv_plan_t* p) {
+  if (!p) return fail(SECN_EINVAL, "NULL plan");
+  secn_conv_plan_t q = *p;
+  if (derive_plan(ctx->n, p->Hw, p->Ww, &q) != 0) return fail(SECN_EINVAL, "plan inconsistent with its geometry");
+  if (q.Cw != p->Cw || q.G != p->G || q.S != p->S || q.O != p->O || q.OH != p->OH || q.OW != p->OW ||
+      q.decim != p->decim || q.nbh != p->nbh || q.nbw != p->nbw)
+    return fail(SECN_EINVAL, "plan fields do not match secn_conv_plan() for this geometry and N");
+  return SECN_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* secn_last_error(void) { return g_err.c_str(); }
+
+int secn_ctx_create(secn_ctx** out, int device, uint32_t log_n, uint32_t n_limbs, const uint64_t* primes,
+                    uint32_t t_bits) {
+  if (!out || !primes) return fail(SECN_EINVAL, "NULL argument");
+  *out = nullptr;
+  if (log_n < 12 || log_n > 14) return fail(SECN_EUNSUPPORTED, "log_n=%u not in [12,14]", log_n);
+  if (n_limbs < 1 || n_limbs > SECN_MAX_LIMBS) return fail(SECN_EUNSUPPORTED, "n_limbs=%u not in [1,4]", n_limbs);
+  if (t_bits < 1 || t_bits > 44) return fail(SECN_EUNSUPPORTED, "t_bits=%u not in [1,44]", t_bits);
+  const uint64_t n = 1ull << log_n;
+  for (uint32_t j = 0; j < n_limbs; ++j) {
+    const uint64_t q = primes[j];
+    if (q >= (1ull << 61)) return fail(SECN_EUNSUPPORTED, "prime %u >= 2^61", j);
+    if (q <= (1ull << t_bits)) return fail(SECN_EUNSUPPORTED, "prime %u <= 2^t_bits", j);
+    if ((q - 1) % (2 * n) != 0) return fail(SECN_EUNSUPPORTED, "prime %u != 1 mod 2N", j);
+    if (!probable_prime(q)) return fail(SECN_EUNSUPPORTED, "modulus %u is not prime", j);
+    for (uint32_t k = 0; k < j; ++k)
+      if (primes[k] == q) return fail(SECN_EUNSUPPORTED, "duplicate prime");
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
+    return fail(SECN_ESTATE, "device %d not available", device);
+  DeviceGuard guard(device);
+
+  secn_ctx* c = new secn_ctx();
+  c->device = device, c->log_n = log_n, c->n = (uint32_t)n, c->L = n_limbs, c->t_bits = t_bits;
+  secn::DevConsts& dc = c->dc;
+  std::memset(&dc, 0, sizeof dc);
+  dc.t_bits = t_bits, dc.log_n = log_n, dc.L = n_limbs;
+  const uint64_t t = 1ull << t_bits, tmask = t - 1;
+  // Q mod t = prod (q_j mod t) mod t (t a power of two)
+  uint64_t qmt = 1;
+  for (uint32_t j = 0; j < n_limbs; ++j) qmt = (uint64_t)(((u128)qmt * (primes[j] & tmask)) & tmask);
+  dc.qmt = qmt;
+
+  std::vector<ulonglong2> tw((size_t)2 * n_limbs * n);
+  for (uint32_t j = 0; j < n_limbs; ++j) {
+    const uint64_t q = primes[j];
+    c->primes[j] = q;
+    const uint64_t psi = min_primitive_root(q, n);
+    c->psi[j] = psi;
+    const uint64_t psi_inv = powmod(psi, q - 2, q);
+    ulonglong2* fw = &tw[(size_t)j * n];
+    ulonglong2* iv = &tw[((size_t)n_limbs + j) * n];
+    for (uint32_t i = 0; i < n; ++i) {
+      const uint32_t e = bitrev(i, log_n);
+      const uint64_t wf = powmod(psi, e, q), wi = powmod(psi_inv, e, q);
+      fw[i] = make_ulonglong2(wf, shoup_companion(wf, q));
+      iv[i] = make_ulonglong2(wi, shoup_companion(wi, q));
+    }
+    dc.q[j] = q, dc.q2[j] = 2 * q;
+    const uint64_t ninv = powmod(n % q, q - 2, q);
+    dc.ninv[j] = ninv, dc.ninv_p[j] = shoup_companion(ninv, q);
+    const uint64_t wl = mulmod(iv[1].x, ninv, q);
+    dc.wlast[j] = wl, dc.wlast_p[j] = shoup_companion(wl, q);
+    // floor(Q/t) = (Q - (Q mod t)) / t and Q = 0 mod q_j  =>  floor(Q/t) = -(Q mod t) t^-1 mod q_j
+    const uint64_t tinv = powmod(t % q, q - 2, q);
+    const uint64_t delta = mulmod((q - qmt % q) % q, tinv, q);
+    dc.delta[j] = delta, dc.delta_p[j] = shoup_companion(delta, q);
+    const uint64_t r64 = (uint64_t)(((u128)1 << 64) % q);
+    dc.r64[j] = r64, dc.r64_p[j] = shoup_companion(r64, q);
+    dc.one_p[j] = ~0ull / q;
+  }
+  const size_t bytes = tw.size() * sizeof(ulonglong2);
+  cudaError_t e = cudaMalloc(&c->d_tables, bytes);
+  if (e != cudaSuccess) {
+    delete c;
+    return fail(e == cudaErrorMemoryAllocation ? SECN_ENOMEM : SECN_ECUDA, "cudaMalloc tables: %s", cudaGetErrorString(e));
+  }
+  e = cudaMalloc(&c->d_flag, sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMemcpy(c->d_tables, tw.data(), bytes, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    cudaFree(c->d_tables);
+    delete c;
+    return cuda_fail(e, "ctx tables");
+  }
+  dc.tw_fwd = static_cast<const ulonglong2*>(c->d_tables);
+  dc.tw_inv = dc.tw_fwd + (size_t)n_limbs * n;
+  *out = c;
+  return SECN_OK;
+}
+
+int secn_ctx_destroy(secn_ctx* ctx) {
+  if (!ctx) return SECN_OK;
+  DeviceGuard guard(ctx->device);
+  cudaFree(ctx->d_tables);
+  cudaFree(ctx->d_flag);
+  delete ctx;
+  return SECN_OK;
+}
+
+int secn_ctx_query(const secn_ctx* ctx, secn_ctx_info* info) {
+  if (!ctx || !info) return fail(SECN_EINVAL, "NULL argument");
+  std::memset(info, 0, sizeof *info);
+  info->log_n = ctx->log_n, info->n = ctx->n, info->n_limbs = ctx->L, info->t_bits = ctx->t_bits;
+  info->device = ctx->device;
+  for (uint32_t j = 0; j < ctx->L; ++j) info->primes[j] = ctx->primes[j], info->psi[j] = ctx->psi[j];
+  return SECN_OK;
+}
+
+int secn_conv_plan(uint32_t log_n, uint32_t n_limbs, secn_conv_plan_t* p) {
+  if (!p) return fail(SECN_EINVAL, "NULL plan");
+  if (log_n < 1 || log_n > 20 || n_limbs < 1) return fail(SECN_EUNSUPPORTED, "bad log_n / n_limbs");
+  const uint32_t n = 1u << log_n;
+  if (!p->C || !p->H || !p->W || !p->M || !p->kh || !p->kw || !p->stride)
+    return fail(SECN_EINVAL, "zero dimension in plan geometry");
+  if ((uint64_t)p->kh * p->kw > n || p->H + 2 * p->pad < p->kh || p->W + 2 * p->pad < p->kw)
+    return fail(SECN_EUNSUPPORTED, "unsupported shape: window larger than N or input");
+  if (p->Hw && p->Ww) {
+    if (derive_plan(n, p->Hw, p->Ww, p) != 0) return fail(SECN_EINVAL, "caller Hw,Ww invalid for this geometry");
+    return SECN_OK;
+  }
+  // reading R6: minimise 8 L N (2GS + MG + 2MS) + 8 N MS; ties: fewer MGS, larger Hw, larger Ww
+  secn_conv_plan_t best{};
+  bool have = false;
+  u128 best_cost = 0;
+  uint64_t best_mgs = 0;
+  const uint32_t Hp = (p->kh == 1 && p->kw == 1 && p->stride > 1) ? (p->H + 2 * p->pad - 1) / p->stride + 1
+                                                                  : p->H + 2 * p->pad;
+  const uint32_t Wp = (p->kh == 1 && p->kw == 1 && p->stride > 1) ? (p->W + 2 * p->pad - 1) / p->stride + 1
+                                                                  : p->W + 2 * p->pad;
+  for (uint32_t Hw = p->kh; Hw <= Hp; ++Hw) {
+    for (uint32_t Ww = p->kw; Ww <= Wp; ++Ww) {
+      if ((uint64_t)Hw * Ww > n) break;
+      secn_conv_plan_t c = *p;
+      if (derive_plan(n, Hw, Ww, &c) != 0) continue;
+      const u128 G = c.G, S = c.S, M = c.M;
+      const u128 cost = (u128)8 * n_limbs * n * (2 * G * S + M * G + 2 * M * S) + (u128)8 * n * M * S;
+      const uint64_t mgs = (uint64_t)(M * G * S);
+      bool better = !have || cost < best_cost || (cost == best_cost && mgs < best_mgs) ||
+                    (cost == best_cost && mgs == best_mgs && (Hw > best.Hw || (Hw == best.Hw && Ww > best.Ww)));
+      if (better) best = c, best_cost = cost, best_mgs = mgs, have = true;
+    }
+  }
+  if (!have) return fail(SECN_EUNSUPPORTED, "unsupported shape: no window fits N");
+  *p = best;
+  return SECN_OK;
+}
+
+int secn_ntt_fwd(secn_ctx* ctx, uint64_t* polys, size_t n_polys, void* stream) {
+  if (int st = check_ctx(ctx)) return st;
+  if (n_polys && !polys) return fail(SECN_EINVAL, "NULL polys");
+  DeviceGuard guard(ctx->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (int st = check_range(ctx, polys, n_polys * ctx->L * ctx->n, 0, s, "secn_ntt_fwd")) return st;
+  cudaError_t e = secn::launch_ntt_fwd(ctx->dc, polys, polys, n_polys * ctx->L, nullptr, s);
+  return e == cudaSuccess ? SECN_OK : cuda_fail(e, "secn_ntt_fwd");
+}
+
+int secn_ntt_inv(secn_ctx* ctx, uint64_t* polys, size_t n_polys, void* stream) {
+  if (int st = check_ctx(ctx)) return st;
+  if (n_polys && !polys) return fail(SECN_EINVAL, "NULL polys");
+  DeviceGuard guard(ctx->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (int st = check_range(ctx, polys, n_polys * ctx->L * ctx->n, 0, s, "secn_ntt_inv")) return st;
+  cudaError_t e = secn::launch_ntt_inv(ctx->dc, polys, n_polys * ctx->L, nullptr, s);
+  return e == cudaSuccess ? SECN_OK : cuda_fail(e, "secn_ntt_inv");
+}
+
+int secn_preprocess_weights(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* kernel, uint64_t* w_ntt,
+                            void* stream) {
+  if (int st = check_ctx(ctx)) return st;
+  if (int st = check_plan(ctx, plan)) return st;
+  if (!kernel || !w_ntt) return fail(SECN_EINVAL, "NULL buffer");
+  DeviceGuard guard(ctx->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t kw = (size_t)plan->M * plan->C * plan->kh * plan->kw;
+  if (int st = check_range(ctx, kernel, kw, 1, s, "secn_preprocess_weights kernel")) return st;
+  const secn::PlanDev pd = plan_dev(plan);
+  cudaError_t e = secn::launch_pack_weights(ctx->dc, pd, kernel, w_ntt, s);
+  if (e == cudaSuccess) e = secn::launch_ntt_fwd(ctx->dc, w_ntt, w_ntt, (size_t)plan->M * plan->G * ctx->L, nullptr, s);
+  return e == cudaSuccess ? SECN_OK : cuda_fail(e, "secn_preprocess_weights");
+}
+
+int secn_share_add(secn_ctx* ctx, uint64_t* ct, const uint64_t* x0, size_t n, void* stream) {
+  if (int st = check_ctx(ctx)) return st;
+  if (n && (!ct || !x0)) return fail(SECN_EINVAL, "NULL buffer");
+  DeviceGuard guard(ctx->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (int st = check_range(ctx, x0, n * ctx->n, 1, s, "secn_share_add x0")) return st;
+  cudaError_t e = secn::launch_enc_add(ctx->dc, ct, x0, n, s);
+  return e == cudaSuccess ? SECN_OK : cuda_fail(e, "secn_share_add");
+}
+
+int secn_mask_add(secn_ctx* ctx, uint64_t* ct, const uint64_t* r, size_t n, void* stream) {
+  if (int st = check_ctx(ctx)) return st;
+  if (n && (!ct || !r)) return fail(SECN_EINVAL, "NULL buffer");
+  DeviceGuard guard(ctx->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (int st = check_range(ctx, r, n * ctx->n, 1, s, "secn_mask_add r")) return st;
+  cudaError_t e = secn::launch_enc_add(ctx->dc, ct, r, n, s);
+  return e == cudaSuccess ? SECN_OK : cuda_fail(e, "secn_mask_add");
+}
+
+size_t secn_he_conv2d_workspace(const secn_ctx* ctx, const secn_conv_plan_t* plan) {
+  if (!ctx || !plan) return 0;
+  return (size_t)plan->G * plan->S * 2 * ctx->L * ctx->n * sizeof(uint64_t);
+}
+
+int secn_he_conv2d(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* ct_in, const uint64_t* x0,
+                   const uint64_t* w_ntt, const uint64_t* r, uint64_t* ct_out, void* workspace, size_t ws_bytes,
+                   void* stream) {
+  if (int st = check_ctx(ctx)) return st;
+  if (int st = check_plan(ctx, plan)) return st;
+  if (!ct_in || !w_ntt || !ct_out || !workspace) return fail(SECN_EINVAL, "NULL buffer");
+  if (ws_bytes < secn_he_conv2d_workspace(ctx, plan)) return fail(SECN_EINVAL, "workspace too small");
+  if (((uintptr_t)workspace | (uintptr_t)ct_in | (uintptr_t)ct_out | (uintptr_t)w_ntt) & 15)
+    return fail(SECN_EINVAL, "buffers must be 16-byte aligned");
+  if (plan->G > 50) return fail(SECN_EUNSUPPORTED, "G=%u > 50 input channel groups", plan->G);
+  DeviceGuard guard(ctx->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t n_in = (size_t)plan->G * plan->S, n_out = (size_t)plan->M * plan->S, N = ctx->n;
+  if (int st = check_range(ctx, ct_in, n_in * 2 * ctx->L * N, 0, s, "secn_he_conv2d ct_in")) return st;
+  if (int st = check_range(ctx, x0, n_in * N, 1, s, "secn_he_conv2d x0")) return st;
+  if (int st = check_range(ctx, r, n_out * N, 1, s, "secn_he_conv2d r")) return st;
+  uint64_t* xhat = static_cast<uint64_t*>(workspace);
+  const secn::PlanDev pd = plan_dev(plan);
+  cudaError_t e = secn::launch_ntt_fwd(ctx->dc, ct_in, xhat, n_in * 2 * ctx->L, x0, s);     // A6 + A1
+  if (e == cudaSuccess) e = secn::launch_mac(ctx->dc, pd, xhat, w_ntt, ct_out, s);           // A4
+  if (e == cudaSuccess) e = secn::launch_ntt_inv(ctx->dc, ct_out, n_out * 2 * ctx->L, r, s);  // A2 + A7
+  return e == cudaSuccess ? SECN_OK : cuda_fail(e, "secn_he_conv2d");
+}
+
+int secn_extract_share(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* r, uint64_t* y0, void* stream) {
+  if (int st = check_ctx(ctx)) return st;
+  if (int st = check_plan(ctx, plan)) return st;
+  if (!r || !y0) return fail(SECN_EINVAL, "NULL buffer");
+  DeviceGuard guard(ctx->device);
+  cudaError_t e = secn::launch_extract_share(ctx->dc, plan_dev(plan), r, y0, (cudaStream_t)stream);
+  return e == cudaSuccess ? SECN_OK : cuda_fail(e, "secn_extract_share");
+}
+
+}  // extern "C"

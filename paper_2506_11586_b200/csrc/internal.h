@@ -1,0 +1,54 @@
+// Internal declarations shared by api.cpp (host) and kernels.cu (device) of libsecn.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+#include "../../include/secn.h"
+
+namespace secn {
+
+// Per-context constants passed by value to every kernel (kernel-parameter space).
+struct DevConsts {
+  uint64_t q[SECN_MAX_LIMBS], q2[SECN_MAX_LIMBS];
+  uint64_t ninv[SECN_MAX_LIMBS], ninv_p[SECN_MAX_LIMBS];    // N^-1 (Shoup)
+  uint64_t wlast[SECN_MAX_LIMBS], wlast_p[SECN_MAX_LIMBS];  // psi^-brv(1) * N^-1 (Shoup)
+  uint64_t delta[SECN_MAX_LIMBS], delta_p[SECN_MAX_LIMBS];  // floor(Q/t) mod q (Shoup)
+  uint64_t r64[SECN_MAX_LIMBS], r64_p[SECN_MAX_LIMBS];      // 2^64 mod q (Shoup)
+  uint64_t one_p[SECN_MAX_LIMBS];                           // floor(2^64 / q)
+  uint64_t qmt;                                             // Q mod t
+  uint32_t t_bits, log_n, L, pad_;
+  const ulonglong2* tw_fwd;  // [L][N] (psi^brv(i), Shoup companion)
+  const ulonglong2* tw_inv;  // [L][N] (psi^-brv(i), Shoup companion)
+};
+
+struct PlanDev {  // the subset of secn_conv_plan the kernels use
+  uint32_t M, G, S, Cw, Hw, Ww, kh, kw, C, O, OH, OW, nbh, nbw, sh;
+};
+
+// ---- launchers (kernels.cu); all return cudaGetLastError() after the launch(es) ----
+cudaError_t launch_ntt_fwd(const DevConsts& c, const uint64_t* in, uint64_t* out, size_t n_limb_polys,
+                           const uint64_t* x0, cudaStream_t s);
+cudaError_t launch_ntt_inv(const DevConsts& c, uint64_t* polys, size_t n_limb_polys, const uint64_t* r,
+                           cudaStream_t s);
+cudaError_t launch_mac(const DevConsts& c, const PlanDev& p, const uint64_t* xhat, const uint64_t* w,
+                       uint64_t* y, cudaStream_t s);
+cudaError_t launch_pack_weights(const DevConsts& c, const PlanDev& p, const uint64_t* kernel, uint64_t* w,
+                                cudaStream_t s);
+cudaError_t launch_enc_add(const DevConsts& c, uint64_t* ct, const uint64_t* v, size_t n, cudaStream_t s);
+cudaError_t launch_extract_share(const DevConsts& c, const PlanDev& p, const uint64_t* r, uint64_t* y0,
+                                 cudaStream_t s);
+cudaError_t launch_check_range(const DevConsts& c, const uint64_t* v, size_t n_limb_polys, int kind,
+                               uint32_t* flag, cudaStream_t s);
+
+}  // namespace secn
+
+struct secn_ctx {
+  int device;
+  uint32_t log_n, n, L, t_bits;
+  uint64_t primes[SECN_MAX_LIMBS], psi[SECN_MAX_LIMBS];
+  secn::DevConsts dc;
+  void* d_tables;
+  uint32_t* d_flag;  // SECN_VALIDATE scratch
+};

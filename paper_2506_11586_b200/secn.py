@@ -1,0 +1,215 @@
+"""Thin Python binding of libsecn (include/secn.h): argument marshalling only.
+
+Every step of the hot path runs in libsecn's CUDA kernels; this module only checks tensor
+shapes/dtypes, passes device pointers and the current torch CUDA stream through ctypes,
+and raises on a non-OK status. Tensors hold the uint64 residues in int64 storage (PyTorch's
+uint64 support is partial); values are never interpreted here. There is no CPU fallback:
+if libsecn.so is missing or no CUDA device is present, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Optional, Sequence
+
+import torch
+
+from . import build as _build
+
+# Reading R1: N = 4096, q0 = 2^60 - 2^14 + 1, q1 = 2^49 - 204799, t = 2^37.
+DEFAULT_LOG_N = 12
+DEFAULT_PRIMES = (0x0FFFFFFFFFFFC001, 0x1FFFFFFFCE001)
+DEFAULT_T_BITS = 37
+
+SECN_MAX_LIMBS = 4
+STATUS = {0: "SECN_OK", -1: "SECN_EINVAL", -2: "SECN_EUNSUPPORTED", -3: "SECN_ERANGE", -4: "SECN_ENOMEM",
+          -5: "SECN_ECUDA", -6: "SECN_ESTATE"}
+
+EXPORTS = ("secn_ctx_create", "secn_ctx_destroy", "secn_ctx_query", "secn_last_error", "secn_conv_plan",
+           "secn_ntt_fwd", "secn_ntt_inv", "secn_preprocess_weights", "secn_share_add", "secn_mask_add",
+           "secn_he_conv2d_workspace", "secn_he_conv2d", "secn_extract_share")
+
+
+class SecnError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Plan(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_uint32) for f in
+                ("C", "H", "W", "M", "kh", "kw", "stride", "pad", "Hw", "Ww", "OH", "OW", "decim", "Hp", "Wp",
+                 "Cw", "G", "S", "nbh", "nbw", "O")]
+
+    def copy(self, **kw) -> "Plan":
+        p = Plan()
+        ctypes.pointer(p)[0] = self
+        for k, v in kw.items():
+            setattr(p, k, v)
+        return p
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+    def __repr__(self):
+        return "Plan(" + ", ".join(f"{k}={v}" for k, v in self.as_dict().items()) + ")"
+
+
+class CtxInfo(ctypes.Structure):
+    _fields_ = [("log_n", ctypes.c_uint32), ("n", ctypes.c_uint32), ("n_limbs", ctypes.c_uint32),
+                ("t_bits", ctypes.c_uint32), ("primes", ctypes.c_uint64 * SECN_MAX_LIMBS),
+                ("psi", ctypes.c_uint64 * SECN_MAX_LIMBS), ("device", ctypes.c_int)]
+
+
+_lib = None
+
+
+def lib(path=None) -> ctypes.CDLL:
+    """Loads libsecn.so (built by __graft_entry__.build()); raises if it is missing."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = path or _build.LIB
+    if not p.exists():
+        raise RuntimeError(f"{p} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = ctypes.CDLL(str(p))
+    vp, i, u32, sz = ctypes.c_void_p, ctypes.c_int, ctypes.c_uint32, ctypes.c_size_t
+    P = ctypes.POINTER(Plan)
+    sig = {
+        "secn_ctx_create": (i, [ctypes.POINTER(vp), i, u32, u32, ctypes.POINTER(ctypes.c_uint64), u32]),
+        "secn_ctx_destroy": (i, [vp]),
+        "secn_ctx_query": (i, [vp, ctypes.POINTER(CtxInfo)]),
+        "secn_last_error": (ctypes.c_char_p, []),
+        "secn_conv_plan": (i, [u32, u32, P]),
+        "secn_ntt_fwd": (i, [vp, vp, sz, vp]),
+        "secn_ntt_inv": (i, [vp, vp, sz, vp]),
+        "secn_preprocess_weights": (i, [vp, P, vp, vp, vp]),
+        "secn_share_add": (i, [vp, vp, vp, sz, vp]),
+        "secn_mask_add": (i, [vp, vp, vp, sz, vp]),
+        "secn_he_conv2d_workspace": (sz, [vp, P]),
+        "secn_he_conv2d": (i, [vp, P, vp, vp, vp, vp, vp, vp, sz, vp]),
+        "secn_extract_share": (i, [vp, P, vp, vp, vp]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype, f.argtypes = res, args
+    if path is None:
+        _lib = L
+    return L
+
+
+def _check(status: int):
+    if status != 0:
+        raise SecnError(status, lib().secn_last_error().decode())
+
+
+def conv_plan(C, H, W, M, kh, kw=None, stride=1, pad=0, log_n=DEFAULT_LOG_N, n_limbs=len(DEFAULT_PRIMES),
+              Hw=0, Ww=0) -> Plan:
+    """secn_conv_plan: packing plan of one conv layer (byte-min rule, reading R6)."""
+    p = Plan(C=C, H=H, W=W, M=M, kh=kh, kw=kh if kw is None else kw, stride=stride, pad=pad, Hw=Hw, Ww=Ww)
+    _check(lib().secn_conv_plan(log_n, n_limbs, ctypes.byref(p)))
+    return p
+
+
+def _ptr(t: Optional[torch.Tensor], shape=None, name="tensor"):
+    if t is None:
+        return None
+    if t.dtype != torch.int64 or not t.is_cuda or not t.is_contiguous():
+        raise TypeError(f"{name}: expected a contiguous int64 CUDA tensor, got {t.dtype} {t.device}")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name}: expected shape {tuple(shape)}, got {tuple(t.shape)}")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+class Context:
+    """A libsecn context on one CUDA device (secn_ctx_create)."""
+
+    def __init__(self, device: int = 0, log_n: int = DEFAULT_LOG_N, primes: Sequence[int] = DEFAULT_PRIMES,
+                 t_bits: int = DEFAULT_T_BITS):
+        self._h = ctypes.c_void_p()
+        arr = (ctypes.c_uint64 * len(primes))(*primes)
+        _check(lib().secn_ctx_create(ctypes.byref(self._h), device, log_n, len(primes), arr, t_bits))
+        info = CtxInfo()
+        _check(lib().secn_ctx_query(self._h, ctypes.byref(info)))
+        self.device = torch.device("cuda", device)
+        self.log_n, self.n, self.L, self.t_bits = info.log_n, info.n, info.n_limbs, info.t_bits
+        self.primes = tuple(info.primes[: self.L])
+        self.psi = tuple(info.psi[: self.L])
+
+    def close(self):
+        if self._h:
+            lib().secn_ctx_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _stream(self, stream):
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        return ctypes.c_void_p(s.cuda_stream)
+
+    def plan(self, C, H, W, M, kh, kw=None, stride=1, pad=0, Hw=0, Ww=0) -> Plan:
+        return conv_plan(C, H, W, M, kh, kw, stride, pad, self.log_n, self.L, Hw, Ww)
+
+    # -- boundary calls ---------------------------------------------------------------------
+    def ntt_fwd(self, polys: torch.Tensor, stream=None) -> torch.Tensor:
+        n = polys.numel() // (self.L * self.n)
+        _check(lib().secn_ntt_fwd(self._h, _ptr(polys, None, "polys"), n, self._stream(stream)))
+        return polys
+
+    def ntt_inv(self, polys: torch.Tensor, stream=None) -> torch.Tensor:
+        n = polys.numel() // (self.L * self.n)
+        _check(lib().secn_ntt_inv(self._h, _ptr(polys, None, "polys"), n, self._stream(stream)))
+        return polys
+
+    def preprocess_weights(self, plan: Plan, kernel: torch.Tensor, out: Optional[torch.Tensor] = None,
+                           stream=None) -> torch.Tensor:
+        shape = (plan.M, plan.G, self.L, self.n)
+        if out is None:
+            out = torch.empty(shape, dtype=torch.int64, device=self.device)
+        _check(lib().secn_preprocess_weights(self._h, ctypes.byref(plan),
+                                             _ptr(kernel, (plan.M, plan.C, plan.kh, plan.kw), "kernel"),
+                                             _ptr(out, shape, "w_ntt"), self._stream(stream)))
+        return out
+
+    def share_add(self, ct: torch.Tensor, x0: torch.Tensor, stream=None) -> torch.Tensor:
+        n = ct.shape[0]
+        _check(lib().secn_share_add(self._h, _ptr(ct, (n, 2, self.L, self.n), "ct"), _ptr(x0, (n, self.n), "x0"), n,
+                                    self._stream(stream)))
+        return ct
+
+    def mask_add(self, ct: torch.Tensor, r: torch.Tensor, stream=None) -> torch.Tensor:
+        n = ct.shape[0]
+        _check(lib().secn_mask_add(self._h, _ptr(ct, (n, 2, self.L, self.n), "ct"), _ptr(r, (n, self.n), "r"), n,
+                                   self._stream(stream)))
+        return ct
+
+    def workspace_bytes(self, plan: Plan) -> int:
+        return lib().secn_he_conv2d_workspace(self._h, ctypes.byref(plan))
+
+    def he_conv2d(self, plan: Plan, ct_in: torch.Tensor, w_ntt: torch.Tensor, x0: Optional[torch.Tensor] = None,
+                  r: Optional[torch.Tensor] = None, out: Optional[torch.Tensor] = None,
+                  workspace: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+        L, n = self.L, self.n
+        n_in, n_out = plan.G * plan.S, plan.M * plan.S
+        if out is None:
+            out = torch.empty((n_out, 2, L, n), dtype=torch.int64, device=self.device)
+        ws_bytes = self.workspace_bytes(plan)
+        if workspace is None:
+            workspace = torch.empty(ws_bytes // 8, dtype=torch.int64, device=self.device)
+        _check(lib().secn_he_conv2d(self._h, ctypes.byref(plan), _ptr(ct_in, (n_in, 2, L, n), "ct_in"),
+                                    _ptr(x0, (n_in, n), "x0"), _ptr(w_ntt, (plan.M, plan.G, L, n), "w_ntt"),
+                                    _ptr(r, (n_out, n), "r"), _ptr(out, (n_out, 2, L, n), "ct_out"),
+                                    _ptr(workspace, None, "workspace"), workspace.numel() * 8, self._stream(stream)))
+        return out
+
+    def extract_share(self, plan: Plan, r: torch.Tensor, out: Optional[torch.Tensor] = None,
+                      stream=None) -> torch.Tensor:
+        shape = (plan.M, plan.OH, plan.OW)
+        if out is None:
+            out = torch.empty(shape, dtype=torch.int64, device=self.device)
+        _check(lib().secn_extract_share(self._h, ctypes.byref(plan), _ptr(r, (plan.M * plan.S, self.n), "r"),
+                                        _ptr(out, shape, "y0"), self._stream(stream)))
+        return out
