@@ -1,0 +1,493 @@
+#!/usr/bin/env python
+"""bench.py -- SecONNds server-side HE-linear-layer time on B200 (BASELINE.json metric).
+
+A step is one pass of the whole hot path over every conv layer of SqueezeNet 1.1 at 224x224
+(BASELINE.json configs[2]) with the paper's 37-bit BFV parameters
+(N = 4096, Q = q0 q1 of 60 + 49 bits, t = 2^37; reading R1): per layer the
+server-share add + forward NTT of the input ciphertexts, the NTT-domain ct x pt MAC against the
+NTT-preprocessed weights, the inverse NTT + random mask, and the extraction of the server's
+output share -- all in libsecn's sm_100a kernels through its C ABI. Inputs are synthetic and
+seeded (workloads/inputs.py); they are resident in HBM before the timed region (2.9 GB per
+step, far larger than the 126 MB L2, so no explicit flush is needed).
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl secn|reference]
+Multi-GPU: torchrun --nproc-per-node N bench.py --gpus N ...  (output-channel sharding, NCCL
+all-gather of the server's output shares; time = max over ranks).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+from workloads import inputs, layers  # noqa: E402
+
+METRIC = "SqueezeNet HE-linear-layer time (s)"
+HBM_PEAK_FALLBACK = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["secn", "reference"], default="secn")
+    ap.add_argument("--net", default="squeezenet1_1")
+    ap.add_argument("--seed", type=int, default=3)
+    ap.add_argument("--cpu-frac", type=float, default=0.05, help="oracle sample fraction for cpu_baseline")
+    ap.add_argument("--ref-frac", type=float, default=0.01, help="oracle sample fraction per --impl reference step")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d.get("hbm_gbs", HBM_PEAK_FALLBACK)), "measured"
+    return HBM_PEAK_FALLBACK, "fallback"
+
+
+# ------------------------------------------------------------------------------------------
+# clocks during the timed region (NVML)
+
+class ClockSampler:
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index: int, period: float = 0.005):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self.period = period
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nv = None
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                bits = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for b, name in self.REASONS.items():
+                    if bits & b and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self._nv:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self._nv:
+            self._stop.set()
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------------------------------
+# workload
+
+def layer_inputs(P_primes, n, t_bits, lay, opl_G, opl_S, M, seed):
+    """Seeded synthetic inputs of one layer (identical on every rank and in the oracle)."""
+    g = inputs.rng(seed)
+    ct = inputs.uniform_residues(g, (opl_G * opl_S, 2), P_primes, n)
+    x0 = inputs.uniform_below(g, (opl_G * opl_S, n), 1 << t_bits)
+    K = inputs.quantized_kernel(g, M, lay.C, lay.k, lay.k, t_bits)
+    r = inputs.uniform_below(g, (M * opl_S, n), 1 << t_bits)
+    return ct, x0, K, r
+
+
+def algorithmic_bytes(plan, L, n):
+    """SURVEY.md §8d per-layer bytes: 8 L N (2GS + MG + 2MS) + 8 N MS (+ 8 N GS for x0)."""
+    G, S, M = plan.G, plan.S, plan.M
+    return 8 * L * n * (2 * G * S + M * G + 2 * M * S) + 8 * n * M * S + 8 * n * G * S
+
+
+def stage_bytes(plan, L, n):
+    """Bytes each launch group reads + writes (its own roofline numerator)."""
+    G, S, M = plan.G, plan.S, plan.M
+    ct_in = 2 * G * S * L * n * 8
+    x0 = G * S * n * 8
+    w = M * G * L * n * 8
+    y = 2 * M * S * L * n * 8
+    r = M * S * n * 8
+    return {0: ct_in + x0 + ct_in, 1: w + ct_in + y, 2: y + r + y}
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl" if args.impl == "secn" else "gloo")
+    if args.impl == "reference":
+        return run_reference(args, world, rank)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    import __graft_entry__
+    from paper_2506_11586_b200 import Context
+    from paper_2506_11586_b200 import dist as sdist
+
+    if rank == 0:
+        __graft_entry__.build()
+    if world > 1:
+        dist.barrier()
+    ctx = Context(local)
+    L, n, t_bits = ctx.L, ctx.n, ctx.t_bits
+    net = layers.network(args.net)
+
+    # ---- setup: plans, inputs, offline weight preprocessing (timed separately) ----
+    st = []
+    for li, lay in enumerate(net):
+        plan = ctx.plan(lay.C, lay.H, lay.W, lay.M, lay.k, stride=lay.stride, pad=lay.pad)
+        m0, mc = sdist.m_slices(plan.M, world)[rank]
+        ct, x0, K, r = layer_inputs(ctx.primes, n, t_bits, lay, plan.G, plan.S, plan.M, args.seed * 1000 + li)
+        S = plan.S
+        d = {"lay": lay, "plan": plan, "m0": m0, "mc": mc, "ct_h": ct, "x0_h": x0, "K_h": K, "r_h": r}
+        if mc > 0:
+            pl = plan.copy(M=mc)
+            d["pl"] = pl
+            d["ct"] = torch.from_numpy(ct.view(np.int64)).to(dev)
+            d["x0"] = torch.from_numpy(x0.view(np.int64)).to(dev)
+            d["K"] = torch.from_numpy(np.ascontiguousarray(K[m0:m0 + mc]).view(np.int64)).to(dev)
+            d["r"] = torch.from_numpy(np.ascontiguousarray(r[m0 * S:(m0 + mc) * S]).view(np.int64)).to(dev)
+            d["out"] = torch.empty((mc * S, 2, L, n), dtype=torch.int64, device=dev)
+            d["ws"] = torch.empty(ctx.workspace_bytes(pl) // 8, dtype=torch.int64, device=dev)
+        st.append(d)
+    dims = [(d["plan"].M, d["plan"].OH, d["plan"].OW) for d in st]
+    layout = sdist.share_layout(dims, world)
+    share_buf = torch.zeros(layout.chunk, dtype=torch.int64, device=dev)
+    for d, off in zip(st, layout.offsets):
+        if d["mc"] > 0:
+            d["y0"] = share_buf[off:off + d["mc"] * d["plan"].OH * d["plan"].OW].view(d["mc"], d["plan"].OH, d["plan"].OW)
+
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for d in st:
+        if d["mc"] > 0:
+            d["w"] = ctx.preprocess_weights(d["pl"], d["K"])
+    e1.record()
+    torch.cuda.synchronize()
+    offline_s = e0.elapsed_time(e1) / 1e3
+
+    def step_public():
+        for d in st:
+            if d["mc"] > 0:
+                ctx.he_conv2d(d["pl"], d["ct"], d["w"], x0=d["x0"], r=d["r"], out=d["out"], workspace=d["ws"])
+                ctx.extract_share(d["pl"], d["r"], out=d["y0"])
+
+    # ---- warmup (eager), then capture the step in a CUDA graph ----
+    for _ in range(max(args.warmup, 3)):
+        step_public()
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    cap = torch.cuda.Stream(dev)
+    cap.wait_stream(torch.cuda.current_stream(dev))
+    with torch.cuda.stream(cap):
+        step_public()
+    torch.cuda.current_stream(dev).wait_stream(cap)
+    torch.cuda.synchronize()
+    with torch.cuda.graph(graph, stream=cap):
+        step_public()
+    torch.cuda.synchronize()
+    for _ in range(args.warmup):
+        graph.replay()
+        sdist.all_gather_shares(share_buf, world)
+    torch.cuda.synchronize()
+
+    # ---- timed region: K graph replays (+ the share all-gather when N > 1) ----
+    K = args.steps
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    wall0 = time.perf_counter()
+    with ClockSampler(local) as clk:
+        for i in range(K):
+            evs[i][0].record()
+            graph.replay()
+            gathered = sdist.all_gather_shares(share_buf, world)
+            evs[i][1].record()
+        torch.cuda.synchronize()
+    wall = time.perf_counter() - wall0
+    if world > 1:
+        dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    total_ms = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(total_ms, op=dist.ReduceOp.MAX)
+    ms_per_step = float(total_ms.item()) / K
+
+    # ---- per-stage live timing (eager stage calls, launches pre-queued behind a sleep) ----
+    stage_ms = stage_profile(ctx, st, K, dev)
+
+    # ---- e2e: host buffers, H2D + public API + D2H every step ----
+    e2e = None if args.no_e2e else run_e2e(ctx, st, K, dev, share_buf, world)
+
+    if world > 1 and rank == 0:
+        full = sdist.reassemble(gathered, layout, dims, world)
+        assert all(f.shape[0] == M for f, (M, _, _) in zip(full, dims))
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    # ---- derived numbers ----
+    hbm_peak, peak_kind = peaks()
+    alg_bytes = sum(algorithmic_bytes(d["plan"], L, n) for d in st)
+    n_ntt = sum((d["plan"].G * d["plan"].S * world + d["plan"].M * d["plan"].S) * 2 * L for d in st)  # limb NTTs per step
+    launches_per_step = sum(4 for d in st if d["mc"] > 0)
+    sb = {s: sum(stage_bytes(d["pl"], L, n)[s] for d in st if d["mc"] > 0) for s in range(3)}
+    names = {0: "k_ntt_fwd (A6 share add + A1 NTT)", 1: "k_mac (A4 NTT-domain MAC)", 2: "k_ntt_inv (A2 INTT + A7 mask)"}
+    dom = max(range(3), key=lambda s: stage_ms[s])
+    n_layers_active = sum(1 for d in st if d["mc"] > 0)
+    achieved = sb[dom] / (stage_ms[dom] / 1e3) / 1e9
+    roofline = {"bound": "hbm", "kernel": names[dom], "achieved": round(achieved, 1), "peak": hbm_peak,
+                "unit": "GB/s", "frac": round(achieved / hbm_peak, 4), "traffic": None,
+                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+                "bytes_per_step": sb[dom], "launches_per_step": n_layers_active,
+                "avg_launch_us": round(stage_ms[dom] / n_layers_active * 1e3, 2),
+                "stage_ms": {names[s]: round(stage_ms[s], 4) for s in range(3)},
+                "stage_GBps": {names[s]: round(sb[s] / (stage_ms[s] / 1e3) / 1e9, 1) for s in range(3)}}
+    step_s = ms_per_step / 1e3
+    out = {
+        "metric": METRIC, "value": round(step_s, 7), "unit": "s", "n_gpus": world, "steps": K,
+        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded uniform cts/shares/masks, "
+        "He-normal 37-bit/scale-12 kernels)",
+        "config": {"workload": f"{args.net}: all {len(net)} conv layers at 224x224 (BASELINE.json configs[2])",
+                   "N": n, "limbs": L, "primes": [hex(q) for q in ctx.primes], "t_bits": t_bits,
+                   "parallelism": f"output-channel shards x{world}", "l2": "inputs 2.9 GB/step >> 126 MB L2 (no flush)",
+                   "timing": "CUDA events around CUDA-graph replays of the whole step"},
+        "throughput": {"ntt_per_s": round(n_ntt / step_s, 1), "alg_bytes_per_step": alg_bytes,
+                       "alg_GBps": round(alg_bytes / step_s / 1e9, 1), "hbm_frac": round(alg_bytes / step_s / 1e9 / hbm_peak, 4),
+                       "offline_preprocess_s": round(offline_s, 5), "wall_s_timed_region": round(wall, 4)},
+        "roofline": roofline,
+        "gpu_launches": launches_per_step * K,
+        "clocks": clk.summary(),
+        "e2e": e2e,
+        "context": {"paper_gpu_online_s": 2.26, "paper_gpu_hw": "RTX A6000 + Troy (PAPER.md:476)",
+                    "paper_cpu_online_s": 3.09},
+    }
+    if not args.no_cpu_baseline and world == 1:
+        out["cpu_baseline"] = cpu_baseline(st, ctx, args.cpu_frac, dev)
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def stage_profile(ctx, st, K, dev):
+    """Per-launch-group device time, CUDA events on the launching stream around each stage;
+    the whole step's launches are enqueued behind a spin kernel so no host gap is timed."""
+    stream = torch.cuda.current_stream(dev)
+
+    def run(evs):
+        for li, d in enumerate(st):
+            if d["mc"] <= 0:
+                continue
+            a = (d["pl"], d["ct"], d["w"], d["x0"], d["r"], d["out"], d["ws"])
+            evs[li][0].record(stream)
+            ctx.he_conv2d_stage(0, a[0], a[1], a[2], a[3], a[4], a[5], a[6])
+            evs[li][1].record(stream)
+            ctx.he_conv2d_stage(1, a[0], a[1], a[2], a[3], a[4], a[5], a[6])
+            evs[li][2].record(stream)
+            ctx.he_conv2d_stage(2, a[0], a[1], a[2], a[3], a[4], a[5], a[6])
+            evs[li][3].record(stream)
+            ctx.extract_share(d["pl"], d["r"], out=d["y0"])
+
+    mk = lambda: [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in st]  # noqa: E731
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    run(mk())
+    host_s = time.perf_counter() - t
+    torch.cuda.synchronize()
+    tot = [0.0, 0.0, 0.0]
+    for _ in range(K):
+        evs = mk()
+        torch.cuda._sleep(int(2.5e9 * (2 * host_s + 1e-3)))
+        run(evs)
+        torch.cuda.synchronize()
+        for li, d in enumerate(st):
+            if d["mc"] > 0:
+                for s in range(3):
+                    tot[s] += evs[li][s].elapsed_time(evs[li][s + 1])
+    return [x / K for x in tot]
+
+
+def run_e2e(ctx, st, K, dev, share_buf, world):
+    """Same metric end to end through the public API: every step copies that step's inputs
+    (ct_in, x0, r) host->device from pinned memory, runs secn_he_conv2d + the share
+    extraction per layer, and copies the output ciphertexts and shares device->host."""
+    host = []
+    h2d = d2h = 0
+    for d in st:
+        if d["mc"] <= 0:
+            continue
+        h = {k: torch.from_numpy(np.ascontiguousarray(v).view(np.int64)).pin_memory()
+             for k, v in (("ct", d["ct_h"]), ("x0", d["x0_h"]))}
+        S = d["plan"].S
+        h["r"] = torch.from_numpy(np.ascontiguousarray(d["r_h"][d["m0"] * S:(d["m0"] + d["mc"]) * S]).view(np.int64)).pin_memory()
+        h["out"] = torch.empty(d["out"].shape, dtype=torch.int64).pin_memory()
+        h["y0"] = torch.empty(d["y0"].shape, dtype=torch.int64).pin_memory()
+        h2d += sum(h[k].numel() * 8 for k in ("ct", "x0", "r"))
+        d2h += (h["out"].numel() + h["y0"].numel()) * 8
+        host.append((d, h))
+
+    def step():
+        for d, h in host:
+            d["ct"].copy_(h["ct"], non_blocking=True)
+            d["x0"].copy_(h["x0"], non_blocking=True)
+            d["r"].copy_(h["r"], non_blocking=True)
+            ctx.he_conv2d(d["pl"], d["ct"], d["w"], x0=d["x0"], r=d["r"], out=d["out"], workspace=d["ws"])
+            ctx.extract_share(d["pl"], d["r"], out=d["y0"])
+            h["out"].copy_(d["out"], non_blocking=True)
+            h["y0"].copy_(d["y0"], non_blocking=True)
+
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    a.record()
+    for _ in range(K):
+        step()
+    b.record()
+    torch.cuda.synchronize()
+    ms = torch.tensor([a.elapsed_time(b) / K], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    return {"value": round(float(ms.item()) / 1e3, 6), "unit": "s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "path": "pinned host -> secn_he_conv2d + secn_extract_share -> pinned host"}
+
+
+# ------------------------------------------------------------------------------------------
+# the oracle on the host cores (cpu_baseline and the --impl reference arm)
+
+def oracle_sample(net_states, frac, seed, check=None):
+    """Runs the oracle's server_conv on a sample of each layer's output ciphertexts and
+    extrapolates to the whole network. Returns (extrapolated seconds, measured seconds,
+    sampled outputs, total outputs, threads, parity mismatches)."""
+    from oracle import _c, he, packing
+    from oracle.params import Params
+
+    P = Params()
+    ext = meas = 0.0
+    n_s = n_t = 0
+    bad = 0
+    for li, d in enumerate(net_states):
+        lay = d["lay"]
+        opl = packing.plan_conv(lay.C, lay.H, lay.W, lay.M, lay.k, lay.k, lay.stride, lay.pad, P.n, P.L)
+        n_out = opl.M * opl.S
+        k = max(1, int(round(frac * n_out)))
+        g = inputs.rng(seed + li)
+        pick = np.sort(g.choice(n_out, size=k, replace=False))
+        sel = np.zeros(n_out, np.uint8)
+        sel[pick] = 1
+        t0 = time.perf_counter()
+        ref = he.server_conv(d["ct_h"], d["x0_h"], d["K_h"], d["r_h"], opl, P, sel=sel)
+        dt = time.perf_counter() - t0
+        meas += dt
+        ext += dt * n_out / k
+        n_s += k
+        n_t += n_out
+        if check is not None:
+            got = check(li, pick)
+            if got is not None:
+                bad += int((got != ref[pick]).sum())
+    return ext, meas, n_s, n_t, _c.lib().orc_num_threads(), bad
+
+
+def cpu_baseline(st, ctx, frac, dev):
+    def check(li, pick):
+        d = st[li]
+        if d["mc"] != d["plan"].M:
+            return None
+        torch.cuda.synchronize()
+        return d["out"][torch.from_numpy(pick).to(dev)].cpu().numpy().view(np.uint64)
+
+    ext, meas, n_s, n_t, thr, bad = oracle_sample(st, frac, 77, check)
+    return {"value": round(ext, 3), "unit": "s", "cores": thr, "kind": "oracle",
+            "sample": f"{n_s} of {n_t} output ciphertexts ({frac:.1%} per layer, >=1), measured {meas:.2f} s, "
+                      f"extrapolated per layer by outputs", "parity_mismatched_words_on_sample": bad}
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the oracle (plain C schoolbook, OpenMP) on the host cores, same metric,
+    each step a bounded sample of the workload extrapolated to the full network."""
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+    net = layers.network(args.net)
+    from oracle import packing
+    from oracle.params import Params
+
+    P = Params()
+    states = []
+    for li, lay in enumerate(net):
+        opl = packing.plan_conv(lay.C, lay.H, lay.W, lay.M, lay.k, lay.k, lay.stride, lay.pad, P.n, P.L)
+        ct, x0, K, r = layer_inputs(P.primes, P.n, P.t_bits, lay, opl.G, opl.S, opl.M, args.seed * 1000 + li)
+        states.append({"lay": lay, "ct_h": ct, "x0_h": x0, "K_h": K, "r_h": r})
+    for w in range(args.warmup):
+        oracle_sample(states, args.ref_frac / 4, 1000 + w)
+    vals, meas_tot, thr, n_s, n_t = [], 0.0, 1, 0, 0
+    for i in range(args.steps):
+        ext, meas, n_s, n_t, thr, _ = oracle_sample(states, args.ref_frac, 2000 + i)
+        vals.append(ext)
+        meas_tot += meas
+    v = statistics.mean(vals)
+    out = {"impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(v * 1e3, 1), "higher_is_better": False,
+           "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+           "config": {"workload": f"{args.net}: all {len(net)} conv layers at 224x224 (BASELINE.json configs[2])",
+                      "N": P.n, "limbs": P.L, "t_bits": P.t_bits},
+           "cpu_baseline": {"value": round(v, 3), "unit": "s", "cores": thr, "kind": "oracle",
+                            "sample": f"per step {n_s} of {n_t} output ciphertexts ({args.ref_frac:.1%} per layer), "
+                                      f"extrapolated; measured CPU time {meas_tot:.1f} s over {args.steps} steps"},
+           "e2e": {"value": round(v, 3), "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -139,6 +139,15 @@ int secn_he_conv2d(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* 
                    const uint64_t* w_ntt, const uint64_t* r, uint64_t* ct_out, void* workspace, size_t ws_bytes,
                    void* stream);
 
+/* The same computation as secn_he_conv2d, one launch group at a time, so a caller can time
+ * each kernel with events on `stream`: stage 0 = A6+A1 (ct_in, x0 -> workspace X^),
+ * stage 1 = A4 (workspace, w_ntt -> ct_out holding Y^ in the NTT domain), stage 2 = A2+A7
+ * (ct_out in place, r). Running stages 0,1,2 in order on one stream equals secn_he_conv2d.
+ * Arguments as for secn_he_conv2d; SECN_EINVAL for any other `stage`. */
+int secn_he_conv2d_stage(secn_ctx* ctx, const secn_conv_plan_t* plan, int stage, const uint64_t* ct_in,
+                         const uint64_t* x0, const uint64_t* w_ntt, const uint64_t* r, uint64_t* ct_out,
+                         void* workspace, size_t ws_bytes, void* stream);
+
 /* Server's output share at the designated coefficients (§7; Cheetah's sparse
  * result): y0[m][oy][ox] = (t - r[m*S+s][O + i*Ww + j]) mod t for the plan's
  * index map, m in [0, plan->M). r [M*S][N], y0 [M][OH][OW]. */

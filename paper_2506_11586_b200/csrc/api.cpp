@@ -372,11 +372,12 @@ size_t secn_he_conv2d_workspace(const secn_ctx* ctx, const secn_conv_plan_t* pla
   return (size_t)plan->G * plan->S * 2 * ctx->L * ctx->n * sizeof(uint64_t);
 }
 
-int secn_he_conv2d(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* ct_in, const uint64_t* x0,
-                   const uint64_t* w_ntt, const uint64_t* r, uint64_t* ct_out, void* workspace, size_t ws_bytes,
-                   void* stream) {
+static int he_conv2d_impl(secn_ctx* ctx, const secn_conv_plan_t* plan, int stage, const uint64_t* ct_in,
+                          const uint64_t* x0, const uint64_t* w_ntt, const uint64_t* r, uint64_t* ct_out,
+                          void* workspace, size_t ws_bytes, void* stream) {
   if (int st = check_ctx(ctx)) return st;
   if (int st = check_plan(ctx, plan)) return st;
+  if (stage < -1 || stage > 2) return fail(SECN_EINVAL, "stage %d not in {0,1,2}", stage);
   if (!ct_in || !w_ntt || !ct_out || !workspace) return fail(SECN_EINVAL, "NULL buffer");
   if (ws_bytes < secn_he_conv2d_workspace(ctx, plan)) return fail(SECN_EINVAL, "workspace too small");
   if (((uintptr_t)workspace | (uintptr_t)ct_in | (uintptr_t)ct_out | (uintptr_t)w_ntt) & 15)
@@ -385,15 +386,33 @@ int secn_he_conv2d(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* 
   DeviceGuard guard(ctx->device);
   cudaStream_t s = (cudaStream_t)stream;
   const size_t n_in = (size_t)plan->G * plan->S, n_out = (size_t)plan->M * plan->S, N = ctx->n;
-  if (int st = check_range(ctx, ct_in, n_in * 2 * ctx->L * N, 0, s, "secn_he_conv2d ct_in")) return st;
-  if (int st = check_range(ctx, x0, n_in * N, 1, s, "secn_he_conv2d x0")) return st;
-  if (int st = check_range(ctx, r, n_out * N, 1, s, "secn_he_conv2d r")) return st;
+  if (stage <= 0) {
+    if (int st = check_range(ctx, ct_in, n_in * 2 * ctx->L * N, 0, s, "secn_he_conv2d ct_in")) return st;
+    if (int st = check_range(ctx, x0, n_in * N, 1, s, "secn_he_conv2d x0")) return st;
+  }
+  if ((stage == -1 || stage == 2))
+    if (int st = check_range(ctx, r, n_out * N, 1, s, "secn_he_conv2d r")) return st;
   uint64_t* xhat = static_cast<uint64_t*>(workspace);
   const secn::PlanDev pd = plan_dev(plan);
-  cudaError_t e = secn::launch_ntt_fwd(ctx->dc, ct_in, xhat, n_in * 2 * ctx->L, x0, s);     // A6 + A1
-  if (e == cudaSuccess) e = secn::launch_mac(ctx->dc, pd, xhat, w_ntt, ct_out, s);           // A4
-  if (e == cudaSuccess) e = secn::launch_ntt_inv(ctx->dc, ct_out, n_out * 2 * ctx->L, r, s);  // A2 + A7
+  cudaError_t e = cudaSuccess;
+  if (stage == -1 || stage == 0) e = secn::launch_ntt_fwd(ctx->dc, ct_in, xhat, n_in * 2 * ctx->L, x0, s);  // A6+A1
+  if (e == cudaSuccess && (stage == -1 || stage == 1)) e = secn::launch_mac(ctx->dc, pd, xhat, w_ntt, ct_out, s);  // A4
+  if (e == cudaSuccess && (stage == -1 || stage == 2))
+    e = secn::launch_ntt_inv(ctx->dc, ct_out, n_out * 2 * ctx->L, r, s);  // A2+A7
   return e == cudaSuccess ? SECN_OK : cuda_fail(e, "secn_he_conv2d");
+}
+
+int secn_he_conv2d(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* ct_in, const uint64_t* x0,
+                   const uint64_t* w_ntt, const uint64_t* r, uint64_t* ct_out, void* workspace, size_t ws_bytes,
+                   void* stream) {
+  return he_conv2d_impl(ctx, plan, -1, ct_in, x0, w_ntt, r, ct_out, workspace, ws_bytes, stream);
+}
+
+int secn_he_conv2d_stage(secn_ctx* ctx, const secn_conv_plan_t* plan, int stage, const uint64_t* ct_in,
+                         const uint64_t* x0, const uint64_t* w_ntt, const uint64_t* r, uint64_t* ct_out,
+                         void* workspace, size_t ws_bytes, void* stream) {
+  if (stage < 0 || stage > 2) return fail(SECN_EINVAL, "stage %d not in {0,1,2}", stage);
+  return he_conv2d_impl(ctx, plan, stage, ct_in, x0, w_ntt, r, ct_out, workspace, ws_bytes, stream);
 }
 
 int secn_extract_share(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* r, uint64_t* y0, void* stream) {

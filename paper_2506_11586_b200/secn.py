@@ -26,7 +26,7 @@ STATUS = {0: "SECN_OK", -1: "SECN_EINVAL", -2: "SECN_EUNSUPPORTED", -3: "SECN_ER
 
 EXPORTS = ("secn_ctx_create", "secn_ctx_destroy", "secn_ctx_query", "secn_last_error", "secn_conv_plan",
            "secn_ntt_fwd", "secn_ntt_inv", "secn_preprocess_weights", "secn_share_add", "secn_mask_add",
-           "secn_he_conv2d_workspace", "secn_he_conv2d", "secn_extract_share")
+           "secn_he_conv2d_workspace", "secn_he_conv2d", "secn_he_conv2d_stage", "secn_extract_share")
 
 
 class SecnError(RuntimeError):
@@ -87,6 +87,7 @@ def lib(path=None) -> ctypes.CDLL:
         "secn_mask_add": (i, [vp, vp, vp, sz, vp]),
         "secn_he_conv2d_workspace": (sz, [vp, P]),
         "secn_he_conv2d": (i, [vp, P, vp, vp, vp, vp, vp, vp, sz, vp]),
+        "secn_he_conv2d_stage": (i, [vp, P, i, vp, vp, vp, vp, vp, vp, sz, vp]),
         "secn_extract_share": (i, [vp, P, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
@@ -203,6 +204,19 @@ class Context:
                                     _ptr(x0, (n_in, n), "x0"), _ptr(w_ntt, (plan.M, plan.G, L, n), "w_ntt"),
                                     _ptr(r, (n_out, n), "r"), _ptr(out, (n_out, 2, L, n), "ct_out"),
                                     _ptr(workspace, None, "workspace"), workspace.numel() * 8, self._stream(stream)))
+        return out
+
+    def he_conv2d_stage(self, stage: int, plan: Plan, ct_in: torch.Tensor, w_ntt: torch.Tensor,
+                        x0: Optional[torch.Tensor], r: Optional[torch.Tensor], out: torch.Tensor,
+                        workspace: torch.Tensor, stream=None) -> torch.Tensor:
+        """One launch group of secn_he_conv2d (0: share add + NTT, 1: MAC, 2: INTT + mask)."""
+        L, n = self.L, self.n
+        n_in, n_out = plan.G * plan.S, plan.M * plan.S
+        _check(lib().secn_he_conv2d_stage(self._h, ctypes.byref(plan), stage, _ptr(ct_in, (n_in, 2, L, n), "ct_in"),
+                                          _ptr(x0, (n_in, n), "x0"), _ptr(w_ntt, (plan.M, plan.G, L, n), "w_ntt"),
+                                          _ptr(r, (n_out, n), "r"), _ptr(out, (n_out, 2, L, n), "ct_out"),
+                                          _ptr(workspace, None, "workspace"), workspace.numel() * 8,
+                                          self._stream(stream)))
         return out
 
     def extract_share(self, plan: Plan, r: torch.Tensor, out: Optional[torch.Tensor] = None,
