@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["secn", "reference"], default="secn")
     ap.add_argument("--net", default="squeezenet1_1")
+    ap.add_argument("--word-bits", type=int, choices=[32, 64], default=64,
+                    help="64: paper parameters (q 60+49 bit, uint64 limbs); 32: four 27-bit uint32 limbs")
     ap.add_argument("--seed", type=int, default=3)
     ap.add_argument("--cpu-frac", type=float, default=0.05, help="oracle sample fraction for cpu_baseline")
     ap.add_argument("--ref-frac", type=float, default=0.01, help="oracle sample fraction per --impl reference step")
@@ -127,19 +129,19 @@ def layer_inputs(P_primes, n, t_bits, lay, opl_G, opl_S, M, seed):
     return ct, x0, K, r
 
 
-def algorithmic_bytes(plan, L, n):
-    """SURVEY.md §8d per-layer bytes: 8 L N (2GS + MG + 2MS) + 8 N MS (+ 8 N GS for x0)."""
+def algorithmic_bytes(plan, L, n, wbytes=8):
+    """SURVEY.md §8d per-layer bytes: wb L N (2GS + MG + 2MS) + 8 N MS (+ 8 N GS for x0)."""
     G, S, M = plan.G, plan.S, plan.M
-    return 8 * L * n * (2 * G * S + M * G + 2 * M * S) + 8 * n * M * S + 8 * n * G * S
+    return wbytes * L * n * (2 * G * S + M * G + 2 * M * S) + 8 * n * M * S + 8 * n * G * S
 
 
-def stage_bytes(plan, L, n):
+def stage_bytes(plan, L, n, wbytes=8):
     """Bytes each launch group reads + writes (its own roofline numerator)."""
     G, S, M = plan.G, plan.S, plan.M
-    ct_in = 2 * G * S * L * n * 8
+    ct_in = 2 * G * S * L * n * wbytes
     x0 = G * S * n * 8
-    w = M * G * L * n * 8
-    y = 2 * M * S * L * n * 8
+    w = M * G * L * n * wbytes
+    y = 2 * M * S * L * n * wbytes
     r = M * S * n * 8
     return {0: ct_in + x0 + ct_in, 1: w + ct_in + y, 2: y + r + y}
 
@@ -164,8 +166,13 @@ def main():
         __graft_entry__.build()
     if world > 1:
         dist.barrier()
-    ctx = Context(local)
+    ctx = Context(local, word_bits=args.word_bits)
     L, n, t_bits = ctx.L, ctx.n, ctx.t_bits
+    wbytes = ctx.word_bits // 8
+
+    def R(a):  # residues -> device tensor of the context's word size
+        a = np.ascontiguousarray(a)
+        return torch.from_numpy(a.view(np.int64) if wbytes == 8 else a.astype(np.uint32).view(np.int32)).to(dev)
     net = layers.network(args.net)
 
     # ---- setup: plans, inputs, offline weight preprocessing (timed separately) ----
@@ -179,11 +186,11 @@ def main():
         if mc > 0:
             pl = plan.copy(M=mc)
             d["pl"] = pl
-            d["ct"] = torch.from_numpy(ct.view(np.int64)).to(dev)
+            d["ct"] = R(ct)
             d["x0"] = torch.from_numpy(x0.view(np.int64)).to(dev)
             d["K"] = torch.from_numpy(np.ascontiguousarray(K[m0:m0 + mc]).view(np.int64)).to(dev)
             d["r"] = torch.from_numpy(np.ascontiguousarray(r[m0 * S:(m0 + mc) * S]).view(np.int64)).to(dev)
-            d["out"] = torch.empty((mc * S, 2, L, n), dtype=torch.int64, device=dev)
+            d["out"] = ctx.empty(mc * S, 2, L, n)
             d["ws"] = torch.empty(ctx.workspace_bytes(pl) // 8, dtype=torch.int64, device=dev)
         st.append(d)
     dims = [(d["plan"].M, d["plan"].OH, d["plan"].OW) for d in st]
@@ -269,10 +276,10 @@ def main():
 
     # ---- derived numbers ----
     hbm_peak, peak_kind = peaks()
-    alg_bytes = sum(algorithmic_bytes(d["plan"], L, n) for d in st)
+    alg_bytes = sum(algorithmic_bytes(d["plan"], L, n, wbytes) for d in st)
     n_ntt = sum((d["plan"].G * d["plan"].S * world + d["plan"].M * d["plan"].S) * 2 * L for d in st)  # limb NTTs per step
     launches_per_step = sum(4 for d in st if d["mc"] > 0)
-    sb = {s: sum(stage_bytes(d["pl"], L, n)[s] for d in st if d["mc"] > 0) for s in range(3)}
+    sb = {s: sum(stage_bytes(d["pl"], L, n, wbytes)[s] for d in st if d["mc"] > 0) for s in range(3)}
     names = {0: "k_ntt_fwd (A6 share add + A1 NTT)", 1: "k_mac (A4 NTT-domain MAC)", 2: "k_ntt_inv (A2 INTT + A7 mask)"}
     dom = max(range(3), key=lambda s: stage_ms[s])
     n_layers_active = sum(1 for d in st if d["mc"] > 0)
@@ -288,7 +295,7 @@ def main():
     out = {
         "metric": METRIC, "value": round(step_s, 7), "unit": "s", "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": False,
-        "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded uniform cts/shares/masks, "
+        "scaling": "strong", "vs_baseline": None, "dtype": f"u{ctx.word_bits}", "data": "synthetic (seeded uniform cts/shares/masks, "
         "He-normal 37-bit/scale-12 kernels)",
         "config": {"workload": f"{args.net}: all {len(net)} conv layers at 224x224 (BASELINE.json configs[2])",
                    "N": n, "limbs": L, "primes": [hex(q) for q in ctx.primes], "t_bits": t_bits,
@@ -305,7 +312,7 @@ def main():
                     "paper_cpu_online_s": 3.09},
     }
     if not args.no_cpu_baseline and world == 1:
-        out["cpu_baseline"] = cpu_baseline(st, ctx, args.cpu_frac, dev)
+        out["cpu_baseline"] = cpu_baseline(st, ctx, args.cpu_frac, dev, wbytes)
     print(json.dumps(out), flush=True)
     if world > 1:
         dist.barrier()
@@ -400,20 +407,20 @@ def run_e2e(ctx, st, K, dev, share_buf, world):
 # ------------------------------------------------------------------------------------------
 # the oracle on the host cores (cpu_baseline and the --impl reference arm)
 
-def oracle_sample(net_states, frac, seed, check=None):
+def oracle_sample(net_states, frac, seed, check=None, primes=None, words64=2):
     """Runs the oracle's server_conv on a sample of each layer's output ciphertexts and
     extrapolates to the whole network. Returns (extrapolated seconds, measured seconds,
     sampled outputs, total outputs, threads, parity mismatches)."""
     from oracle import _c, he, packing
     from oracle.params import Params
 
-    P = Params()
+    P = Params() if primes is None else Params(primes=primes)
     ext = meas = 0.0
     n_s = n_t = 0
     bad = 0
     for li, d in enumerate(net_states):
         lay = d["lay"]
-        opl = packing.plan_conv(lay.C, lay.H, lay.W, lay.M, lay.k, lay.k, lay.stride, lay.pad, P.n, P.L)
+        opl = packing.plan_conv(lay.C, lay.H, lay.W, lay.M, lay.k, lay.k, lay.stride, lay.pad, P.n, words64)
         n_out = opl.M * opl.S
         k = max(1, int(round(frac * n_out)))
         g = inputs.rng(seed + li)
@@ -434,15 +441,16 @@ def oracle_sample(net_states, frac, seed, check=None):
     return ext, meas, n_s, n_t, _c.lib().orc_num_threads(), bad
 
 
-def cpu_baseline(st, ctx, frac, dev):
+def cpu_baseline(st, ctx, frac, dev, wbytes):
     def check(li, pick):
         d = st[li]
         if d["mc"] != d["plan"].M:
             return None
         torch.cuda.synchronize()
-        return d["out"][torch.from_numpy(pick).to(dev)].cpu().numpy().view(np.uint64)
+        x = d["out"][torch.from_numpy(pick).to(dev)].cpu().numpy()
+        return x.view(np.uint64) if wbytes == 8 else x.view(np.uint32).astype(np.uint64)
 
-    ext, meas, n_s, n_t, thr, bad = oracle_sample(st, frac, 77, check)
+    ext, meas, n_s, n_t, thr, bad = oracle_sample(st, frac, 77, check, ctx.primes, ctx.coef_words64)
     return {"value": round(ext, 3), "unit": "s", "cores": thr, "kind": "oracle",
             "sample": f"{n_s} of {n_t} output ciphertexts ({frac:.1%} per layer, >=1), measured {meas:.2f} s, "
                       f"extrapolated per layer by outputs", "parity_mismatched_words_on_sample": bad}
@@ -460,23 +468,26 @@ def run_reference(args, world, rank):
     from oracle import packing
     from oracle.params import Params
 
-    P = Params()
+    from oracle import params as oparams
+
+    P = Params(primes=oparams.DEFAULT_PRIMES if args.word_bits == 64 else oparams.PRIMES32)
+    words64 = max(1, P.L * args.word_bits // 64)
     states = []
     for li, lay in enumerate(net):
-        opl = packing.plan_conv(lay.C, lay.H, lay.W, lay.M, lay.k, lay.k, lay.stride, lay.pad, P.n, P.L)
+        opl = packing.plan_conv(lay.C, lay.H, lay.W, lay.M, lay.k, lay.k, lay.stride, lay.pad, P.n, words64)
         ct, x0, K, r = layer_inputs(P.primes, P.n, P.t_bits, lay, opl.G, opl.S, opl.M, args.seed * 1000 + li)
         states.append({"lay": lay, "ct_h": ct, "x0_h": x0, "K_h": K, "r_h": r})
     for w in range(args.warmup):
-        oracle_sample(states, args.ref_frac / 4, 1000 + w)
+        oracle_sample(states, args.ref_frac / 4, 1000 + w, None, P.primes, words64)
     vals, meas_tot, thr, n_s, n_t = [], 0.0, 1, 0, 0
     for i in range(args.steps):
-        ext, meas, n_s, n_t, thr, _ = oracle_sample(states, args.ref_frac, 2000 + i)
+        ext, meas, n_s, n_t, thr, _ = oracle_sample(states, args.ref_frac, 2000 + i, None, P.primes, words64)
         vals.append(ext)
         meas_tot += meas
     v = statistics.mean(vals)
     out = {"impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "s", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(v * 1e3, 1), "higher_is_better": False,
-           "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+           "scaling": "strong", "vs_baseline": None, "dtype": f"u{ctx.word_bits}", "data": "synthetic",
            "config": {"workload": f"{args.net}: all {len(net)} conv layers at 224x224 (BASELINE.json configs[2])",
                       "N": P.n, "limbs": P.L, "t_bits": P.t_bits},
            "cpu_baseline": {"value": round(v, 3), "unit": "s", "cores": thr, "kind": "oracle",

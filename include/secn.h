@@ -80,6 +80,7 @@ typedef struct {
   uint64_t primes[SECN_MAX_LIMBS];
   uint64_t psi[SECN_MAX_LIMBS]; /* minimal primitive 2N-th roots (reading R4)              */
   int device;
+  uint32_t word_bits; /* 64: secn_* residue calls (uint64 words); 32: secn32_* calls (uint32)    */
 } secn_ctx_info;
 
 /* Creates a context on CUDA device `device`: copies the primes, finds psi_j, and builds the
@@ -93,10 +94,12 @@ int secn_ctx_destroy(secn_ctx* ctx);
 int secn_ctx_query(const secn_ctx* ctx, secn_ctx_info* info);
 const char* secn_last_error(void);
 
-/* Host only. Fills `p` from its geometry for ring degree 2^log_n and n_limbs limbs using the
- * byte-min rule of reading R6 (or validates the caller's Hw,Ww when both are nonzero).
+/* Host only. Fills `p` from its geometry for ring degree 2^log_n using the byte-min rule of
+ * reading R6 (or validates the caller's Hw,Ww when both are nonzero). coef_words64 = 8-byte
+ * words per coefficient of one ciphertext component (L for 64-bit limbs, L/2 for 32-bit limbs);
+ * it only weighs residue bytes against the 8-byte mask words in the byte model.
  * SECN_EUNSUPPORTED if no window fits (kh*kw > N or Hp < kh). */
-int secn_conv_plan(uint32_t log_n, uint32_t n_limbs, secn_conv_plan_t* p);
+int secn_conv_plan(uint32_t log_n, uint32_t coef_words64, secn_conv_plan_t* p);
 
 /* A1: in-place forward negacyclic NTT of n_polys polys [n_polys][L][N] (coefficient domain ->
  * NTT domain), PAPER.md:378-380 (§6.2), App. C.1. */
@@ -121,7 +124,7 @@ int secn_share_add(secn_ctx* ctx, uint64_t* ct, const uint64_t* x0, size_t n, vo
 int secn_mask_add(secn_ctx* ctx, uint64_t* ct, const uint64_t* r, size_t n, void* stream);
 
 /* Bytes of device workspace secn_he_conv2d needs for `plan` (the NTT-domain inputs
- * X^ = G*S*2*L*N*8 bytes). */
+ * X^ = G*S*2*L*N words of the context's word size). */
 size_t secn_he_conv2d_workspace(const secn_ctx* ctx, const secn_conv_plan_t* plan);
 
 /* The hot path (PAPER.md:380 §6.2, :431 §7), one layer:
@@ -152,6 +155,31 @@ int secn_he_conv2d_stage(secn_ctx* ctx, const secn_conv_plan_t* plan, int stage,
  * result): y0[m][oy][ox] = (t - r[m*S+s][O + i*Ww + j]) mod t for the plan's
  * index map, m in [0, plan->M). r [M*S][N], y0 [M][OH][OW]. */
 int secn_extract_share(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* r, uint64_t* y0, void* stream);
+
+/* ------------------------------------------------------------------------------------------
+ * 32-bit RNS limbs (reading R1b). Identical semantics to the
+ * calls above with residues stored as uint32 ([..][L][N] uint32 words) for moduli q_j < 2^28,
+ * e.g. four 27-bit primes = 1 mod 2^16 (Q = 108 bits <= 109, the 128-bit-security bound for
+ * N = 4096). The same bytes per coefficient as two 64-bit limbs, but every modular product is a
+ * 32x32-bit Shoup/IMAD.WIDE operation. Plaintext-side arrays (x0, r, kernels, y0) stay uint64.
+ * A 32-bit context rejects the 64-bit residue calls (and vice versa) with SECN_ESTATE;
+ * secn_ctx_destroy/query, secn_conv_plan, secn_he_conv2d_workspace (bytes for the context's word
+ * size) and secn_extract_share serve both.
+ * ------------------------------------------------------------------------------------------ */
+int secn32_ctx_create(secn_ctx** out, int device, uint32_t log_n, uint32_t n_limbs, const uint32_t* primes,
+                      uint32_t t_bits);
+int secn32_ntt_fwd(secn_ctx* ctx, uint32_t* polys, size_t n_polys, void* stream);
+int secn32_ntt_inv(secn_ctx* ctx, uint32_t* polys, size_t n_polys, void* stream);
+int secn32_preprocess_weights(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* kernel, uint32_t* w_ntt,
+                              void* stream);
+int secn32_share_add(secn_ctx* ctx, uint32_t* ct, const uint64_t* x0, size_t n, void* stream);
+int secn32_mask_add(secn_ctx* ctx, uint32_t* ct, const uint64_t* r, size_t n, void* stream);
+int secn32_he_conv2d(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint32_t* ct_in, const uint64_t* x0,
+                     const uint32_t* w_ntt, const uint64_t* r, uint32_t* ct_out, void* workspace, size_t ws_bytes,
+                     void* stream);
+int secn32_he_conv2d_stage(secn_ctx* ctx, const secn_conv_plan_t* plan, int stage, const uint32_t* ct_in,
+                           const uint64_t* x0, const uint32_t* w_ntt, const uint64_t* r, uint32_t* ct_out,
+                           void* workspace, size_t ws_bytes, void* stream);
 
 #ifdef __cplusplus
 }

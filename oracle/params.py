@@ -76,6 +76,8 @@ def minimal_psi(q: int, n: int) -> int:
 DEFAULT_PRIMES = (0x0FFFFFFFFFFFC001, 0x1FFFFFFFCE001)
 ALT54_PRIMES = (0x3FFFFFFFFD6001, 0x3FFFFFFFFD2001)
 SWEEP_PRIMES = (0xFFFFFFFFFFC0001, 0xFFFFFFFFF840001, 0xFFFFFFFFF6A0001, 0xFFFFFFFFF5A0001)
+# Reading R1b: 32-bit RNS limbs -- the four largest 27-bit primes = 1 (mod 2^16); Q = 108 bits.
+PRIMES32 = (0x7E90001, 0x7E00001, 0x7DD0001, 0x7D70001)
 
 
 @dataclass

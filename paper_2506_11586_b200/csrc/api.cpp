@@ -108,7 +108,7 @@ bool validate_env() {
 
 // With SECN_VALIDATE=1: synchronously check that `n_words` words are in range
 // (kind 0: residues < q_j by limb, kind 1: < 2^t_bits).
-int check_range(secn_ctx* ctx, const uint64_t* v, size_t n_words, int kind, cudaStream_t s, const char* what) {
+int check_range(secn_ctx* ctx, const void* v, size_t n_words, int kind, cudaStream_t s, const char* what) {
   if (!validate_env() || v == nullptr || n_words == 0) return SECN_OK;
   cudaError_t e = cudaMemsetAsync(ctx->d_flag, 0, sizeof(uint32_t), s);
   if (e == cudaSuccess) e = secn::launch_check_range(ctx->dc, v, n_words, kind, ctx->d_flag, s);
@@ -152,8 +152,11 @@ int derive_plan(uint32_t n, uint32_t Hw, uint32_t Ww, secn_conv_plan_t* p) {
   return 0;
 }
 
-int check_ctx(const secn_ctx* ctx) {
+int check_ctx(const secn_ctx* ctx, uint32_t want_bits = 0) {
   if (!ctx) return fail(SECN_EINVAL, "NULL context");
+  if (want_bits && ctx->word_bits != want_bits)
+    return fail(SECN_ESTATE, "context has %u-bit residues; use the secn%s_ entry points", ctx->word_bits,
+                ctx->word_bits == 32 ? "32" : "");
   int dev;
   if (cudaGetDevice(&dev) != cudaSuccess) return fail(SECN_ESTATE, "no current CUDA device");
   return SECN_OK;
@@ -175,18 +178,19 @@ extern "C" {
 
 const char* secn_last_error(void) { return g_err.c_str(); }
 
-int secn_ctx_create(secn_ctx** out, int device, uint32_t log_n, uint32_t n_limbs, const uint64_t* primes,
-                    uint32_t t_bits) {
+static int ctx_create_impl(secn_ctx** out, int device, uint32_t log_n, uint32_t n_limbs, const uint64_t* primes,
+                           uint32_t t_bits, uint32_t word_bits) {
   if (!out || !primes) return fail(SECN_EINVAL, "NULL argument");
   *out = nullptr;
   if (log_n < 12 || log_n > 14) return fail(SECN_EUNSUPPORTED, "log_n=%u not in [12,14]", log_n);
   if (n_limbs < 1 || n_limbs > SECN_MAX_LIMBS) return fail(SECN_EUNSUPPORTED, "n_limbs=%u not in [1,4]", n_limbs);
   if (t_bits < 1 || t_bits > 44) return fail(SECN_EUNSUPPORTED, "t_bits=%u not in [1,44]", t_bits);
   const uint64_t n = 1ull << log_n;
+  const uint64_t qmax = word_bits == 64 ? (1ull << 61) : (1ull << 28);
   for (uint32_t j = 0; j < n_limbs; ++j) {
     const uint64_t q = primes[j];
-    if (q >= (1ull << 61)) return fail(SECN_EUNSUPPORTED, "prime %u >= 2^61", j);
-    if (q <= (1ull << t_bits)) return fail(SECN_EUNSUPPORTED, "prime %u <= 2^t_bits", j);
+    if (q >= qmax) return fail(SECN_EUNSUPPORTED, "prime %u >= 2^%d", j, word_bits == 64 ? 61 : 28);
+    if (word_bits == 64 && q <= (1ull << t_bits)) return fail(SECN_EUNSUPPORTED, "prime %u <= 2^t_bits", j);
     if ((q - 1) % (2 * n) != 0) return fail(SECN_EUNSUPPORTED, "prime %u != 1 mod 2N", j);
     if (!probable_prime(q)) return fail(SECN_EUNSUPPORTED, "modulus %u is not prime", j);
     for (uint32_t k = 0; k < j; ++k)
@@ -199,35 +203,46 @@ int secn_ctx_create(secn_ctx** out, int device, uint32_t log_n, uint32_t n_limbs
 
   secn_ctx* c = new secn_ctx();
   c->device = device, c->log_n = log_n, c->n = (uint32_t)n, c->L = n_limbs, c->t_bits = t_bits;
+  c->word_bits = word_bits;
   secn::DevConsts& dc = c->dc;
   std::memset(&dc, 0, sizeof dc);
-  dc.t_bits = t_bits, dc.log_n = log_n, dc.L = n_limbs;
+  dc.t_bits = t_bits, dc.log_n = log_n, dc.L = n_limbs, dc.word_bits = word_bits;
   const uint64_t t = 1ull << t_bits, tmask = t - 1;
   // Q mod t = prod (q_j mod t) mod t (t a power of two)
   uint64_t qmt = 1;
   for (uint32_t j = 0; j < n_limbs; ++j) qmt = (uint64_t)(((u128)qmt * (primes[j] & tmask)) & tmask);
   dc.qmt = qmt;
-
-  std::vector<ulonglong2> tw((size_t)2 * n_limbs * n);
+  // Shoup companion over the word size
+  auto comp = [&](uint64_t w, uint64_t q) {
+    return word_bits == 64 ? shoup_companion(w, q) : (uint64_t)((((u128)w) << 32) / q);
+  };
+  const size_t tw_bytes = (word_bits == 64 ? sizeof(ulonglong2) : sizeof(uint2)) * 2 * n_limbs * n;
+  std::vector<unsigned char> tw(tw_bytes);
+  ulonglong2* tw64 = reinterpret_cast<ulonglong2*>(tw.data());
+  uint2* tw32 = reinterpret_cast<uint2*>(tw.data());
   for (uint32_t j = 0; j < n_limbs; ++j) {
     const uint64_t q = primes[j];
     c->primes[j] = q;
     const uint64_t psi = min_primitive_root(q, n);
     c->psi[j] = psi;
     const uint64_t psi_inv = powmod(psi, q - 2, q);
-    ulonglong2* fw = &tw[(size_t)j * n];
-    ulonglong2* iv = &tw[((size_t)n_limbs + j) * n];
     for (uint32_t i = 0; i < n; ++i) {
       const uint32_t e = bitrev(i, log_n);
       const uint64_t wf = powmod(psi, e, q), wi = powmod(psi_inv, e, q);
-      fw[i] = make_ulonglong2(wf, shoup_companion(wf, q));
-      iv[i] = make_ulonglong2(wi, shoup_companion(wi, q));
+      const size_t fi = (size_t)j * n + i, ii = ((size_t)n_limbs + j) * n + i;
+      if (word_bits == 64) {
+        tw64[fi] = make_ulonglong2(wf, comp(wf, q));
+        tw64[ii] = make_ulonglong2(wi, comp(wi, q));
+      } else {
+        tw32[fi] = make_uint2((uint32_t)wf, (uint32_t)comp(wf, q));
+        tw32[ii] = make_uint2((uint32_t)wi, (uint32_t)comp(wi, q));
+      }
     }
-    dc.q[j] = q, dc.q2[j] = 2 * q;
+    dc.q[j] = q;
     const uint64_t ninv = powmod(n % q, q - 2, q);
-    dc.ninv[j] = ninv, dc.ninv_p[j] = shoup_companion(ninv, q);
-    const uint64_t wl = mulmod(iv[1].x, ninv, q);
-    dc.wlast[j] = wl, dc.wlast_p[j] = shoup_companion(wl, q);
+    dc.ninv[j] = ninv, dc.ninv_p[j] = comp(ninv, q);
+    const uint64_t wl = mulmod(powmod(psi_inv, bitrev(1, log_n), q), ninv, q);
+    dc.wlast[j] = wl, dc.wlast_p[j] = comp(wl, q);
     // floor(Q/t) = (Q - (Q mod t)) / t and Q = 0 mod q_j  =>  floor(Q/t) = -(Q mod t) t^-1 mod q_j
     const uint64_t tinv = powmod(t % q, q - 2, q);
     const uint64_t delta = mulmod((q - qmt % q) % q, tinv, q);
@@ -236,23 +251,40 @@ int secn_ctx_create(secn_ctx** out, int device, uint32_t log_n, uint32_t n_limbs
     dc.r64[j] = r64, dc.r64_p[j] = shoup_companion(r64, q);
     dc.one_p[j] = ~0ull / q;
   }
-  const size_t bytes = tw.size() * sizeof(ulonglong2);
-  cudaError_t e = cudaMalloc(&c->d_tables, bytes);
+  cudaError_t e = cudaMalloc(&c->d_tables, tw_bytes);
   if (e != cudaSuccess) {
     delete c;
     return fail(e == cudaErrorMemoryAllocation ? SECN_ENOMEM : SECN_ECUDA, "cudaMalloc tables: %s", cudaGetErrorString(e));
   }
   e = cudaMalloc(&c->d_flag, sizeof(uint32_t));
-  if (e == cudaSuccess) e = cudaMemcpy(c->d_tables, tw.data(), bytes, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(c->d_tables, tw.data(), tw_bytes, cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
     cudaFree(c->d_tables);
     delete c;
     return cuda_fail(e, "ctx tables");
   }
-  dc.tw_fwd = static_cast<const ulonglong2*>(c->d_tables);
-  dc.tw_inv = dc.tw_fwd + (size_t)n_limbs * n;
+  if (word_bits == 64) {
+    dc.tw_fwd = static_cast<const ulonglong2*>(c->d_tables);
+    dc.tw_inv = dc.tw_fwd + (size_t)n_limbs * n;
+  } else {
+    dc.tw32_fwd = static_cast<const uint2*>(c->d_tables);
+    dc.tw32_inv = dc.tw32_fwd + (size_t)n_limbs * n;
+  }
   *out = c;
   return SECN_OK;
+}
+
+int secn_ctx_create(secn_ctx** out, int device, uint32_t log_n, uint32_t n_limbs, const uint64_t* primes,
+                    uint32_t t_bits) {
+  return ctx_create_impl(out, device, log_n, n_limbs, primes, t_bits, 64);
+}
+
+int secn32_ctx_create(secn_ctx** out, int device, uint32_t log_n, uint32_t n_limbs, const uint32_t* primes,
+                      uint32_t t_bits) {
+  if (!primes) return fail(SECN_EINVAL, "NULL argument");
+  uint64_t p64[SECN_MAX_LIMBS] = {0, 0, 0, 0};
+  for (uint32_t j = 0; j < n_limbs && j < SECN_MAX_LIMBS; ++j) p64[j] = primes[j];
+  return ctx_create_impl(out, device, log_n, n_limbs, p64, t_bits, 32);
 }
 
 int secn_ctx_destroy(secn_ctx* ctx) {
@@ -269,11 +301,12 @@ int secn_ctx_query(const secn_ctx* ctx, secn_ctx_info* info) {
   std::memset(info, 0, sizeof *info);
   info->log_n = ctx->log_n, info->n = ctx->n, info->n_limbs = ctx->L, info->t_bits = ctx->t_bits;
   info->device = ctx->device;
+  info->word_bits = ctx->word_bits;
   for (uint32_t j = 0; j < ctx->L; ++j) info->primes[j] = ctx->primes[j], info->psi[j] = ctx->psi[j];
   return SECN_OK;
 }
 
-int secn_conv_plan(uint32_t log_n, uint32_t n_limbs, secn_conv_plan_t* p) {
+int secn_conv_plan(uint32_t log_n, uint32_t n_limbs /* coef_words64 */, secn_conv_plan_t* p) {
   if (!p) return fail(SECN_EINVAL, "NULL plan");
   if (log_n < 1 || log_n > 20 || n_limbs < 1) return fail(SECN_EUNSUPPORTED, "bad log_n / n_limbs");
   const uint32_t n = 1u << log_n;
@@ -312,29 +345,22 @@ int secn_conv_plan(uint32_t log_n, uint32_t n_limbs, secn_conv_plan_t* p) {
   return SECN_OK;
 }
 
-int secn_ntt_fwd(secn_ctx* ctx, uint64_t* polys, size_t n_polys, void* stream) {
-  if (int st = check_ctx(ctx)) return st;
+// ---- residue-buffer calls, generic over the context's word size ----
+static int ntt_impl(secn_ctx* ctx, uint32_t bits, void* polys, size_t n_polys, void* stream, bool inverse) {
+  if (int st = check_ctx(ctx, bits)) return st;
   if (n_polys && !polys) return fail(SECN_EINVAL, "NULL polys");
   DeviceGuard guard(ctx->device);
   cudaStream_t s = (cudaStream_t)stream;
-  if (int st = check_range(ctx, polys, n_polys * ctx->L * ctx->n, 0, s, "secn_ntt_fwd")) return st;
-  cudaError_t e = secn::launch_ntt_fwd(ctx->dc, polys, polys, n_polys * ctx->L, nullptr, s);
-  return e == cudaSuccess ? SECN_OK : cuda_fail(e, "secn_ntt_fwd");
+  const char* name = inverse ? "secn_ntt_inv" : "secn_ntt_fwd";
+  if (int st = check_range(ctx, polys, n_polys * ctx->L * ctx->n, 0, s, name)) return st;
+  cudaError_t e = inverse ? secn::launch_ntt_inv(ctx->dc, polys, n_polys * ctx->L, nullptr, s)
+                          : secn::launch_ntt_fwd(ctx->dc, polys, polys, n_polys * ctx->L, nullptr, s);
+  return e == cudaSuccess ? SECN_OK : cuda_fail(e, name);
 }
 
-int secn_ntt_inv(secn_ctx* ctx, uint64_t* polys, size_t n_polys, void* stream) {
-  if (int st = check_ctx(ctx)) return st;
-  if (n_polys && !polys) return fail(SECN_EINVAL, "NULL polys");
-  DeviceGuard guard(ctx->device);
-  cudaStream_t s = (cudaStream_t)stream;
-  if (int st = check_range(ctx, polys, n_polys * ctx->L * ctx->n, 0, s, "secn_ntt_inv")) return st;
-  cudaError_t e = secn::launch_ntt_inv(ctx->dc, polys, n_polys * ctx->L, nullptr, s);
-  return e == cudaSuccess ? SECN_OK : cuda_fail(e, "secn_ntt_inv");
-}
-
-int secn_preprocess_weights(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* kernel, uint64_t* w_ntt,
-                            void* stream) {
-  if (int st = check_ctx(ctx)) return st;
+static int preprocess_impl(secn_ctx* ctx, uint32_t bits, const secn_conv_plan_t* plan, const uint64_t* kernel,
+                           void* w_ntt, void* stream) {
+  if (int st = check_ctx(ctx, bits)) return st;
   if (int st = check_plan(ctx, plan)) return st;
   if (!kernel || !w_ntt) return fail(SECN_EINVAL, "NULL buffer");
   DeviceGuard guard(ctx->device);
@@ -347,42 +373,68 @@ int secn_preprocess_weights(secn_ctx* ctx, const secn_conv_plan_t* plan, const u
   return e == cudaSuccess ? SECN_OK : cuda_fail(e, "secn_preprocess_weights");
 }
 
-int secn_share_add(secn_ctx* ctx, uint64_t* ct, const uint64_t* x0, size_t n, void* stream) {
-  if (int st = check_ctx(ctx)) return st;
-  if (n && (!ct || !x0)) return fail(SECN_EINVAL, "NULL buffer");
+static int enc_add_impl(secn_ctx* ctx, uint32_t bits, void* ct, const uint64_t* v, size_t n, void* stream,
+                        const char* name) {
+  if (int st = check_ctx(ctx, bits)) return st;
+  if (n && (!ct || !v)) return fail(SECN_EINVAL, "NULL buffer");
   DeviceGuard guard(ctx->device);
   cudaStream_t s = (cudaStream_t)stream;
-  if (int st = check_range(ctx, x0, n * ctx->n, 1, s, "secn_share_add x0")) return st;
-  cudaError_t e = secn::launch_enc_add(ctx->dc, ct, x0, n, s);
-  return e == cudaSuccess ? SECN_OK : cuda_fail(e, "secn_share_add");
+  if (int st = check_range(ctx, v, n * ctx->n, 1, s, name)) return st;
+  cudaError_t e = secn::launch_enc_add(ctx->dc, ct, v, n, s);
+  return e == cudaSuccess ? SECN_OK : cuda_fail(e, name);
 }
 
+int secn_ntt_fwd(secn_ctx* ctx, uint64_t* polys, size_t n_polys, void* stream) {
+  return ntt_impl(ctx, 64, polys, n_polys, stream, false);
+}
+int secn_ntt_inv(secn_ctx* ctx, uint64_t* polys, size_t n_polys, void* stream) {
+  return ntt_impl(ctx, 64, polys, n_polys, stream, true);
+}
+int secn32_ntt_fwd(secn_ctx* ctx, uint32_t* polys, size_t n_polys, void* stream) {
+  return ntt_impl(ctx, 32, polys, n_polys, stream, false);
+}
+int secn32_ntt_inv(secn_ctx* ctx, uint32_t* polys, size_t n_polys, void* stream) {
+  return ntt_impl(ctx, 32, polys, n_polys, stream, true);
+}
+
+int secn_preprocess_weights(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* kernel, uint64_t* w_ntt,
+                            void* stream) {
+  return preprocess_impl(ctx, 64, plan, kernel, w_ntt, stream);
+}
+int secn32_preprocess_weights(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* kernel, uint32_t* w_ntt,
+                              void* stream) {
+  return preprocess_impl(ctx, 32, plan, kernel, w_ntt, stream);
+}
+
+int secn_share_add(secn_ctx* ctx, uint64_t* ct, const uint64_t* x0, size_t n, void* stream) {
+  return enc_add_impl(ctx, 64, ct, x0, n, stream, "secn_share_add");
+}
 int secn_mask_add(secn_ctx* ctx, uint64_t* ct, const uint64_t* r, size_t n, void* stream) {
-  if (int st = check_ctx(ctx)) return st;
-  if (n && (!ct || !r)) return fail(SECN_EINVAL, "NULL buffer");
-  DeviceGuard guard(ctx->device);
-  cudaStream_t s = (cudaStream_t)stream;
-  if (int st = check_range(ctx, r, n * ctx->n, 1, s, "secn_mask_add r")) return st;
-  cudaError_t e = secn::launch_enc_add(ctx->dc, ct, r, n, s);
-  return e == cudaSuccess ? SECN_OK : cuda_fail(e, "secn_mask_add");
+  return enc_add_impl(ctx, 64, ct, r, n, stream, "secn_mask_add");
+}
+int secn32_share_add(secn_ctx* ctx, uint32_t* ct, const uint64_t* x0, size_t n, void* stream) {
+  return enc_add_impl(ctx, 32, ct, x0, n, stream, "secn32_share_add");
+}
+int secn32_mask_add(secn_ctx* ctx, uint32_t* ct, const uint64_t* r, size_t n, void* stream) {
+  return enc_add_impl(ctx, 32, ct, r, n, stream, "secn32_mask_add");
 }
 
 size_t secn_he_conv2d_workspace(const secn_ctx* ctx, const secn_conv_plan_t* plan) {
   if (!ctx || !plan) return 0;
-  return (size_t)plan->G * plan->S * 2 * ctx->L * ctx->n * sizeof(uint64_t);
+  return (size_t)plan->G * plan->S * 2 * ctx->L * ctx->n * (ctx->word_bits / 8);
 }
 
-static int he_conv2d_impl(secn_ctx* ctx, const secn_conv_plan_t* plan, int stage, const uint64_t* ct_in,
-                          const uint64_t* x0, const uint64_t* w_ntt, const uint64_t* r, uint64_t* ct_out,
-                          void* workspace, size_t ws_bytes, void* stream) {
-  if (int st = check_ctx(ctx)) return st;
+static int he_conv2d_impl(secn_ctx* ctx, uint32_t bits, const secn_conv_plan_t* plan, int stage, const void* ct_in,
+                          const uint64_t* x0, const void* w_ntt, const uint64_t* r, void* ct_out, void* workspace,
+                          size_t ws_bytes, void* stream) {
+  if (int st = check_ctx(ctx, bits)) return st;
   if (int st = check_plan(ctx, plan)) return st;
   if (stage < -1 || stage > 2) return fail(SECN_EINVAL, "stage %d not in {0,1,2}", stage);
   if (!ct_in || !w_ntt || !ct_out || !workspace) return fail(SECN_EINVAL, "NULL buffer");
   if (ws_bytes < secn_he_conv2d_workspace(ctx, plan)) return fail(SECN_EINVAL, "workspace too small");
   if (((uintptr_t)workspace | (uintptr_t)ct_in | (uintptr_t)ct_out | (uintptr_t)w_ntt) & 15)
     return fail(SECN_EINVAL, "buffers must be 16-byte aligned");
-  if (plan->G > 50) return fail(SECN_EUNSUPPORTED, "G=%u > 50 input channel groups", plan->G);
+  if (plan->G > (bits == 64 ? 50u : 32u)) return fail(SECN_EUNSUPPORTED, "G=%u input channel groups too many", plan->G);
   DeviceGuard guard(ctx->device);
   cudaStream_t s = (cudaStream_t)stream;
   const size_t n_in = (size_t)plan->G * plan->S, n_out = (size_t)plan->M * plan->S, N = ctx->n;
@@ -390,13 +442,12 @@ static int he_conv2d_impl(secn_ctx* ctx, const secn_conv_plan_t* plan, int stage
     if (int st = check_range(ctx, ct_in, n_in * 2 * ctx->L * N, 0, s, "secn_he_conv2d ct_in")) return st;
     if (int st = check_range(ctx, x0, n_in * N, 1, s, "secn_he_conv2d x0")) return st;
   }
-  if ((stage == -1 || stage == 2))
+  if (stage == -1 || stage == 2)
     if (int st = check_range(ctx, r, n_out * N, 1, s, "secn_he_conv2d r")) return st;
-  uint64_t* xhat = static_cast<uint64_t*>(workspace);
   const secn::PlanDev pd = plan_dev(plan);
   cudaError_t e = cudaSuccess;
-  if (stage == -1 || stage == 0) e = secn::launch_ntt_fwd(ctx->dc, ct_in, xhat, n_in * 2 * ctx->L, x0, s);  // A6+A1
-  if (e == cudaSuccess && (stage == -1 || stage == 1)) e = secn::launch_mac(ctx->dc, pd, xhat, w_ntt, ct_out, s);  // A4
+  if (stage == -1 || stage == 0) e = secn::launch_ntt_fwd(ctx->dc, ct_in, workspace, n_in * 2 * ctx->L, x0, s);  // A6+A1
+  if (e == cudaSuccess && (stage == -1 || stage == 1)) e = secn::launch_mac(ctx->dc, pd, workspace, w_ntt, ct_out, s);  // A4
   if (e == cudaSuccess && (stage == -1 || stage == 2))
     e = secn::launch_ntt_inv(ctx->dc, ct_out, n_out * 2 * ctx->L, r, s);  // A2+A7
   return e == cudaSuccess ? SECN_OK : cuda_fail(e, "secn_he_conv2d");
@@ -405,14 +456,27 @@ static int he_conv2d_impl(secn_ctx* ctx, const secn_conv_plan_t* plan, int stage
 int secn_he_conv2d(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* ct_in, const uint64_t* x0,
                    const uint64_t* w_ntt, const uint64_t* r, uint64_t* ct_out, void* workspace, size_t ws_bytes,
                    void* stream) {
-  return he_conv2d_impl(ctx, plan, -1, ct_in, x0, w_ntt, r, ct_out, workspace, ws_bytes, stream);
+  return he_conv2d_impl(ctx, 64, plan, -1, ct_in, x0, w_ntt, r, ct_out, workspace, ws_bytes, stream);
 }
 
 int secn_he_conv2d_stage(secn_ctx* ctx, const secn_conv_plan_t* plan, int stage, const uint64_t* ct_in,
                          const uint64_t* x0, const uint64_t* w_ntt, const uint64_t* r, uint64_t* ct_out,
                          void* workspace, size_t ws_bytes, void* stream) {
   if (stage < 0 || stage > 2) return fail(SECN_EINVAL, "stage %d not in {0,1,2}", stage);
-  return he_conv2d_impl(ctx, plan, stage, ct_in, x0, w_ntt, r, ct_out, workspace, ws_bytes, stream);
+  return he_conv2d_impl(ctx, 64, plan, stage, ct_in, x0, w_ntt, r, ct_out, workspace, ws_bytes, stream);
+}
+
+int secn32_he_conv2d(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint32_t* ct_in, const uint64_t* x0,
+                     const uint32_t* w_ntt, const uint64_t* r, uint32_t* ct_out, void* workspace, size_t ws_bytes,
+                     void* stream) {
+  return he_conv2d_impl(ctx, 32, plan, -1, ct_in, x0, w_ntt, r, ct_out, workspace, ws_bytes, stream);
+}
+
+int secn32_he_conv2d_stage(secn_ctx* ctx, const secn_conv_plan_t* plan, int stage, const uint32_t* ct_in,
+                           const uint64_t* x0, const uint32_t* w_ntt, const uint64_t* r, uint32_t* ct_out,
+                           void* workspace, size_t ws_bytes, void* stream) {
+  if (stage < 0 || stage > 2) return fail(SECN_EINVAL, "stage %d not in {0,1,2}", stage);
+  return he_conv2d_impl(ctx, 32, plan, stage, ct_in, x0, w_ntt, r, ct_out, workspace, ws_bytes, stream);
 }
 
 int secn_extract_share(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* r, uint64_t* y0, void* stream) {

@@ -10,17 +10,23 @@
 namespace secn {
 
 // Per-context constants passed by value to every kernel (kernel-parameter space).
+// word_bits = 64: residues are uint64 (q < 2^61), twiddles in tw_fwd/tw_inv (Shoup w' over 2^64).
+// word_bits = 32: residues are uint32 (q < 2^30), twiddles in tw32_fwd/tw32_inv (w' over 2^32).
+// The 64-bit companions of delta / one_p are kept for both (encoding and reductions use 64-bit
+// arithmetic in either case).
 struct DevConsts {
-  uint64_t q[SECN_MAX_LIMBS], q2[SECN_MAX_LIMBS];
-  uint64_t ninv[SECN_MAX_LIMBS], ninv_p[SECN_MAX_LIMBS];    // N^-1 (Shoup)
-  uint64_t wlast[SECN_MAX_LIMBS], wlast_p[SECN_MAX_LIMBS];  // psi^-brv(1) * N^-1 (Shoup)
-  uint64_t delta[SECN_MAX_LIMBS], delta_p[SECN_MAX_LIMBS];  // floor(Q/t) mod q (Shoup)
-  uint64_t r64[SECN_MAX_LIMBS], r64_p[SECN_MAX_LIMBS];      // 2^64 mod q (Shoup)
+  uint64_t q[SECN_MAX_LIMBS];
+  uint64_t ninv[SECN_MAX_LIMBS], ninv_p[SECN_MAX_LIMBS];    // N^-1 (Shoup, word-sized companion)
+  uint64_t wlast[SECN_MAX_LIMBS], wlast_p[SECN_MAX_LIMBS];  // psi^-brv(1) N^-1 (Shoup, word-sized)
+  uint64_t delta[SECN_MAX_LIMBS], delta_p[SECN_MAX_LIMBS];  // floor(Q/t) mod q (Shoup over 2^64)
+  uint64_t r64[SECN_MAX_LIMBS], r64_p[SECN_MAX_LIMBS];      // 2^64 mod q (Shoup over 2^64)
   uint64_t one_p[SECN_MAX_LIMBS];                           // floor(2^64 / q)
   uint64_t qmt;                                             // Q mod t
-  uint32_t t_bits, log_n, L, pad_;
-  const ulonglong2* tw_fwd;  // [L][N] (psi^brv(i), Shoup companion)
-  const ulonglong2* tw_inv;  // [L][N] (psi^-brv(i), Shoup companion)
+  uint32_t t_bits, log_n, L, word_bits;
+  const ulonglong2* tw_fwd;  // [L][N] (psi^brv(i), w')      word_bits = 64
+  const ulonglong2* tw_inv;  // [L][N] (psi^-brv(i), w')
+  const uint2* tw32_fwd;     // [L][N]                        word_bits = 32
+  const uint2* tw32_inv;
 };
 
 struct PlanDev {  // the subset of secn_conv_plan the kernels use
@@ -28,25 +34,25 @@ struct PlanDev {  // the subset of secn_conv_plan the kernels use
 };
 
 // ---- launchers (kernels.cu); all return cudaGetLastError() after the launch(es) ----
-cudaError_t launch_ntt_fwd(const DevConsts& c, const uint64_t* in, uint64_t* out, size_t n_limb_polys,
-                           const uint64_t* x0, cudaStream_t s);
-cudaError_t launch_ntt_inv(const DevConsts& c, uint64_t* polys, size_t n_limb_polys, const uint64_t* r,
+// Residue buffers are void* of the context's word size.
+cudaError_t launch_ntt_fwd(const DevConsts& c, const void* in, void* out, size_t n_limb_polys, const uint64_t* x0,
                            cudaStream_t s);
-cudaError_t launch_mac(const DevConsts& c, const PlanDev& p, const uint64_t* xhat, const uint64_t* w,
-                       uint64_t* y, cudaStream_t s);
-cudaError_t launch_pack_weights(const DevConsts& c, const PlanDev& p, const uint64_t* kernel, uint64_t* w,
-                                cudaStream_t s);
-cudaError_t launch_enc_add(const DevConsts& c, uint64_t* ct, const uint64_t* v, size_t n, cudaStream_t s);
+cudaError_t launch_ntt_inv(const DevConsts& c, void* polys, size_t n_limb_polys, const uint64_t* r, cudaStream_t s);
+cudaError_t launch_mac(const DevConsts& c, const PlanDev& p, const void* xhat, const void* w, void* y, cudaStream_t s);
+cudaError_t launch_pack_weights(const DevConsts& c, const PlanDev& p, const uint64_t* kernel, void* w, cudaStream_t s);
+cudaError_t launch_enc_add(const DevConsts& c, void* ct, const uint64_t* v, size_t n, cudaStream_t s);
 cudaError_t launch_extract_share(const DevConsts& c, const PlanDev& p, const uint64_t* r, uint64_t* y0,
                                  cudaStream_t s);
-cudaError_t launch_check_range(const DevConsts& c, const uint64_t* v, size_t n_limb_polys, int kind,
-                               uint32_t* flag, cudaStream_t s);
+// kind 0: residues (n_words of the context's word size, limb = (idx / N) mod L, < q_j);
+// kind 1: uint64 plaintext-side values (< 2^t_bits).
+cudaError_t launch_check_range(const DevConsts& c, const void* v, size_t n_words, int kind, uint32_t* flag,
+                               cudaStream_t s);
 
 }  // namespace secn
 
 struct secn_ctx {
   int device;
-  uint32_t log_n, n, L, t_bits;
+  uint32_t log_n, n, L, t_bits, word_bits;
   uint64_t primes[SECN_MAX_LIMBS], psi[SECN_MAX_LIMBS];
   secn::DevConsts dc;
   void* d_tables;

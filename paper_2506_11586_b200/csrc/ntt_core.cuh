@@ -1,0 +1,189 @@
+// Shared-memory negacyclic NTT core for one limb-poly per CTA (N = 2^LOGN, T = N/16 threads,
+// 16 words per thread in registers), parameterised by an arithmetic policy A (modarith.cuh).
+//
+// Forward = Cooley-Tukey with psi^brv twiddles, natural order in, bit-reversed order out
+// (reading R4: entry k holds a(psi^(2 brv(k)+1))); inverse = Gentleman-Sande with psi^-brv
+// twiddles and N^-1 folded into the last level (App. C.1).
+//
+// A "round" performs K <= 4 consecutive stages in registers: the 2^K elements of a task are
+// blk*B + off + i*D (i < 2^K) and every thread owns 16/2^K tasks. Rounds exchange data through
+// shared memory, XOR-swizzled (swz) so every round pattern is bank-conflict free.
+#pragma once
+#include <cstdint>
+
+#include "modarith.cuh"
+
+namespace secn {
+
+__device__ __forceinline__ uint32_t swz(uint32_t e) { return e ^ ((e >> 4) & 15u); }
+
+template <int LOGN, int S0>
+struct CtRound {
+  static constexpr int K = (LOGN - S0) >= 4 ? 4 : (LOGN - S0);
+  static constexpr int GK = 1 << K, NT = 16 / GK, T = (1 << LOGN) / 16;
+  static constexpr int logB = LOGN - S0, logD = logB - K;
+  __device__ static __forceinline__ uint32_t blk(int k) { return (threadIdx.x + k * T) >> logD; }
+  __device__ static __forceinline__ uint32_t addr(int k, int i) {
+    const uint32_t tau = threadIdx.x + k * T;
+    return ((tau >> logD) << logB) + (tau & ((1u << logD) - 1)) + (i << logD);
+  }
+};
+
+// stages S0 .. S0+K-1 on x[] (stage s: 2^s groups, group i uses psi^brv(2^s + i))
+template <class A, int LOGN, int S0>
+__device__ __forceinline__ void ct_compute(typename A::W (&x)[16], const typename A::Tw* __restrict__ tw,
+                                           typename A::W q, typename A::W qb) {
+  using R = CtRound<LOGN, S0>;
+#pragma unroll
+  for (int p = 0; p < R::K; ++p) {
+    const int half = R::GK >> (p + 1);
+#pragma unroll
+    for (int k = 0; k < R::NT; ++k) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (u < (1 << p)) {
+          const typename A::Tw w = __ldg(&tw[(1u << (S0 + p)) + (R::blk(k) << p) + u]);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            if (i < half) {
+              const int a = k * R::GK + u * (R::GK >> p) + i;
+              A::ct(x[a], x[a + half], w, q, qb);
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
+template <class A, int LOGN, int S0>
+__device__ __forceinline__ void ct_load(typename A::W (&x)[16], const typename A::W* sm) {
+  using R = CtRound<LOGN, S0>;
+#pragma unroll
+  for (int k = 0; k < R::NT; ++k)
+#pragma unroll
+    for (int i = 0; i < R::GK; ++i) x[k * R::GK + i] = sm[swz(R::addr(k, i))];
+}
+
+template <class A, int LOGN, int S0>
+__device__ __forceinline__ void ct_store(const typename A::W (&x)[16], typename A::W* sm) {
+  using R = CtRound<LOGN, S0>;
+#pragma unroll
+  for (int k = 0; k < R::NT; ++k)
+#pragma unroll
+    for (int i = 0; i < R::GK; ++i) sm[swz(R::addr(k, i))] = x[k * R::GK + i];
+}
+
+// Rounds S0.. to the end, each smem -> regs -> smem, separated by barriers.
+template <class A, int LOGN, int S0>
+__device__ __forceinline__ void ct_rounds_smem(typename A::W* sm, const typename A::Tw* __restrict__ tw,
+                                               typename A::W q, typename A::W qb) {
+  if constexpr (S0 < LOGN) {
+    typename A::W x[16];
+    ct_load<A, LOGN, S0>(x, sm);
+    ct_compute<A, LOGN, S0>(x, tw, q, qb);
+    ct_store<A, LOGN, S0>(x, sm);
+    __syncthreads();
+    ct_rounds_smem<A, LOGN, S0 + CtRound<LOGN, S0>::K>(sm, tw, q, qb);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Gentleman-Sande: levels L0 .. L0+K-1 (level l: half-distance 2^l, N/2^(l+1) groups, group i
+// uses psi^-brv(N/2^(l+1) + i)); the last level (l = LOGN-1) multiplies by N^-1 instead.
+template <int LOGN, int L0>
+struct GsRound {
+  static constexpr int K = (LOGN - L0) >= 4 ? 4 : (LOGN - L0);
+  static constexpr int GK = 1 << K, NT = 16 / GK, T = (1 << LOGN) / 16;
+  static constexpr int logB = L0 + K, logD = L0;
+  __device__ static __forceinline__ uint32_t blk(int k) { return (threadIdx.x + k * T) >> logD; }
+  __device__ static __forceinline__ uint32_t addr(int k, int i) {
+    const uint32_t tau = threadIdx.x + k * T;
+    return ((tau >> logD) << logB) + (tau & ((1u << logD) - 1)) + (i << logD);
+  }
+};
+
+template <class A, int LOGN, int L0>
+__device__ __forceinline__ void gs_compute(typename A::W (&x)[16], const typename A::Tw* __restrict__ tw,
+                                           typename A::W q, typename A::W qb, typename A::Tw ninv,
+                                           typename A::Tw wlast) {
+  using R = GsRound<LOGN, L0>;
+#pragma unroll
+  for (int p = 0; p < R::K; ++p) {
+    const int dist = 1 << p;
+    if (L0 + p == LOGN - 1) {  // compile-time after unrolling
+#pragma unroll
+      for (int k = 0; k < R::NT; ++k)
+#pragma unroll
+        for (int i = 0; i < R::GK; ++i) {
+          if (i & dist) continue;
+          const typename A::W u = x[k * R::GK + i], v = x[k * R::GK + i + dist];
+          x[k * R::GK + i] = A::mul4(u + v, ninv, q);
+          x[k * R::GK + i + dist] = A::mul4(u - v + qb, wlast, q);
+        }
+    } else {
+      const uint32_t h = (1u << LOGN) >> (L0 + p + 1);
+#pragma unroll
+      for (int k = 0; k < R::NT; ++k) {
+#pragma unroll
+        for (int gi = 0; gi < 8; ++gi) {
+          if (gi < (R::GK >> (p + 1))) {
+            const typename A::Tw w = __ldg(&tw[h + (R::blk(k) << (R::K - p - 1)) + gi]);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              if (i < dist) {
+                const int a = k * R::GK + gi * (2 * dist) + i;
+                A::gs(x[a], x[a + dist], w, q, qb);
+              }
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
+template <class A, int LOGN, int L0>
+__device__ __forceinline__ void gs_load(typename A::W (&x)[16], const typename A::W* sm) {
+  using R = GsRound<LOGN, L0>;
+#pragma unroll
+  for (int k = 0; k < R::NT; ++k)
+#pragma unroll
+    for (int i = 0; i < R::GK; ++i) x[k * R::GK + i] = sm[swz(R::addr(k, i))];
+}
+
+template <class A, int LOGN, int L0>
+__device__ __forceinline__ void gs_store(const typename A::W (&x)[16], typename A::W* sm) {
+  using R = GsRound<LOGN, L0>;
+#pragma unroll
+  for (int k = 0; k < R::NT; ++k)
+#pragma unroll
+    for (int i = 0; i < R::GK; ++i) sm[swz(R::addr(k, i))] = x[k * R::GK + i];
+}
+
+// All GS rounds except the last one, smem -> regs -> smem.
+template <class A, int LOGN, int L0>
+__device__ __forceinline__ void gs_rounds_smem_but_last(typename A::W* sm, const typename A::Tw* __restrict__ tw,
+                                                        typename A::W q, typename A::W qb, typename A::Tw ninv,
+                                                        typename A::Tw wlast) {
+  if constexpr (L0 + GsRound<LOGN, L0>::K < LOGN) {
+    typename A::W x[16];
+    gs_load<A, LOGN, L0>(x, sm);
+    gs_compute<A, LOGN, L0>(x, tw, q, qb, ninv, wlast);
+    gs_store<A, LOGN, L0>(x, sm);
+    __syncthreads();
+    gs_rounds_smem_but_last<A, LOGN, L0 + GsRound<LOGN, L0>::K>(sm, tw, q, qb, ninv, wlast);
+  }
+}
+
+template <int LOGN, int L0 = 0>
+struct GsLast {
+  static constexpr int value =
+      (L0 + GsRound<LOGN, L0>::K >= LOGN) ? L0 : GsLast<LOGN, L0 + GsRound<LOGN, L0>::K>::value;
+};
+template <int LOGN>
+struct GsLast<LOGN, LOGN> {
+  static constexpr int value = LOGN;
+};
+
+}  // namespace secn

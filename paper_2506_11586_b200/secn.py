@@ -19,6 +19,8 @@ from . import build as _build
 DEFAULT_LOG_N = 12
 DEFAULT_PRIMES = (0x0FFFFFFFFFFFC001, 0x1FFFFFFFCE001)
 DEFAULT_T_BITS = 37
+# Reading R1b: 32-bit RNS limbs -- the four largest 27-bit primes = 1 mod 2^16.
+DEFAULT_PRIMES32 = (0x7E90001, 0x7E00001, 0x7DD0001, 0x7D70001)
 
 SECN_MAX_LIMBS = 4
 STATUS = {0: "SECN_OK", -1: "SECN_EINVAL", -2: "SECN_EUNSUPPORTED", -3: "SECN_ERANGE", -4: "SECN_ENOMEM",
@@ -26,7 +28,9 @@ STATUS = {0: "SECN_OK", -1: "SECN_EINVAL", -2: "SECN_EUNSUPPORTED", -3: "SECN_ER
 
 EXPORTS = ("secn_ctx_create", "secn_ctx_destroy", "secn_ctx_query", "secn_last_error", "secn_conv_plan",
            "secn_ntt_fwd", "secn_ntt_inv", "secn_preprocess_weights", "secn_share_add", "secn_mask_add",
-           "secn_he_conv2d_workspace", "secn_he_conv2d", "secn_he_conv2d_stage", "secn_extract_share")
+           "secn_he_conv2d_workspace", "secn_he_conv2d", "secn_he_conv2d_stage", "secn_extract_share",
+           "secn32_ctx_create", "secn32_ntt_fwd", "secn32_ntt_inv", "secn32_preprocess_weights",
+           "secn32_share_add", "secn32_mask_add", "secn32_he_conv2d", "secn32_he_conv2d_stage")
 
 
 class SecnError(RuntimeError):
@@ -57,7 +61,7 @@ class Plan(ctypes.Structure):
 class CtxInfo(ctypes.Structure):
     _fields_ = [("log_n", ctypes.c_uint32), ("n", ctypes.c_uint32), ("n_limbs", ctypes.c_uint32),
                 ("t_bits", ctypes.c_uint32), ("primes", ctypes.c_uint64 * SECN_MAX_LIMBS),
-                ("psi", ctypes.c_uint64 * SECN_MAX_LIMBS), ("device", ctypes.c_int)]
+                ("psi", ctypes.c_uint64 * SECN_MAX_LIMBS), ("device", ctypes.c_int), ("word_bits", ctypes.c_uint32)]
 
 
 _lib = None
@@ -89,7 +93,10 @@ def lib(path=None) -> ctypes.CDLL:
         "secn_he_conv2d": (i, [vp, P, vp, vp, vp, vp, vp, vp, sz, vp]),
         "secn_he_conv2d_stage": (i, [vp, P, i, vp, vp, vp, vp, vp, vp, sz, vp]),
         "secn_extract_share": (i, [vp, P, vp, vp, vp]),
+        "secn32_ctx_create": (i, [ctypes.POINTER(vp), i, u32, u32, ctypes.POINTER(ctypes.c_uint32), u32]),
     }
+    for f in ("ntt_fwd", "ntt_inv", "preprocess_weights", "share_add", "mask_add", "he_conv2d", "he_conv2d_stage"):
+        sig["secn32_" + f] = sig["secn_" + f]
     for name, (res, args) in sig.items():
         f = getattr(L, name)
         f.restype, f.argtypes = res, args
@@ -111,30 +118,53 @@ def conv_plan(C, H, W, M, kh, kw=None, stride=1, pad=0, log_n=DEFAULT_LOG_N, n_l
     return p
 
 
-def _ptr(t: Optional[torch.Tensor], shape=None, name="tensor"):
+def _ptr(t: Optional[torch.Tensor], shape=None, name="tensor", dtype=torch.int64):
     if t is None:
         return None
-    if t.dtype != torch.int64 or not t.is_cuda or not t.is_contiguous():
-        raise TypeError(f"{name}: expected a contiguous int64 CUDA tensor, got {t.dtype} {t.device}")
+    if t.dtype != dtype or not t.is_cuda or not t.is_contiguous():
+        raise TypeError(f"{name}: expected a contiguous {dtype} CUDA tensor, got {t.dtype} {t.device}")
     if shape is not None and tuple(t.shape) != tuple(shape):
         raise ValueError(f"{name}: expected shape {tuple(shape)}, got {tuple(t.shape)}")
     return ctypes.c_void_p(t.data_ptr())
 
 
 class Context:
-    """A libsecn context on one CUDA device (secn_ctx_create)."""
+    """A libsecn context on one CUDA device (secn_ctx_create, or secn32_ctx_create with
+    word_bits=32). Residue tensors are int64 (64-bit words) or int32 (32-bit words); plaintext
+    side tensors (x0, r, kernels, y0) are always int64."""
 
-    def __init__(self, device: int = 0, log_n: int = DEFAULT_LOG_N, primes: Sequence[int] = DEFAULT_PRIMES,
-                 t_bits: int = DEFAULT_T_BITS):
+    def __init__(self, device: int = 0, log_n: int = DEFAULT_LOG_N, primes: Optional[Sequence[int]] = None,
+                 t_bits: int = DEFAULT_T_BITS, word_bits: int = 64):
+        if word_bits not in (32, 64):
+            raise ValueError("word_bits must be 32 or 64")
+        if primes is None:
+            primes = DEFAULT_PRIMES if word_bits == 64 else DEFAULT_PRIMES32
         self._h = ctypes.c_void_p()
-        arr = (ctypes.c_uint64 * len(primes))(*primes)
-        _check(lib().secn_ctx_create(ctypes.byref(self._h), device, log_n, len(primes), arr, t_bits))
+        self.word_bits = word_bits
+        self.rdtype = torch.int64 if word_bits == 64 else torch.int32
+        self._pre = "secn_" if word_bits == 64 else "secn32_"
+        if word_bits == 64:
+            arr = (ctypes.c_uint64 * len(primes))(*primes)
+            _check(lib().secn_ctx_create(ctypes.byref(self._h), device, log_n, len(primes), arr, t_bits))
+        else:
+            arr = (ctypes.c_uint32 * len(primes))(*primes)
+            _check(lib().secn32_ctx_create(ctypes.byref(self._h), device, log_n, len(primes), arr, t_bits))
         info = CtxInfo()
         _check(lib().secn_ctx_query(self._h, ctypes.byref(info)))
         self.device = torch.device("cuda", device)
         self.log_n, self.n, self.L, self.t_bits = info.log_n, info.n, info.n_limbs, info.t_bits
         self.primes = tuple(info.primes[: self.L])
         self.psi = tuple(info.psi[: self.L])
+
+    def _f(self, name):
+        return getattr(lib(), self._pre + name)
+
+    def _rp(self, t, shape=None, name="residues"):
+        return _ptr(t, shape, name, self.rdtype)
+
+    def empty(self, *shape) -> torch.Tensor:
+        """An uninitialised residue tensor of this context's word size."""
+        return torch.empty(shape, dtype=self.rdtype, device=self.device)
 
     def close(self):
         if self._h:
@@ -151,39 +181,44 @@ class Context:
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         return ctypes.c_void_p(s.cuda_stream)
 
+    @property
+    def coef_words64(self) -> int:
+        """8-byte words per coefficient of a ciphertext component (the plan's byte model)."""
+        return max(1, self.L * self.word_bits // 64)
+
     def plan(self, C, H, W, M, kh, kw=None, stride=1, pad=0, Hw=0, Ww=0) -> Plan:
-        return conv_plan(C, H, W, M, kh, kw, stride, pad, self.log_n, self.L, Hw, Ww)
+        return conv_plan(C, H, W, M, kh, kw, stride, pad, self.log_n, self.coef_words64, Hw, Ww)
 
     # -- boundary calls ---------------------------------------------------------------------
     def ntt_fwd(self, polys: torch.Tensor, stream=None) -> torch.Tensor:
         n = polys.numel() // (self.L * self.n)
-        _check(lib().secn_ntt_fwd(self._h, _ptr(polys, None, "polys"), n, self._stream(stream)))
+        _check(self._f("ntt_fwd")(self._h, self._rp(polys, None, "polys"), n, self._stream(stream)))
         return polys
 
     def ntt_inv(self, polys: torch.Tensor, stream=None) -> torch.Tensor:
         n = polys.numel() // (self.L * self.n)
-        _check(lib().secn_ntt_inv(self._h, _ptr(polys, None, "polys"), n, self._stream(stream)))
+        _check(self._f("ntt_inv")(self._h, self._rp(polys, None, "polys"), n, self._stream(stream)))
         return polys
 
     def preprocess_weights(self, plan: Plan, kernel: torch.Tensor, out: Optional[torch.Tensor] = None,
                            stream=None) -> torch.Tensor:
         shape = (plan.M, plan.G, self.L, self.n)
         if out is None:
-            out = torch.empty(shape, dtype=torch.int64, device=self.device)
-        _check(lib().secn_preprocess_weights(self._h, ctypes.byref(plan),
+            out = self.empty(*shape)
+        _check(self._f("preprocess_weights")(self._h, ctypes.byref(plan),
                                              _ptr(kernel, (plan.M, plan.C, plan.kh, plan.kw), "kernel"),
-                                             _ptr(out, shape, "w_ntt"), self._stream(stream)))
+                                             self._rp(out, shape, "w_ntt"), self._stream(stream)))
         return out
 
     def share_add(self, ct: torch.Tensor, x0: torch.Tensor, stream=None) -> torch.Tensor:
         n = ct.shape[0]
-        _check(lib().secn_share_add(self._h, _ptr(ct, (n, 2, self.L, self.n), "ct"), _ptr(x0, (n, self.n), "x0"), n,
-                                    self._stream(stream)))
+        _check(self._f("share_add")(self._h, self._rp(ct, (n, 2, self.L, self.n), "ct"), _ptr(x0, (n, self.n), "x0"),
+                                    n, self._stream(stream)))
         return ct
 
     def mask_add(self, ct: torch.Tensor, r: torch.Tensor, stream=None) -> torch.Tensor:
         n = ct.shape[0]
-        _check(lib().secn_mask_add(self._h, _ptr(ct, (n, 2, self.L, self.n), "ct"), _ptr(r, (n, self.n), "r"), n,
+        _check(self._f("mask_add")(self._h, self._rp(ct, (n, 2, self.L, self.n), "ct"), _ptr(r, (n, self.n), "r"), n,
                                    self._stream(stream)))
         return ct
 
@@ -196,14 +231,15 @@ class Context:
         L, n = self.L, self.n
         n_in, n_out = plan.G * plan.S, plan.M * plan.S
         if out is None:
-            out = torch.empty((n_out, 2, L, n), dtype=torch.int64, device=self.device)
+            out = self.empty(n_out, 2, L, n)
         ws_bytes = self.workspace_bytes(plan)
         if workspace is None:
             workspace = torch.empty(ws_bytes // 8, dtype=torch.int64, device=self.device)
-        _check(lib().secn_he_conv2d(self._h, ctypes.byref(plan), _ptr(ct_in, (n_in, 2, L, n), "ct_in"),
-                                    _ptr(x0, (n_in, n), "x0"), _ptr(w_ntt, (plan.M, plan.G, L, n), "w_ntt"),
-                                    _ptr(r, (n_out, n), "r"), _ptr(out, (n_out, 2, L, n), "ct_out"),
-                                    _ptr(workspace, None, "workspace"), workspace.numel() * 8, self._stream(stream)))
+        _check(self._f("he_conv2d")(self._h, ctypes.byref(plan), self._rp(ct_in, (n_in, 2, L, n), "ct_in"),
+                                    _ptr(x0, (n_in, n), "x0"), self._rp(w_ntt, (plan.M, plan.G, L, n), "w_ntt"),
+                                    _ptr(r, (n_out, n), "r"), self._rp(out, (n_out, 2, L, n), "ct_out"),
+                                    ctypes.c_void_p(workspace.data_ptr()), workspace.numel() * workspace.element_size(),
+                                    self._stream(stream)))
         return out
 
     def he_conv2d_stage(self, stage: int, plan: Plan, ct_in: torch.Tensor, w_ntt: torch.Tensor,
@@ -212,11 +248,12 @@ class Context:
         """One launch group of secn_he_conv2d (0: share add + NTT, 1: MAC, 2: INTT + mask)."""
         L, n = self.L, self.n
         n_in, n_out = plan.G * plan.S, plan.M * plan.S
-        _check(lib().secn_he_conv2d_stage(self._h, ctypes.byref(plan), stage, _ptr(ct_in, (n_in, 2, L, n), "ct_in"),
-                                          _ptr(x0, (n_in, n), "x0"), _ptr(w_ntt, (plan.M, plan.G, L, n), "w_ntt"),
-                                          _ptr(r, (n_out, n), "r"), _ptr(out, (n_out, 2, L, n), "ct_out"),
-                                          _ptr(workspace, None, "workspace"), workspace.numel() * 8,
-                                          self._stream(stream)))
+        _check(self._f("he_conv2d_stage")(self._h, ctypes.byref(plan), stage,
+                                          self._rp(ct_in, (n_in, 2, L, n), "ct_in"), _ptr(x0, (n_in, n), "x0"),
+                                          self._rp(w_ntt, (plan.M, plan.G, L, n), "w_ntt"), _ptr(r, (n_out, n), "r"),
+                                          self._rp(out, (n_out, 2, L, n), "ct_out"),
+                                          ctypes.c_void_p(workspace.data_ptr()),
+                                          workspace.numel() * workspace.element_size(), self._stream(stream)))
         return out
 
     def extract_share(self, plan: Plan, r: torch.Tensor, out: Optional[torch.Tensor] = None,

@@ -25,7 +25,7 @@ def secn():
 def _header_functions():
     text = (ROOT / "include" / "secn.h").read_text()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    return sorted(set(re.findall(r"\b(secn_[a-z0-9_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(secn(?:32)?_[a-z0-9_]+)\s*\(", text)))
 
 
 def test_library_exports_every_declared_symbol(secn):

@@ -1,5 +1,8 @@
 """GPU parity: libsecn (through its C ABI, via the ctypes binding) against the oracle,
-element by element on identical seeded inputs. Integer work => bit-exact (every uint64 word).
+element by element on identical seeded inputs. Integer work => bit-exact (every word).
+
+Both residue word sizes are covered: 64-bit limbs at the paper parameters (reading R1:
+q0 = 60 bit, q1 = 49 bit) and 32-bit limbs (reading R1b: four 27-bit primes).
 
 Run on a B200 with: python -m pytest tests -m gpu
 """
@@ -17,15 +20,37 @@ from workloads import inputs, layers
 pytestmark = pytest.mark.gpu
 
 DEV = torch.device("cuda:0")
+PRIMES = {64: params.DEFAULT_PRIMES, 32: params.PRIMES32}
 
 
-def T(a: np.ndarray) -> torch.Tensor:
-    return torch.from_numpy(np.ascontiguousarray(a).view(np.int64)).to(DEV)
+def TP(a: np.ndarray) -> torch.Tensor:
+    """plaintext-side uint64 array -> int64 CUDA tensor"""
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.uint64).view(np.int64)).to(DEV)
 
 
-def U(t: torch.Tensor) -> np.ndarray:
+def UP(t: torch.Tensor) -> np.ndarray:
     torch.cuda.synchronize()
     return t.cpu().numpy().view(np.uint64)
+
+
+class Dev:
+    """Residue conversions for one context word size."""
+
+    def __init__(self, ctx):
+        self.ctx = ctx
+        self.wb = ctx.word_bits
+
+    def R(self, a: np.ndarray) -> torch.Tensor:
+        a = np.ascontiguousarray(a, dtype=np.uint64)
+        if self.wb == 64:
+            return torch.from_numpy(a.view(np.int64)).to(DEV)
+        assert (a >> np.uint64(32)).max(initial=0) == 0
+        return torch.from_numpy(a.astype(np.uint32).view(np.int32)).to(DEV)
+
+    def U(self, t: torch.Tensor) -> np.ndarray:
+        torch.cuda.synchronize()
+        x = t.cpu().numpy()
+        return x.view(np.uint64) if self.wb == 64 else x.view(np.uint32).astype(np.uint64)
 
 
 @pytest.fixture(scope="module")
@@ -38,26 +63,43 @@ def secn():
     return m
 
 
-@pytest.fixture(scope="module")
-def ctx(secn):
-    return secn.Context(0)
+@pytest.fixture(scope="module", params=[64, 32], ids=["w64", "w32"])
+def env(request, secn):
+    wb = request.param
+    ctx = secn.Context(0, word_bits=wb)
+    P = Params(primes=PRIMES[wb])
+    yield ctx, P, Dev(ctx)
+    ctx.close()
 
 
-@pytest.fixture(scope="module")
-def P():
-    return Params()
+def oplan(P, ctx, lay):
+    return packing.plan_conv(lay.C, lay.H, lay.W, lay.M, lay.k, lay.k, lay.stride, lay.pad, P.n, ctx.coef_words64)
 
 
 # ---------------------------------------------------------------------------------------------
 # context tables
 
-@pytest.mark.parametrize("logn,primes", [(12, params.DEFAULT_PRIMES), (12, params.ALT54_PRIMES),
-                                         (12, params.SWEEP_PRIMES), (13, params.SWEEP_PRIMES),
-                                         (14, params.SWEEP_PRIMES[:2])])
-def test_ctx_psi_matches_oracle(secn, logn, primes):
-    c = secn.Context(0, log_n=logn, primes=primes)
+@pytest.mark.parametrize("logn,primes,wb", [(12, params.DEFAULT_PRIMES, 64), (12, params.ALT54_PRIMES, 64),
+                                            (12, params.SWEEP_PRIMES, 64), (13, params.SWEEP_PRIMES, 64),
+                                            (14, params.SWEEP_PRIMES[:2], 64), (12, params.PRIMES32, 32),
+                                            (14, params.PRIMES32, 32)])
+def test_ctx_psi_matches_oracle(secn, logn, primes, wb):
+    c = secn.Context(0, log_n=logn, primes=primes, word_bits=wb)
     assert c.psi == tuple(Params(logn=logn, primes=primes).psi)
     c.close()
+
+
+def test_ctx_rejects_wrong_word_size_calls(secn):
+    c32 = secn.Context(0, word_bits=32)
+    lib = secn.lib()
+    import ctypes
+
+    assert lib.secn_ntt_fwd(c32._h, None, 0, None) == -6
+    c64 = secn.Context(0)
+    assert lib.secn32_ntt_fwd(c64._h, None, 0, None) == -6
+    big = (ctypes.c_uint32 * 1)(0x1FFF0001)  # 29-bit prime > 2^28 bound of 32-bit limbs
+    h = ctypes.c_void_p()
+    assert lib.secn32_ctx_create(ctypes.byref(h), 0, 12, 1, big, 37) == -2
 
 
 # ---------------------------------------------------------------------------------------------
@@ -68,69 +110,74 @@ def _edge_polys(P, g):
     polys = [inputs.uniform_residues(g, (), P.primes, n)]
     z = np.zeros((P.L, n), np.uint64)
     polys.append(z.copy())                                           # zero
-    c = z.copy(); c[:, 0] = 123456789; polys.append(c)                # constant
+    c = z.copy(); c[:, 0] = 1234567; polys.append(c)                  # constant
     top = np.stack([np.full(n, q - 1, np.uint64) for q in P.primes]); polys.append(top)  # all q-1
     mono = z.copy(); mono[:, n - 1] = 1; polys.append(mono)           # X^(N-1)
     return np.stack(polys)
 
 
-def test_ntt_fwd_matches_direct_evaluation(ctx, P):
+def test_ntt_fwd_matches_direct_evaluation(env):
+    ctx, P, D = env
     g = inputs.rng(100)
     polys = _edge_polys(P, g)
-    got = U(ctx.ntt_fwd(T(polys)))
+    got = D.U(ctx.ntt_fwd(D.R(polys)))
     for i in range(polys.shape[0]):
         for j in range(P.L):
-            if i >= 2 and j == 0:
-                continue  # closed-form edge polys: limb 1 suffices, keeps the test fast
+            if (i >= 2 and j != P.L - 1) or (i == 0 and j >= 2):
+                continue  # keeps the O(N^2) oracle calls few
             assert (got[i, j] == he.ntt(polys[i, j], P, j)).all(), (i, j)
-    # constant -> constant vector, on every limb
-    assert (got[2] == 123456789).all()
+    assert (got[2] == 1234567).all()  # constant -> constant vector, on every limb
 
 
-def test_ntt_inv_matches_direct_and_roundtrips(ctx, P):
+def test_ntt_inv_matches_direct_and_roundtrips(env):
+    ctx, P, D = env
     g = inputs.rng(101)
     A = inputs.uniform_residues(g, (2,), P.primes, P.n)
-    got = U(ctx.ntt_inv(T(A)))
+    got = D.U(ctx.ntt_inv(D.R(A)))
     assert (got[0, 0] == he.intt(A[0, 0], P, 0)).all()
     assert (got[1, 1] == he.intt(A[1, 1], P, 1)).all()
     big = inputs.uniform_residues(g, (3001,), P.primes, P.n)         # multi-wave batch
-    t = T(big)
+    t = D.R(big)
     ctx.ntt_fwd(t)
     ctx.ntt_inv(t)
-    assert (U(t) == big).all()
+    assert (D.U(t) == big).all()
 
 
-def test_ntt_pointwise_product_is_negacyclic_product(ctx, P):
+def test_ntt_pointwise_product_is_negacyclic_product(env):
+    ctx, P, D = env
     g = inputs.rng(102)
     a = inputs.uniform_residues(g, (), P.primes, P.n)
     b = inputs.uniform_residues(g, (), P.primes, P.n)
-    A, B = U(ctx.ntt_fwd(T(a[None]))), U(ctx.ntt_fwd(T(b[None])))
+    A, B = D.U(ctx.ntt_fwd(D.R(a[None]))), D.U(ctx.ntt_fwd(D.R(b[None])))
     prod = np.stack([np.array([int(x) * int(y) % q for x, y in zip(A[0, j], B[0, j])], np.uint64)
                      for j, q in enumerate(P.primes)])
-    c = U(ctx.ntt_inv(T(prod[None])))[0]
+    c = D.U(ctx.ntt_inv(D.R(prod[None])))[0]
     for j, q in enumerate(P.primes):
         assert (c[j] == he.negacyclic_mul(a[j], b[j], q)).all()
 
 
-@pytest.mark.parametrize("logn,L", [(12, 4), (13, 1), (13, 3), (14, 2), (14, 4)])
-def test_ntt_sweep_sampled(secn, logn, L):
-    primes = params.SWEEP_PRIMES[:L]
-    c = secn.Context(0, log_n=logn, primes=primes)
+@pytest.mark.parametrize("logn,L,wb", [(12, 4, 64), (13, 1, 64), (13, 3, 64), (14, 2, 64), (14, 4, 64),
+                                       (13, 4, 32), (14, 2, 32)])
+def test_ntt_sweep_sampled(secn, logn, L, wb):
+    primes = (params.SWEEP_PRIMES if wb == 64 else params.PRIMES32)[:L]
+    c = secn.Context(0, log_n=logn, primes=primes, word_bits=wb)
+    D = Dev(c)
     P = Params(logn=logn, primes=primes)
     g = inputs.rng(103 + logn * 10 + L)
     x = inputs.uniform_residues(g, (7,), primes, P.n)
-    got = U(c.ntt_fwd(T(x)))
+    got = D.U(c.ntt_fwd(D.R(x)))
     ks = np.concatenate([[0, 1, P.n // 2, P.n - 1], g.integers(0, P.n, 28)]).astype(np.uint32)
     for i in (0, 6):
         for j in range(L):
             assert (got[i, j, ks] == he.ntt_sampled(x[i, j], ks, P, j)).all(), (i, j)
-    back = U(c.ntt_inv(T(got)))
+    back = D.U(c.ntt_inv(D.R(got)))
     assert (back == x).all()
     c.close()
 
 
-def test_empty_batch_is_noop(ctx):
-    t = torch.zeros(0, dtype=torch.int64, device=DEV)
+def test_empty_batch_is_noop(env):
+    ctx, P, D = env
+    t = torch.zeros(0, dtype=ctx.rdtype, device=DEV)
     ctx.ntt_fwd(t)
     ctx.ntt_inv(t)
     torch.cuda.synchronize()
@@ -139,15 +186,16 @@ def test_empty_batch_is_noop(ctx):
 # ---------------------------------------------------------------------------------------------
 # A6 / A7: server-share add and output mask
 
-def test_mask_and_share_add_match_oracle_enc(ctx, P):
+def test_mask_and_share_add_match_oracle_enc(env):
+    ctx, P, D = env
     g = inputs.rng(104)
     n = 5
     ct = inputs.uniform_residues(g, (n, 2), P.primes, P.n)
     r = inputs.uniform_below(g, (n, P.n), P.t)
     r[0, :4] = [0, 1, P.t - 1, P.t // 2]
-    got = U(ctx.mask_add(T(ct), T(r)))
+    got = D.U(ctx.mask_add(D.R(ct), TP(r)))
     assert (got == he.mask_add(ct, r, P)).all()
-    got2 = U(ctx.share_add(T(ct), T(r)))
+    got2 = D.U(ctx.share_add(D.R(ct), TP(r)))
     assert (got2 == got).all()
 
 
@@ -155,36 +203,38 @@ def test_mask_and_share_add_match_oracle_enc(ctx, P):
 # A3: weight preprocessing
 
 @pytest.mark.parametrize("shape", [(4, 16, 16, 8, 3, 1, 1), (40, 6, 6, 6, 1, 1, 0), (3, 30, 30, 5, 7, 2, 3)])
-def test_preprocess_weights_matches_oracle(ctx, P, shape):
+def test_preprocess_weights_matches_oracle(env, shape):
+    ctx, P, D = env
     C, H, W, M, k, st, pad = shape
     plan = ctx.plan(C, H, W, M, k, stride=st, pad=pad)
-    opl = packing.plan_conv(C, H, W, M, k, k, st, pad, P.n, P.L)
+    opl = oplan(P, ctx, layers.ConvLayer("w", C, H, W, M, k, st, pad))
     g = inputs.rng(105)
     K = inputs.full_range_kernel(g, M, C, k, k)
-    w = ctx.preprocess_weights(plan, T(K))
-    wn = U(w)
+    w = ctx.preprocess_weights(plan, TP(K))
+    wn = D.U(w)
     # lifted coefficient-domain polys (oracle packing + centred lift) ...
     kp = packing.kernel_polys(K, opl, P.n)
     lifted = np.zeros((M, opl.G, P.L, P.n), np.uint64)
     for j, q in enumerate(P.primes):
         for m in range(M):
             for gg in range(opl.G):
-                v = kp[m, gg].astype(object)
-                lifted[m, gg, j] = np.array([(int(x) - P.t) % q if x >= P.t // 2 else int(x) for x in v], np.uint64)
+                lifted[m, gg, j] = np.array([(int(x) - P.t) % q if x >= P.t // 2 else int(x) % q for x in kp[m, gg]],
+                                            np.uint64)
     # ... equal the GPU output brought back by the (separately pinned) GPU inverse NTT
-    assert (U(ctx.ntt_inv(w.clone())) == lifted).all()
+    assert (D.U(ctx.ntt_inv(w.clone())) == lifted).all()
     # and a sample of NTT-domain words equals direct evaluation of the oracle's lifted polys
     ks = g.integers(0, P.n, 16).astype(np.uint32)
     for j in range(P.L):
         assert (wn[0, 0, j, ks] == he.ntt_sampled(lifted[0, 0, j], ks, P, j)).all()
     # idempotent
-    assert (U(ctx.preprocess_weights(plan, T(K))) == wn).all()
+    assert (D.U(ctx.preprocess_weights(plan, TP(K))) == wn).all()
 
 
-def test_zero_kernel_gives_zero_weights(ctx, P):
+def test_zero_kernel_gives_zero_weights(env):
+    ctx, P, D = env
     plan = ctx.plan(4, 16, 16, 8, 3, pad=1)
     w = ctx.preprocess_weights(plan, torch.zeros((8, 4, 3, 3), dtype=torch.int64, device=DEV))
-    assert not U(w).any()
+    assert not D.U(w).any()
 
 
 # ---------------------------------------------------------------------------------------------
@@ -200,21 +250,38 @@ def _layer_inputs(P, lay, seed, opl):
     return ct, x0, K, r
 
 
-def _run_layer(ctx, lay, ct, x0, K, r, use_x0=True, use_r=True):
+def _run_layer(ctx, D, lay, ct, x0, K, r, use_x0=True, use_r=True):
     plan = ctx.plan(lay.C, lay.H, lay.W, lay.M, lay.k, stride=lay.stride, pad=lay.pad)
-    w = ctx.preprocess_weights(plan, T(K))
-    out = ctx.he_conv2d(plan, T(ct), w, x0=T(x0) if use_x0 else None, r=T(r) if use_r else None)
-    return plan, U(out)
+    w = ctx.preprocess_weights(plan, TP(K))
+    out = ctx.he_conv2d(plan, D.R(ct), w, x0=TP(x0) if use_x0 else None, r=TP(r) if use_r else None)
+    return plan, D.U(out)
 
 
 @pytest.mark.parametrize("use_x0,use_r", [(True, True), (False, False), (True, False), (False, True)])
-def test_he_conv2d_tiny_exact(ctx, P, use_x0, use_r):
+def test_he_conv2d_tiny_exact(env, use_x0, use_r):
+    ctx, P, D = env
     lay = layers.tiny()[0]
-    opl = packing.plan_conv(lay.C, lay.H, lay.W, lay.M, lay.k, lay.k, lay.stride, lay.pad, P.n, P.L)
+    opl = oplan(P, ctx, lay)
     ct, x0, K, r = _layer_inputs(P, lay, 1, opl)
-    _, got = _run_layer(ctx, lay, ct, x0, K, r, use_x0, use_r)
+    _, got = _run_layer(ctx, D, lay, ct, x0, K, r, use_x0, use_r)
     ref = he.server_conv(ct, x0 if use_x0 else None, K, r if use_r else None, opl, P)
     assert (got == ref).all()
+
+
+def test_he_conv2d_stages_equal_fused_call(env):
+    ctx, P, D = env
+    lay = layers.ConvLayer("st", 20, 30, 30, 6, 3, 1, 1)
+    opl = oplan(P, ctx, lay)
+    ct, x0, K, r = _layer_inputs(P, lay, 3, opl)
+    plan = ctx.plan(lay.C, lay.H, lay.W, lay.M, lay.k, stride=lay.stride, pad=lay.pad)
+    w = ctx.preprocess_weights(plan, TP(K))
+    cti, x0t, rt = D.R(ct), TP(x0), TP(r)
+    fused = D.U(ctx.he_conv2d(plan, cti, w, x0=x0t, r=rt))
+    out = ctx.empty(plan.M * plan.S, 2, ctx.L, ctx.n)
+    ws = torch.empty(ctx.workspace_bytes(plan) // 8, dtype=torch.int64, device=DEV)
+    for s in range(3):
+        ctx.he_conv2d_stage(s, plan, cti, w, x0t, rt, out, ws)
+    assert (D.U(out) == fused).all()
 
 
 L_ = layers.ConvLayer
@@ -228,19 +295,21 @@ L_ = layers.ConvLayer
     L_("k7", 3, 64, 64, 4, 7, 2, 3),             # 7x7 / stride 2 / pad 3
     L_("mtile", 8, 8, 8, 37, 1, 1, 0),           # M not a multiple of the m-tile
     L_("scalar", 1, 1, 1, 1, 1, 1, 0),           # 1x1 input, 1x1 kernel
-])
-def test_he_conv2d_shapes_exact(ctx, P, lay):
-    opl = packing.plan_conv(lay.C, lay.H, lay.W, lay.M, lay.k, lay.k, lay.stride, lay.pad, P.n, P.L)
+    L_("g19", 512, 14, 14, 4, 3, 1, 1),          # G = 19 (GMAX 32 variants)
+], ids=lambda l: l.name)
+def test_he_conv2d_shapes_exact(env, lay):
+    ctx, P, D = env
+    opl = oplan(P, ctx, lay)
     ct, x0, K, r = _layer_inputs(P, lay, 2, opl)
-    _, got = _run_layer(ctx, lay, ct, x0, K, r)
+    _, got = _run_layer(ctx, D, lay, ct, x0, K, r)
     ref = he.server_conv(ct, x0, K, r, opl, P)
     assert (got == ref).all()
 
 
-def _sampled_check(ctx, P, lay, seed, n_samples=3):
-    opl = packing.plan_conv(lay.C, lay.H, lay.W, lay.M, lay.k, lay.k, lay.stride, lay.pad, P.n, P.L)
+def _sampled_check(ctx, P, D, lay, seed, n_samples=3):
+    opl = oplan(P, ctx, lay)
     ct, x0, K, r = _layer_inputs(P, lay, seed, opl)
-    _, got = _run_layer(ctx, lay, ct, x0, K, r)
+    _, got = _run_layer(ctx, D, lay, ct, x0, K, r)
     g = inputs.rng(seed + 1)
     n_out = opl.M * opl.S
     pick = np.unique(np.concatenate([[0, n_out - 1], g.integers(0, n_out, n_samples)]))
@@ -251,31 +320,35 @@ def _sampled_check(ctx, P, lay, seed, n_samples=3):
 
 
 @pytest.mark.parametrize("lay", layers.squeezenet11(), ids=lambda l: l.name)
-def test_he_conv2d_squeezenet11_full_size_sampled(ctx, P, lay):
+def test_he_conv2d_squeezenet11_full_size_sampled(env, lay):
     """Every SqueezeNet-1.1 layer at full size, in the launch configuration bench.py times."""
-    _sampled_check(ctx, P, lay, 300 + zlib.crc32(lay.name.encode()) % 1000)
+    ctx, P, D = env
+    _sampled_check(ctx, P, D, lay, 300 + zlib.crc32(lay.name.encode()) % 1000)
 
 
 @pytest.mark.parametrize("name", ["conv1", "l1.b0.c2", "l2.b0.ds", "l4.b0.c2", "l4.b2.c3"])
-def test_he_conv2d_resnet50_layers_sampled(ctx, P, name):
+def test_he_conv2d_resnet50_layers_sampled(env, name):
+    ctx, P, D = env
     lay = next(l for l in layers.resnet50() if l.name == name)
-    _sampled_check(ctx, P, lay, 400, n_samples=2)
+    _sampled_check(ctx, P, D, lay, 400, n_samples=2)
 
 
-def test_extract_share_matches_oracle(ctx, P):
+def test_extract_share_matches_oracle(env):
+    ctx, P, D = env
     for lay in [layers.tiny()[0], L_("s2", 3, 40, 40, 5, 3, 2, 0), L_("ds", 24, 28, 28, 9, 1, 2, 0)]:
         plan = ctx.plan(lay.C, lay.H, lay.W, lay.M, lay.k, stride=lay.stride, pad=lay.pad)
-        opl = packing.plan_conv(lay.C, lay.H, lay.W, lay.M, lay.k, lay.k, lay.stride, lay.pad, P.n, P.L)
+        opl = oplan(P, ctx, lay)
         r = inputs.uniform_below(inputs.rng(5), (opl.M * opl.S, P.n), P.t)
-        got = U(ctx.extract_share(plan, T(r)))
+        got = UP(ctx.extract_share(plan, TP(r)))
         assert (got == packing.extract((P.t - r) % P.t, opl)).all()
 
 
-def test_end_to_end_decrypts_to_plain_conv(ctx, P):
+def test_end_to_end_decrypts_to_plain_conv(env):
     """Client (oracle harness) encrypts its share; the GPU server path runs; decrypt + the
     GPU-extracted server share reconstruct conv(x0 + x1, K) mod 2^37 exactly."""
+    ctx, P, D = env
     lay = L_("e2e", 6, 20, 20, 4, 3, 2, 1)
-    opl = packing.plan_conv(lay.C, lay.H, lay.W, lay.M, lay.k, lay.k, lay.stride, lay.pad, P.n, P.L)
+    opl = oplan(P, ctx, lay)
     g = inputs.rng(77)
     x1 = inputs.uniform_below(g, (lay.C, lay.H, lay.W), P.t)
     x0 = inputs.uniform_below(g, (lay.C, lay.H, lay.W), P.t)
@@ -285,8 +358,8 @@ def test_end_to_end_decrypts_to_plain_conv(ctx, P):
     ct = np.stack([he.encrypt(xin[i], sk, inputs.uniform_residues(g, (), P.primes, P.n),
                               inputs.rounded_gaussian(g, P.n), P) for i in range(opl.G * opl.S)])
     r = inputs.uniform_below(g, (opl.M * opl.S, P.n), P.t)
-    plan, out = _run_layer(ctx, lay, ct, packing.pack_input(x0, opl, P.n), K, r)
-    y0 = U(ctx.extract_share(plan, T(r)))
+    plan, out = _run_layer(ctx, D, lay, ct, packing.pack_input(x0, opl, P.n), K, r)
+    y0 = UP(ctx.extract_share(plan, TP(r)))
     s_idx, coef = packing.designated_map(opl)
     y1 = np.zeros_like(y0)
     for m in range(opl.M):

@@ -12,7 +12,7 @@ from fractions import Fraction
 import numpy as np
 import pytest
 
-from oracle import conv, he, packing
+from oracle import conv, he, packing, params
 from oracle.params import Params
 from workloads import inputs, layers
 
@@ -137,8 +137,11 @@ def _e2e(layer, P, seed, full_range=False, with_x0=True):
     return pl, y, ref
 
 
-def test_e2e_tiny_config_exact(P):
-    """BASELINE.json configs[0] at the paper parameters: N=4096, Q = q0 q1, t = 2^37."""
+@pytest.mark.parametrize("primes", [params.DEFAULT_PRIMES, params.PRIMES32], ids=["q60_49", "q27x4"])
+def test_e2e_tiny_config_exact(primes):
+    """BASELINE.json configs[0] at the paper parameters: N=4096, t = 2^37, Q = q0 q1 (109 bits) and
+    the 32-bit-limb reading R1b (four 27-bit primes, 108 bits)."""
+    P = Params(primes=primes)
     pl, y, ref = _e2e(layers.tiny()[0], P, 1)
     assert (pl.Cw, pl.Hw, pl.Ww, pl.G, pl.S, pl.O) == (4, 18, 18, 1, 1, 1010)
     assert (y == ref).all()
@@ -156,7 +159,7 @@ L = layers.ConvLayer
     (L("pointwise", 40, 6, 6, 6, 1, 1, 0), 26, False),         # many channel groups
 ])
 def test_e2e_small_shapes_exact_n256(layer, seed, full):
-    P = Params(logn=8)
+    P = Params(logn=8, primes=params.PRIMES32 if seed % 2 else params.DEFAULT_PRIMES)
     pl, y, ref = _e2e(layer, P, seed, full_range=full)
     assert pl.G * pl.S > 1
     assert (y == ref).all()

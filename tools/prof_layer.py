@@ -1,0 +1,41 @@
+"""Runs one layer of the hot path a few times (for ncu captures of single kernels).
+Usage: python tools/prof_layer.py [layer_name] [net] [reps]"""
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+import numpy as np
+import torch
+
+import __graft_entry__
+from paper_2506_11586_b200 import Context
+from workloads import inputs, layers
+
+name = sys.argv[1] if len(sys.argv) > 1 else "conv10"
+net = sys.argv[2] if len(sys.argv) > 2 else "squeezenet1_1"
+reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+__graft_entry__.build()
+ctx = Context(0)
+lay = next(l for l in layers.network(net) if l.name == name)
+plan = ctx.plan(lay.C, lay.H, lay.W, lay.M, lay.k, stride=lay.stride, pad=lay.pad)
+g = inputs.rng(5)
+dev = torch.device("cuda:0")
+T = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int64)).to(dev)
+ct = T(inputs.uniform_residues(g, (plan.G * plan.S, 2), ctx.primes, ctx.n))
+x0 = T(inputs.uniform_below(g, (plan.G * plan.S, ctx.n), 1 << ctx.t_bits))
+K = T(inputs.quantized_kernel(g, plan.M, lay.C, lay.k, lay.k))
+r = T(inputs.uniform_below(g, (plan.M * plan.S, ctx.n), 1 << ctx.t_bits))
+w = ctx.preprocess_weights(plan, K)
+out = torch.empty((plan.M * plan.S, 2, ctx.L, ctx.n), dtype=torch.int64, device=dev)
+ws = torch.empty(ctx.workspace_bytes(plan) // 8, dtype=torch.int64, device=dev)
+for _ in range(reps):
+    ctx.he_conv2d(plan, ct, w, x0=x0, r=r, out=out, workspace=ws)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(reps):
+    ctx.he_conv2d(plan, ct, w, x0=x0, r=r, out=out, workspace=ws)
+e1.record()
+torch.cuda.synchronize()
+print(name, plan, f"{e0.elapsed_time(e1) / reps:.4f} ms/layer")
