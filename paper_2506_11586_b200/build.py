@@ -9,7 +9,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libsecn.so"
 SOURCES = [CSRC / "api.cpp", CSRC / "kernels.cu"]
-DEPS = SOURCES + [CSRC / "internal.h", CSRC / "modarith.cuh", CSRC / "ntt_core.cuh", PKG.parent / "include" / "secn.h"]
+DEPS = SOURCES + [CSRC / "internal.h", CSRC / "modarith.cuh", CSRC / "ntt_core.cuh", CSRC / "tma.cuh", PKG.parent / "include" / "secn.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-shared", "-Xcompiler", "-fPIC", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",
          "-std=c++17", "-Xptxas", "-v"]

@@ -434,7 +434,7 @@ static int he_conv2d_impl(secn_ctx* ctx, uint32_t bits, const secn_conv_plan_t* 
   if (ws_bytes < secn_he_conv2d_workspace(ctx, plan)) return fail(SECN_EINVAL, "workspace too small");
   if (((uintptr_t)workspace | (uintptr_t)ct_in | (uintptr_t)ct_out | (uintptr_t)w_ntt) & 15)
     return fail(SECN_EINVAL, "buffers must be 16-byte aligned");
-  if (plan->G > (bits == 64 ? 50u : 32u)) return fail(SECN_EUNSUPPORTED, "G=%u input channel groups too many", plan->G);
+  if (plan->G > 32u) return fail(SECN_EUNSUPPORTED, "G=%u input channel groups too many", plan->G);
   DeviceGuard guard(ctx->device);
   cudaStream_t s = (cudaStream_t)stream;
   const size_t n_in = (size_t)plan->G * plan->S, n_out = (size_t)plan->M * plan->S, N = ctx->n;

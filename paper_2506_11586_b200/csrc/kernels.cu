@@ -12,6 +12,7 @@
 #include "internal.h"
 #include "modarith.cuh"
 #include "ntt_core.cuh"
+#include "tma.cuh"
 
 namespace secn {
 
@@ -45,15 +46,15 @@ __device__ __forceinline__ uint64_t enc_mod(uint64_t v, int j, const DevConsts& 
   return csub(csub(a + b, 2 * q), q);
 }
 
-template <int LOGN>
-constexpr int ntt_min_blocks() { return LOGN == 12 ? 3 : 1; }
+template <class A, int LOGN>
+constexpr int ntt_min_blocks() { return LOGN == 12 ? (sizeof(typename A::W) == 4 ? 3 : 2) : 1; }
 
 // ------------------------------------------------------------------------------------------
 // K1: forward NTT of limb-polys [P][N] (limb j = p mod L), optionally fused server-share add
 // on the b component of ciphertexts [n][2][L][N]: b_j += enc_j(x0[n]). The
 // first radix-16 round reads global memory directly (its tasks are coalesced).
 template <class A, int LOGN>
-__global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<LOGN>())
+__global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN>())
     k_ntt_fwd(const typename A::W* in, typename A::W* out, const __grid_constant__ DevConsts c,
               const uint64_t* __restrict__ x0) {
   using W = typename A::W;
@@ -86,7 +87,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<LOGN>())
 #pragma unroll
   for (int k = 0; k < 16; ++k) {
     const uint32_t e = threadIdx.x + k * T;
-    dst[e] = A::canon_ct(sm[swz(e)], q);
+    dst[e] = A::canon_ct(sm[swz<A>(e)], q);
   }
 }
 
@@ -94,7 +95,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<LOGN>())
 // ciphertexts [n][2][L][N]: b_j += enc_j(r[n]) after the transform. The last
 // radix-16 round writes global memory directly (its tasks are coalesced).
 template <class A, int LOGN>
-__global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<LOGN>())
+__global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN>())
     k_ntt_inv(typename A::W* polys, const __grid_constant__ DevConsts c, const uint64_t* __restrict__ r) {
   using W = typename A::W;
   constexpr int N = 1 << LOGN, T = N / 16;
@@ -112,15 +113,24 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<LOGN>())
 #pragma unroll
   for (int k = 0; k < 16; ++k) {
     const uint32_t e = threadIdx.x + k * T;
-    sm[swz(e)] = buf[e];
+    sm[swz<A>(e)] = buf[e];
+  }
+  // the mask words this thread adds at the end, loaded now so their latency hides behind the
+  // transform (the last round's tasks are coalesced: element RL::addr(k, i))
+  const bool mask = r != nullptr && ((p / c.L) & 1);
+  const uint64_t* rs = mask ? r + (p / (2 * c.L)) * N : nullptr;
+  uint64_t rv[16];
+  if (mask) {
+#pragma unroll
+    for (int k = 0; k < RL::NT; ++k)
+#pragma unroll
+      for (int i = 0; i < RL::GK; ++i) rv[k * RL::GK + i] = __ldg(&rs[RL::addr(k, i)]);
   }
   __syncthreads();
   gs_rounds_smem_but_last<A, LOGN, 0>(sm, tw, q, qb, ninv, wl);
   W x[16];
   gs_load<A, LOGN, LL>(x, sm);
   gs_compute<A, LOGN, LL>(x, tw, q, qb, ninv, wl);
-  const bool mask = r != nullptr && ((p / c.L) & 1);
-  const uint64_t* rs = mask ? r + (p / (2 * c.L)) * N : nullptr;
 #pragma unroll
   for (int k = 0; k < RL::NT; ++k)
 #pragma unroll
@@ -128,7 +138,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<LOGN>())
       const uint32_t e = RL::addr(k, i);
       W v = A::canon_gs(x[k * RL::GK + i], q);
       if (mask) {
-        v += (W)enc_mod(__ldg(&rs[e]), j, c);  // < 2q
+        v += (W)enc_mod(rv[k * RL::GK + i], j, c);  // < 2q
         v = v >= q ? v - q : v;
       }
       buf[e] = v;
@@ -139,118 +149,147 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<LOGN>())
 // A4: NTT-domain multiply-accumulate ("performs all HE MAC operations in NTT"):
 //   Y^[m,s,c,j,e] = sum_g X^[g,s,c,j,e] * W[m,g,j,e] mod q_j
 // Per coefficient e this is a small (M x G) . (G x 2S) matrix product. A CTA owns 256
-// coefficients of limb j (one per thread), a tile of output channels and a group of SG spatial
-// blocks (both ciphertext components). The thread's X^ values are staged once and reused for
-// every m of the tile, so the weights stream from HBM exactly once; each thread keeps the
-// weight row W[m+1, :, j, e] in flight in registers while it multiplies row m. Products
-// accumulate lazily (128-bit for 64-bit words, 64-bit for 32-bit words) with one reduction per
-// output word.
-constexpr int MAC_THREADS = 256;
+// coefficients of limb j (one per consumer thread), a tile of output channels and a group of SG
+// spatial blocks (both ciphertext components). The weights stream from HBM exactly once through
+// a TMA ring: a producer warp issues one cp.async.bulk per (m, g) row segment (256 words) into an
+// NS-stage shared-memory ring guarded by full/empty mbarriers, so the bytes in flight do not
+// depend on registers or occupancy. The consumers' X^ values are staged once per CTA (registers
+// for 32-bit words, shared memory for 64-bit words) and reused for every m of the tile. Products
+// accumulate lazily (64-bit sums of 32x32 products; 128-bit sums of 64x64 products) with one
+// reduction per output word. CTAs that share a weight tile (different s-groups) are adjacent in
+// the grid so the second read of a tile hits L2.
+constexpr int MAC_THREADS = 256;  // consumers; +32 producer threads
 
-// 64-bit words: X^ staged in shared memory ([G][2*SG][256] thread-private columns).
-template <int SG, int GMAX>
-__global__ void __launch_bounds__(MAC_THREADS, GMAX <= 16 ? 2 : 1)
-    k_mac64(const uint64_t* __restrict__ xhat, const uint64_t* __restrict__ w, uint64_t* __restrict__ y,
-            const __grid_constant__ DevConsts c, PlanDev pl, int m_tile, int n_mtiles) {
-  extern __shared__ uint64_t xs[];
-  const int N = 1 << c.log_n, L = c.L, G = pl.G, S = pl.S;
-  const int j = blockIdx.y;
-  const uint32_t e = blockIdx.x * MAC_THREADS + threadIdx.x;
-  const int mt = blockIdx.z % n_mtiles, sgi = blockIdx.z / n_mtiles;
-  const int s0 = sgi * SG;
-  const int ns = min(SG, S - s0);
-  const uint64_t q = c.q[j], r64 = c.r64[j], r64p = c.r64_p[j], onep = c.one_p[j];
-  for (int g = 0; g < G; ++g)
-    for (int a = 0; a < 2 * ns; ++a)
-      xs[(g * 2 * SG + a) * MAC_THREADS + threadIdx.x] =
-          xhat[((((size_t)g * S + s0 + (a >> 1)) * 2 + (a & 1)) * L + j) * N + e];
-  const int m_begin = mt * m_tile, m_end = min((int)pl.M, m_begin + m_tile);
-  const size_t gstride = (size_t)L * N, mstride = (size_t)G * L * N;
-  const uint64_t* wp = w + ((size_t)m_begin * G * L + j) * N + e;
-  uint64_t wr[GMAX];
-#pragma unroll
-  for (int g = 0; g < GMAX; ++g)
-    if (g < G) wr[g] = __ldg(wp + g * gstride);
-  for (int m = m_begin; m < m_end; ++m) {
-    const bool more = m + 1 < m_end;
-    const uint64_t* wn = wp + (size_t)(m + 1 - m_begin) * mstride;
-    uint64_t lo[2 * SG], hi[2 * SG];
-#pragma unroll
-    for (int a = 0; a < 2 * SG; ++a) lo[a] = hi[a] = 0;
-#pragma unroll
-    for (int g = 0; g < GMAX; ++g) {
-      if (g < G) {
-        const uint64_t wc = wr[g];
-        if (more) wr[g] = __ldg(wn + g * gstride);
-#pragma unroll
-        for (int a = 0; a < 2 * SG; ++a)
-          if (a < 2 * ns) mac128(lo[a], hi[a], xs[(g * 2 * SG + a) * MAC_THREADS + threadIdx.x], wc);
-        if (g % 62 == 61) {  // keep the 128-bit sums below 2^128 (q < 2^61)
-#pragma unroll
-          for (int a = 0; a < 2 * SG; ++a) {
-            lo[a] = reduce128(lo[a], hi[a], q, r64, r64p, onep);
-            hi[a] = 0;
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int a = 0; a < 2 * SG; ++a)
-      if (a < 2 * ns)
-        y[((((size_t)m * S + s0 + (a >> 1)) * 2 + (a & 1)) * L + j) * N + e] = reduce128(lo[a], hi[a], q, r64, r64p, onep);
-  }
-}
-
-// 32-bit words: X^ held in registers ([GMAX][2*SG] words per thread), products summed exactly
-// in 64 bits (32-bit contexts require q < 2^28, so each product is < 2^56 and any G <= 256
-// fits), one IMAD.WIDE per MAC.
 __device__ __forceinline__ uint32_t reduce64(uint64_t a, uint64_t q, uint64_t onep) {
   const uint64_t r = a - mulhi(a, onep) * q;  // [0, 2q)
   return (uint32_t)(r >= q ? r - q : r);
 }
 
-template <int SG, int GMAX>
-__global__ void __launch_bounds__(MAC_THREADS, GMAX <= 16 ? 2 : 1)
-    k_mac32(const uint32_t* __restrict__ xhat, const uint32_t* __restrict__ w, uint32_t* __restrict__ y,
-            const __grid_constant__ DevConsts c, PlanDev pl, int m_tile, int n_mtiles) {
+// Register blocking: each consumer thread accumulates an [MT][2*SG] block of outputs (MT output
+// channels x SG spatial blocks x 2 components) for its coefficient; the g loop is the runtime
+// reduction loop. Per (m-block, g) the producer lands MT weight rows (MT x 256 words) in one ring
+// stage; the consumer reads its 2*SG X^ values for g from the shared-memory X^ tile and does
+// MT * 2 * SG multiply-accumulates.
+template <class W, int SG, int MT>
+__global__ void __launch_bounds__(MAC_THREADS + 32, 2)
+    k_mac(const W* __restrict__ xhat, const W* __restrict__ w, W* __restrict__ y, const __grid_constant__ DevConsts c,
+          PlanDev pl, int m_range, int n_sg, int NS) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  constexpr int A2 = 2 * SG;
   const int N = 1 << c.log_n, L = c.L, G = pl.G, S = pl.S;
   const int j = blockIdx.y;
-  const uint32_t e = blockIdx.x * MAC_THREADS + threadIdx.x;
-  const int mt = blockIdx.z % n_mtiles, sgi = blockIdx.z / n_mtiles;
+  const int sgi = blockIdx.x % n_sg, et = blockIdx.x / n_sg;
+  const uint32_t e0 = et * MAC_THREADS;
   const int s0 = sgi * SG;
   const int ns = min(SG, S - s0);
-  const uint64_t q = c.q[j], onep = c.one_p[j];
-  uint32_t xr[GMAX][2 * SG];
-#pragma unroll
-  for (int g = 0; g < GMAX; ++g)
-#pragma unroll
-    for (int a = 0; a < 2 * SG; ++a)
-      xr[g][a] = (g < G && a < 2 * ns) ? xhat[((((size_t)g * S + s0 + (a >> 1)) * 2 + (a & 1)) * L + j) * N + e] : 0u;
-  const int m_begin = mt * m_tile, m_end = min((int)pl.M, m_begin + m_tile);
-  const size_t gstride = (size_t)L * N, mstride = (size_t)G * L * N;
-  const uint32_t* wp = w + ((size_t)m_begin * G * L + j) * N + e;
-  uint32_t wr[GMAX];
-#pragma unroll
-  for (int g = 0; g < GMAX; ++g)
-    if (g < G) wr[g] = __ldg(wp + g * gstride);
-  for (int m = m_begin; m < m_end; ++m) {
-    const bool more = m + 1 < m_end;
-    const uint32_t* wn = wp + (size_t)(m + 1 - m_begin) * mstride;
-    uint64_t acc[2 * SG];
-#pragma unroll
-    for (int a = 0; a < 2 * SG; ++a) acc[a] = 0;
-#pragma unroll
-    for (int g = 0; g < GMAX; ++g) {
-      if (g < G) {
-        const uint32_t wc = wr[g];
-        if (more) wr[g] = __ldg(wn + g * gstride);
-#pragma unroll
-        for (int a = 0; a < 2 * SG; ++a) acc[a] += (uint64_t)xr[g][a] * wc;
+  const int m_begin = blockIdx.z * m_range, m_end = min((int)pl.M, m_begin + m_range);
+  const uint32_t row_bytes = MAC_THREADS * sizeof(W);
+  // shared memory: [G][2SG][256] X^ tile, [NS][MT][256] weight ring, 2*NS + 1 mbarriers
+  W* xs = reinterpret_cast<W*>(smraw);
+  W* ring = xs + (size_t)G * A2 * MAC_THREADS;
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)NS * MT * MAC_THREADS);
+  uint64_t* empty = full + NS;
+  uint64_t* xbar = empty + NS;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], MAC_THREADS / 32);
+    }
+    mbar_init(xbar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (tid >= MAC_THREADS) {  // ---- producer warp: one elected lane streams X^ once, then the weights ----
+    if (tid == MAC_THREADS) {
+      mbar_arrive_expect_tx(xbar, G * 2 * ns * row_bytes);
+      for (int g = 0; g < G; ++g)
+        for (int a = 0; a < 2 * ns; ++a)
+          tma_load_1d(xs + (g * A2 + a) * MAC_THREADS,
+                      xhat + ((((size_t)g * S + s0 + (a >> 1)) * 2 + (a & 1)) * L + j) * N + e0, row_bytes, xbar);
+      int i = 0;
+      for (int mb = m_begin; mb < m_end; mb += MT) {
+        const int rows = min(MT, m_end - mb);
+        for (int g = 0; g < G; ++g, ++i) {
+          const int st = i % NS;
+          if (i >= NS) mbar_wait(&empty[st], ((i / NS) - 1) & 1);
+          mbar_arrive_expect_tx(&full[st], rows * row_bytes);
+          for (int r = 0; r < rows; ++r)
+            tma_load_1d(ring + ((size_t)st * MT + r) * MAC_THREADS, w + (((size_t)(mb + r) * G + g) * L + j) * N + e0,
+                        row_bytes, &full[st]);
+        }
       }
     }
+    return;
+  }
+
+  // ---- consumers: one coefficient each (X^ rows beyond 2*ns hold stale data; never stored) ----
+  const uint32_t e = e0 + tid;
+  const uint64_t q = c.q[j], onep = c.one_p[j];
+  mbar_wait(xbar, 0);
+  int i = 0;
+  for (int mb = m_begin; mb < m_end; mb += MT) {
+    const int rows = min(MT, m_end - mb);
+    if constexpr (sizeof(W) == 4) {
+      uint64_t acc[MT][A2];
 #pragma unroll
-    for (int a = 0; a < 2 * SG; ++a)
-      if (a < 2 * ns) y[((((size_t)m * S + s0 + (a >> 1)) * 2 + (a & 1)) * L + j) * N + e] = reduce64(acc[a], q, onep);
+      for (int r = 0; r < MT; ++r)
+#pragma unroll
+        for (int a = 0; a < A2; ++a) acc[r][a] = 0;
+      for (int g = 0; g < G; ++g, ++i) {
+        const int st = i % NS;
+        uint32_t xv[A2];
+#pragma unroll
+        for (int a = 0; a < A2; ++a) xv[a] = xs[(g * A2 + a) * MAC_THREADS + tid];
+        mbar_wait(&full[st], (i / NS) & 1);
+        const W* wst = ring + (size_t)st * MT * MAC_THREADS + tid;
+#pragma unroll
+        for (int r = 0; r < MT; ++r) {
+          const uint32_t wv = wst[r * MAC_THREADS];
+#pragma unroll
+          for (int a = 0; a < A2; ++a) acc[r][a] += (uint64_t)xv[a] * wv;  // < 2^56 each (q < 2^28), G <= 32
+        }
+        __syncwarp();
+        if ((tid & 31) == 0) mbar_arrive(&empty[st]);
+      }
+#pragma unroll
+      for (int r = 0; r < MT; ++r)
+#pragma unroll
+        for (int a = 0; a < A2; ++a)
+          if (r < rows && a < 2 * ns)
+            y[((((size_t)(mb + r) * S + s0 + (a >> 1)) * 2 + (a & 1)) * L + j) * N + e] = (W)reduce64(acc[r][a], q, onep);
+    } else {
+      const uint64_t r64 = c.r64[j], r64p = c.r64_p[j];
+      uint64_t lo[MT][A2], hi[MT][A2];
+#pragma unroll
+      for (int r = 0; r < MT; ++r)
+#pragma unroll
+        for (int a = 0; a < A2; ++a) lo[r][a] = hi[r][a] = 0;
+      for (int g = 0; g < G; ++g, ++i) {
+        const int st = i % NS;
+        uint64_t xv[A2];
+#pragma unroll
+        for (int a = 0; a < A2; ++a) xv[a] = xs[(g * A2 + a) * MAC_THREADS + tid];
+        mbar_wait(&full[st], (i / NS) & 1);
+        const W* wst = ring + (size_t)st * MT * MAC_THREADS + tid;
+#pragma unroll
+        for (int r = 0; r < MT; ++r) {
+          const uint64_t wv = wst[r * MAC_THREADS];
+#pragma unroll
+          for (int a = 0; a < A2; ++a) mac128(lo[r][a], hi[r][a], xv[a], wv);  // G <= 32 < 64 terms of < 2^122
+        }
+        __syncwarp();
+        if ((tid & 31) == 0) mbar_arrive(&empty[st]);
+      }
+#pragma unroll
+      for (int r = 0; r < MT; ++r)
+#pragma unroll
+        for (int a = 0; a < A2; ++a)
+          if (r < rows && a < 2 * ns)
+            y[((((size_t)(mb + r) * S + s0 + (a >> 1)) * 2 + (a & 1)) * L + j) * N + e] =
+                (W)reduce128(lo[r][a], hi[r][a], q, r64, r64p, onep);
+    }
   }
 }
 
@@ -401,94 +440,63 @@ cudaError_t launch_ntt_inv(const DevConsts& c, void* polys, size_t P, const uint
   return cudaErrorInvalidValue;
 }
 
-// m-tile: about 4 waves of 2 CTAs per SM, at least 8 channels per CTA to amortise the X^ staging
-static int mac_m_tile(const DevConsts& c, const PlanDev& p, int n_sg) {
-  const long ctas_no_m = (long)((1 << c.log_n) / MAC_THREADS) * c.L * n_sg;
-  int m_tile = (int)(((long)p.M * ctas_no_m + 1183) / 1184);
-  if (m_tile < 8) m_tile = 8;
-  if (m_tile > (int)p.M) m_tile = p.M;
-  return m_tile;
-}
-
-template <int SG, int GMAX>
-static cudaError_t mac64_t(const DevConsts& c, const PlanDev& p, const void* xhat, const void* w, void* y,
-                           cudaStream_t s) {
+template <class W, int SG, int MT>
+static cudaError_t mac_t(const DevConsts& c, const PlanDev& p, const void* xhat, const void* w, void* y,
+                         cudaStream_t s) {
   const int N = 1 << c.log_n;
-  const size_t smem = (size_t)p.G * 2 * SG * MAC_THREADS * sizeof(uint64_t);
+  const size_t xtile = (size_t)p.G * 2 * SG * MAC_THREADS * sizeof(W);
+  const size_t stage = (size_t)MT * MAC_THREADS * sizeof(W);
+  // ring depth: ~40 KiB of weights in flight per CTA (2 CTAs per SM), 3..12 stages
+  int NS = (int)((40 * 1024) / stage);
+  NS = NS < 3 ? 3 : NS > 12 ? 12 : NS;
+  const size_t smem = xtile + NS * stage + (2 * NS + 1) * sizeof(uint64_t);
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
   static size_t attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_mac64<SG, GMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (smem > attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_mac<W, SG, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(smem > 48 * 1024 ? smem : 48 * 1024));
     if (e != cudaSuccess) return e;
     attr = smem;
   }
   const int n_sg = (p.S + SG - 1) / SG;
-  const int m_tile = mac_m_tile(c, p, n_sg);
-  const int n_mtiles = (p.M + m_tile - 1) / m_tile;
-  dim3 grid(N / MAC_THREADS, c.L, n_mtiles * n_sg);
-  k_mac64<SG, GMAX><<<grid, MAC_THREADS, smem, s>>>(static_cast<const uint64_t*>(xhat), static_cast<const uint64_t*>(w),
-                                                    static_cast<uint64_t*>(y), c, p, m_tile, n_mtiles);
+  // m-range per CTA: about 4 waves of 2 CTAs per SM, a multiple of MT, at least 2 m-blocks
+  const long ctas_no_m = (long)(N / MAC_THREADS) * n_sg * c.L;
+  long mr = ((long)p.M * ctas_no_m + 148 * 8 - 1) / (148 * 8);
+  mr = (mr + MT - 1) / MT * MT;
+  if (mr < 2 * MT) mr = 2 * MT;
+  const int m_range = (int)(mr < (long)p.M ? mr : (long)p.M);
+  const int n_mr = (p.M + m_range - 1) / m_range;
+  dim3 grid((N / MAC_THREADS) * n_sg, c.L, n_mr);
+  k_mac<W, SG, MT><<<grid, MAC_THREADS + 32, smem, s>>>(static_cast<const W*>(xhat), static_cast<const W*>(w),
+                                                      static_cast<W*>(y), c, p, m_range, n_sg, NS);
   return cudaGetLastError();
-}
-
-template <int GMAX>
-static cudaError_t mac64_g(int sg, const DevConsts& c, const PlanDev& p, const void* xhat, const void* w, void* y,
-                           cudaStream_t s) {
-  switch (sg) {
-    case 1: return mac64_t<1, GMAX>(c, p, xhat, w, y, s);
-    case 2: return mac64_t<2, GMAX>(c, p, xhat, w, y, s);
-    case 3: return mac64_t<3, GMAX>(c, p, xhat, w, y, s);
-    default: return mac64_t<4, GMAX>(c, p, xhat, w, y, s);
-  }
-}
-
-template <int SG, int GMAX>
-static cudaError_t mac32_t(const DevConsts& c, const PlanDev& p, const void* xhat, const void* w, void* y,
-                           cudaStream_t s) {
-  const int N = 1 << c.log_n;
-  const int n_sg = (p.S + SG - 1) / SG;
-  const int m_tile = mac_m_tile(c, p, n_sg);
-  const int n_mtiles = (p.M + m_tile - 1) / m_tile;
-  dim3 grid(N / MAC_THREADS, c.L, n_mtiles * n_sg);
-  k_mac32<SG, GMAX><<<grid, MAC_THREADS, 0, s>>>(static_cast<const uint32_t*>(xhat), static_cast<const uint32_t*>(w),
-                                                 static_cast<uint32_t*>(y), c, p, m_tile, n_mtiles);
-  return cudaGetLastError();
-}
-
-template <int GMAX>
-static cudaError_t mac32_g(int sg, const DevConsts& c, const PlanDev& p, const void* xhat, const void* w, void* y,
-                           cudaStream_t s) {
-  // X^ registers: GMAX * 2 * SG <= 48 words per thread (no spills at 128 registers)
-  constexpr int SGMAX = GMAX >= 16 ? 1 : (24 / GMAX < 4 ? 24 / GMAX : 4);
-  if (sg > SGMAX) sg = SGMAX;
-  switch (sg) {
-    case 1: return mac32_t<1, GMAX>(c, p, xhat, w, y, s);
-    case 2: return mac32_t<(SGMAX >= 2 ? 2 : 1), GMAX>(c, p, xhat, w, y, s);
-    case 3: return mac32_t<(SGMAX >= 3 ? 3 : 1), GMAX>(c, p, xhat, w, y, s);
-    default: return mac32_t<SGMAX, GMAX>(c, p, xhat, w, y, s);
-  }
 }
 
 cudaError_t launch_mac(const DevConsts& c, const PlanDev& p, const void* xhat, const void* w, void* y,
                        cudaStream_t s) {
   if (p.M == 0 || p.S == 0) return cudaSuccess;
-  if (c.word_bits == 64) {
-    // s-group: as many spatial blocks (<= 4) as keep the X^ tile within 100 KiB (2 CTAs / SM)
-    const size_t per_s = (size_t)p.G * 2 * MAC_THREADS * sizeof(uint64_t);
-    if (per_s > 200 * 1024) return cudaErrorInvalidValue;  // G > 50
-    int sg = 4;
-    while (sg > 1 && per_s * sg > 100 * 1024) --sg;
-    if (sg > (int)p.S) sg = p.S;
-    if (p.G <= 8) return mac64_g<8>(sg, c, p, xhat, w, y, s);
-    if (p.G <= 16) return mac64_g<16>(sg, c, p, xhat, w, y, s);
-    if (p.G <= 32) return mac64_g<32>(sg < 2 ? sg : 2, c, p, xhat, w, y, s);
-    return mac64_g<64>(1, c, p, xhat, w, y, s);
-  }
   if (p.G > 32) return cudaErrorInvalidValue;
-  const int sg = p.S < 4 ? (int)p.S : 4;
-  if (p.G <= 4) return mac32_g<4>(sg, c, p, xhat, w, y, s);
-  if (p.G <= 8) return mac32_g<8>(sg, c, p, xhat, w, y, s);
-  if (p.G <= 16) return mac32_g<16>(sg, c, p, xhat, w, y, s);
-  return mac32_g<32>(sg, c, p, xhat, w, y, s);
+  // s-group: as many spatial blocks (<= 4) as keep the X^ tile within 64 KiB; accumulator block
+  // MT x 2SG <= 32 64-bit sums (32-bit limbs) or <= 12 128-bit sums (64-bit limbs), spill-free at
+  // the 96 registers two 288-thread CTAs per SM allow
+  const size_t wb = c.word_bits / 8;
+  int sg = 4;
+  while (sg > 1 && (size_t)p.G * 2 * sg * MAC_THREADS * wb > 64 * 1024) --sg;
+  if (sg > (int)p.S) sg = p.S;
+  if (c.word_bits == 32) {
+    switch (sg) {
+      case 1: return mac_t<uint32_t, 1, 16>(c, p, xhat, w, y, s);
+      case 2: return mac_t<uint32_t, 2, 8>(c, p, xhat, w, y, s);
+      case 3: return mac_t<uint32_t, 3, 5>(c, p, xhat, w, y, s);
+      default: return mac_t<uint32_t, 4, 3>(c, p, xhat, w, y, s);
+    }
+  }
+  switch (sg) {
+    case 1: return mac_t<uint64_t, 1, 4>(c, p, xhat, w, y, s);
+    case 2: return mac_t<uint64_t, 2, 2>(c, p, xhat, w, y, s);
+    case 3: return mac_t<uint64_t, 3, 2>(c, p, xhat, w, y, s);
+    default: return mac_t<uint64_t, 4, 1>(c, p, xhat, w, y, s);
+  }
 }
 
 cudaError_t launch_pack_weights(const DevConsts& c, const PlanDev& p, const uint64_t* kernel, void* w,

@@ -15,7 +15,16 @@
 
 namespace secn {
 
-__device__ __forceinline__ uint32_t swz(uint32_t e) { return e ^ ((e >> 4) & 15u); }
+// 64-bit words: XOR bits 0..3 with bits 4..7 (a half-warp's 16 lanes hit 16 distinct bank pairs);
+// 32-bit words: XOR bits 0..4 with bits 4..8 (32 distinct banks per warp at N = 4096; at most
+// 2-way for a few rounds at larger N). Both are bijections on [0, N).
+template <class A>
+__device__ __forceinline__ uint32_t swz(uint32_t e) {
+  if constexpr (sizeof(typename A::W) == 4)
+    return e ^ ((e >> 4) & 31u);
+  else
+    return e ^ ((e >> 4) & 15u);
+}
 
 template <int LOGN, int S0>
 struct CtRound {
@@ -62,7 +71,7 @@ __device__ __forceinline__ void ct_load(typename A::W (&x)[16], const typename A
 #pragma unroll
   for (int k = 0; k < R::NT; ++k)
 #pragma unroll
-    for (int i = 0; i < R::GK; ++i) x[k * R::GK + i] = sm[swz(R::addr(k, i))];
+    for (int i = 0; i < R::GK; ++i) x[k * R::GK + i] = sm[swz<A>(R::addr(k, i))];
 }
 
 template <class A, int LOGN, int S0>
@@ -71,7 +80,7 @@ __device__ __forceinline__ void ct_store(const typename A::W (&x)[16], typename 
 #pragma unroll
   for (int k = 0; k < R::NT; ++k)
 #pragma unroll
-    for (int i = 0; i < R::GK; ++i) sm[swz(R::addr(k, i))] = x[k * R::GK + i];
+    for (int i = 0; i < R::GK; ++i) sm[swz<A>(R::addr(k, i))] = x[k * R::GK + i];
 }
 
 // Rounds S0.. to the end, each smem -> regs -> smem, separated by barriers.
@@ -149,7 +158,7 @@ __device__ __forceinline__ void gs_load(typename A::W (&x)[16], const typename A
 #pragma unroll
   for (int k = 0; k < R::NT; ++k)
 #pragma unroll
-    for (int i = 0; i < R::GK; ++i) x[k * R::GK + i] = sm[swz(R::addr(k, i))];
+    for (int i = 0; i < R::GK; ++i) x[k * R::GK + i] = sm[swz<A>(R::addr(k, i))];
 }
 
 template <class A, int LOGN, int L0>
@@ -158,7 +167,7 @@ __device__ __forceinline__ void gs_store(const typename A::W (&x)[16], typename 
 #pragma unroll
   for (int k = 0; k < R::NT; ++k)
 #pragma unroll
-    for (int i = 0; i < R::GK; ++i) sm[swz(R::addr(k, i))] = x[k * R::GK + i];
+    for (int i = 0; i < R::GK; ++i) sm[swz<A>(R::addr(k, i))] = x[k * R::GK + i];
 }
 
 // All GS rounds except the last one, smem -> regs -> smem.

@@ -1,0 +1,38 @@
+"""Summarise an ncu report: per kernel duration, throughput, pipes, occupancy, stall reasons.
+Usage: python tools/ncu_summary.py report.ncu-rep"""
+import csv
+import io
+import subprocess
+import sys
+
+rep = sys.argv[1]
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(raw)))
+hdr = rows[0]
+ki = hdr.index("Kernel Name")
+want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "dram__throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_bytes.sum",
+        "sm__throughput.avg.pct_of_peak_sustained_elapsed", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+        "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+        "smsp__inst_executed.sum", "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smsp__thread_inst_executed_per_inst_executed.ratio"]
+stall = [h for h in hdr if h.startswith("smsp__average_warp_latency_issue_stalled") and h.endswith(".ratio")]
+for row in rows[2:]:
+    print("=" * 100)
+    print(row[ki][:110])
+    for w in want:
+        if w in hdr:
+            print(f"  {w:70s} {row[hdr.index(w)]}")
+    st = []
+    for h in stall:
+        try:
+            v = float(row[hdr.index(h)])
+        except ValueError:
+            continue
+        if v > 0.05:
+            st.append((v, h.replace("smsp__average_warp_latency_issue_stalled_", "").replace(".ratio", "")))
+    print("  stalls (cycles per issued instr):", ", ".join(f"{n}={v:.2f}" for v, n in sorted(st, reverse=True)[:8]))

@@ -15,19 +15,21 @@ from workloads import inputs, layers
 name = sys.argv[1] if len(sys.argv) > 1 else "conv10"
 net = sys.argv[2] if len(sys.argv) > 2 else "squeezenet1_1"
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+wb = int(sys.argv[4]) if len(sys.argv) > 4 else 64
 __graft_entry__.build()
-ctx = Context(0)
+ctx = Context(0, word_bits=wb)
 lay = next(l for l in layers.network(net) if l.name == name)
 plan = ctx.plan(lay.C, lay.H, lay.W, lay.M, lay.k, stride=lay.stride, pad=lay.pad)
 g = inputs.rng(5)
 dev = torch.device("cuda:0")
 T = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int64)).to(dev)
-ct = T(inputs.uniform_residues(g, (plan.G * plan.S, 2), ctx.primes, ctx.n))
+ctn = inputs.uniform_residues(g, (plan.G * plan.S, 2), ctx.primes, ctx.n)
+ct = T(ctn) if wb == 64 else torch.from_numpy(ctn.astype(np.uint32).view(np.int32)).to(dev)
 x0 = T(inputs.uniform_below(g, (plan.G * plan.S, ctx.n), 1 << ctx.t_bits))
 K = T(inputs.quantized_kernel(g, plan.M, lay.C, lay.k, lay.k))
 r = T(inputs.uniform_below(g, (plan.M * plan.S, ctx.n), 1 << ctx.t_bits))
 w = ctx.preprocess_weights(plan, K)
-out = torch.empty((plan.M * plan.S, 2, ctx.L, ctx.n), dtype=torch.int64, device=dev)
+out = ctx.empty(plan.M * plan.S, 2, ctx.L, ctx.n)
 ws = torch.empty(ctx.workspace_bytes(plan) // 8, dtype=torch.int64, device=dev)
 for _ in range(reps):
     ctx.he_conv2d(plan, ct, w, x0=x0, r=r, out=out, workspace=ws)
@@ -38,4 +40,4 @@ for _ in range(reps):
     ctx.he_conv2d(plan, ct, w, x0=x0, r=r, out=out, workspace=ws)
 e1.record()
 torch.cuda.synchronize()
-print(name, plan, f"{e0.elapsed_time(e1) / reps:.4f} ms/layer")
+print(name, wb, plan, f"{e0.elapsed_time(e1) / reps:.4f} ms/layer")
