@@ -247,6 +247,9 @@ static int ctx_create_impl(secn_ctx** out, int device, uint32_t log_n, uint32_t 
     const uint64_t tinv = powmod(t % q, q - 2, q);
     const uint64_t delta = mulmod((q - qmt % q) % q, tinv, q);
     dc.delta[j] = delta, dc.delta_p[j] = shoup_companion(delta, q);
+    dc.tinv[j] = tinv, dc.tinv_p[j] = comp(tinv, q);
+    const uint64_t tinv_hi = (uint64_t)((((u128)tinv) << 32) % q);
+    dc.tinv_hi[j] = tinv_hi, dc.tinv_hi_p[j] = comp(tinv_hi, q);
     const uint64_t r64 = (uint64_t)(((u128)1 << 64) % q);
     dc.r64[j] = r64, dc.r64_p[j] = shoup_companion(r64, q);
     dc.one_p[j] = ~0ull / q;

@@ -33,17 +33,29 @@ struct Tab<Arith32> {
   __device__ static uint2 pair(uint64_t w, uint64_t wp) { return make_uint2((uint32_t)w, (uint32_t)wp); }
 };
 
-// enc_j(v) = round(Q v / t) mod q_j (reading R2) = floor(Q/t) v + floor(((Q mod t) v + t/2) / t),
-// canonical in [0, q), with 64-bit arithmetic (any q < 2^61, v < 2^44).
-__device__ __forceinline__ uint64_t enc_mod(uint64_t v, int j, const DevConsts& c) {
-  const uint64_t q = c.q[j];
-  const uint64_t a = shoup(v, c.delta[j], c.delta_p[j], q);  // [0, 2q)
-  uint64_t lo = c.qmt * v, hi = mulhi(c.qmt, v);
-  const uint64_t half = 1ull << (c.t_bits - 1);
-  asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, 0;" : "+l"(lo), "+l"(hi) : "l"(half));
-  const uint64_t frac = (hi << (64 - c.t_bits)) | (lo >> c.t_bits);  // < Q mod t < 2^t_bits
-  const uint64_t b = frac - mulhi(frac, c.one_p[j]) * q;              // [0, 2q)
-  return csub(csub(a + b, 2 * q), q);
+// enc_j(v) = round(Q v / t) mod q_j (reading R2), computed through the identity
+//   round(Q v / t) = (Q v - rho) / t + [rho >= t/2],  rho = Q v mod t = (Q mod t) v mod t,
+// and Q = 0 (mod q_j):  enc_j(v) = -rho t^-1 + [rho >= t/2]  (mod q_j).
+// rho is one 64-bit low product; rho t^-1 one Shoup product (64-bit limbs) or two 32-bit Shoup
+// products on the 32-bit halves of rho (32-bit limbs). Canonical result in [0, q).
+template <class A>
+__device__ __forceinline__ typename A::W enc_mod(uint64_t v, int j, const DevConsts& c) {
+  const uint64_t tmask = (1ull << c.t_bits) - 1;
+  const uint64_t rho = (c.qmt * v) & tmask;
+  const uint32_t up = rho >= (1ull << (c.t_bits - 1));
+  if constexpr (sizeof(typename A::W) == 8) {
+    const uint64_t q = c.q[j];
+    const uint64_t a = shoup(rho, c.tinv[j], c.tinv_p[j], q);  // [0, 2q)
+    const uint64_t e = 2 * q - a + up;                           // [1, 2q + 1]
+    return csub(csub(e, q), q);
+  } else {
+    const uint32_t q = (uint32_t)c.q[j];
+    const uint32_t a = Arith32::shoup32((uint32_t)rho, (uint32_t)c.tinv[j], (uint32_t)c.tinv_p[j], q) +
+                       Arith32::shoup32((uint32_t)(rho >> 32), (uint32_t)c.tinv_hi[j], (uint32_t)c.tinv_hi_p[j], q);
+    uint32_t e = 4 * q - a + up;                                 // [1, 4q + 1]
+    e = csub32(e, 2 * q);
+    return csub32(csub32(e, q), q);
+  }
 }
 
 template <class A, int LOGN>
@@ -76,13 +88,16 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN>())
     for (int i = 0; i < R0::GK; ++i) {
       const uint32_t e = R0::addr(k, i);
       W v = src[e];
-      if (share) v += (W)enc_mod(__ldg(&xs[e]), j, c);  // < 2q: inside the CT domain
+      if (share) v += enc_mod<A>(__ldg(&xs[e]), j, c);  // < 2q: inside the CT domain
       x[k * R0::GK + i] = v;
     }
-  ct_compute<A, LOGN, 0>(x, tw, q, qb);
+  {
+    typename A::Tw tws[15];
+    ct_twiddles<A, LOGN, 0>(tws, tw);
+    ct_compute<A, LOGN, 0>(x, tws, q, qb);
+  }
   ct_store<A, LOGN, 0>(x, sm);
-  __syncthreads();
-  ct_rounds_smem<A, LOGN, R0::K>(sm, tw, q, qb);
+  ct_rounds_smem<A, LOGN, R0::K>(sm, tw, q, qb);  // ends with a barrier
   W* dst = out + p * N;
 #pragma unroll
   for (int k = 0; k < 16; ++k) {
@@ -126,11 +141,13 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN>())
 #pragma unroll
       for (int i = 0; i < RL::GK; ++i) rv[k * RL::GK + i] = __ldg(&rs[RL::addr(k, i)]);
   }
-  __syncthreads();
   gs_rounds_smem_but_last<A, LOGN, 0>(sm, tw, q, qb, ninv, wl);
+  typename A::Tw tws[15];
+  gs_twiddles<A, LOGN, LL>(tws, tw);
+  __syncthreads();
   W x[16];
   gs_load<A, LOGN, LL>(x, sm);
-  gs_compute<A, LOGN, LL>(x, tw, q, qb, ninv, wl);
+  gs_compute<A, LOGN, LL>(x, tws, q, qb, ninv, wl);
 #pragma unroll
   for (int k = 0; k < RL::NT; ++k)
 #pragma unroll
@@ -138,7 +155,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN>())
       const uint32_t e = RL::addr(k, i);
       W v = A::canon_gs(x[k * RL::GK + i], q);
       if (mask) {
-        v += (W)enc_mod(rv[k * RL::GK + i], j, c);  // < 2q
+        v += enc_mod<A>(rv[k * RL::GK + i], j, c);  // < 2q
         v = v >= q ? v - q : v;
       }
       buf[e] = v;
@@ -208,16 +225,17 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
         for (int a = 0; a < 2 * ns; ++a)
           tma_load_1d(xs + (g * A2 + a) * MAC_THREADS,
                       xhat + ((((size_t)g * S + s0 + (a >> 1)) * 2 + (a & 1)) * L + j) * N + e0, row_bytes, xbar);
-      int i = 0;
+      int st = 0;
+      uint32_t ph = 0, first = 1;  // ring position, its phase, and "first lap" (no wait needed)
       for (int mb = m_begin; mb < m_end; mb += MT) {
         const int rows = min(MT, m_end - mb);
-        for (int g = 0; g < G; ++g, ++i) {
-          const int st = i % NS;
-          if (i >= NS) mbar_wait(&empty[st], ((i / NS) - 1) & 1);
+        for (int g = 0; g < G; ++g) {
+          if (!first) mbar_wait(&empty[st], ph ^ 1);
           mbar_arrive_expect_tx(&full[st], rows * row_bytes);
           for (int r = 0; r < rows; ++r)
             tma_load_1d(ring + ((size_t)st * MT + r) * MAC_THREADS, w + (((size_t)(mb + r) * G + g) * L + j) * N + e0,
                         row_bytes, &full[st]);
+          if (++st == NS) st = 0, ph ^= 1, first = 0;
         }
       }
     }
@@ -228,7 +246,8 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
   const uint32_t e = e0 + tid;
   const uint64_t q = c.q[j], onep = c.one_p[j];
   mbar_wait(xbar, 0);
-  int i = 0;
+  int st = 0;
+  uint32_t ph = 0;
   for (int mb = m_begin; mb < m_end; mb += MT) {
     const int rows = min(MT, m_end - mb);
     if constexpr (sizeof(W) == 4) {
@@ -237,12 +256,11 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
       for (int r = 0; r < MT; ++r)
 #pragma unroll
         for (int a = 0; a < A2; ++a) acc[r][a] = 0;
-      for (int g = 0; g < G; ++g, ++i) {
-        const int st = i % NS;
+      for (int g = 0; g < G; ++g) {
         uint32_t xv[A2];
 #pragma unroll
         for (int a = 0; a < A2; ++a) xv[a] = xs[(g * A2 + a) * MAC_THREADS + tid];
-        mbar_wait(&full[st], (i / NS) & 1);
+        mbar_wait(&full[st], ph);
         const W* wst = ring + (size_t)st * MT * MAC_THREADS + tid;
 #pragma unroll
         for (int r = 0; r < MT; ++r) {
@@ -252,6 +270,7 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
         }
         __syncwarp();
         if ((tid & 31) == 0) mbar_arrive(&empty[st]);
+        if (++st == NS) st = 0, ph ^= 1;
       }
 #pragma unroll
       for (int r = 0; r < MT; ++r)
@@ -266,12 +285,11 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
       for (int r = 0; r < MT; ++r)
 #pragma unroll
         for (int a = 0; a < A2; ++a) lo[r][a] = hi[r][a] = 0;
-      for (int g = 0; g < G; ++g, ++i) {
-        const int st = i % NS;
+      for (int g = 0; g < G; ++g) {
         uint64_t xv[A2];
 #pragma unroll
         for (int a = 0; a < A2; ++a) xv[a] = xs[(g * A2 + a) * MAC_THREADS + tid];
-        mbar_wait(&full[st], (i / NS) & 1);
+        mbar_wait(&full[st], ph);
         const W* wst = ring + (size_t)st * MT * MAC_THREADS + tid;
 #pragma unroll
         for (int r = 0; r < MT; ++r) {
@@ -281,6 +299,7 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
         }
         __syncwarp();
         if ((tid & 31) == 0) mbar_arrive(&empty[st]);
+        if (++st == NS) st = 0, ph ^= 1;
       }
 #pragma unroll
       for (int r = 0; r < MT; ++r)
@@ -320,9 +339,10 @@ __global__ void k_pack_weights(const uint64_t* __restrict__ kern, W* __restrict_
 }
 
 // A6 / A7 standalone: ct [n][2][L][N], b_j += enc_j(v[n][N]).
-template <class W>
-__global__ void k_enc_add(W* __restrict__ ct, const uint64_t* __restrict__ v, const __grid_constant__ DevConsts c,
-                          size_t n) {
+template <class A>
+__global__ void k_enc_add(typename A::W* __restrict__ ct, const uint64_t* __restrict__ v,
+                          const __grid_constant__ DevConsts c, size_t n) {
+  using W = typename A::W;
   const size_t N = 1ull << c.log_n;
   const size_t total = n * c.L * N;
   for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
@@ -331,7 +351,7 @@ __global__ void k_enc_add(W* __restrict__ ct, const uint64_t* __restrict__ v, co
     const size_t i = idx / (N * c.L);
     W* b = ct + ((i * 2 + 1) * c.L + j) * N + e;
     const uint64_t q = c.q[j];
-    const uint64_t s = (uint64_t)*b + enc_mod(v[i * N + e], j, c);  // [0, 2q)
+    const uint64_t s = (uint64_t)*b + (uint64_t)enc_mod<A>(v[i * N + e], j, c);  // [0, 2q)
     *b = (W)(s >= q ? s - q : s);
   }
 }
@@ -521,9 +541,9 @@ cudaError_t launch_enc_add(const DevConsts& c, void* ct, const uint64_t* v, size
   const size_t blocks = (total + 255) / 256;
   const unsigned b = (unsigned)(blocks < 148 * 32 ? blocks : 148 * 32);
   if (c.word_bits == 64)
-    k_enc_add<uint64_t><<<b, 256, 0, s>>>(static_cast<uint64_t*>(ct), v, c, n);
+    k_enc_add<Arith64><<<b, 256, 0, s>>>(static_cast<uint64_t*>(ct), v, c, n);
   else
-    k_enc_add<uint32_t><<<b, 256, 0, s>>>(static_cast<uint32_t*>(ct), v, c, n);
+    k_enc_add<Arith32><<<b, 256, 0, s>>>(static_cast<uint32_t*>(ct), v, c, n);
   return cudaGetLastError();
 }
 

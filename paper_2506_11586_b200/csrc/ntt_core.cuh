@@ -38,9 +38,23 @@ struct CtRound {
   }
 };
 
+// Twiddles of one round, gathered into registers before the round's barrier so their load
+// latency overlaps it: task k, stage p, group u -> tws[k * (GK - 1) + (1 << p) - 1 + u] (<= 15).
+template <class A, int LOGN, int S0>
+__device__ __forceinline__ void ct_twiddles(typename A::Tw (&tws)[15], const typename A::Tw* __restrict__ tw) {
+  using R = CtRound<LOGN, S0>;
+#pragma unroll
+  for (int p = 0; p < R::K; ++p)
+#pragma unroll
+    for (int k = 0; k < R::NT; ++k)
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (u < (1 << p)) tws[k * (R::GK - 1) + (1 << p) - 1 + u] = __ldg(&tw[(1u << (S0 + p)) + (R::blk(k) << p) + u]);
+}
+
 // stages S0 .. S0+K-1 on x[] (stage s: 2^s groups, group i uses psi^brv(2^s + i))
 template <class A, int LOGN, int S0>
-__device__ __forceinline__ void ct_compute(typename A::W (&x)[16], const typename A::Tw* __restrict__ tw,
+__device__ __forceinline__ void ct_compute(typename A::W (&x)[16], const typename A::Tw (&tws)[15],
                                            typename A::W q, typename A::W qb) {
   using R = CtRound<LOGN, S0>;
 #pragma unroll
@@ -51,7 +65,7 @@ __device__ __forceinline__ void ct_compute(typename A::W (&x)[16], const typenam
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         if (u < (1 << p)) {
-          const typename A::Tw w = __ldg(&tw[(1u << (S0 + p)) + (R::blk(k) << p) + u]);
+          const typename A::Tw w = tws[k * (R::GK - 1) + (1 << p) - 1 + u];
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             if (i < half) {
@@ -83,17 +97,22 @@ __device__ __forceinline__ void ct_store(const typename A::W (&x)[16], typename 
     for (int i = 0; i < R::GK; ++i) sm[swz<A>(R::addr(k, i))] = x[k * R::GK + i];
 }
 
-// Rounds S0.. to the end, each smem -> regs -> smem, separated by barriers.
+// Rounds S0.. to the end, each: gather twiddles, barrier (the previous round's stores), smem ->
+// regs -> smem. A final barrier follows the last round.
 template <class A, int LOGN, int S0>
 __device__ __forceinline__ void ct_rounds_smem(typename A::W* sm, const typename A::Tw* __restrict__ tw,
                                                typename A::W q, typename A::W qb) {
   if constexpr (S0 < LOGN) {
+    typename A::Tw tws[15];
+    ct_twiddles<A, LOGN, S0>(tws, tw);
+    __syncthreads();
     typename A::W x[16];
     ct_load<A, LOGN, S0>(x, sm);
-    ct_compute<A, LOGN, S0>(x, tw, q, qb);
+    ct_compute<A, LOGN, S0>(x, tws, q, qb);
     ct_store<A, LOGN, S0>(x, sm);
-    __syncthreads();
     ct_rounds_smem<A, LOGN, S0 + CtRound<LOGN, S0>::K>(sm, tw, q, qb);
+  } else {
+    __syncthreads();
   }
 }
 
@@ -112,8 +131,26 @@ struct GsRound {
   }
 };
 
+// Twiddles of one GS round: task k, level p, group gi -> tws[k * (GK - 1) + GK - (GK >> p) + gi]
+// (the final level uses N^-1 and psi^-brv(1) N^-1 instead and gathers nothing).
 template <class A, int LOGN, int L0>
-__device__ __forceinline__ void gs_compute(typename A::W (&x)[16], const typename A::Tw* __restrict__ tw,
+__device__ __forceinline__ void gs_twiddles(typename A::Tw (&tws)[15], const typename A::Tw* __restrict__ tw) {
+  using R = GsRound<LOGN, L0>;
+#pragma unroll
+  for (int p = 0; p < R::K; ++p) {
+    if (L0 + p == LOGN - 1) continue;
+    const uint32_t h = (1u << LOGN) >> (L0 + p + 1);
+#pragma unroll
+    for (int k = 0; k < R::NT; ++k)
+#pragma unroll
+      for (int gi = 0; gi < 8; ++gi)
+        if (gi < (R::GK >> (p + 1)))
+          tws[k * (R::GK - 1) + R::GK - (R::GK >> p) + gi] = __ldg(&tw[h + (R::blk(k) << (R::K - p - 1)) + gi]);
+  }
+}
+
+template <class A, int LOGN, int L0>
+__device__ __forceinline__ void gs_compute(typename A::W (&x)[16], const typename A::Tw (&tws)[15],
                                            typename A::W q, typename A::W qb, typename A::Tw ninv,
                                            typename A::Tw wlast) {
   using R = GsRound<LOGN, L0>;
@@ -131,13 +168,12 @@ __device__ __forceinline__ void gs_compute(typename A::W (&x)[16], const typenam
           x[k * R::GK + i + dist] = A::mul4(u - v + qb, wlast, q);
         }
     } else {
-      const uint32_t h = (1u << LOGN) >> (L0 + p + 1);
 #pragma unroll
       for (int k = 0; k < R::NT; ++k) {
 #pragma unroll
         for (int gi = 0; gi < 8; ++gi) {
           if (gi < (R::GK >> (p + 1))) {
-            const typename A::Tw w = __ldg(&tw[h + (R::blk(k) << (R::K - p - 1)) + gi]);
+            const typename A::Tw w = tws[k * (R::GK - 1) + R::GK - (R::GK >> p) + gi];
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
               if (i < dist) {
@@ -170,17 +206,20 @@ __device__ __forceinline__ void gs_store(const typename A::W (&x)[16], typename 
     for (int i = 0; i < R::GK; ++i) sm[swz<A>(R::addr(k, i))] = x[k * R::GK + i];
 }
 
-// All GS rounds except the last one, smem -> regs -> smem.
+// All GS rounds except the last one, each: gather twiddles, barrier, smem -> regs -> smem. The
+// caller gathers the last round's twiddles and places the last barrier.
 template <class A, int LOGN, int L0>
 __device__ __forceinline__ void gs_rounds_smem_but_last(typename A::W* sm, const typename A::Tw* __restrict__ tw,
                                                         typename A::W q, typename A::W qb, typename A::Tw ninv,
                                                         typename A::Tw wlast) {
   if constexpr (L0 + GsRound<LOGN, L0>::K < LOGN) {
+    typename A::Tw tws[15];
+    gs_twiddles<A, LOGN, L0>(tws, tw);
+    __syncthreads();
     typename A::W x[16];
     gs_load<A, LOGN, L0>(x, sm);
-    gs_compute<A, LOGN, L0>(x, tw, q, qb, ninv, wlast);
+    gs_compute<A, LOGN, L0>(x, tws, q, qb, ninv, wlast);
     gs_store<A, LOGN, L0>(x, sm);
-    __syncthreads();
     gs_rounds_smem_but_last<A, LOGN, L0 + GsRound<LOGN, L0>::K>(sm, tw, q, qb, ninv, wlast);
   }
 }
