@@ -305,6 +305,7 @@ def main():
                        "alg_GBps": round(alg_bytes / step_s / 1e9, 1), "hbm_frac": round(alg_bytes / step_s / 1e9 / hbm_peak, 4),
                        "offline_preprocess_s": round(offline_s, 5), "wall_s_timed_region": round(wall, 4)},
         "roofline": roofline,
+        "per_layer_stage_us": stage_profile.per_layer_us,
         "gpu_launches": launches_per_step * K,
         "clocks": clk.summary(),
         "e2e": e2e,
@@ -345,6 +346,7 @@ def stage_profile(ctx, st, K, dev):
     host_s = time.perf_counter() - t
     torch.cuda.synchronize()
     tot = [0.0, 0.0, 0.0]
+    per_layer = {d["lay"].name: [0.0, 0.0, 0.0] for d in st}
     for _ in range(K):
         evs = mk()
         torch.cuda._sleep(int(2.5e9 * (2 * host_s + 1e-3)))
@@ -353,7 +355,10 @@ def stage_profile(ctx, st, K, dev):
         for li, d in enumerate(st):
             if d["mc"] > 0:
                 for s in range(3):
-                    tot[s] += evs[li][s].elapsed_time(evs[li][s + 1])
+                    dt = evs[li][s].elapsed_time(evs[li][s + 1])
+                    tot[s] += dt
+                    per_layer[d["lay"].name][s] += dt
+    stage_profile.per_layer_us = {k: [round(v * 1e3 / K, 1) for v in vs] for k, vs in per_layer.items()}
     return [x / K for x in tot]
 
 

@@ -250,6 +250,8 @@ static int ctx_create_impl(secn_ctx** out, int device, uint32_t log_n, uint32_t 
     dc.tinv[j] = tinv, dc.tinv_p[j] = comp(tinv, q);
     const uint64_t tinv_hi = (uint64_t)((((u128)tinv) << 32) % q);
     dc.tinv_hi[j] = tinv_hi, dc.tinv_hi_p[j] = comp(tinv_hi, q);
+    const uint64_t r32 = (uint64_t)((1ull << 32) % q);
+    dc.r32[j] = r32, dc.r32_p[j] = word_bits == 32 ? (uint64_t)((((u128)r32) << 32) / q) : 0;
     const uint64_t r64 = (uint64_t)(((u128)1 << 64) % q);
     dc.r64[j] = r64, dc.r64_p[j] = shoup_companion(r64, q);
     dc.one_p[j] = ~0ull / q;

@@ -23,6 +23,7 @@ struct DevConsts {
   uint64_t one_p[SECN_MAX_LIMBS];                           // floor(2^64 / q)
   uint64_t tinv[SECN_MAX_LIMBS], tinv_p[SECN_MAX_LIMBS];    // t^-1 mod q (Shoup, word-sized companion)
   uint64_t tinv_hi[SECN_MAX_LIMBS], tinv_hi_p[SECN_MAX_LIMBS];  // 2^32 t^-1 mod q (32-bit limbs)
+  uint64_t r32[SECN_MAX_LIMBS], r32_p[SECN_MAX_LIMBS];      // 2^32 mod q (32-bit Shoup; 32-bit limbs)
   uint64_t qmt;                                             // Q mod t
   uint32_t t_bits, log_n, L, word_bits;
   const ulonglong2* tw_fwd;  // [L][N] (psi^brv(i), w')      word_bits = 64

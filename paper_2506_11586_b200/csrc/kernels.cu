@@ -14,6 +14,8 @@
 #include "ntt_core.cuh"
 #include "tma.cuh"
 
+#include <cudaTypedefs.h>
+
 namespace secn {
 
 // ------------------------------------------------------------------------------------------
@@ -38,21 +40,28 @@ struct Tab<Arith32> {
 // and Q = 0 (mod q_j):  enc_j(v) = -rho t^-1 + [rho >= t/2]  (mod q_j).
 // rho is one 64-bit low product; rho t^-1 one Shoup product (64-bit limbs) or two 32-bit Shoup
 // products on the 32-bit halves of rho (32-bit limbs). Canonical result in [0, q).
+// Per-limb encoding constants, loaded once per thread.
+struct EncK {
+  uint64_t qmt, q, tinv, tinv_p, tinv_hi, tinv_hi_p;
+  uint32_t tbits;
+  __device__ __forceinline__ EncK(const DevConsts& c, int j)
+      : qmt(c.qmt), q(c.q[j]), tinv(c.tinv[j]), tinv_p(c.tinv_p[j]), tinv_hi(c.tinv_hi[j]),
+        tinv_hi_p(c.tinv_hi_p[j]), tbits(c.t_bits) {}
+};
+
 template <class A>
-__device__ __forceinline__ typename A::W enc_mod(uint64_t v, int j, const DevConsts& c) {
-  const uint64_t tmask = (1ull << c.t_bits) - 1;
-  const uint64_t rho = (c.qmt * v) & tmask;
-  const uint32_t up = rho >= (1ull << (c.t_bits - 1));
+__device__ __forceinline__ typename A::W enc_mod(uint64_t v, const EncK& k) {
+  const uint64_t rho = (k.qmt * v) & ((1ull << k.tbits) - 1);
+  const uint32_t up = rho >= (1ull << (k.tbits - 1));
   if constexpr (sizeof(typename A::W) == 8) {
-    const uint64_t q = c.q[j];
-    const uint64_t a = shoup(rho, c.tinv[j], c.tinv_p[j], q);  // [0, 2q)
-    const uint64_t e = 2 * q - a + up;                           // [1, 2q + 1]
-    return csub(csub(e, q), q);
+    const uint64_t a = shoup(rho, k.tinv, k.tinv_p, k.q);  // [0, 2q)
+    const uint64_t e = 2 * k.q - a + up;                     // [1, 2q + 1]
+    return csub(csub(e, k.q), k.q);
   } else {
-    const uint32_t q = (uint32_t)c.q[j];
-    const uint32_t a = Arith32::shoup32((uint32_t)rho, (uint32_t)c.tinv[j], (uint32_t)c.tinv_p[j], q) +
-                       Arith32::shoup32((uint32_t)(rho >> 32), (uint32_t)c.tinv_hi[j], (uint32_t)c.tinv_hi_p[j], q);
-    uint32_t e = 4 * q - a + up;                                 // [1, 4q + 1]
+    const uint32_t q = (uint32_t)k.q;
+    const uint32_t a = Arith32::shoup32((uint32_t)rho, (uint32_t)k.tinv, (uint32_t)k.tinv_p, q) +
+                       Arith32::shoup32((uint32_t)(rho >> 32), (uint32_t)k.tinv_hi, (uint32_t)k.tinv_hi_p, q);
+    uint32_t e = 4 * q - a + up;                             // [1, 4q + 1]
     e = csub32(e, 2 * q);
     return csub32(csub32(e, q), q);
   }
@@ -81,6 +90,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN>())
   const W* src = in + p * N;
   const bool share = x0 != nullptr && ((p / c.L) & 1);
   const uint64_t* xs = share ? x0 + (p / (2 * c.L)) * N : nullptr;
+  const EncK ek(c, j);
   W x[16];
 #pragma unroll
   for (int k = 0; k < R0::NT; ++k)
@@ -88,7 +98,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN>())
     for (int i = 0; i < R0::GK; ++i) {
       const uint32_t e = R0::addr(k, i);
       W v = src[e];
-      if (share) v += enc_mod<A>(__ldg(&xs[e]), j, c);  // < 2q: inside the CT domain
+      if (share) v += enc_mod<A>(__ldg(&xs[e]), ek);  // < 2q: inside the CT domain
       x[k * R0::GK + i] = v;
     }
   {
@@ -102,7 +112,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN>())
 #pragma unroll
   for (int k = 0; k < 16; ++k) {
     const uint32_t e = threadIdx.x + k * T;
-    dst[e] = A::canon_ct(sm[swz<A>(e)], q);
+    dst[e] = A::canon_ct(sm[phys(e)], q);
   }
 }
 
@@ -128,7 +138,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN>())
 #pragma unroll
   for (int k = 0; k < 16; ++k) {
     const uint32_t e = threadIdx.x + k * T;
-    sm[swz<A>(e)] = buf[e];
+    sm[phys(e)] = buf[e];
   }
   // the mask words this thread adds at the end, loaded now so their latency hides behind the
   // transform (the last round's tasks are coalesced: element RL::addr(k, i))
@@ -148,6 +158,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN>())
   W x[16];
   gs_load<A, LOGN, LL>(x, sm);
   gs_compute<A, LOGN, LL>(x, tws, q, qb, ninv, wl);
+  const EncK ek(c, j);
 #pragma unroll
   for (int k = 0; k < RL::NT; ++k)
 #pragma unroll
@@ -155,7 +166,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN>())
       const uint32_t e = RL::addr(k, i);
       W v = A::canon_gs(x[k * RL::GK + i], q);
       if (mask) {
-        v += enc_mod<A>(rv[k * RL::GK + i], j, c);  // < 2q
+        v += enc_mod<A>(rv[k * RL::GK + i], ek);  // < 2q
         v = v >= q ? v - q : v;
       }
       buf[e] = v;
@@ -177,9 +188,12 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN>())
 // the grid so the second read of a tile hits L2.
 constexpr int MAC_THREADS = 256;  // consumers; +32 producer threads
 
-__device__ __forceinline__ uint32_t reduce64(uint64_t a, uint64_t q, uint64_t onep) {
-  const uint64_t r = a - mulhi(a, onep) * q;  // [0, 2q)
-  return (uint32_t)(r >= q ? r - q : r);
+// a mod q for a < 2^64, q < 2^28: a = hi 2^32 + lo with r32 = 2^32 mod q and the 32-bit Shoup
+// companions r32p (of r32) and onep32 (of 1); three IMADs per half.
+__device__ __forceinline__ uint32_t reduce64(uint64_t a, uint32_t q, uint32_t r32, uint32_t r32p, uint32_t onep32) {
+  const uint32_t lo = (uint32_t)a, hi = (uint32_t)(a >> 32);
+  const uint32_t x = Arith32::shoup32(hi, r32, r32p, q) + (lo - __umulhi(lo, onep32) * q);  // [0, 4q)
+  return csub32(csub32(x, 2 * q), q);
 }
 
 // Register blocking: each consumer thread accumulates an [MT][2*SG] block of outputs (MT output
@@ -189,8 +203,8 @@ __device__ __forceinline__ uint32_t reduce64(uint64_t a, uint64_t q, uint64_t on
 // MT * 2 * SG multiply-accumulates.
 template <class W, int SG, int MT>
 __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
-    k_mac(const W* __restrict__ xhat, const W* __restrict__ w, W* __restrict__ y, const __grid_constant__ DevConsts c,
-          PlanDev pl, int m_range, int n_sg, int NS) {
+    k_mac(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmw, W* __restrict__ y,
+          const __grid_constant__ DevConsts c, PlanDev pl, int m_range, int n_sg, int NS) {
   extern __shared__ __align__(128) unsigned char smraw[];
   constexpr int A2 = 2 * SG;
   const int N = 1 << c.log_n, L = c.L, G = pl.G, S = pl.S;
@@ -220,21 +234,19 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
 
   if (tid >= MAC_THREADS) {  // ---- producer warp: one elected lane streams X^ once, then the weights ----
     if (tid == MAC_THREADS) {
-      mbar_arrive_expect_tx(xbar, G * 2 * ns * row_bytes);
-      for (int g = 0; g < G; ++g)
-        for (int a = 0; a < 2 * ns; ++a)
-          tma_load_1d(xs + (g * A2 + a) * MAC_THREADS,
-                      xhat + ((((size_t)g * S + s0 + (a >> 1)) * 2 + (a & 1)) * L + j) * N + e0, row_bytes, xbar);
+      prefetch_tmap(&tmx);
+      prefetch_tmap(&tmw);
+      // X^ tile: box (256 coefficients, limb j, 2*SG rows (s, c), G groups) in [g][a][256] order
+      mbar_arrive_expect_tx(xbar, G * A2 * row_bytes);
+      tma_load_4d(xs, &tmx, e0, j, 2 * s0, 0, xbar);
       int st = 0;
       uint32_t ph = 0, first = 1;  // ring position, its phase, and "first lap" (no wait needed)
       for (int mb = m_begin; mb < m_end; mb += MT) {
-        const int rows = min(MT, m_end - mb);
         for (int g = 0; g < G; ++g) {
           if (!first) mbar_wait(&empty[st], ph ^ 1);
-          mbar_arrive_expect_tx(&full[st], rows * row_bytes);
-          for (int r = 0; r < rows; ++r)
-            tma_load_1d(ring + ((size_t)st * MT + r) * MAC_THREADS, w + (((size_t)(mb + r) * G + g) * L + j) * N + e0,
-                        row_bytes, &full[st]);
+          // weights: box (256 coefficients, row g*L + j, MT output channels from mb)
+          mbar_arrive_expect_tx(&full[st], MT * row_bytes);
+          tma_load_3d(ring + (size_t)st * MT * MAC_THREADS, &tmw, e0, g * L + j, mb, &full[st]);
           if (++st == NS) st = 0, ph ^= 1, first = 0;
         }
       }
@@ -242,9 +254,10 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
     return;
   }
 
-  // ---- consumers: one coefficient each (X^ rows beyond 2*ns hold stale data; never stored) ----
+  // ---- consumers: one coefficient each (X^ rows beyond 2*ns are zero-filled; never stored) ----
   const uint32_t e = e0 + tid;
   const uint64_t q = c.q[j], onep = c.one_p[j];
+  const uint32_t r32 = (uint32_t)c.r32[j], r32p = (uint32_t)c.r32_p[j], onep32 = (uint32_t)(onep >> 32);
   mbar_wait(xbar, 0);
   int st = 0;
   uint32_t ph = 0;
@@ -277,7 +290,8 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
 #pragma unroll
         for (int a = 0; a < A2; ++a)
           if (r < rows && a < 2 * ns)
-            y[((((size_t)(mb + r) * S + s0 + (a >> 1)) * 2 + (a & 1)) * L + j) * N + e] = (W)reduce64(acc[r][a], q, onep);
+            y[((((size_t)(mb + r) * S + s0 + (a >> 1)) * 2 + (a & 1)) * L + j) * N + e] =
+                (W)reduce64(acc[r][a], (uint32_t)q, r32, r32p, onep32);
     } else {
       const uint64_t r64 = c.r64[j], r64p = c.r64_p[j];
       uint64_t lo[MT][A2], hi[MT][A2];
@@ -351,7 +365,7 @@ __global__ void k_enc_add(typename A::W* __restrict__ ct, const uint64_t* __rest
     const size_t i = idx / (N * c.L);
     W* b = ct + ((i * 2 + 1) * c.L + j) * N + e;
     const uint64_t q = c.q[j];
-    const uint64_t s = (uint64_t)*b + (uint64_t)enc_mod<A>(v[i * N + e], j, c);  // [0, 2q)
+    const uint64_t s = (uint64_t)*b + (uint64_t)enc_mod<A>(v[i * N + e], EncK(c, j));  // [0, 2q)
     *b = (W)(s >= q ? s - q : s);
   }
 }
@@ -392,7 +406,7 @@ static cudaError_t ntt_fwd_t(const DevConsts& c, const void* in, void* out, size
                              cudaStream_t s) {
   using W = typename A::W;
   constexpr int N = 1 << LOGN;
-  const size_t smem = N * sizeof(W);
+  const size_t smem = smem_words<LOGN>() * sizeof(W);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_ntt_fwd<A, LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -410,7 +424,7 @@ template <class A, int LOGN>
 static cudaError_t ntt_inv_t(const DevConsts& c, void* polys, size_t P, const uint64_t* r, cudaStream_t s) {
   using W = typename A::W;
   constexpr int N = 1 << LOGN;
-  const size_t smem = N * sizeof(W);
+  const size_t smem = smem_words<LOGN>() * sizeof(W);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_ntt_inv<A, LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -460,15 +474,40 @@ cudaError_t launch_ntt_inv(const DevConsts& c, void* polys, size_t P, const uint
   return cudaErrorInvalidValue;
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link dependency)
+static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+static bool encode_tmap(CUtensorMap* m, int wb, int rank, const void* base, const cuuint64_t* dims,
+                        const cuuint64_t* strides_bytes, const cuuint32_t* box) {
+  auto enc = tmap_encoder();
+  if (!enc) return false;
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  return enc(m, wb == 4 ? CU_TENSOR_MAP_DATA_TYPE_UINT32 : CU_TENSOR_MAP_DATA_TYPE_UINT64, rank,
+             const_cast<void*>(base), dims, strides_bytes, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <class W, int SG, int MT>
 static cudaError_t mac_t(const DevConsts& c, const PlanDev& p, const void* xhat, const void* w, void* y,
                          cudaStream_t s) {
   const int N = 1 << c.log_n;
   const size_t xtile = (size_t)p.G * 2 * SG * MAC_THREADS * sizeof(W);
   const size_t stage = (size_t)MT * MAC_THREADS * sizeof(W);
-  // ring depth: ~40 KiB of weights in flight per CTA (2 CTAs per SM), 3..12 stages
-  int NS = (int)((40 * 1024) / stage);
-  NS = NS < 3 ? 3 : NS > 12 ? 12 : NS;
+  // ring depth: fill ~110 KiB per CTA (two CTAs per SM) after the X^ tile, 4..32 stages
+  const size_t budget = 110 * 1024 > xtile + 4 * stage ? 110 * 1024 - xtile : 4 * stage;
+  int NS = (int)(budget / stage);
+  NS = NS < 4 ? 4 : NS > 32 ? 32 : NS;
   const size_t smem = xtile + NS * stage + (2 * NS + 1) * sizeof(uint64_t);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   static size_t attr = 0;
@@ -486,9 +525,19 @@ static cudaError_t mac_t(const DevConsts& c, const PlanDev& p, const void* xhat,
   if (mr < 2 * MT) mr = 2 * MT;
   const int m_range = (int)(mr < (long)p.M ? mr : (long)p.M);
   const int n_mr = (p.M + m_range - 1) / m_range;
+  // tensor maps: X^ [G][S*2][L][N] viewed as (N, L, 2S, G); W [M][G][L][N] as (N, G*L, M)
+  const cuuint64_t wb = sizeof(W);
+  CUtensorMap tmx, tmw;
+  const cuuint64_t xd[4] = {(cuuint64_t)N, c.L, 2ull * p.S, p.G};
+  const cuuint64_t xs_[3] = {N * wb, (cuuint64_t)c.L * N * wb, 2ull * p.S * c.L * N * wb};
+  const cuuint32_t xb[4] = {MAC_THREADS, 1, 2 * SG, p.G};
+  const cuuint64_t wd[3] = {(cuuint64_t)N, (cuuint64_t)p.G * c.L, p.M};
+  const cuuint64_t ws_[2] = {N * wb, (cuuint64_t)p.G * c.L * N * wb};
+  const cuuint32_t wbx[3] = {MAC_THREADS, 1, MT};
+  if (!encode_tmap(&tmx, (int)wb, 4, xhat, xd, xs_, xb) || !encode_tmap(&tmw, (int)wb, 3, w, wd, ws_, wbx))
+    return cudaErrorInvalidValue;
   dim3 grid((N / MAC_THREADS) * n_sg, c.L, n_mr);
-  k_mac<W, SG, MT><<<grid, MAC_THREADS + 32, smem, s>>>(static_cast<const W*>(xhat), static_cast<const W*>(w),
-                                                      static_cast<W*>(y), c, p, m_range, n_sg, NS);
+  k_mac<W, SG, MT><<<grid, MAC_THREADS + 32, smem, s>>>(tmx, tmw, static_cast<W*>(y), c, p, m_range, n_sg, NS);
   return cudaGetLastError();
 }
 

@@ -7,7 +7,7 @@
 //
 // A "round" performs K <= 4 consecutive stages in registers: the 2^K elements of a task are
 // blk*B + off + i*D (i < 2^K) and every thread owns 16/2^K tasks. Rounds exchange data through
-// shared memory, XOR-swizzled (swz) so every round pattern is bank-conflict free.
+// shared memory in a padded layout (phys) that makes every round's addresses immediate offsets.
 #pragma once
 #include <cstdint>
 
@@ -15,16 +15,14 @@
 
 namespace secn {
 
-// 64-bit words: XOR bits 0..3 with bits 4..7 (a half-warp's 16 lanes hit 16 distinct bank pairs);
-// 32-bit words: XOR bits 0..4 with bits 4..8 (32 distinct banks per warp at N = 4096; at most
-// 2-way for a few rounds at larger N). Both are bijections on [0, N).
-template <class A>
-__device__ __forceinline__ uint32_t swz(uint32_t e) {
-  if constexpr (sizeof(typename A::W) == 4)
-    return e ^ ((e >> 4) & 31u);
-  else
-    return e ^ ((e >> 4) & 15u);
-}
+// Shared-memory layout: word e lives at phys(e) = e + (e >> 4) (one pad word per 16). Every
+// round's task pattern then maps to phys(base) + const, so addresses are immediate offsets from
+// one per-task base register, and 64-bit words are bank-conflict free in every pattern (16 lanes
+// hit 16 distinct bank pairs); 32-bit words see at most 2-way conflicts on the contiguous
+// patterns. A buffer of N words needs N + N/16 words.
+__host__ __device__ __forceinline__ constexpr uint32_t phys(uint32_t e) { return e + (e >> 4); }
+template <int LOGN>
+constexpr int smem_words() { return (1 << LOGN) + (1 << LOGN) / 16; }
 
 template <int LOGN, int S0>
 struct CtRound {
@@ -36,6 +34,9 @@ struct CtRound {
     const uint32_t tau = threadIdx.x + k * T;
     return ((tau >> logD) << logB) + (tau & ((1u << logD) - 1)) + (i << logD);
   }
+  // phys(addr(k, i)) = pbase(k) + poff(i) (see phys)
+  __device__ static __forceinline__ uint32_t pbase(int k) { return phys(addr(k, 0)); }
+  __host__ __device__ static constexpr uint32_t poff(int i) { return (i << logD) + ((i << logD) >> 4); }
 };
 
 // Twiddles of one round, gathered into registers before the round's barrier so their load
@@ -85,7 +86,7 @@ __device__ __forceinline__ void ct_load(typename A::W (&x)[16], const typename A
 #pragma unroll
   for (int k = 0; k < R::NT; ++k)
 #pragma unroll
-    for (int i = 0; i < R::GK; ++i) x[k * R::GK + i] = sm[swz<A>(R::addr(k, i))];
+    for (int i = 0; i < R::GK; ++i) x[k * R::GK + i] = sm[R::pbase(k) + R::poff(i)];
 }
 
 template <class A, int LOGN, int S0>
@@ -94,7 +95,7 @@ __device__ __forceinline__ void ct_store(const typename A::W (&x)[16], typename 
 #pragma unroll
   for (int k = 0; k < R::NT; ++k)
 #pragma unroll
-    for (int i = 0; i < R::GK; ++i) sm[swz<A>(R::addr(k, i))] = x[k * R::GK + i];
+    for (int i = 0; i < R::GK; ++i) sm[R::pbase(k) + R::poff(i)] = x[k * R::GK + i];
 }
 
 // Rounds S0.. to the end, each: gather twiddles, barrier (the previous round's stores), smem ->
@@ -129,6 +130,9 @@ struct GsRound {
     const uint32_t tau = threadIdx.x + k * T;
     return ((tau >> logD) << logB) + (tau & ((1u << logD) - 1)) + (i << logD);
   }
+  // phys(addr(k, i)) = pbase(k) + poff(i) (see phys)
+  __device__ static __forceinline__ uint32_t pbase(int k) { return phys(addr(k, 0)); }
+  __host__ __device__ static constexpr uint32_t poff(int i) { return (i << logD) + ((i << logD) >> 4); }
 };
 
 // Twiddles of one GS round: task k, level p, group gi -> tws[k * (GK - 1) + GK - (GK >> p) + gi]
@@ -194,7 +198,7 @@ __device__ __forceinline__ void gs_load(typename A::W (&x)[16], const typename A
 #pragma unroll
   for (int k = 0; k < R::NT; ++k)
 #pragma unroll
-    for (int i = 0; i < R::GK; ++i) x[k * R::GK + i] = sm[swz<A>(R::addr(k, i))];
+    for (int i = 0; i < R::GK; ++i) x[k * R::GK + i] = sm[R::pbase(k) + R::poff(i)];
 }
 
 template <class A, int LOGN, int L0>
@@ -203,7 +207,7 @@ __device__ __forceinline__ void gs_store(const typename A::W (&x)[16], typename 
 #pragma unroll
   for (int k = 0; k < R::NT; ++k)
 #pragma unroll
-    for (int i = 0; i < R::GK; ++i) sm[swz<A>(R::addr(k, i))] = x[k * R::GK + i];
+    for (int i = 0; i < R::GK; ++i) sm[R::pbase(k) + R::poff(i)] = x[k * R::GK + i];
 }
 
 // All GS rounds except the last one, each: gather twiddles, barrier, smem -> regs -> smem. The
