@@ -67,15 +67,19 @@ __device__ __forceinline__ typename A::W enc_mod(uint64_t v, const EncK& k) {
   }
 }
 
-template <class A, int LOGN>
-constexpr int ntt_min_blocks() { return LOGN == 12 ? (sizeof(typename A::W) == 4 ? 3 : 2) : 1; }
+template <class A, int LOGN, int NP>
+constexpr int ntt_min_blocks() {
+  return LOGN == 12 ? (sizeof(typename A::W) * NP == 4 ? 3 : 2) : 1;
+}
 
 // ------------------------------------------------------------------------------------------
 // K1: forward NTT of limb-polys [P][N] (limb j = p mod L), optionally fused server-share add
-// on the b component of ciphertexts [n][2][L][N]: b_j += enc_j(x0[n]). The
-// first radix-16 round reads global memory directly (its tasks are coalesced).
-template <class A, int LOGN>
-__global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN>())
+// on the b component of ciphertexts [n][2][L][N]: b_j += enc_j(x0[n]).
+// A CTA transforms NP polys of the same limb j: polys (g*NP + pp)*L + j, pp < NP, where g is
+// the CTA's poly group (blockIdx.x / L); with NP = 2 these are the a and b components of one
+// ciphertext. The first radix-16 round reads global memory directly (its tasks are coalesced).
+template <class A, int LOGN, int NP>
+__global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN, NP>())
     k_ntt_fwd(const typename A::W* in, typename A::W* out, const __grid_constant__ DevConsts c,
               const uint64_t* __restrict__ x0) {
   using W = typename A::W;
@@ -83,44 +87,50 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN>())
   constexpr int N = 1 << LOGN, T = N / 16;
   extern __shared__ __align__(16) unsigned char smraw[];
   W* sm = reinterpret_cast<W*>(smraw);
-  const size_t p = blockIdx.x;
-  const int j = (int)(p % c.L);
+  const int j = (int)(blockIdx.x % c.L);
+  const size_t grp = blockIdx.x / c.L;
   const W q = (W)c.q[j], qb = A::bound(q);
   const typename A::Tw* tw = Tab<A>::fwd(c) + (size_t)j * N;
-  const W* src = in + p * N;
-  const bool share = x0 != nullptr && ((p / c.L) & 1);
-  const uint64_t* xs = share ? x0 + (p / (2 * c.L)) * N : nullptr;
   const EncK ek(c, j);
-  W x[16];
+  typename A::Tw tws[15];
+  ct_twiddles<A, LOGN, 0>(tws, tw);
+  W x[NP][16];
 #pragma unroll
-  for (int k = 0; k < R0::NT; ++k)
+  for (int pp = 0; pp < NP; ++pp) {
+    const size_t pi = grp * NP + pp;  // poly index (ct * 2 + component for ciphertext batches)
+    const W* src = in + (pi * c.L + j) * N;
+    const bool share = x0 != nullptr && (pi & 1);
+    const uint64_t* xs = share ? x0 + (pi >> 1) * N : nullptr;
 #pragma unroll
-    for (int i = 0; i < R0::GK; ++i) {
-      const uint32_t e = R0::addr(k, i);
-      W v = src[e];
-      if (share) v += enc_mod<A>(__ldg(&xs[e]), ek);  // < 2q: inside the CT domain
-      x[k * R0::GK + i] = v;
-    }
-  {
-    typename A::Tw tws[15];
-    ct_twiddles<A, LOGN, 0>(tws, tw);
-    ct_compute<A, LOGN, 0>(x, tws, q, qb);
+    for (int k = 0; k < R0::NT; ++k)
+#pragma unroll
+      for (int i = 0; i < R0::GK; ++i) {
+        const uint32_t e = R0::addr(k, i);
+        W v = src[e];
+        if (share) v += enc_mod<A>(__ldg(&xs[e]), ek);  // < 2q: inside the CT domain
+        x[pp][k * R0::GK + i] = v;
+      }
   }
-  ct_store<A, LOGN, 0>(x, sm);
-  ct_rounds_smem<A, LOGN, R0::K>(sm, tw, q, qb);  // ends with a barrier
-  W* dst = out + p * N;
+  ct_compute<A, LOGN, 0, NP>(x, tws, q, qb);
+  round_store<R0, W, NP, LOGN>(x, sm);
+  ct_rounds_smem<A, LOGN, R0::K, NP>(sm, tw, q, qb);  // ends with a barrier
 #pragma unroll
-  for (int k = 0; k < 16; ++k) {
-    const uint32_t e = threadIdx.x + k * T;
-    dst[e] = A::canon_ct(sm[phys(e)], q);
+  for (int pp = 0; pp < NP; ++pp) {
+    W* dst = out + ((grp * NP + pp) * c.L + j) * N;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const uint32_t e = threadIdx.x + k * T;
+      dst[e] = A::canon_ct(sm[pp * smem_words<LOGN>() + phys(e)], q);
+    }
   }
 }
 
 // K3 (+A7 fused): inverse NTT of limb-polys in place; if r != NULL, on the b component of
-// ciphertexts [n][2][L][N]: b_j += enc_j(r[n]) after the transform. The last
-// radix-16 round writes global memory directly (its tasks are coalesced).
-template <class A, int LOGN>
-__global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN>())
+// ciphertexts [n][2][L][N]: b_j += enc_j(r[n]) after the transform. NP polys of
+// limb j per CTA as in K1. The last radix-16 round writes global memory directly (its tasks are
+// coalesced); the mask words are loaded at the start so their latency hides behind the transform.
+template <class A, int LOGN, int NP>
+__global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN, NP>())
     k_ntt_inv(typename A::W* polys, const __grid_constant__ DevConsts c, const uint64_t* __restrict__ r) {
   using W = typename A::W;
   constexpr int N = 1 << LOGN, T = N / 16;
@@ -128,49 +138,60 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN>())
   using RL = GsRound<LOGN, LL>;
   extern __shared__ __align__(16) unsigned char smraw[];
   W* sm = reinterpret_cast<W*>(smraw);
-  const size_t p = blockIdx.x;
-  const int j = (int)(p % c.L);
+  const int j = (int)(blockIdx.x % c.L);
+  const size_t grp = blockIdx.x / c.L;
   const W q = (W)c.q[j], qb = A::bound(q);
   const typename A::Tw* tw = Tab<A>::inv(c) + (size_t)j * N;
   const typename A::Tw ninv = Tab<A>::pair(c.ninv[j], c.ninv_p[j]);
   const typename A::Tw wl = Tab<A>::pair(c.wlast[j], c.wlast_p[j]);
-  W* buf = polys + p * N;
 #pragma unroll
-  for (int k = 0; k < 16; ++k) {
-    const uint32_t e = threadIdx.x + k * T;
-    sm[phys(e)] = buf[e];
+  for (int pp = 0; pp < NP; ++pp) {
+    const W* buf = polys + ((grp * NP + pp) * c.L + j) * N;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const uint32_t e = threadIdx.x + k * T;
+      sm[pp * smem_words<LOGN>() + phys(e)] = buf[e];
+    }
   }
-  // the mask words this thread adds at the end, loaded now so their latency hides behind the
-  // transform (the last round's tasks are coalesced: element RL::addr(k, i))
-  const bool mask = r != nullptr && ((p / c.L) & 1);
-  const uint64_t* rs = mask ? r + (p / (2 * c.L)) * N : nullptr;
-  uint64_t rv[16];
-  if (mask) {
+  // mask words for the b polys of this CTA (odd poly index), prefetched
+  uint64_t rv[NP][16];
 #pragma unroll
-    for (int k = 0; k < RL::NT; ++k)
+  for (int pp = 0; pp < NP; ++pp) {
+    const size_t pi = grp * NP + pp;
+    if (r != nullptr && (pi & 1)) {
+      const uint64_t* rs = r + (pi >> 1) * N;
 #pragma unroll
-      for (int i = 0; i < RL::GK; ++i) rv[k * RL::GK + i] = __ldg(&rs[RL::addr(k, i)]);
+      for (int k = 0; k < RL::NT; ++k)
+#pragma unroll
+        for (int i = 0; i < RL::GK; ++i) rv[pp][k * RL::GK + i] = __ldg(&rs[RL::addr(k, i)]);
+    }
   }
-  gs_rounds_smem_but_last<A, LOGN, 0>(sm, tw, q, qb, ninv, wl);
+  gs_rounds_smem_but_last<A, LOGN, 0, NP>(sm, tw, q, qb, ninv, wl);
   typename A::Tw tws[15];
   gs_twiddles<A, LOGN, LL>(tws, tw);
   __syncthreads();
-  W x[16];
-  gs_load<A, LOGN, LL>(x, sm);
-  gs_compute<A, LOGN, LL>(x, tws, q, qb, ninv, wl);
+  W x[NP][16];
+  round_load<RL, W, NP, LOGN>(x, sm);
+  gs_compute<A, LOGN, LL, NP>(x, tws, q, qb, ninv, wl);
   const EncK ek(c, j);
 #pragma unroll
-  for (int k = 0; k < RL::NT; ++k)
+  for (int pp = 0; pp < NP; ++pp) {
+    const size_t pi = grp * NP + pp;
+    const bool mask = r != nullptr && (pi & 1);
+    W* buf = polys + (pi * c.L + j) * N;
 #pragma unroll
-    for (int i = 0; i < RL::GK; ++i) {
-      const uint32_t e = RL::addr(k, i);
-      W v = A::canon_gs(x[k * RL::GK + i], q);
-      if (mask) {
-        v += enc_mod<A>(rv[k * RL::GK + i], ek);  // < 2q
-        v = v >= q ? v - q : v;
+    for (int k = 0; k < RL::NT; ++k)
+#pragma unroll
+      for (int i = 0; i < RL::GK; ++i) {
+        const uint32_t e = RL::addr(k, i);
+        W v = A::canon_gs(x[pp][k * RL::GK + i], q);
+        if (mask) {
+          v += enc_mod<A>(rv[pp][k * RL::GK + i], ek);  // < 2q
+          v = v >= q ? v - q : v;
+        }
+        buf[e] = v;
       }
-      buf[e] = v;
-    }
+  }
 }
 
 // ------------------------------------------------------------------------------------------
@@ -401,40 +422,67 @@ __global__ void k_check_range(const W* __restrict__ v, size_t n_words, const __g
 // ------------------------------------------------------------------------------------------
 // launchers
 
-template <class A, int LOGN>
-static cudaError_t ntt_fwd_t(const DevConsts& c, const void* in, void* out, size_t P, const uint64_t* x0,
-                             cudaStream_t s) {
+// Launch geometry of the NTT kernels: NP = 2 (two polys of one limb per CTA, shared twiddles)
+// for 32-bit limbs at N = 4096 when the batch has an even poly count and fills the GPU several
+// times over; otherwise NP = 1. Both poly-index parities (ct, component) are preserved.
+template <class A, int LOGN, int NP>
+static cudaError_t ntt_fwd_np(const DevConsts& c, const void* in, void* out, size_t n_polys, const uint64_t* x0,
+                              cudaStream_t s) {
   using W = typename A::W;
   constexpr int N = 1 << LOGN;
-  const size_t smem = smem_words<LOGN>() * sizeof(W);
+  const size_t smem = (size_t)NP * smem_words<LOGN>() * sizeof(W);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_ntt_fwd<A, LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_ntt_fwd<A, LOGN, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  for (size_t off = 0; off < P; off += 0x7fffffff) {
-    const size_t cnt = P - off < 0x7fffffff ? P - off : 0x7fffffff;
-    k_ntt_fwd<A, LOGN><<<(unsigned)cnt, N / 16, smem, s>>>(static_cast<const W*>(in) + off * N,
-                                                          static_cast<W*>(out) + off * N, c, x0);
+  // groups per launch: an even number so that x0's ct index stays (poly index) / 2
+  const size_t gmax = (0x7fffffffull / c.L) & ~(size_t)1;
+  const size_t ngroups = n_polys / NP;
+  for (size_t g0 = 0; g0 < ngroups; g0 += gmax) {
+    const size_t ng = ngroups - g0 < gmax ? ngroups - g0 : gmax;
+    const size_t off = g0 * NP * c.L * N;
+    k_ntt_fwd<A, LOGN, NP><<<(unsigned)(ng * c.L), N / 16, smem, s>>>(
+        static_cast<const W*>(in) + off, static_cast<W*>(out) + off, c, x0 ? x0 + g0 * NP / 2 * N : nullptr);
+  }
+  return cudaGetLastError();
+}
+
+template <class A, int LOGN, int NP>
+static cudaError_t ntt_inv_np(const DevConsts& c, void* polys, size_t n_polys, const uint64_t* r, cudaStream_t s) {
+  using W = typename A::W;
+  constexpr int N = 1 << LOGN;
+  const size_t smem = (size_t)NP * smem_words<LOGN>() * sizeof(W);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_ntt_inv<A, LOGN, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  const size_t gmax = (0x7fffffffull / c.L) & ~(size_t)1;
+  const size_t ngroups = n_polys / NP;
+  for (size_t g0 = 0; g0 < ngroups; g0 += gmax) {
+    const size_t ng = ngroups - g0 < gmax ? ngroups - g0 : gmax;
+    k_ntt_inv<A, LOGN, NP><<<(unsigned)(ng * c.L), N / 16, smem, s>>>(static_cast<W*>(polys) + g0 * NP * c.L * N, c,
+                                                                     r ? r + g0 * NP / 2 * N : nullptr);
   }
   return cudaGetLastError();
 }
 
 template <class A, int LOGN>
+static cudaError_t ntt_fwd_t(const DevConsts& c, const void* in, void* out, size_t P, const uint64_t* x0,
+                             cudaStream_t s) {
+  const size_t n_polys = P / c.L;
+  if (sizeof(typename A::W) == 4 && LOGN == 12 && n_polys % 2 == 0 && P >= 2 * 148 * 6)
+    return ntt_fwd_np<A, LOGN, 2>(c, in, out, n_polys, x0, s);
+  return ntt_fwd_np<A, LOGN, 1>(c, in, out, n_polys, x0, s);
+}
+
+template <class A, int LOGN>
 static cudaError_t ntt_inv_t(const DevConsts& c, void* polys, size_t P, const uint64_t* r, cudaStream_t s) {
-  using W = typename A::W;
-  constexpr int N = 1 << LOGN;
-  const size_t smem = smem_words<LOGN>() * sizeof(W);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_ntt_inv<A, LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
-  for (size_t off = 0; off < P; off += 0x7fffffff) {
-    const size_t cnt = P - off < 0x7fffffff ? P - off : 0x7fffffff;
-    k_ntt_inv<A, LOGN><<<(unsigned)cnt, N / 16, smem, s>>>(static_cast<W*>(polys) + off * N, c, r);
-  }
-  return cudaGetLastError();
+  const size_t n_polys = P / c.L;
+  if (sizeof(typename A::W) == 4 && LOGN == 12 && n_polys % 2 == 0 && P >= 2 * 148 * 6)
+    return ntt_inv_np<A, LOGN, 2>(c, polys, n_polys, r, s);
+  return ntt_inv_np<A, LOGN, 1>(c, polys, n_polys, r, s);
 }
 
 cudaError_t launch_ntt_fwd(const DevConsts& c, const void* in, void* out, size_t P, const uint64_t* x0,

@@ -1,5 +1,6 @@
-// Shared-memory negacyclic NTT core for one limb-poly per CTA (N = 2^LOGN, T = N/16 threads,
-// 16 words per thread in registers), parameterised by an arithmetic policy A (modarith.cuh).
+// Shared-memory negacyclic NTT core: NP limb-polys of the same limb per CTA (they share every
+// twiddle), N = 2^LOGN, T = N/16 threads, 16 words per poly per thread in registers;
+// parameterised by an arithmetic policy A (modarith.cuh).
 //
 // Forward = Cooley-Tukey with psi^brv twiddles, natural order in, bit-reversed order out
 // (reading R4: entry k holds a(psi^(2 brv(k)+1))); inverse = Gentleman-Sande with psi^-brv
@@ -19,10 +20,11 @@ namespace secn {
 // round's task pattern then maps to phys(base) + const, so addresses are immediate offsets from
 // one per-task base register, and 64-bit words are bank-conflict free in every pattern (16 lanes
 // hit 16 distinct bank pairs); 32-bit words see at most 2-way conflicts on the contiguous
-// patterns. A buffer of N words needs N + N/16 words.
+// patterns. A buffer of N words needs N + N/16 words (smem_words); poly p of a CTA starts at
+// p * smem_words.
 __host__ __device__ __forceinline__ constexpr uint32_t phys(uint32_t e) { return e + (e >> 4); }
 template <int LOGN>
-constexpr int smem_words() { return (1 << LOGN) + (1 << LOGN) / 16; }
+__host__ __device__ constexpr int smem_words() { return (1 << LOGN) + (1 << LOGN) / 16; }
 
 template <int LOGN, int S0>
 struct CtRound {
@@ -39,7 +41,48 @@ struct CtRound {
   __host__ __device__ static constexpr uint32_t poff(int i) { return (i << logD) + ((i << logD) >> 4); }
 };
 
-// Twiddles of one round, gathered into registers before the round's barrier so their load
+template <int LOGN, int L0>
+struct GsRound {
+  static constexpr int K = (LOGN - L0) >= 4 ? 4 : (LOGN - L0);
+  static constexpr int GK = 1 << K, NT = 16 / GK, T = (1 << LOGN) / 16;
+  static constexpr int logB = L0 + K, logD = L0;
+  __device__ static __forceinline__ uint32_t blk(int k) { return (threadIdx.x + k * T) >> logD; }
+  __device__ static __forceinline__ uint32_t addr(int k, int i) {
+    const uint32_t tau = threadIdx.x + k * T;
+    return ((tau >> logD) << logB) + (tau & ((1u << logD) - 1)) + (i << logD);
+  }
+  __device__ static __forceinline__ uint32_t pbase(int k) { return phys(addr(k, 0)); }
+  __host__ __device__ static constexpr uint32_t poff(int i) { return (i << logD) + ((i << logD) >> 4); }
+};
+
+// shared-memory round trip of the x[NP][16] register block of round R
+template <class R, class W, int NP, int LOGN>
+__device__ __forceinline__ void round_load(W (&x)[NP][16], const W* sm) {
+#pragma unroll
+  for (int k = 0; k < R::NT; ++k) {
+    const uint32_t b = R::pbase(k);
+#pragma unroll
+    for (int pp = 0; pp < NP; ++pp)
+#pragma unroll
+      for (int i = 0; i < R::GK; ++i) x[pp][k * R::GK + i] = sm[pp * smem_words<LOGN>() + b + R::poff(i)];
+  }
+}
+
+template <class R, class W, int NP, int LOGN>
+__device__ __forceinline__ void round_store(const W (&x)[NP][16], W* sm) {
+#pragma unroll
+  for (int k = 0; k < R::NT; ++k) {
+    const uint32_t b = R::pbase(k);
+#pragma unroll
+    for (int pp = 0; pp < NP; ++pp)
+#pragma unroll
+      for (int i = 0; i < R::GK; ++i) sm[pp * smem_words<LOGN>() + b + R::poff(i)] = x[pp][k * R::GK + i];
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Cooley-Tukey: stages S0 .. S0+K-1 (stage s: 2^s groups, group i uses psi^brv(2^s + i)).
+// Twiddles of one round are gathered into registers before the round's barrier so their load
 // latency overlaps it: task k, stage p, group u -> tws[k * (GK - 1) + (1 << p) - 1 + u] (<= 15).
 template <class A, int LOGN, int S0>
 __device__ __forceinline__ void ct_twiddles(typename A::Tw (&tws)[15], const typename A::Tw* __restrict__ tw) {
@@ -53,9 +96,8 @@ __device__ __forceinline__ void ct_twiddles(typename A::Tw (&tws)[15], const typ
         if (u < (1 << p)) tws[k * (R::GK - 1) + (1 << p) - 1 + u] = __ldg(&tw[(1u << (S0 + p)) + (R::blk(k) << p) + u]);
 }
 
-// stages S0 .. S0+K-1 on x[] (stage s: 2^s groups, group i uses psi^brv(2^s + i))
-template <class A, int LOGN, int S0>
-__device__ __forceinline__ void ct_compute(typename A::W (&x)[16], const typename A::Tw (&tws)[15],
+template <class A, int LOGN, int S0, int NP>
+__device__ __forceinline__ void ct_compute(typename A::W (&x)[NP][16], const typename A::Tw (&tws)[15],
                                            typename A::W q, typename A::W qb) {
   using R = CtRound<LOGN, S0>;
 #pragma unroll
@@ -71,7 +113,8 @@ __device__ __forceinline__ void ct_compute(typename A::W (&x)[16], const typenam
           for (int i = 0; i < 8; ++i) {
             if (i < half) {
               const int a = k * R::GK + u * (R::GK >> p) + i;
-              A::ct(x[a], x[a + half], w, q, qb);
+#pragma unroll
+              for (int pp = 0; pp < NP; ++pp) A::ct(x[pp][a], x[pp][a + half], w, q, qb);
             }
           }
         }
@@ -80,38 +123,21 @@ __device__ __forceinline__ void ct_compute(typename A::W (&x)[16], const typenam
   }
 }
 
-template <class A, int LOGN, int S0>
-__device__ __forceinline__ void ct_load(typename A::W (&x)[16], const typename A::W* sm) {
-  using R = CtRound<LOGN, S0>;
-#pragma unroll
-  for (int k = 0; k < R::NT; ++k)
-#pragma unroll
-    for (int i = 0; i < R::GK; ++i) x[k * R::GK + i] = sm[R::pbase(k) + R::poff(i)];
-}
-
-template <class A, int LOGN, int S0>
-__device__ __forceinline__ void ct_store(const typename A::W (&x)[16], typename A::W* sm) {
-  using R = CtRound<LOGN, S0>;
-#pragma unroll
-  for (int k = 0; k < R::NT; ++k)
-#pragma unroll
-    for (int i = 0; i < R::GK; ++i) sm[R::pbase(k) + R::poff(i)] = x[k * R::GK + i];
-}
-
 // Rounds S0.. to the end, each: gather twiddles, barrier (the previous round's stores), smem ->
 // regs -> smem. A final barrier follows the last round.
-template <class A, int LOGN, int S0>
+template <class A, int LOGN, int S0, int NP>
 __device__ __forceinline__ void ct_rounds_smem(typename A::W* sm, const typename A::Tw* __restrict__ tw,
                                                typename A::W q, typename A::W qb) {
   if constexpr (S0 < LOGN) {
+    using R = CtRound<LOGN, S0>;
     typename A::Tw tws[15];
     ct_twiddles<A, LOGN, S0>(tws, tw);
     __syncthreads();
-    typename A::W x[16];
-    ct_load<A, LOGN, S0>(x, sm);
-    ct_compute<A, LOGN, S0>(x, tws, q, qb);
-    ct_store<A, LOGN, S0>(x, sm);
-    ct_rounds_smem<A, LOGN, S0 + CtRound<LOGN, S0>::K>(sm, tw, q, qb);
+    typename A::W x[NP][16];
+    round_load<R, typename A::W, NP, LOGN>(x, sm);
+    ct_compute<A, LOGN, S0, NP>(x, tws, q, qb);
+    round_store<R, typename A::W, NP, LOGN>(x, sm);
+    ct_rounds_smem<A, LOGN, S0 + R::K, NP>(sm, tw, q, qb);
   } else {
     __syncthreads();
   }
@@ -120,23 +146,7 @@ __device__ __forceinline__ void ct_rounds_smem(typename A::W* sm, const typename
 // ------------------------------------------------------------------------------------------
 // Gentleman-Sande: levels L0 .. L0+K-1 (level l: half-distance 2^l, N/2^(l+1) groups, group i
 // uses psi^-brv(N/2^(l+1) + i)); the last level (l = LOGN-1) multiplies by N^-1 instead.
-template <int LOGN, int L0>
-struct GsRound {
-  static constexpr int K = (LOGN - L0) >= 4 ? 4 : (LOGN - L0);
-  static constexpr int GK = 1 << K, NT = 16 / GK, T = (1 << LOGN) / 16;
-  static constexpr int logB = L0 + K, logD = L0;
-  __device__ static __forceinline__ uint32_t blk(int k) { return (threadIdx.x + k * T) >> logD; }
-  __device__ static __forceinline__ uint32_t addr(int k, int i) {
-    const uint32_t tau = threadIdx.x + k * T;
-    return ((tau >> logD) << logB) + (tau & ((1u << logD) - 1)) + (i << logD);
-  }
-  // phys(addr(k, i)) = pbase(k) + poff(i) (see phys)
-  __device__ static __forceinline__ uint32_t pbase(int k) { return phys(addr(k, 0)); }
-  __host__ __device__ static constexpr uint32_t poff(int i) { return (i << logD) + ((i << logD) >> 4); }
-};
-
-// Twiddles of one GS round: task k, level p, group gi -> tws[k * (GK - 1) + GK - (GK >> p) + gi]
-// (the final level uses N^-1 and psi^-brv(1) N^-1 instead and gathers nothing).
+// Twiddles: task k, level p, group gi -> tws[k * (GK - 1) + GK - (GK >> p) + gi].
 template <class A, int LOGN, int L0>
 __device__ __forceinline__ void gs_twiddles(typename A::Tw (&tws)[15], const typename A::Tw* __restrict__ tw) {
   using R = GsRound<LOGN, L0>;
@@ -153,8 +163,8 @@ __device__ __forceinline__ void gs_twiddles(typename A::Tw (&tws)[15], const typ
   }
 }
 
-template <class A, int LOGN, int L0>
-__device__ __forceinline__ void gs_compute(typename A::W (&x)[16], const typename A::Tw (&tws)[15],
+template <class A, int LOGN, int L0, int NP>
+__device__ __forceinline__ void gs_compute(typename A::W (&x)[NP][16], const typename A::Tw (&tws)[15],
                                            typename A::W q, typename A::W qb, typename A::Tw ninv,
                                            typename A::Tw wlast) {
   using R = GsRound<LOGN, L0>;
@@ -167,9 +177,12 @@ __device__ __forceinline__ void gs_compute(typename A::W (&x)[16], const typenam
 #pragma unroll
         for (int i = 0; i < R::GK; ++i) {
           if (i & dist) continue;
-          const typename A::W u = x[k * R::GK + i], v = x[k * R::GK + i + dist];
-          x[k * R::GK + i] = A::mul4(u + v, ninv, q);
-          x[k * R::GK + i + dist] = A::mul4(u - v + qb, wlast, q);
+#pragma unroll
+          for (int pp = 0; pp < NP; ++pp) {
+            const typename A::W u = x[pp][k * R::GK + i], v = x[pp][k * R::GK + i + dist];
+            x[pp][k * R::GK + i] = A::mul4(u + v, ninv, q);
+            x[pp][k * R::GK + i + dist] = A::mul4(u - v + qb, wlast, q);
+          }
         }
     } else {
 #pragma unroll
@@ -182,7 +195,8 @@ __device__ __forceinline__ void gs_compute(typename A::W (&x)[16], const typenam
             for (int i = 0; i < 8; ++i) {
               if (i < dist) {
                 const int a = k * R::GK + gi * (2 * dist) + i;
-                A::gs(x[a], x[a + dist], w, q, qb);
+#pragma unroll
+                for (int pp = 0; pp < NP; ++pp) A::gs(x[pp][a], x[pp][a + dist], w, q, qb);
               }
             }
           }
@@ -192,39 +206,22 @@ __device__ __forceinline__ void gs_compute(typename A::W (&x)[16], const typenam
   }
 }
 
-template <class A, int LOGN, int L0>
-__device__ __forceinline__ void gs_load(typename A::W (&x)[16], const typename A::W* sm) {
-  using R = GsRound<LOGN, L0>;
-#pragma unroll
-  for (int k = 0; k < R::NT; ++k)
-#pragma unroll
-    for (int i = 0; i < R::GK; ++i) x[k * R::GK + i] = sm[R::pbase(k) + R::poff(i)];
-}
-
-template <class A, int LOGN, int L0>
-__device__ __forceinline__ void gs_store(const typename A::W (&x)[16], typename A::W* sm) {
-  using R = GsRound<LOGN, L0>;
-#pragma unroll
-  for (int k = 0; k < R::NT; ++k)
-#pragma unroll
-    for (int i = 0; i < R::GK; ++i) sm[R::pbase(k) + R::poff(i)] = x[k * R::GK + i];
-}
-
 // All GS rounds except the last one, each: gather twiddles, barrier, smem -> regs -> smem. The
 // caller gathers the last round's twiddles and places the last barrier.
-template <class A, int LOGN, int L0>
+template <class A, int LOGN, int L0, int NP>
 __device__ __forceinline__ void gs_rounds_smem_but_last(typename A::W* sm, const typename A::Tw* __restrict__ tw,
                                                         typename A::W q, typename A::W qb, typename A::Tw ninv,
                                                         typename A::Tw wlast) {
-  if constexpr (L0 + GsRound<LOGN, L0>::K < LOGN) {
+  using R = GsRound<LOGN, L0>;
+  if constexpr (L0 + R::K < LOGN) {
     typename A::Tw tws[15];
     gs_twiddles<A, LOGN, L0>(tws, tw);
     __syncthreads();
-    typename A::W x[16];
-    gs_load<A, LOGN, L0>(x, sm);
-    gs_compute<A, LOGN, L0>(x, tws, q, qb, ninv, wlast);
-    gs_store<A, LOGN, L0>(x, sm);
-    gs_rounds_smem_but_last<A, LOGN, L0 + GsRound<LOGN, L0>::K>(sm, tw, q, qb, ninv, wlast);
+    typename A::W x[NP][16];
+    round_load<R, typename A::W, NP, LOGN>(x, sm);
+    gs_compute<A, LOGN, L0, NP>(x, tws, q, qb, ninv, wlast);
+    round_store<R, typename A::W, NP, LOGN>(x, sm);
+    gs_rounds_smem_but_last<A, LOGN, L0 + R::K, NP>(sm, tw, q, qb, ninv, wlast);
   }
 }
 
