@@ -8,6 +8,7 @@
 // performs all HE MAC operations in NTT, and only transforms the final HE results back"),
 // PAPER.md:431 (§7: server share add, random mask), PAPER.md:668-679 (App. C.1 NTT).
 #include <cstdio>
+#include <utility>
 
 #include "internal.h"
 #include "modarith.cuh"
@@ -94,6 +95,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN, NP>(
   const EncK ek(c, j);
   typename A::Tw tws[15];
   ct_twiddles<A, LOGN, 0>(tws, tw);
+  pdl_wait();  // inputs may come from the preceding kernel
   W x[NP][16];
 #pragma unroll
   for (int pp = 0; pp < NP; ++pp) {
@@ -114,6 +116,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN, NP>(
   ct_compute<A, LOGN, 0, NP>(x, tws, q, qb);
   round_store<R0, W, NP, LOGN>(x, sm);
   ct_rounds_smem<A, LOGN, R0::K, NP>(sm, tw, q, qb);  // ends with a barrier
+  pdl_trigger();
 #pragma unroll
   for (int pp = 0; pp < NP; ++pp) {
     W* dst = out + ((grp * NP + pp) * c.L + j) * N;
@@ -144,16 +147,8 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN, NP>(
   const typename A::Tw* tw = Tab<A>::inv(c) + (size_t)j * N;
   const typename A::Tw ninv = Tab<A>::pair(c.ninv[j], c.ninv_p[j]);
   const typename A::Tw wl = Tab<A>::pair(c.wlast[j], c.wlast_p[j]);
-#pragma unroll
-  for (int pp = 0; pp < NP; ++pp) {
-    const W* buf = polys + ((grp * NP + pp) * c.L + j) * N;
-#pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      const uint32_t e = threadIdx.x + k * T;
-      sm[pp * smem_words<LOGN>() + phys(e)] = buf[e];
-    }
-  }
-  // mask words for the b polys of this CTA (odd poly index), prefetched
+  // mask words for the b polys of this CTA (odd poly index), prefetched; r is an input of the
+  // call, never produced by the preceding kernel, so it is read before the dependency wait
   uint64_t rv[NP][16];
 #pragma unroll
   for (int pp = 0; pp < NP; ++pp) {
@@ -166,6 +161,16 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN, NP>(
         for (int i = 0; i < RL::GK; ++i) rv[pp][k * RL::GK + i] = __ldg(&rs[RL::addr(k, i)]);
     }
   }
+  pdl_wait();  // the polys are produced by the preceding kernel (the MAC)
+#pragma unroll
+  for (int pp = 0; pp < NP; ++pp) {
+    const W* buf = polys + ((grp * NP + pp) * c.L + j) * N;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const uint32_t e = threadIdx.x + k * T;
+      sm[pp * smem_words<LOGN>() + phys(e)] = buf[e];
+    }
+  }
   gs_rounds_smem_but_last<A, LOGN, 0, NP>(sm, tw, q, qb, ninv, wl);
   typename A::Tw tws[15];
   gs_twiddles<A, LOGN, LL>(tws, tw);
@@ -173,6 +178,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN, NP>(
   W x[NP][16];
   round_load<RL, W, NP, LOGN>(x, sm);
   gs_compute<A, LOGN, LL, NP>(x, tws, q, qb, ninv, wl);
+  pdl_trigger();
   const EncK ek(c, j);
 #pragma unroll
   for (int pp = 0; pp < NP; ++pp) {
@@ -257,19 +263,36 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
     if (tid == MAC_THREADS) {
       prefetch_tmap(&tmx);
       prefetch_tmap(&tmw);
-      // X^ tile: box (256 coefficients, limb j, 2*SG rows (s, c), G groups) in [g][a][256] order
-      mbar_arrive_expect_tx(xbar, G * A2 * row_bytes);
-      tma_load_4d(xs, &tmx, e0, j, 2 * s0, 0, xbar);
-      int st = 0;
+      const uint64_t evict_first = policy_evict_first();  // weights are read once per query
+      // The weights are inputs of the call (never produced by the preceding kernel): the first
+      // lap of the ring is filled before the dependency wait, overlapping the forward NTT.
+      int st = 0, issued = 0;
       uint32_t ph = 0, first = 1;  // ring position, its phase, and "first lap" (no wait needed)
+      bool waited = false;
       for (int mb = m_begin; mb < m_end; mb += MT) {
         for (int g = 0; g < G; ++g) {
-          if (!first) mbar_wait(&empty[st], ph ^ 1);
+          if (!first) {
+            if (!waited) {
+              pdl_wait();
+              waited = true;
+              // X^ tile (written by the forward NTT): box (256 coefficients, limb j, 2*SG rows
+              // (s, c), G groups) in [g][a][256] order
+              mbar_arrive_expect_tx(xbar, G * A2 * row_bytes);
+              tma_load_4d(xs, &tmx, e0, j, 2 * s0, 0, xbar);
+            }
+            mbar_wait(&empty[st], ph ^ 1);
+          }
           // weights: box (256 coefficients, row g*L + j, MT output channels from mb)
           mbar_arrive_expect_tx(&full[st], MT * row_bytes);
-          tma_load_3d(ring + (size_t)st * MT * MAC_THREADS, &tmw, e0, g * L + j, mb, &full[st]);
+          tma_load_3d_hint(ring + (size_t)st * MT * MAC_THREADS, &tmw, e0, g * L + j, mb, &full[st], evict_first);
+          ++issued;
           if (++st == NS) st = 0, ph ^= 1, first = 0;
         }
+      }
+      if (!waited) {
+        pdl_wait();
+        mbar_arrive_expect_tx(xbar, G * A2 * row_bytes);
+        tma_load_4d(xs, &tmx, e0, j, 2 * s0, 0, xbar);
       }
     }
     return;
@@ -345,6 +368,7 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
                 (W)reduce128(lo[r][a], hi[r][a], q, r64, r64p, onep);
     }
   }
+  pdl_trigger();
 }
 
 // ------------------------------------------------------------------------------------------
@@ -394,6 +418,8 @@ __global__ void k_enc_add(typename A::W* __restrict__ ct, const uint64_t* __rest
 // Designated server share y0[m][oy][ox] = (t - r[m*S+s][O + i*Ww + j]) mod t.
 __global__ void k_extract_share(const uint64_t* __restrict__ r, uint64_t* __restrict__ y0,
                                 const __grid_constant__ DevConsts c, PlanDev pl) {
+  pdl_wait();
+  pdl_trigger();
   const size_t total = (size_t)pl.M * pl.OH * pl.OW;
   const size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   if (idx >= total) return;
@@ -422,6 +448,25 @@ __global__ void k_check_range(const W* __restrict__ v, size_t n_words, const __g
 // ------------------------------------------------------------------------------------------
 // launchers
 
+// Launch with programmatic stream serialization (PDL): the kernel may be scheduled while the
+// preceding kernel in the stream finishes; it synchronises with pdl_wait() before reading that
+// kernel's outputs. Captured into CUDA graphs as programmatic edges.
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 // Launch geometry of the NTT kernels: NP = 2 (two polys of one limb per CTA, shared twiddles)
 // for 32-bit limbs at N = 4096 when the batch has an even poly count and fills the GPU several
 // times over; otherwise NP = 1. Both poly-index parities (ct, component) are preserved.
@@ -442,8 +487,11 @@ static cudaError_t ntt_fwd_np(const DevConsts& c, const void* in, void* out, siz
   for (size_t g0 = 0; g0 < ngroups; g0 += gmax) {
     const size_t ng = ngroups - g0 < gmax ? ngroups - g0 : gmax;
     const size_t off = g0 * NP * c.L * N;
-    k_ntt_fwd<A, LOGN, NP><<<(unsigned)(ng * c.L), N / 16, smem, s>>>(
-        static_cast<const W*>(in) + off, static_cast<W*>(out) + off, c, x0 ? x0 + g0 * NP / 2 * N : nullptr);
+    const W* src = static_cast<const W*>(in) + off;
+    W* dst = static_cast<W*>(out) + off;
+    const uint64_t* xs = x0 ? x0 + g0 * NP / 2 * N : nullptr;
+    cudaError_t e = launch_pdl(k_ntt_fwd<A, LOGN, NP>, dim3((unsigned)(ng * c.L)), dim3(N / 16), smem, s, src, dst, c, xs);
+    if (e != cudaSuccess) return e;
   }
   return cudaGetLastError();
 }
@@ -462,8 +510,10 @@ static cudaError_t ntt_inv_np(const DevConsts& c, void* polys, size_t n_polys, c
   const size_t ngroups = n_polys / NP;
   for (size_t g0 = 0; g0 < ngroups; g0 += gmax) {
     const size_t ng = ngroups - g0 < gmax ? ngroups - g0 : gmax;
-    k_ntt_inv<A, LOGN, NP><<<(unsigned)(ng * c.L), N / 16, smem, s>>>(static_cast<W*>(polys) + g0 * NP * c.L * N, c,
-                                                                     r ? r + g0 * NP / 2 * N : nullptr);
+    W* buf = static_cast<W*>(polys) + g0 * NP * c.L * N;
+    const uint64_t* rs = r ? r + g0 * NP / 2 * N : nullptr;
+    cudaError_t e = launch_pdl(k_ntt_inv<A, LOGN, NP>, dim3((unsigned)(ng * c.L)), dim3(N / 16), smem, s, buf, c, rs);
+    if (e != cudaSuccess) return e;
   }
   return cudaGetLastError();
 }
@@ -472,16 +522,16 @@ template <class A, int LOGN>
 static cudaError_t ntt_fwd_t(const DevConsts& c, const void* in, void* out, size_t P, const uint64_t* x0,
                              cudaStream_t s) {
   const size_t n_polys = P / c.L;
-  if (sizeof(typename A::W) == 4 && LOGN == 12 && n_polys % 2 == 0 && P >= 2 * 148 * 6)
-    return ntt_fwd_np<A, LOGN, 2>(c, in, out, n_polys, x0, s);
+  if constexpr (sizeof(typename A::W) == 4 && LOGN == 12)
+    if (n_polys % 2 == 0 && P >= 2 * 148 * 6) return ntt_fwd_np<A, LOGN, 2>(c, in, out, n_polys, x0, s);
   return ntt_fwd_np<A, LOGN, 1>(c, in, out, n_polys, x0, s);
 }
 
 template <class A, int LOGN>
 static cudaError_t ntt_inv_t(const DevConsts& c, void* polys, size_t P, const uint64_t* r, cudaStream_t s) {
   const size_t n_polys = P / c.L;
-  if (sizeof(typename A::W) == 4 && LOGN == 12 && n_polys % 2 == 0 && P >= 2 * 148 * 6)
-    return ntt_inv_np<A, LOGN, 2>(c, polys, n_polys, r, s);
+  if constexpr (sizeof(typename A::W) == 4 && LOGN == 12)
+    if (n_polys % 2 == 0 && P >= 2 * 148 * 6) return ntt_inv_np<A, LOGN, 2>(c, polys, n_polys, r, s);
   return ntt_inv_np<A, LOGN, 1>(c, polys, n_polys, r, s);
 }
 
@@ -585,7 +635,10 @@ static cudaError_t mac_t(const DevConsts& c, const PlanDev& p, const void* xhat,
   if (!encode_tmap(&tmx, (int)wb, 4, xhat, xd, xs_, xb) || !encode_tmap(&tmw, (int)wb, 3, w, wd, ws_, wbx))
     return cudaErrorInvalidValue;
   dim3 grid((N / MAC_THREADS) * n_sg, c.L, n_mr);
-  k_mac<W, SG, MT><<<grid, MAC_THREADS + 32, smem, s>>>(tmx, tmw, static_cast<W*>(y), c, p, m_range, n_sg, NS);
+  W* yp = static_cast<W*>(y);
+  cudaError_t e = launch_pdl(k_mac<W, SG, MT>, grid, dim3(MAC_THREADS + 32), smem, s, tmx, tmw, yp, c, p, m_range,
+                             n_sg, NS);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
@@ -647,7 +700,10 @@ cudaError_t launch_enc_add(const DevConsts& c, void* ct, const uint64_t* v, size
 cudaError_t launch_extract_share(const DevConsts& c, const PlanDev& p, const uint64_t* r, uint64_t* y0,
                                  cudaStream_t s) {
   const size_t total = (size_t)p.M * p.OH * p.OW;
-  if (total) k_extract_share<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(r, y0, c, p);
+  if (total) {
+    cudaError_t e = launch_pdl(k_extract_share, dim3((unsigned)((total + 255) / 256)), dim3(256), 0, s, r, y0, c, p);
+    if (e != cudaSuccess) return e;
+  }
   return cudaGetLastError();
 }
 

@@ -13,6 +13,7 @@
 #include <cstdint>
 
 #include "modarith.cuh"
+#include "tma.cuh"
 
 namespace secn {
 
@@ -87,13 +88,15 @@ __device__ __forceinline__ void round_store(const W (&x)[NP][16], W* sm) {
 template <class A, int LOGN, int S0>
 __device__ __forceinline__ void ct_twiddles(typename A::Tw (&tws)[15], const typename A::Tw* __restrict__ tw) {
   using R = CtRound<LOGN, S0>;
+  const uint64_t pol = policy_evict_last();  // the tables are reused by every layer: keep them in L2
 #pragma unroll
   for (int p = 0; p < R::K; ++p)
 #pragma unroll
     for (int k = 0; k < R::NT; ++k)
 #pragma unroll
       for (int u = 0; u < 8; ++u)
-        if (u < (1 << p)) tws[k * (R::GK - 1) + (1 << p) - 1 + u] = __ldg(&tw[(1u << (S0 + p)) + (R::blk(k) << p) + u]);
+        if (u < (1 << p))
+          tws[k * (R::GK - 1) + (1 << p) - 1 + u] = ldg_hint(&tw[(1u << (S0 + p)) + (R::blk(k) << p) + u], pol);
 }
 
 template <class A, int LOGN, int S0, int NP>
@@ -150,6 +153,7 @@ __device__ __forceinline__ void ct_rounds_smem(typename A::W* sm, const typename
 template <class A, int LOGN, int L0>
 __device__ __forceinline__ void gs_twiddles(typename A::Tw (&tws)[15], const typename A::Tw* __restrict__ tw) {
   using R = GsRound<LOGN, L0>;
+  const uint64_t pol = policy_evict_last();
 #pragma unroll
   for (int p = 0; p < R::K; ++p) {
     if (L0 + p == LOGN - 1) continue;
@@ -159,7 +163,7 @@ __device__ __forceinline__ void gs_twiddles(typename A::Tw (&tws)[15], const typ
 #pragma unroll
       for (int gi = 0; gi < 8; ++gi)
         if (gi < (R::GK >> (p + 1)))
-          tws[k * (R::GK - 1) + R::GK - (R::GK >> p) + gi] = __ldg(&tw[h + (R::blk(k) << (R::K - p - 1)) + gi]);
+          tws[k * (R::GK - 1) + R::GK - (R::GK >> p) + gi] = ldg_hint(&tw[h + (R::blk(k) << (R::K - p - 1)) + gi], pol);
   }
 }
 
