@@ -70,7 +70,7 @@ __device__ __forceinline__ typename A::W enc_mod(uint64_t v, const EncK& k) {
 
 template <class A, int LOGN, int NP>
 constexpr int ntt_min_blocks() {
-  return LOGN == 12 ? (sizeof(typename A::W) * NP == 4 ? 3 : 2) : 1;
+  return LOGN == 12 ? (sizeof(typename A::W) == 4 ? 3 : 2) : 1;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -147,19 +147,22 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN, NP>(
   const typename A::Tw* tw = Tab<A>::inv(c) + (size_t)j * N;
   const typename A::Tw ninv = Tab<A>::pair(c.ninv[j], c.ninv_p[j]);
   const typename A::Tw wl = Tab<A>::pair(c.wlast[j], c.wlast_p[j]);
-  // mask words for the b polys of this CTA (odd poly index), prefetched; r is an input of the
-  // call, never produced by the preceding kernel, so it is read before the dependency wait
-  uint64_t rv[NP][16];
+  // Encoded mask words enc_j(r) for the b poly of this CTA (odd poly index; with NP = 2 the pair
+  // is (a, b) of one ciphertext, so at most one poly is masked). r is an input of the call, never
+  // produced by the preceding kernel, so it is loaded and encoded before the dependency wait --
+  // this work overlaps the previous kernel's tail -- and only the word-sized results are kept.
+  const EncK ek(c, j);
+  int mpp = -1;
 #pragma unroll
-  for (int pp = 0; pp < NP; ++pp) {
-    const size_t pi = grp * NP + pp;
-    if (r != nullptr && (pi & 1)) {
-      const uint64_t* rs = r + (pi >> 1) * N;
+  for (int pp = 0; pp < NP; ++pp)
+    if (r != nullptr && ((grp * NP + pp) & 1)) mpp = pp;
+  W em[16];
+  if (mpp >= 0) {
+    const uint64_t* rs = r + ((grp * NP + mpp) >> 1) * N;
 #pragma unroll
-      for (int k = 0; k < RL::NT; ++k)
+    for (int k = 0; k < RL::NT; ++k)
 #pragma unroll
-        for (int i = 0; i < RL::GK; ++i) rv[pp][k * RL::GK + i] = __ldg(&rs[RL::addr(k, i)]);
-    }
+      for (int i = 0; i < RL::GK; ++i) em[k * RL::GK + i] = enc_mod<A>(__ldg(&rs[RL::addr(k, i)]), ek);
   }
   pdl_wait();  // the polys are produced by the preceding kernel (the MAC)
 #pragma unroll
@@ -179,11 +182,9 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN, NP>(
   round_load<RL, W, NP, LOGN>(x, sm);
   gs_compute<A, LOGN, LL, NP>(x, tws, q, qb, ninv, wl);
   pdl_trigger();
-  const EncK ek(c, j);
 #pragma unroll
   for (int pp = 0; pp < NP; ++pp) {
     const size_t pi = grp * NP + pp;
-    const bool mask = r != nullptr && (pi & 1);
     W* buf = polys + (pi * c.L + j) * N;
 #pragma unroll
     for (int k = 0; k < RL::NT; ++k)
@@ -191,8 +192,8 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN, NP>(
       for (int i = 0; i < RL::GK; ++i) {
         const uint32_t e = RL::addr(k, i);
         W v = A::canon_gs(x[pp][k * RL::GK + i], q);
-        if (mask) {
-          v += enc_mod<A>(rv[pp][k * RL::GK + i], ek);  // < 2q
+        if (pp == mpp) {
+          v += em[k * RL::GK + i];  // < 2q
           v = v >= q ? v - q : v;
         }
         buf[e] = v;
