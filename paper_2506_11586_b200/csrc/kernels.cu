@@ -115,17 +115,23 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN, NP>(
   }
   ct_compute<A, LOGN, 0, NP>(x, tws, q, qb);
   round_store<R0, W, NP, LOGN>(x, sm);
-  ct_rounds_smem<A, LOGN, R0::K, NP>(sm, tw, q, qb);  // ends with a barrier
+  ct_rounds_smem_but_last<A, LOGN, R0::K, NP>(sm, tw, q, qb);
+  // last round: its tasks are contiguous, so the results go straight to global memory
+  constexpr int SL = CtLast<LOGN>::value;
+  using RL = CtRound<LOGN, SL>;
+  ct_twiddles<A, LOGN, SL>(tws, tw);
+  __syncthreads();
+  round_load<RL, W, NP, LOGN>(x, sm);
+  ct_compute<A, LOGN, SL, NP>(x, tws, q, qb);
   pdl_trigger();
 #pragma unroll
-  for (int pp = 0; pp < NP; ++pp) {
-    W* dst = out + ((grp * NP + pp) * c.L + j) * N;
+  for (int pp = 0; pp < NP; ++pp)
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      const uint32_t e = threadIdx.x + k * T;
-      dst[e] = A::canon_ct(sm[pp * smem_words<LOGN>() + phys(e)], q);
-    }
-  }
+    for (int i = 0; i < 16; ++i) x[pp][i] = A::canon_ct(x[pp][i], q);
+  W* dst[NP];
+#pragma unroll
+  for (int pp = 0; pp < NP; ++pp) dst[pp] = out + ((grp * NP + pp) * c.L + j) * N;
+  round_gstore<RL, W, NP>(x, dst);
 }
 
 // K3 (+A7 fused): inverse NTT of limb-polys in place; if r != NULL, on the b component of
@@ -164,21 +170,23 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN, NP>(
 #pragma unroll
       for (int i = 0; i < RL::GK; ++i) em[k * RL::GK + i] = enc_mod<A>(__ldg(&rs[RL::addr(k, i)]), ek);
   }
-  pdl_wait();  // the polys are produced by the preceding kernel (the MAC)
-#pragma unroll
-  for (int pp = 0; pp < NP; ++pp) {
-    const W* buf = polys + ((grp * NP + pp) * c.L + j) * N;
-#pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      const uint32_t e = threadIdx.x + k * T;
-      sm[pp * smem_words<LOGN>() + phys(e)] = buf[e];
-    }
-  }
-  gs_rounds_smem_but_last<A, LOGN, 0, NP>(sm, tw, q, qb, ninv, wl);
+  // round 0 (levels 0..3, contiguous tasks) straight from global memory
+  using R0 = GsRound<LOGN, 0>;
   typename A::Tw tws[15];
+  gs_twiddles<A, LOGN, 0>(tws, tw);
+  pdl_wait();  // the polys are produced by the preceding kernel (the MAC)
+  W x[NP][16];
+  {
+    const W* src[NP];
+#pragma unroll
+    for (int pp = 0; pp < NP; ++pp) src[pp] = polys + ((grp * NP + pp) * c.L + j) * N;
+    round_gload<R0, W, NP>(x, src);
+  }
+  gs_compute<A, LOGN, 0, NP>(x, tws, q, qb, ninv, wl);
+  round_store<R0, W, NP, LOGN>(x, sm);
+  gs_rounds_smem_but_last<A, LOGN, R0::K, NP>(sm, tw, q, qb, ninv, wl);
   gs_twiddles<A, LOGN, LL>(tws, tw);
   __syncthreads();
-  W x[NP][16];
   round_load<RL, W, NP, LOGN>(x, sm);
   gs_compute<A, LOGN, LL, NP>(x, tws, q, qb, ninv, wl);
   pdl_trigger();

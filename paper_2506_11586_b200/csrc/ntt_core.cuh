@@ -81,6 +81,59 @@ __device__ __forceinline__ void round_store(const W (&x)[NP][16], W* sm) {
   }
 }
 
+// Global-memory load / store of a round whose tasks are contiguous (logD == 0: the GS round at
+// level 0, the last CT round): task k's GK words are consecutive, moved as 16-byte (or narrower)
+// vectors. The warp-level access is not coalesced per instruction, but every thread moves whole
+// 32-byte sectors, so the sectors are used in full across the round's vector instructions.
+template <class W, int VW>
+struct Vec;
+template <> struct Vec<uint32_t, 4> { using T = uint4; };
+template <> struct Vec<uint32_t, 2> { using T = uint2; };
+template <> struct Vec<uint32_t, 1> { using T = uint32_t; };
+template <> struct Vec<uint64_t, 2> { using T = ulonglong2; };
+template <> struct Vec<uint64_t, 1> { using T = uint64_t; };
+
+template <class R, class W, int NP>
+__device__ __forceinline__ void round_gload(W (&x)[NP][16], const W* const (&src)[NP]) {
+  static_assert(R::logD == 0, "contiguous tasks only");
+  constexpr int VW = (int)(16 / sizeof(W)) < R::GK ? (int)(16 / sizeof(W)) : R::GK;
+  using V = typename Vec<W, VW>::T;
+#pragma unroll
+  for (int k = 0; k < R::NT; ++k) {
+    const uint32_t b = R::addr(k, 0);
+#pragma unroll
+    for (int pp = 0; pp < NP; ++pp)
+#pragma unroll
+      for (int v = 0; v < R::GK / VW; ++v) {
+        const V t = *reinterpret_cast<const V*>(src[pp] + b + v * VW);
+        const W* tw = reinterpret_cast<const W*>(&t);
+#pragma unroll
+        for (int u = 0; u < VW; ++u) x[pp][k * R::GK + v * VW + u] = tw[u];
+      }
+  }
+}
+
+template <class R, class W, int NP>
+__device__ __forceinline__ void round_gstore(const W (&x)[NP][16], W* const (&dst)[NP]) {
+  static_assert(R::logD == 0, "contiguous tasks only");
+  constexpr int VW = (int)(16 / sizeof(W)) < R::GK ? (int)(16 / sizeof(W)) : R::GK;
+  using V = typename Vec<W, VW>::T;
+#pragma unroll
+  for (int k = 0; k < R::NT; ++k) {
+    const uint32_t b = R::addr(k, 0);
+#pragma unroll
+    for (int pp = 0; pp < NP; ++pp)
+#pragma unroll
+      for (int v = 0; v < R::GK / VW; ++v) {
+        V t;
+        W* tw = reinterpret_cast<W*>(&t);
+#pragma unroll
+        for (int u = 0; u < VW; ++u) tw[u] = x[pp][k * R::GK + v * VW + u];
+        *reinterpret_cast<V*>(dst[pp] + b + v * VW) = t;
+      }
+  }
+}
+
 // ------------------------------------------------------------------------------------------
 // Cooley-Tukey: stages S0 .. S0+K-1 (stage s: 2^s groups, group i uses psi^brv(2^s + i)).
 // Twiddles of one round are gathered into registers before the round's barrier so their load
@@ -126,13 +179,24 @@ __device__ __forceinline__ void ct_compute(typename A::W (&x)[NP][16], const typ
   }
 }
 
-// Rounds S0.. to the end, each: gather twiddles, barrier (the previous round's stores), smem ->
-// regs -> smem. A final barrier follows the last round.
+// S0 of the last CT round
+template <int LOGN, int S0 = 0>
+struct CtLast {
+  static constexpr int value =
+      (S0 + CtRound<LOGN, S0>::K >= LOGN) ? S0 : CtLast<LOGN, S0 + CtRound<LOGN, S0>::K>::value;
+};
+template <int LOGN>
+struct CtLast<LOGN, LOGN> {
+  static constexpr int value = LOGN;
+};
+
+// Rounds S0.. up to (not including) the last one, each: gather twiddles, barrier (the previous
+// round's stores), smem -> regs -> smem. The caller runs the last round.
 template <class A, int LOGN, int S0, int NP>
-__device__ __forceinline__ void ct_rounds_smem(typename A::W* sm, const typename A::Tw* __restrict__ tw,
-                                               typename A::W q, typename A::W qb) {
-  if constexpr (S0 < LOGN) {
-    using R = CtRound<LOGN, S0>;
+__device__ __forceinline__ void ct_rounds_smem_but_last(typename A::W* sm, const typename A::Tw* __restrict__ tw,
+                                                        typename A::W q, typename A::W qb) {
+  using R = CtRound<LOGN, S0>;
+  if constexpr (S0 + R::K < LOGN) {
     typename A::Tw tws[15];
     ct_twiddles<A, LOGN, S0>(tws, tw);
     __syncthreads();
@@ -140,9 +204,7 @@ __device__ __forceinline__ void ct_rounds_smem(typename A::W* sm, const typename
     round_load<R, typename A::W, NP, LOGN>(x, sm);
     ct_compute<A, LOGN, S0, NP>(x, tws, q, qb);
     round_store<R, typename A::W, NP, LOGN>(x, sm);
-    ct_rounds_smem<A, LOGN, S0 + R::K, NP>(sm, tw, q, qb);
-  } else {
-    __syncthreads();
+    ct_rounds_smem_but_last<A, LOGN, S0 + R::K, NP>(sm, tw, q, qb);
   }
 }
 
