@@ -625,12 +625,24 @@ static cudaError_t mac_t(const DevConsts& c, const PlanDev& p, const void* xhat,
     attr = smem;
   }
   const int n_sg = (p.S + SG - 1) / SG;
-  // m-range per CTA: about 4 waves of 2 CTAs per SM, a multiple of MT, at least 2 m-blocks
+  // m-range per CTA: the split of M into n_mr ranges (each >= MT channels, a multiple of MT)
+  // whose CTA count fills whole waves of two CTAs per SM best; ties go to fewer, longer CTAs
+  // (each CTA pays one X^ tile load and one pipeline fill).
   const long ctas_no_m = (long)(N / MAC_THREADS) * n_sg * c.L;
-  long mr = ((long)p.M * ctas_no_m + 148 * 8 - 1) / (148 * 8);
-  mr = (mr + MT - 1) / MT * MT;
-  if (mr < 2 * MT) mr = 2 * MT;
-  const int m_range = (int)(mr < (long)p.M ? mr : (long)p.M);
+  const long wave = 148 * 2;
+  const int mblocks = (p.M + MT - 1) / MT;
+  int best_nmr = 1;
+  double best_eff = -1.0;
+  for (int nmr = 1; nmr <= mblocks; ++nmr) {
+    const int per = (mblocks + nmr - 1) / nmr;  // m-blocks per CTA
+    const int used = (mblocks + per - 1) / per;
+    if (used != nmr) continue;
+    const long ctas = (long)nmr * ctas_no_m;
+    const long waves = (ctas + wave - 1) / wave;
+    const double eff = (double)ctas / (double)(waves * wave) - 0.02 * (double)waves;
+    if (eff > best_eff + 1e-9) best_eff = eff, best_nmr = nmr;
+  }
+  const int m_range = ((mblocks + best_nmr - 1) / best_nmr) * MT;
   const int n_mr = (p.M + m_range - 1) / m_range;
   // tensor maps: X^ [G][S*2][L][N] viewed as (N, L, 2S, G); W [M][G][L][N] as (N, G*L, M)
   const cuuint64_t wb = sizeof(W);
