@@ -371,14 +371,16 @@ def run_e2e(ctx, st, K, dev, share_buf, world):
     for d in st:
         if d["mc"] <= 0:
             continue
-        h = {k: torch.from_numpy(np.ascontiguousarray(v).view(np.int64)).pin_memory()
-             for k, v in (("ct", d["ct_h"]), ("x0", d["x0_h"]))}
+        ct = np.ascontiguousarray(d["ct_h"])
+        ct = ct.view(np.int64) if d["ct"].dtype == torch.int64 else ct.astype(np.uint32).view(np.int32)
+        h = {"ct": torch.from_numpy(ct).pin_memory(),
+             "x0": torch.from_numpy(np.ascontiguousarray(d["x0_h"]).view(np.int64)).pin_memory()}
         S = d["plan"].S
         h["r"] = torch.from_numpy(np.ascontiguousarray(d["r_h"][d["m0"] * S:(d["m0"] + d["mc"]) * S]).view(np.int64)).pin_memory()
-        h["out"] = torch.empty(d["out"].shape, dtype=torch.int64).pin_memory()
+        h["out"] = torch.empty(d["out"].shape, dtype=d["out"].dtype).pin_memory()
         h["y0"] = torch.empty(d["y0"].shape, dtype=torch.int64).pin_memory()
-        h2d += sum(h[k].numel() * 8 for k in ("ct", "x0", "r"))
-        d2h += (h["out"].numel() + h["y0"].numel()) * 8
+        h2d += sum(h[k].numel() * h[k].element_size() for k in ("ct", "x0", "r"))
+        d2h += h["out"].numel() * h["out"].element_size() + h["y0"].numel() * 8
         host.append((d, h))
 
     def step():
