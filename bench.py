@@ -280,7 +280,8 @@ def main():
     n_ntt = sum((d["plan"].G * d["plan"].S * world + d["plan"].M * d["plan"].S) * 2 * L for d in st)  # limb NTTs per step
     launches_per_step = sum(4 for d in st if d["mc"] > 0)
     sb = {s: sum(stage_bytes(d["pl"], L, n, wbytes)[s] for d in st if d["mc"] > 0) for s in range(3)}
-    names = {0: "k_ntt_fwd (A6 share add + A1 NTT)", 1: "k_mac (A4 NTT-domain MAC)", 2: "k_ntt_inv (A2 INTT + A7 mask)"}
+    names = {0: "k_ntt_fwd (A6 share add + A1 NTT)", 1: "k_mac (A4 NTT-domain MAC + INTT levels 0-7)",
+             2: "k_ntt_inv_tail (A2 INTT levels 8-11 + A7 mask)"}
     dom = max(range(3), key=lambda s: stage_ms[s])
     n_layers_active = sum(1 for d in st if d["mc"] > 0)
     achieved = sb[dom] / (stage_ms[dom] / 1e3) / 1e9

@@ -452,9 +452,10 @@ static int he_conv2d_impl(secn_ctx* ctx, uint32_t bits, const secn_conv_plan_t* 
   const secn::PlanDev pd = plan_dev(plan);
   cudaError_t e = cudaSuccess;
   if (stage == -1 || stage == 0) e = secn::launch_ntt_fwd(ctx->dc, ct_in, workspace, n_in * 2 * ctx->L, x0, s);  // A6+A1
-  if (e == cudaSuccess && (stage == -1 || stage == 1)) e = secn::launch_mac(ctx->dc, pd, workspace, w_ntt, ct_out, s);  // A4
+  // A4 + A2 levels 0..7
+  if (e == cudaSuccess && (stage == -1 || stage == 1)) e = secn::launch_mac(ctx->dc, pd, workspace, w_ntt, ct_out, s);
   if (e == cudaSuccess && (stage == -1 || stage == 2))
-    e = secn::launch_ntt_inv(ctx->dc, ct_out, n_out * 2 * ctx->L, r, s);  // A2+A7
+    e = secn::launch_ntt_inv_tail(ctx->dc, ct_out, n_out * 2 * ctx->L, r, s);  // A2 (levels 8..) + A7
   return e == cudaSuccess ? SECN_OK : cuda_fail(e, "secn_he_conv2d");
 }
 

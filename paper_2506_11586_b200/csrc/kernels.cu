@@ -209,6 +209,70 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN, NP>(
   }
 }
 
+// K3' (+A7 fused), the second half of secn_he_conv2d's inverse NTT: levels 8 .. LOGN-1 (with
+// N^-1) on limb-polys whose levels 0..7 were applied by the MAC kernel (inputs in the lazy GS
+// domain), then the mask on the b component. At N = 4096 this is one radix-16 round whose tasks
+// (coefficients o + 256 i) are coalesced in global memory, with the same 15 twiddles for every
+// thread: no shared memory, one load and one store per word.
+template <class A, int LOGN>
+__global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN, 1>())
+    k_ntt_inv_tail(typename A::W* polys, const __grid_constant__ DevConsts c, const uint64_t* __restrict__ r) {
+  using W = typename A::W;
+  constexpr int N = 1 << LOGN;
+  constexpr int LS = 8;
+  constexpr int LL = GsLast<LOGN>::value;
+  using RS = GsRound<LOGN, LS>;
+  using RL = GsRound<LOGN, LL>;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  W* sm = reinterpret_cast<W*>(smraw);
+  const int j = (int)(blockIdx.x % c.L);
+  const size_t pi = blockIdx.x / c.L;
+  const W q = (W)c.q[j], qb = A::bound(q);
+  const typename A::Tw* tw = Tab<A>::inv(c) + (size_t)j * N;
+  const typename A::Tw ninv = Tab<A>::pair(c.ninv[j], c.ninv_p[j]);
+  const typename A::Tw wl = Tab<A>::pair(c.wlast[j], c.wlast_p[j]);
+  const EncK ek(c, j);
+  const bool mask = r != nullptr && (pi & 1);
+  W em[16];
+  if (mask) {
+    const uint64_t* rs = r + (pi >> 1) * N;
+#pragma unroll
+    for (int k = 0; k < RL::NT; ++k)
+#pragma unroll
+      for (int i = 0; i < RL::GK; ++i) em[k * RL::GK + i] = enc_mod<A>(__ldg(&rs[RL::addr(k, i)]), ek);
+  }
+  typename A::Tw tws[15];
+  gs_twiddles<A, LOGN, LS>(tws, tw);
+  pdl_wait();  // the polys are produced by the preceding kernel (the MAC)
+  W* buf = polys + (pi * c.L + j) * N;
+  W x[1][16];
+#pragma unroll
+  for (int k = 0; k < RS::NT; ++k)
+#pragma unroll
+    for (int i = 0; i < RS::GK; ++i) x[0][k * RS::GK + i] = buf[RS::addr(k, i)];
+  gs_compute<A, LOGN, LS, 1>(x, tws, q, qb, ninv, wl);
+  if constexpr (LL != LS) {  // N > 4096: the remaining levels go through shared memory
+    round_store<RS, W, 1, LOGN>(x, sm);
+    gs_rounds_smem_but_last<A, LOGN, LS + RS::K, 1>(sm, tw, q, qb, ninv, wl);
+    gs_twiddles<A, LOGN, LL>(tws, tw);
+    __syncthreads();
+    round_load<RL, W, 1, LOGN>(x, sm);
+    gs_compute<A, LOGN, LL, 1>(x, tws, q, qb, ninv, wl);
+  }
+  pdl_trigger();
+#pragma unroll
+  for (int k = 0; k < RL::NT; ++k)
+#pragma unroll
+    for (int i = 0; i < RL::GK; ++i) {
+      W v = A::canon_gs(x[0][k * RL::GK + i], q);
+      if (mask) {
+        v += em[k * RL::GK + i];
+        v = v >= q ? v - q : v;
+      }
+      buf[RL::addr(k, i)] = v;
+    }
+}
+
 // ------------------------------------------------------------------------------------------
 // A4: NTT-domain multiply-accumulate ("performs all HE MAC operations in NTT"):
 //   Y^[m,s,c,j,e] = sum_g X^[g,s,c,j,e] * W[m,g,j,e] mod q_j
@@ -232,6 +296,76 @@ __device__ __forceinline__ uint32_t reduce64(uint64_t a, uint32_t q, uint32_t r3
   return csub32(csub32(x, 2 * q), q);
 }
 
+template <class W>
+struct ArithOf;
+template <>
+struct ArithOf<uint32_t> {
+  using A = Arith32;
+};
+template <>
+struct ArithOf<uint64_t> {
+  using A = Arith64;
+};
+
+// barrier among the MAC_THREADS consumer threads only (the producer warp never joins)
+__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(MAC_THREADS) : "memory"); }
+
+// Gentleman-Sande levels 0..7 of the inverse NTT on nch chunks of 256 coefficients (one e-tile of
+// each output poly) held in shared memory in the padded layout (chunk ch at ch * MAC_CHS, word e
+// at phys(e)). Levels 0..7 only pair coefficients inside an aligned block of 256, so the MAC CTA
+// that owns the e-tile can apply them before Y^ leaves the SM (the INTT kernel does the rest).
+// twe holds the e-tile's 255 twiddles: level l, local group g at twe[256 - (256 >> l) + g].
+constexpr int MAC_CHS = MAC_THREADS + MAC_THREADS / 16;
+
+template <class A>
+__device__ __forceinline__ void mac_intt_levels_0_7(typename A::W* cbuf, const typename A::Tw* twe, int nch,
+                                                    typename A::W q, typename A::W qb) {
+  using W = typename A::W;
+  const int ntask = nch * 16;
+  // round A: levels 0..3, task = 16 consecutive coefficients 16b .. 16b+15 (phys: 17b + i)
+  for (int tau = threadIdx.x; tau < ntask; tau += MAC_THREADS) {
+    W* base = cbuf + (tau >> 4) * MAC_CHS + 17 * (tau & 15);
+    const int b = tau & 15;
+    W x[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) x[i] = base[i];
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const int d = 1 << p;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        if (i & d) continue;
+        const typename A::Tw w = twe[256 - (256 >> p) + b * (8 >> p) + (i >> (p + 1))];
+        A::gs(x[i], x[i + d], w, q, qb);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) base[i] = x[i];
+  }
+  consumer_sync();
+  // round B: levels 4..7, task = coefficients 16i + o (phys: 17i + o); the twiddles do not
+  // depend on the task
+  for (int tau = threadIdx.x; tau < ntask; tau += MAC_THREADS) {
+    W* base = cbuf + (tau >> 4) * MAC_CHS + (tau & 15);
+    W x[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) x[i] = base[17 * i];
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const int d = 1 << p;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        if (i & d) continue;
+        const typename A::Tw w = twe[256 - (256 >> (4 + p)) + (i >> (p + 1))];
+        A::gs(x[i], x[i + d], w, q, qb);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) base[17 * i] = x[i];
+  }
+  consumer_sync();
+}
+
 // Register blocking: each consumer thread accumulates an [MT][2*SG] block of outputs (MT output
 // channels x SG spatial blocks x 2 components) for its coefficient; the g loop is the runtime
 // reduction loop. Per (m-block, g) the producer lands MT weight rows (MT x 256 words) in one ring
@@ -251,10 +385,15 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
   const int ns = min(SG, S - s0);
   const int m_begin = blockIdx.z * m_range, m_end = min((int)pl.M, m_begin + m_range);
   const uint32_t row_bytes = MAC_THREADS * sizeof(W);
-  // shared memory: [G][2SG][256] X^ tile, [NS][MT][256] weight ring, 2*NS + 1 mbarriers
+  using AR = typename ArithOf<W>::A;
+  using Tw = typename AR::Tw;
+  // shared memory: [G][2SG][256] X^ tile, [NS][MT][256] weight ring, [MT*2SG][MAC_CHS] output
+  // chunks, [256] e-tile twiddles, 2*NS + 1 mbarriers
   W* xs = reinterpret_cast<W*>(smraw);
   W* ring = xs + (size_t)G * A2 * MAC_THREADS;
-  uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)NS * MT * MAC_THREADS);
+  W* cbuf = ring + (size_t)NS * MT * MAC_THREADS;
+  Tw* twe = reinterpret_cast<Tw*>(cbuf + (size_t)MT * A2 * MAC_CHS);
+  uint64_t* full = reinterpret_cast<uint64_t*>(twe + MAC_THREADS);
   uint64_t* empty = full + NS;
   uint64_t* xbar = empty + NS;
   const int tid = threadIdx.x;
@@ -310,6 +449,15 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
   // ---- consumers: one coefficient each (X^ rows beyond 2*ns are zero-filled; never stored) ----
   const uint32_t e = e0 + tid;
   const uint64_t q = c.q[j], onep = c.one_p[j];
+  {  // the e-tile's inverse-NTT twiddles for levels 0..7 (constant tables: read before any wait)
+    const Tw* tinv = Tab<AR>::inv(c) + (size_t)j * N;
+    if (tid < 255) {
+      int l = 0;
+      while (tid >= 256 - (256 >> (l + 1))) ++l;
+      const int g = tid - (256 - (256 >> l));
+      twe[tid] = tinv[(N >> (l + 1)) + (e0 >> (l + 1)) + g];
+    }
+  }
   const uint32_t r32 = (uint32_t)c.r32[j], r32p = (uint32_t)c.r32_p[j], onep32 = (uint32_t)(onep >> 32);
   mbar_wait(xbar, 0);
   int st = 0;
@@ -338,13 +486,12 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
         if ((tid & 31) == 0) mbar_arrive(&empty[st]);
         if (++st == NS) st = 0, ph ^= 1;
       }
+      consumer_sync();  // the previous m-block's chunks have been written out
 #pragma unroll
       for (int r = 0; r < MT; ++r)
 #pragma unroll
         for (int a = 0; a < A2; ++a)
-          if (r < rows && a < 2 * ns)
-            y[((((size_t)(mb + r) * S + s0 + (a >> 1)) * 2 + (a & 1)) * L + j) * N + e] =
-                (W)reduce64(acc[r][a], (uint32_t)q, r32, r32p, onep32);
+          cbuf[(r * A2 + a) * MAC_CHS + phys(tid)] = (W)reduce64(acc[r][a], (uint32_t)q, r32, r32p, onep32);
     } else {
       const uint64_t r64 = c.r64[j], r64p = c.r64_p[j];
       uint64_t lo[MT][A2], hi[MT][A2];
@@ -368,14 +515,24 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
         if ((tid & 31) == 0) mbar_arrive(&empty[st]);
         if (++st == NS) st = 0, ph ^= 1;
       }
+      consumer_sync();  // the previous m-block's chunks have been written out
 #pragma unroll
       for (int r = 0; r < MT; ++r)
 #pragma unroll
         for (int a = 0; a < A2; ++a)
-          if (r < rows && a < 2 * ns)
-            y[((((size_t)(mb + r) * S + s0 + (a >> 1)) * 2 + (a & 1)) * L + j) * N + e] =
-                (W)reduce128(lo[r][a], hi[r][a], q, r64, r64p, onep);
+          cbuf[(r * A2 + a) * MAC_CHS + phys(tid)] = (W)reduce128(lo[r][a], hi[r][a], q, r64, r64p, onep);
     }
+    // inverse-NTT levels 0..7 of every staged output chunk, then the chunks leave the SM (lazy
+    // GS domain values, finished by the INTT kernel)
+    consumer_sync();
+    mac_intt_levels_0_7<AR>(cbuf, twe, MT * A2, (W)q, AR::bound((W)q));
+#pragma unroll
+    for (int r = 0; r < MT; ++r)
+#pragma unroll
+      for (int a = 0; a < A2; ++a)
+        if (r < rows && a < 2 * ns)
+          y[((((size_t)(mb + r) * S + s0 + (a >> 1)) * 2 + (a & 1)) * L + j) * N + e] =
+              cbuf[(r * A2 + a) * MAC_CHS + phys(tid)];
   }
   pdl_trigger();
 }
@@ -544,6 +701,46 @@ static cudaError_t ntt_inv_t(const DevConsts& c, void* polys, size_t P, const ui
   return ntt_inv_np<A, LOGN, 1>(c, polys, n_polys, r, s);
 }
 
+template <class A, int LOGN>
+static cudaError_t ntt_inv_tail_t(const DevConsts& c, void* polys, size_t P, const uint64_t* r, cudaStream_t s) {
+  using W = typename A::W;
+  constexpr int N = 1 << LOGN;
+  const size_t smem = LOGN > 12 ? smem_words<LOGN>() * sizeof(W) : 0;
+  static bool attr = false;
+  if (!attr && smem > 48 * 1024) {
+    cudaFuncSetAttribute(k_ntt_inv_tail<A, LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  const size_t pmax = (0x7fffffffull / c.L / 2) * 2;  // polys per launch: even, so r's index is p/2
+  const size_t n_polys = P / c.L;
+  for (size_t p0 = 0; p0 < n_polys; p0 += pmax) {
+    const size_t np = n_polys - p0 < pmax ? n_polys - p0 : pmax;
+    W* buf = static_cast<W*>(polys) + p0 * c.L * N;
+    const uint64_t* rs = r ? r + p0 / 2 * N : nullptr;
+    cudaError_t e = launch_pdl(k_ntt_inv_tail<A, LOGN>, dim3((unsigned)(np * c.L)), dim3(N / 16), smem, s, buf, c, rs);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ntt_inv_tail(const DevConsts& c, void* polys, size_t P, const uint64_t* r, cudaStream_t s) {
+  if (P == 0) return cudaSuccess;
+  if (c.word_bits == 64) {
+    switch (c.log_n) {
+      case 12: return ntt_inv_tail_t<Arith64, 12>(c, polys, P, r, s);
+      case 13: return ntt_inv_tail_t<Arith64, 13>(c, polys, P, r, s);
+      case 14: return ntt_inv_tail_t<Arith64, 14>(c, polys, P, r, s);
+    }
+  } else {
+    switch (c.log_n) {
+      case 12: return ntt_inv_tail_t<Arith32, 12>(c, polys, P, r, s);
+      case 13: return ntt_inv_tail_t<Arith32, 13>(c, polys, P, r, s);
+      case 14: return ntt_inv_tail_t<Arith32, 14>(c, polys, P, r, s);
+    }
+  }
+  return cudaErrorInvalidValue;
+}
+
 cudaError_t launch_ntt_fwd(const DevConsts& c, const void* in, void* out, size_t P, const uint64_t* x0,
                            cudaStream_t s) {
   if (P == 0) return cudaSuccess;
@@ -612,10 +809,12 @@ static cudaError_t mac_t(const DevConsts& c, const PlanDev& p, const void* xhat,
   const size_t xtile = (size_t)p.G * 2 * SG * MAC_THREADS * sizeof(W);
   const size_t stage = (size_t)MT * MAC_THREADS * sizeof(W);
   // ring depth: fill ~110 KiB per CTA (two CTAs per SM) after the X^ tile, 4..32 stages
-  const size_t budget = 110 * 1024 > xtile + 4 * stage ? 110 * 1024 - xtile : 4 * stage;
+  const size_t chunks = (size_t)MT * 2 * SG * MAC_CHS * sizeof(W) + MAC_THREADS * 2 * sizeof(W);
+  const size_t fixed = xtile + chunks;
+  const size_t budget = 110 * 1024 > fixed + 4 * stage ? 110 * 1024 - fixed : 4 * stage;
   int NS = (int)(budget / stage);
   NS = NS < 4 ? 4 : NS > 32 ? 32 : NS;
-  const size_t smem = xtile + NS * stage + (2 * NS + 1) * sizeof(uint64_t);
+  const size_t smem = fixed + NS * stage + (2 * NS + 1) * sizeof(uint64_t);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   static size_t attr = 0;
   if (smem > attr) {
