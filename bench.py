@@ -45,8 +45,11 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["secn", "reference"], default="secn")
     ap.add_argument("--net", default="squeezenet1_1")
-    ap.add_argument("--word-bits", type=int, choices=[32, 64], default=64,
-                    help="64: paper parameters (q 60+49 bit, uint64 limbs); 32: four 27-bit uint32 limbs")
+    ap.add_argument("--word-bits", type=int, choices=[32, 64], default=32,
+                    help="32: four 27-bit uint32 RNS limbs (reading R1b, headline); 64: q 60+49 bit uint64 limbs "
+                         "(reading R1)")
+    ap.add_argument("--no-companion", action="store_true",
+                    help="skip the timing-only run of the other word size reported under 'companion'")
     ap.add_argument("--seed", type=int, default=3)
     ap.add_argument("--cpu-frac", type=float, default=0.05, help="oracle sample fraction for cpu_baseline")
     ap.add_argument("--ref-frac", type=float, default=0.01, help="oracle sample fraction per --impl reference step")
@@ -157,16 +160,33 @@ def main():
         return run_reference(args, world, rank)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-
     import __graft_entry__
-    from paper_2506_11586_b200 import Context
-    from paper_2506_11586_b200 import dist as sdist
 
     if rank == 0:
         __graft_entry__.build()
     if world > 1:
         dist.barrier()
-    ctx = Context(local, word_bits=args.word_bits)
+    out = run_secn(args, args.word_bits, world, rank, local, dev, full=True)
+    if not args.no_companion:
+        other = 64 if args.word_bits == 32 else 32
+        torch.cuda.empty_cache()
+        comp = run_secn(args, other, world, rank, local, dev, full=False)
+        if rank == 0:
+            out["companion"] = comp
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_secn(args, word_bits, world, rank, local, dev, full):
+    """Builds the workload at one residue word size, times K graph replays of the step and (full)
+    the per-stage, e2e and cpu_baseline legs. Returns the JSON dict on rank 0 (None elsewhere)."""
+    from paper_2506_11586_b200 import Context
+    from paper_2506_11586_b200 import dist as sdist
+
+    ctx = Context(local, word_bits=word_bits)
     L, n, t_bits = ctx.L, ctx.n, ctx.t_bits
     wbytes = ctx.word_bits // 8
 
@@ -192,6 +212,8 @@ def main():
             d["r"] = torch.from_numpy(np.ascontiguousarray(r[m0 * S:(m0 + mc) * S]).view(np.int64)).to(dev)
             d["out"] = ctx.empty(mc * S, 2, L, n)
             d["ws"] = torch.empty(ctx.workspace_bytes(pl) // 8, dtype=torch.int64, device=dev)
+        else:
+            d["pl"] = None
         st.append(d)
     dims = [(d["plan"].M, d["plan"].OH, d["plan"].OW) for d in st]
     layout = sdist.share_layout(dims, world)
@@ -258,25 +280,31 @@ def main():
         dist.all_reduce(total_ms, op=dist.ReduceOp.MAX)
     ms_per_step = float(total_ms.item()) / K
 
+    if world > 1 and rank == 0:
+        shares = sdist.reassemble(gathered, layout, dims, world)
+        assert all(f.shape[0] == M for f, (M, _, _) in zip(shares, dims))
+    hbm_peak, peak_kind = peaks()
+    alg_bytes = sum(algorithmic_bytes(d["plan"], L, n, wbytes) for d in st)
+    step_s = ms_per_step / 1e3
+    if not full:
+        del graph
+        if rank != 0:
+            return None
+        return {"dtype": f"u{ctx.word_bits}", "primes": [hex(q) for q in ctx.primes], "limbs": L,
+                "value": round(step_s, 7), "unit": "s", "ms_per_step": round(ms_per_step, 4),
+                "alg_bytes_per_step": alg_bytes, "hbm_frac": round(alg_bytes / step_s / 1e9 / hbm_peak, 4),
+                "clocks": clk.summary(), "timing": "CUDA events around CUDA-graph replays of the whole step"}
+
     # ---- per-stage live timing (eager stage calls, launches pre-queued behind a sleep) ----
     stage_ms = stage_profile(ctx, st, K, dev)
 
     # ---- e2e: host buffers, H2D + public API + D2H every step ----
     e2e = None if args.no_e2e else run_e2e(ctx, st, K, dev, share_buf, world)
 
-    if world > 1 and rank == 0:
-        full = sdist.reassemble(gathered, layout, dims, world)
-        assert all(f.shape[0] == M for f, (M, _, _) in zip(full, dims))
-
     if rank != 0:
-        if world > 1:
-            dist.barrier()
-            dist.destroy_process_group()
-        return
+        return None
 
     # ---- derived numbers ----
-    hbm_peak, peak_kind = peaks()
-    alg_bytes = sum(algorithmic_bytes(d["plan"], L, n, wbytes) for d in st)
     n_ntt = sum((d["plan"].G * d["plan"].S * world + d["plan"].M * d["plan"].S) * 2 * L for d in st)  # limb NTTs per step
     launches_per_step = sum(4 for d in st if d["mc"] > 0)
     sb = {s: sum(stage_bytes(d["pl"], L, n, wbytes)[s] for d in st if d["mc"] > 0) for s in range(3)}
@@ -292,7 +320,6 @@ def main():
                 "avg_launch_us": round(stage_ms[dom] / n_layers_active * 1e3, 2),
                 "stage_ms": {names[s]: round(stage_ms[s], 4) for s in range(3)},
                 "stage_GBps": {names[s]: round(sb[s] / (stage_ms[s] / 1e3) / 1e9, 1) for s in range(3)}}
-    step_s = ms_per_step / 1e3
     out = {
         "metric": METRIC, "value": round(step_s, 7), "unit": "s", "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": False,
@@ -315,10 +342,7 @@ def main():
     }
     if not args.no_cpu_baseline and world == 1:
         out["cpu_baseline"] = cpu_baseline(st, ctx, args.cpu_frac, dev, wbytes)
-    print(json.dumps(out), flush=True)
-    if world > 1:
-        dist.barrier()
-        dist.destroy_process_group()
+    return out
 
 
 def stage_profile(ctx, st, K, dev):
