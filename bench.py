@@ -41,7 +41,7 @@ HBM_PEAK_FALLBACK = 6650.0
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["secn", "reference"], default="secn")
     ap.add_argument("--net", default="squeezenet1_1")
@@ -70,53 +70,59 @@ def peaks():
 # clocks during the timed region (NVML)
 
 class ClockSampler:
+    """Samples SM clocks and clock-event reasons with `nvidia-smi -lms` in a separate process for
+    the duration of the timed region (the B200_PROFILING.md clocks line)."""
     REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
                0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
                0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
 
-    def __init__(self, index: int, period: float = 0.005):
+    def __init__(self, index: int, period_ms: int = 20):
+        self.index, self.period_ms = index, period_ms
         self.samples, self.reasons, self.max_mhz = [], set(), None
-        self._stop = threading.Event()
-        self.period = period
-        try:
-            import pynvml
-
-            pynvml.nvmlInit()
-            self._nv = pynvml
-            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
-        except Exception:
-            self._nv = None
-
-    def _run(self):
-        nv = self._nv
-        while not self._stop.is_set():
-            try:
-                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
-                bits = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
-                for b, name in self.REASONS.items():
-                    if bits & b and name != "gpu_idle":
-                        self.reasons.add(name)
-            except Exception:
-                pass
-            time.sleep(self.period)
+        self._p = None
 
     def __enter__(self):
-        if self._nv:
-            self._t = threading.Thread(target=self._run, daemon=True)
-            self._t.start()
+        import subprocess
+
+        try:
+            self._p = subprocess.Popen(
+                ["nvidia-smi", "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active", "--format=csv,noheader,nounits",
+                 "-i", str(self.index), "-lms", str(self.period_ms)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+            time.sleep(0.3)  # let the sampler start before the timed region
+        except Exception:
+            self._p = None
         return self
 
     def __exit__(self, *a):
-        if self._nv:
-            self._stop.set()
-            self._t.join()
+        if self._p is None:
+            return
+        time.sleep(0.05)
+        self._p.terminate()
+        try:
+            out, _ = self._p.communicate(timeout=5)
+        except Exception:
+            return
+        for line in out.splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 3:
+                continue
+            try:
+                sm, mx, bits = float(f[0]), float(f[1]), int(f[2], 16)
+            except ValueError:
+                continue
+            self.max_mhz = mx
+            if bits & ~0x1:  # ignore samples where only gpu_idle is set (between launches)
+                for b, name in self.REASONS.items():
+                    if bits & b and name != "gpu_idle":
+                        self.reasons.add(name)
+            self.samples.append(sm)
 
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
         return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+                "reasons": sorted(self.reasons), "samples": len(self.samples), "sampler": "nvidia-smi -lms 20"}
 
 
 # ------------------------------------------------------------------------------------------
