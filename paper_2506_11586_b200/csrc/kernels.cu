@@ -307,23 +307,23 @@ struct ArithOf<uint64_t> {
   using A = Arith64;
 };
 
+// barrier among the MAC_THREADS consumer threads only (the producer warp never joins)
+__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(MAC_THREADS) : "memory"); }
+
 // Gentleman-Sande levels 0..7 of the inverse NTT on nch chunks of 256 coefficients (one e-tile of
 // each output poly) held in shared memory in the padded layout (chunk ch at ch * MAC_CHS, word e
 // at phys(e)). Levels 0..7 only pair coefficients inside an aligned block of 256, so the MAC CTA
-// that owns the e-tile applies them before Y^ leaves the SM (the INTT kernel does the rest).
+// that owns the e-tile can apply them before Y^ leaves the SM (the INTT kernel does the rest).
 // twe holds the e-tile's 255 twiddles: level l, local group g at twe[256 - (256 >> l) + g].
-// Executed by the CTA's INTT warp group (MAC_THREADS threads, thread index it, named barrier 2).
 constexpr int MAC_CHS = MAC_THREADS + MAC_THREADS / 16;
 
-__device__ __forceinline__ void intt_group_sync() { asm volatile("bar.sync 2, %0;" ::"n"(MAC_THREADS) : "memory"); }
-
 template <class A>
-__device__ __forceinline__ void mac_intt_levels_0_7(typename A::W* cbuf, const typename A::Tw* twe, int nch, int it,
+__device__ __forceinline__ void mac_intt_levels_0_7(typename A::W* cbuf, const typename A::Tw* twe, int nch,
                                                     typename A::W q, typename A::W qb) {
   using W = typename A::W;
   const int ntask = nch * 16;
   // round A: levels 0..3, task = 16 consecutive coefficients 16b .. 16b+15 (phys: 17b + i)
-  for (int tau = it; tau < ntask; tau += MAC_THREADS) {
+  for (int tau = threadIdx.x; tau < ntask; tau += MAC_THREADS) {
     W* base = cbuf + (tau >> 4) * MAC_CHS + 17 * (tau & 15);
     const int b = tau & 15;
     W x[16];
@@ -342,9 +342,10 @@ __device__ __forceinline__ void mac_intt_levels_0_7(typename A::W* cbuf, const t
 #pragma unroll
     for (int i = 0; i < 16; ++i) base[i] = x[i];
   }
-  intt_group_sync();
-  // round B: levels 4..7, task = coefficients 16i + o (phys: 17i + o); task-independent twiddles
-  for (int tau = it; tau < ntask; tau += MAC_THREADS) {
+  consumer_sync();
+  // round B: levels 4..7, task = coefficients 16i + o (phys: 17i + o); the twiddles do not
+  // depend on the task
+  for (int tau = threadIdx.x; tau < ntask; tau += MAC_THREADS) {
     W* base = cbuf + (tau >> 4) * MAC_CHS + (tau & 15);
     W x[16];
 #pragma unroll
@@ -362,28 +363,20 @@ __device__ __forceinline__ void mac_intt_levels_0_7(typename A::W* cbuf, const t
 #pragma unroll
     for (int i = 0; i < 16; ++i) base[17 * i] = x[i];
   }
-  intt_group_sync();
+  consumer_sync();
 }
 
-// Warp-specialised CTA (1 producer warp, MAC_THREADS/32 MAC warps, MAC_THREADS/32 INTT warps,
-// one CTA per SM):
-//  * producer (one elected lane): the first lap of the weight ring before the dependency wait,
-//    then the X^ tile (4-D TMA) and the rest of the weights (3-D TMA boxes of MT rows);
-//  * MAC warps: one coefficient each; an [MT][2*SG] register block of lazy sums over the runtime
-//    g loop per m-block, reduced and staged into chunk buffer (k & 1);
-//  * INTT warps: inverse-NTT levels 0..7 of the staged chunks of m-block k while the MAC warps
-//    accumulate m-block k+1, then the chunks leave the SM (coalesced, lazy GS domain).
-// Hand-offs: full/empty mbarriers for the weight ring (TMA transactions), cfull/cempty mbarriers
-// (MAC_THREADS arrivals each) for the two chunk buffers.
+// Register blocking: each consumer thread accumulates an [MT][2*SG] block of outputs (MT output
+// channels x SG spatial blocks x 2 components) for its coefficient; the g loop is the runtime
+// reduction loop. Per (m-block, g) the producer lands MT weight rows (MT x 256 words) in one ring
+// stage; the consumer reads its 2*SG X^ values for g from the shared-memory X^ tile and does
+// MT * 2 * SG multiply-accumulates.
 template <class W, int SG, int MT>
-__global__ void __launch_bounds__(2 * MAC_THREADS + 32, 1)
+__global__ void __launch_bounds__(MAC_THREADS + 32, 2)
     k_mac(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmw, W* __restrict__ y,
           const __grid_constant__ DevConsts c, PlanDev pl, int m_range, int n_sg, int NS) {
   extern __shared__ __align__(128) unsigned char smraw[];
-  using AR = typename ArithOf<W>::A;
-  using Tw = typename AR::Tw;
   constexpr int A2 = 2 * SG;
-  constexpr int NCH = MT * A2;
   const int N = 1 << c.log_n, L = c.L, G = pl.G, S = pl.S;
   const int j = blockIdx.y;
   const int sgi = blockIdx.x % n_sg, et = blockIdx.x / n_sg;
@@ -392,17 +385,17 @@ __global__ void __launch_bounds__(2 * MAC_THREADS + 32, 1)
   const int ns = min(SG, S - s0);
   const int m_begin = blockIdx.z * m_range, m_end = min((int)pl.M, m_begin + m_range);
   const uint32_t row_bytes = MAC_THREADS * sizeof(W);
-  // shared memory: [G][2SG][256] X^ tile, [NS][MT][256] weight ring, 2 x [MT*2SG][MAC_CHS] chunk
-  // buffers, [256] e-tile twiddles, mbarriers
+  using AR = typename ArithOf<W>::A;
+  using Tw = typename AR::Tw;
+  // shared memory: [G][2SG][256] X^ tile, [NS][MT][256] weight ring, [MT*2SG][MAC_CHS] output
+  // chunks, [256] e-tile twiddles, 2*NS + 1 mbarriers
   W* xs = reinterpret_cast<W*>(smraw);
   W* ring = xs + (size_t)G * A2 * MAC_THREADS;
-  W* cbuf0 = ring + (size_t)NS * MT * MAC_THREADS;
-  Tw* twe = reinterpret_cast<Tw*>(cbuf0 + 2 * (size_t)NCH * MAC_CHS);
+  W* cbuf = ring + (size_t)NS * MT * MAC_THREADS;
+  Tw* twe = reinterpret_cast<Tw*>(cbuf + (size_t)MT * A2 * MAC_CHS);
   uint64_t* full = reinterpret_cast<uint64_t*>(twe + MAC_THREADS);
   uint64_t* empty = full + NS;
   uint64_t* xbar = empty + NS;
-  uint64_t* cfull = xbar + 1;   // [2]
-  uint64_t* cempty = cfull + 2;  // [2]
   const int tid = threadIdx.x;
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) {
@@ -410,23 +403,19 @@ __global__ void __launch_bounds__(2 * MAC_THREADS + 32, 1)
       mbar_init(&empty[s], MAC_THREADS / 32);
     }
     mbar_init(xbar, 1);
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&cfull[b], MAC_THREADS);
-      mbar_init(&cempty[b], MAC_THREADS);
-    }
     fence_mbar_init();
   }
   __syncthreads();
 
-  if (tid >= 2 * MAC_THREADS) {  // ---- producer warp ----
-    if (tid == 2 * MAC_THREADS) {
+  if (tid >= MAC_THREADS) {  // ---- producer warp: one elected lane streams X^ once, then the weights ----
+    if (tid == MAC_THREADS) {
       prefetch_tmap(&tmx);
       prefetch_tmap(&tmw);
       const uint64_t evict_first = policy_evict_first();  // weights are read once per query
       // The weights are inputs of the call (never produced by the preceding kernel): the first
       // lap of the ring is filled before the dependency wait, overlapping the forward NTT.
-      int st = 0;
-      uint32_t ph = 0, first = 1;
+      int st = 0, issued = 0;
+      uint32_t ph = 0, first = 1;  // ring position, its phase, and "first lap" (no wait needed)
       bool waited = false;
       for (int mb = m_begin; mb < m_end; mb += MT) {
         for (int g = 0; g < G; ++g) {
@@ -434,13 +423,17 @@ __global__ void __launch_bounds__(2 * MAC_THREADS + 32, 1)
             if (!waited) {
               pdl_wait();
               waited = true;
+              // X^ tile (written by the forward NTT): box (256 coefficients, limb j, 2*SG rows
+              // (s, c), G groups) in [g][a][256] order
               mbar_arrive_expect_tx(xbar, G * A2 * row_bytes);
               tma_load_4d(xs, &tmx, e0, j, 2 * s0, 0, xbar);
             }
             mbar_wait(&empty[st], ph ^ 1);
           }
+          // weights: box (256 coefficients, row g*L + j, MT output channels from mb)
           mbar_arrive_expect_tx(&full[st], MT * row_bytes);
           tma_load_3d_hint(ring + (size_t)st * MT * MAC_THREADS, &tmw, e0, g * L + j, mb, &full[st], evict_first);
+          ++issued;
           if (++st == NS) st = 0, ph ^= 1, first = 0;
         }
       }
@@ -453,51 +446,24 @@ __global__ void __launch_bounds__(2 * MAC_THREADS + 32, 1)
     return;
   }
 
-  const uint64_t q = c.q[j];
-  if (tid >= MAC_THREADS) {  // ---- INTT warps: levels 0..7 of the staged outputs, then store ----
-    const int it = tid - MAC_THREADS;
-    const uint32_t e = e0 + it;
-    {  // the e-tile's inverse-NTT twiddles for levels 0..7 (constant tables)
-      const Tw* tinv = Tab<AR>::inv(c) + (size_t)j * N;
-      if (it < 255) {
-        int l = 0;
-        while (it >= 256 - (256 >> (l + 1))) ++l;
-        const int g = it - (256 - (256 >> l));
-        twe[it] = tinv[(N >> (l + 1)) + (e0 >> (l + 1)) + g];
-      }
+  // ---- consumers: one coefficient each (X^ rows beyond 2*ns are zero-filled; never stored) ----
+  const uint32_t e = e0 + tid;
+  const uint64_t q = c.q[j], onep = c.one_p[j];
+  {  // the e-tile's inverse-NTT twiddles for levels 0..7 (constant tables: read before any wait)
+    const Tw* tinv = Tab<AR>::inv(c) + (size_t)j * N;
+    if (tid < 255) {
+      int l = 0;
+      while (tid >= 256 - (256 >> (l + 1))) ++l;
+      const int g = tid - (256 - (256 >> l));
+      twe[tid] = tinv[(N >> (l + 1)) + (e0 >> (l + 1)) + g];
     }
-    intt_group_sync();
-    int k = 0;
-    for (int mb = m_begin; mb < m_end; mb += MT, ++k) {
-      const int rows = min(MT, m_end - mb);
-      const int b = k & 1;
-      W* cbuf = cbuf0 + (size_t)b * NCH * MAC_CHS;
-      mbar_wait(&cfull[b], (k >> 1) & 1);
-      mac_intt_levels_0_7<AR>(cbuf, twe, NCH, it, (W)q, AR::bound((W)q));
-#pragma unroll
-      for (int r = 0; r < MT; ++r)
-#pragma unroll
-        for (int a = 0; a < A2; ++a)
-          if (r < rows && a < 2 * ns)
-            y[((((size_t)(mb + r) * S + s0 + (a >> 1)) * 2 + (a & 1)) * L + j) * N + e] =
-                cbuf[(r * A2 + a) * MAC_CHS + phys(it)];
-      intt_group_sync();  // every INTT thread has read the buffer
-      mbar_arrive(&cempty[b]);
-    }
-    pdl_trigger();
-    return;
   }
-
-  // ---- MAC warps: one coefficient each (X^ rows beyond 2*ns are zero-filled; never stored) ----
-  const uint64_t onep = c.one_p[j];
   const uint32_t r32 = (uint32_t)c.r32[j], r32p = (uint32_t)c.r32_p[j], onep32 = (uint32_t)(onep >> 32);
   mbar_wait(xbar, 0);
   int st = 0;
   uint32_t ph = 0;
-  int k = 0;
-  for (int mb = m_begin; mb < m_end; mb += MT, ++k) {
-    const int b = k & 1;
-    W* cbuf = cbuf0 + (size_t)b * NCH * MAC_CHS;
+  for (int mb = m_begin; mb < m_end; mb += MT) {
+    const int rows = min(MT, m_end - mb);
     if constexpr (sizeof(W) == 4) {
       uint64_t acc[MT][A2];
 #pragma unroll
@@ -520,7 +486,7 @@ __global__ void __launch_bounds__(2 * MAC_THREADS + 32, 1)
         if ((tid & 31) == 0) mbar_arrive(&empty[st]);
         if (++st == NS) st = 0, ph ^= 1;
       }
-      if (k >= 2) mbar_wait(&cempty[b], ((k >> 1) - 1) & 1);
+      consumer_sync();  // the previous m-block's chunks have been written out
 #pragma unroll
       for (int r = 0; r < MT; ++r)
 #pragma unroll
@@ -549,14 +515,24 @@ __global__ void __launch_bounds__(2 * MAC_THREADS + 32, 1)
         if ((tid & 31) == 0) mbar_arrive(&empty[st]);
         if (++st == NS) st = 0, ph ^= 1;
       }
-      if (k >= 2) mbar_wait(&cempty[b], ((k >> 1) - 1) & 1);
+      consumer_sync();  // the previous m-block's chunks have been written out
 #pragma unroll
       for (int r = 0; r < MT; ++r)
 #pragma unroll
         for (int a = 0; a < A2; ++a)
           cbuf[(r * A2 + a) * MAC_CHS + phys(tid)] = (W)reduce128(lo[r][a], hi[r][a], q, r64, r64p, onep);
     }
-    mbar_arrive(&cfull[b]);  // release: this thread's chunk words are visible to the INTT warps
+    // inverse-NTT levels 0..7 of every staged output chunk, then the chunks leave the SM (lazy
+    // GS domain values, finished by the INTT kernel)
+    consumer_sync();
+    mac_intt_levels_0_7<AR>(cbuf, twe, MT * A2, (W)q, AR::bound((W)q));
+#pragma unroll
+    for (int r = 0; r < MT; ++r)
+#pragma unroll
+      for (int a = 0; a < A2; ++a)
+        if (r < rows && a < 2 * ns)
+          y[((((size_t)(mb + r) * S + s0 + (a >> 1)) * 2 + (a & 1)) * L + j) * N + e] =
+              cbuf[(r * A2 + a) * MAC_CHS + phys(tid)];
   }
   pdl_trigger();
 }
@@ -833,13 +809,12 @@ static cudaError_t mac_t(const DevConsts& c, const PlanDev& p, const void* xhat,
   const size_t xtile = (size_t)p.G * 2 * SG * MAC_THREADS * sizeof(W);
   const size_t stage = (size_t)MT * MAC_THREADS * sizeof(W);
   // ring depth: fill ~110 KiB per CTA (two CTAs per SM) after the X^ tile, 4..32 stages
-  // one CTA per SM: X^ tile + two chunk buffers + twiddles, the rest (up to 216 KiB) is ring
-  const size_t chunks = 2 * (size_t)MT * 2 * SG * MAC_CHS * sizeof(W) + MAC_THREADS * 2 * sizeof(W);
+  const size_t chunks = (size_t)MT * 2 * SG * MAC_CHS * sizeof(W) + MAC_THREADS * 2 * sizeof(W);
   const size_t fixed = xtile + chunks;
-  const size_t budget = 216 * 1024 > fixed + 4 * stage ? 216 * 1024 - fixed : 4 * stage;
+  const size_t budget = 110 * 1024 > fixed + 4 * stage ? 110 * 1024 - fixed : 4 * stage;
   int NS = (int)(budget / stage);
-  NS = NS < 4 ? 4 : NS > 48 ? 48 : NS;
-  const size_t smem = fixed + NS * stage + (2 * NS + 5) * sizeof(uint64_t);
+  NS = NS < 4 ? 4 : NS > 32 ? 32 : NS;
+  const size_t smem = fixed + NS * stage + (2 * NS + 1) * sizeof(uint64_t);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   static size_t attr = 0;
   if (smem > attr) {
@@ -853,7 +828,7 @@ static cudaError_t mac_t(const DevConsts& c, const PlanDev& p, const void* xhat,
   // whose CTA count fills whole waves of two CTAs per SM best; ties go to fewer, longer CTAs
   // (each CTA pays one X^ tile load and one pipeline fill).
   const long ctas_no_m = (long)(N / MAC_THREADS) * n_sg * c.L;
-  const long wave = 148;
+  const long wave = 148 * 2;
   const int mblocks = (p.M + MT - 1) / MT;
   int best_nmr = 1;
   double best_eff = -1.0;
@@ -881,8 +856,8 @@ static cudaError_t mac_t(const DevConsts& c, const PlanDev& p, const void* xhat,
     return cudaErrorInvalidValue;
   dim3 grid((N / MAC_THREADS) * n_sg, c.L, n_mr);
   W* yp = static_cast<W*>(y);
-  cudaError_t e = launch_pdl(k_mac<W, SG, MT>, grid, dim3(2 * MAC_THREADS + 32), smem, s, tmx, tmw, yp, c, p,
-                             m_range, n_sg, NS);
+  cudaError_t e = launch_pdl(k_mac<W, SG, MT>, grid, dim3(MAC_THREADS + 32), smem, s, tmx, tmw, yp, c, p, m_range,
+                             n_sg, NS);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
