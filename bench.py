@@ -241,8 +241,8 @@ def run_secn(args, word_bits, world, rank, local, dev, full):
     def step_public():
         for d in st:
             if d["mc"] > 0:
-                ctx.he_conv2d(d["pl"], d["ct"], d["w"], x0=d["x0"], r=d["r"], out=d["out"], workspace=d["ws"])
-                ctx.extract_share(d["pl"], d["r"], out=d["y0"])
+                ctx.he_conv2d(d["pl"], d["ct"], d["w"], x0=d["x0"], r=d["r"], out=d["out"], workspace=d["ws"],
+                              y0=d["y0"])
 
     # ---- warmup (eager), then capture the step in a CUDA graph ----
     for _ in range(max(args.warmup, 3)):
@@ -312,7 +312,7 @@ def run_secn(args, word_bits, world, rank, local, dev, full):
 
     # ---- derived numbers ----
     n_ntt = sum((d["plan"].G * d["plan"].S * world + d["plan"].M * d["plan"].S) * 2 * L for d in st)  # limb NTTs per step
-    launches_per_step = sum(4 for d in st if d["mc"] > 0)
+    launches_per_step = sum(3 for d in st if d["mc"] > 0)  # NTT, MAC(+INTT 0-7), INTT tail(+mask, share)
     sb = {s: sum(stage_bytes(d["pl"], L, n, wbytes)[s] for d in st if d["mc"] > 0) for s in range(3)}
     names = {0: "k_ntt_fwd (A6 share add + A1 NTT)", 1: "k_mac (A4 NTT-domain MAC + INTT levels 0-7)",
              2: "k_ntt_inv_tail (A2 INTT levels 8-11 + A7 mask)"}
@@ -419,8 +419,8 @@ def run_e2e(ctx, st, K, dev, share_buf, world):
             d["ct"].copy_(h["ct"], non_blocking=True)
             d["x0"].copy_(h["x0"], non_blocking=True)
             d["r"].copy_(h["r"], non_blocking=True)
-            ctx.he_conv2d(d["pl"], d["ct"], d["w"], x0=d["x0"], r=d["r"], out=d["out"], workspace=d["ws"])
-            ctx.extract_share(d["pl"], d["r"], out=d["y0"])
+            ctx.he_conv2d(d["pl"], d["ct"], d["w"], x0=d["x0"], r=d["r"], out=d["out"], workspace=d["ws"],
+                          y0=d["y0"])
             h["out"].copy_(d["out"], non_blocking=True)
             h["y0"].copy_(d["y0"], non_blocking=True)
 
@@ -439,7 +439,7 @@ def run_e2e(ctx, st, K, dev, share_buf, world):
     if world > 1:
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     return {"value": round(float(ms.item()) / 1e3, 6), "unit": "s", "h2d_bytes_per_step": h2d,
-            "d2h_bytes_per_step": d2h, "path": "pinned host -> secn_he_conv2d + secn_extract_share -> pinned host"}
+            "d2h_bytes_per_step": d2h, "path": "pinned host -> secn_he_conv2d_ex -> pinned host"}
 
 
 # ------------------------------------------------------------------------------------------

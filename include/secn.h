@@ -153,6 +153,14 @@ int secn_he_conv2d_stage(secn_ctx* ctx, const secn_conv_plan_t* plan, int stage,
                          const uint64_t* x0, const uint64_t* w_ntt, const uint64_t* r, uint64_t* ct_out,
                          void* workspace, size_t ws_bytes, void* stream);
 
+/* secn_he_conv2d plus the server's output share (A8, as secn_extract_share) in the same
+ * launches: y0 [M][OH][OW] (uint64, < 2^t_bits) is written from r by the inverse-NTT tail
+ * kernel. y0 may be NULL (then identical to secn_he_conv2d); y0 != NULL needs r != NULL
+ * (else SECN_EINVAL). y0 must not alias any other argument. */
+int secn_he_conv2d_ex(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* ct_in, const uint64_t* x0,
+                      const uint64_t* w_ntt, const uint64_t* r, uint64_t* ct_out, uint64_t* y0, void* workspace,
+                      size_t ws_bytes, void* stream);
+
 /* Server's output share at the designated coefficients (§7; Cheetah's sparse
  * result): y0[m][oy][ox] = (t - r[m*S+s][O + i*Ww + j]) mod t for the plan's
  * index map, m in [0, plan->M). r [M*S][N], y0 [M][OH][OW]. */
@@ -179,6 +187,9 @@ int secn32_mask_add(secn_ctx* ctx, uint32_t* ct, const uint64_t* r, size_t n, vo
 int secn32_he_conv2d(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint32_t* ct_in, const uint64_t* x0,
                      const uint32_t* w_ntt, const uint64_t* r, uint32_t* ct_out, void* workspace, size_t ws_bytes,
                      void* stream);
+int secn32_he_conv2d_ex(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint32_t* ct_in, const uint64_t* x0,
+                        const uint32_t* w_ntt, const uint64_t* r, uint32_t* ct_out, uint64_t* y0, void* workspace,
+                        size_t ws_bytes, void* stream);
 int secn32_he_conv2d_stage(secn_ctx* ctx, const secn_conv_plan_t* plan, int stage, const uint32_t* ct_in,
                            const uint64_t* x0, const uint32_t* w_ntt, const uint64_t* r, uint32_t* ct_out,
                            void* workspace, size_t ws_bytes, void* stream);

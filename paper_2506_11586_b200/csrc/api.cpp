@@ -430,12 +430,13 @@ size_t secn_he_conv2d_workspace(const secn_ctx* ctx, const secn_conv_plan_t* pla
 }
 
 static int he_conv2d_impl(secn_ctx* ctx, uint32_t bits, const secn_conv_plan_t* plan, int stage, const void* ct_in,
-                          const uint64_t* x0, const void* w_ntt, const uint64_t* r, void* ct_out, void* workspace,
-                          size_t ws_bytes, void* stream) {
+                          const uint64_t* x0, const void* w_ntt, const uint64_t* r, void* ct_out, uint64_t* y0,
+                          void* workspace, size_t ws_bytes, void* stream) {
   if (int st = check_ctx(ctx, bits)) return st;
   if (int st = check_plan(ctx, plan)) return st;
   if (stage < -1 || stage > 2) return fail(SECN_EINVAL, "stage %d not in {0,1,2}", stage);
   if (!ct_in || !w_ntt || !ct_out || !workspace) return fail(SECN_EINVAL, "NULL buffer");
+  if (y0 && !r) return fail(SECN_EINVAL, "y0 needs the mask r");
   if (ws_bytes < secn_he_conv2d_workspace(ctx, plan)) return fail(SECN_EINVAL, "workspace too small");
   if (((uintptr_t)workspace | (uintptr_t)ct_in | (uintptr_t)ct_out | (uintptr_t)w_ntt) & 15)
     return fail(SECN_EINVAL, "buffers must be 16-byte aligned");
@@ -455,34 +456,46 @@ static int he_conv2d_impl(secn_ctx* ctx, uint32_t bits, const secn_conv_plan_t* 
   // A4 + A2 levels 0..7
   if (e == cudaSuccess && (stage == -1 || stage == 1)) e = secn::launch_mac(ctx->dc, pd, workspace, w_ntt, ct_out, s);
   if (e == cudaSuccess && (stage == -1 || stage == 2))
-    e = secn::launch_ntt_inv_tail(ctx->dc, ct_out, n_out * 2 * ctx->L, r, s);  // A2 (levels 8..) + A7
+    e = secn::launch_ntt_inv_tail(ctx->dc, ct_out, n_out * 2 * ctx->L, r, y0, pd, s);  // A2 (levels 8..) + A7 (+A8)
   return e == cudaSuccess ? SECN_OK : cuda_fail(e, "secn_he_conv2d");
 }
 
 int secn_he_conv2d(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* ct_in, const uint64_t* x0,
                    const uint64_t* w_ntt, const uint64_t* r, uint64_t* ct_out, void* workspace, size_t ws_bytes,
                    void* stream) {
-  return he_conv2d_impl(ctx, 64, plan, -1, ct_in, x0, w_ntt, r, ct_out, workspace, ws_bytes, stream);
+  return he_conv2d_impl(ctx, 64, plan, -1, ct_in, x0, w_ntt, r, ct_out, nullptr, workspace, ws_bytes, stream);
+}
+
+int secn_he_conv2d_ex(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* ct_in, const uint64_t* x0,
+                      const uint64_t* w_ntt, const uint64_t* r, uint64_t* ct_out, uint64_t* y0, void* workspace,
+                      size_t ws_bytes, void* stream) {
+  return he_conv2d_impl(ctx, 64, plan, -1, ct_in, x0, w_ntt, r, ct_out, y0, workspace, ws_bytes, stream);
+}
+
+int secn32_he_conv2d_ex(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint32_t* ct_in, const uint64_t* x0,
+                        const uint32_t* w_ntt, const uint64_t* r, uint32_t* ct_out, uint64_t* y0, void* workspace,
+                        size_t ws_bytes, void* stream) {
+  return he_conv2d_impl(ctx, 32, plan, -1, ct_in, x0, w_ntt, r, ct_out, y0, workspace, ws_bytes, stream);
 }
 
 int secn_he_conv2d_stage(secn_ctx* ctx, const secn_conv_plan_t* plan, int stage, const uint64_t* ct_in,
                          const uint64_t* x0, const uint64_t* w_ntt, const uint64_t* r, uint64_t* ct_out,
                          void* workspace, size_t ws_bytes, void* stream) {
   if (stage < 0 || stage > 2) return fail(SECN_EINVAL, "stage %d not in {0,1,2}", stage);
-  return he_conv2d_impl(ctx, 64, plan, stage, ct_in, x0, w_ntt, r, ct_out, workspace, ws_bytes, stream);
+  return he_conv2d_impl(ctx, 64, plan, stage, ct_in, x0, w_ntt, r, ct_out, nullptr, workspace, ws_bytes, stream);
 }
 
 int secn32_he_conv2d(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint32_t* ct_in, const uint64_t* x0,
                      const uint32_t* w_ntt, const uint64_t* r, uint32_t* ct_out, void* workspace, size_t ws_bytes,
                      void* stream) {
-  return he_conv2d_impl(ctx, 32, plan, -1, ct_in, x0, w_ntt, r, ct_out, workspace, ws_bytes, stream);
+  return he_conv2d_impl(ctx, 32, plan, -1, ct_in, x0, w_ntt, r, ct_out, nullptr, workspace, ws_bytes, stream);
 }
 
 int secn32_he_conv2d_stage(secn_ctx* ctx, const secn_conv_plan_t* plan, int stage, const uint32_t* ct_in,
                            const uint64_t* x0, const uint32_t* w_ntt, const uint64_t* r, uint32_t* ct_out,
                            void* workspace, size_t ws_bytes, void* stream) {
   if (stage < 0 || stage > 2) return fail(SECN_EINVAL, "stage %d not in {0,1,2}", stage);
-  return he_conv2d_impl(ctx, 32, plan, stage, ct_in, x0, w_ntt, r, ct_out, workspace, ws_bytes, stream);
+  return he_conv2d_impl(ctx, 32, plan, stage, ct_in, x0, w_ntt, r, ct_out, nullptr, workspace, ws_bytes, stream);
 }
 
 int secn_extract_share(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* r, uint64_t* y0, void* stream) {

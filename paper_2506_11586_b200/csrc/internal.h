@@ -41,9 +41,10 @@ struct PlanDev {  // the subset of secn_conv_plan the kernels use
 cudaError_t launch_ntt_fwd(const DevConsts& c, const void* in, void* out, size_t n_limb_polys, const uint64_t* x0,
                            cudaStream_t s);
 cudaError_t launch_ntt_inv(const DevConsts& c, void* polys, size_t n_limb_polys, const uint64_t* r, cudaStream_t s);
-// levels 8.. of the inverse NTT (+N^-1, +mask) after launch_mac applied levels 0..7
-cudaError_t launch_ntt_inv_tail(const DevConsts& c, void* polys, size_t n_limb_polys, const uint64_t* r,
-                                cudaStream_t s);
+// levels 8.. of the inverse NTT (+N^-1, +mask) after launch_mac applied levels 0..7; if
+// y0 != NULL also the server share (A8) for plan pl
+cudaError_t launch_ntt_inv_tail(const DevConsts& c, void* polys, size_t n_limb_polys, const uint64_t* r, uint64_t* y0,
+                                const PlanDev& pl, cudaStream_t s);
 // NTT-domain MAC (A4) followed by inverse-NTT levels 0..7 of its outputs (lazy GS domain)
 cudaError_t launch_mac(const DevConsts& c, const PlanDev& p, const void* xhat, const void* w, void* y, cudaStream_t s);
 cudaError_t launch_pack_weights(const DevConsts& c, const PlanDev& p, const uint64_t* kernel, void* w, cudaStream_t s);

@@ -216,7 +216,8 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN, NP>(
 // thread: no shared memory, one load and one store per word.
 template <class A, int LOGN>
 __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN, 1>())
-    k_ntt_inv_tail(typename A::W* polys, const __grid_constant__ DevConsts c, const uint64_t* __restrict__ r) {
+    k_ntt_inv_tail(typename A::W* polys, const __grid_constant__ DevConsts c, const uint64_t* __restrict__ r,
+                   uint64_t* __restrict__ y0, const __grid_constant__ PlanDev pl, size_t ct0) {
   using W = typename A::W;
   constexpr int N = 1 << LOGN;
   constexpr int LS = 8;
@@ -271,6 +272,23 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN, 1>()
       }
       buf[RL::addr(k, i)] = v;
     }
+  // A8 fused (secn_he_conv2d_ex): the server's output share y0 = -r mod t at the designated
+  // coefficients of this ciphertext (one CTA per ciphertext does it: limb 0, b component). It
+  // depends on r only, so it never waits on the transform; it saves a launch per layer.
+  if (y0 != nullptr && mask && j == 0) {
+    const uint32_t ct = (uint32_t)(ct0 + (pi >> 1)), m = ct / pl.S, sidx = ct % pl.S;
+    const uint32_t bh = sidx / pl.nbw, bw = sidx % pl.nbw;
+    const uint32_t dh = pl.Hw - pl.kh + 1, dw = pl.Ww - pl.kw + 1;
+    const uint64_t* rs = r + (pi >> 1) * N;
+    const uint64_t tm = (1ull << c.t_bits) - 1;
+    for (uint32_t d = threadIdx.x; d < dh * dw; d += N / 16) {
+      const uint32_t i = d / dw, jj = d - i * dw;
+      const uint32_t py = bh * dh + i, px = bw * dw + jj;
+      const uint32_t oy = py / pl.sh, ox = px / pl.sh;
+      if (oy * pl.sh != py || ox * pl.sh != px || oy >= pl.OH || ox >= pl.OW) continue;
+      y0[((size_t)m * pl.OH + oy) * pl.OW + ox] = (tm + 1 - rs[pl.O + i * pl.Ww + jj]) & tm;
+    }
+  }
 }
 
 // ------------------------------------------------------------------------------------------
@@ -702,7 +720,8 @@ static cudaError_t ntt_inv_t(const DevConsts& c, void* polys, size_t P, const ui
 }
 
 template <class A, int LOGN>
-static cudaError_t ntt_inv_tail_t(const DevConsts& c, void* polys, size_t P, const uint64_t* r, cudaStream_t s) {
+static cudaError_t ntt_inv_tail_t(const DevConsts& c, void* polys, size_t P, const uint64_t* r, uint64_t* y0,
+                                  const PlanDev& pl, cudaStream_t s) {
   using W = typename A::W;
   constexpr int N = 1 << LOGN;
   const size_t smem = LOGN > 12 ? smem_words<LOGN>() * sizeof(W) : 0;
@@ -717,25 +736,27 @@ static cudaError_t ntt_inv_tail_t(const DevConsts& c, void* polys, size_t P, con
     const size_t np = n_polys - p0 < pmax ? n_polys - p0 : pmax;
     W* buf = static_cast<W*>(polys) + p0 * c.L * N;
     const uint64_t* rs = r ? r + p0 / 2 * N : nullptr;
-    cudaError_t e = launch_pdl(k_ntt_inv_tail<A, LOGN>, dim3((unsigned)(np * c.L)), dim3(N / 16), smem, s, buf, c, rs);
+    cudaError_t e = launch_pdl(k_ntt_inv_tail<A, LOGN>, dim3((unsigned)(np * c.L)), dim3(N / 16), smem, s, buf, c,
+                               rs, y0, pl, p0 / 2);
     if (e != cudaSuccess) return e;
   }
   return cudaGetLastError();
 }
 
-cudaError_t launch_ntt_inv_tail(const DevConsts& c, void* polys, size_t P, const uint64_t* r, cudaStream_t s) {
+cudaError_t launch_ntt_inv_tail(const DevConsts& c, void* polys, size_t P, const uint64_t* r, uint64_t* y0,
+                                const PlanDev& pl, cudaStream_t s) {
   if (P == 0) return cudaSuccess;
   if (c.word_bits == 64) {
     switch (c.log_n) {
-      case 12: return ntt_inv_tail_t<Arith64, 12>(c, polys, P, r, s);
-      case 13: return ntt_inv_tail_t<Arith64, 13>(c, polys, P, r, s);
-      case 14: return ntt_inv_tail_t<Arith64, 14>(c, polys, P, r, s);
+      case 12: return ntt_inv_tail_t<Arith64, 12>(c, polys, P, r, y0, pl, s);
+      case 13: return ntt_inv_tail_t<Arith64, 13>(c, polys, P, r, y0, pl, s);
+      case 14: return ntt_inv_tail_t<Arith64, 14>(c, polys, P, r, y0, pl, s);
     }
   } else {
     switch (c.log_n) {
-      case 12: return ntt_inv_tail_t<Arith32, 12>(c, polys, P, r, s);
-      case 13: return ntt_inv_tail_t<Arith32, 13>(c, polys, P, r, s);
-      case 14: return ntt_inv_tail_t<Arith32, 14>(c, polys, P, r, s);
+      case 12: return ntt_inv_tail_t<Arith32, 12>(c, polys, P, r, y0, pl, s);
+      case 13: return ntt_inv_tail_t<Arith32, 13>(c, polys, P, r, y0, pl, s);
+      case 14: return ntt_inv_tail_t<Arith32, 14>(c, polys, P, r, y0, pl, s);
     }
   }
   return cudaErrorInvalidValue;

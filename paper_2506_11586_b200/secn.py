@@ -30,7 +30,8 @@ EXPORTS = ("secn_ctx_create", "secn_ctx_destroy", "secn_ctx_query", "secn_last_e
            "secn_ntt_fwd", "secn_ntt_inv", "secn_preprocess_weights", "secn_share_add", "secn_mask_add",
            "secn_he_conv2d_workspace", "secn_he_conv2d", "secn_he_conv2d_stage", "secn_extract_share",
            "secn32_ctx_create", "secn32_ntt_fwd", "secn32_ntt_inv", "secn32_preprocess_weights",
-           "secn32_share_add", "secn32_mask_add", "secn32_he_conv2d", "secn32_he_conv2d_stage")
+           "secn32_share_add", "secn32_mask_add", "secn32_he_conv2d", "secn32_he_conv2d_stage",
+           "secn_he_conv2d_ex", "secn32_he_conv2d_ex")
 
 
 class SecnError(RuntimeError):
@@ -92,10 +93,11 @@ def lib(path=None) -> ctypes.CDLL:
         "secn_he_conv2d_workspace": (sz, [vp, P]),
         "secn_he_conv2d": (i, [vp, P, vp, vp, vp, vp, vp, vp, sz, vp]),
         "secn_he_conv2d_stage": (i, [vp, P, i, vp, vp, vp, vp, vp, vp, sz, vp]),
+        "secn_he_conv2d_ex": (i, [vp, P, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
         "secn_extract_share": (i, [vp, P, vp, vp, vp]),
         "secn32_ctx_create": (i, [ctypes.POINTER(vp), i, u32, u32, ctypes.POINTER(ctypes.c_uint32), u32]),
     }
-    for f in ("ntt_fwd", "ntt_inv", "preprocess_weights", "share_add", "mask_add", "he_conv2d", "he_conv2d_stage"):
+    for f in ("ntt_fwd", "ntt_inv", "preprocess_weights", "share_add", "mask_add", "he_conv2d", "he_conv2d_stage", "he_conv2d_ex"):
         sig["secn32_" + f] = sig["secn_" + f]
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -227,7 +229,10 @@ class Context:
 
     def he_conv2d(self, plan: Plan, ct_in: torch.Tensor, w_ntt: torch.Tensor, x0: Optional[torch.Tensor] = None,
                   r: Optional[torch.Tensor] = None, out: Optional[torch.Tensor] = None,
-                  workspace: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+                  workspace: Optional[torch.Tensor] = None, stream=None, y0: Optional[torch.Tensor] = None
+                  ) -> torch.Tensor:
+        """secn_he_conv2d; with y0 (int64 [M][OH][OW]) secn_he_conv2d_ex, which also writes the
+        server's output share in the same launches."""
         L, n = self.L, self.n
         n_in, n_out = plan.G * plan.S, plan.M * plan.S
         if out is None:
@@ -235,11 +240,15 @@ class Context:
         ws_bytes = self.workspace_bytes(plan)
         if workspace is None:
             workspace = torch.empty(ws_bytes // 8, dtype=torch.int64, device=self.device)
-        _check(self._f("he_conv2d")(self._h, ctypes.byref(plan), self._rp(ct_in, (n_in, 2, L, n), "ct_in"),
-                                    _ptr(x0, (n_in, n), "x0"), self._rp(w_ntt, (plan.M, plan.G, L, n), "w_ntt"),
-                                    _ptr(r, (n_out, n), "r"), self._rp(out, (n_out, 2, L, n), "ct_out"),
-                                    ctypes.c_void_p(workspace.data_ptr()), workspace.numel() * workspace.element_size(),
-                                    self._stream(stream)))
+        args = [self._h, ctypes.byref(plan), self._rp(ct_in, (n_in, 2, L, n), "ct_in"),
+                _ptr(x0, (n_in, n), "x0"), self._rp(w_ntt, (plan.M, plan.G, L, n), "w_ntt"),
+                _ptr(r, (n_out, n), "r"), self._rp(out, (n_out, 2, L, n), "ct_out")]
+        tail = [ctypes.c_void_p(workspace.data_ptr()), workspace.numel() * workspace.element_size(),
+                self._stream(stream)]
+        if y0 is None:
+            _check(self._f("he_conv2d")(*args, *tail))
+        else:
+            _check(self._f("he_conv2d_ex")(*args, _ptr(y0, (plan.M, plan.OH, plan.OW), "y0"), *tail))
         return out
 
     def he_conv2d_stage(self, stage: int, plan: Plan, ct_in: torch.Tensor, w_ntt: torch.Tensor,

@@ -343,6 +343,37 @@ def test_extract_share_matches_oracle(env):
         assert (got == packing.extract((P.t - r) % P.t, opl)).all()
 
 
+@pytest.mark.parametrize("lay", [layers.tiny()[0], L_("s2", 3, 40, 40, 5, 3, 2, 0), L_("ds", 24, 28, 28, 9, 1, 2, 0),
+                                 L_("multi_s", 2, 70, 70, 3, 3, 1, 0), L_("k7", 3, 64, 64, 4, 7, 2, 3)],
+                         ids=lambda l: l.name)
+def test_he_conv2d_ex_fused_share_matches_oracle(env, lay):
+    """secn_he_conv2d_ex: the same ciphertexts as secn_he_conv2d, and y0 equal to the oracle's
+    designated-coefficient extraction of (t - r) mod t."""
+    ctx, P, D = env
+    opl = oplan(P, ctx, lay)
+    ct, x0, K, r = _layer_inputs(P, lay, 9, opl)
+    plan = ctx.plan(lay.C, lay.H, lay.W, lay.M, lay.k, stride=lay.stride, pad=lay.pad)
+    w = ctx.preprocess_weights(plan, TP(K))
+    y0 = torch.full((plan.M, plan.OH, plan.OW), -1, dtype=torch.int64, device=DEV)
+    out = D.U(ctx.he_conv2d(plan, D.R(ct), w, x0=TP(x0), r=TP(r), y0=y0))
+    assert (out == he.server_conv(ct, x0, K, r, opl, P)).all()
+    assert (UP(y0) == packing.extract((P.t - r) % P.t, opl)).all()
+
+
+def test_he_conv2d_ex_needs_r(env):
+    ctx, P, D = env
+    lay = layers.tiny()[0]
+    opl = oplan(P, ctx, lay)
+    ct, x0, K, r = _layer_inputs(P, lay, 1, opl)
+    plan = ctx.plan(lay.C, lay.H, lay.W, lay.M, lay.k, stride=lay.stride, pad=lay.pad)
+    w = ctx.preprocess_weights(plan, TP(K))
+    y0 = torch.empty((plan.M, plan.OH, plan.OW), dtype=torch.int64, device=DEV)
+    from paper_2506_11586_b200 import secn as m
+
+    with pytest.raises(m.SecnError):
+        ctx.he_conv2d(plan, D.R(ct), w, x0=TP(x0), r=None, y0=y0)
+
+
 def test_end_to_end_decrypts_to_plain_conv(env):
     """Client (oracle harness) encrypts its share; the GPU server path runs; decrypt + the
     GPU-extracted server share reconstruct conv(x0 + x1, K) mod 2^37 exactly."""
@@ -358,8 +389,11 @@ def test_end_to_end_decrypts_to_plain_conv(env):
     ct = np.stack([he.encrypt(xin[i], sk, inputs.uniform_residues(g, (), P.primes, P.n),
                               inputs.rounded_gaussian(g, P.n), P) for i in range(opl.G * opl.S)])
     r = inputs.uniform_below(g, (opl.M * opl.S, P.n), P.t)
-    plan, out = _run_layer(ctx, D, lay, ct, packing.pack_input(x0, opl, P.n), K, r)
-    y0 = UP(ctx.extract_share(plan, TP(r)))
+    plan = ctx.plan(lay.C, lay.H, lay.W, lay.M, lay.k, stride=lay.stride, pad=lay.pad)
+    w = ctx.preprocess_weights(plan, TP(K))
+    y0t = torch.empty((plan.M, plan.OH, plan.OW), dtype=torch.int64, device=DEV)
+    out = D.U(ctx.he_conv2d(plan, D.R(ct), w, x0=TP(packing.pack_input(x0, opl, P.n)), r=TP(r), y0=y0t))
+    y0 = UP(y0t)
     s_idx, coef = packing.designated_map(opl)
     y1 = np.zeros_like(y0)
     for m in range(opl.M):
