@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--ref-frac", type=float, default=0.01, help="oracle sample fraction per --impl reference step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--serial", action="store_true",
+                    help="run every layer in network order on one stream (no fire e1/e3 or ResNet c1/ds overlap)")
     return ap.parse_args()
 
 
@@ -191,6 +193,7 @@ def run_secn(args, word_bits, world, rank, local, dev, full):
     the per-stage, e2e and cpu_baseline legs. Returns the JSON dict on rank 0 (None elsewhere)."""
     from paper_2506_11586_b200 import Context
     from paper_2506_11586_b200 import dist as sdist
+    from paper_2506_11586_b200.schedule import GroupRunner, concurrent_groups
 
     ctx = Context(local, word_bits=word_bits)
     L, n, t_bits = ctx.L, ctx.n, ctx.t_bits
@@ -238,11 +241,20 @@ def run_secn(args, word_bits, world, rank, local, dev, full):
     torch.cuda.synchronize()
     offline_s = e0.elapsed_time(e1) / 1e3
 
+    # layers that read the same input tensor (fire e1/e3, ResNet c1/ds) overlap on side streams;
+    # everything else keeps network order (paper_2506_11586_b200/schedule.py)
+    names = [d["lay"].name for d in st]
+    groups = [[i] for i in range(len(st))] if args.serial else concurrent_groups(names)
+    runner = GroupRunner(groups, dev)
+
+    def layer_call(i):
+        d = st[i]
+        if d["mc"] > 0:
+            ctx.he_conv2d(d["pl"], d["ct"], d["w"], x0=d["x0"], r=d["r"], out=d["out"], workspace=d["ws"],
+                          y0=d["y0"])
+
     def step_public():
-        for d in st:
-            if d["mc"] > 0:
-                ctx.he_conv2d(d["pl"], d["ct"], d["w"], x0=d["x0"], r=d["r"], out=d["out"], workspace=d["ws"],
-                              y0=d["y0"])
+        runner(layer_call)
 
     # ---- warmup (eager), then capture the step in a CUDA graph ----
     for _ in range(max(args.warmup, 3)):
@@ -305,7 +317,7 @@ def run_secn(args, word_bits, world, rank, local, dev, full):
     stage_ms = stage_profile(ctx, st, K, dev)
 
     # ---- e2e: host buffers, H2D + public API + D2H every step ----
-    e2e = None if args.no_e2e else run_e2e(ctx, st, K, dev, share_buf, world)
+    e2e = None if args.no_e2e else run_e2e(ctx, st, K, dev, share_buf, world, runner)
 
     if rank != 0:
         return None
@@ -334,7 +346,10 @@ def run_secn(args, word_bits, world, rank, local, dev, full):
         "config": {"workload": f"{args.net}: all {len(net)} conv layers at 224x224 (BASELINE.json configs[2])",
                    "N": n, "limbs": L, "primes": [hex(q) for q in ctx.primes], "t_bits": t_bits,
                    "parallelism": f"output-channel shards x{world}", "l2": "inputs 2.9 GB/step >> 126 MB L2 (no flush)",
-                   "timing": "CUDA events around CUDA-graph replays of the whole step"},
+                   "timing": "CUDA events around CUDA-graph replays of the whole step",
+                   "layer_overlap": ("none (--serial)" if args.serial else
+                                     "layers reading the same input tensor (fire e1/e3, ResNet c1/ds) on side "
+                                     "streams; all else in network order")},
         "throughput": {"ntt_per_s": round(n_ntt / step_s, 1), "alg_bytes_per_step": alg_bytes,
                        "alg_GBps": round(alg_bytes / step_s / 1e9, 1), "hbm_frac": round(alg_bytes / step_s / 1e9 / hbm_peak, 4),
                        "offline_preprocess_s": round(offline_s, 5), "wall_s_timed_region": round(wall, 4)},
@@ -393,7 +408,7 @@ def stage_profile(ctx, st, K, dev):
     return [x / K for x in tot]
 
 
-def run_e2e(ctx, st, K, dev, share_buf, world):
+def run_e2e(ctx, st, K, dev, share_buf, world, runner):
     """Same metric end to end through the public API: every step copies that step's inputs
     (ct_in, x0, r) host->device from pinned memory, runs secn_he_conv2d + the share
     extraction per layer, and copies the output ciphertexts and shares device->host."""
@@ -414,15 +429,23 @@ def run_e2e(ctx, st, K, dev, share_buf, world):
         d2h += h["out"].numel() * h["out"].element_size() + h["y0"].numel() * 8
         host.append((d, h))
 
+    hmap = {id(d): h for d, h in host}
+
+    def layer_io(i):
+        d = st[i]
+        h = hmap.get(id(d))
+        if h is None:
+            return
+        d["ct"].copy_(h["ct"], non_blocking=True)
+        d["x0"].copy_(h["x0"], non_blocking=True)
+        d["r"].copy_(h["r"], non_blocking=True)
+        ctx.he_conv2d(d["pl"], d["ct"], d["w"], x0=d["x0"], r=d["r"], out=d["out"], workspace=d["ws"],
+                      y0=d["y0"])
+        h["out"].copy_(d["out"], non_blocking=True)
+        h["y0"].copy_(d["y0"], non_blocking=True)
+
     def step():
-        for d, h in host:
-            d["ct"].copy_(h["ct"], non_blocking=True)
-            d["x0"].copy_(h["x0"], non_blocking=True)
-            d["r"].copy_(h["r"], non_blocking=True)
-            ctx.he_conv2d(d["pl"], d["ct"], d["w"], x0=d["x0"], r=d["r"], out=d["out"], workspace=d["ws"],
-                          y0=d["y0"])
-            h["out"].copy_(d["out"], non_blocking=True)
-            h["y0"].copy_(d["y0"], non_blocking=True)
+        runner(layer_io)
 
     for _ in range(2):
         step()

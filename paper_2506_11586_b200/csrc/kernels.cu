@@ -335,6 +335,43 @@ __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;"
 // twe holds the e-tile's 255 twiddles: level l, local group g at twe[256 - (256 >> l) + g].
 constexpr int MAC_CHS = MAC_THREADS + MAC_THREADS / 16;
 
+// Position of twiddle (level l, local group g) in twe. Round A reads, per task b = tau & 15, the
+// 8 >> p twiddles b * (8 >> p) .. of level p < 4 as 16-byte chunks; lanes b = 0..7 of an LDS.128
+// phase would hit the same bank group (row stride 64 B for 32-bit, 128 B for 64-bit words), so
+// the chunks of row b are XOR-swizzled by b (conflict-free for every level and word size).
+template <class Tw>
+__host__ __device__ __forceinline__ int twe_pos(int l, int g) {
+  constexpr int CPW = 16 / (int)sizeof(Tw);  // twiddles per 16-byte chunk: 2 (32-bit), 1 (64-bit)
+  const int base = 256 - (256 >> l);
+  if (l >= 4) return base + g;
+  const int n = 8 >> l;      // twiddles per task row
+  const int cpr = n / CPW;    // chunks per row (>= 1 except 32-bit level 3)
+  if (cpr <= 1) return base + g;
+  const int b = g / n, w = g % n, v = w / CPW;
+  const int sw = (b / (8 / cpr)) & (cpr - 1);
+  return base + b * n + (v ^ sw) * CPW + w % CPW;
+}
+
+// the 8 >> l twiddles of task row b at level l < 4, as whole 16-byte chunks (see twe_pos)
+template <class Tw, int l>
+__device__ __forceinline__ void twe_row(Tw* out, const Tw* twe, int b) {
+  constexpr int CPW = 16 / (int)sizeof(Tw), n = 8 >> l, cpr = n / CPW;
+  const Tw* row = twe + 256 - (256 >> l) + b * n;
+  if constexpr (cpr <= 1) {
+#pragma unroll
+    for (int w = 0; w < n; ++w) out[w] = row[w];
+  } else {
+    const int sw = (b / (8 / cpr)) & (cpr - 1);
+#pragma unroll
+    for (int v = 0; v < cpr; ++v) {
+      const uint4 ch = reinterpret_cast<const uint4*>(row)[v ^ sw];
+      const Tw* t = reinterpret_cast<const Tw*>(&ch);
+#pragma unroll
+      for (int k = 0; k < CPW; ++k) out[v * CPW + k] = t[k];
+    }
+  }
+}
+
 template <class A>
 __device__ __forceinline__ void mac_intt_levels_0_7(typename A::W* cbuf, const typename A::Tw* twe, int nch,
                                                     typename A::W q, typename A::W qb) {
@@ -347,14 +384,31 @@ __device__ __forceinline__ void mac_intt_levels_0_7(typename A::W* cbuf, const t
     W x[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) x[i] = base[i];
+    using Tw = typename A::Tw;
+    if constexpr (sizeof(Tw) == 8) {  // 32-bit words: row b's twiddles of levels 0..3 in registers
+      Tw tr[15];                      // level p at tr[16 - (16 >> p) + k]
+      twe_row<Tw, 0>(tr, twe, b);
+      twe_row<Tw, 1>(tr + 8, twe, b);
+      twe_row<Tw, 2>(tr + 12, twe, b);
+      twe_row<Tw, 3>(tr + 14, twe, b);
 #pragma unroll
-    for (int p = 0; p < 4; ++p) {
-      const int d = 1 << p;
+      for (int p = 0; p < 4; ++p) {
+        const int d = 1 << p;
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        if (i & d) continue;
-        const typename A::Tw w = twe[256 - (256 >> p) + b * (8 >> p) + (i >> (p + 1))];
-        A::gs(x[i], x[i + d], w, q, qb);
+        for (int i = 0; i < 16; ++i) {
+          if (i & d) continue;
+          A::gs(x[i], x[i + d], tr[16 - (16 >> p) + (i >> (p + 1))], q, qb);
+        }
+      }
+    } else {  // 64-bit words: one 16-byte twiddle per butterfly group, read at its use
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        const int d = 1 << p;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          if (i & d) continue;
+          A::gs(x[i], x[i + d], twe[twe_pos<Tw>(p, b * (8 >> p) + (i >> (p + 1)))], q, qb);
+        }
       }
     }
 #pragma unroll
@@ -473,7 +527,7 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
       int l = 0;
       while (tid >= 256 - (256 >> (l + 1))) ++l;
       const int g = tid - (256 - (256 >> l));
-      twe[tid] = tinv[(N >> (l + 1)) + (e0 >> (l + 1)) + g];
+      twe[twe_pos<Tw>(l, g)] = tinv[(N >> (l + 1)) + (e0 >> (l + 1)) + g];
     }
   }
   const uint32_t r32 = (uint32_t)c.r32[j], r32p = (uint32_t)c.r32_p[j], onep32 = (uint32_t)(onep >> 32);

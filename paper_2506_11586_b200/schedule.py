@@ -1,0 +1,65 @@
+"""Layer scheduling for a network's HE-linear layers on one GPU: which layers the network's
+data flow lets the server run at the same time, and a stream fork/join executor for them.
+
+The server evaluates a network's convolutions one layer at a time because each layer's input
+share comes out of the nonlinear protocol that follows the previous one (§7).
+Two layers that read the SAME input tensor are independent:
+  * SqueezeNet fire modules: expand1x1 (``fireK.e1``) and expand3x3 (``fireK.e3``) both read the
+    squeeze output (their results are concatenated afterwards);
+  * ResNet bottleneck blocks with a projection: ``lX.b0.c1`` and ``lX.b0.ds`` both read the
+    block input.
+Only such groups overlap (on separate CUDA streams); everything else keeps the network order,
+so the step time stays what the protocol would see layer by layer.
+"""
+from __future__ import annotations
+
+from typing import Callable, List, Sequence
+
+import torch
+
+
+def concurrent_groups(names: Sequence[str]) -> List[List[int]]:
+    """Partitions layer indices into groups that may run concurrently, ordered by each group's
+    first layer. A later member moves up to its group (valid: it reads the same input as the
+    group's first layer, which is ready then), e.g. a ResNet projection ``ds`` runs beside ``c1``."""
+    groups: List[List[int]] = []
+    key_of = {}
+    for i, n in enumerate(names):
+        key = None
+        if n.endswith(".e1") or n.endswith(".e3"):
+            key = ("fire", n[:-3])
+        elif n.endswith(".b0.c1") or n.endswith(".b0.ds"):
+            key = ("proj", n.rsplit(".", 1)[0])
+        if key is not None and key in key_of:  # same input as an earlier layer: joins its group
+            groups[key_of[key]].append(i)
+            continue
+        if key is not None:
+            key_of[key] = len(groups)
+        groups.append([i])
+    return groups
+
+
+class GroupRunner:
+    """Runs ``fn(i)`` for every layer index in ``groups``: a group's first layer on the current
+    stream, the others on side streams forked from it and joined back before the next group.
+    Works eagerly and under CUDA-graph capture (the fork/join become graph edges)."""
+
+    def __init__(self, groups: List[List[int]], device):
+        self.groups = groups
+        width = max((len(g) for g in groups), default=1)
+        self.side = [torch.cuda.Stream(device) for _ in range(width - 1)]
+
+    def __call__(self, fn: Callable[[int], None]) -> None:
+        main = torch.cuda.current_stream()
+        for g in self.groups:
+            if len(g) == 1:
+                fn(g[0])
+                continue
+            for s in self.side[:len(g) - 1]:
+                s.wait_stream(main)
+            for s, i in zip(self.side, g[1:]):
+                with torch.cuda.stream(s):
+                    fn(i)
+            fn(g[0])
+            for s in self.side[:len(g) - 1]:
+                main.wait_stream(s)
