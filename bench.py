@@ -44,7 +44,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["secn", "reference"], default="secn")
-    ap.add_argument("--net", default="squeezenet1_1")
+    ap.add_argument("--net", default="squeezenet1_1",
+                    help="squeezenet1_1 (C3, default) | squeezenet1_0 | resnet50 (C4) | tiny (C1) | ntt_sweep (C5)")
     ap.add_argument("--word-bits", type=int, choices=[32, 64], default=32,
                     help="32: four 27-bit uint32 RNS limbs (reading R1b, headline); 64: q 60+49 bit uint64 limbs "
                          "(reading R1)")
@@ -55,6 +56,8 @@ def parse():
     ap.add_argument("--ref-frac", type=float, default=0.01, help="oracle sample fraction per --impl reference step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-online", action="store_true", help="skip the online-NTT-preprocessing (f4) leg")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the compact NTT sweep (C5) in the default run")
     ap.add_argument("--serial", action="store_true",
                     help="run every layer in network order on one stream (no fire e1/e3 or ResNet c1/ds overlap)")
     return ap.parse_args()
@@ -174,7 +177,14 @@ def main():
         __graft_entry__.build()
     if world > 1:
         dist.barrier()
+    if args.net == "ntt_sweep":
+        return run_ntt_sweep_line(args, world, rank, local, dev)
     out = run_secn(args, args.word_bits, world, rank, local, dev, full=True)
+    if not args.no_sweep:
+        torch.cuda.empty_cache()
+        sw = ntt_sweep(args, world, local, dev, word_bits=(args.word_bits,), steps=10)
+        if rank == 0:
+            out["ntt_sweep"] = sw
     if not args.no_companion:
         other = 64 if args.word_bits == 32 else 32
         torch.cuda.empty_cache()
@@ -182,6 +192,72 @@ def main():
         if rank == 0:
             out["companion"] = comp
     if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+SWEEP_PRIMES = {64: (0xFFFFFFFFFFC0001, 0xFFFFFFFFF840001, 0xFFFFFFFFF6A0001, 0xFFFFFFFFF5A0001),
+                32: (0x7E90001, 0x7E00001, 0x7DD0001, 0x7D70001)}  # = 1 mod 2^16: every N <= 2^15
+
+
+def ntt_sweep(args, world, local, dev, word_bits=(32, 64), steps=20, logns=(12, 13, 14, 15), limbs=(1, 2, 3, 4)):
+    """batched RNS NTT / INTT over N = 2^12..2^15 and 1..4 limbs, each call on
+    a batch of >= 1 GiB of uniform residues (independent batches per rank). Device time per call
+    from CUDA-graph replays (max over ranks); NTT/s counts limb-poly transforms (all ranks)."""
+    from paper_2506_11586_b200 import Context
+
+    hbm_peak, _ = peaks()
+    gib = 1 << 30
+    buf = torch.empty(gib // 8, dtype=torch.int64, device=dev)
+    g = torch.Generator(device=dev)
+    g.manual_seed(5)
+    rows = []
+    for wb in word_bits:
+        wbytes = wb // 8
+        for logn in logns:
+            for L in limbs:
+                primes = SWEEP_PRIMES[wb][:L]
+                ctx = Context(local, log_n=logn, primes=primes, word_bits=wb)
+                n = 1 << logn
+                n_polys = max(1, gib // (n * wbytes * L))
+                words = n_polys * L * n
+                t = buf.view(torch.int32 if wb == 32 else torch.int64)[:words].view(n_polys, L, n)
+                t.random_(0, min(primes), generator=g)
+                res = {"word_bits": wb, "N": n, "L": L, "limb_polys": n_polys * L}
+                for name, fn in (("fwd", ctx.ntt_fwd), ("inv", ctx.ntt_inv)):
+                    ms = graph_ms(lambda: fn(t), steps, 3, dev, world)
+                    res[name + "_us"] = round(ms * 1e3, 2)
+                    res[name + "_ntt_per_s"] = round(n_polys * L * world / (ms / 1e3), 1)
+                    gbps = 2 * words * wbytes / (ms / 1e3) / 1e9
+                    res[name + "_hbm_frac"] = round(gbps / hbm_peak, 4)
+                rows.append(res)
+                ctx.close()
+    del buf
+    torch.cuda.empty_cache()
+    return rows
+
+
+def run_ntt_sweep_line(args, world, rank, local, dev):
+    """`--net ntt_sweep`: the C5 configuration as its own bench line. value = forward NTT/s at
+    N = 4096 with four 27-bit limbs (all ranks); the full grid is under "sweep"."""
+    if rank == 0:
+        import __graft_entry__  # noqa: F401  (built by main)
+    with ClockSampler(local) as clk:
+        rows = ntt_sweep(args, world, local, dev, word_bits=(32, 64), steps=args.steps)
+    head = next(r for r in rows if r["word_bits"] == args.word_bits and r["N"] == 4096 and r["L"] == (4 if args.word_bits == 32 else 2))
+    if rank == 0:
+        out = {"metric": "batched RNS NTT throughput (limb-poly transforms/s)", "value": head["fwd_ntt_per_s"],
+               "unit": "NTT/s", "n_gpus": world, "steps": args.steps, "warmup": 3,
+               "ms_per_step": round(head["fwd_us"] / 1e3, 4), "higher_is_better": True, "scaling": "weak",
+               "vs_baseline": None, "dtype": f"u{args.word_bits}", "data": "synthetic uniform residues",
+               "config": {"workload": "ntt_sweep: N=2^12..2^15 x L=1..4, >= 1 GiB per call (BASELINE.json configs[4])",
+                          "headline": f"N=4096, L={head['L']}, {args.word_bits}-bit limbs, forward",
+                          "l2": "1 GiB per call >> 126 MB L2"},
+               "roofline": {"bound": "hbm", "achieved": round(head["fwd_hbm_frac"] * peaks()[0], 1), "peak": peaks()[0],
+                            "unit": "GB/s", "frac": head["fwd_hbm_frac"], "traffic": None},
+               "gpu_launches": args.steps, "clocks": clk.summary(), "sweep": rows}
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.barrier()
@@ -319,6 +395,9 @@ def run_secn(args, word_bits, world, rank, local, dev, full):
     # ---- e2e: host buffers, H2D + public API + D2H every step ----
     e2e = None if args.no_e2e else run_e2e(ctx, st, K, dev, share_buf, world, runner)
 
+    # ---- f4: online NTT preprocessing (weights in coefficient form, transformed in each call) ----
+    online = None if args.no_online else run_online(ctx, st, K, args.warmup, dev, world, runner)
+
     if rank != 0:
         return None
 
@@ -357,7 +436,7 @@ def run_secn(args, word_bits, world, rank, local, dev, full):
         "per_layer_stage_us": stage_profile.per_layer_us,
         "gpu_launches": launches_per_step * K,
         "clocks": clk.summary(),
-        "e2e": e2e,
+        "e2e": e2e, "online_ntt_preprocessing": online,
         "context": {"paper_gpu_online_s": 2.26, "paper_gpu_hw": "RTX A6000 + Troy (PAPER.md:476)",
                     "paper_cpu_online_s": 3.09},
     }
@@ -406,6 +485,60 @@ def stage_profile(ctx, st, K, dev):
                     per_layer[d["lay"].name][s] += dt
     stage_profile.per_layer_us = {k: [round(v * 1e3 / K, 1) for v in vs] for k, vs in per_layer.items()}
     return [x / K for x in tot]
+
+
+def graph_ms(fn, K, warmup, dev, world):
+    """Captures fn() in a CUDA graph and returns the device ms per replay (max over ranks)."""
+    for _ in range(max(warmup, 3)):
+        fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    cap = torch.cuda.Stream(dev)
+    cap.wait_stream(torch.cuda.current_stream(dev))
+    with torch.cuda.graph(g, stream=cap):
+        fn()
+    torch.cuda.synchronize()
+    for _ in range(max(warmup, 3)):
+        g.replay()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    a.record()
+    for _ in range(K):
+        g.replay()
+    b.record()
+    torch.cuda.synchronize()
+    ms = torch.tensor([a.elapsed_time(b) / K], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    del g
+    return float(ms.item())
+
+
+def run_online(ctx, st, K, warmup, dev, world, runner):
+    """SURVEY.md §8f row 4 / PAPER.md:433, :498: the same step with the weights held in coefficient
+    form (the tiny quantised kernels) and packed + transformed inside every secn32_he_conv2d_online
+    call, instead of the offline-preprocessed NTT-domain weights."""
+    for d in st:
+        if d["mc"] > 0:
+            d["ws_on"] = torch.empty((ctx.online_workspace_bytes(d["pl"]) + 7) // 8, dtype=torch.int64, device=dev)
+
+    def layer_online(i):
+        d = st[i]
+        if d["mc"] > 0:
+            ctx.he_conv2d_online(d["pl"], d["ct"], d["K"], x0=d["x0"], r=d["r"], out=d["out"], workspace=d["ws_on"],
+                                 y0=d["y0"])
+
+    ms = graph_ms(lambda: runner(layer_online), K, warmup, dev, world)
+    for d in st:
+        d.pop("ws_on", None)
+    torch.cuda.empty_cache()
+    held = sum(d["K"].numel() * 8 for d in st if d["mc"] > 0)
+    return {"value": round(ms / 1e3, 7), "unit": "s", "ms_per_step": round(ms, 4),
+            "weights_held_bytes": held, "weights_held_offline_bytes": sum(d["w"].numel() * d["w"].element_size()
+                                                                            for d in st if d["mc"] > 0),
+            "path": "secn_he_conv2d_online: pack + NTT of the weights, then share add + NTT, MAC, INTT + mask"}
 
 
 def run_e2e(ctx, st, K, dev, share_buf, world, runner):

@@ -85,9 +85,11 @@ typedef struct {
 
 /* Creates a context on CUDA device `device`: copies the primes, finds psi_j, and builds the
  * device tables (psi^brv(i) and psi^-brv(i) with Shoup companions, N^-1, floor(Q/t) mod q_j,
- * Q mod t). Supported: 12 <= log_n <= 14, 1 <= n_limbs <= 4, every prime q_j < 2^61 with
+ * Q mod t). Supported: 12 <= log_n <= 15, 1 <= n_limbs <= 4, every prime q_j < 2^61 with
  * q_j = 1 (mod 2N) (probable-prime tested), distinct; 1 <= t_bits <= 44.
- * Returns SECN_EUNSUPPORTED otherwise, SECN_ENOMEM / SECN_ECUDA on device failure. */
+ * log_n = 15 (the NTT sweep's largest ring) serves the NTT / mask / share
+ * calls only: secn_preprocess_weights and the secn_he_conv2d family return SECN_EUNSUPPORTED
+ * for it. Returns SECN_EUNSUPPORTED otherwise, SECN_ENOMEM / SECN_ECUDA on device failure. */
 int secn_ctx_create(secn_ctx** out, int device, uint32_t log_n, uint32_t n_limbs, const uint64_t* primes,
                     uint32_t t_bits);
 int secn_ctx_destroy(secn_ctx* ctx);
@@ -102,7 +104,8 @@ const char* secn_last_error(void);
 int secn_conv_plan(uint32_t log_n, uint32_t coef_words64, secn_conv_plan_t* p);
 
 /* A1: in-place forward negacyclic NTT of n_polys polys [n_polys][L][N] (coefficient domain ->
- * NTT domain), PAPER.md:378-380 (§6.2), App. C.1. */
+ * NTT domain), PAPER.md:378-380 (§6.2), App. C.1. At N = 2^15 (and 64-bit words at 2^14) each
+ * limb-poly is transformed by a cluster of two CTAs (cluster NTT). */
 int secn_ntt_fwd(secn_ctx* ctx, uint64_t* polys, size_t n_polys, void* stream);
 
 /* A2: in-place inverse of secn_ntt_fwd, N^-1 included. */
@@ -161,6 +164,18 @@ int secn_he_conv2d_ex(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_
                       const uint64_t* w_ntt, const uint64_t* r, uint64_t* ct_out, uint64_t* y0, void* workspace,
                       size_t ws_bytes, void* stream);
 
+/* Online NTT preprocessing ("linear layers with
+ * online/offline/no NTT preprocessing"): the same result as secn_preprocess_weights followed by
+ * secn_he_conv2d_ex, in one call, with the kernel in coefficient form ([M][C][kh][kw] uint64
+ * < 2^t_bits, as for secn_preprocess_weights). The transformed weights live in the workspace
+ * (>= secn_he_conv2d_online_workspace bytes, 16-byte aligned), so nothing query-independent
+ * is kept between calls: the server trades the weight bytes it would hold for an NTT per query.
+ * y0 may be NULL. Errors as for secn_preprocess_weights and secn_he_conv2d_ex. */
+size_t secn_he_conv2d_online_workspace(const secn_ctx* ctx, const secn_conv_plan_t* plan);
+int secn_he_conv2d_online(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* ct_in, const uint64_t* x0,
+                          const uint64_t* kernel, const uint64_t* r, uint64_t* ct_out, uint64_t* y0, void* workspace,
+                          size_t ws_bytes, void* stream);
+
 /* Server's output share at the designated coefficients (§7; Cheetah's sparse
  * result): y0[m][oy][ox] = (t - r[m*S+s][O + i*Ww + j]) mod t for the plan's
  * index map, m in [0, plan->M). r [M*S][N], y0 [M][OH][OW]. */
@@ -190,6 +205,9 @@ int secn32_he_conv2d(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint32_t
 int secn32_he_conv2d_ex(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint32_t* ct_in, const uint64_t* x0,
                         const uint32_t* w_ntt, const uint64_t* r, uint32_t* ct_out, uint64_t* y0, void* workspace,
                         size_t ws_bytes, void* stream);
+int secn32_he_conv2d_online(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint32_t* ct_in, const uint64_t* x0,
+                            const uint64_t* kernel, const uint64_t* r, uint32_t* ct_out, uint64_t* y0,
+                            void* workspace, size_t ws_bytes, void* stream);
 int secn32_he_conv2d_stage(secn_ctx* ctx, const secn_conv_plan_t* plan, int stage, const uint32_t* ct_in,
                            const uint64_t* x0, const uint32_t* w_ntt, const uint64_t* r, uint32_t* ct_out,
                            void* workspace, size_t ws_bytes, void* stream);

@@ -182,7 +182,7 @@ static int ctx_create_impl(secn_ctx** out, int device, uint32_t log_n, uint32_t 
                            uint32_t t_bits, uint32_t word_bits) {
   if (!out || !primes) return fail(SECN_EINVAL, "NULL argument");
   *out = nullptr;
-  if (log_n < 12 || log_n > 14) return fail(SECN_EUNSUPPORTED, "log_n=%u not in [12,14]", log_n);
+  if (log_n < 12 || log_n > 15) return fail(SECN_EUNSUPPORTED, "log_n=%u not in [12,15]", log_n);
   if (n_limbs < 1 || n_limbs > SECN_MAX_LIMBS) return fail(SECN_EUNSUPPORTED, "n_limbs=%u not in [1,4]", n_limbs);
   if (t_bits < 1 || t_bits > 44) return fail(SECN_EUNSUPPORTED, "t_bits=%u not in [1,44]", t_bits);
   const uint64_t n = 1ull << log_n;
@@ -216,7 +216,10 @@ static int ctx_create_impl(secn_ctx** out, int device, uint32_t log_n, uint32_t 
   auto comp = [&](uint64_t w, uint64_t q) {
     return word_bits == 64 ? shoup_companion(w, q) : (uint64_t)((((u128)w) << 32) / q);
   };
-  const size_t tw_bytes = (word_bits == 64 ? sizeof(ulonglong2) : sizeof(uint2)) * 2 * n_limbs * n;
+  // full tables [2][L][N] (fwd, inv); for the cluster NTT (N = 2^15, or 64-bit words at 2^14)
+  // also the per-half tables [2][L][2][N/2]
+  const bool halves = log_n == 15 || (log_n == 14 && word_bits == 64);
+  const size_t tw_bytes = (word_bits == 64 ? sizeof(ulonglong2) : sizeof(uint2)) * 2 * n_limbs * n * (halves ? 2 : 1);
   std::vector<unsigned char> tw(tw_bytes);
   ulonglong2* tw64 = reinterpret_cast<ulonglong2*>(tw.data());
   uint2* tw32 = reinterpret_cast<uint2*>(tw.data());
@@ -255,6 +258,24 @@ static int ctx_create_impl(secn_ctx** out, int device, uint32_t log_n, uint32_t 
     const uint64_t r64 = (uint64_t)(((u128)1 << 64) % q);
     dc.r64[j] = r64, dc.r64_p[j] = shoup_companion(r64, q);
     dc.one_p[j] = ~0ull / q;
+    dc.one_wp[j] = comp(1, q);
+    if (halves) {  // half tables: th[k] = t[k + hp2(k) (1 + h)] (see DevConsts)
+      const size_t nh = n / 2, base = 2 * (size_t)n_limbs * n;
+      for (uint32_t h = 0; h < 2; ++h)
+        for (uint32_t k = 0; k < nh; ++k) {
+          uint32_t hp2 = 1;
+          while (k && hp2 * 2 <= k) hp2 *= 2;
+          const size_t src = k ? k + (size_t)hp2 * (1 + h) : 0;
+          for (uint32_t dir = 0; dir < 2; ++dir) {
+            const size_t from = ((size_t)dir * n_limbs + j) * n + src;
+            const size_t to = base + (((size_t)dir * n_limbs + j) * 2 + h) * nh + k;
+            if (word_bits == 64)
+              tw64[to] = tw64[from];
+            else
+              tw32[to] = tw32[from];
+          }
+        }
+    }
   }
   cudaError_t e = cudaMalloc(&c->d_tables, tw_bytes);
   if (e != cudaSuccess) {
@@ -271,9 +292,12 @@ static int ctx_create_impl(secn_ctx** out, int device, uint32_t log_n, uint32_t 
   if (word_bits == 64) {
     dc.tw_fwd = static_cast<const ulonglong2*>(c->d_tables);
     dc.tw_inv = dc.tw_fwd + (size_t)n_limbs * n;
+    if (halves) dc.tw_fwd_h = dc.tw_fwd + 2 * (size_t)n_limbs * n, dc.tw_inv_h = dc.tw_fwd_h + (size_t)n_limbs * n;
   } else {
     dc.tw32_fwd = static_cast<const uint2*>(c->d_tables);
     dc.tw32_inv = dc.tw32_fwd + (size_t)n_limbs * n;
+    if (halves)
+      dc.tw32_fwd_h = dc.tw32_fwd + 2 * (size_t)n_limbs * n, dc.tw32_inv_h = dc.tw32_fwd_h + (size_t)n_limbs * n;
   }
   *out = c;
   return SECN_OK;
@@ -368,6 +392,7 @@ static int preprocess_impl(secn_ctx* ctx, uint32_t bits, const secn_conv_plan_t*
   if (int st = check_ctx(ctx, bits)) return st;
   if (int st = check_plan(ctx, plan)) return st;
   if (!kernel || !w_ntt) return fail(SECN_EINVAL, "NULL buffer");
+  if (ctx->log_n > 14) return fail(SECN_EUNSUPPORTED, "convolutions need log_n <= 14 (N = 2^15 is NTT-only)");
   DeviceGuard guard(ctx->device);
   cudaStream_t s = (cudaStream_t)stream;
   const size_t kw = (size_t)plan->M * plan->C * plan->kh * plan->kw;
@@ -436,6 +461,7 @@ static int he_conv2d_impl(secn_ctx* ctx, uint32_t bits, const secn_conv_plan_t* 
   if (int st = check_plan(ctx, plan)) return st;
   if (stage < -1 || stage > 2) return fail(SECN_EINVAL, "stage %d not in {0,1,2}", stage);
   if (!ct_in || !w_ntt || !ct_out || !workspace) return fail(SECN_EINVAL, "NULL buffer");
+  if (ctx->log_n > 14) return fail(SECN_EUNSUPPORTED, "convolutions need log_n <= 14 (N = 2^15 is NTT-only)");
   if (y0 && !r) return fail(SECN_EINVAL, "y0 needs the mask r");
   if (ws_bytes < secn_he_conv2d_workspace(ctx, plan)) return fail(SECN_EINVAL, "workspace too small");
   if (((uintptr_t)workspace | (uintptr_t)ct_in | (uintptr_t)ct_out | (uintptr_t)w_ntt) & 15)
@@ -476,6 +502,43 @@ int secn32_he_conv2d_ex(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint3
                         const uint32_t* w_ntt, const uint64_t* r, uint32_t* ct_out, uint64_t* y0, void* workspace,
                         size_t ws_bytes, void* stream) {
   return he_conv2d_impl(ctx, 32, plan, -1, ct_in, x0, w_ntt, r, ct_out, y0, workspace, ws_bytes, stream);
+}
+
+// f4 ("online/offline/no NTT preprocessing"): the weights arrive in
+// coefficient form and are packed + transformed inside the online call, into workspace scratch
+// after X^; then the same three launches as secn_he_conv2d_ex.
+static size_t xhat_bytes_aligned(const secn_ctx* ctx, const secn_conv_plan_t* plan) {
+  return (secn_he_conv2d_workspace(ctx, plan) + 255) & ~(size_t)255;
+}
+
+size_t secn_he_conv2d_online_workspace(const secn_ctx* ctx, const secn_conv_plan_t* plan) {
+  if (!ctx || !plan) return 0;
+  return xhat_bytes_aligned(ctx, plan) + (size_t)plan->M * plan->G * ctx->L * ctx->n * (ctx->word_bits / 8);
+}
+
+static int he_conv2d_online_impl(secn_ctx* ctx, uint32_t bits, const secn_conv_plan_t* plan, const void* ct_in,
+                                 const uint64_t* x0, const uint64_t* kernel, const uint64_t* r, void* ct_out,
+                                 uint64_t* y0, void* workspace, size_t ws_bytes, void* stream) {
+  if (int st = check_ctx(ctx, bits)) return st;
+  if (int st = check_plan(ctx, plan)) return st;
+  if (!workspace || !kernel) return fail(SECN_EINVAL, "NULL buffer");
+  if (ws_bytes < secn_he_conv2d_online_workspace(ctx, plan)) return fail(SECN_EINVAL, "workspace too small");
+  void* w_ntt = static_cast<unsigned char*>(workspace) + xhat_bytes_aligned(ctx, plan);
+  if (int st = preprocess_impl(ctx, bits, plan, kernel, w_ntt, stream)) return st;
+  return he_conv2d_impl(ctx, bits, plan, -1, ct_in, x0, w_ntt, r, ct_out, y0, workspace, xhat_bytes_aligned(ctx, plan),
+                        stream);
+}
+
+int secn_he_conv2d_online(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* ct_in, const uint64_t* x0,
+                          const uint64_t* kernel, const uint64_t* r, uint64_t* ct_out, uint64_t* y0, void* workspace,
+                          size_t ws_bytes, void* stream) {
+  return he_conv2d_online_impl(ctx, 64, plan, ct_in, x0, kernel, r, ct_out, y0, workspace, ws_bytes, stream);
+}
+
+int secn32_he_conv2d_online(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint32_t* ct_in, const uint64_t* x0,
+                            const uint64_t* kernel, const uint64_t* r, uint32_t* ct_out, uint64_t* y0,
+                            void* workspace, size_t ws_bytes, void* stream) {
+  return he_conv2d_online_impl(ctx, 32, plan, ct_in, x0, kernel, r, ct_out, y0, workspace, ws_bytes, stream);
 }
 
 int secn_he_conv2d_stage(secn_ctx* ctx, const secn_conv_plan_t* plan, int stage, const uint64_t* ct_in,

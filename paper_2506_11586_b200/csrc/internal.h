@@ -30,6 +30,13 @@ struct DevConsts {
   const ulonglong2* tw_inv;  // [L][N] (psi^-brv(i), w')
   const uint2* tw32_fwd;     // [L][N]                        word_bits = 32
   const uint2* tw32_inv;
+  // N = 2^15 only: per-half tables [L][2][N/2] for the two 2^14-point halves of the cluster NTT:
+  // th[k] = t[k + hp2(k) (1 + h)], hp2(k) = the largest power of two <= k (k >= 1)
+  const ulonglong2* tw_fwd_h;
+  const ulonglong2* tw_inv_h;
+  const uint2* tw32_fwd_h;
+  const uint2* tw32_inv_h;
+  uint64_t one_wp[SECN_MAX_LIMBS];  // word-sized Shoup companion of 1
 };
 
 struct PlanDev {  // the subset of secn_conv_plan the kernels use

@@ -28,12 +28,16 @@ struct Tab<Arith64> {
   __device__ static const ulonglong2* fwd(const DevConsts& c) { return c.tw_fwd; }
   __device__ static const ulonglong2* inv(const DevConsts& c) { return c.tw_inv; }
   __device__ static ulonglong2 pair(uint64_t w, uint64_t wp) { return make_ulonglong2(w, wp); }
+  __device__ static const ulonglong2* fwd_half(const DevConsts& c) { return c.tw_fwd_h; }
+  __device__ static const ulonglong2* inv_half(const DevConsts& c) { return c.tw_inv_h; }
 };
 template <>
 struct Tab<Arith32> {
   __device__ static const uint2* fwd(const DevConsts& c) { return c.tw32_fwd; }
   __device__ static const uint2* inv(const DevConsts& c) { return c.tw32_inv; }
   __device__ static uint2 pair(uint64_t w, uint64_t wp) { return make_uint2((uint32_t)w, (uint32_t)wp); }
+  __device__ static const uint2* fwd_half(const DevConsts& c) { return c.tw32_fwd_h; }
+  __device__ static const uint2* inv_half(const DevConsts& c) { return c.tw32_inv_h; }
 };
 
 // enc_j(v) = round(Q v / t) mod q_j (reading R2), computed through the identity
@@ -207,6 +211,167 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN, NP>(
         buf[e] = v;
       }
   }
+}
+
+// ------------------------------------------------------------------------------------------
+// Cluster NTT (N = 2^15; and 64-bit words at N = 2^14): at N = 2^15,
+// T = N/16 = 2048 threads would exceed a CTA and 64-bit words need 272 KiB of shared memory; at
+// 2^14 a 1024-thread CTA leaves 64 registers per thread, too few for 64-bit words. So a limb-poly
+// is transformed by a CLUSTER of two CTAs of 2^LOGH = N/2 points each. The first CT level (and
+// the last GS level) pairs coefficient e with e + N/2; every other level stays inside one half.
+// CTA h (cluster rank) owns half h and runs the 2^LOGH-point core on it with its own twiddle
+// table th (DevConsts::tw_*_h: the full table's entries of that half's groups).
+
+__device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// generic address of the same shared-memory location in CTA `rank` of the cluster (DSMEM)
+template <class T>
+__device__ __forceinline__ const T* cluster_peer(const T* p, uint32_t rank) {
+  uint64_t out;
+  asm volatile("mapa.u64 %0, %1, %2;" : "=l"(out) : "l"(reinterpret_cast<uint64_t>(p)), "r"(rank));
+  return reinterpret_cast<const T*>(out);
+}
+
+// Forward: CTA h loads both halves (the partner's loads of the same lines hit L2), applies the
+// cross-half level-0 butterfly (twiddle psi^brv(1)) and keeps its half; the share add (x0) is
+// fused as in k_ntt_fwd. In-place calls are safe: no CTA stores before both passed the cluster
+// barrier that follows their loads.
+template <class A, int LOGH>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((1 << LOGH) / 16, 1)
+    k_ntt_fwd_cl(const typename A::W* in, typename A::W* out, const __grid_constant__ DevConsts c,
+                 const uint64_t* __restrict__ x0) {
+  using W = typename A::W;
+  constexpr int NH = 1 << LOGH, N = 2 * NH;
+  using R0 = CtRound<LOGH, 0>;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  W* sm = reinterpret_cast<W*>(smraw);
+  const uint32_t h = cluster_rank();
+  const size_t pl = blockIdx.x >> 1;  // limb-poly
+  const int j = (int)(pl % c.L);
+  const size_t pi = pl / c.L;
+  const W q = (W)c.q[j], qb = A::bound(q);
+  const typename A::Tw* th = Tab<A>::fwd_half(c) + ((size_t)j * 2 + h) * NH;
+  const typename A::Tw w0 = Tab<A>::fwd(c)[(size_t)j * N + 1];
+  const EncK ek(c, j);
+  typename A::Tw tws[15];
+  ct_twiddles<A, LOGH, 0>(tws, th);
+  pdl_wait();
+  const W* src = in + pl * N;
+  const bool share = x0 != nullptr && (pi & 1);
+  const uint64_t* xs = share ? x0 + (pi >> 1) * N : nullptr;
+  W x[1][16];
+#pragma unroll
+  for (int k = 0; k < R0::NT; ++k)
+#pragma unroll
+    for (int i = 0; i < R0::GK; ++i) {
+      const uint32_t e = R0::addr(k, i);
+      W a = src[e], b = src[e + NH];
+      if (share) {
+        a += enc_mod<A>(__ldg(&xs[e]), ek);
+        b += enc_mod<A>(__ldg(&xs[e + NH]), ek);
+      }
+      A::ct(a, b, w0, q, qb);
+      x[0][k * R0::GK + i] = h ? b : a;
+    }
+  cluster_arrive();  // this CTA's global reads are done
+  ct_compute<A, LOGH, 0, 1>(x, tws, q, qb);
+  round_store<R0, W, 1, LOGH>(x, sm);
+  ct_rounds_smem_but_last<A, LOGH, R0::K, 1>(sm, th, q, qb);
+  constexpr int SL = CtLast<LOGH>::value;
+  using RL = CtRound<LOGH, SL>;
+  ct_twiddles<A, LOGH, SL>(tws, th);
+  __syncthreads();
+  round_load<RL, W, 1, LOGH>(x, sm);
+  ct_compute<A, LOGH, SL, 1>(x, tws, q, qb);
+  pdl_trigger();
+#pragma unroll
+  for (int i = 0; i < 16; ++i) x[0][i] = A::canon_ct(x[0][i], q);
+  W* dst[1] = {out + pl * N + h * NH};
+  cluster_wait();  // the partner has read both halves
+  round_gstore<RL, W, 1>(x, dst);
+}
+
+// Inverse: CTA h runs GS levels 0..13 on its half (level 13 with twiddle th[1] and no N^-1),
+// leaves the result in shared memory, and after a cluster barrier reads the partner's half
+// through DSMEM for the cross-half level 14 (with N^-1 folded in, as in k_ntt_inv); then the
+// mask on the b component. A second cluster barrier keeps each CTA's shared memory alive until
+// its partner has read it.
+template <class A, int LOGH>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((1 << LOGH) / 16, 1)
+    k_ntt_inv_cl(typename A::W* polys, const __grid_constant__ DevConsts c, const uint64_t* __restrict__ r) {
+  using W = typename A::W;
+  constexpr int NH = 1 << LOGH, N = 2 * NH, T = NH / 16;
+  constexpr int LL = GsLast<LOGH>::value;
+  using R0 = GsRound<LOGH, 0>;
+  using RL = GsRound<LOGH, LL>;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  W* sm = reinterpret_cast<W*>(smraw);
+  const uint32_t h = cluster_rank();
+  const size_t pl = blockIdx.x >> 1;
+  const int j = (int)(pl % c.L);
+  const size_t pi = pl / c.L;
+  const W q = (W)c.q[j], qb = A::bound(q);
+  const typename A::Tw* th = Tab<A>::inv_half(c) + ((size_t)j * 2 + h) * NH;
+  const typename A::Tw one = Tab<A>::pair(1, c.one_wp[j]);
+  const typename A::Tw w13 = th[1];
+  const typename A::Tw ninv = Tab<A>::pair(c.ninv[j], c.ninv_p[j]);
+  const typename A::Tw wl = Tab<A>::pair(c.wlast[j], c.wlast_p[j]);
+  const EncK ek(c, j);
+  const bool mask = r != nullptr && (pi & 1);
+  const uint64_t* rs = mask ? r + (pi >> 1) * N + h * NH : nullptr;
+  // 32-bit words: the encoded mask is computed up front (16 registers); 64-bit words would need
+  // 32 more registers than the 64 a 1024-thread CTA has, so they encode at the store instead
+  constexpr bool early = sizeof(W) == 4;
+  W em[early ? 16 : 1];
+  if (early && mask) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) em[early ? k : 0] = enc_mod<A>(__ldg(&rs[threadIdx.x + k * T]), ek);
+  }
+  typename A::Tw tws[15];
+  gs_twiddles<A, LOGH, 0>(tws, th);
+  pdl_wait();
+  W* buf = polys + pl * N + h * NH;
+  W x[1][16];
+  {
+    const W* src[1] = {buf};
+    round_gload<R0, W, 1>(x, src);
+  }
+  gs_compute<A, LOGH, 0, 1>(x, tws, q, qb, one, w13);
+  round_store<R0, W, 1, LOGH>(x, sm);
+  gs_rounds_smem_but_last<A, LOGH, R0::K, 1>(sm, th, q, qb, one, w13);
+  gs_twiddles<A, LOGH, LL>(tws, th);
+  __syncthreads();
+  round_load<RL, W, 1, LOGH>(x, sm);
+  gs_compute<A, LOGH, LL, 1>(x, tws, q, qb, one, w13);
+  __syncthreads();  // every thread has read its last-round inputs before they are overwritten
+  round_store<RL, W, 1, LOGH>(x, sm);
+  cluster_arrive();
+  cluster_wait();  // both halves are in shared memory
+  pdl_trigger();
+  const W* peer = cluster_peer(sm, h ^ 1);
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    const uint32_t e = threadIdx.x + k * T, pe = phys(e);
+    const W mine = sm[pe], other = peer[pe];
+    const W u = h ? other : mine, v = h ? mine : other;
+    W o = h ? A::mul4(u - v + qb, wl, q) : A::mul4(u + v, ninv, q);
+    o = A::canon_gs(o, q);
+    if (mask) {
+      if constexpr (early)
+        o += em[k];
+      else
+        o += enc_mod<A>(__ldg(&rs[e]), ek);
+      o = o >= q ? o - q : o;
+    }
+    buf[e] = o;
+  }
+  cluster_arrive();
+  cluster_wait();  // the partner is done reading this CTA's shared memory
 }
 
 // K3' (+A7 fused), the second half of secn_he_conv2d's inverse NTT: levels 8 .. LOGN-1 (with
@@ -816,9 +981,45 @@ cudaError_t launch_ntt_inv_tail(const DevConsts& c, void* polys, size_t P, const
   return cudaErrorInvalidValue;
 }
 
+// Cluster NTT: one cluster of two CTAs per limb-poly (launches of <= 2^30 polys)
+template <class A, int LOGH>
+static cudaError_t ntt_cl(const DevConsts& c, const void* in, void* out, size_t P, const uint64_t* x0,
+                          const uint64_t* r, bool inverse, cudaStream_t s) {
+  using W = typename A::W;
+  constexpr int N = 2 << LOGH, T = (1 << LOGH) / 16;
+  const size_t smem = smem_words<LOGH>() * sizeof(W);
+  static bool attr[2] = {false, false};
+  if (!attr[inverse]) {
+    cudaError_t e = inverse ? cudaFuncSetAttribute(k_ntt_inv_cl<A, LOGH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+                            : cudaFuncSetAttribute(k_ntt_fwd_cl<A, LOGH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr[inverse] = true;
+  }
+  // polys per launch: a multiple of 2L so that the ct index of x0 / r stays (poly / L) / 2
+  const size_t pmax = ((size_t)1 << 30) / (2 * c.L) * (2 * c.L);
+  for (size_t p0 = 0; p0 < P; p0 += pmax) {
+    const size_t np = P - p0 < pmax ? P - p0 : pmax;
+    const size_t off = p0 * N;
+    cudaError_t e;
+    if (inverse)
+      e = launch_pdl(k_ntt_inv_cl<A, LOGH>, dim3((unsigned)(2 * np)), dim3(T), smem, s, static_cast<W*>(out) + off, c,
+                     r ? r + p0 / c.L / 2 * N : nullptr);
+    else
+      e = launch_pdl(k_ntt_fwd_cl<A, LOGH>, dim3((unsigned)(2 * np)), dim3(T), smem, s,
+                     static_cast<const W*>(in) + off, static_cast<W*>(out) + off, c,
+                     x0 ? x0 + p0 / c.L / 2 * N : nullptr);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaGetLastError();
+}
+
 cudaError_t launch_ntt_fwd(const DevConsts& c, const void* in, void* out, size_t P, const uint64_t* x0,
                            cudaStream_t s) {
   if (P == 0) return cudaSuccess;
+  if (c.log_n == 15)
+    return c.word_bits == 64 ? ntt_cl<Arith64, 14>(c, in, out, P, x0, nullptr, false, s)
+                             : ntt_cl<Arith32, 14>(c, in, out, P, x0, nullptr, false, s);
+  if (c.log_n == 14 && c.word_bits == 64) return ntt_cl<Arith64, 13>(c, in, out, P, x0, nullptr, false, s);
   if (c.word_bits == 64) {
     switch (c.log_n) {
       case 12: return ntt_fwd_t<Arith64, 12>(c, in, out, P, x0, s);
@@ -837,6 +1038,10 @@ cudaError_t launch_ntt_fwd(const DevConsts& c, const void* in, void* out, size_t
 
 cudaError_t launch_ntt_inv(const DevConsts& c, void* polys, size_t P, const uint64_t* r, cudaStream_t s) {
   if (P == 0) return cudaSuccess;
+  if (c.log_n == 15)
+    return c.word_bits == 64 ? ntt_cl<Arith64, 14>(c, nullptr, polys, P, nullptr, r, true, s)
+                             : ntt_cl<Arith32, 14>(c, nullptr, polys, P, nullptr, r, true, s);
+  if (c.log_n == 14 && c.word_bits == 64) return ntt_cl<Arith64, 13>(c, nullptr, polys, P, nullptr, r, true, s);
   if (c.word_bits == 64) {
     switch (c.log_n) {
       case 12: return ntt_inv_t<Arith64, 12>(c, polys, P, r, s);

@@ -31,7 +31,8 @@ EXPORTS = ("secn_ctx_create", "secn_ctx_destroy", "secn_ctx_query", "secn_last_e
            "secn_he_conv2d_workspace", "secn_he_conv2d", "secn_he_conv2d_stage", "secn_extract_share",
            "secn32_ctx_create", "secn32_ntt_fwd", "secn32_ntt_inv", "secn32_preprocess_weights",
            "secn32_share_add", "secn32_mask_add", "secn32_he_conv2d", "secn32_he_conv2d_stage",
-           "secn_he_conv2d_ex", "secn32_he_conv2d_ex")
+           "secn_he_conv2d_ex", "secn32_he_conv2d_ex", "secn_he_conv2d_online_workspace",
+           "secn_he_conv2d_online", "secn32_he_conv2d_online")
 
 
 class SecnError(RuntimeError):
@@ -94,10 +95,13 @@ def lib(path=None) -> ctypes.CDLL:
         "secn_he_conv2d": (i, [vp, P, vp, vp, vp, vp, vp, vp, sz, vp]),
         "secn_he_conv2d_stage": (i, [vp, P, i, vp, vp, vp, vp, vp, vp, sz, vp]),
         "secn_he_conv2d_ex": (i, [vp, P, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
+        "secn_he_conv2d_online_workspace": (sz, [vp, P]),
+        "secn_he_conv2d_online": (i, [vp, P, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
         "secn_extract_share": (i, [vp, P, vp, vp, vp]),
         "secn32_ctx_create": (i, [ctypes.POINTER(vp), i, u32, u32, ctypes.POINTER(ctypes.c_uint32), u32]),
     }
-    for f in ("ntt_fwd", "ntt_inv", "preprocess_weights", "share_add", "mask_add", "he_conv2d", "he_conv2d_stage", "he_conv2d_ex"):
+    for f in ("ntt_fwd", "ntt_inv", "preprocess_weights", "share_add", "mask_add", "he_conv2d", "he_conv2d_stage", "he_conv2d_ex",
+              "he_conv2d_online"):
         sig["secn32_" + f] = sig["secn_" + f]
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -249,6 +253,31 @@ class Context:
             _check(self._f("he_conv2d")(*args, *tail))
         else:
             _check(self._f("he_conv2d_ex")(*args, _ptr(y0, (plan.M, plan.OH, plan.OW), "y0"), *tail))
+        return out
+
+    def online_workspace_bytes(self, plan: Plan) -> int:
+        return int(lib().secn_he_conv2d_online_workspace(self._h, ctypes.byref(plan)))
+
+    def he_conv2d_online(self, plan: Plan, ct_in: torch.Tensor, kernel: torch.Tensor,
+                         x0: Optional[torch.Tensor] = None, r: Optional[torch.Tensor] = None,
+                         out: Optional[torch.Tensor] = None, workspace: Optional[torch.Tensor] = None,
+                         y0: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+        """secn_he_conv2d_online: weights in coefficient form (int64 [M][C][kh][kw]), transformed
+        inside the call (online NTT preprocessing)."""
+        L, n = self.L, self.n
+        n_in, n_out = plan.G * plan.S, plan.M * plan.S
+        if out is None:
+            out = self.empty(n_out, 2, L, n)
+        if workspace is None:
+            workspace = torch.empty((self.online_workspace_bytes(plan) + 7) // 8, dtype=torch.int64,
+                                    device=self.device)
+        _check(self._f("he_conv2d_online")(
+            self._h, ctypes.byref(plan), self._rp(ct_in, (n_in, 2, L, n), "ct_in"), _ptr(x0, (n_in, n), "x0"),
+            _ptr(kernel, (plan.M, plan.C, plan.kh, plan.kw), "kernel"), _ptr(r, (n_out, n), "r"),
+            self._rp(out, (n_out, 2, L, n), "ct_out"),
+            _ptr(y0, (plan.M, plan.OH, plan.OW), "y0") if y0 is not None else None,
+            ctypes.c_void_p(workspace.data_ptr()), workspace.numel() * workspace.element_size(),
+            self._stream(stream)))
         return out
 
     def he_conv2d_stage(self, stage: int, plan: Plan, ct_in: torch.Tensor, w_ntt: torch.Tensor,

@@ -82,7 +82,8 @@ def oplan(P, ctx, lay):
 @pytest.mark.parametrize("logn,primes,wb", [(12, params.DEFAULT_PRIMES, 64), (12, params.ALT54_PRIMES, 64),
                                             (12, params.SWEEP_PRIMES, 64), (13, params.SWEEP_PRIMES, 64),
                                             (14, params.SWEEP_PRIMES[:2], 64), (12, params.PRIMES32, 32),
-                                            (14, params.PRIMES32, 32)])
+                                            (14, params.PRIMES32, 32), (15, params.SWEEP_PRIMES, 64),
+                                            (15, params.PRIMES32, 32)])
 def test_ctx_psi_matches_oracle(secn, logn, primes, wb):
     c = secn.Context(0, log_n=logn, primes=primes, word_bits=wb)
     assert c.psi == tuple(Params(logn=logn, primes=primes).psi)
@@ -157,7 +158,8 @@ def test_ntt_pointwise_product_is_negacyclic_product(env):
 
 
 @pytest.mark.parametrize("logn,L,wb", [(12, 4, 64), (13, 1, 64), (13, 3, 64), (14, 2, 64), (14, 4, 64),
-                                       (13, 4, 32), (14, 2, 32)])
+                                       (13, 4, 32), (14, 2, 32),
+                                       (15, 1, 64), (15, 4, 64), (15, 1, 32), (15, 4, 32)])  # 15: cluster NTT
 def test_ntt_sweep_sampled(secn, logn, L, wb):
     primes = (params.SWEEP_PRIMES if wb == 64 else params.PRIMES32)[:L]
     c = secn.Context(0, log_n=logn, primes=primes, word_bits=wb)
@@ -172,6 +174,56 @@ def test_ntt_sweep_sampled(secn, logn, L, wb):
             assert (got[i, j, ks] == he.ntt_sampled(x[i, j], ks, P, j)).all(), (i, j)
     back = D.U(c.ntt_inv(D.R(got)))
     assert (back == x).all()
+    c.close()
+
+
+@pytest.mark.parametrize("wb", [64, 32])
+def test_cluster_ntt_in_place_multi_wave_roundtrip(secn, wb):
+    """N = 2^15 (two-CTA clusters, DSMEM exchange in the inverse): a batch of several waves
+    transformed in place round-trips, and sampled outputs equal direct evaluation."""
+    primes = (params.SWEEP_PRIMES if wb == 64 else params.PRIMES32)[:2]
+    c = secn.Context(0, log_n=15, primes=primes, word_bits=wb)
+    D = Dev(c)
+    P = Params(logn=15, primes=primes)
+    g = inputs.rng(777 + wb)
+    x = inputs.uniform_residues(g, (301,), primes, P.n)
+    t = D.R(x)
+    c.ntt_fwd(t)
+    got = D.U(t)
+    ks = np.concatenate([[0, P.n // 2 - 1, P.n // 2, P.n - 1], g.integers(0, P.n, 12)]).astype(np.uint32)
+    for i in (0, 150, 300):
+        assert (got[i, 1, ks] == he.ntt_sampled(x[i, 1], ks, P, 1)).all(), i
+    c.ntt_inv(t)
+    assert (D.U(t) == x).all()
+    c.close()
+
+
+@pytest.mark.parametrize("logn", [13, 14])
+@pytest.mark.parametrize("wb", [64, 32])
+def test_he_conv2d_other_ring_degrees(secn, logn, wb):
+    """The hot path at N = 2^13 and 2^14 (64-bit words at 2^14 use the cluster forward NTT)."""
+    primes = (params.SWEEP_PRIMES[:2] if wb == 64 else params.PRIMES32)
+    ctx = secn.Context(0, log_n=logn, primes=primes, word_bits=wb)
+    P = Params(logn=logn, primes=primes)
+    D = Dev(ctx)
+    lay = L_("n", 20, 30, 30, 6, 3, 1, 1)
+    opl = packing.plan_conv(lay.C, lay.H, lay.W, lay.M, lay.k, lay.k, lay.stride, lay.pad, P.n, ctx.coef_words64)
+    ct, x0, K, r = _layer_inputs(P, lay, 21, opl)
+    plan = ctx.plan(lay.C, lay.H, lay.W, lay.M, lay.k, stride=lay.stride, pad=lay.pad)
+    w = ctx.preprocess_weights(plan, TP(K))
+    y0 = torch.empty((plan.M, plan.OH, plan.OW), dtype=torch.int64, device=DEV)
+    got = D.U(ctx.he_conv2d(plan, D.R(ct), w, x0=TP(x0), r=TP(r), y0=y0))
+    assert (got == he.server_conv(ct, x0, K, r, opl, P)).all()
+    assert (UP(y0) == packing.extract((P.t - r) % P.t, opl)).all()
+    ctx.close()
+
+
+def test_conv_rejects_n32768(secn):
+    c = secn.Context(0, log_n=15, primes=params.PRIMES32, word_bits=32)
+    plan = c.plan(4, 16, 16, 8, 3, stride=1, pad=1)
+    K = torch.zeros((8, 4, 3, 3), dtype=torch.int64, device=DEV)
+    with pytest.raises(secn.SecnError):
+        c.preprocess_weights(plan, K)
     c.close()
 
 
@@ -356,6 +408,22 @@ def test_he_conv2d_ex_fused_share_matches_oracle(env, lay):
     w = ctx.preprocess_weights(plan, TP(K))
     y0 = torch.full((plan.M, plan.OH, plan.OW), -1, dtype=torch.int64, device=DEV)
     out = D.U(ctx.he_conv2d(plan, D.R(ct), w, x0=TP(x0), r=TP(r), y0=y0))
+    assert (out == he.server_conv(ct, x0, K, r, opl, P)).all()
+    assert (UP(y0) == packing.extract((P.t - r) % P.t, opl)).all()
+
+
+@pytest.mark.parametrize("lay", [layers.tiny()[0], L_("multi_g", 40, 12, 12, 7, 3, 1, 1), L_("ds", 24, 28, 28, 9, 1, 2, 0)],
+                         ids=lambda l: l.name)
+def test_he_conv2d_online_weights_match_oracle(env, lay):
+    """f4 toggle (PAPER.md:433, :498): weights in coefficient form, transformed inside the call;
+    the ciphertexts and the share equal the oracle's (and so the offline-preprocessed path)."""
+    ctx, P, D = env
+    opl = oplan(P, ctx, lay)
+    ct, x0, K, r = _layer_inputs(P, lay, 12, opl)
+    plan = ctx.plan(lay.C, lay.H, lay.W, lay.M, lay.k, stride=lay.stride, pad=lay.pad)
+    y0 = torch.empty((plan.M, plan.OH, plan.OW), dtype=torch.int64, device=DEV)
+    ws = torch.full(((ctx.online_workspace_bytes(plan) + 7) // 8,), -1, dtype=torch.int64, device=DEV)
+    out = D.U(ctx.he_conv2d_online(plan, D.R(ct), TP(K), x0=TP(x0), r=TP(r), y0=y0, workspace=ws))
     assert (out == he.server_conv(ct, x0, K, r, opl, P)).all()
     assert (UP(y0) == packing.extract((P.t - r) % P.t, opl)).all()
 
