@@ -114,18 +114,26 @@ def server_conv(ct_in: np.ndarray, x0: Optional[np.ndarray], K: np.ndarray, r: O
 
     ct_in [G*S][2][L][N], x0 [G*S][N] or None, K (M,C,kh,kw) < 2^t, r [M*S][N] or None.
     Returns [M*S][2][L][N]; with `sel` ([M*S] bool) only the selected outputs are computed."""
-    kp = kernel_polys(K, plan, P.n)
+    return server_mac(ct_in, x0, kernel_polys(K, plan, P.n), r, plan.G, plan.S, plan.M, P, sel, out)
+
+
+def server_mac(ct_in: np.ndarray, x0: Optional[np.ndarray], kp: np.ndarray, r: Optional[np.ndarray],
+               G: int, S: int, M: int, P: Params, sel: Optional[np.ndarray] = None,
+               out: Optional[np.ndarray] = None) -> np.ndarray:
+    """The server's linear-layer computation for any packing:
+    out[m,s] = sum_{g<G} (in[g,s] + enc(x0[g,s]) on b) (*) lift(kp[m,g])  (+ enc(r[m,s]) on b),
+    with kp [M][G][N] the raw plaintext polys (values < 2^t, centred-lifted per limb)."""
     koff, kidx, kval = sparse(kp)
     ct_in = np.ascontiguousarray(ct_in, dtype=np.uint64)
-    assert ct_in.shape == (plan.G * plan.S, 2, P.L, P.n), ct_in.shape
+    assert ct_in.shape == (G * S, 2, P.L, P.n), ct_in.shape
     if out is None:
-        out = np.zeros((plan.M * plan.S, 2, P.L, P.n), dtype=np.uint64)
+        out = np.zeros((M * S, 2, P.L, P.n), dtype=np.uint64)
     x0c = None if x0 is None else np.ascontiguousarray(x0, dtype=np.uint64)
     rc = None if r is None else np.ascontiguousarray(r, dtype=np.uint64)
     selc = None if sel is None else np.ascontiguousarray(sel, dtype=np.uint8)
     _c.lib().orc_he_conv_server(P.logn, P.L, np.array(P.primes, dtype=np.uint64), P.t_bits,
                                 np.array(P.delta_mod_q, dtype=np.uint64), P.q_mod_t,
-                                plan.G, plan.S, plan.M, ct_in, _c.ptr_or_null(x0c), koff, kidx, kval,
+                                G, S, M, ct_in, _c.ptr_or_null(x0c), koff, kidx, kval,
                                 _c.ptr_or_null(rc), _c.ptr_or_null(selc), out)
     return out
 
