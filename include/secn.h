@@ -182,6 +182,42 @@ int secn_he_conv2d_online(secn_ctx* ctx, const secn_conv_plan_t* plan, const uin
 int secn_extract_share(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* r, uint64_t* y0, void* stream);
 
 /* ------------------------------------------------------------------------------------------
+ * HE fully-connected layer / matrix-vector product (§6
+ * "fully-connected/matrix multiplication layers"; SPEC.md:612-619 fc_secure). The server's work
+ * is the convolution's -- share add + NTT of the input cts, NTT-domain MAC over input blocks,
+ * inverse NTT + mask -- with the matrix-vector packing of DESIGN.md reading R15:
+ *   input ct g:           coeff[i]                   = x[g*nib + i]                 (i < nib)
+ *   weight poly (m, g):   coeff[j*nib + nib - 1 - i] = W[m*nob + j][g*nib + i]      (j < nob)
+ *   output ct m holds y[m*nob + j] at coefficient j*nib + nib - 1.
+ * ------------------------------------------------------------------------------------------ */
+typedef struct {
+  uint32_t n_i, n_o; /* matrix W: n_o rows x n_i columns (caller)                                */
+  uint32_t nib;      /* input values per ct: 0 = choose (byte-min rule R15); else validated      */
+  uint32_t nob;      /* filled: output rows per ct = min(n_o, N / nib)                            */
+  uint32_t G, M;     /* filled: input cts ceil(n_i/nib), output cts ceil(n_o/nob)                 */
+} secn_fc_plan_t;
+
+/* Host only: fills nob, G, M (and nib when 0) for ring degree 2^log_n; coef_words64 as for
+ * secn_conv_plan. SECN_EINVAL for n_i or n_o = 0 or an invalid nib (0 < nib <= min(n_i, N)). */
+int secn_fc_plan(uint32_t log_n, uint32_t coef_words64, secn_fc_plan_t* p);
+
+/* Offline NTT preprocessing of the matrix: W [n_o][n_i] uint64 (< 2^t_bits, two's complement
+ * mod 2^t) -> w_ntt [M][G][L][N] (NTT domain, centred lift per limb, reading R3). */
+int secn_fc_preprocess_weights(secn_ctx* ctx, const secn_fc_plan_t* plan, const uint64_t* W, uint64_t* w_ntt,
+                               void* stream);
+
+/* Workspace bytes for secn_he_fc (the NTT-domain inputs, G*2*L*N words). */
+size_t secn_he_fc_workspace(const secn_ctx* ctx, const secn_fc_plan_t* plan);
+
+/* One FC layer: ct_in [G][2][L][N] (coefficient domain, read only), x0 [G][N] or NULL (the
+ * server's input share, packed like x), w_ntt from secn_fc_preprocess_weights, r [M][N] or NULL,
+ * ct_out [M][2][L][N] (overwritten), y0 [n_o] or NULL (needs r): the server's output share
+ * (t - r[m][j*nib + nib - 1]) mod t. SECN_EUNSUPPORTED if G > 32 or log_n > 14. */
+int secn_he_fc(secn_ctx* ctx, const secn_fc_plan_t* plan, const uint64_t* ct_in, const uint64_t* x0,
+               const uint64_t* w_ntt, const uint64_t* r, uint64_t* ct_out, uint64_t* y0, void* workspace,
+               size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------------------------------
  * 32-bit RNS limbs (reading R1b). Identical semantics to the
  * calls above with residues stored as uint32 ([..][L][N] uint32 words) for moduli q_j < 2^28,
  * e.g. four 27-bit primes = 1 mod 2^16 (Q = 108 bits <= 109, the 128-bit-security bound for
@@ -208,6 +244,11 @@ int secn32_he_conv2d_ex(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint3
 int secn32_he_conv2d_online(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint32_t* ct_in, const uint64_t* x0,
                             const uint64_t* kernel, const uint64_t* r, uint32_t* ct_out, uint64_t* y0,
                             void* workspace, size_t ws_bytes, void* stream);
+int secn32_fc_preprocess_weights(secn_ctx* ctx, const secn_fc_plan_t* plan, const uint64_t* W, uint32_t* w_ntt,
+                                 void* stream);
+int secn32_he_fc(secn_ctx* ctx, const secn_fc_plan_t* plan, const uint32_t* ct_in, const uint64_t* x0,
+                 const uint32_t* w_ntt, const uint64_t* r, uint32_t* ct_out, uint64_t* y0, void* workspace,
+                 size_t ws_bytes, void* stream);
 int secn32_he_conv2d_stage(secn_ctx* ctx, const secn_conv_plan_t* plan, int stage, const uint32_t* ct_in,
                            const uint64_t* x0, const uint32_t* w_ntt, const uint64_t* r, uint32_t* ct_out,
                            void* workspace, size_t ws_bytes, void* stream);

@@ -121,7 +121,7 @@ int check_range(secn_ctx* ctx, const void* v, size_t n_words, int kind, cudaStre
 }
 
 secn::PlanDev plan_dev(const secn_conv_plan_t* p) {
-  secn::PlanDev d;
+  secn::PlanDev d{};
   d.M = p->M, d.G = p->G, d.S = p->S, d.Cw = p->Cw, d.Hw = p->Hw, d.Ww = p->Ww, d.kh = p->kh, d.kw = p->kw;
   d.C = p->C, d.O = p->O, d.OH = p->OH, d.OW = p->OW, d.nbh = p->nbh, d.nbw = p->nbw;
   d.sh = p->decim ? 1 : p->stride;
@@ -539,6 +539,111 @@ int secn32_he_conv2d_online(secn_ctx* ctx, const secn_conv_plan_t* plan, const u
                             const uint64_t* kernel, const uint64_t* r, uint32_t* ct_out, uint64_t* y0,
                             void* workspace, size_t ws_bytes, void* stream) {
   return he_conv2d_online_impl(ctx, 32, plan, ct_in, x0, kernel, r, ct_out, y0, workspace, ws_bytes, stream);
+}
+
+// ---- f3: fully connected (matrix-vector) layers ----
+
+int secn_fc_plan(uint32_t log_n, uint32_t coef_words64, secn_fc_plan_t* p) {
+  if (!p) return fail(SECN_EINVAL, "NULL plan");
+  if (log_n < 1 || log_n > 20 || coef_words64 < 1) return fail(SECN_EUNSUPPORTED, "bad log_n / coef_words64");
+  if (!p->n_i || !p->n_o) return fail(SECN_EINVAL, "empty matrix");
+  const uint64_t n = 1ull << log_n, lim = p->n_i < n ? p->n_i : n;
+  if (p->nib > lim) return fail(SECN_EINVAL, "nib=%u not in [1, min(n_i, N)]", p->nib);
+  // reading R15: minimise 8 W N (2G + MG + 2M) + 8 N M; ties: fewer MG, then larger nib
+  u128 best_cost = 0, best_mg = 0;
+  uint32_t best = 0;
+  for (uint64_t a = p->nib ? p->nib : 1; a <= (p->nib ? p->nib : lim); ++a) {
+    const uint64_t b = p->n_o < n / a ? p->n_o : n / a;
+    const uint64_t G = (p->n_i + a - 1) / a, M = (p->n_o + b - 1) / b;
+    const u128 cost = (u128)8 * coef_words64 * n * (2 * G + M * G + 2 * M) + (u128)8 * n * M;
+    const u128 mg = (u128)M * G;
+    if (!best || cost < best_cost || (cost == best_cost && (mg < best_mg || (mg == best_mg && a > best)))) {
+      best = (uint32_t)a, best_cost = cost, best_mg = mg;
+    }
+  }
+  p->nib = best;
+  p->nob = p->n_o < n / best ? p->n_o : (uint32_t)(n / best);
+  p->G = (p->n_i + best - 1) / best;
+  p->M = (p->n_o + p->nob - 1) / p->nob;
+  return SECN_OK;
+}
+
+static int check_fc_plan(const secn_ctx* ctx, const secn_fc_plan_t* p) {
+  if (!p) return fail(SECN_EINVAL, "NULL plan");
+  secn_fc_plan_t q = *p;
+  q.nob = q.G = q.M = 0;
+  if (!p->nib || secn_fc_plan(ctx->log_n, 1, &q) != SECN_OK || q.nob != p->nob || q.G != p->G || q.M != p->M)
+    return fail(SECN_EINVAL, "fc plan fields do not match secn_fc_plan() for this matrix and N");
+  if (ctx->log_n > 14) return fail(SECN_EUNSUPPORTED, "fc layers need log_n <= 14 (N = 2^15 is NTT-only)");
+  return SECN_OK;
+}
+
+static secn::PlanDev fc_plan_dev(const secn_fc_plan_t* p) {
+  secn::PlanDev d{};
+  d.kind = 1, d.M = p->M, d.G = p->G, d.S = 1, d.C = p->n_i, d.nib = p->nib, d.nob = p->nob, d.no = p->n_o;
+  return d;
+}
+
+static int fc_preprocess_impl(secn_ctx* ctx, uint32_t bits, const secn_fc_plan_t* plan, const uint64_t* W,
+                              void* w_ntt, void* stream) {
+  if (int st = check_ctx(ctx, bits)) return st;
+  if (int st = check_fc_plan(ctx, plan)) return st;
+  if (!W || !w_ntt) return fail(SECN_EINVAL, "NULL buffer");
+  DeviceGuard guard(ctx->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (int st = check_range(ctx, W, (size_t)plan->n_o * plan->n_i, 1, s, "secn_fc_preprocess_weights W")) return st;
+  const secn::PlanDev pd = fc_plan_dev(plan);
+  cudaError_t e = secn::launch_pack_fc_weights(ctx->dc, pd, W, w_ntt, s);
+  if (e == cudaSuccess) e = secn::launch_ntt_fwd(ctx->dc, w_ntt, w_ntt, (size_t)plan->M * plan->G * ctx->L, nullptr, s);
+  return e == cudaSuccess ? SECN_OK : cuda_fail(e, "secn_fc_preprocess_weights");
+}
+
+size_t secn_he_fc_workspace(const secn_ctx* ctx, const secn_fc_plan_t* plan) {
+  if (!ctx || !plan) return 0;
+  return (size_t)plan->G * 2 * ctx->L * ctx->n * (ctx->word_bits / 8);
+}
+
+static int he_fc_impl(secn_ctx* ctx, uint32_t bits, const secn_fc_plan_t* plan, const void* ct_in, const uint64_t* x0,
+                      const void* w_ntt, const uint64_t* r, void* ct_out, uint64_t* y0, void* workspace,
+                      size_t ws_bytes, void* stream) {
+  if (int st = check_ctx(ctx, bits)) return st;
+  if (int st = check_fc_plan(ctx, plan)) return st;
+  if (!ct_in || !w_ntt || !ct_out || !workspace) return fail(SECN_EINVAL, "NULL buffer");
+  if (y0 && !r) return fail(SECN_EINVAL, "y0 needs the mask r");
+  if (ws_bytes < secn_he_fc_workspace(ctx, plan)) return fail(SECN_EINVAL, "workspace too small");
+  if (((uintptr_t)workspace | (uintptr_t)ct_in | (uintptr_t)ct_out | (uintptr_t)w_ntt) & 15)
+    return fail(SECN_EINVAL, "buffers must be 16-byte aligned");
+  if (plan->G > 32u) return fail(SECN_EUNSUPPORTED, "G=%u input blocks too many", plan->G);
+  DeviceGuard guard(ctx->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t N = ctx->n;
+  if (int st = check_range(ctx, ct_in, (size_t)plan->G * 2 * ctx->L * N, 0, s, "secn_he_fc ct_in")) return st;
+  if (int st = check_range(ctx, x0, (size_t)plan->G * N, 1, s, "secn_he_fc x0")) return st;
+  if (int st = check_range(ctx, r, (size_t)plan->M * N, 1, s, "secn_he_fc r")) return st;
+  const secn::PlanDev pd = fc_plan_dev(plan);
+  cudaError_t e = secn::launch_ntt_fwd(ctx->dc, ct_in, workspace, (size_t)plan->G * 2 * ctx->L, x0, s);
+  if (e == cudaSuccess) e = secn::launch_mac(ctx->dc, pd, workspace, w_ntt, ct_out, s);
+  if (e == cudaSuccess) e = secn::launch_ntt_inv_tail(ctx->dc, ct_out, (size_t)plan->M * 2 * ctx->L, r, y0, pd, s);
+  return e == cudaSuccess ? SECN_OK : cuda_fail(e, "secn_he_fc");
+}
+
+int secn_fc_preprocess_weights(secn_ctx* ctx, const secn_fc_plan_t* plan, const uint64_t* W, uint64_t* w_ntt,
+                               void* stream) {
+  return fc_preprocess_impl(ctx, 64, plan, W, w_ntt, stream);
+}
+int secn32_fc_preprocess_weights(secn_ctx* ctx, const secn_fc_plan_t* plan, const uint64_t* W, uint32_t* w_ntt,
+                                 void* stream) {
+  return fc_preprocess_impl(ctx, 32, plan, W, w_ntt, stream);
+}
+int secn_he_fc(secn_ctx* ctx, const secn_fc_plan_t* plan, const uint64_t* ct_in, const uint64_t* x0,
+               const uint64_t* w_ntt, const uint64_t* r, uint64_t* ct_out, uint64_t* y0, void* workspace,
+               size_t ws_bytes, void* stream) {
+  return he_fc_impl(ctx, 64, plan, ct_in, x0, w_ntt, r, ct_out, y0, workspace, ws_bytes, stream);
+}
+int secn32_he_fc(secn_ctx* ctx, const secn_fc_plan_t* plan, const uint32_t* ct_in, const uint64_t* x0,
+                 const uint32_t* w_ntt, const uint64_t* r, uint32_t* ct_out, uint64_t* y0, void* workspace,
+                 size_t ws_bytes, void* stream) {
+  return he_fc_impl(ctx, 32, plan, ct_in, x0, w_ntt, r, ct_out, y0, workspace, ws_bytes, stream);
 }
 
 int secn_he_conv2d_stage(secn_ctx* ctx, const secn_conv_plan_t* plan, int stage, const uint64_t* ct_in,

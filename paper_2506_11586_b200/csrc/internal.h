@@ -39,8 +39,10 @@ struct DevConsts {
   uint64_t one_wp[SECN_MAX_LIMBS];  // word-sized Shoup companion of 1
 };
 
-struct PlanDev {  // the subset of secn_conv_plan the kernels use
+struct PlanDev {  // the subset of secn_conv_plan (kind 0) / secn_fc_plan (kind 1) the kernels use
   uint32_t M, G, S, Cw, Hw, Ww, kh, kw, C, O, OH, OW, nbh, nbw, sh;
+  uint32_t kind;         // 0: convolution, 1: fully connected (S = 1)
+  uint32_t nib, nob, no; // fc: inputs per ct, output rows per ct, n_o (C holds n_i)
 };
 
 // ---- launchers (kernels.cu); all return cudaGetLastError() after the launch(es) ----
@@ -55,6 +57,8 @@ cudaError_t launch_ntt_inv_tail(const DevConsts& c, void* polys, size_t n_limb_p
 // NTT-domain MAC (A4) followed by inverse-NTT levels 0..7 of its outputs (lazy GS domain)
 cudaError_t launch_mac(const DevConsts& c, const PlanDev& p, const void* xhat, const void* w, void* y, cudaStream_t s);
 cudaError_t launch_pack_weights(const DevConsts& c, const PlanDev& p, const uint64_t* kernel, void* w, cudaStream_t s);
+// fc weights W [n_o][n_i] -> mirrored polys [M][G][L][N] (coefficient domain, zero-filled first)
+cudaError_t launch_pack_fc_weights(const DevConsts& c, const PlanDev& p, const uint64_t* W, void* w, cudaStream_t s);
 cudaError_t launch_enc_add(const DevConsts& c, void* ct, const uint64_t* v, size_t n, cudaStream_t s);
 cudaError_t launch_extract_share(const DevConsts& c, const PlanDev& p, const uint64_t* r, uint64_t* y0,
                                  cudaStream_t s);

@@ -440,7 +440,15 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN, 1>()
   // A8 fused (secn_he_conv2d_ex): the server's output share y0 = -r mod t at the designated
   // coefficients of this ciphertext (one CTA per ciphertext does it: limb 0, b component). It
   // depends on r only, so it never waits on the transform; it saves a launch per layer.
-  if (y0 != nullptr && mask && j == 0) {
+  if (y0 != nullptr && mask && j == 0 && pl.kind == 1) {  // fc: y[m*nob + d] at d*nib + nib - 1
+    const uint32_t m = (uint32_t)(ct0 + (pi >> 1));
+    const uint64_t* rs = r + (pi >> 1) * N;
+    const uint64_t tm = (1ull << c.t_bits) - 1;
+    for (uint32_t d = threadIdx.x; d < pl.nob; d += N / 16) {
+      const uint32_t o = m * pl.nob + d;
+      if (o < pl.no) y0[o] = (tm + 1 - rs[d * pl.nib + pl.nib - 1]) & tm;
+    }
+  } else if (y0 != nullptr && mask && j == 0) {
     const uint32_t ct = (uint32_t)(ct0 + (pi >> 1)), m = ct / pl.S, sidx = ct % pl.S;
     const uint32_t bh = sidx / pl.nbw, bw = sidx % pl.nbw;
     const uint32_t dh = pl.Hw - pl.kh + 1, dw = pl.Ww - pl.kw + 1;
@@ -792,6 +800,27 @@ __global__ void k_pack_weights(const uint64_t* __restrict__ kern, W* __restrict_
   const uint32_t coef = pl.O - cc * pl.Hw * pl.Ww - l * pl.Ww - l2;
   const uint64_t t = 1ull << c.t_bits;
   const uint64_t v = kern[idx] & (t - 1);
+  const size_t N = 1ull << c.log_n;
+  for (uint32_t j = 0; j < c.L; ++j) {
+    const uint64_t q = c.q[j];
+    const uint64_t lifted = v >= t / 2 ? (q - (t - v) % q) % q : v % q;
+    w[(((size_t)m * pl.G + g) * c.L + j) * N + coef] = (W)lifted;
+  }
+}
+
+// f3 packing: W [n_o][n_i] (< 2^t) -> w[m][g][j][d*nib + nib - 1 - i] = lift_j(W[m*nob + d][g*nib + i])
+// (reading R15, the matrix-vector packing; centred lift R3). One thread per matrix entry.
+template <class W>
+__global__ void k_pack_fc_weights(const uint64_t* __restrict__ Wm, W* __restrict__ w,
+                                  const __grid_constant__ DevConsts c, PlanDev pl) {
+  const size_t total = (size_t)pl.no * pl.C;
+  const size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (idx >= total) return;
+  const uint32_t col = idx % pl.C, o = idx / pl.C;
+  const uint32_t m = o / pl.nob, d = o % pl.nob, g = col / pl.nib, i = col % pl.nib;
+  const uint32_t coef = d * pl.nib + pl.nib - 1 - i;
+  const uint64_t t = 1ull << c.t_bits;
+  const uint64_t v = Wm[idx] & (t - 1);
   const size_t N = 1ull << c.log_n;
   for (uint32_t j = 0; j < c.L; ++j) {
     const uint64_t q = c.q[j];
@@ -1182,6 +1211,21 @@ cudaError_t launch_pack_weights(const DevConsts& c, const PlanDev& p, const uint
     k_pack_weights<uint64_t><<<blocks, 256, 0, s>>>(kernel, static_cast<uint64_t*>(w), c, p);
   else
     k_pack_weights<uint32_t><<<blocks, 256, 0, s>>>(kernel, static_cast<uint32_t*>(w), c, p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_fc_weights(const DevConsts& c, const PlanDev& p, const uint64_t* Wm, void* w, cudaStream_t s) {
+  const size_t N = 1ull << c.log_n;
+  const size_t wb = c.word_bits / 8;
+  cudaError_t e = cudaMemsetAsync(w, 0, (size_t)p.M * p.G * c.L * N * wb, s);
+  if (e != cudaSuccess) return e;
+  const size_t total = (size_t)p.no * p.C;
+  if (!total) return cudaGetLastError();
+  const unsigned blocks = (unsigned)((total + 255) / 256);
+  if (c.word_bits == 64)
+    k_pack_fc_weights<uint64_t><<<blocks, 256, 0, s>>>(Wm, static_cast<uint64_t*>(w), c, p);
+  else
+    k_pack_fc_weights<uint32_t><<<blocks, 256, 0, s>>>(Wm, static_cast<uint32_t*>(w), c, p);
   return cudaGetLastError();
 }
 

@@ -32,13 +32,21 @@ EXPORTS = ("secn_ctx_create", "secn_ctx_destroy", "secn_ctx_query", "secn_last_e
            "secn32_ctx_create", "secn32_ntt_fwd", "secn32_ntt_inv", "secn32_preprocess_weights",
            "secn32_share_add", "secn32_mask_add", "secn32_he_conv2d", "secn32_he_conv2d_stage",
            "secn_he_conv2d_ex", "secn32_he_conv2d_ex", "secn_he_conv2d_online_workspace",
-           "secn_he_conv2d_online", "secn32_he_conv2d_online")
+           "secn_he_conv2d_online", "secn32_he_conv2d_online", "secn_fc_plan", "secn_fc_preprocess_weights",
+           "secn32_fc_preprocess_weights", "secn_he_fc_workspace", "secn_he_fc", "secn32_he_fc")
 
 
 class SecnError(RuntimeError):
     def __init__(self, status: int, msg: str):
         super().__init__(f"{STATUS.get(status, status)}: {msg}")
         self.status = status
+
+
+class FcPlan(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_uint32) for f in ("n_i", "n_o", "nib", "nob", "G", "M")]
+
+    def __repr__(self):
+        return "FcPlan(" + ", ".join(f"{f}={getattr(self, f)}" for f, _ in self._fields_) + ")"
 
 
 class Plan(ctypes.Structure):
@@ -96,12 +104,16 @@ def lib(path=None) -> ctypes.CDLL:
         "secn_he_conv2d_stage": (i, [vp, P, i, vp, vp, vp, vp, vp, vp, sz, vp]),
         "secn_he_conv2d_ex": (i, [vp, P, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
         "secn_he_conv2d_online_workspace": (sz, [vp, P]),
+        "secn_fc_plan": (i, [u32, u32, ctypes.POINTER(FcPlan)]),
+        "secn_fc_preprocess_weights": (i, [vp, ctypes.POINTER(FcPlan), vp, vp, vp]),
+        "secn_he_fc_workspace": (sz, [vp, ctypes.POINTER(FcPlan)]),
+        "secn_he_fc": (i, [vp, ctypes.POINTER(FcPlan), vp, vp, vp, vp, vp, vp, vp, sz, vp]),
         "secn_he_conv2d_online": (i, [vp, P, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
         "secn_extract_share": (i, [vp, P, vp, vp, vp]),
         "secn32_ctx_create": (i, [ctypes.POINTER(vp), i, u32, u32, ctypes.POINTER(ctypes.c_uint32), u32]),
     }
     for f in ("ntt_fwd", "ntt_inv", "preprocess_weights", "share_add", "mask_add", "he_conv2d", "he_conv2d_stage", "he_conv2d_ex",
-              "he_conv2d_online"):
+              "he_conv2d_online", "fc_preprocess_weights", "he_fc"):
         sig["secn32_" + f] = sig["secn_" + f]
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -121,6 +133,13 @@ def conv_plan(C, H, W, M, kh, kw=None, stride=1, pad=0, log_n=DEFAULT_LOG_N, n_l
     """secn_conv_plan: packing plan of one conv layer (byte-min rule, reading R6)."""
     p = Plan(C=C, H=H, W=W, M=M, kh=kh, kw=kh if kw is None else kw, stride=stride, pad=pad, Hw=Hw, Ww=Ww)
     _check(lib().secn_conv_plan(log_n, n_limbs, ctypes.byref(p)))
+    return p
+
+
+def fc_plan(n_i, n_o, log_n=DEFAULT_LOG_N, coef_words64=len(DEFAULT_PRIMES), nib=0) -> FcPlan:
+    """secn_fc_plan: matrix-vector packing of an n_o x n_i fully-connected layer (reading R15)."""
+    p = FcPlan(n_i=n_i, n_o=n_o, nib=nib)
+    _check(lib().secn_fc_plan(log_n, coef_words64, ctypes.byref(p)))
     return p
 
 
@@ -214,6 +233,38 @@ class Context:
         _check(self._f("preprocess_weights")(self._h, ctypes.byref(plan),
                                              _ptr(kernel, (plan.M, plan.C, plan.kh, plan.kw), "kernel"),
                                              self._rp(out, shape, "w_ntt"), self._stream(stream)))
+        return out
+
+    # ---- fully connected (f3) ----
+    def fc_plan(self, n_i: int, n_o: int, nib: int = 0) -> FcPlan:
+        return fc_plan(n_i, n_o, self.log_n, self.coef_words64, nib)
+
+    def fc_preprocess_weights(self, plan: FcPlan, W: torch.Tensor, out: Optional[torch.Tensor] = None,
+                              stream=None) -> torch.Tensor:
+        """W int64 [n_o][n_i] (< 2^t) -> w_ntt [M][G][L][N] (NTT domain)."""
+        shape = (plan.M, plan.G, self.L, self.n)
+        if out is None:
+            out = self.empty(*shape)
+        _check(self._f("fc_preprocess_weights")(self._h, ctypes.byref(plan), _ptr(W, (plan.n_o, plan.n_i), "W"),
+                                                self._rp(out, shape, "w_ntt"), self._stream(stream)))
+        return out
+
+    def he_fc(self, plan: FcPlan, ct_in: torch.Tensor, w_ntt: torch.Tensor, x0: Optional[torch.Tensor] = None,
+              r: Optional[torch.Tensor] = None, out: Optional[torch.Tensor] = None,
+              y0: Optional[torch.Tensor] = None, workspace: Optional[torch.Tensor] = None,
+              stream=None) -> torch.Tensor:
+        """secn_he_fc: ct_in [G][2][L][N] -> ct_out [M][2][L][N]; y0 int64 [n_o] (server share)."""
+        L, n = self.L, self.n
+        if out is None:
+            out = self.empty(plan.M, 2, L, n)
+        if workspace is None:
+            ws = int(lib().secn_he_fc_workspace(self._h, ctypes.byref(plan)))
+            workspace = torch.empty((ws + 7) // 8, dtype=torch.int64, device=self.device)
+        _check(self._f("he_fc")(self._h, ctypes.byref(plan), self._rp(ct_in, (plan.G, 2, L, n), "ct_in"),
+                                _ptr(x0, (plan.G, n), "x0"), self._rp(w_ntt, (plan.M, plan.G, L, n), "w_ntt"),
+                                _ptr(r, (plan.M, n), "r"), self._rp(out, (plan.M, 2, L, n), "ct_out"),
+                                _ptr(y0, (plan.n_o,), "y0"), ctypes.c_void_p(workspace.data_ptr()),
+                                workspace.numel() * workspace.element_size(), self._stream(stream)))
         return out
 
     def share_add(self, ct: torch.Tensor, x0: torch.Tensor, stream=None) -> torch.Tensor:

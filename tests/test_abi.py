@@ -66,6 +66,28 @@ def test_c_plan_other_ring_sizes_and_explicit_windows(secn):
     assert (c.Cw, c.G, c.S, c.nbh, c.nbw, c.O) == (o.Cw, o.G, o.S, o.nbh, o.nbw, o.O)
 
 
+@pytest.mark.parametrize("n_i,n_o,logn,cw", [(2048, 1000, 12, 2), (512, 1000, 12, 2), (64, 16, 12, 2), (4096, 1, 12, 1),
+                                             (1, 4096, 12, 2), (100, 37, 8, 2), (2048, 1000, 13, 2), (9216, 4096, 14, 4)])
+def test_c_fc_plan_matches_oracle_plan(secn, n_i, n_o, logn, cw):
+    from oracle import fc
+
+    c = secn.fc_plan(n_i, n_o, log_n=logn, coef_words64=cw)
+    o = fc.plan_fc(n_i, n_o, 1 << logn, cw)
+    assert (c.nib, c.nob, c.G, c.M) == (o.nib, o.nob, o.G, o.M)
+    c2 = secn.fc_plan(n_i, n_o, log_n=logn, coef_words64=cw, nib=max(1, o.nib // 2))
+    o2 = fc.plan_fc(n_i, n_o, 1 << logn, cw, nib=max(1, o.nib // 2))
+    assert (c2.nib, c2.nob, c2.G, c2.M) == (o2.nib, o2.nob, o2.G, o2.M)
+
+
+def test_c_fc_plan_errors(secn):
+    for args in [(0, 5), (5, 0)]:
+        with pytest.raises(secn.SecnError) as e:
+            secn.fc_plan(*args)
+        assert e.value.status == -1
+    with pytest.raises(secn.SecnError):
+        secn.fc_plan(10, 10, nib=11)
+
+
 def test_error_paths_return_status(secn):
     lib = secn.lib()
     with pytest.raises(secn.SecnError) as e:
