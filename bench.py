@@ -28,6 +28,8 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
+import ctypes  # noqa: E402
+
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
@@ -409,6 +411,9 @@ def run_secn(args, word_bits, world, rank, local, dev, full):
     # ---- f4: online NTT preprocessing (weights in coefficient form, transformed in each call) ----
     online = None if args.no_online else run_online(ctx, st, K, args.warmup, dev, world, runner)
 
+    # ---- f2: extracted outputs (modulus switch + designated coefficients) ----
+    lwe = run_lwe(ctx, st, K, args.warmup, dev, world, runner)
+
     # ---- f3: the ResNet-50 fully-connected layer through secn_he_fc ----
     fc_leg = run_fc(ctx, K, args.warmup, dev, world)
 
@@ -451,7 +456,7 @@ def run_secn(args, word_bits, world, rank, local, dev, full):
         "per_layer_stage_us": stage_profile.per_layer_us,
         "gpu_launches": launches_per_step * K,
         "clocks": clk.summary(),
-        "e2e": e2e, "online_ntt_preprocessing": online, "fc": fc_leg,
+        "e2e": e2e, "online_ntt_preprocessing": online, "extracted_outputs": lwe, "fc": fc_leg,
         "context": {"paper_gpu_online_s": 2.26, "paper_gpu_hw": "RTX A6000 + Troy (PAPER.md:476)",
                     "paper_cpu_online_s": 3.09},
     }
@@ -500,6 +505,12 @@ def stage_profile(ctx, st, K, dev):
                     per_layer[d["lay"].name][s] += dt
     stage_profile.per_layer_us = {k: [round(v * 1e3 / K, 1) for v in vs] for k, vs in per_layer.items()}
     return [x / K for x in tot]
+
+
+def ctx_lib():
+    from paper_2506_11586_b200 import secn
+
+    return secn.lib()
 
 
 def graph_ms(fn, K, warmup, dev, world):
@@ -554,6 +565,36 @@ def run_online(ctx, st, K, warmup, dev, world, runner):
             "weights_held_bytes": held, "weights_held_offline_bytes": sum(d["w"].numel() * d["w"].element_size()
                                                                             for d in st if d["mc"] > 0),
             "path": "secn_he_conv2d_online: pack + NTT of the weights, then share add + NTT, MAC, INTT + mask"}
+
+
+def run_lwe(ctx, st, K, warmup, dev, world, runner):
+    """the same step returning extracted outputs (secn32_he_conv2d_lwe: the
+    INTT tail switches every output ct to half of its limbs and keeps the b component only at the
+    designated coefficients), i.e. what Cheetah's server sends back."""
+    keep = ctx.L // 2
+    for d in st:
+        if d["mc"] > 0:
+            pl = d["pl"]
+            d["ws_lwe"] = torch.empty((int(ctx_lib().secn_he_conv2d_lwe_workspace(ctx._h, ctypes.byref(pl))) + 7) // 8,
+                                      dtype=torch.int64, device=dev)
+
+    def layer_lwe(i):
+        d = st[i]
+        if d["mc"] > 0:
+            d["lwe_out"] = ctx.he_conv2d_lwe(d["pl"], d["ct"], d["w"], keep, x0=d["x0"], r=d["r"], y0=d["y0"],
+                                             workspace=d["ws_lwe"])
+
+    ms = graph_ms(lambda: runner(layer_lwe), K, warmup, dev, world)
+    out_bytes = sum(a.numel() * a.element_size() + b.numel() * b.element_size()
+                    for a, b in (d["lwe_out"] for d in st if d["mc"] > 0))
+    full_bytes = sum(d["out"].numel() * d["out"].element_size() for d in st if d["mc"] > 0)
+    for d in st:
+        d.pop("ws_lwe", None)
+        d.pop("lwe_out", None)
+    torch.cuda.empty_cache()
+    return {"value": round(ms / 1e3, 7), "unit": "s", "ms_per_step": round(ms, 4), "keep_limbs": keep,
+            "output_bytes_per_step": out_bytes, "full_ct_output_bytes_per_step": full_bytes,
+            "path": "secn32_he_conv2d_lwe: share add + NTT, MAC, INTT tail + mask + modulus switch + extraction"}
 
 
 def run_fc(ctx, K, warmup, dev, world, n_i=2048, n_o=1000, seed=11):

@@ -218,6 +218,29 @@ int secn_he_fc(secn_ctx* ctx, const secn_fc_plan_t* plan, const uint64_t* ct_in,
                size_t ws_bytes, void* stream);
 
 /* ------------------------------------------------------------------------------------------
+ * Extracted outputs (Cheetah's sparse result PAPER.md:131 §2.3; the result
+ * returned to the client PAPER.md:431 §7; reading R16). The same computation as
+ * secn_he_conv2d_ex / secn_he_fc, but each output ciphertext leaves the kernel
+ *   (1) switched to the first keep_limbs primes Q' = q_0..q_{keep-1}: every coefficient c (both
+ *       components) becomes round(c Q'/Q) mod Q' (exact, RNS, no ties since Q/Q' is odd);
+ *   (2) extracted: the a component whole, a_out [n_ct][keep][N]; the b component only at its
+ *       designated coefficients, b_out [value][keep] with value = (m, oy, ox) row-major for a
+ *       convolution ([M][OH][OW]) and the output row o for a matrix-vector product ([n_o]).
+ * The client decrypts value k of ct n as round(t (b'_k - (a'_n * sk)_k) / Q') mod t (an LWE
+ * decryption). y0 as for secn_he_conv2d_ex. N = 4096 only; keep_limbs in [1, L-1] with the
+ * dropped primes' product < 2^62 (SECN_EUNSUPPORTED otherwise; Q'/t must leave room for the
+ * switching noise: keep 2 of 4 27-bit limbs, or 1 of the 60+49-bit pair). The workspace holds
+ * X^ and the output cts before switching (secn_he_*_lwe_workspace bytes). */
+size_t secn_he_conv2d_lwe_workspace(const secn_ctx* ctx, const secn_conv_plan_t* plan);
+int secn_he_conv2d_lwe(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* ct_in, const uint64_t* x0,
+                       const uint64_t* w_ntt, const uint64_t* r, uint32_t keep_limbs, uint64_t* a_out,
+                       uint64_t* b_out, uint64_t* y0, void* workspace, size_t ws_bytes, void* stream);
+size_t secn_he_fc_lwe_workspace(const secn_ctx* ctx, const secn_fc_plan_t* plan);
+int secn_he_fc_lwe(secn_ctx* ctx, const secn_fc_plan_t* plan, const uint64_t* ct_in, const uint64_t* x0,
+                   const uint64_t* w_ntt, const uint64_t* r, uint32_t keep_limbs, uint64_t* a_out, uint64_t* b_out,
+                   uint64_t* y0, void* workspace, size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------------------------------
  * 32-bit RNS limbs (reading R1b). Identical semantics to the
  * calls above with residues stored as uint32 ([..][L][N] uint32 words) for moduli q_j < 2^28,
  * e.g. four 27-bit primes = 1 mod 2^16 (Q = 108 bits <= 109, the 128-bit-security bound for
@@ -249,6 +272,12 @@ int secn32_fc_preprocess_weights(secn_ctx* ctx, const secn_fc_plan_t* plan, cons
 int secn32_he_fc(secn_ctx* ctx, const secn_fc_plan_t* plan, const uint32_t* ct_in, const uint64_t* x0,
                  const uint32_t* w_ntt, const uint64_t* r, uint32_t* ct_out, uint64_t* y0, void* workspace,
                  size_t ws_bytes, void* stream);
+int secn32_he_conv2d_lwe(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint32_t* ct_in, const uint64_t* x0,
+                         const uint32_t* w_ntt, const uint64_t* r, uint32_t keep_limbs, uint32_t* a_out,
+                         uint32_t* b_out, uint64_t* y0, void* workspace, size_t ws_bytes, void* stream);
+int secn32_he_fc_lwe(secn_ctx* ctx, const secn_fc_plan_t* plan, const uint32_t* ct_in, const uint64_t* x0,
+                     const uint32_t* w_ntt, const uint64_t* r, uint32_t keep_limbs, uint32_t* a_out, uint32_t* b_out,
+                     uint64_t* y0, void* workspace, size_t ws_bytes, void* stream);
 int secn32_he_conv2d_stage(secn_ctx* ctx, const secn_conv_plan_t* plan, int stage, const uint32_t* ct_in,
                            const uint64_t* x0, const uint32_t* w_ntt, const uint64_t* r, uint32_t* ct_out,
                            void* workspace, size_t ws_bytes, void* stream);

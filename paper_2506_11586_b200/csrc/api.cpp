@@ -646,6 +646,121 @@ int secn32_he_fc(secn_ctx* ctx, const secn_fc_plan_t* plan, const uint32_t* ct_i
   return he_fc_impl(ctx, 32, plan, ct_in, x0, w_ntt, r, ct_out, y0, workspace, ws_bytes, stream);
 }
 
+// ---- f2: modulus switching + coefficient extraction of the outputs (reading R16) ----
+
+static int make_ms(const secn_ctx* ctx, uint32_t keep, secn::MsConsts* ms) {
+  const uint32_t L = ctx->L;
+  if (ctx->log_n != 12) return fail(SECN_EUNSUPPORTED, "extracted outputs need N = 4096");
+  if (keep < 1 || keep >= L) return fail(SECN_EUNSUPPORTED, "keep_limbs=%u not in [1, L-1] (L=%u)", keep, L);
+  std::memset(ms, 0, sizeof *ms);
+  ms->Lk = keep;
+  u128 P = 1;
+  for (uint32_t j = keep; j < L; ++j) P *= ctx->primes[j];
+  if (P * (L - keep) >= ((u128)1 << 63)) return fail(SECN_EUNSUPPORTED, "dropped primes' product too large (> 2^62)");
+  if (L - keep > (ctx->word_bits == 64 ? 1u : 2u))
+    return fail(SECN_EUNSUPPORTED, "at most %u dropped limbs", ctx->word_bits == 64 ? 1u : 2u);
+  ms->P = (uint64_t)P;
+  auto comp = [&](uint64_t w, uint64_t q) {
+    return ctx->word_bits == 64 ? shoup_companion(w, q) : (uint64_t)((((u128)w) << 32) / q);
+  };
+  for (uint32_t j = keep; j < L; ++j) {
+    const uint64_t q = ctx->primes[j], pq = ms->P / q;
+    ms->pq[j] = pq;
+    ms->inv[j] = powmod(pq % q, q - 2, q);
+    ms->inv_p[j] = comp(ms->inv[j], q);
+  }
+  for (uint32_t i = 0; i < keep; ++i) {
+    const uint64_t q = ctx->primes[i];
+    ms->pinv[i] = powmod(ms->P % q, q - 2, q);
+    ms->pinv_p[i] = comp(ms->pinv[i], q);
+  }
+  return SECN_OK;
+}
+
+size_t secn_he_conv2d_lwe_workspace(const secn_ctx* ctx, const secn_conv_plan_t* plan) {
+  if (!ctx || !plan) return 0;
+  const size_t wb = ctx->word_bits / 8;
+  return xhat_bytes_aligned(ctx, plan) + (size_t)plan->M * plan->S * 2 * ctx->L * ctx->n * wb;
+}
+
+static int he_conv2d_lwe_impl(secn_ctx* ctx, uint32_t bits, const secn_conv_plan_t* plan, const void* ct_in,
+                              const uint64_t* x0, const void* w_ntt, const uint64_t* r, uint32_t keep, void* a_out,
+                              void* b_out, uint64_t* y0, void* workspace, size_t ws_bytes, void* stream) {
+  if (int st = check_ctx(ctx, bits)) return st;
+  if (int st = check_plan(ctx, plan)) return st;
+  secn::MsConsts ms;
+  if (int st = make_ms(ctx, keep, &ms)) return st;
+  if (!a_out || !b_out || !workspace) return fail(SECN_EINVAL, "NULL buffer");
+  if (ws_bytes < secn_he_conv2d_lwe_workspace(ctx, plan)) return fail(SECN_EINVAL, "workspace too small");
+  if (y0 && !r) return fail(SECN_EINVAL, "y0 needs the mask r");
+  // X^ then Y^ (levels 0..7 applied) in the workspace; stages 0-1 of the full path
+  void* yhat = static_cast<unsigned char*>(workspace) + xhat_bytes_aligned(ctx, plan);
+  if (int st = he_conv2d_impl(ctx, bits, plan, 0, ct_in, x0, w_ntt, r, yhat, nullptr, workspace,
+                              xhat_bytes_aligned(ctx, plan), stream))
+    return st;
+  if (int st = he_conv2d_impl(ctx, bits, plan, 1, ct_in, x0, w_ntt, r, yhat, nullptr, workspace,
+                              xhat_bytes_aligned(ctx, plan), stream))
+    return st;
+  DeviceGuard guard(ctx->device);
+  cudaError_t e = secn::launch_ntt_inv_tail_lwe(ctx->dc, ms, yhat, (size_t)plan->M * plan->S, r, a_out, b_out, y0,
+                                                plan_dev(plan), (cudaStream_t)stream);
+  return e == cudaSuccess ? SECN_OK : cuda_fail(e, "secn_he_conv2d_lwe");
+}
+
+int secn_he_conv2d_lwe(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* ct_in, const uint64_t* x0,
+                       const uint64_t* w_ntt, const uint64_t* r, uint32_t keep_limbs, uint64_t* a_out,
+                       uint64_t* b_out, uint64_t* y0, void* workspace, size_t ws_bytes, void* stream) {
+  return he_conv2d_lwe_impl(ctx, 64, plan, ct_in, x0, w_ntt, r, keep_limbs, a_out, b_out, y0, workspace, ws_bytes,
+                            stream);
+}
+int secn32_he_conv2d_lwe(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint32_t* ct_in, const uint64_t* x0,
+                         const uint32_t* w_ntt, const uint64_t* r, uint32_t keep_limbs, uint32_t* a_out,
+                         uint32_t* b_out, uint64_t* y0, void* workspace, size_t ws_bytes, void* stream) {
+  return he_conv2d_lwe_impl(ctx, 32, plan, ct_in, x0, w_ntt, r, keep_limbs, a_out, b_out, y0, workspace, ws_bytes,
+                            stream);
+}
+
+size_t secn_he_fc_lwe_workspace(const secn_ctx* ctx, const secn_fc_plan_t* plan) {
+  if (!ctx || !plan) return 0;
+  const size_t wb = ctx->word_bits / 8;
+  return ((secn_he_fc_workspace(ctx, plan) + 255) & ~(size_t)255) + (size_t)plan->M * 2 * ctx->L * ctx->n * wb;
+}
+
+static int he_fc_lwe_impl(secn_ctx* ctx, uint32_t bits, const secn_fc_plan_t* plan, const void* ct_in,
+                          const uint64_t* x0, const void* w_ntt, const uint64_t* r, uint32_t keep, void* a_out,
+                          void* b_out, uint64_t* y0, void* workspace, size_t ws_bytes, void* stream) {
+  if (int st = check_ctx(ctx, bits)) return st;
+  if (int st = check_fc_plan(ctx, plan)) return st;
+  secn::MsConsts ms;
+  if (int st = make_ms(ctx, keep, &ms)) return st;
+  if (!ct_in || !w_ntt || !a_out || !b_out || !workspace) return fail(SECN_EINVAL, "NULL buffer");
+  if (ws_bytes < secn_he_fc_lwe_workspace(ctx, plan)) return fail(SECN_EINVAL, "workspace too small");
+  if (y0 && !r) return fail(SECN_EINVAL, "y0 needs the mask r");
+  if (((uintptr_t)workspace | (uintptr_t)ct_in | (uintptr_t)w_ntt) & 15)
+    return fail(SECN_EINVAL, "buffers must be 16-byte aligned");
+  if (plan->G > 32u) return fail(SECN_EUNSUPPORTED, "G=%u input blocks too many", plan->G);
+  DeviceGuard guard(ctx->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t xb = (secn_he_fc_workspace(ctx, plan) + 255) & ~(size_t)255;
+  void* yhat = static_cast<unsigned char*>(workspace) + xb;
+  const secn::PlanDev pd = fc_plan_dev(plan);
+  cudaError_t e = secn::launch_ntt_fwd(ctx->dc, ct_in, workspace, (size_t)plan->G * 2 * ctx->L, x0, s);
+  if (e == cudaSuccess) e = secn::launch_mac(ctx->dc, pd, workspace, w_ntt, yhat, s);
+  if (e == cudaSuccess) e = secn::launch_ntt_inv_tail_lwe(ctx->dc, ms, yhat, plan->M, r, a_out, b_out, y0, pd, s);
+  return e == cudaSuccess ? SECN_OK : cuda_fail(e, "secn_he_fc_lwe");
+}
+
+int secn_he_fc_lwe(secn_ctx* ctx, const secn_fc_plan_t* plan, const uint64_t* ct_in, const uint64_t* x0,
+                   const uint64_t* w_ntt, const uint64_t* r, uint32_t keep_limbs, uint64_t* a_out, uint64_t* b_out,
+                   uint64_t* y0, void* workspace, size_t ws_bytes, void* stream) {
+  return he_fc_lwe_impl(ctx, 64, plan, ct_in, x0, w_ntt, r, keep_limbs, a_out, b_out, y0, workspace, ws_bytes, stream);
+}
+int secn32_he_fc_lwe(secn_ctx* ctx, const secn_fc_plan_t* plan, const uint32_t* ct_in, const uint64_t* x0,
+                     const uint32_t* w_ntt, const uint64_t* r, uint32_t keep_limbs, uint32_t* a_out, uint32_t* b_out,
+                     uint64_t* y0, void* workspace, size_t ws_bytes, void* stream) {
+  return he_fc_lwe_impl(ctx, 32, plan, ct_in, x0, w_ntt, r, keep_limbs, a_out, b_out, y0, workspace, ws_bytes, stream);
+}
+
 int secn_he_conv2d_stage(secn_ctx* ctx, const secn_conv_plan_t* plan, int stage, const uint64_t* ct_in,
                          const uint64_t* x0, const uint64_t* w_ntt, const uint64_t* r, uint64_t* ct_out,
                          void* workspace, size_t ws_bytes, void* stream) {

@@ -45,6 +45,16 @@ struct PlanDev {  // the subset of secn_conv_plan (kind 0) / secn_fc_plan (kind 
   uint32_t nib, nob, no; // fc: inputs per ct, output rows per ct, n_o (C holds n_i)
 };
 
+// Modulus switch Q -> Q' = q_0 .. q_{Lk-1} (reading R16): P = the product of the dropped primes
+// q_Lk .. q_{L-1}; for a dropped limb j: pq[j] = P / q_j and inv[j] = (P / q_j)^-1 mod q_j; for a
+// kept limb i: pinv[i] = P^-1 mod q_i (companions word-sized). Built per call on the host.
+struct MsConsts {
+  uint32_t Lk;
+  uint64_t P;
+  uint64_t pq[SECN_MAX_LIMBS], inv[SECN_MAX_LIMBS], inv_p[SECN_MAX_LIMBS];
+  uint64_t pinv[SECN_MAX_LIMBS], pinv_p[SECN_MAX_LIMBS];
+};
+
 // ---- launchers (kernels.cu); all return cudaGetLastError() after the launch(es) ----
 // Residue buffers are void* of the context's word size.
 cudaError_t launch_ntt_fwd(const DevConsts& c, const void* in, void* out, size_t n_limb_polys, const uint64_t* x0,
@@ -57,6 +67,12 @@ cudaError_t launch_ntt_inv_tail(const DevConsts& c, void* polys, size_t n_limb_p
 // NTT-domain MAC (A4) followed by inverse-NTT levels 0..7 of its outputs (lazy GS domain)
 cudaError_t launch_mac(const DevConsts& c, const PlanDev& p, const void* xhat, const void* w, void* y, cudaStream_t s);
 cudaError_t launch_pack_weights(const DevConsts& c, const PlanDev& p, const uint64_t* kernel, void* w, cudaStream_t s);
+// f2: levels 8.. of the inverse NTT + mask + modulus switch to ms.Lk limbs + extraction, N = 4096
+// only: polys [n_ct][2][L][N] (after launch_mac) -> a_out [n_ct][Lk][N], b_out [values][Lk] at the
+// designated coefficients of plan pl (conv or fc), and y0 (if not NULL) the server share.
+cudaError_t launch_ntt_inv_tail_lwe(const DevConsts& c, const MsConsts& ms, const void* polys, size_t n_ct,
+                                    const uint64_t* r, void* a_out, void* b_out, uint64_t* y0, const PlanDev& pl,
+                                    cudaStream_t s);
 // fc weights W [n_o][n_i] -> mirrored polys [M][G][L][N] (coefficient domain, zero-filled first)
 cudaError_t launch_pack_fc_weights(const DevConsts& c, const PlanDev& p, const uint64_t* W, void* w, cudaStream_t s);
 cudaError_t launch_enc_add(const DevConsts& c, void* ct, const uint64_t* v, size_t n, cudaStream_t s);

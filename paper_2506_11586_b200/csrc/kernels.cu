@@ -783,6 +783,152 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
 }
 
 // ------------------------------------------------------------------------------------------
+// f2 (reading R16): the INTT tail with the output switched to Lk limbs and
+// extracted. One CTA per (output ct, component), 256 threads, 16 coefficients o + 256 i per
+// thread (N = 4096). Modulus switching needs all L residues of a coefficient: the dropped limbs
+// go first and fold into the centred CRT value v = [c]_P of the dropped part,
+//   v = sum_j ((c_j (P/q_j)^-1) mod q_j) (P/q_j)  mod P,  then centred into (-P/2, P/2);
+// every kept limb i then yields c'_i = (c_i - v) P^-1 mod q_i = round(c Q'/Q) mod q_i exactly
+// (c - [c]_P is the multiple of P nearest to c; P is odd, so there are no ties). The a
+// component is written whole (a' is shared by every designated coefficient), the b component only
+// at its designated coefficients, as b'[value][Lk].
+
+// canonical a mod q for any 64-bit a
+template <class A>
+__device__ __forceinline__ typename A::W reduce_u64(uint64_t a, const DevConsts& c, int j);
+template <>
+__device__ __forceinline__ uint64_t reduce_u64<Arith64>(uint64_t a, const DevConsts& c, int j) {
+  return reduce128(a, 0, c.q[j], c.r64[j], c.r64_p[j], c.one_p[j]);
+}
+template <>
+__device__ __forceinline__ uint32_t reduce_u64<Arith32>(uint64_t a, const DevConsts& c, int j) {
+  return reduce64(a, (uint32_t)c.q[j], (uint32_t)c.r32[j], (uint32_t)c.r32_p[j], (uint32_t)(c.one_p[j] >> 32));
+}
+
+// output index of coefficient e of output ct `ct` under plan pl, or -1 (not designated)
+__device__ __forceinline__ int64_t designated_index(const PlanDev& pl, uint32_t ct, uint32_t e) {
+  if (pl.kind == 1) {  // fc: y[m*nob + d] at d*nib + nib - 1
+    if ((e + 1) % pl.nib != 0) return -1;
+    const uint32_t d = (e + 1) / pl.nib - 1;
+    const uint32_t o = ct * pl.nob + d;
+    return d < pl.nob && o < pl.no ? (int64_t)o : -1;
+  }
+  if (e < pl.O) return -1;
+  const uint32_t dd = e - pl.O, i = dd / pl.Ww, jj = dd % pl.Ww;
+  if (i > pl.Hw - pl.kh || jj > pl.Ww - pl.kw) return -1;
+  const uint32_t m = ct / pl.S, s = ct % pl.S, bh = s / pl.nbw, bw = s % pl.nbw;
+  const uint32_t py = bh * (pl.Hw - pl.kh + 1) + i, px = bw * (pl.Ww - pl.kw + 1) + jj;
+  const uint32_t oy = py / pl.sh, ox = px / pl.sh;
+  if (oy * pl.sh != py || ox * pl.sh != px || oy >= pl.OH || ox >= pl.OW) return -1;
+  return ((int64_t)m * pl.OH + oy) * pl.OW + ox;
+}
+
+// Launch shape: one CTA per (output ct, component, half of the 256 radix-16 tasks), L warp groups of
+// 128 threads, group j = limb j, so every limb's loads are in flight at once. Task o = h*128 + lt
+// covers coefficients o + 256 i (i < 16). Dropped-limb groups leave y_j = c_j (P/q_j)^-1 mod q_j
+// in shared memory; after one barrier the kept-limb groups fold v = sum_j y_j (P/q_j) mod P,
+// centre it and write their switched residues.
+constexpr int LWE_G = 128;
+
+template <class A, int ND>  // ND = L - Lk dropped limbs
+__global__ void __launch_bounds__(LWE_G * SECN_MAX_LIMBS)
+    k_ntt_inv_tail_lwe(const typename A::W* __restrict__ polys, const __grid_constant__ DevConsts c,
+                       const __grid_constant__ MsConsts ms, const uint64_t* __restrict__ r, typename A::W* a_out,
+                       typename A::W* b_out, uint64_t* y0, const __grid_constant__ PlanDev pl) {
+  using W = typename A::W;
+  constexpr int LOGN = 12, N = 1 << LOGN;
+  using RS = GsRound<LOGN, 8>;
+  static_assert(RS::NT == 1 && RS::GK == 16, "one radix-16 task per thread");
+  __shared__ W ys[ND][16][LWE_G];
+  const size_t pi = blockIdx.x >> 1, ct = pi >> 1;
+  const uint32_t o = (blockIdx.x & 1) * LWE_G + threadIdx.x % LWE_G;  // radix-16 task: coefficients o + 256 i
+  const int j = threadIdx.x / LWE_G;                                   // this group's limb
+  const bool isb = pi & 1, mask = isb && r != nullptr;
+  const uint64_t* rs = mask ? r + ct * N : nullptr;
+  const int L = (int)c.L, Lk = L - ND;
+  const W q = (W)c.q[j], qb = A::bound(q);
+  typename A::Tw tws[15];
+  {  // twiddles of levels 8..11: the round has a single block, so every task uses the same 15
+     // (level 8 + p, group gi at tw[N / 2^(9+p) + gi]; layout as in gs_twiddles)
+    const typename A::Tw* tw = Tab<A>::inv(c) + (size_t)j * N;
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+      for (int gi = 0; gi < (8 >> p); ++gi) tws[16 - (16 >> p) + gi] = tw[(N >> (9 + p)) + gi];
+  }
+  // b component: only designated coefficients leave the kernel, so a task none of whose 16
+  // coefficients is designated does no work (convolutions: they lie in [O, O + (Hw-kh) Ww + Ww-kw])
+  bool work = true;
+  if (isb && pl.kind == 0) {
+    const uint32_t lo = pl.O, hi = pl.O + (pl.Hw - pl.kh) * pl.Ww + (pl.Ww - pl.kw);
+    work = false;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) work |= (o + 256 * i >= lo) && (o + 256 * i <= hi);
+  }
+  const EncK ek(c, j);
+  W em[16];
+  if (mask && work) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) em[i] = enc_mod<A>(__ldg(&rs[o + 256 * i]), ek);
+  }
+  pdl_wait();
+  W x[1][16];
+  if (work) {
+    const W* buf = polys + (pi * L + j) * N;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) x[0][i] = buf[o + 256 * i];
+    gs_compute<A, LOGN, 8, 1>(x, tws, q, qb, Tab<A>::pair(c.ninv[j], c.ninv_p[j]),
+                              Tab<A>::pair(c.wlast[j], c.wlast_p[j]));
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      W v = A::canon_gs(x[0][i], q);
+      if (mask) {
+        v += em[i];
+        v = v >= q ? v - q : v;
+      }
+      x[0][i] = v;
+    }
+    if (j >= Lk) {  // dropped limb: y_j = c_j (P/q_j)^-1 mod q_j
+      const typename A::Tw inv = Tab<A>::pair(ms.inv[j], ms.inv_p[j]);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) ys[j - Lk][i][threadIdx.x % LWE_G] = A::canon_gs(A::mul4(x[0][i], inv, q), q);
+    }
+  }
+  pdl_trigger();
+  __syncthreads();  // every thread, converged (aligned barrier)
+  if (!work || j >= Lk) return;
+  const typename A::Tw pinv = Tab<A>::pair(ms.pinv[j], ms.pinv_p[j]);
+  uint64_t pq[ND];
+#pragma unroll
+  for (int d = 0; d < ND; ++d) pq[d] = ms.pq[Lk + d];
+  const uint32_t lt = threadIdx.x % LWE_G;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const uint32_t e = o + 256 * i;
+    const int64_t oi = isb ? designated_index(pl, (uint32_t)ct, e) : 0;
+    if (oi < 0) continue;  // b: not designated
+    uint64_t v = 0;
+#pragma unroll
+    for (int d = 0; d < ND; ++d) v += (uint64_t)ys[d][i][lt] * pq[d];
+#pragma unroll
+    for (int d = 1; d < ND; ++d) v = v >= ms.P ? v - ms.P : v;  // v < ND P
+    const bool neg = v > ms.P / 2;                                   // centred [c]_P = neg ? v - P : v
+    const W rm = reduce_u64<A>(neg ? ms.P - v : v, c, j);
+    const W t = neg ? x[0][i] + rm : x[0][i] + (q - rm);              // (c - [c]_P) mod q, in [0, 2q)
+    const W out = A::canon_gs(A::mul4(t, pinv, q), q);
+    if (!isb) {
+      a_out[(ct * Lk + j) * N + e] = out;
+    } else {
+      b_out[(size_t)oi * Lk + j] = out;
+      if (j == 0 && y0 != nullptr && mask) {
+        const uint64_t tm = (1ull << c.t_bits) - 1;
+        y0[oi] = (tm + 1 - rs[e]) & tm;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
 // A3 packing: kernel [M][C][kh][kw] (< 2^t) -> mirrored coefficient-domain polys
 // w[m][g][j][O - c*Hw*Ww - l*Ww - l'] = lift_j(K[m, g*Cw+c, l, l']) (reading R3: centred lift).
 // The target must be zero-filled before.
@@ -1227,6 +1373,26 @@ cudaError_t launch_pack_fc_weights(const DevConsts& c, const PlanDev& p, const u
   else
     k_pack_fc_weights<uint32_t><<<blocks, 256, 0, s>>>(Wm, static_cast<uint32_t*>(w), c, p);
   return cudaGetLastError();
+}
+
+cudaError_t launch_ntt_inv_tail_lwe(const DevConsts& c, const MsConsts& ms, const void* polys, size_t n_ct,
+                                    const uint64_t* r, void* a_out, void* b_out, uint64_t* y0, const PlanDev& pl,
+                                    cudaStream_t s) {
+  if (n_ct == 0) return cudaSuccess;
+  if (c.log_n != 12 || 4 * n_ct > 0x7fffffffull) return cudaErrorInvalidValue;
+  const dim3 grid((unsigned)(4 * n_ct)), block(LWE_G * c.L);  // (ct, component, half) x limbs
+  const int nd = (int)(c.L - ms.Lk);
+#define SECN_LWE(AR, WT, ND)                                                                                   \
+  return launch_pdl(k_ntt_inv_tail_lwe<AR, ND>, grid, block, 0, s, static_cast<const WT*>(polys), c, ms, r,    \
+                    static_cast<WT*>(a_out), static_cast<WT*>(b_out), y0, pl)
+  if (c.word_bits == 64) {
+    if (nd == 1) SECN_LWE(Arith64, uint64_t, 1);  // 64-bit limbs: one dropped prime (P < 2^62)
+  } else {
+    if (nd == 1) SECN_LWE(Arith32, uint32_t, 1);
+    if (nd == 2) SECN_LWE(Arith32, uint32_t, 2);
+  }
+#undef SECN_LWE
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_enc_add(const DevConsts& c, void* ct, const uint64_t* v, size_t n, cudaStream_t s) {

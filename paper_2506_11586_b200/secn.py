@@ -33,7 +33,9 @@ EXPORTS = ("secn_ctx_create", "secn_ctx_destroy", "secn_ctx_query", "secn_last_e
            "secn32_share_add", "secn32_mask_add", "secn32_he_conv2d", "secn32_he_conv2d_stage",
            "secn_he_conv2d_ex", "secn32_he_conv2d_ex", "secn_he_conv2d_online_workspace",
            "secn_he_conv2d_online", "secn32_he_conv2d_online", "secn_fc_plan", "secn_fc_preprocess_weights",
-           "secn32_fc_preprocess_weights", "secn_he_fc_workspace", "secn_he_fc", "secn32_he_fc")
+           "secn32_fc_preprocess_weights", "secn_he_fc_workspace", "secn_he_fc", "secn32_he_fc",
+           "secn_he_conv2d_lwe_workspace", "secn_he_conv2d_lwe", "secn32_he_conv2d_lwe", "secn_he_fc_lwe_workspace",
+           "secn_he_fc_lwe", "secn32_he_fc_lwe")
 
 
 class SecnError(RuntimeError):
@@ -105,6 +107,10 @@ def lib(path=None) -> ctypes.CDLL:
         "secn_he_conv2d_ex": (i, [vp, P, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
         "secn_he_conv2d_online_workspace": (sz, [vp, P]),
         "secn_fc_plan": (i, [u32, u32, ctypes.POINTER(FcPlan)]),
+        "secn_he_conv2d_lwe_workspace": (sz, [vp, P]),
+        "secn_he_conv2d_lwe": (i, [vp, P, vp, vp, vp, vp, u32, vp, vp, vp, vp, sz, vp]),
+        "secn_he_fc_lwe_workspace": (sz, [vp, ctypes.POINTER(FcPlan)]),
+        "secn_he_fc_lwe": (i, [vp, ctypes.POINTER(FcPlan), vp, vp, vp, vp, u32, vp, vp, vp, vp, sz, vp]),
         "secn_fc_preprocess_weights": (i, [vp, ctypes.POINTER(FcPlan), vp, vp, vp]),
         "secn_he_fc_workspace": (sz, [vp, ctypes.POINTER(FcPlan)]),
         "secn_he_fc": (i, [vp, ctypes.POINTER(FcPlan), vp, vp, vp, vp, vp, vp, vp, sz, vp]),
@@ -113,7 +119,7 @@ def lib(path=None) -> ctypes.CDLL:
         "secn32_ctx_create": (i, [ctypes.POINTER(vp), i, u32, u32, ctypes.POINTER(ctypes.c_uint32), u32]),
     }
     for f in ("ntt_fwd", "ntt_inv", "preprocess_weights", "share_add", "mask_add", "he_conv2d", "he_conv2d_stage", "he_conv2d_ex",
-              "he_conv2d_online", "fc_preprocess_weights", "he_fc"):
+              "he_conv2d_online", "fc_preprocess_weights", "he_fc", "he_conv2d_lwe", "he_fc_lwe"):
         sig["secn32_" + f] = sig["secn_" + f]
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -266,6 +272,42 @@ class Context:
                                 _ptr(y0, (plan.n_o,), "y0"), ctypes.c_void_p(workspace.data_ptr()),
                                 workspace.numel() * workspace.element_size(), self._stream(stream)))
         return out
+
+    # ---- extracted outputs (f2): modulus switch to `keep` limbs + designated coefficients ----
+    def he_conv2d_lwe(self, plan: Plan, ct_in: torch.Tensor, w_ntt: torch.Tensor, keep: int,
+                      x0: Optional[torch.Tensor] = None, r: Optional[torch.Tensor] = None,
+                      y0: Optional[torch.Tensor] = None, workspace: Optional[torch.Tensor] = None, stream=None):
+        """secn_he_conv2d_lwe -> (a' [M*S][keep][N], b' [M][OH][OW][keep]) in the residue dtype."""
+        L, n = self.L, self.n
+        a = self.empty(plan.M * plan.S, keep, n)
+        b = self.empty(plan.M, plan.OH, plan.OW, keep)
+        if workspace is None:
+            ws = int(lib().secn_he_conv2d_lwe_workspace(self._h, ctypes.byref(plan)))
+            workspace = torch.empty((ws + 7) // 8, dtype=torch.int64, device=self.device)
+        _check(self._f("he_conv2d_lwe")(
+            self._h, ctypes.byref(plan), self._rp(ct_in, (plan.G * plan.S, 2, L, n), "ct_in"),
+            _ptr(x0, (plan.G * plan.S, n), "x0"), self._rp(w_ntt, (plan.M, plan.G, L, n), "w_ntt"),
+            _ptr(r, (plan.M * plan.S, n), "r"), keep, self._rp(a), self._rp(b),
+            _ptr(y0, (plan.M, plan.OH, plan.OW), "y0"), ctypes.c_void_p(workspace.data_ptr()),
+            workspace.numel() * workspace.element_size(), self._stream(stream)))
+        return a, b
+
+    def he_fc_lwe(self, plan: FcPlan, ct_in: torch.Tensor, w_ntt: torch.Tensor, keep: int,
+                  x0: Optional[torch.Tensor] = None, r: Optional[torch.Tensor] = None,
+                  y0: Optional[torch.Tensor] = None, workspace: Optional[torch.Tensor] = None, stream=None):
+        """secn_he_fc_lwe -> (a' [M][keep][N], b' [n_o][keep])."""
+        L, n = self.L, self.n
+        a = self.empty(plan.M, keep, n)
+        b = self.empty(plan.n_o, keep)
+        if workspace is None:
+            ws = int(lib().secn_he_fc_lwe_workspace(self._h, ctypes.byref(plan)))
+            workspace = torch.empty((ws + 7) // 8, dtype=torch.int64, device=self.device)
+        _check(self._f("he_fc_lwe")(
+            self._h, ctypes.byref(plan), self._rp(ct_in, (plan.G, 2, L, n), "ct_in"), _ptr(x0, (plan.G, n), "x0"),
+            self._rp(w_ntt, (plan.M, plan.G, L, n), "w_ntt"), _ptr(r, (plan.M, n), "r"), keep, self._rp(a),
+            self._rp(b), _ptr(y0, (plan.n_o,), "y0"), ctypes.c_void_p(workspace.data_ptr()),
+            workspace.numel() * workspace.element_size(), self._stream(stream)))
+        return a, b
 
     def share_add(self, ct: torch.Tensor, x0: torch.Tensor, stream=None) -> torch.Tensor:
         n = ct.shape[0]

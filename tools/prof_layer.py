@@ -1,5 +1,5 @@
 """Runs one layer of the hot path a few times (for ncu captures of single kernels).
-Usage: python tools/prof_layer.py [layer_name] [net] [reps]"""
+Usage: python tools/prof_layer.py [layer_name] [net] [reps] [word_bits] [mode: full|lwe]"""
 import sys
 from pathlib import Path
 
@@ -16,6 +16,7 @@ name = sys.argv[1] if len(sys.argv) > 1 else "conv10"
 net = sys.argv[2] if len(sys.argv) > 2 else "squeezenet1_1"
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
 wb = int(sys.argv[4]) if len(sys.argv) > 4 else 64
+mode = sys.argv[5] if len(sys.argv) > 5 else "full"
 __graft_entry__.build()
 ctx = Context(0, word_bits=wb)
 lay = next(l for l in layers.network(net) if l.name == name)
@@ -31,13 +32,23 @@ r = T(inputs.uniform_below(g, (plan.M * plan.S, ctx.n), 1 << ctx.t_bits))
 w = ctx.preprocess_weights(plan, K)
 out = ctx.empty(plan.M * plan.S, 2, ctx.L, ctx.n)
 ws = torch.empty(ctx.workspace_bytes(plan) // 8, dtype=torch.int64, device=dev)
+y0 = torch.empty((plan.M, plan.OH, plan.OW), dtype=torch.int64, device=dev)
+
+
+def call():
+    if mode == "lwe":
+        ctx.he_conv2d_lwe(plan, ct, w, ctx.L // 2, x0=x0, r=r, y0=y0)
+    else:
+        ctx.he_conv2d(plan, ct, w, x0=x0, r=r, out=out, workspace=ws, y0=y0)
+
+
 for _ in range(reps):
-    ctx.he_conv2d(plan, ct, w, x0=x0, r=r, out=out, workspace=ws)
+    call()
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
 for _ in range(reps):
-    ctx.he_conv2d(plan, ct, w, x0=x0, r=r, out=out, workspace=ws)
+    call()
 e1.record()
 torch.cuda.synchronize()
 print(name, wb, plan, f"{e0.elapsed_time(e1) / reps:.4f} ms/layer")
