@@ -223,6 +223,9 @@ static int ctx_create_impl(secn_ctx** out, int device, uint32_t log_n, uint32_t 
   std::vector<unsigned char> tw(tw_bytes);
   ulonglong2* tw64 = reinterpret_cast<ulonglong2*>(tw.data());
   uint2* tw32 = reinterpret_cast<uint2*>(tw.data());
+  bool redc = word_bits == 32;  // k_mac's Montgomery REDC needs G q < 2^32 for G <= 32: q < 2^27
+  for (uint32_t j = 0; j < n_limbs; ++j) redc = redc && primes[j] < (1ull << 27);
+  dc.mac_redc = redc ? 1u : 0u;
   for (uint32_t j = 0; j < n_limbs; ++j) {
     const uint64_t q = primes[j];
     c->primes[j] = q;
@@ -246,6 +249,15 @@ static int ctx_create_impl(secn_ctx** out, int device, uint32_t log_n, uint32_t 
     dc.ninv[j] = ninv, dc.ninv_p[j] = comp(ninv, q);
     const uint64_t wl = mulmod(powmod(psi_inv, bitrev(1, log_n), q), ninv, q);
     dc.wlast[j] = wl, dc.wlast_p[j] = comp(wl, q);
+    {
+      const uint64_t scale = redc ? (uint64_t)((((u128)1) << 32) % q) : 1;  // undoes REDC's 2^-32
+      const uint64_t nm = mulmod(ninv, scale, q), wm = mulmod(wl, scale, q);
+      dc.ninv_mac[j] = nm, dc.ninv_mac_p[j] = comp(nm, q);
+      dc.wlast_mac[j] = wm, dc.wlast_mac_p[j] = comp(wm, q);
+      uint32_t qi = 1;  // q^-1 mod 2^32 by Newton iteration (q odd)
+      for (int it = 0; it < 5; ++it) qi *= 2u - (uint32_t)q * qi;
+      dc.qneg_inv32[j] = (uint32_t)(0u - qi);
+    }
     // floor(Q/t) = (Q - (Q mod t)) / t and Q = 0 mod q_j  =>  floor(Q/t) = -(Q mod t) t^-1 mod q_j
     const uint64_t tinv = powmod(t % q, q - 2, q);
     const uint64_t delta = mulmod((q - qmt % q) % q, tinv, q);

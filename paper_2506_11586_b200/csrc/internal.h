@@ -37,6 +37,13 @@ struct DevConsts {
   const uint2* tw32_fwd_h;
   const uint2* tw32_inv_h;
   uint64_t one_wp[SECN_MAX_LIMBS];  // word-sized Shoup companion of 1
+  // inverse NTT after the NTT-domain MAC (k_mac's outputs): when mac_redc, k_mac reduces the MAC
+  // sums by Montgomery REDC (x 2^-32), so these are N^-1 2^32 and psi^-brv(1) N^-1 2^32
+  // (otherwise equal to ninv / wlast); qneg_inv32 = -q^-1 mod 2^32
+  uint64_t ninv_mac[SECN_MAX_LIMBS], ninv_mac_p[SECN_MAX_LIMBS];
+  uint64_t wlast_mac[SECN_MAX_LIMBS], wlast_mac_p[SECN_MAX_LIMBS];
+  uint64_t qneg_inv32[SECN_MAX_LIMBS];
+  uint32_t mac_redc;  // 1: 32-bit limbs with every q < 2^27 (G q < 2^32 for G <= 32): k_mac uses REDC
 };
 
 struct PlanDev {  // the subset of secn_conv_plan (kind 0) / secn_fc_plan (kind 1) the kernels use

@@ -8,6 +8,7 @@
 // performs all HE MAC operations in NTT, and only transforms the final HE results back"),
 // PAPER.md:431 (§7: server share add, random mask), PAPER.md:668-679 (App. C.1 NTT).
 #include <cstdio>
+#include <cstdlib>
 #include <utility>
 
 #include "internal.h"
@@ -395,8 +396,8 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN, 1>()
   const size_t pi = blockIdx.x / c.L;
   const W q = (W)c.q[j], qb = A::bound(q);
   const typename A::Tw* tw = Tab<A>::inv(c) + (size_t)j * N;
-  const typename A::Tw ninv = Tab<A>::pair(c.ninv[j], c.ninv_p[j]);
-  const typename A::Tw wl = Tab<A>::pair(c.wlast[j], c.wlast_p[j]);
+  const typename A::Tw ninv = Tab<A>::pair(c.ninv_mac[j], c.ninv_mac_p[j]);  // inputs are k_mac outputs
+  const typename A::Tw wl = Tab<A>::pair(c.wlast_mac[j], c.wlast_mac_p[j]);
   const EncK ek(c, j);
   const bool mask = r != nullptr && (pi & 1);
   W em[16];
@@ -485,6 +486,13 @@ __device__ __forceinline__ uint32_t reduce64(uint64_t a, uint32_t q, uint32_t r3
   const uint32_t lo = (uint32_t)a, hi = (uint32_t)(a >> 32);
   const uint32_t x = Arith32::shoup32(hi, r32, r32p, q) + (lo - __umulhi(lo, onep32) * q);  // [0, 4q)
   return csub32(csub32(x, 2 * q), q);
+}
+
+// Montgomery REDC of a 64-bit MAC sum: a 2^-32 mod q in [0, 2q) for a < q 2^32, with
+// qn = -q^-1 mod 2^32 (one IMAD and one IMAD.WIDE; the 2^32 is folded into the INTT's N^-1)
+__device__ __forceinline__ uint32_t redc32(uint64_t a, uint32_t q, uint32_t qn) {
+  const uint32_t m = (uint32_t)a * qn;
+  return (uint32_t)((a + (uint64_t)m * q) >> 32);
 }
 
 template <class W>
@@ -703,6 +711,7 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
       twe[twe_pos<Tw>(l, g)] = tinv[(N >> (l + 1)) + (e0 >> (l + 1)) + g];
     }
   }
+  const uint32_t qn = (uint32_t)c.qneg_inv32[j];
   const uint32_t r32 = (uint32_t)c.r32[j], r32p = (uint32_t)c.r32_p[j], onep32 = (uint32_t)(onep >> 32);
   mbar_wait(xbar, 0);
   int st = 0;
@@ -719,7 +728,7 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
         uint32_t xv[A2];
 #pragma unroll
         for (int a = 0; a < A2; ++a) xv[a] = xs[(g * A2 + a) * MAC_THREADS + tid];
-        mbar_wait(&full[st], ph);
+        mbar_wait_sleep(&full[st], ph);
         const W* wst = ring + (size_t)st * MT * MAC_THREADS + tid;
 #pragma unroll
         for (int r = 0; r < MT; ++r) {
@@ -736,7 +745,9 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
       for (int r = 0; r < MT; ++r)
 #pragma unroll
         for (int a = 0; a < A2; ++a)
-          cbuf[(r * A2 + a) * MAC_CHS + phys(tid)] = (W)reduce64(acc[r][a], (uint32_t)q, r32, r32p, onep32);
+          cbuf[(r * A2 + a) * MAC_CHS + phys(tid)] =
+              c.mac_redc ? (W)redc32(acc[r][a], (uint32_t)q, qn)  // G q < 2^32; 2^-32 undone by ninv_mac
+                         : (W)reduce64(acc[r][a], (uint32_t)q, r32, r32p, onep32);
     } else {
       const uint64_t r64 = c.r64[j], r64p = c.r64_p[j];
       uint64_t lo[MT][A2], hi[MT][A2];
@@ -748,7 +759,7 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
         uint64_t xv[A2];
 #pragma unroll
         for (int a = 0; a < A2; ++a) xv[a] = xs[(g * A2 + a) * MAC_THREADS + tid];
-        mbar_wait(&full[st], ph);
+        mbar_wait_sleep(&full[st], ph);
         const W* wst = ring + (size_t)st * MT * MAC_THREADS + tid;
 #pragma unroll
         for (int r = 0; r < MT; ++r) {
@@ -877,8 +888,8 @@ __global__ void __launch_bounds__(LWE_G * SECN_MAX_LIMBS)
     const W* buf = polys + (pi * L + j) * N;
 #pragma unroll
     for (int i = 0; i < 16; ++i) x[0][i] = buf[o + 256 * i];
-    gs_compute<A, LOGN, 8, 1>(x, tws, q, qb, Tab<A>::pair(c.ninv[j], c.ninv_p[j]),
-                              Tab<A>::pair(c.wlast[j], c.wlast_p[j]));
+    gs_compute<A, LOGN, 8, 1>(x, tws, q, qb, Tab<A>::pair(c.ninv_mac[j], c.ninv_mac_p[j]),
+                              Tab<A>::pair(c.wlast_mac[j], c.wlast_mac_p[j]));
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       W v = A::canon_gs(x[0][i], q);
@@ -1257,6 +1268,12 @@ static bool encode_tmap(CUtensorMap* m, int wb, int rank, const void* base, cons
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// tuning knobs read at every launch (SECN_MAC_SG, SECN_MAC_KB): used by tools/variant_sweep.py
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
+}
+
 template <class W, int SG, int MT>
 static cudaError_t mac_t(const DevConsts& c, const PlanDev& p, const void* xhat, const void* w, void* y,
                          cudaStream_t s) {
@@ -1266,7 +1283,8 @@ static cudaError_t mac_t(const DevConsts& c, const PlanDev& p, const void* xhat,
   // ring depth: fill ~110 KiB per CTA (two CTAs per SM) after the X^ tile, 4..32 stages
   const size_t chunks = (size_t)MT * 2 * SG * MAC_CHS * sizeof(W) + MAC_THREADS * 2 * sizeof(W);
   const size_t fixed = xtile + chunks;
-  const size_t budget = 110 * 1024 > fixed + 4 * stage ? 110 * 1024 - fixed : 4 * stage;
+  const size_t cta_budget = (size_t)env_int("SECN_MAC_KB", 110) * 1024;
+  const size_t budget = cta_budget > fixed + 4 * stage ? cta_budget - fixed : 4 * stage;
   int NS = (int)(budget / stage);
   NS = NS < 4 ? 4 : NS > 32 ? 32 : NS;
   const size_t smem = fixed + NS * stage + (2 * NS + 1) * sizeof(uint64_t);
@@ -1296,6 +1314,10 @@ static cudaError_t mac_t(const DevConsts& c, const PlanDev& p, const void* xhat,
     const double eff = (double)ctas / (double)(waves * wave) - 0.02 * (double)waves;
     if (eff > best_eff + 1e-9) best_eff = eff, best_nmr = nmr;
   }
+  // layers with few input groups or few output channels: one m-block per CTA (more, shorter CTAs
+  // hide the INTT-level latency better; measured on the SqueezeNet fire layers)
+  if (p.G <= 4 || p.M <= 48) best_nmr = mblocks;
+  if (const int nmr_env = env_int("SECN_MAC_NMR", 0)) best_nmr = nmr_env < mblocks ? nmr_env : mblocks;
   const int m_range = ((mblocks + best_nmr - 1) / best_nmr) * MT;
   const int n_mr = (p.M + m_range - 1) / m_range;
   // tensor maps: X^ [G][S*2][L][N] viewed as (N, L, 2S, G); W [M][G][L][N] as (N, G*L, M)
@@ -1321,13 +1343,19 @@ cudaError_t launch_mac(const DevConsts& c, const PlanDev& p, const void* xhat, c
                        cudaStream_t s) {
   if (p.M == 0 || p.S == 0) return cudaSuccess;
   if (p.G > 32) return cudaErrorInvalidValue;
-  // s-group: as many spatial blocks (<= 4) as keep the X^ tile within 64 KiB; accumulator block
-  // MT x 2SG <= 32 64-bit sums (32-bit limbs) or <= 12 128-bit sums (64-bit limbs), spill-free at
-  // the 96 registers two 288-thread CTAs per SM allow
+  // s-group: among the SG <= 4 whose X^ tile fits in 64 KiB, the one minimising
+  // n_sg (SG + 1/2), n_sg = ceil(S / SG): the MAC work including zero-padded blocks plus half a
+  // block per pass over the weights (fitted to the per-layer sweep in profiles/); ties go to the
+  // smaller SG. Accumulator block MT x 2SG <= 32 64-bit sums (32-bit limbs) or <= 12 128-bit sums
+  // (64-bit limbs), spill-free at the 96 registers two 288-thread CTAs per SM allow.
   const size_t wb = c.word_bits / 8;
-  int sg = 4;
-  while (sg > 1 && (size_t)p.G * 2 * sg * MAC_THREADS * wb > 64 * 1024) --sg;
-  if (sg > (int)p.S) sg = p.S;
+  int sg = 1;
+  for (int cand = 2; cand <= 4 && cand <= (int)p.S; ++cand) {
+    if ((size_t)p.G * 2 * cand * MAC_THREADS * wb > 64 * 1024) break;
+    const int nc = (int)((p.S + cand - 1) / cand), nb = (int)((p.S + sg - 1) / sg);
+    if (nc * (2 * cand + 1) < nb * (2 * sg + 1)) sg = cand;
+  }
+  if (const int sg_env = env_int("SECN_MAC_SG", 0)) sg = sg_env;
   if (c.word_bits == 32) {
     switch (sg) {
       case 1: return mac_t<uint32_t, 1, 16>(c, p, xhat, w, y, s);

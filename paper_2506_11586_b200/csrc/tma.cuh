@@ -34,6 +34,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// the same wait with a suspend-time hint: the warp sleeps in the try_wait until the phase
+// completes (or the hint expires) instead of re-issuing the poll loop
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n"
+      "WAITS_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1, %2;\n\t"
+      "@!P bra WAITS_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(1000000u)
+      : "memory");
+}
+
 // 1-D bulk copy of `bytes` (multiple of 16, both addresses 16-byte aligned) global -> shared,
 // completing `bytes` transactions on `bar`.
 __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
