@@ -106,17 +106,23 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN, NP>(
   for (int pp = 0; pp < NP; ++pp) {
     const size_t pi = grp * NP + pp;  // poly index (ct * 2 + component for ciphertext batches)
     const W* src = in + (pi * c.L + j) * N;
-    const bool share = x0 != nullptr && (pi & 1);
-    const uint64_t* xs = share ? x0 + (pi >> 1) * N : nullptr;
+    const bool share = x0 != nullptr && (pi & 1);  // uniform over the CTA
+    // every load of the poly (and of its share words) is issued before any is used, so their
+    // latencies overlap instead of chaining through the share-add branches
 #pragma unroll
     for (int k = 0; k < R0::NT; ++k)
 #pragma unroll
-      for (int i = 0; i < R0::GK; ++i) {
-        const uint32_t e = R0::addr(k, i);
-        W v = src[e];
-        if (share) v += enc_mod<A>(__ldg(&xs[e]), ek);  // < 2q: inside the CT domain
-        x[pp][k * R0::GK + i] = v;
-      }
+      for (int i = 0; i < R0::GK; ++i) x[pp][k * R0::GK + i] = src[R0::addr(k, i)];
+    if (share) {
+      const uint64_t* xs = x0 + (pi >> 1) * N;
+      uint64_t xv[16];
+#pragma unroll
+      for (int k = 0; k < R0::NT; ++k)
+#pragma unroll
+        for (int i = 0; i < R0::GK; ++i) xv[k * R0::GK + i] = __ldg(&xs[R0::addr(k, i)]);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) x[pp][i] += enc_mod<A>(xv[i], ek);  // < 2q: inside the CT domain
+    }
   }
   ct_compute<A, LOGN, 0, NP>(x, tws, q, qb);
   round_store<R0, W, NP, LOGN>(x, sm);
