@@ -429,8 +429,19 @@ def run_secn(args, word_bits, world, rank, local, dev, full):
     dom = max(range(3), key=lambda s: stage_ms[s])
     n_layers_active = sum(1 for d in st if d["mc"] > 0)
     achieved = sb[dom] / (stage_ms[dom] / 1e3) / 1e9
+    # DRAM traffic of the dominant kernel from the committed ncu --set full capture (per launch,
+    # its largest launch: conv10), next to that launch's algorithmic bytes
+    tr = None
+    trf = ROOT / "profiles" / "kmac_traffic.json"
+    if dom == 1 and trf.exists():
+        tr = json.loads(trf.read_text())
     roofline = {"bound": "hbm", "kernel": names[dom], "achieved": round(achieved, 1), "peak": hbm_peak,
-                "unit": "GB/s", "frac": round(achieved / hbm_peak, 4), "traffic": None,
+                "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
+                "traffic": tr["dram_bytes_per_launch"] if tr else None,
+                "traffic_note": (f"ncu DRAM read+write of one {tr['layer']} launch; algorithmic bytes of that launch "
+                                 f"{tr['algorithmic_bytes_per_launch']}; integer-multiply (fmaheavy) pipe "
+                                 f"{tr['fmaheavy_pct_of_peak_elapsed']}% busy: the launch is integer-pipe bound"
+                                 f" ({tr['source']})") if tr else None,
                 "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
                 "bytes_per_step": sb[dom], "launches_per_step": n_layers_active,
                 "avg_launch_us": round(stage_ms[dom] / n_layers_active * 1e3, 2),

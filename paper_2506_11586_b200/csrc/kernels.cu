@@ -387,7 +387,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((1 << LOGH) / 16, 1)
 // (coefficients o + 256 i) are coalesced in global memory, with the same 15 twiddles for every
 // thread: no shared memory, one load and one store per word.
 template <class A, int LOGN>
-__global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN, 1>())
+__global__ void __launch_bounds__((1 << LOGN) / 16, sizeof(typename A::W) == 4 && LOGN == 12 ? 4 : ntt_min_blocks<A, LOGN, 1>())
     k_ntt_inv_tail(typename A::W* polys, const __grid_constant__ DevConsts c, const uint64_t* __restrict__ r,
                    uint64_t* __restrict__ y0, const __grid_constant__ PlanDev pl, size_t ct0) {
   using W = typename A::W;
