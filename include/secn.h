@@ -96,11 +96,19 @@ int secn_ctx_destroy(secn_ctx* ctx);
 int secn_ctx_query(const secn_ctx* ctx, secn_ctx_info* info);
 const char* secn_last_error(void);
 
-/* Host only. Fills `p` from its geometry for ring degree 2^log_n using the byte-min rule of
- * reading R6 (or validates the caller's Hw,Ww when both are nonzero). coef_words64 = 8-byte
- * words per coefficient of one ciphertext component (L for 64-bit limbs, L/2 for 32-bit limbs);
- * it only weighs residue bytes against the 8-byte mask words in the byte model.
- * SECN_EUNSUPPORTED if no window fits (kh*kw > N or Hp < kh). */
+/* Host only. Fills `p` from its geometry for ring degree 2^log_n (or validates the caller's
+ * Hw,Ww when both are nonzero), choosing the packing window by `rule`:
+ *   SECN_PLAN_BYTES: the byte-min rule of reading R6 (the oracle's plan_conv);
+ *   SECN_PLAN_TIME:  reading R6b, the modelled device time of the integer-issue-bound path
+ *                    (output, MAC and input limb-polys plus bytes), G <= 32.
+ * The packing (and so the oracle's result for the same window) is exact for every window; the
+ * rule only picks the fastest. coef_words64 = 8-byte words per coefficient of one ciphertext
+ * component (L for 64-bit limbs, L/2 for 32-bit limbs). SECN_EUNSUPPORTED if no window fits
+ * (kh*kw > N or Hp < kh), SECN_EINVAL for an unknown rule. */
+#define SECN_PLAN_BYTES 0u
+#define SECN_PLAN_TIME 1u
+int secn_conv_plan_ex(uint32_t log_n, uint32_t coef_words64, uint32_t rule, secn_conv_plan_t* p);
+/* secn_conv_plan_ex with SECN_PLAN_TIME (the default the bench and the Python binding use). */
 int secn_conv_plan(uint32_t log_n, uint32_t coef_words64, secn_conv_plan_t* p);
 
 /* A1: in-place forward negacyclic NTT of n_polys polys [n_polys][L][N] (coefficient domain ->

@@ -347,9 +347,10 @@ int secn_ctx_query(const secn_ctx* ctx, secn_ctx_info* info) {
   return SECN_OK;
 }
 
-int secn_conv_plan(uint32_t log_n, uint32_t n_limbs /* coef_words64 */, secn_conv_plan_t* p) {
+int secn_conv_plan_ex(uint32_t log_n, uint32_t n_limbs /* coef_words64 */, uint32_t rule, secn_conv_plan_t* p) {
   if (!p) return fail(SECN_EINVAL, "NULL plan");
   if (log_n < 1 || log_n > 20 || n_limbs < 1) return fail(SECN_EUNSUPPORTED, "bad log_n / n_limbs");
+  if (rule > SECN_PLAN_TIME) return fail(SECN_EINVAL, "unknown plan rule %u", rule);
   const uint32_t n = 1u << log_n;
   if (!p->C || !p->H || !p->W || !p->M || !p->kh || !p->kw || !p->stride)
     return fail(SECN_EINVAL, "zero dimension in plan geometry");
@@ -359,15 +360,22 @@ int secn_conv_plan(uint32_t log_n, uint32_t n_limbs /* coef_words64 */, secn_con
     if (derive_plan(n, p->Hw, p->Ww, p) != 0) return fail(SECN_EINVAL, "caller Hw,Ww invalid for this geometry");
     return SECN_OK;
   }
-  // reading R6: minimise 8 L N (2GS + MG + 2MS) + 8 N MS; ties: fewer MGS, larger Hw, larger Ww
+  // SECN_PLAN_BYTES (reading R6): minimise 8 L N (2GS + MG + 2MS) + 8 N MS; ties: fewer MGS, larger
+  // Hw, larger Ww. SECN_PLAN_TIME (reading R6b): minimise the modelled device time of the
+  // integer-issue-bound path, in ns per limb-poly of 4096 coefficients:
+  //   13 per output limb-poly (INTT + mask), 1.3 per output limb-poly and input group (MAC),
+  //   6 per input limb-poly (share add + NTT), and 0.3 x the bytes at 6.45 TB/s;
+  // only plans with G <= 32 (the MAC kernel's limit); ties: fewer bytes, larger Hw, larger Ww.
   secn_conv_plan_t best{};
   bool have = false;
+  double best_t = 0;
   u128 best_cost = 0;
   uint64_t best_mgs = 0;
   const uint32_t Hp = (p->kh == 1 && p->kw == 1 && p->stride > 1) ? (p->H + 2 * p->pad - 1) / p->stride + 1
                                                                   : p->H + 2 * p->pad;
   const uint32_t Wp = (p->kh == 1 && p->kw == 1 && p->stride > 1) ? (p->W + 2 * p->pad - 1) / p->stride + 1
                                                                   : p->W + 2 * p->pad;
+  const double limb_polys = 2.0 * n_limbs * (double)n / 4096.0;  // limb-polys of 4096 words per ct component
   for (uint32_t Hw = p->kh; Hw <= Hp; ++Hw) {
     for (uint32_t Ww = p->kw; Ww <= Wp; ++Ww) {
       if ((uint64_t)Hw * Ww > n) break;
@@ -376,14 +384,29 @@ int secn_conv_plan(uint32_t log_n, uint32_t n_limbs /* coef_words64 */, secn_con
       const u128 G = c.G, S = c.S, M = c.M;
       const u128 cost = (u128)8 * n_limbs * n * (2 * G * S + M * G + 2 * M * S) + (u128)8 * n * M * S;
       const uint64_t mgs = (uint64_t)(M * G * S);
-      bool better = !have || cost < best_cost || (cost == best_cost && mgs < best_mgs) ||
-                    (cost == best_cost && mgs == best_mgs && (Hw > best.Hw || (Hw == best.Hw && Ww > best.Ww)));
+      bool better;
+      if (rule == SECN_PLAN_BYTES) {
+        better = !have || cost < best_cost || (cost == best_cost && mgs < best_mgs) ||
+                 (cost == best_cost && mgs == best_mgs && (Hw > best.Hw || (Hw == best.Hw && Ww > best.Ww)));
+      } else {
+        if (c.G > 32) continue;
+        const double ms = (double)(M * S), gs = (double)(G * S);
+        const double t = 2.0 * limb_polys * (13.0 * ms + 1.3 * ms * (double)c.G + 6.0 * gs) + 0.3 * (double)cost / 6450.0;
+        better = !have || t < best_t * (1 - 1e-12) ||
+                 (t <= best_t * (1 + 1e-12) &&
+                  (cost < best_cost || (cost == best_cost && (Hw > best.Hw || (Hw == best.Hw && Ww > best.Ww)))));
+        if (better) best_t = t;
+      }
       if (better) best = c, best_cost = cost, best_mgs = mgs, have = true;
     }
   }
   if (!have) return fail(SECN_EUNSUPPORTED, "unsupported shape: no window fits N");
   *p = best;
   return SECN_OK;
+}
+
+int secn_conv_plan(uint32_t log_n, uint32_t n_limbs /* coef_words64 */, secn_conv_plan_t* p) {
+  return secn_conv_plan_ex(log_n, n_limbs, SECN_PLAN_TIME, p);
 }
 
 // ---- residue-buffer calls, generic over the context's word size ----

@@ -27,6 +27,7 @@ STATUS = {0: "SECN_OK", -1: "SECN_EINVAL", -2: "SECN_EUNSUPPORTED", -3: "SECN_ER
           -5: "SECN_ECUDA", -6: "SECN_ESTATE"}
 
 EXPORTS = ("secn_ctx_create", "secn_ctx_destroy", "secn_ctx_query", "secn_last_error", "secn_conv_plan",
+           "secn_conv_plan_ex",
            "secn_ntt_fwd", "secn_ntt_inv", "secn_preprocess_weights", "secn_share_add", "secn_mask_add",
            "secn_he_conv2d_workspace", "secn_he_conv2d", "secn_he_conv2d_stage", "secn_extract_share",
            "secn32_ctx_create", "secn32_ntt_fwd", "secn32_ntt_inv", "secn32_preprocess_weights",
@@ -96,6 +97,7 @@ def lib(path=None) -> ctypes.CDLL:
         "secn_ctx_query": (i, [vp, ctypes.POINTER(CtxInfo)]),
         "secn_last_error": (ctypes.c_char_p, []),
         "secn_conv_plan": (i, [u32, u32, P]),
+        "secn_conv_plan_ex": (i, [u32, u32, u32, P]),
         "secn_ntt_fwd": (i, [vp, vp, sz, vp]),
         "secn_ntt_inv": (i, [vp, vp, sz, vp]),
         "secn_preprocess_weights": (i, [vp, P, vp, vp, vp]),
@@ -134,11 +136,15 @@ def _check(status: int):
         raise SecnError(status, lib().secn_last_error().decode())
 
 
+PLAN_BYTES, PLAN_TIME = 0, 1  # SECN_PLAN_BYTES (reading R6), SECN_PLAN_TIME (reading R6b)
+
+
 def conv_plan(C, H, W, M, kh, kw=None, stride=1, pad=0, log_n=DEFAULT_LOG_N, n_limbs=len(DEFAULT_PRIMES),
-              Hw=0, Ww=0) -> Plan:
-    """secn_conv_plan: packing plan of one conv layer (byte-min rule, reading R6)."""
+              Hw=0, Ww=0, rule=PLAN_TIME) -> Plan:
+    """secn_conv_plan_ex: packing plan of one conv layer (rule PLAN_TIME: modelled device time,
+    reading R6b, the default; PLAN_BYTES: byte-min, reading R6; explicit Hw, Ww are validated)."""
     p = Plan(C=C, H=H, W=W, M=M, kh=kh, kw=kh if kw is None else kw, stride=stride, pad=pad, Hw=Hw, Ww=Ww)
-    _check(lib().secn_conv_plan(log_n, n_limbs, ctypes.byref(p)))
+    _check(lib().secn_conv_plan_ex(log_n, n_limbs, rule, ctypes.byref(p)))
     return p
 
 
@@ -217,8 +223,8 @@ class Context:
         """8-byte words per coefficient of a ciphertext component (the plan's byte model)."""
         return max(1, self.L * self.word_bits // 64)
 
-    def plan(self, C, H, W, M, kh, kw=None, stride=1, pad=0, Hw=0, Ww=0) -> Plan:
-        return conv_plan(C, H, W, M, kh, kw, stride, pad, self.log_n, self.coef_words64, Hw, Ww)
+    def plan(self, C, H, W, M, kh, kw=None, stride=1, pad=0, Hw=0, Ww=0, rule=PLAN_TIME) -> Plan:
+        return conv_plan(C, H, W, M, kh, kw, stride, pad, self.log_n, self.coef_words64, Hw, Ww, rule)
 
     # -- boundary calls ---------------------------------------------------------------------
     def ntt_fwd(self, polys: torch.Tensor, stream=None) -> torch.Tensor:

@@ -50,7 +50,7 @@ def test_library_is_sm100a_only():
 def test_c_plan_matches_oracle_plan(secn, net):
     fields = ("OH", "OW", "decim", "Hp", "Wp", "Cw", "Hw", "Ww", "G", "S", "nbh", "nbw", "O")
     for l in layers.network(net):
-        c = secn.conv_plan(l.C, l.H, l.W, l.M, l.k, stride=l.stride, pad=l.pad)
+        c = secn.conv_plan(l.C, l.H, l.W, l.M, l.k, stride=l.stride, pad=l.pad, rule=secn.PLAN_BYTES)
         o = packing.plan_conv(l.C, l.H, l.W, l.M, l.k, l.k, l.stride, l.pad, 4096, 2)
         assert tuple(getattr(c, f) for f in fields) == tuple(getattr(o, f) for f in fields), l.name
 
@@ -58,12 +58,47 @@ def test_c_plan_matches_oracle_plan(secn, net):
 def test_c_plan_other_ring_sizes_and_explicit_windows(secn):
     for l in [layers.ConvLayer("a", 64, 56, 56, 64, 3, 1, 1), layers.ConvLayer("b", 3, 224, 224, 64, 7, 2, 3)]:
         for logn, L in [(13, 2), (14, 4)]:
-            c = secn.conv_plan(l.C, l.H, l.W, l.M, l.k, stride=l.stride, pad=l.pad, log_n=logn, n_limbs=L)
+            c = secn.conv_plan(l.C, l.H, l.W, l.M, l.k, stride=l.stride, pad=l.pad, log_n=logn, n_limbs=L,
+                               rule=secn.PLAN_BYTES)
             o = packing.plan_conv(l.C, l.H, l.W, l.M, l.k, l.k, l.stride, l.pad, 1 << logn, L)
             assert (c.Cw, c.Hw, c.Ww, c.G, c.S, c.O) == (o.Cw, o.Hw, o.Ww, o.G, o.S, o.O)
     c = secn.conv_plan(8, 16, 16, 3, 3, pad=1, Hw=10, Ww=9)
     o = packing.plan_conv(8, 16, 16, 3, 3, 3, 1, 1, 4096, 2, Hw=10, Ww=9)
     assert (c.Cw, c.G, c.S, c.nbh, c.nbw, c.O) == (o.Cw, o.G, o.S, o.nbh, o.nbw, o.O)
+
+
+def _time_rule(l, n, cw):
+    """Reading R6b restated: the window minimising the modelled time (include/secn.h)."""
+    OH, OW, decim, Hp, Wp, Ph, Pw = packing._geometry(l.C, l.H, l.W, l.k, l.k, l.stride, l.pad)
+    best = None
+    for a in range(l.k, Hp + 1):
+        for b in range(l.k, Wp + 1):
+            if a * b > n:
+                break
+            o = packing.plan_conv(l.C, l.H, l.W, l.M, l.k, l.k, l.stride, l.pad, n, cw, Hw=a, Ww=b)
+            if o.G > 32:
+                continue
+            G, S, M = o.G, o.S, l.M
+            cost = 8 * cw * n * (2 * G * S + M * G + 2 * M * S) + 8 * n * M * S
+            lp = 2.0 * cw * n / 4096.0
+            t = 2.0 * lp * (13.0 * M * S + 1.3 * M * S * G + 6.0 * G * S) + 0.3 * cost / 6450.0
+            key = (t, cost, -a, -b)
+            if best is None or key[0] < best[0][0] * (1 - 1e-12) or (
+                    key[0] <= best[0][0] * (1 + 1e-12) and key[1:] < best[0][1:]):
+                best = (key, o)
+    return best[1]
+
+
+@pytest.mark.parametrize("net", ["tiny", "squeezenet1_1", "squeezenet1_0"])
+def test_c_time_plan_matches_python_rule(secn, net):
+    """The default plan (reading R6b): a valid window of the oracle's packing, G <= 32, equal to
+    the rule restated in Python, and never modelled slower than the byte-min plan."""
+    fields = ("OH", "OW", "decim", "Hp", "Wp", "Cw", "Hw", "Ww", "G", "S", "nbh", "nbw", "O")
+    for l in layers.network(net):
+        c = secn.conv_plan(l.C, l.H, l.W, l.M, l.k, stride=l.stride, pad=l.pad)
+        o = _time_rule(l, 4096, 2)
+        assert tuple(getattr(c, f) for f in fields) == tuple(getattr(o, f) for f in fields), l.name
+        assert c.G <= 32
 
 
 @pytest.mark.parametrize("n_i,n_o,logn,cw", [(2048, 1000, 12, 2), (512, 1000, 12, 2), (64, 16, 12, 2), (4096, 1, 12, 1),

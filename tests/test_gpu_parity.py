@@ -73,7 +73,11 @@ def env(request, secn):
 
 
 def oplan(P, ctx, lay):
-    return packing.plan_conv(lay.C, lay.H, lay.W, lay.M, lay.k, lay.k, lay.stride, lay.pad, P.n, ctx.coef_words64)
+    """The oracle's plan for the packing window the library chose (the window is a performance
+    choice; the oracle computes the same packing for any valid window)."""
+    c = ctx.plan(lay.C, lay.H, lay.W, lay.M, lay.k, stride=lay.stride, pad=lay.pad)
+    return packing.plan_conv(lay.C, lay.H, lay.W, lay.M, lay.k, lay.k, lay.stride, lay.pad, P.n, ctx.coef_words64,
+                             Hw=c.Hw, Ww=c.Ww)
 
 
 # ---------------------------------------------------------------------------------------------
@@ -207,7 +211,7 @@ def test_he_conv2d_other_ring_degrees(secn, logn, wb):
     P = Params(logn=logn, primes=primes)
     D = Dev(ctx)
     lay = L_("n", 20, 30, 30, 6, 3, 1, 1)
-    opl = packing.plan_conv(lay.C, lay.H, lay.W, lay.M, lay.k, lay.k, lay.stride, lay.pad, P.n, ctx.coef_words64)
+    opl = oplan(P, ctx, lay)
     ct, x0, K, r = _layer_inputs(P, lay, 21, opl)
     plan = ctx.plan(lay.C, lay.H, lay.W, lay.M, lay.k, stride=lay.stride, pad=lay.pad)
     w = ctx.preprocess_weights(plan, TP(K))
