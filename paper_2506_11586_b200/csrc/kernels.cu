@@ -1363,6 +1363,10 @@ cudaError_t launch_mac(const DevConsts& c, const PlanDev& p, const void* xhat, c
   }
   if (const int sg_env = env_int("SECN_MAC_SG", 0)) sg = sg_env;
   if (c.word_bits == 32) {
+    // SG = 1 with a large X^ tile: 8 output channels per m-block keep two CTAs per SM (the
+    // 16-channel block's chunks and 16 KiB ring stages would leave one)
+    const bool half = sg == 1 && env_int("SECN_MAC_MT", (size_t)p.G * 2 * MAC_THREADS * wb > 24 * 1024 ? 8 : 16) == 8;
+    if (half) return mac_t<uint32_t, 1, 8>(c, p, xhat, w, y, s);
     switch (sg) {
       case 1: return mac_t<uint32_t, 1, 16>(c, p, xhat, w, y, s);
       case 2: return mac_t<uint32_t, 2, 8>(c, p, xhat, w, y, s);
