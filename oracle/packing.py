@@ -10,18 +10,26 @@ pinned by the end-to-end test decrypt(server(Enc(x))) = conv(x, K) mod 2^t.
 
 Geometry
     Xe      effective input: zero-padded by `pad`, and for a 1x1 kernel with stride > 1
-            pre-decimated to Xe[c, i, j] = Xpad[c, i*stride, j*stride] (reading R7)
+            pre-decimated to Xe[c, i, j] = Xpad[c, i*stride, j*stride] (reading R7, decim = 1);
+            for a larger kernel with stride s > 1 optionally split into its s^2 polyphase
+            components (reading R7b, decim = 2): Ce = C s^2 channels
+                Xe[(c s + u) s + v, i, j] = Xpad[c, i s + u, j s + v],
+            and the kernel likewise, Ke[m, (c s + u) s + v, a, b] = K[m, c, s a + u, s b + v]
+            (0 where s a + u >= kh or s b + v >= kw), of size khe x kwe = ceil(kh/s) x ceil(kw/s).
+            Then y[oy, ox] = sum_{c',a,b} Xe[c', oy+a, ox+b] Ke[m, c', a, b] -- a stride-1
+            correlation whose every window position is an output (no strided designation).
+    Ce, khe, kwe   the channel count and kernel extent the windows use (C, kh, kw unless decim = 2)
     Hp, Wp  extent of Xe;  Ph, Pw = number of stride-1 window positions that must be covered
     window  Cw channels x Hw rows x Ww cols per polynomial, Cw*Hw*Ww <= N
-    G       = ceil(C / Cw) channel groups;  S = nbh * nbw spatial blocks
-    O       = (Cw-1)*Hw*Ww + (kh-1)*Ww + (kw-1)
+    G       = ceil(Ce / Cw) channel groups;  S = nbh * nbw spatial blocks
+    O       = (Cw-1)*Hw*Ww + (khe-1)*Ww + (kwe-1)
 
-    input poly (g, s), s = bh*nbw + bw, origin (h0, w0) = (bh*(Hw-kh+1), bw*(Ww-kw+1)):
+    input poly (g, s), s = bh*nbw + bw, origin (h0, w0) = (bh*(Hw-khe+1), bw*(Ww-kwe+1)):
         coeff[c*Hw*Ww + i*Ww + j] = Xe[g*Cw + c, h0+i, w0+j]      (0 outside Xe)
     kernel poly (m, g):
-        coeff[O - c*Hw*Ww - l*Ww - l'] = K[m, g*Cw + c, l, l']
-    output poly (m, s), designated coefficient O + i*Ww + j (0 <= i <= Hw-kh, 0 <= j <= Ww-kw)
-        = sum_{c,l,l'} Xe[c, h0+i+l, w0+j+l'] K[m, c, l, l']  = stride-1 output at (h0+i, w0+j)
+        coeff[O - c*Hw*Ww - l*Ww - l'] = Ke[m, g*Cw + c, l, l']
+    output poly (m, s), designated coefficient O + i*Ww + j (0 <= i <= Hw-khe, 0 <= j <= Ww-kwe)
+        = sum_{c,l,l'} Xe[c, h0+i+l, w0+j+l'] Ke[m, c, l, l']  = stride-1 output at (h0+i, w0+j)
 """
 from __future__ import annotations
 
@@ -54,37 +62,65 @@ class Plan:
     nbw: int
     O: int
 
+    @property
+    def ps(self) -> int:
+        """polyphase factor (reading R7b): the stride when decim = 2, else 1"""
+        return self.stride if self.decim == 2 else 1
 
-def _geometry(C, H, W, kh, kw, stride, pad):
+    @property
+    def Ce(self) -> int:
+        return self.C * self.ps * self.ps
+
+    @property
+    def khe(self) -> int:
+        return -(-self.kh // self.ps)
+
+    @property
+    def kwe(self) -> int:
+        return -(-self.kw // self.ps)
+
+
+def _geometry(C, H, W, kh, kw, stride, pad, poly=False):
+    """(OH, OW, decim, Hp, Wp, Ph, Pw); poly requests the polyphase split (reading R7b), which
+    applies to strided kernels larger than 1x1 only."""
     OH = (H + 2 * pad - kh) // stride + 1
     OW = (W + 2 * pad - kw) // stride + 1
     decim = 1 if (kh == 1 and kw == 1 and stride > 1) else 0
-    if decim:
+    if poly:
+        if decim or stride == 1:
+            raise ValueError("polyphase packing needs stride > 1 and a kernel larger than 1x1")
+        decim = 2
+    if decim == 1:
         Hp, Wp, Ph, Pw = OH, OW, OH, OW
+    elif decim == 2:
+        Hp, Wp, Ph, Pw = -(-(H + 2 * pad) // stride), -(-(W + 2 * pad) // stride), OH, OW
     else:
         Hp, Wp = H + 2 * pad, W + 2 * pad
         Ph, Pw = (OH - 1) * stride + 1, (OW - 1) * stride + 1
     return OH, OW, decim, Hp, Wp, Ph, Pw
 
 
-def plan_conv(C, H, W, M, kh, kw, stride=1, pad=0, n=4096, L=2, Hw=None, Ww=None) -> Plan:
-    """Reading R6: enumerate Hw in [kh, Hp], Ww in [kw, Wp] with Hw*Ww <= N, take
-    Cw = min(C, N // (Hw*Ww)), and minimise the algorithmic bytes
+def plan_conv(C, H, W, M, kh, kw, stride=1, pad=0, n=4096, L=2, Hw=None, Ww=None, poly=False) -> Plan:
+    """Reading R6: enumerate Hw in [khe, Hp], Ww in [kwe, Wp] with Hw*Ww <= N, take
+    Cw = min(Ce, N // (Hw*Ww)), and minimise the algorithmic bytes
         8*L*N*(2*G*S + M*G + 2*M*S) + 8*N*M*S
     tie-breaking on fewer M*G*S products, then larger Hw, then larger Ww.
-    An explicit (Hw, Ww) is validated and used instead."""
-    OH, OW, decim, Hp, Wp, Ph, Pw = _geometry(C, H, W, kh, kw, stride, pad)
+    An explicit (Hw, Ww) is validated and used instead. poly: the polyphase split of reading
+    R7b (strided kernels larger than 1x1)."""
+    OH, OW, decim, Hp, Wp, Ph, Pw = _geometry(C, H, W, kh, kw, stride, pad, poly)
     if OH <= 0 or OW <= 0 or kh * kw > n:
         raise ValueError("unsupported shape")
+    ps = stride if decim == 2 else 1
+    Ce, khe, kwe = C * ps * ps, -(-kh // ps), -(-kw // ps)
     best = None
-    cands = [(Hw, Ww)] if Hw is not None else [(a, b) for a in range(kh, Hp + 1) for b in range(kw, Wp + 1)]
+    cands = [(Hw, Ww)] if Hw is not None else [(a, b) for a in range(khe, Hp + 1) for b in range(kwe, Wp + 1)]
     for a, b in cands:
-        if a < kh or b < kw or a * b > n:
+        if a < khe or b < kwe or a * b > n or a > Hp or b > Wp:
             continue
-        Cw = min(C, n // (a * b))
-        G = -(-C // Cw)
-        nbh = -(-Ph // (a - kh + 1))
-        nbw = -(-Pw // (b - kw + 1))
+        Cw = min(Ce, n // (a * b))
+        G = -(-Ce // Cw)
+        nbh = -(-Ph // (a - khe + 1))
+        nbw = -(-Pw // (b - kwe + 1))
         S = nbh * nbw
         cost = 8 * L * n * (2 * G * S + M * G + 2 * M * S) + 8 * n * M * S
         key = (cost, M * G * S, -a, -b)
@@ -93,16 +129,26 @@ def plan_conv(C, H, W, M, kh, kw, stride=1, pad=0, n=4096, L=2, Hw=None, Ww=None
     if best is None:
         raise ValueError("unsupported shape: no window fits N")
     _, a, b, Cw, G, S, nbh, nbw = best
-    O = (Cw - 1) * a * b + (kh - 1) * b + (kw - 1)
+    O = (Cw - 1) * a * b + (khe - 1) * b + (kwe - 1)
     return Plan(C, H, W, M, kh, kw, stride, pad, OH, OW, decim, Hp, Wp, Cw, a, b, G, S, nbh, nbw, O)
 
 
 def effective_input(x: np.ndarray, p: Plan) -> np.ndarray:
-    """Zero-pad (and for decimated 1x1/stride>1 plans, subsample) the input share (C,H,W)."""
+    """Zero-pad the input share (C,H,W); for decimated 1x1/stride>1 plans subsample it, for
+    polyphase plans split it into Xe[(c s + u) s + v, i, j] = Xpad[c, i s + u, j s + v]."""
     xp = np.zeros((p.C, p.H + 2 * p.pad, p.W + 2 * p.pad), dtype=np.uint64)
     xp[:, p.pad:p.pad + p.H, p.pad:p.pad + p.W] = x
-    if p.decim:
+    if p.decim == 1:
         xp = xp[:, ::p.stride, ::p.stride][:, :p.OH, :p.OW]
+    elif p.decim == 2:
+        s = p.stride
+        xe = np.zeros((p.Ce, p.Hp, p.Wp), dtype=np.uint64)
+        for c in range(p.C):
+            for u in range(s):
+                for v in range(s):
+                    comp = xp[c, u::s, v::s]
+                    xe[(c * s + u) * s + v, :comp.shape[0], :comp.shape[1]] = comp
+        xp = xe
     return np.ascontiguousarray(xp)
 
 
@@ -114,10 +160,10 @@ def pack_input(x: np.ndarray, p: Plan, n: int) -> np.ndarray:
         for bh in range(p.nbh):
             for bw in range(p.nbw):
                 s = bh * p.nbw + bw
-                h0, w0 = bh * (p.Hw - p.kh + 1), bw * (p.Ww - p.kw + 1)
+                h0, w0 = bh * (p.Hw - p.khe + 1), bw * (p.Ww - p.kwe + 1)
                 for c in range(p.Cw):
                     cc = g * p.Cw + c
-                    if cc >= p.C:
+                    if cc >= p.Ce:
                         break
                     for i in range(p.Hw):
                         if h0 + i >= p.Hp:
@@ -128,18 +174,33 @@ def pack_input(x: np.ndarray, p: Plan, n: int) -> np.ndarray:
     return out
 
 
+def effective_kernel(K: np.ndarray, p: Plan) -> np.ndarray:
+    """Kernel (M,C,kh,kw) -> (M,Ce,khe,kwe): itself, or its polyphase split (reading R7b)."""
+    if p.decim != 2:
+        return K
+    s = p.stride
+    Ke = np.zeros((K.shape[0], p.Ce, p.khe, p.kwe), dtype=K.dtype)
+    for c in range(p.C):
+        for u in range(s):
+            for v in range(s):
+                comp = K[:, c, u::s, v::s]
+                Ke[:, (c * s + u) * s + v, :comp.shape[1], :comp.shape[2]] = comp
+    return Ke
+
+
 def kernel_polys(K: np.ndarray, p: Plan, n: int) -> np.ndarray:
     """Kernel (M,C,kh,kw) values < 2^t -> raw mirrored plaintext polys [M][G][N] (not lifted)."""
+    Ke = effective_kernel(K, p)
     out = np.zeros((p.M, p.G, n), dtype=np.uint64)
     for m in range(p.M):
         for g in range(p.G):
             for c in range(p.Cw):
                 cc = g * p.Cw + c
-                if cc >= p.C:
+                if cc >= p.Ce:
                     break
-                for l in range(p.kh):
-                    for l2 in range(p.kw):
-                        out[m, g, p.O - c * p.Hw * p.Ww - l * p.Ww - l2] = K[m, cc, l, l2]
+                for l in range(p.khe):
+                    for l2 in range(p.kwe):
+                        out[m, g, p.O - c * p.Hw * p.Ww - l * p.Ww - l2] = Ke[m, cc, l, l2]
     return out
 
 
@@ -165,8 +226,8 @@ def designated_map(p: Plan):
     sh = 1 if p.decim else p.stride
     oy, ox = np.meshgrid(np.arange(p.OH), np.arange(p.OW), indexing="ij")
     py, px = oy * sh, ox * sh
-    bh, i = py // (p.Hw - p.kh + 1), py % (p.Hw - p.kh + 1)
-    bw, j = px // (p.Ww - p.kw + 1), px % (p.Ww - p.kw + 1)
+    bh, i = py // (p.Hw - p.khe + 1), py % (p.Hw - p.khe + 1)
+    bw, j = px // (p.Ww - p.kwe + 1), px % (p.Ww - p.kwe + 1)
     return bh * p.nbw + bw, p.O + i * p.Ww + j
 
 

@@ -112,8 +112,9 @@ def test_mask_zero_and_unmask():
     assert ((dec - r[0]) % np.uint64(P.t) == m).all()
 
 
-def _e2e(layer, P, seed, full_range=False, with_x0=True):
-    pl = packing.plan_conv(layer.C, layer.H, layer.W, layer.M, layer.k, layer.k, layer.stride, layer.pad, P.n, P.L)
+def _e2e(layer, P, seed, full_range=False, with_x0=True, poly=False, Hw=None, Ww=None):
+    pl = packing.plan_conv(layer.C, layer.H, layer.W, layer.M, layer.k, layer.k, layer.stride, layer.pad, P.n, P.L,
+                           Hw=Hw, Ww=Ww, poly=poly)
     g = inputs.rng(seed)
     x1 = inputs.uniform_below(g, (layer.C, layer.H, layer.W), P.t)
     x0 = inputs.uniform_below(g, (layer.C, layer.H, layer.W), P.t) if with_x0 else np.zeros_like(x1)
@@ -163,6 +164,43 @@ def test_e2e_small_shapes_exact_n256(layer, seed, full):
     pl, y, ref = _e2e(layer, P, seed, full_range=full)
     assert pl.G * pl.S > 1
     assert (y == ref).all()
+
+
+@pytest.mark.parametrize("layer,seed,win", [
+    (L("poly_s2k3", 3, 23, 19, 4, 3, 2, 0), 31, None),          # conv1-like, odd extents
+    (L("poly_s2k3p1", 4, 16, 16, 3, 3, 2, 1), 32, (5, 6)),      # padded, several blocks
+    (L("poly_k7s2p3", 2, 20, 20, 3, 7, 2, 3), 33, None),        # 7x7 / 2 (ResNet conv1-like)
+    (L("poly_s3k5", 2, 17, 17, 2, 5, 3, 1), 34, (4, 4)),        # stride 3: 9 phases
+])
+def test_e2e_polyphase_exact_n256(layer, seed, win):
+    """Reading R7b: the polyphase packing of a strided kernel (Ce = C s^2 phase channels,
+    ceil(k/s)-sized kernel, every window position an output) decrypts to conv(x, K) mod 2^t."""
+    P = Params(logn=8, primes=params.PRIMES32 if seed % 2 else params.DEFAULT_PRIMES)
+    Hw, Ww = win if win else (None, None)
+    pl, y, ref = _e2e(layer, P, seed, poly=True, Hw=Hw, Ww=Ww)
+    assert pl.decim == 2 and pl.Ce == layer.C * layer.stride ** 2 and pl.khe == -(-layer.k // layer.stride)
+    assert (y == ref).all()
+
+
+def test_polyphase_split_reassembles():
+    """The polyphase split of input and kernel is a permutation (with zero fill) of the padded
+    input and the kernel: the phase correlation equals the strided correlation by brute force."""
+    g = inputs.rng(35)
+    C, H, W, M, k, s, pad = 2, 11, 9, 3, 3, 2, 1
+    pl = packing.plan_conv(C, H, W, M, k, k, s, pad, 256, 2, poly=True)
+    x = g.integers(0, 100, (C, H, W)).astype(np.uint64)
+    K = g.integers(0, 100, (M, C, k, k)).astype(np.uint64)
+    Xe, Ke = packing.effective_input(x, pl), packing.effective_kernel(K, pl)
+    xp = np.zeros((C, H + 2 * pad, W + 2 * pad), np.uint64)
+    xp[:, pad:pad + H, pad:pad + W] = x
+    for m in range(M):
+        for oy in range(pl.OH):
+            for ox in range(pl.OW):
+                a = sum(int(xp[c, oy * s + l, ox * s + l2]) * int(K[m, c, l, l2])
+                        for c in range(C) for l in range(k) for l2 in range(k))
+                b = sum(int(Xe[c2, oy + i, ox + j]) * int(Ke[m, c2, i, j])
+                        for c2 in range(pl.Ce) for i in range(pl.khe) for j in range(pl.kwe))
+                assert a == b
 
 
 def test_e2e_no_server_share():
