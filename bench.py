@@ -300,7 +300,7 @@ def run_secn(args, word_bits, world, rank, local, dev, full):
         m0, mc = sdist.m_slices(plan.M, world)[rank]
         ct, x0, K, r = layer_inputs(ctx.primes, n, t_bits, lay, plan.G, plan.S, plan.M, args.seed * 1000 + li)
         S = plan.S
-        d = {"lay": lay, "plan": plan, "win": (plan.Hw, plan.Ww), "m0": m0, "mc": mc, "ct_h": ct, "x0_h": x0,
+        d = {"lay": lay, "plan": plan, "win": (plan.Hw, plan.Ww, plan.decim == 2), "m0": m0, "mc": mc, "ct_h": ct, "x0_h": x0,
              "K_h": K, "r_h": r}
         if mc > 0:
             pl = plan.copy(M=mc)
@@ -704,9 +704,9 @@ def oracle_sample(net_states, frac, seed, check=None, primes=None, words64=2):
     bad = 0
     for li, d in enumerate(net_states):
         lay = d["lay"]
-        hw, ww = d["win"]  # the packing window the GPU path used (the oracle packs any valid window)
+        hw, ww, pz = d["win"]  # the packing window the GPU path used (the oracle packs any valid window)
         opl = packing.plan_conv(lay.C, lay.H, lay.W, lay.M, lay.k, lay.k, lay.stride, lay.pad, P.n, words64,
-                                Hw=hw, Ww=ww)
+                                Hw=hw, Ww=ww, poly=pz)
         n_out = opl.M * opl.S
         k = max(1, int(round(frac * n_out)))
         g = inputs.rng(seed + li)
@@ -764,9 +764,9 @@ def run_reference(args, world, rank):
     for li, lay in enumerate(net):
         win = _secn.conv_plan(lay.C, lay.H, lay.W, lay.M, lay.k, stride=lay.stride, pad=lay.pad, n_limbs=words64)
         opl = packing.plan_conv(lay.C, lay.H, lay.W, lay.M, lay.k, lay.k, lay.stride, lay.pad, P.n, words64,
-                                Hw=win.Hw, Ww=win.Ww)
+                                Hw=win.Hw, Ww=win.Ww, poly=win.decim == 2)
         ct, x0, K, r = layer_inputs(P.primes, P.n, P.t_bits, lay, opl.G, opl.S, opl.M, args.seed * 1000 + li)
-        states.append({"lay": lay, "win": (win.Hw, win.Ww), "ct_h": ct, "x0_h": x0, "K_h": K, "r_h": r})
+        states.append({"lay": lay, "win": (win.Hw, win.Ww, win.decim == 2), "ct_h": ct, "x0_h": x0, "K_h": K, "r_h": r})
     for w in range(args.warmup):
         oracle_sample(states, args.ref_frac / 4, 1000 + w, None, P.primes, words64)
     vals, meas_tot, thr, n_s, n_t = [], 0.0, 1, 0, 0

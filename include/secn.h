@@ -58,8 +58,13 @@ typedef enum {
 /* Packing plan for one convolution layer (reading R6-R8; Cheetah packing PAPER.md:131 §2.3,
  * :374 §6.1). Inputs: C,H,W,M,kh,kw,stride,pad (and optionally Hw,Ww). secn_conv_plan fills
  * the rest:
- *   OH,OW   output extent;  decim = 1 for a 1x1 kernel with stride > 1 (input pre-decimated)
- *   Hp,Wp   extent of the effective (padded, decimated) input the windows tile
+ *   OH,OW   output extent;  decim = 1 for a 1x1 kernel with stride > 1 (input pre-decimated);
+ *           decim = 2: polyphase packing of a strided kernel larger than 1x1 (reading R7b): the
+ *           window math below uses Ce = C s^2 phase channels Xe[(c s + u) s + v, i, j] =
+ *           Xpad[c, i s + u, j s + v] and the kernel extent khe x kwe = ceil(kh/s) x ceil(kw/s)
+ *           in place of C, kh, kw, and sh = 1 (every window position is an output). As an input
+ *           with explicit Hw, Ww, decim = 2 requests that packing.
+ *   Hp,Wp   extent of the effective (padded, decimated or phase-split) input the windows tile
  *   Cw,Hw,Ww window: Cw channels x Hw rows x Ww cols per polynomial, Cw*Hw*Ww <= N
  *   G = ceil(C/Cw) input channel groups; S = nbh*nbw spatial blocks
  *   O = (Cw-1)*Hw*Ww + (kh-1)*Ww + (kw-1), the offset of the first designated coefficient
@@ -70,8 +75,8 @@ typedef enum {
  * sh = stride (1 if decim). */
 typedef struct {
   uint32_t C, H, W, M, kh, kw, stride, pad; /* layer geometry (caller)                   */
-  uint32_t Hw, Ww;                          /* 0 = choose (byte-min rule); else validated  */
-  uint32_t OH, OW, decim, Hp, Wp;           /* filled                                      */
+  uint32_t Hw, Ww;                          /* 0 = choose (secn_conv_plan_ex rule); else validated */
+  uint32_t OH, OW, decim, Hp, Wp;           /* filled (decim = 2 also an input, see above) */
   uint32_t Cw, G, S, nbh, nbw, O;           /* filled                                      */
 } secn_conv_plan_t;
 

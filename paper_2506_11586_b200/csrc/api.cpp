@@ -120,35 +120,49 @@ int check_range(secn_ctx* ctx, const void* v, size_t n_words, int kind, cudaStre
   return SECN_OK;
 }
 
+// polyphase factor of a plan (reading R7b): the stride when decim = 2, else 1
+uint32_t plan_ps(const secn_conv_plan_t* p) { return p->decim == 2 ? p->stride : 1; }
+
 secn::PlanDev plan_dev(const secn_conv_plan_t* p) {
   secn::PlanDev d{};
-  d.M = p->M, d.G = p->G, d.S = p->S, d.Cw = p->Cw, d.Hw = p->Hw, d.Ww = p->Ww, d.kh = p->kh, d.kw = p->kw;
+  const uint32_t ps = plan_ps(p);
+  d.M = p->M, d.G = p->G, d.S = p->S, d.Cw = p->Cw, d.Hw = p->Hw, d.Ww = p->Ww;
+  d.kh = (p->kh + ps - 1) / ps, d.kw = (p->kw + ps - 1) / ps;  // the window's kernel extent
+  d.kh0 = p->kh, d.kw0 = p->kw, d.ps = ps;                      // the caller's kernel tensor
   d.C = p->C, d.O = p->O, d.OH = p->OH, d.OW = p->OW, d.nbh = p->nbh, d.nbw = p->nbw;
   d.sh = p->decim ? 1 : p->stride;
   return d;
 }
 
-// Recompute the derived fields of a plan from its geometry and (Hw, Ww); 0 if consistent.
-int derive_plan(uint32_t n, uint32_t Hw, uint32_t Ww, secn_conv_plan_t* p) {
+// Recompute the derived fields of a plan from its geometry, (Hw, Ww) and the polyphase choice
+// (reading R7b, strided kernels larger than 1x1 only); 0 if consistent.
+int derive_plan(uint32_t n, uint32_t Hw, uint32_t Ww, bool poly, secn_conv_plan_t* p) {
   const uint32_t C = p->C, kh = p->kh, kw = p->kw, st = p->stride, pad = p->pad;
   if (!C || !p->H || !p->W || !p->M || !kh || !kw || !st) return -1;
   if (p->H + 2 * pad < kh || p->W + 2 * pad < kw) return -1;
   const uint32_t OH = (p->H + 2 * pad - kh) / st + 1, OW = (p->W + 2 * pad - kw) / st + 1;
-  const uint32_t decim = (kh == 1 && kw == 1 && st > 1) ? 1 : 0;
+  uint32_t decim = (kh == 1 && kw == 1 && st > 1) ? 1 : 0;
+  if (poly) {
+    if (decim || st == 1) return -1;
+    decim = 2;
+  }
   uint32_t Hp, Wp, Ph, Pw;
-  if (decim) {
+  if (decim == 1) {
     Hp = Ph = OH, Wp = Pw = OW;
+  } else if (decim == 2) {
+    Hp = (p->H + 2 * pad + st - 1) / st, Wp = (p->W + 2 * pad + st - 1) / st, Ph = OH, Pw = OW;
   } else {
     Hp = p->H + 2 * pad, Wp = p->W + 2 * pad, Ph = (OH - 1) * st + 1, Pw = (OW - 1) * st + 1;
   }
-  if (Hw < kh || Ww < kw || Hw > Hp || Ww > Wp || (uint64_t)Hw * Ww > n) return -1;
-  const uint32_t Cw = C < n / (Hw * Ww) ? C : n / (Hw * Ww);
+  const uint32_t ps = decim == 2 ? st : 1, Ce = C * ps * ps, khe = (kh + ps - 1) / ps, kwe = (kw + ps - 1) / ps;
+  if (Hw < khe || Ww < kwe || Hw > Hp || Ww > Wp || (uint64_t)Hw * Ww > n) return -1;
+  const uint32_t Cw = Ce < n / (Hw * Ww) ? Ce : n / (Hw * Ww);
   p->OH = OH, p->OW = OW, p->decim = decim, p->Hp = Hp, p->Wp = Wp, p->Hw = Hw, p->Ww = Ww, p->Cw = Cw;
-  p->G = (C + Cw - 1) / Cw;
-  p->nbh = (Ph + (Hw - kh)) / (Hw - kh + 1);
-  p->nbw = (Pw + (Ww - kw)) / (Ww - kw + 1);
+  p->G = (Ce + Cw - 1) / Cw;
+  p->nbh = (Ph + (Hw - khe)) / (Hw - khe + 1);
+  p->nbw = (Pw + (Ww - kwe)) / (Ww - kwe + 1);
   p->S = p->nbh * p->nbw;
-  p->O = (Cw - 1) * Hw * Ww + (kh - 1) * Ww + (kw - 1);
+  p->O = (Cw - 1) * Hw * Ww + (khe - 1) * Ww + (kwe - 1);
   return 0;
 }
 
@@ -165,7 +179,8 @@ int check_ctx(const secn_ctx* ctx, uint32_t want_bits = 0) {
 int check_plan(const secn_ctx* ctx, const secn_conv_plan_t* p) {
   if (!p) return fail(SECN_EINVAL, "NULL plan");
   secn_conv_plan_t q = *p;
-  if (derive_plan(ctx->n, p->Hw, p->Ww, &q) != 0) return fail(SECN_EINVAL, "plan inconsistent with its geometry");
+  if (derive_plan(ctx->n, p->Hw, p->Ww, p->decim == 2, &q) != 0)
+    return fail(SECN_EINVAL, "plan inconsistent with its geometry");
   if (q.Cw != p->Cw || q.G != p->G || q.S != p->S || q.O != p->O || q.OH != p->OH || q.OW != p->OW ||
       q.decim != p->decim || q.nbh != p->nbh || q.nbw != p->nbw)
     return fail(SECN_EINVAL, "plan fields do not match secn_conv_plan() for this geometry and N");
@@ -356,8 +371,9 @@ int secn_conv_plan_ex(uint32_t log_n, uint32_t n_limbs /* coef_words64 */, uint3
     return fail(SECN_EINVAL, "zero dimension in plan geometry");
   if ((uint64_t)p->kh * p->kw > n || p->H + 2 * p->pad < p->kh || p->W + 2 * p->pad < p->kw)
     return fail(SECN_EUNSUPPORTED, "unsupported shape: window larger than N or input");
-  if (p->Hw && p->Ww) {
-    if (derive_plan(n, p->Hw, p->Ww, p) != 0) return fail(SECN_EINVAL, "caller Hw,Ww invalid for this geometry");
+  if (p->Hw && p->Ww) {  // explicit window; decim = 2 on input requests the polyphase packing
+    if (derive_plan(n, p->Hw, p->Ww, p->decim == 2, p) != 0)
+      return fail(SECN_EINVAL, "caller Hw,Ww (decim) invalid for this geometry");
     return SECN_OK;
   }
   // SECN_PLAN_BYTES (reading R6): minimise 8 L N (2GS + MG + 2MS) + 8 N MS; ties: fewer MGS, larger
@@ -371,33 +387,40 @@ int secn_conv_plan_ex(uint32_t log_n, uint32_t n_limbs /* coef_words64 */, uint3
   double best_t = 0;
   u128 best_cost = 0;
   uint64_t best_mgs = 0;
-  const uint32_t Hp = (p->kh == 1 && p->kw == 1 && p->stride > 1) ? (p->H + 2 * p->pad - 1) / p->stride + 1
-                                                                  : p->H + 2 * p->pad;
-  const uint32_t Wp = (p->kh == 1 && p->kw == 1 && p->stride > 1) ? (p->W + 2 * p->pad - 1) / p->stride + 1
-                                                                  : p->W + 2 * p->pad;
   const double limb_polys = 2.0 * n_limbs * (double)n / 4096.0;  // limb-polys of 4096 words per ct component
-  for (uint32_t Hw = p->kh; Hw <= Hp; ++Hw) {
-    for (uint32_t Ww = p->kw; Ww <= Wp; ++Ww) {
-      if ((uint64_t)Hw * Ww > n) break;
-      secn_conv_plan_t c = *p;
-      if (derive_plan(n, Hw, Ww, &c) != 0) continue;
-      const u128 G = c.G, S = c.S, M = c.M;
-      const u128 cost = (u128)8 * n_limbs * n * (2 * G * S + M * G + 2 * M * S) + (u128)8 * n * M * S;
-      const uint64_t mgs = (uint64_t)(M * G * S);
-      bool better;
-      if (rule == SECN_PLAN_BYTES) {
-        better = !have || cost < best_cost || (cost == best_cost && mgs < best_mgs) ||
-                 (cost == best_cost && mgs == best_mgs && (Hw > best.Hw || (Hw == best.Hw && Ww > best.Ww)));
-      } else {
-        if (c.G > 32) continue;
-        const double ms = (double)(M * S), gs = (double)(G * S);
-        const double t = 2.0 * limb_polys * (13.0 * ms + 1.3 * ms * (double)c.G + 6.0 * gs) + 0.3 * (double)cost / 6450.0;
-        better = !have || t < best_t * (1 - 1e-12) ||
-                 (t <= best_t * (1 + 1e-12) &&
-                  (cost < best_cost || (cost == best_cost && (Hw > best.Hw || (Hw == best.Hw && Ww > best.Ww)))));
-        if (better) best_t = t;
+  const bool can_poly = p->stride > 1 && !(p->kh == 1 && p->kw == 1);
+  for (int poly = 0; poly <= (rule == SECN_PLAN_TIME && can_poly ? 1 : 0); ++poly) {
+    const uint32_t ps = poly ? p->stride : 1;
+    const uint32_t khe = (p->kh + ps - 1) / ps, kwe = (p->kw + ps - 1) / ps;
+    const uint32_t Hp = poly ? (p->H + 2 * p->pad + ps - 1) / ps
+                              : ((p->kh == 1 && p->kw == 1 && p->stride > 1) ? (p->H + 2 * p->pad - 1) / p->stride + 1
+                                                                             : p->H + 2 * p->pad);
+    const uint32_t Wp = poly ? (p->W + 2 * p->pad + ps - 1) / ps
+                              : ((p->kh == 1 && p->kw == 1 && p->stride > 1) ? (p->W + 2 * p->pad - 1) / p->stride + 1
+                                                                             : p->W + 2 * p->pad);
+    for (uint32_t Hw = khe; Hw <= Hp; ++Hw) {
+      for (uint32_t Ww = kwe; Ww <= Wp; ++Ww) {
+        if ((uint64_t)Hw * Ww > n) break;
+        secn_conv_plan_t c = *p;
+        if (derive_plan(n, Hw, Ww, poly, &c) != 0) continue;
+        const u128 G = c.G, S = c.S, M = c.M;
+        const u128 cost = (u128)8 * n_limbs * n * (2 * G * S + M * G + 2 * M * S) + (u128)8 * n * M * S;
+        const uint64_t mgs = (uint64_t)(M * G * S);
+        bool better;
+        if (rule == SECN_PLAN_BYTES) {
+          better = !have || cost < best_cost || (cost == best_cost && mgs < best_mgs) ||
+                   (cost == best_cost && mgs == best_mgs && (Hw > best.Hw || (Hw == best.Hw && Ww > best.Ww)));
+        } else {
+          if (c.G > 32) continue;
+          const double ms = (double)(M * S), gs = (double)(G * S);
+          const double t = 2.0 * limb_polys * (13.0 * ms + 1.3 * ms * (double)c.G + 6.0 * gs) + 0.3 * (double)cost / 6450.0;
+          better = !have || t < best_t * (1 - 1e-12) ||
+                   (t <= best_t * (1 + 1e-12) &&
+                    (cost < best_cost || (cost == best_cost && (Hw > best.Hw || (Hw == best.Hw && Ww > best.Ww)))));
+          if (better) best_t = t;
+        }
+        if (better) best = c, best_cost = cost, best_mgs = mgs, have = true;
       }
-      if (better) best = c, best_cost = cost, best_mgs = mgs, have = true;
     }
   }
   if (!have) return fail(SECN_EUNSUPPORTED, "unsupported shape: no window fits N");

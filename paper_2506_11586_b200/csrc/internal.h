@@ -48,6 +48,8 @@ struct DevConsts {
 
 struct PlanDev {  // the subset of secn_conv_plan (kind 0) / secn_fc_plan (kind 1) the kernels use
   uint32_t M, G, S, Cw, Hw, Ww, kh, kw, C, O, OH, OW, nbh, nbw, sh;
+  uint32_t kh0, kw0, ps;  // the caller's kernel extent and the polyphase factor (reading R7b; kh, kw
+                          // above are the window's extent ceil(kh0/ps) x ceil(kw0/ps))
   uint32_t kind;         // 0: convolution, 1: fully connected (S = 1)
   uint32_t nib, nob, no; // fc: inputs per ct, output rows per ct, n_o (C holds n_i)
 };

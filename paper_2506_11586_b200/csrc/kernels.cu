@@ -952,15 +952,19 @@ __global__ void __launch_bounds__(LWE_G * SECN_MAX_LIMBS)
 template <class W>
 __global__ void k_pack_weights(const uint64_t* __restrict__ kern, W* __restrict__ w,
                                const __grid_constant__ DevConsts c, PlanDev pl) {
-  const size_t total = (size_t)pl.M * pl.C * pl.kh * pl.kw;
+  const size_t total = (size_t)pl.M * pl.C * pl.kh0 * pl.kw0;
   const size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   if (idx >= total) return;
-  const uint32_t l2 = idx % pl.kw;
-  const uint32_t l = (idx / pl.kw) % pl.kh;
-  const uint32_t ch = (idx / ((size_t)pl.kw * pl.kh)) % pl.C;
-  const uint32_t m = idx / ((size_t)pl.kw * pl.kh * pl.C);
-  const uint32_t g = ch / pl.Cw, cc = ch % pl.Cw;
-  const uint32_t coef = pl.O - cc * pl.Hw * pl.Ww - l * pl.Ww - l2;
+  const uint32_t l2 = idx % pl.kw0;
+  const uint32_t l = (idx / pl.kw0) % pl.kh0;
+  const uint32_t ch = (idx / ((size_t)pl.kw0 * pl.kh0)) % pl.C;
+  const uint32_t m = idx / ((size_t)pl.kw0 * pl.kh0 * pl.C);
+  // polyphase (reading R7b): tap (l, l2) of channel ch is tap (l / s, l2 / s) of phase channel
+  // (ch s + l % s) s + l2 % s; ps = 1 leaves everything as it is
+  const uint32_t s = pl.ps;
+  const uint32_t ce = (ch * s + l % s) * s + l2 % s, a = l / s, b = l2 / s;
+  const uint32_t g = ce / pl.Cw, cc = ce % pl.Cw;
+  const uint32_t coef = pl.O - cc * pl.Hw * pl.Ww - a * pl.Ww - b;
   const uint64_t t = 1ull << c.t_bits;
   const uint64_t v = kern[idx] & (t - 1);
   const size_t N = 1ull << c.log_n;
@@ -1388,7 +1392,7 @@ cudaError_t launch_pack_weights(const DevConsts& c, const PlanDev& p, const uint
   const size_t wb = c.word_bits / 8;
   cudaError_t e = cudaMemsetAsync(w, 0, (size_t)p.M * p.G * c.L * N * wb, s);
   if (e != cudaSuccess) return e;
-  const size_t total = (size_t)p.M * p.C * p.kh * p.kw;
+  const size_t total = (size_t)p.M * p.C * p.kh0 * p.kw0;
   if (!total) return cudaGetLastError();
   const unsigned blocks = (unsigned)((total + 255) / 256);
   if (c.word_bits == 64)

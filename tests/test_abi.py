@@ -68,24 +68,27 @@ def test_c_plan_other_ring_sizes_and_explicit_windows(secn):
 
 
 def _time_rule(l, n, cw):
-    """Reading R6b restated: the window minimising the modelled time (include/secn.h)."""
-    OH, OW, decim, Hp, Wp, Ph, Pw = packing._geometry(l.C, l.H, l.W, l.k, l.k, l.stride, l.pad)
+    """Reading R6b restated: the window (plain or, for strided kernels larger than 1x1,
+    polyphase, reading R7b) minimising the modelled time (include/secn.h)."""
     best = None
-    for a in range(l.k, Hp + 1):
-        for b in range(l.k, Wp + 1):
-            if a * b > n:
-                break
-            o = packing.plan_conv(l.C, l.H, l.W, l.M, l.k, l.k, l.stride, l.pad, n, cw, Hw=a, Ww=b)
-            if o.G > 32:
-                continue
-            G, S, M = o.G, o.S, l.M
-            cost = 8 * cw * n * (2 * G * S + M * G + 2 * M * S) + 8 * n * M * S
-            lp = 2.0 * cw * n / 4096.0
-            t = 2.0 * lp * (13.0 * M * S + 1.3 * M * S * G + 6.0 * G * S) + 0.3 * cost / 6450.0
-            key = (t, cost, -a, -b)
-            if best is None or key[0] < best[0][0] * (1 - 1e-12) or (
-                    key[0] <= best[0][0] * (1 + 1e-12) and key[1:] < best[0][1:]):
-                best = (key, o)
+    for poly in ([False, True] if l.stride > 1 and l.k > 1 else [False]):
+        OH, OW, decim, Hp, Wp, Ph, Pw = packing._geometry(l.C, l.H, l.W, l.k, l.k, l.stride, l.pad, poly)
+        ke = -(-l.k // l.stride) if poly else l.k
+        for a in range(ke, Hp + 1):
+            for b in range(ke, Wp + 1):
+                if a * b > n:
+                    break
+                o = packing.plan_conv(l.C, l.H, l.W, l.M, l.k, l.k, l.stride, l.pad, n, cw, Hw=a, Ww=b, poly=poly)
+                if o.G > 32:
+                    continue
+                G, S, M = o.G, o.S, l.M
+                cost = 8 * cw * n * (2 * G * S + M * G + 2 * M * S) + 8 * n * M * S
+                lp = 2.0 * cw * n / 4096.0
+                t = 2.0 * lp * (13.0 * M * S + 1.3 * M * S * G + 6.0 * G * S) + 0.3 * cost / 6450.0
+                key = (t, cost, -a, -b)
+                if best is None or key[0] < best[0][0] * (1 - 1e-12) or (
+                        key[0] <= best[0][0] * (1 + 1e-12) and key[1:] < best[0][1:]):
+                    best = (key, o)
     return best[1]
 
 

@@ -77,7 +77,7 @@ def oplan(P, ctx, lay):
     choice; the oracle computes the same packing for any valid window)."""
     c = ctx.plan(lay.C, lay.H, lay.W, lay.M, lay.k, stride=lay.stride, pad=lay.pad)
     return packing.plan_conv(lay.C, lay.H, lay.W, lay.M, lay.k, lay.k, lay.stride, lay.pad, P.n, ctx.coef_words64,
-                             Hw=c.Hw, Ww=c.Ww)
+                             Hw=c.Hw, Ww=c.Ww, poly=c.decim == 2)
 
 
 # ---------------------------------------------------------------------------------------------
