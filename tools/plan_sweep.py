@@ -25,22 +25,25 @@ T = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int64)).to(dev)
 
 def candidates(lay):
     C, H, W, M, k, st, pad = lay.C, lay.H, lay.W, lay.M, lay.k, lay.stride, lay.pad
-    OH, OW, decim, Hp, Wp, Ph, Pw = packing._geometry(C, H, W, k, k, st, pad)
     out = {}
-    for a in range(k, Hp + 1):
-        for b in range(k, Wp + 1):
-            if a * b > n:
-                continue
-            Cw = min(C, n // (a * b))
-            G = -(-C // Cw)
-            if G > 32:
-                continue
-            S = (-(-Ph // (a - k + 1))) * (-(-Pw // (b - k + 1)))
-            byt = 16 * n * (2 * G * S + M * G + 2 * M * S) + 8 * n * M * S
-            t = 13e-3 * (2 * L * M * S) + 1.3e-3 * (2 * L * M * S * G) + 6e-3 * (2 * L * G * S) + byt / 6450e3 * 0.3
-            key = (G, S)  # plans with the same (G, S) cost the same: keep the first (largest window)
-            if key not in out or (a * b) > out[key][1] * out[key][2]:
-                out[key] = (t, a, b)
+    for poly in ([False, True] if st > 1 and k > 1 else [False]):
+        OH, OW, decim, Hp, Wp, Ph, Pw = packing._geometry(C, H, W, k, k, st, pad, poly)
+        ps = st if poly else 1
+        Ce, ke = C * ps * ps, -(-k // ps)
+        for a in range(ke, Hp + 1):
+            for b in range(ke, Wp + 1):
+                if a * b > n:
+                    continue
+                Cw = min(Ce, n // (a * b))
+                G = -(-Ce // Cw)
+                if G > 32:
+                    continue
+                S = (-(-Ph // (a - ke + 1))) * (-(-Pw // (b - ke + 1)))
+                byt = 16 * n * (2 * G * S + M * G + 2 * M * S) + 8 * n * M * S
+                t = 13e-3 * (2 * L * M * S) + 1.3e-3 * (2 * L * M * S * G) + 6e-3 * (2 * L * G * S) + byt / 6450e3 * 0.3
+                key = (G, S, poly)  # plans with the same (G, S) cost the same: keep the largest window
+                if key not in out or (a * b) > out[key][1] * out[key][2]:
+                    out[key] = (t, a, b, poly)
     return sorted(out.values())[:ncand]
 
 
@@ -74,19 +77,36 @@ def time_plan(plan, lay, g):
     return e0.elapsed_time(e1) / 20 * 1e3
 
 
+def _poly_plan(lay, a, b):
+    import ctypes
+
+    from paper_2506_11586_b200 import secn as m
+
+    p = m.Plan(C=lay.C, H=lay.H, W=lay.W, M=lay.M, kh=lay.k, kw=lay.k, stride=lay.stride, pad=lay.pad, Hw=a, Ww=b,
+               decim=2)
+    m._check(m.lib().secn_conv_plan_ex(ctx.log_n, ctx.coef_words64, 1, ctypes.byref(p)))
+    return p
+
+
 tot_def = tot_best = 0.0
 for lay in layers.network(net):
     g = inputs.rng(9)
     pdef = ctx.plan(lay.C, lay.H, lay.W, lay.M, lay.k, stride=lay.stride, pad=lay.pad)
     tdef = time_plan(pdef, lay, g)
-    res = [(tdef, pdef.Hw, pdef.Ww, pdef.G, pdef.S, "default")]
-    for tm, a, b in candidates(lay):
-        if (a, b) == (pdef.Hw, pdef.Ww):
+    res = [(tdef, pdef.Hw, pdef.Ww, pdef.G, pdef.S, f"default d{pdef.decim}")]
+    for tm, a, b, poly in candidates(lay):
+        if (a, b, poly) == (pdef.Hw, pdef.Ww, pdef.decim == 2):
             continue
         p = ctx.plan(lay.C, lay.H, lay.W, lay.M, lay.k, stride=lay.stride, pad=lay.pad, Hw=a, Ww=b)
-        res.append((time_plan(p, lay, g), a, b, p.G, p.S, f"model {tm:.1f}"))
+        if poly:
+            from paper_2506_11586_b200.secn import Plan, conv_plan  # noqa: F401
+            p = p.copy(decim=2)
+            p = conv_plan(lay.C, lay.H, lay.W, lay.M, lay.k, lay.k, lay.stride, lay.pad, ctx.log_n, ctx.coef_words64,
+                          a, b) if False else _poly_plan(lay, a, b)
+        res.append((time_plan(p, lay, g), a, b, p.G, p.S, f"model {tm:.1f}{' poly' if poly else ''}"))
     best = min(res)
     tot_def += tdef
     tot_best += best[0]
-    print(f"{lay.name:10s} " + "  ".join(f"[Hw={a} Ww={b} G={G} S={S}: {t:6.1f}us]" for t, a, b, G, S, _ in res), flush=True)
+    print(f"{lay.name:10s} " + "  ".join(f"[{tag} Hw={a} Ww={b} G={G} S={S}: {t:6.1f}us]" for t, a, b, G, S, tag in res),
+          flush=True)
 print(f"total default {tot_def:.1f} us, best-of-candidates {tot_best:.1f} us")
