@@ -381,6 +381,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((1 << LOGH) / 16, 1)
   cluster_wait();  // the partner is done reading this CTA's shared memory
 }
 
+// A8: y0 = -r mod t at the designated coefficients of output ciphertext `ct` (its mask row rs),
+// split over the CTA's threads: fc plans (kind 1) put output row m*nob + d at coefficient
+// d*nib + nib - 1; conv plans use the designation of include/secn.h (stride sh, window Hw x Ww).
+__device__ __forceinline__ void write_server_share_ct(const uint64_t* __restrict__ rs, uint64_t* __restrict__ y0,
+                                                      const PlanDev& pl, uint32_t ct, uint32_t t_bits) {
+  const uint64_t tm = (1ull << t_bits) - 1;
+  if (pl.kind == 1) {
+    for (uint32_t d = threadIdx.x; d < pl.nob; d += blockDim.x) {
+      const uint32_t o = ct * pl.nob + d;
+      if (o < pl.no) y0[o] = (tm + 1 - rs[d * pl.nib + pl.nib - 1]) & tm;
+    }
+    return;
+  }
+  const uint32_t m = ct / pl.S, sidx = ct % pl.S;
+  const uint32_t bh = sidx / pl.nbw, bw = sidx % pl.nbw;
+  const uint32_t dh = pl.Hw - pl.kh + 1, dw = pl.Ww - pl.kw + 1;
+  for (uint32_t d = threadIdx.x; d < dh * dw; d += blockDim.x) {
+    const uint32_t i = d / dw, jj = d - i * dw;
+    const uint32_t py = bh * dh + i, px = bw * dw + jj;
+    const uint32_t oy = py / pl.sh, ox = px / pl.sh;
+    if (oy * pl.sh != py || ox * pl.sh != px || oy >= pl.OH || ox >= pl.OW) continue;
+    y0[((size_t)m * pl.OH + oy) * pl.OW + ox] = (tm + 1 - rs[pl.O + i * pl.Ww + jj]) & tm;
+  }
+}
+
 // K3' (+A7 fused), the second half of secn_he_conv2d's inverse NTT: levels 8 .. LOGN-1 (with
 // N^-1) on limb-polys whose levels 0..7 were applied by the MAC kernel (inputs in the lazy GS
 // domain), then the mask on the b component. At N = 4096 this is one radix-16 round whose tasks
@@ -447,28 +472,60 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, sizeof(typename A::W) == 4 &
   // A8 fused (secn_he_conv2d_ex): the server's output share y0 = -r mod t at the designated
   // coefficients of this ciphertext (one CTA per ciphertext does it: limb 0, b component). It
   // depends on r only, so it never waits on the transform; it saves a launch per layer.
-  if (y0 != nullptr && mask && j == 0 && pl.kind == 1) {  // fc: y[m*nob + d] at d*nib + nib - 1
-    const uint32_t m = (uint32_t)(ct0 + (pi >> 1));
-    const uint64_t* rs = r + (pi >> 1) * N;
-    const uint64_t tm = (1ull << c.t_bits) - 1;
-    for (uint32_t d = threadIdx.x; d < pl.nob; d += N / 16) {
-      const uint32_t o = m * pl.nob + d;
-      if (o < pl.no) y0[o] = (tm + 1 - rs[d * pl.nib + pl.nib - 1]) & tm;
-    }
-  } else if (y0 != nullptr && mask && j == 0) {
-    const uint32_t ct = (uint32_t)(ct0 + (pi >> 1)), m = ct / pl.S, sidx = ct % pl.S;
-    const uint32_t bh = sidx / pl.nbw, bw = sidx % pl.nbw;
-    const uint32_t dh = pl.Hw - pl.kh + 1, dw = pl.Ww - pl.kw + 1;
-    const uint64_t* rs = r + (pi >> 1) * N;
-    const uint64_t tm = (1ull << c.t_bits) - 1;
-    for (uint32_t d = threadIdx.x; d < dh * dw; d += N / 16) {
-      const uint32_t i = d / dw, jj = d - i * dw;
-      const uint32_t py = bh * dh + i, px = bw * dw + jj;
-      const uint32_t oy = py / pl.sh, ox = px / pl.sh;
-      if (oy * pl.sh != py || ox * pl.sh != px || oy >= pl.OH || ox >= pl.OW) continue;
-      y0[((size_t)m * pl.OH + oy) * pl.OW + ox] = (tm + 1 - rs[pl.O + i * pl.Ww + jj]) & tm;
-    }
+  if (y0 != nullptr && mask && j == 0) write_server_share_ct(r + (pi >> 1) * N, y0, pl, (uint32_t)(ct0 + (pi >> 1)), c.t_bits);
+}
+
+// The same tail at N = 4096 with both components of one (ciphertext, limb) per CTA: the pair
+// shares the twiddles and the index arithmetic and every thread keeps 32 independent words in
+// flight (the 16-word version is latency bound on small layers). Mask and A8 on component b.
+template <class A>
+__global__ void __launch_bounds__(256, 3)
+    k_ntt_inv_tail2(typename A::W* polys, const __grid_constant__ DevConsts c, const uint64_t* __restrict__ r,
+                    uint64_t* __restrict__ y0, const __grid_constant__ PlanDev pl, size_t ct0) {
+  using W = typename A::W;
+  constexpr int LOGN = 12, N = 1 << LOGN, LS = 8;
+  using RS = GsRound<LOGN, LS>;
+  static_assert(GsLast<LOGN>::value == LS, "one round");
+  const int j = (int)(blockIdx.x % c.L);
+  const size_t ct = blockIdx.x / c.L;
+  const W q = (W)c.q[j], qb = A::bound(q);
+  const typename A::Tw* tw = Tab<A>::inv(c) + (size_t)j * N;
+  const typename A::Tw ninv = Tab<A>::pair(c.ninv_mac[j], c.ninv_mac_p[j]);  // inputs are k_mac outputs
+  const typename A::Tw wl = Tab<A>::pair(c.wlast_mac[j], c.wlast_mac_p[j]);
+  const EncK ek(c, j);
+  const bool mask = r != nullptr;
+  const uint64_t* rs = mask ? r + ct * N : nullptr;
+  W em[16];
+  if (mask) {
+    uint64_t rv[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) rv[i] = __ldg(&rs[RS::addr(0, i)]);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) em[i] = enc_mod<A>(rv[i], ek);
   }
+  typename A::Tw tws[15];
+  gs_twiddles<A, LOGN, LS>(tws, tw);
+  pdl_wait();  // the polys are produced by the preceding kernel (the MAC)
+  W* buf[2] = {polys + ((ct * 2) * c.L + j) * N, polys + ((ct * 2 + 1) * c.L + j) * N};
+  W x[2][16];
+#pragma unroll
+  for (int pp = 0; pp < 2; ++pp)
+#pragma unroll
+    for (int i = 0; i < 16; ++i) x[pp][i] = buf[pp][RS::addr(0, i)];
+  gs_compute<A, LOGN, LS, 2>(x, tws, q, qb, ninv, wl);
+  pdl_trigger();
+#pragma unroll
+  for (int i = 0; i < 16; ++i) buf[0][RS::addr(0, i)] = A::canon_gs(x[0][i], q);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    W v = A::canon_gs(x[1][i], q);
+    if (mask) {
+      v += em[i];
+      v = v >= q ? v - q : v;
+    }
+    buf[1][RS::addr(0, i)] = v;
+  }
+  if (y0 != nullptr && mask && j == 0) write_server_share_ct(rs, y0, pl, (uint32_t)(ct0 + ct), c.t_bits);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -485,6 +542,22 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, sizeof(typename A::W) == 4 &
 // reduction per output word. CTAs that share a weight tile (different s-groups) are adjacent in
 // the grid so the second read of a tile hits L2.
 constexpr int MAC_THREADS = 256;  // consumers; +32 producer threads
+
+#ifdef SECN_PROBE  // timeline probes for tools/probe_mac.py (a separate build; off in libsecn.so)
+__device__ unsigned long long g_probe[65536 * 2 + 64];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define PROBE_CTA(slot) \
+  if (threadIdx.x == 0) g_probe[64 + 2 * (blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)) + (slot)] = gtimer()
+#define PROBE0(k) \
+  if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) g_probe[k] = gtimer()
+#else
+#define PROBE_CTA(slot)
+#define PROBE0(k)
+#endif
 
 // a mod q for a < 2^64, q < 2^28: a = hi 2^32 + lo with r32 = 2^32 mod q and the 32-bit Shoup
 // companions r32p (of r32) and onep32 (of 1); three IMADs per half.
@@ -635,6 +708,8 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
     k_mac(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmw, W* __restrict__ y,
           const __grid_constant__ DevConsts c, PlanDev pl, int m_range, int n_sg, int NS) {
   extern __shared__ __align__(128) unsigned char smraw[];
+  PROBE_CTA(0);
+  PROBE0(0);
   constexpr int A2 = 2 * SG;
   const int N = 1 << c.log_n, L = c.L, G = pl.G, S = pl.S;
   const int j = blockIdx.y;
@@ -719,7 +794,9 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
   }
   const uint32_t qn = (uint32_t)c.qneg_inv32[j];
   const uint32_t r32 = (uint32_t)c.r32[j], r32p = (uint32_t)c.r32_p[j], onep32 = (uint32_t)(onep >> 32);
+  PROBE0(1);
   mbar_wait(xbar, 0);
+  PROBE0(2);
   int st = 0;
   uint32_t ph = 0;
   for (int mb = m_begin; mb < m_end; mb += MT) {
@@ -787,7 +864,9 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
     // inverse-NTT levels 0..7 of every staged output chunk, then the chunks leave the SM (lazy
     // GS domain values, finished by the INTT kernel)
     consumer_sync();
+    PROBE0(3);
     mac_intt_levels_0_7<AR>(cbuf, twe, MT * A2, (W)q, AR::bound((W)q));
+    PROBE0(4);
 #pragma unroll
     for (int r = 0; r < MT; ++r)
 #pragma unroll
@@ -796,6 +875,8 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
           y[((((size_t)(mb + r) * S + s0 + (a >> 1)) * 2 + (a & 1)) * L + j) * N + e] =
               cbuf[(r * A2 + a) * MAC_CHS + phys(tid)];
   }
+  PROBE0(5);
+  PROBE_CTA(1);
   pdl_trigger();
 }
 
@@ -1050,6 +1131,12 @@ __global__ void k_check_range(const W* __restrict__ v, size_t n_words, const __g
 // Launch with programmatic stream serialization (PDL): the kernel may be scheduled while the
 // preceding kernel in the stream finishes; it synchronises with pdl_wait() before reading that
 // kernel's outputs. Captured into CUDA graphs as programmatic edges.
+// tuning knobs read at every launch (SECN_MAC_*, SECN_TAIL1): used by tools/variant_sweep.py
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
+}
+
 template <typename... KArgs, typename... Args>
 static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                               Args&&... args) {
@@ -1151,8 +1238,17 @@ static cudaError_t ntt_inv_tail_t(const DevConsts& c, void* polys, size_t P, con
     const size_t np = n_polys - p0 < pmax ? n_polys - p0 : pmax;
     W* buf = static_cast<W*>(polys) + p0 * c.L * N;
     const uint64_t* rs = r ? r + p0 / 2 * N : nullptr;
-    cudaError_t e = launch_pdl(k_ntt_inv_tail<A, LOGN>, dim3((unsigned)(np * c.L)), dim3(N / 16), smem, s, buf, c,
-                               rs, y0, pl, p0 / 2);
+    cudaError_t e;
+    if constexpr (LOGN == 12 && sizeof(W) == 4) {
+      if (env_int("SECN_TAIL1", 0))
+        e = launch_pdl(k_ntt_inv_tail<A, LOGN>, dim3((unsigned)(np * c.L)), dim3(N / 16), smem, s, buf, c, rs, y0, pl,
+                       p0 / 2);
+      else  // both components of a (ciphertext, limb) per CTA
+        e = launch_pdl(k_ntt_inv_tail2<A>, dim3((unsigned)(np / 2 * c.L)), dim3(256), 0, s, buf, c, rs, y0, pl, p0 / 2);
+    } else {
+      e = launch_pdl(k_ntt_inv_tail<A, LOGN>, dim3((unsigned)(np * c.L)), dim3(N / 16), smem, s, buf, c, rs, y0, pl,
+                     p0 / 2);
+    }
     if (e != cudaSuccess) return e;
   }
   return cudaGetLastError();
@@ -1278,11 +1374,6 @@ static bool encode_tmap(CUtensorMap* m, int wb, int rank, const void* base, cons
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// tuning knobs read at every launch (SECN_MAC_SG, SECN_MAC_KB): used by tools/variant_sweep.py
-static int env_int(const char* name, int dflt) {
-  const char* v = getenv(name);
-  return v && *v ? atoi(v) : dflt;
-}
 
 template <class W, int SG, int MT>
 static cudaError_t mac_t(const DevConsts& c, const PlanDev& p, const void* xhat, const void* w, void* y,
@@ -1367,10 +1458,25 @@ cudaError_t launch_mac(const DevConsts& c, const PlanDev& p, const void* xhat, c
   }
   if (const int sg_env = env_int("SECN_MAC_SG", 0)) sg = sg_env;
   if (c.word_bits == 32) {
-    // SG = 1 with a large X^ tile: 8 output channels per m-block keep two CTAs per SM (the
-    // 16-channel block's chunks and 16 KiB ring stages would leave one)
-    const bool half = sg == 1 && env_int("SECN_MAC_MT", (size_t)p.G * 2 * MAC_THREADS * wb > 24 * 1024 ? 8 : 16) == 8;
-    if (half) return mac_t<uint32_t, 1, 8>(c, p, xhat, w, y, s);
+    // output channels per m-block: the larger register block (more weight reuse) unless its
+    // staged chunks plus a 4-stage ring would leave one CTA per SM; then the smaller one
+    // (SG = 1 also takes the smaller block once the X^ tile exceeds 24 KiB: measured on conv10)
+    static const int mt_big[5] = {0, 16, 8, 5, 3}, mt_small[5] = {0, 8, 4, 2, 2};
+    const size_t xtile = (size_t)p.G * 2 * sg * MAC_THREADS * wb;
+    const auto fits2 = [&](int mt) {
+      const size_t chunks = (size_t)mt * 2 * sg * MAC_CHS * wb + MAC_THREADS * 2 * wb;
+      return xtile + chunks + 4 * (size_t)mt * MAC_THREADS * wb <= 110 * 1024;
+    };
+    bool small = !fits2(mt_big[sg]) || (sg == 1 && xtile > 24 * 1024);
+    if (const int mt_env = env_int("SECN_MAC_MT", 0)) small = mt_env == mt_small[sg];
+    if (small) {
+      switch (sg) {
+        case 1: return mac_t<uint32_t, 1, 8>(c, p, xhat, w, y, s);
+        case 2: return mac_t<uint32_t, 2, 4>(c, p, xhat, w, y, s);
+        case 3: return mac_t<uint32_t, 3, 2>(c, p, xhat, w, y, s);
+        default: return mac_t<uint32_t, 4, 2>(c, p, xhat, w, y, s);
+      }
+    }
     switch (sg) {
       case 1: return mac_t<uint32_t, 1, 16>(c, p, xhat, w, y, s);
       case 2: return mac_t<uint32_t, 2, 8>(c, p, xhat, w, y, s);
@@ -1472,3 +1578,13 @@ cudaError_t launch_check_range(const DevConsts& c, const void* v, size_t n_words
 }
 
 }  // namespace secn
+
+#ifdef SECN_PROBE
+extern "C" int secn_probe_read(unsigned long long* dst, size_t n) {
+  return cudaMemcpyFromSymbol(dst, secn::g_probe, n * sizeof(unsigned long long)) == cudaSuccess ? 0 : -5;
+}
+extern "C" int secn_probe_clear(void) {
+  static unsigned long long z[65536 * 2 + 64];
+  return cudaMemcpyToSymbol(secn::g_probe, z, sizeof(z)) == cudaSuccess ? 0 : -5;
+}
+#endif
