@@ -632,7 +632,11 @@ __device__ __forceinline__ void twe_row(Tw* out, const Tw* twe, int b) {
   }
 }
 
-template <class A>
+// kDense: round B leaves chunk ch DENSE at cbuf + ch * MAC_CHS (word e at offset e, for bulk
+// stores to global memory): every task is loaded before a barrier and written after it, so the
+// in-place change of layout cannot overwrite words another task has not read (needs
+// nch <= 2 MAC_THREADS / 16 = 32 chunks).
+template <class A, bool kDense = false>
 __device__ __forceinline__ void mac_intt_levels_0_7(typename A::W* cbuf, const typename A::Tw* twe, int nch,
                                                     typename A::W q, typename A::W qb) {
   using W = typename A::W;
@@ -675,6 +679,46 @@ __device__ __forceinline__ void mac_intt_levels_0_7(typename A::W* cbuf, const t
     for (int i = 0; i < 16; ++i) base[i] = x[i];
   }
   consumer_sync();
+  if constexpr (kDense) {
+    W x[2][16];
+    const int t0 = threadIdx.x, t1 = threadIdx.x + MAC_THREADS;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) x[0][i] = cbuf[(t0 >> 4) * MAC_CHS + (t0 & 15) + 17 * i];
+    if (t1 < ntask) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) x[1][i] = cbuf[(t1 >> 4) * MAC_CHS + (t1 & 15) + 17 * i];
+    }
+    consumer_sync();  // every task's words are in registers: the chunks may change layout
+    if (t0 < ntask) {
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        const int d = 1 << p;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          if (i & d) continue;
+          A::gs(x[0][i], x[0][i + d], twe[256 - (256 >> (4 + p)) + (i >> (p + 1))], q, qb);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 16; ++i) cbuf[(t0 >> 4) * MAC_CHS + (t0 & 15) + 16 * i] = x[0][i];
+    }
+    if (t1 < ntask) {
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        const int d = 1 << p;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          if (i & d) continue;
+          A::gs(x[1][i], x[1][i + d], twe[256 - (256 >> (4 + p)) + (i >> (p + 1))], q, qb);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 16; ++i) cbuf[(t1 >> 4) * MAC_CHS + (t1 & 15) + 16 * i] = x[1][i];
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the bulk stores read these words
+    consumer_sync();
+    return;
+  }
   // round B: levels 4..7, task = coefficients 16i + o (phys: 17i + o); the twiddles do not
   // depend on the task
   for (int tau = threadIdx.x; tau < ntask; tau += MAC_THREADS) {
@@ -823,7 +867,8 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
         if ((tid & 31) == 0) mbar_arrive(&empty[st]);
         if (++st == NS) st = 0, ph ^= 1;
       }
-      consumer_sync();  // the previous m-block's chunks have been written out
+      if (tid < 32) bulk_wait_read0();  // the previous m-block's bulk stores have read the chunks
+      consumer_sync();                    // ... and every thread knows it
 #pragma unroll
       for (int r = 0; r < MT; ++r)
 #pragma unroll
@@ -865,16 +910,31 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
     // GS domain values, finished by the INTT kernel)
     consumer_sync();
     PROBE0(3);
-    mac_intt_levels_0_7<AR>(cbuf, twe, MT * A2, (W)q, AR::bound((W)q));
-    PROBE0(4);
+    if constexpr (sizeof(W) == 4) {
+      // 32-bit words: the chunks leave dense through TMA bulk stores (one 1 KiB row segment per
+      // output limb-poly), asynchronous to the next m-block's MAC
+      mac_intt_levels_0_7<AR, true>(cbuf, twe, MT * A2, (W)q, AR::bound((W)q));
+      PROBE0(4);
+      if (tid < 32) {  // warp 0: lane ch issues chunk ch's store (MT x 2SG <= 32)
+        const int r = tid / A2, a = tid % A2;
+        if (tid < MT * A2 && r < rows && a < 2 * ns)
+          bulk_store_s2g(y + ((((size_t)(mb + r) * S + s0 + (a >> 1)) * 2 + (a & 1)) * L + j) * N + e0,
+                         cbuf + tid * MAC_CHS, MAC_THREADS * sizeof(W));
+        bulk_commit();
+      }
+    } else {
+      mac_intt_levels_0_7<AR>(cbuf, twe, MT * A2, (W)q, AR::bound((W)q));
+      PROBE0(4);
 #pragma unroll
-    for (int r = 0; r < MT; ++r)
+      for (int r = 0; r < MT; ++r)
 #pragma unroll
-      for (int a = 0; a < A2; ++a)
-        if (r < rows && a < 2 * ns)
-          y[((((size_t)(mb + r) * S + s0 + (a >> 1)) * 2 + (a & 1)) * L + j) * N + e] =
-              cbuf[(r * A2 + a) * MAC_CHS + phys(tid)];
+        for (int a = 0; a < A2; ++a)
+          if (r < rows && a < 2 * ns)
+            y[((((size_t)(mb + r) * S + s0 + (a >> 1)) * 2 + (a & 1)) * L + j) * N + e] =
+                cbuf[(r * A2 + a) * MAC_CHS + phys(tid)];
+    }
   }
+  if (sizeof(W) == 4 && tid < 32) bulk_wait_read0();  // shared memory stays valid until the stores have read it
   PROBE0(5);
   PROBE_CTA(1);
   pdl_trigger();

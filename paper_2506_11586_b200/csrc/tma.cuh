@@ -55,6 +55,18 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
       : "memory");
 }
 
+// 1-D bulk copy shared -> global (bulk async-group completion): `bytes` a multiple of 16, both
+// addresses 16-byte aligned. commit groups the issued copies; wait_read 0 returns once their
+// shared-memory sources may be overwritten, wait 0 once the writes are performed.
+__device__ __forceinline__ void bulk_store_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
 // Tiled TMA loads through a tensor map (cp.async.bulk.tensor, SASS UTMALDG): the whole box lands
 // in shared memory in box order (dimension 0 fastest); out-of-bounds elements are zero-filled and
 // still counted in the transaction bytes. `map` is the address of a __grid_constant__ CUtensorMap.
