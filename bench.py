@@ -71,8 +71,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-online", action="store_true", help="skip the online-NTT-preprocessing (f4) leg")
     ap.add_argument("--no-sweep", action="store_true", help="skip the compact NTT sweep (C5) in the default run")
-    ap.add_argument("--serial", action="store_true",
-                    help="run every layer in network order on one stream (no fire e1/e3 or ResNet c1/ds overlap)")
+    ap.add_argument("--concurrent", action="store_true",
+                    help="overlap layers that read the same input (fire e1/e3, ResNet c1/ds) on side streams; "
+                         "EXPERIMENTAL: tools/race_check.py shows wrong outputs under this overlap (DESIGN.md §9b)")
     return ap.parse_args()
 
 
@@ -334,7 +335,7 @@ def run_secn(args, word_bits, world, rank, local, dev, full):
     # layers that read the same input tensor (fire e1/e3, ResNet c1/ds) overlap on side streams;
     # everything else keeps network order (paper_2506_11586_b200/schedule.py)
     names = [d["lay"].name for d in st]
-    groups = [[i] for i in range(len(st))] if args.serial else concurrent_groups(names)
+    groups = concurrent_groups(names) if args.concurrent else [[i] for i in range(len(st))]
     runner = GroupRunner(groups, dev)
 
     def layer_call(i):
@@ -458,9 +459,9 @@ def run_secn(args, word_bits, world, rank, local, dev, full):
                    "parallelism": f"output-channel shards x{world}", "l2": (f"inputs {alg_bytes / 1e9:.2f} GB/step >> 126 MB L2 (no flush)" if alg_bytes > 5e8 else
                           "step footprint below 4x L2: timing includes L2 reuse across replays"),
                    "timing": "CUDA events around CUDA-graph replays of the whole step",
-                   "layer_overlap": ("none (--serial)" if args.serial else
-                                     "layers reading the same input tensor (fire e1/e3, ResNet c1/ds) on side "
-                                     "streams; all else in network order")},
+                   "layer_overlap": ("EXPERIMENTAL (--concurrent): layers reading the same input tensor "
+                                     "(fire e1/e3, ResNet c1/ds) on side streams" if args.concurrent else
+                                     "none: every layer in network order on one stream")},
         "throughput": {"ntt_per_s": round(n_ntt / step_s, 1), "alg_bytes_per_step": alg_bytes,
                        "alg_GBps": round(alg_bytes / step_s / 1e9, 1), "hbm_frac": round(alg_bytes / step_s / 1e9 / hbm_peak, 4),
                        "offline_preprocess_s": round(offline_s, 5), "wall_s_timed_region": round(wall, 4)},

@@ -1209,7 +1209,7 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = env_int("SECN_NO_PDL", 0) ? 0 : 1;  // SECN_NO_PDL=1: plain stream order (debugging)
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 

@@ -475,3 +475,46 @@ def test_end_to_end_decrypts_to_plain_conv(env):
                 y1[m][sel] = he.decrypt(out[m * opl.S + s], sk, P, coef[sel])
     y = (y0 + y1) & np.uint64(P.t - 1)
     assert (y == conv.conv2d_mod((x0 + x1) & np.uint64(P.t - 1), K, lay.stride, lay.pad, P.t_bits)).all()
+
+
+def test_network_step_graph_equals_layerwise(secn):
+    """The bench's step (all SqueezeNet-1.1 layers in one CUDA graph, network order, programmatic
+    dependent launches between the kernels) gives, on every layer, the words of the same layers
+    run one call at a time with a synchronisation after each: no cross-layer hazard."""
+    ctx = secn.Context(0, word_bits=32)
+    st = []
+    for li, lay in enumerate(layers.squeezenet11()):
+        plan = ctx.plan(lay.C, lay.H, lay.W, lay.M, lay.k, stride=lay.stride, pad=lay.pad)
+        g = inputs.rng(500 + li)
+        ct = torch.from_numpy(inputs.uniform_residues(g, (plan.G * plan.S, 2), ctx.primes, ctx.n)
+                              .astype(np.uint32).view(np.int32)).to(DEV)
+        d = dict(plan=plan, ct=ct, x0=TP(inputs.uniform_below(g, (plan.G * plan.S, ctx.n), 1 << ctx.t_bits)),
+                 r=TP(inputs.uniform_below(g, (plan.M * plan.S, ctx.n), 1 << ctx.t_bits)),
+                 out=ctx.empty(plan.M * plan.S, 2, ctx.L, ctx.n),
+                 ws=torch.empty(ctx.workspace_bytes(plan) // 8 + 1, dtype=torch.int64, device=DEV),
+                 y0=torch.empty((plan.M, plan.OH, plan.OW), dtype=torch.int64, device=DEV))
+        d["w"] = ctx.preprocess_weights(plan, TP(inputs.quantized_kernel(g, plan.M, lay.C, lay.k, lay.k)))
+        st.append(d)
+
+    def call(d):
+        ctx.he_conv2d(d["plan"], d["ct"], d["w"], x0=d["x0"], r=d["r"], out=d["out"], workspace=d["ws"], y0=d["y0"])
+
+    ref = []
+    for d in st:
+        call(d)
+        torch.cuda.synchronize()
+        ref.append((d["out"].clone(), d["y0"].clone()))
+    graph = torch.cuda.CUDAGraph()
+    cap = torch.cuda.Stream(DEV)
+    with torch.cuda.graph(graph, stream=cap):
+        for d in st:
+            call(d)
+    for _ in range(3):
+        for d in st:
+            d["out"].zero_()
+            d["y0"].zero_()
+        graph.replay()
+        torch.cuda.synchronize()
+        for d, (o, y) in zip(st, ref):
+            assert torch.equal(d["out"], o) and torch.equal(d["y0"], y)
+    ctx.close()

@@ -34,7 +34,11 @@ for li, lay in enumerate(layers.network(net)):
              y0=torch.empty((plan.M, plan.OH, plan.OW), dtype=torch.int64, device=dev))
     d["w"] = ctx.preprocess_weights(plan, T(inputs.quantized_kernel(g, plan.M, lay.C, lay.k, lay.k)))
     st.append(d)
-runner = GroupRunner(concurrent_groups([d["lay"].name for d in st]), dev)
+import os  # noqa: E402
+
+# the bench's schedule: every layer in network order (CONCURRENT=1: the experimental side streams)
+runner = GroupRunner(concurrent_groups([d["lay"].name for d in st]) if os.environ.get("CONCURRENT") else
+                     [[i] for i in range(len(st))], dev)
 
 
 def call(i):
