@@ -440,10 +440,10 @@ def run_secn(args, word_bits, world, rank, local, dev, full):
     roofline = {"bound": "hbm", "kernel": names[dom], "achieved": round(achieved, 1), "peak": hbm_peak,
                 "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
                 "traffic": tr["dram_bytes_per_launch"] if tr else None,
-                "traffic_note": (f"ncu DRAM read+write of one {tr['layer']} launch; algorithmic bytes of that launch "
+                "traffic_note": (f"ncu DRAM read+write of one {tr['layer']} launch ({tr.get('dram_GBps_ncu')} GB/s in "
+                                 f"{tr['duration_us_ncu']} us); algorithmic bytes of that launch "
                                  f"{tr['algorithmic_bytes_per_launch']}; integer-multiply (fmaheavy) pipe "
-                                 f"{tr['fmaheavy_pct_of_peak_elapsed']}% busy: the launch is integer-pipe bound"
-                                 f" ({tr['source']})") if tr else None,
+                                 f"{tr['fmaheavy_pct_of_peak_elapsed']}% busy ({tr['source']})") if tr else None,
                 "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
                 "bytes_per_step": sb[dom], "launches_per_step": n_layers_active,
                 "avg_launch_us": round(stage_ms[dom] / n_layers_active * 1e3, 2),
