@@ -810,7 +810,10 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
           }
           // weights: box (256 coefficients, row g*L + j, MT output channels from mb)
           mbar_arrive_expect_tx(&full[st], MT * row_bytes);
-          tma_load_3d_hint(ring + (size_t)st * MT * MAC_THREADS, &tmw, e0, g * L + j, mb, &full[st], evict_first);
+          if (c.word_bits & 0x400)  // debug: no L2 cache hint on the weight stream
+            tma_load_3d(ring + (size_t)st * MT * MAC_THREADS, &tmw, e0, g * L + j, mb, &full[st]);
+          else
+            tma_load_3d_hint(ring + (size_t)st * MT * MAC_THREADS, &tmw, e0, g * L + j, mb, &full[st], evict_first);
           ++issued;
           if (++st == NS) st = 0, ph ^= 1, first = 0;
         }
@@ -1494,7 +1497,9 @@ static cudaError_t mac_t(const DevConsts& c, const PlanDev& p, const void* xhat,
     return cudaErrorInvalidValue;
   dim3 grid((N / MAC_THREADS) * n_sg, c.L, n_mr);
   W* yp = static_cast<W*>(y);
-  cudaError_t e = launch_pdl(k_mac<W, SG, MT>, grid, dim3(MAC_THREADS + 32), smem, s, tmx, tmw, yp, c, p, m_range,
+  DevConsts cc = c;  // debugging knobs ride in unused word_bits bits
+  if (env_int("SECN_MAC_NOHINT", 0)) cc.word_bits |= 0x400;
+  cudaError_t e = launch_pdl(k_mac<W, SG, MT>, grid, dim3(MAC_THREADS + 32), smem, s, tmx, tmw, yp, cc, p, m_range,
                              n_sg, NS);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();

@@ -32,6 +32,9 @@ for li, lay in enumerate([l for l in net if l.name in (fire + ".e1", fire + ".e3
              ws=torch.zeros(ctx.workspace_bytes(plan) // 8 + 1, dtype=torch.int64, device=dev))
     d["w"] = ctx.preprocess_weights(d["plan"], d["K"])
     st.append(d)
+W0 = [d["w"].clone() for d in st]
+BIG_A = torch.ones(1 << 28, dtype=torch.int32, device=dev)
+BIG_B = torch.empty_like(BIG_A)
 runner = GroupRunner([[0], [1, 2]], dev)  # sq, then e1 | e3
 NL = 3
 
@@ -98,6 +101,9 @@ for trial in range(4):
                 # e1 chain on main while e3 runs fwd+mac on the side; e3's tail after the join
                 runner(lambda i: stage([0, 1, 2] if i != 2 else [0, 1])(i))
                 stage([2])(2)
+            elif MODE == "e3mac_vs_copy" and upto == 2:
+                BIG_B.copy_(BIG_A)  # main: heavy memory traffic beside e3's forward NTT + MAC
+                runner(lambda i: (BIG_B.copy_(BIG_A), BIG_A.copy_(BIG_B), BIG_B.copy_(BIG_A)) if i == 1 else stage([0, 1])(i))
             elif MODE == "e3mac_check" and upto == 2:
                 runner(lambda i: stage([0, 1, 2] if i != 2 else [0, 1])(i))
             elif MODE == "e3_serial" and upto == 2:
@@ -116,10 +122,11 @@ for trial in range(4):
         msg = []
         for i in range(NL):
             ws_ref, out_ref = refs[(i, upto)]
-            if MODE == "e3mac_check" and upto == 2 and i == 2:
+            if MODE in ("e3mac_check", "e3mac_vs_copy") and upto == 2 and i == 2:
                 ws_ref, out_ref = refs[(i, 1)]
             nx = int((st[i]["ws"] != ws_ref).sum())
-            if MODE == "e3mac_check" and upto == 2 and i == 2:
+            if MODE in ("e3mac_check", "e3mac_vs_copy") and upto == 2 and i == 2:
+                print("   weights intact:", all(torch.equal(x["w"], w0) for x, w0 in zip(st, W0)))
                 got = st[i]["out"].view(-1, 256).cpu()
                 ref_ = out_ref.view(-1, 256).cpu()
                 badc = (got != ref_).any(1).nonzero().flatten().tolist()
