@@ -71,9 +71,13 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-online", action="store_true", help="skip the online-NTT-preprocessing (f4) leg")
     ap.add_argument("--no-sweep", action="store_true", help="skip the compact NTT sweep (C5) in the default run")
-    ap.add_argument("--concurrent", action="store_true",
-                    help="overlap layers that read the same input (fire e1/e3, ResNet c1/ds) on side streams; "
-                         "EXPERIMENTAL: tools/race_check.py shows wrong outputs under this overlap (DESIGN.md §9b)")
+    ap.add_argument("--overlap", choices=["none", "staged", "free"], default="staged",
+                    help="layers reading the same input (fire e1/e3, ResNet c1/ds): none = network order; "
+                         "staged = the group's layers run each launch group (NTT, MAC, tail) side by side and "
+                         "join between groups; free = whole layers on side streams, EXPERIMENTAL: "
+                         "tools/race_check.py shows wrong outputs under this overlap (DESIGN.md §9b)")
+    ap.add_argument("--concurrent", action="store_const", const="free", dest="overlap",
+                    help="alias of --overlap free")
     return ap.parse_args()
 
 
@@ -283,7 +287,7 @@ def run_secn(args, word_bits, world, rank, local, dev, full):
     the per-stage, e2e and cpu_baseline legs. Returns the JSON dict on rank 0 (None elsewhere)."""
     from paper_2506_11586_b200 import Context
     from paper_2506_11586_b200 import dist as sdist
-    from paper_2506_11586_b200.schedule import GroupRunner, concurrent_groups
+    from paper_2506_11586_b200.schedule import GroupRunner, StagedGroupRunner, concurrent_groups
 
     ctx = Context(local, word_bits=word_bits)
     L, n, t_bits = ctx.L, ctx.n, ctx.t_bits
@@ -335,8 +339,8 @@ def run_secn(args, word_bits, world, rank, local, dev, full):
     # layers that read the same input tensor (fire e1/e3, ResNet c1/ds) overlap on side streams;
     # everything else keeps network order (paper_2506_11586_b200/schedule.py)
     names = [d["lay"].name for d in st]
-    groups = concurrent_groups(names) if args.concurrent else [[i] for i in range(len(st))]
-    runner = GroupRunner(groups, dev)
+    groups = concurrent_groups(names) if args.overlap != "none" else [[i] for i in range(len(st))]
+    runner = StagedGroupRunner(groups, dev) if args.overlap == "staged" else GroupRunner(groups, dev)
 
     def layer_call(i):
         d = st[i]
@@ -344,8 +348,16 @@ def run_secn(args, word_bits, world, rank, local, dev, full):
             ctx.he_conv2d(d["pl"], d["ct"], d["w"], x0=d["x0"], r=d["r"], out=d["out"], workspace=d["ws"],
                           y0=d["y0"])
 
+    def stage_call(i, k):
+        d = st[i]
+        if d["mc"] > 0:
+            ctx.he_conv2d_stage_ex(k, d["pl"], d["ct"], d["w"], d["x0"], d["r"], d["out"], d["y0"], d["ws"])
+
     def step_public():
-        runner(layer_call)
+        if args.overlap == "staged":
+            runner(layer_call, stage_call)
+        else:
+            runner(layer_call)
 
     # ---- warmup (eager), then capture the step in a CUDA graph ----
     for _ in range(max(args.warmup, 3)):
@@ -459,9 +471,11 @@ def run_secn(args, word_bits, world, rank, local, dev, full):
                    "parallelism": f"output-channel shards x{world}", "l2": (f"inputs {alg_bytes / 1e9:.2f} GB/step >> 126 MB L2 (no flush)" if alg_bytes > 5e8 else
                           "step footprint below 4x L2: timing includes L2 reuse across replays"),
                    "timing": "CUDA events around CUDA-graph replays of the whole step",
-                   "layer_overlap": ("EXPERIMENTAL (--concurrent): layers reading the same input tensor "
-                                     "(fire e1/e3, ResNet c1/ds) on side streams" if args.concurrent else
-                                     "none: every layer in network order on one stream")},
+                   "layer_overlap": {"none": "none: every layer in network order on one stream",
+                                     "staged": "staged: layers reading the same input tensor (fire e1/e3, ResNet "
+                                               "c1/ds) run each launch group side by side, joined between groups",
+                                     "free": "EXPERIMENTAL (--overlap free): layers reading the same input "
+                                             "tensor on side streams"}[args.overlap]},
         "throughput": {"ntt_per_s": round(n_ntt / step_s, 1), "alg_bytes_per_step": alg_bytes,
                        "alg_GBps": round(alg_bytes / step_s / 1e9, 1), "hbm_frac": round(alg_bytes / step_s / 1e9 / hbm_peak, 4),
                        "offline_preprocess_s": round(offline_s, 5), "wall_s_timed_region": round(wall, 4)},
@@ -577,7 +591,8 @@ def run_online(ctx, st, K, warmup, dev, world, runner):
     return {"value": round(ms / 1e3, 7), "unit": "s", "ms_per_step": round(ms, 4),
             "weights_held_bytes": held, "weights_held_offline_bytes": sum(d["w"].numel() * d["w"].element_size()
                                                                             for d in st if d["mc"] > 0),
-            "path": "secn_he_conv2d_online: pack + NTT of the weights, then share add + NTT, MAC, INTT + mask"}
+            "path": "secn_he_conv2d_online: pack + NTT of the weights, then share add + NTT, MAC, INTT + mask",
+            "layer_overlap": "none (no stage-split form of this entry point): compare with the main step at --overlap none"}
 
 
 def run_lwe(ctx, st, K, warmup, dev, world, runner):
@@ -607,7 +622,8 @@ def run_lwe(ctx, st, K, warmup, dev, world, runner):
     torch.cuda.empty_cache()
     return {"value": round(ms / 1e3, 7), "unit": "s", "ms_per_step": round(ms, 4), "keep_limbs": keep,
             "output_bytes_per_step": out_bytes, "full_ct_output_bytes_per_step": full_bytes,
-            "path": "secn32_he_conv2d_lwe: share add + NTT, MAC, INTT tail + mask + modulus switch + extraction"}
+            "path": "secn32_he_conv2d_lwe: share add + NTT, MAC, INTT tail + mask + modulus switch + extraction",
+            "layer_overlap": "none (no stage-split form of this entry point)"}
 
 
 def run_fc(ctx, K, warmup, dev, world, n_i=2048, n_o=1000, seed=11):

@@ -294,6 +294,16 @@ int secn32_he_fc_lwe(secn_ctx* ctx, const secn_fc_plan_t* plan, const uint32_t* 
 int secn32_he_conv2d_stage(secn_ctx* ctx, const secn_conv_plan_t* plan, int stage, const uint32_t* ct_in,
                            const uint64_t* x0, const uint32_t* w_ntt, const uint64_t* r, uint32_t* ct_out,
                            void* workspace, size_t ws_bytes, void* stream);
+/* secn_he_conv2d_stage with the server's output share: y0 (as in secn_he_conv2d_ex; may be NULL)
+ * is written by stage 2 (the kernel that also adds the mask), which is where the fused call
+ * writes it; stages 0 and 1 ignore y0. Lets a caller overlap one launch group of several
+ * independent layers at a time (bench.py --overlap staged). */
+int secn_he_conv2d_stage_ex(secn_ctx* ctx, const secn_conv_plan_t* plan, int stage, const uint64_t* ct_in,
+                            const uint64_t* x0, const uint64_t* w_ntt, const uint64_t* r, uint64_t* ct_out, uint64_t* y0,
+                            void* workspace, size_t ws_bytes, void* stream);
+int secn32_he_conv2d_stage_ex(secn_ctx* ctx, const secn_conv_plan_t* plan, int stage, const uint32_t* ct_in,
+                              const uint64_t* x0, const uint32_t* w_ntt, const uint64_t* r, uint32_t* ct_out,
+                              uint64_t* y0, void* workspace, size_t ws_bytes, void* stream);
 
 #ifdef __cplusplus
 }

@@ -839,6 +839,20 @@ int secn32_he_conv2d_stage(secn_ctx* ctx, const secn_conv_plan_t* plan, int stag
   return he_conv2d_impl(ctx, 32, plan, stage, ct_in, x0, w_ntt, r, ct_out, nullptr, workspace, ws_bytes, stream);
 }
 
+int secn_he_conv2d_stage_ex(secn_ctx* ctx, const secn_conv_plan_t* plan, int stage, const uint64_t* ct_in,
+                            const uint64_t* x0, const uint64_t* w_ntt, const uint64_t* r, uint64_t* ct_out, uint64_t* y0,
+                            void* workspace, size_t ws_bytes, void* stream) {
+  if (stage < 0 || stage > 2) return fail(SECN_EINVAL, "stage %d not in {0,1,2}", stage);
+  return he_conv2d_impl(ctx, 64, plan, stage, ct_in, x0, w_ntt, r, ct_out, y0, workspace, ws_bytes, stream);
+}
+
+int secn32_he_conv2d_stage_ex(secn_ctx* ctx, const secn_conv_plan_t* plan, int stage, const uint32_t* ct_in,
+                              const uint64_t* x0, const uint32_t* w_ntt, const uint64_t* r, uint32_t* ct_out,
+                              uint64_t* y0, void* workspace, size_t ws_bytes, void* stream) {
+  if (stage < 0 || stage > 2) return fail(SECN_EINVAL, "stage %d not in {0,1,2}", stage);
+  return he_conv2d_impl(ctx, 32, plan, stage, ct_in, x0, w_ntt, r, ct_out, y0, workspace, ws_bytes, stream);
+}
+
 int secn_extract_share(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* r, uint64_t* y0, void* stream) {
   if (int st = check_ctx(ctx)) return st;
   if (int st = check_plan(ctx, plan)) return st;

@@ -13,7 +13,7 @@ so the step time stays what the protocol would see layer by layer.
 """
 from __future__ import annotations
 
-from typing import Callable, List, Sequence
+from typing import Callable, List, Optional, Sequence
 
 import torch
 
@@ -63,3 +63,35 @@ class GroupRunner:
             fn(g[0])
             for s in self.side[:len(g) - 1]:
                 main.wait_stream(s)
+
+
+class StagedGroupRunner:
+    """Like GroupRunner, but a group's layers advance stage by stage: ``stage_fn(i, k)`` runs launch
+    group k (0: share add + NTT, 1: MAC, 2: INTT tail + mask) of layer i, the group's layers run
+    stage k concurrently on their streams, and the streams join before stage k + 1. So kernels of
+    the same kind overlap (two MACs, two tails), but a tail never runs beside another layer's MAC --
+    the overlap that produced wrong words in tools/race_check.py."""
+
+    def __init__(self, groups: List[List[int]], device, n_stages: int = 3):
+        self.groups = groups
+        self.n_stages = n_stages
+        width = max((len(g) for g in groups), default=1)
+        self.side = [torch.cuda.Stream(device) for _ in range(width - 1)]
+
+    def __call__(self, fn: Callable[[int], None], stage_fn: Optional[Callable[[int, int], None]] = None) -> None:
+        """Without ``stage_fn`` (an entry point with no staged form) every layer runs whole, in order."""
+        main = torch.cuda.current_stream()
+        for g in self.groups:
+            if len(g) == 1 or stage_fn is None:
+                for i in g:
+                    fn(i)
+                continue
+            for k in range(self.n_stages):
+                for s in self.side[:len(g) - 1]:
+                    s.wait_stream(main)
+                for s, i in zip(self.side, g[1:]):
+                    with torch.cuda.stream(s):
+                        stage_fn(i, k)
+                stage_fn(g[0], k)
+                for s in self.side[:len(g) - 1]:
+                    main.wait_stream(s)

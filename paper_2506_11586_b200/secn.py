@@ -32,6 +32,7 @@ EXPORTS = ("secn_ctx_create", "secn_ctx_destroy", "secn_ctx_query", "secn_last_e
            "secn_he_conv2d_workspace", "secn_he_conv2d", "secn_he_conv2d_stage", "secn_extract_share",
            "secn32_ctx_create", "secn32_ntt_fwd", "secn32_ntt_inv", "secn32_preprocess_weights",
            "secn32_share_add", "secn32_mask_add", "secn32_he_conv2d", "secn32_he_conv2d_stage",
+           "secn_he_conv2d_stage_ex", "secn32_he_conv2d_stage_ex",
            "secn_he_conv2d_ex", "secn32_he_conv2d_ex", "secn_he_conv2d_online_workspace",
            "secn_he_conv2d_online", "secn32_he_conv2d_online", "secn_fc_plan", "secn_fc_preprocess_weights",
            "secn32_fc_preprocess_weights", "secn_he_fc_workspace", "secn_he_fc", "secn32_he_fc",
@@ -106,6 +107,7 @@ def lib(path=None) -> ctypes.CDLL:
         "secn_he_conv2d_workspace": (sz, [vp, P]),
         "secn_he_conv2d": (i, [vp, P, vp, vp, vp, vp, vp, vp, sz, vp]),
         "secn_he_conv2d_stage": (i, [vp, P, i, vp, vp, vp, vp, vp, vp, sz, vp]),
+        "secn_he_conv2d_stage_ex": (i, [vp, P, i, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
         "secn_he_conv2d_ex": (i, [vp, P, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
         "secn_he_conv2d_online_workspace": (sz, [vp, P]),
         "secn_fc_plan": (i, [u32, u32, ctypes.POINTER(FcPlan)]),
@@ -120,7 +122,8 @@ def lib(path=None) -> ctypes.CDLL:
         "secn_extract_share": (i, [vp, P, vp, vp, vp]),
         "secn32_ctx_create": (i, [ctypes.POINTER(vp), i, u32, u32, ctypes.POINTER(ctypes.c_uint32), u32]),
     }
-    for f in ("ntt_fwd", "ntt_inv", "preprocess_weights", "share_add", "mask_add", "he_conv2d", "he_conv2d_stage", "he_conv2d_ex",
+    for f in ("ntt_fwd", "ntt_inv", "preprocess_weights", "share_add", "mask_add", "he_conv2d", "he_conv2d_stage",
+              "he_conv2d_stage_ex", "he_conv2d_ex",
               "he_conv2d_online", "fc_preprocess_weights", "he_fc", "he_conv2d_lwe", "he_fc_lwe"):
         sig["secn32_" + f] = sig["secn_" + f]
     for name, (res, args) in sig.items():
@@ -391,6 +394,21 @@ class Context:
                                           self._rp(out, (n_out, 2, L, n), "ct_out"),
                                           ctypes.c_void_p(workspace.data_ptr()),
                                           workspace.numel() * workspace.element_size(), self._stream(stream)))
+        return out
+
+    def he_conv2d_stage_ex(self, stage: int, plan: Plan, ct_in: torch.Tensor, w_ntt: torch.Tensor,
+                           x0: Optional[torch.Tensor], r: Optional[torch.Tensor], out: torch.Tensor,
+                           y0: Optional[torch.Tensor], workspace: torch.Tensor, stream=None) -> torch.Tensor:
+        """secn_he_conv2d_stage_ex: one launch group, stage 2 also writing the share y0."""
+        L, n = self.L, self.n
+        n_in, n_out = plan.G * plan.S, plan.M * plan.S
+        _check(self._f("he_conv2d_stage_ex")(self._h, ctypes.byref(plan), stage,
+                                             self._rp(ct_in, (n_in, 2, L, n), "ct_in"), _ptr(x0, (n_in, n), "x0"),
+                                             self._rp(w_ntt, (plan.M, plan.G, L, n), "w_ntt"), _ptr(r, (n_out, n), "r"),
+                                             self._rp(out, (n_out, 2, L, n), "ct_out"),
+                                             _ptr(y0, (plan.M, plan.OH, plan.OW), "y0") if y0 is not None else None,
+                                             ctypes.c_void_p(workspace.data_ptr()),
+                                             workspace.numel() * workspace.element_size(), self._stream(stream)))
         return out
 
     def extract_share(self, plan: Plan, r: torch.Tensor, out: Optional[torch.Tensor] = None,

@@ -338,6 +338,14 @@ def test_he_conv2d_stages_equal_fused_call(env):
     for s in range(3):
         ctx.he_conv2d_stage(s, plan, cti, w, x0t, rt, out, ws)
     assert (D.U(out) == fused).all()
+    # secn_he_conv2d_stage_ex: stage 2 also writes the share, as secn_he_conv2d_ex does
+    y0f = torch.full((plan.M, plan.OH, plan.OW), -1, dtype=torch.int64, device=DEV)
+    ctx.he_conv2d(plan, cti, w, x0=x0t, r=rt, y0=y0f)
+    y0s = torch.full_like(y0f, -2)
+    out.zero_()
+    for s in range(3):
+        ctx.he_conv2d_stage_ex(s, plan, cti, w, x0t, rt, out, y0s, ws)
+    assert (D.U(out) == fused).all() and torch.equal(y0s, y0f)
 
 
 L_ = layers.ConvLayer
@@ -477,10 +485,13 @@ def test_end_to_end_decrypts_to_plain_conv(env):
     assert (y == conv.conv2d_mod((x0 + x1) & np.uint64(P.t - 1), K, lay.stride, lay.pad, P.t_bits)).all()
 
 
-def test_network_step_graph_equals_layerwise(secn):
-    """The bench's step (all SqueezeNet-1.1 layers in one CUDA graph, network order, programmatic
-    dependent launches between the kernels) gives, on every layer, the words of the same layers
-    run one call at a time with a synchronisation after each: no cross-layer hazard."""
+@pytest.mark.parametrize("overlap", ["none", "staged"])
+def test_network_step_graph_equals_layerwise(secn, overlap):
+    """The bench's step (all SqueezeNet-1.1 layers in one CUDA graph, programmatic dependent
+    launches between the kernels; network order, or bench.py --overlap staged) gives, on every
+    layer, the words of the same layers run one call at a time with a synchronisation after each:
+    no cross-layer hazard."""
+    from paper_2506_11586_b200.schedule import StagedGroupRunner, concurrent_groups
     ctx = secn.Context(0, word_bits=32)
     st = []
     for li, lay in enumerate(layers.squeezenet11()):
@@ -499,16 +510,24 @@ def test_network_step_graph_equals_layerwise(secn):
     def call(d):
         ctx.he_conv2d(d["plan"], d["ct"], d["w"], x0=d["x0"], r=d["r"], out=d["out"], workspace=d["ws"], y0=d["y0"])
 
+    def stage(d, k):
+        ctx.he_conv2d_stage_ex(k, d["plan"], d["ct"], d["w"], d["x0"], d["r"], d["out"], d["y0"], d["ws"])
+
     ref = []
     for d in st:
         call(d)
         torch.cuda.synchronize()
         ref.append((d["out"].clone(), d["y0"].clone()))
+    names = [lay.name for lay in layers.squeezenet11()]
+    runner = StagedGroupRunner(concurrent_groups(names), DEV)
     graph = torch.cuda.CUDAGraph()
     cap = torch.cuda.Stream(DEV)
     with torch.cuda.graph(graph, stream=cap):
-        for d in st:
-            call(d)
+        if overlap == "staged":
+            runner(lambda i: call(st[i]), lambda i, k: stage(st[i], k))
+        else:
+            for d in st:
+                call(d)
     for _ in range(3):
         for d in st:
             d["out"].zero_()

@@ -57,6 +57,9 @@ import os  # noqa: E402
 
 runner = GroupRunner([[i] for i in range(len(st))] if os.environ.get("SERIAL") else
                      concurrent_groups([d["lay"].name for d in st]), dev)
+from paper_2506_11586_b200.schedule import StagedGroupRunner  # noqa: E402
+
+STAGED_RUNNER = StagedGroupRunner(concurrent_groups([d["lay"].name for d in st]), dev)
 for i in range(len(st)):  # serial reference
     ctx.he_conv2d(st[i]["plan"], st[i]["ct"], st[i]["w"], x0=st[i]["x0"], r=st[i]["r"], out=st[i]["out"],
                   workspace=st[i]["ws"])
@@ -65,6 +68,15 @@ ref = [d["out"].clone() for d in st]
 
 
 def offline_step():
+    if os.environ.get("STAGED"):
+        from paper_2506_11586_b200.schedule import StagedGroupRunner
+
+        sr = STAGED_RUNNER
+        sr(lambda i: ctx.he_conv2d(st[i]["plan"], st[i]["ct"], st[i]["w"], x0=st[i]["x0"], r=st[i]["r"],
+                                   out=st[i]["out"], workspace=st[i]["ws"]),
+           lambda i, k: ctx.he_conv2d_stage(k, st[i]["plan"], st[i]["ct"], st[i]["w"], st[i]["x0"], st[i]["r"],
+                                            st[i]["out"], st[i]["ws"]))
+        return
     runner(lambda i: ctx.he_conv2d(st[i]["plan"], st[i]["ct"], st[i]["w"], x0=st[i]["x0"], r=st[i]["r"],
                                    out=st[i]["out"], workspace=st[i]["ws"]))
 
@@ -74,8 +86,8 @@ def online_step():
                                           out=st[i]["out"], workspace=st[i]["ws_on"]))
 
 
-for mode, step in (("offline-eager", offline_step), ("offline-graph", offline_step), ("eager", online_step),
-                   ("graph", online_step)):
+for mode, step in (("offline-eager", offline_step), ("offline-graph", offline_step)) + (
+        () if os.environ.get("STAGED") else (("eager", online_step), ("graph", online_step))):
     for d in st:
         d["out"].zero_()
     if mode.endswith("eager"):
