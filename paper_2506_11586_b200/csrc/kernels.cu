@@ -73,9 +73,12 @@ __device__ __forceinline__ typename A::W enc_mod(uint64_t v, const EncK& k) {
   }
 }
 
+// CTAs per SM the NTT kernels are compiled for (register cap 65536 / (N/16 threads * this)). N =
+// 4096, 32-bit words: 4 (64 registers) for the two-poly batches of the plain calls (+8% on the
+// sweep), 3 for the one-poly share-add variant of the conv path (4 was slower in the step).
 template <class A, int LOGN, int NP>
 constexpr int ntt_min_blocks() {
-  return LOGN == 12 ? (sizeof(typename A::W) == 4 ? 3 : 2) : 1;
+  return LOGN == 12 ? (sizeof(typename A::W) == 4 ? (NP == 2 ? 4 : 3) : 2) : 1;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -479,7 +482,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, sizeof(typename A::W) == 4 &
 // shares the twiddles and the index arithmetic and every thread keeps 32 independent words in
 // flight (the 16-word version is latency bound on small layers). Mask and A8 on component b.
 template <class A>
-__global__ void __launch_bounds__(256, 3)
+__global__ void __launch_bounds__(256, 4)
     k_ntt_inv_tail2(typename A::W* polys, const __grid_constant__ DevConsts c, const uint64_t* __restrict__ r,
                     uint64_t* __restrict__ y0, const __grid_constant__ PlanDev pl, size_t ct0) {
   using W = typename A::W;

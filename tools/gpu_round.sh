@@ -17,3 +17,4 @@ if [ "${SKIP_NCU:-0}" != 1 ]; then
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_mac -c 1 -f -o $O/conv10_$TAG \
     python tools/prof_layer.py conv10 squeezenet1_1 2 32 > $O/ncu_full_$TAG.log 2>&1; echo "ncu full rc=$?"
 fi
+timeout 300 python tools/trace_step.py squeezenet1_1 32 > $O/trace_step_$TAG.txt 2>&1; echo "trace rc=$?"; tail -3 $O/trace_step_$TAG.txt

@@ -11,7 +11,7 @@ import torch
 
 import __graft_entry__
 from paper_2506_11586_b200 import Context
-from paper_2506_11586_b200.schedule import GroupRunner, concurrent_groups
+from paper_2506_11586_b200.schedule import GroupRunner, StagedGroupRunner, concurrent_groups
 from workloads import inputs, layers
 
 __graft_entry__.build()
@@ -36,9 +36,11 @@ for li, lay in enumerate(layers.network(net)):
     st.append(d)
 import os  # noqa: E402
 
-# the bench's schedule: every layer in network order (CONCURRENT=1: the experimental side streams)
-runner = GroupRunner(concurrent_groups([d["lay"].name for d in st]) if os.environ.get("CONCURRENT") else
-                     [[i] for i in range(len(st))], dev)
+# the bench's schedule (OVERLAP=staged, the default | none | free), as bench.py --overlap
+OVERLAP = os.environ.get("OVERLAP", "staged")
+names = [d["lay"].name for d in st]
+groups = concurrent_groups(names) if OVERLAP != "none" else [[i] for i in range(len(st))]
+runner = StagedGroupRunner(groups, dev) if OVERLAP == "staged" else GroupRunner(groups, dev)
 
 
 def call(i):
@@ -46,13 +48,25 @@ def call(i):
     ctx.he_conv2d(d["plan"], d["ct"], d["w"], x0=d["x0"], r=d["r"], out=d["out"], workspace=d["ws"], y0=d["y0"])
 
 
+def stage(i, k):
+    d = st[i]
+    ctx.he_conv2d_stage_ex(k, d["plan"], d["ct"], d["w"], d["x0"], d["r"], d["out"], d["y0"], d["ws"])
+
+
+def step():
+    if OVERLAP == "staged":
+        runner(call, stage)
+    else:
+        runner(call)
+
+
 for _ in range(3):
-    runner(call)
+    step()
 torch.cuda.synchronize()
 graph = torch.cuda.CUDAGraph()
 cap = torch.cuda.Stream(dev)
 with torch.cuda.graph(graph, stream=cap):
-    runner(call)
+    step()
 for _ in range(5):
     graph.replay()
 torch.cuda.synchronize()
