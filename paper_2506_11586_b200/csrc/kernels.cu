@@ -753,7 +753,7 @@ __device__ __forceinline__ void mac_intt_levels_0_7(typename A::W* cbuf, const t
 template <class W, int SG, int MT>
 __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
     k_mac(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmw, W* __restrict__ y,
-          const __grid_constant__ DevConsts c, PlanDev pl, int m_range, int n_sg, int NS) {
+          const __grid_constant__ DevConsts c, PlanDev pl, int m_range, int n_sg, int NS, int n_pre) {
   extern __shared__ __align__(128) unsigned char smraw[];
   PROBE_CTA(0);
   PROBE0(0);
@@ -794,23 +794,23 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
       prefetch_tmap(&tmw);
       const uint64_t evict_first = policy_evict_first();  // weights are read once per query
       // The weights are inputs of the call (never produced by the preceding kernel): the first
-      // lap of the ring is filled before the dependency wait, overlapping the forward NTT.
+      // n_pre stages of the ring are filled before the dependency wait, overlapping the forward
+      // NTT; then the X^ tile, so that it does not queue behind a whole lap of weights (the
+      // consumers need it before any stage), then the rest of the lap.
       int st = 0, issued = 0;
       uint32_t ph = 0, first = 1;  // ring position, its phase, and "first lap" (no wait needed)
       bool waited = false;
       for (int mb = m_begin; mb < m_end; mb += MT) {
         for (int g = 0; g < G; ++g) {
-          if (!first) {
-            if (!waited) {
-              pdl_wait();
-              waited = true;
-              // X^ tile (written by the forward NTT): box (256 coefficients, limb j, 2*SG rows
-              // (s, c), G groups) in [g][a][256] order
-              mbar_arrive_expect_tx(xbar, G * A2 * row_bytes);
-              tma_load_4d(xs, &tmx, e0, j, 2 * s0, 0, xbar);
-            }
-            mbar_wait(&empty[st], ph ^ 1);
+          if (!waited && (!first || issued == n_pre)) {
+            pdl_wait();
+            waited = true;
+            // X^ tile (written by the forward NTT): box (256 coefficients, limb j, 2*SG rows
+            // (s, c), G groups) in [g][a][256] order
+            mbar_arrive_expect_tx(xbar, G * A2 * row_bytes);
+            tma_load_4d(xs, &tmx, e0, j, 2 * s0, 0, xbar);
           }
+          if (!first) mbar_wait(&empty[st], ph ^ 1);
           // weights: box (256 coefficients, row g*L + j, MT output channels from mb)
           mbar_arrive_expect_tx(&full[st], MT * row_bytes);
           if (c.word_bits & 0x400)  // debug: no L2 cache hint on the weight stream
@@ -1502,8 +1502,10 @@ static cudaError_t mac_t(const DevConsts& c, const PlanDev& p, const void* xhat,
   W* yp = static_cast<W*>(y);
   DevConsts cc = c;  // debugging knobs ride in unused word_bits bits
   if (env_int("SECN_MAC_NOHINT", 0)) cc.word_bits |= 0x400;
+  // ring stages issued before the X^ tile (SECN_MAC_PRE: tuning knob)
+  const int n_pre = env_int("SECN_MAC_PRE", 2);
   cudaError_t e = launch_pdl(k_mac<W, SG, MT>, grid, dim3(MAC_THREADS + 32), smem, s, tmx, tmw, yp, cc, p, m_range,
-                             n_sg, NS);
+                             n_sg, NS, n_pre);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
