@@ -76,9 +76,10 @@ __device__ __forceinline__ typename A::W enc_mod(uint64_t v, const EncK& k) {
 // CTAs per SM the NTT kernels are compiled for (register cap 65536 / (N/16 threads * this)). N =
 // 4096, 32-bit words: 4 (64 registers) for the two-poly batches of the plain calls (+8% on the
 // sweep), 3 for the one-poly share-add variant of the conv path (4 was slower in the step).
+// N = 8192, 32-bit words: 2 (a lone CTA per SM idles at every barrier; +35% forward NTT/s).
 template <class A, int LOGN, int NP>
 constexpr int ntt_min_blocks() {
-  return LOGN == 12 ? (sizeof(typename A::W) == 4 ? (NP == 2 ? 4 : 3) : 2) : 1;
+  return LOGN == 12 ? (sizeof(typename A::W) == 4 ? (NP == 2 ? 4 : 3) : 2) : LOGN == 13 && sizeof(typename A::W) == 4 ? 2 : 1;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -226,7 +227,8 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN, NP>(
 // ------------------------------------------------------------------------------------------
 // Cluster NTT (N = 2^15; and 64-bit words at N = 2^14): at N = 2^15,
 // T = N/16 = 2048 threads would exceed a CTA and 64-bit words need 272 KiB of shared memory; at
-// 2^14 a 1024-thread CTA leaves 64 registers per thread, too few for 64-bit words. So a limb-poly
+// 2^14 a 1024-thread CTA leaves 64 registers per thread, too few for 64-bit words. (32-bit words
+// at 2^14 through two 512-thread cluster CTAs per SM measured slower: 10.8 vs 15.1 M NTT/s.) So a limb-poly
 // is transformed by a CLUSTER of two CTAs of 2^LOGH = N/2 points each. The first CT level (and
 // the last GS level) pairs coefficient e with e + N/2; every other level stays inside one half.
 // CTA h (cluster rank) owns half h and runs the 2^LOGH-point core on it with its own twiddle
