@@ -794,7 +794,7 @@ def run_reference(args, world, rank):
     v = statistics.mean(vals)
     out = {"impl": "reference", "metric": net_info(args.net)[0], "value": round(v, 3), "unit": "s", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(v * 1e3, 1), "higher_is_better": False,
-           "scaling": "strong", "vs_baseline": None, "dtype": f"u{ctx.word_bits}", "data": "synthetic",
+           "scaling": "strong", "vs_baseline": None, "dtype": f"u{args.word_bits}", "data": "synthetic",
            "config": {"workload": net_info(args.net)[1],
                       "N": P.n, "limbs": P.L, "t_bits": P.t_bits},
            "cpu_baseline": {"value": round(v, 3), "unit": "s", "cores": thr, "kind": "oracle",
