@@ -59,20 +59,53 @@ def full(i):
     ctx.he_conv2d(d["plan"], d["ct"], d["w"], x0=d["x0"], r=d["r"], out=d["out"], workspace=d["ws"])
 
 
+def full_mode(i):
+    # fork_empty: e3's branch does nothing; fork_copy: e3's branch only copies 1 GiB
+    if MODE == "fork_empty" and i == 2:
+        return
+    if MODE == "fork_copy" and i == 2:
+        BIG_B.copy_(BIG_A)
+        return
+    full(i)
+
+
 for trial in range(5):
     for d in st:
         d["out"].zero_()
     if trial % 2:
-        gr = torch.cuda.CUDAGraph()
+        gr = torch.cuda.CUDAGraph(keep_graph=(trial == 1))
+        if trial == 1:
+            gr.enable_debug_mode()
         cap = torch.cuda.Stream(dev)
         with torch.cuda.graph(gr, stream=cap):
-            runner(full)
+            runner(full_mode)
+        if trial == 1:
+            gr.debug_dump("gpurun_out/race_full_graph.dot")
         for d in st:
             d["out"].zero_()
         gr.replay()
     else:
-        runner(full)
+        runner(full_mode)
     torch.cuda.synchronize()
+    if trial % 2 and MODE == "classify":
+        # classify each wrong (ct, limb) unit of e1 / e3: which known array does it equal?
+        L4 = ctx.L
+        for i in (1, 2):
+            got = st[i]["out"].view(-1, 2, L4, ctx.n).cpu()
+            fin = refs[(i, 2)][1].view(-1, 2, L4, ctx.n).cpu()
+            mac = refs[(i, 1)][1].view(-1, 2, L4, ctx.n).cpu()
+            other = refs[(3 - i, 2)][1].view(-1, 2, L4, ctx.n).cpu()
+            for ct_ in range(got.shape[0]):
+                for jl in range(L4):
+                    g_ = got[ct_, :, jl]
+                    if torch.equal(g_, fin[ct_, :, jl]):
+                        continue
+                    tags = []
+                    if torch.equal(g_, mac[ct_, :, jl]): tags.append("=MAC output (Y^ after levels 0-7)")
+                    if bool((g_[0] == 0).all()): tags.append("a=0")
+                    if ct_ < other.shape[0] and torch.equal(g_, other[ct_, :, jl]): tags.append("=other layer final")
+                    nbad = int((g_ != fin[ct_, :, jl]).sum())
+                    print(f"   {st[i]['lay'].name} ct {ct_} limb {jl}: {nbad} words differ {tags}")
     for i in range(NL):
         got = st[i]["out"].view(-1, 256).cpu()
         ref_ = refs[(i, 2)][1].view(-1, 256).cpu()
