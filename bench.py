@@ -71,11 +71,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-online", action="store_true", help="skip the online-NTT-preprocessing (f4) leg")
     ap.add_argument("--no-sweep", action="store_true", help="skip the compact NTT sweep (C5) in the default run")
-    ap.add_argument("--overlap", choices=["none", "staged", "free"], default="staged",
-                    help="layers reading the same input (fire e1/e3, ResNet c1/ds): none = network order; "
-                         "staged = the group's layers run each launch group (NTT, MAC, tail) side by side and "
-                         "join between groups; free = whole layers on side streams, EXPERIMENTAL: "
-                         "tools/race_check.py shows wrong outputs under this overlap (DESIGN.md §9b)")
+    ap.add_argument("--overlap", choices=["none", "staged", "free"], default="free",
+                    help="layers reading the same input (fire e1/e3, ResNet c1/ds): free (default) = whole layers "
+                         "on side streams; staged = the group's layers run each launch group (NTT, MAC, tail) side "
+                         "by side and join between groups; none = network order on one stream")
     ap.add_argument("--concurrent", action="store_const", const="free", dest="overlap",
                     help="alias of --overlap free")
     return ap.parse_args()
@@ -474,8 +473,8 @@ def run_secn(args, word_bits, world, rank, local, dev, full):
                    "layer_overlap": {"none": "none: every layer in network order on one stream",
                                      "staged": "staged: layers reading the same input tensor (fire e1/e3, ResNet "
                                                "c1/ds) run each launch group side by side, joined between groups",
-                                     "free": "EXPERIMENTAL (--overlap free): layers reading the same input "
-                                             "tensor on side streams"}[args.overlap]},
+                                     "free": "free: layers reading the same input tensor (fire e1/e3, ResNet "
+                                             "c1/ds) on two streams; the rest in network order"}[args.overlap]},
         "throughput": {"ntt_per_s": round(n_ntt / step_s, 1), "alg_bytes_per_step": alg_bytes,
                        "alg_GBps": round(alg_bytes / step_s / 1e9, 1), "hbm_frac": round(alg_bytes / step_s / 1e9 / hbm_peak, 4),
                        "offline_preprocess_s": round(offline_s, 5), "wall_s_timed_region": round(wall, 4)},

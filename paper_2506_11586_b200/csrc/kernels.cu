@@ -590,6 +590,19 @@ struct ArithOf<uint64_t> {
   using A = Arith64;
 };
 
+// A consumer warp hands ring stage `bar` back to the producer, whose next TMA load overwrites it.
+// The stage's LDS must have READ shared memory first. ptxas issues the LDS, then sinks the
+// multiply-adds that consume their results below a plain arrive, so the arrive can complete
+// while the loads are still pending. A TMA write (async proxy) could then land under them: the
+// race that corrupted whole weight rows when another kernel's CTAs shared the SM and slowed the
+// LDS. The proxy fence orders each lane's generic-proxy reads before the
+// async-proxy writes that follow the release.
+__device__ __forceinline__ void consumer_release(uint64_t* bar) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive(bar);
+}
+
 // barrier among the MAC_THREADS consumer threads only (the producer warp never joins)
 __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(MAC_THREADS) : "memory"); }
 
@@ -871,8 +884,7 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
 #pragma unroll
           for (int a = 0; a < A2; ++a) acc[r][a] += (uint64_t)xv[a] * wv;  // < 2^56 each (q < 2^28), G <= 32
         }
-        __syncwarp();
-        if ((tid & 31) == 0) mbar_arrive(&empty[st]);
+        consumer_release(&empty[st]);
         if (++st == NS) st = 0, ph ^= 1;
       }
       if (tid < 32) bulk_wait_read0();  // the previous m-block's bulk stores have read the chunks
@@ -903,8 +915,7 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
 #pragma unroll
           for (int a = 0; a < A2; ++a) mac128(lo[r][a], hi[r][a], xv[a], wv);  // G <= 32 < 64 terms of < 2^122
         }
-        __syncwarp();
-        if ((tid & 31) == 0) mbar_arrive(&empty[st]);
+        consumer_release(&empty[st]);
         if (++st == NS) st = 0, ph ^= 1;
       }
       consumer_sync();  // the previous m-block's chunks have been written out

@@ -485,13 +485,14 @@ def test_end_to_end_decrypts_to_plain_conv(env):
     assert (y == conv.conv2d_mod((x0 + x1) & np.uint64(P.t - 1), K, lay.stride, lay.pad, P.t_bits)).all()
 
 
-@pytest.mark.parametrize("overlap", ["none", "staged"])
+@pytest.mark.parametrize("overlap", ["none", "staged", "free"])
 def test_network_step_graph_equals_layerwise(secn, overlap):
     """The bench's step (all SqueezeNet-1.1 layers in one CUDA graph, programmatic dependent
-    launches between the kernels; network order, or bench.py --overlap staged) gives, on every
-    layer, the words of the same layers run one call at a time with a synchronisation after each:
-    no cross-layer hazard."""
-    from paper_2506_11586_b200.schedule import StagedGroupRunner, concurrent_groups
+    launches between the kernels; network order, or bench.py --overlap staged / free) gives, on
+    every layer, the words of the same layers run one call at a time with a synchronisation after
+    each: no cross-layer hazard. Before k_mac released its ring stages through consumer_release
+    (proxy fence), the free overlap failed this in every replay."""
+    from paper_2506_11586_b200.schedule import GroupRunner, StagedGroupRunner, concurrent_groups
     ctx = secn.Context(0, word_bits=32)
     st = []
     for li, lay in enumerate(layers.squeezenet11()):
@@ -520,15 +521,18 @@ def test_network_step_graph_equals_layerwise(secn, overlap):
         ref.append((d["out"].clone(), d["y0"].clone()))
     names = [lay.name for lay in layers.squeezenet11()]
     runner = StagedGroupRunner(concurrent_groups(names), DEV)
+    free = GroupRunner(concurrent_groups(names), DEV)
     graph = torch.cuda.CUDAGraph()
     cap = torch.cuda.Stream(DEV)
     with torch.cuda.graph(graph, stream=cap):
         if overlap == "staged":
             runner(lambda i: call(st[i]), lambda i, k: stage(st[i], k))
+        elif overlap == "free":
+            free(lambda i: call(st[i]))
         else:
             for d in st:
                 call(d)
-    for _ in range(3):
+    for _ in range(10 if overlap == "free" else 3):
         for d in st:
             d["out"].zero_()
             d["y0"].zero_()

@@ -36,8 +36,8 @@ for li, lay in enumerate(layers.network(net)):
     st.append(d)
 import os  # noqa: E402
 
-# the bench's schedule (OVERLAP=staged, the default | none | free), as bench.py --overlap
-OVERLAP = os.environ.get("OVERLAP", "staged")
+# the bench's schedule (OVERLAP=free, the default | staged | none), as bench.py --overlap
+OVERLAP = os.environ.get("OVERLAP", "free")
 names = [d["lay"].name for d in st]
 groups = concurrent_groups(names) if OVERLAP != "none" else [[i] for i in range(len(st))]
 runner = StagedGroupRunner(groups, dev) if OVERLAP == "staged" else GroupRunner(groups, dev)
