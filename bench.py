@@ -568,6 +568,15 @@ def graph_ms(fn, K, warmup, dev, world):
     return float(ms.item())
 
 
+def _leg_overlap(runner):
+    """The schedule a secondary leg ran under: GroupRunner overlaps its groups on two streams; the
+    StagedGroupRunner has no staged form of these entry points and runs them in network order."""
+    from paper_2506_11586_b200.schedule import StagedGroupRunner
+    if isinstance(runner, StagedGroupRunner) or all(len(g) == 1 for g in runner.groups):
+        return "none: network order"
+    return "free: layers reading the same input on two streams"
+
+
 def run_online(ctx, st, K, warmup, dev, world, runner):
     """SURVEY.md §8f row 4 / PAPER.md:433, :498: the same step with the weights held in coefficient
     form (the tiny quantised kernels) and packed + transformed inside every secn32_he_conv2d_online
@@ -591,7 +600,7 @@ def run_online(ctx, st, K, warmup, dev, world, runner):
             "weights_held_bytes": held, "weights_held_offline_bytes": sum(d["w"].numel() * d["w"].element_size()
                                                                             for d in st if d["mc"] > 0),
             "path": "secn_he_conv2d_online: pack + NTT of the weights, then share add + NTT, MAC, INTT + mask",
-            "layer_overlap": "none (no stage-split form of this entry point): compare with the main step at --overlap none"}
+            "layer_overlap": _leg_overlap(runner)}
 
 
 def run_lwe(ctx, st, K, warmup, dev, world, runner):
@@ -622,7 +631,7 @@ def run_lwe(ctx, st, K, warmup, dev, world, runner):
     return {"value": round(ms / 1e3, 7), "unit": "s", "ms_per_step": round(ms, 4), "keep_limbs": keep,
             "output_bytes_per_step": out_bytes, "full_ct_output_bytes_per_step": full_bytes,
             "path": "secn32_he_conv2d_lwe: share add + NTT, MAC, INTT tail + mask + modulus switch + extraction",
-            "layer_overlap": "none (no stage-split form of this entry point)"}
+            "layer_overlap": _leg_overlap(runner)}
 
 
 def run_fc(ctx, K, warmup, dev, world, n_i=2048, n_o=1000, seed=11):
