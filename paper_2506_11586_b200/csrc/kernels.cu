@@ -1496,7 +1496,12 @@ static cudaError_t mac_t(const DevConsts& c, const PlanDev& p, const void* xhat,
   }
   // layers with few input groups or few output channels: one m-block per CTA (more, shorter CTAs
   // hide the INTT-level latency better; measured on the SqueezeNet fire layers)
-  if (p.G <= 4 || p.M <= 48) best_nmr = mblocks;
+  if (p.G <= 4 || p.M <= 48)
+    best_nmr = mblocks;
+  else if (xtile >= (size_t)MT * p.G * MAC_THREADS * sizeof(W) && env_int("SECN_MAC_XAMORT", 1))
+    // the X^ tile is at least one m-block of weights: a CTA takes >= 2 m-blocks so the tile load
+    // is amortised (conv1 of SqueezeNet-1.1: 79 -> 69 us)
+    best_nmr = best_nmr < (mblocks + 1) / 2 ? best_nmr : (mblocks + 1) / 2;
   if (const int nmr_env = env_int("SECN_MAC_NMR", 0)) best_nmr = nmr_env < mblocks ? nmr_env : mblocks;
   const int m_range = ((mblocks + best_nmr - 1) / best_nmr) * MT;
   const int n_mr = (p.M + m_range - 1) / m_range;
