@@ -700,8 +700,10 @@ __device__ __forceinline__ void mac_intt_levels_0_7(typename A::W* cbuf, const t
   if constexpr (kDense) {
     W x[2][16];
     const int t0 = threadIdx.x, t1 = threadIdx.x + MAC_THREADS;
+    if (t0 < ntask) {  // fewer than 16 chunks (MT x 2SG = 12 for SG = 3, MT = 2): not every thread has a task
 #pragma unroll
-    for (int i = 0; i < 16; ++i) x[0][i] = cbuf[(t0 >> 4) * MAC_CHS + (t0 & 15) + 17 * i];
+      for (int i = 0; i < 16; ++i) x[0][i] = cbuf[(t0 >> 4) * MAC_CHS + (t0 & 15) + 17 * i];
+    }
     if (t1 < ntask) {
 #pragma unroll
       for (int i = 0; i < 16; ++i) x[1][i] = cbuf[(t1 >> 4) * MAC_CHS + (t1 & 15) + 17 * i];

@@ -370,6 +370,33 @@ def test_he_conv2d_shapes_exact(env, lay):
     assert (got == ref).all()
 
 
+_MT32 = {1: (16, 8), 2: (8, 4), 3: (5, 2), 4: (3, 2)}  # k_mac m-block per s-group: (big, small), 32-bit
+
+
+@pytest.mark.parametrize("sg", [1, 2, 3, 4])
+@pytest.mark.parametrize("small", [False, True])
+def test_mac_register_blocks_exact(env, sg, small, monkeypatch):
+    """Every k_mac register-block instantiation (s-group SG x m-block MT, forced through the
+    SECN_MAC_SG / SECN_MAC_MT knobs) on a layer with G = 10, S = 3 (explicit 11 x 28 window),
+    exact against the oracle. SG = 3, MT = 2 stages only 12 chunks, fewer than the 16 that give
+    every thread an INTT task; its epilogue read past the end of shared memory before the guard
+    (found by tools/plan_sweep.py on a ResNet-50 candidate window)."""
+    ctx, P, D = env
+    if ctx.word_bits == 64 and small:
+        pytest.skip("64-bit limbs have one m-block size per s-group")
+    lay = L_("cfg", 128, 28, 28, 6, 1, 1, 0)
+    plan = ctx.plan(lay.C, lay.H, lay.W, lay.M, lay.k, stride=1, pad=0, Hw=11, Ww=28)
+    assert (plan.G, plan.S) == (10, 3)
+    opl = packing.plan_conv(lay.C, lay.H, lay.W, lay.M, 1, 1, 1, 0, P.n, ctx.coef_words64, Hw=11, Ww=28)
+    ct, x0, K, r = _layer_inputs(P, lay, 21, opl)
+    monkeypatch.setenv("SECN_MAC_SG", str(sg))
+    if ctx.word_bits == 32:
+        monkeypatch.setenv("SECN_MAC_MT", str(_MT32[sg][1 if small else 0]))
+    w = ctx.preprocess_weights(plan, TP(K))
+    got = D.U(ctx.he_conv2d(plan, D.R(ct), w, x0=TP(x0), r=TP(r)))
+    assert (got == he.server_conv(ct, x0, K, r, opl, P)).all()
+
+
 def _sampled_check(ctx, P, D, lay, seed, n_samples=3):
     opl = oplan(P, ctx, lay)
     ct, x0, K, r = _layer_inputs(P, lay, seed, opl)

@@ -88,8 +88,16 @@ def _poly_plan(lay, a, b):
     return p
 
 
+import os  # noqa: E402
+
+FROM = os.environ.get("PLAN_SWEEP_FROM")  # start at this layer (debugging)
+VERBOSE = bool(os.environ.get("PLAN_SWEEP_VERBOSE"))
 tot_def = tot_best = 0.0
+started = FROM is None
 for lay in layers.network(net):
+    started = started or lay.name == FROM
+    if not started:
+        continue
     g = inputs.rng(9)
     pdef = ctx.plan(lay.C, lay.H, lay.W, lay.M, lay.k, stride=lay.stride, pad=lay.pad)
     tdef = time_plan(pdef, lay, g)
@@ -103,6 +111,8 @@ for lay in layers.network(net):
             p = p.copy(decim=2)
             p = conv_plan(lay.C, lay.H, lay.W, lay.M, lay.k, lay.k, lay.stride, lay.pad, ctx.log_n, ctx.coef_words64,
                           a, b) if False else _poly_plan(lay, a, b)
+        if VERBOSE:
+            print("   timing", lay.name, p, flush=True)
         res.append((time_plan(p, lay, g), a, b, p.G, p.S, f"model {tm:.1f}{' poly' if poly else ''}"))
     best = min(res)
     tot_def += tdef
