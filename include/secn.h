@@ -105,7 +105,8 @@ const char* secn_last_error(void);
  * Hw,Ww when both are nonzero), choosing the packing window by `rule`:
  *   SECN_PLAN_BYTES: the byte-min rule of reading R6 (the oracle's plan_conv);
  *   SECN_PLAN_TIME:  reading R6b, the modelled device time of the integer-issue-bound path
- *                    (output, MAC and input limb-polys plus bytes), G <= 32.
+ *                    (output, MAC and input limb-polys plus bytes), G <= 30
+ *                    (G <= 32 when no window has G <= 30).
  * The packing (and so the oracle's result for the same window) is exact for every window; the
  * rule only picks the fastest. coef_words64 = 8-byte words per coefficient of one ciphertext
  * component (L for 64-bit limbs, L/2 for 32-bit limbs). SECN_EUNSUPPORTED if no window fits

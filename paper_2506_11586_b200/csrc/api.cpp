@@ -381,7 +381,11 @@ int secn_conv_plan_ex(uint32_t log_n, uint32_t n_limbs /* coef_words64 */, uint3
   // integer-issue-bound path, in ns per limb-poly of 4096 coefficients:
   //   13 per output limb-poly (INTT + mask), 1.3 per output limb-poly and input group (MAC),
   //   6 per input limb-poly (share add + NTT), and 0.3 x the bytes at 6.45 TB/s;
-  // only plans with G <= 32 (the MAC kernel's limit); ties: fewer bytes, larger Hw, larger Ww.
+  // only plans with G <= 30 (above, the MAC's X^ tile and a 4-stage ring leave one CTA per SM
+  // (ResNet-50 layer1 c3 takes 312 us at G = 32 and 241 us at G = 13;
+  // tools/plan_sweep.py); G <= 32, the MAC kernel's limit, when no window has G <= 30;
+  // ties: fewer bytes, larger Hw, larger Ww.
+  for (uint32_t gmax = rule == SECN_PLAN_TIME ? 30u : 32u;; gmax = 32u) {
   secn_conv_plan_t best{};
   bool have = false;
   double best_t = 0;
@@ -411,7 +415,7 @@ int secn_conv_plan_ex(uint32_t log_n, uint32_t n_limbs /* coef_words64 */, uint3
           better = !have || cost < best_cost || (cost == best_cost && mgs < best_mgs) ||
                    (cost == best_cost && mgs == best_mgs && (Hw > best.Hw || (Hw == best.Hw && Ww > best.Ww)));
         } else {
-          if (c.G > 32) continue;
+          if (c.G > gmax) continue;
           const double ms = (double)(M * S), gs = (double)(G * S);
           const double t = 2.0 * limb_polys * (13.0 * ms + 1.3 * ms * (double)c.G + 6.0 * gs) + 0.3 * (double)cost / 6450.0;
           better = !have || t < best_t * (1 - 1e-12) ||
@@ -423,9 +427,11 @@ int secn_conv_plan_ex(uint32_t log_n, uint32_t n_limbs /* coef_words64 */, uint3
       }
     }
   }
+  if (!have && gmax < 32u) continue;  // no window with G <= 30: allow up to the kernel's limit
   if (!have) return fail(SECN_EUNSUPPORTED, "unsupported shape: no window fits N");
   *p = best;
   return SECN_OK;
+  }
 }
 
 int secn_conv_plan(uint32_t log_n, uint32_t n_limbs /* coef_words64 */, secn_conv_plan_t* p) {
