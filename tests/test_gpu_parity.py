@@ -568,3 +568,42 @@ def test_network_step_graph_equals_layerwise(secn, overlap):
         for d, (o, y) in zip(st, ref):
             assert torch.equal(d["out"], o) and torch.equal(d["y0"], y)
     ctx.close()
+
+
+def _fuzz_layers(n=20, seed=2026):
+    g = np.random.default_rng(seed)
+    out = []
+    for i in range(n):
+        k = int(g.choice([1, 3, 5, 7]))
+        st = int(g.choice([1, 2]))
+        pad = int(g.integers(0, k // 2 + 1))
+        H = int(g.integers(max(k, 2), 41))
+        W = int(g.integers(max(k, 2), 41))
+        C = int(g.integers(1, 97))
+        M = int(g.integers(1, 49))
+        out.append(L_(f"fz{i}_c{C}h{H}w{W}m{M}k{k}s{st}p{pad}", C, H, W, M, k, st, pad))
+    return out
+
+
+@pytest.mark.parametrize("rule", ["time", "bytes"])
+@pytest.mark.parametrize("lay", _fuzz_layers(), ids=lambda l: l.name)
+def test_he_conv2d_ex_random_shapes_exact(env, lay, rule):
+    """Seeded random layer geometries (kernel 1-7, stride 1-2, padding, odd sizes), each under the
+    time-rule window (polyphase where it wins) and the byte-min window: ciphertexts and the fused
+    share y0 equal to the oracle word for word."""
+    ctx, P, D = env
+    plan = ctx.plan(lay.C, lay.H, lay.W, lay.M, lay.k, stride=lay.stride, pad=lay.pad,
+                    rule=secn_mod().PLAN_TIME if rule == "time" else secn_mod().PLAN_BYTES)
+    opl = packing.plan_conv(lay.C, lay.H, lay.W, lay.M, lay.k, lay.k, lay.stride, lay.pad, P.n, ctx.coef_words64,
+                            Hw=plan.Hw, Ww=plan.Ww, poly=plan.decim == 2)
+    ct, x0, K, r = _layer_inputs(P, lay, 31, opl)
+    w = ctx.preprocess_weights(plan, TP(K))
+    y0 = torch.full((plan.M, plan.OH, plan.OW), -1, dtype=torch.int64, device=DEV)
+    got = D.U(ctx.he_conv2d(plan, D.R(ct), w, x0=TP(x0), r=TP(r), y0=y0))
+    assert (got == he.server_conv(ct, x0, K, r, opl, P)).all()
+    assert (UP(y0) == packing.extract((P.t - r) % P.t, opl)).all()
+
+
+def secn_mod():
+    from paper_2506_11586_b200 import secn as m
+    return m
