@@ -102,3 +102,21 @@ def test_lwe_rejects_bad_keep(env):
     for keep in (0, ctx.L):
         with pytest.raises(m.SecnError):
             ctx.he_conv2d_lwe(plan, ct, w, keep)
+
+
+@pytest.mark.parametrize("lay", __import__("test_gpu_parity")._fuzz_layers(8, seed=77), ids=lambda l: l.name)
+def test_he_conv2d_lwe_random_shapes(env, lay):
+    """The extracted outputs (modulus switch + designated coefficients) on seeded random layer
+    geometries, every keep, against the oracle word for word."""
+    ctx, P, D = env
+    opl = oplan(P, ctx, lay)
+    ct, x0, K, r = _layer_inputs(P, lay, 63, opl)
+    plan = ctx.plan(lay.C, lay.H, lay.W, lay.M, lay.k, stride=lay.stride, pad=lay.pad)
+    w = ctx.preprocess_weights(plan, TP(K))
+    full = he.server_conv(ct, x0, K, r, opl, P)
+    s_idx, coef = packing.designated_map(opl)
+    for keep in _keeps(P):
+        a, b = ctx.he_conv2d_lwe(plan, D.R(ct), w, keep, x0=TP(x0), r=TP(r))
+        ra, rb = extract.server_lwe_outputs(full, keep, P, s_idx, coef, opl.M, opl.S)
+        assert (D.U(a) == ra).all(), keep
+        assert (D.U(b) == rb).all(), keep
