@@ -426,6 +426,8 @@ def run_secn(args, word_bits, world, rank, local, dev, full):
 
     # ---- f2: extracted outputs (modulus switch + designated coefficients) ----
     lwe = run_lwe(ctx, st, K, args.warmup, dev, world, runner)
+    if not args.no_e2e:  # the same step end to end, sending back only the extracted outputs
+        lwe["e2e"] = run_e2e(ctx, st, K, dev, share_buf, world, runner, lwe_keep=ctx.L // 2)
 
     # ---- f3: the ResNet-50 fully-connected layer through secn_he_fc ----
     fc_leg = run_fc(ctx, K, args.warmup, dev, world)
@@ -656,25 +658,38 @@ def run_fc(ctx, K, warmup, dev, world, n_i=2048, n_o=1000, seed=11):
             "hbm_frac": round(alg / (ms / 1e3) / 1e9 / peaks()[0], 4), "launches": 3}
 
 
-def run_e2e(ctx, st, K, dev, share_buf, world, runner):
+def run_e2e(ctx, st, K, dev, share_buf, world, runner, lwe_keep=None):
     """Same metric end to end through the public API: every step copies that step's inputs
     (ct_in, x0, r) host->device from pinned memory, runs secn_he_conv2d_ex (ciphertexts and the
-    server's shares) per layer, and copies the output ciphertexts and shares device->host."""
+    server's shares) per layer, and copies the output ciphertexts and shares device->host.
+    With lwe_keep, the call is secn32_he_conv2d_lwe instead and the device->host copy is the
+    extracted, modulus-switched outputs (what Cheetah's server sends)."""
     host = []
     h2d = d2h = 0
     for d in st:
         if d["mc"] <= 0:
             continue
+        if lwe_keep:
+            pl = d["plan"]
+            d["ws_lwe"] = torch.empty((int(ctx_lib().secn_he_conv2d_lwe_workspace(ctx._h, ctypes.byref(d["pl"]))) + 7)
+                                      // 8, dtype=torch.int64, device=dev)
+            d["lwe_out"] = (ctx.empty(d["mc"] * pl.S, lwe_keep, ctx.n), ctx.empty(d["mc"], pl.OH, pl.OW, lwe_keep))
         ct = np.ascontiguousarray(d["ct_h"])
         ct = ct.view(np.int64) if d["ct"].dtype == torch.int64 else ct.astype(np.uint32).view(np.int32)
         h = {"ct": torch.from_numpy(ct).pin_memory(),
              "x0": torch.from_numpy(np.ascontiguousarray(d["x0_h"]).view(np.int64)).pin_memory()}
         S = d["plan"].S
         h["r"] = torch.from_numpy(np.ascontiguousarray(d["r_h"][d["m0"] * S:(d["m0"] + d["mc"]) * S]).view(np.int64)).pin_memory()
-        h["out"] = torch.empty(d["out"].shape, dtype=d["out"].dtype).pin_memory()
+        if lwe_keep:
+            h["lwe_out"] = tuple(torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in d["lwe_out"])
+            h["out"] = torch.empty(0, dtype=d["out"].dtype)
+            d2h += sum(t.numel() * t.element_size() for t in h["lwe_out"])
+        else:
+            h["out"] = torch.empty(d["out"].shape, dtype=d["out"].dtype).pin_memory()
+            d2h += h["out"].numel() * h["out"].element_size()
         h["y0"] = torch.empty(d["y0"].shape, dtype=torch.int64).pin_memory()
         h2d += sum(h[k].numel() * h[k].element_size() for k in ("ct", "x0", "r"))
-        d2h += h["out"].numel() * h["out"].element_size() + h["y0"].numel() * 8
+        d2h += h["y0"].numel() * 8
         host.append((d, h))
 
     # Three streams, as a serving loop would run them: host->device copies, the library calls and
@@ -700,13 +715,21 @@ def run_e2e(ctx, st, K, dev, share_buf, world, runner):
             cs.wait_event(e_in)
             if k in out_done:
                 cs.wait_event(out_done[k])
-            ctx.he_conv2d(d["pl"], d["ct"], d["w"], x0=d["x0"], r=d["r"], out=d["out"], workspace=d["ws"],
-                          y0=d["y0"])
+            if lwe_keep:
+                ctx.he_conv2d_lwe(d["pl"], d["ct"], d["w"], lwe_keep, x0=d["x0"], r=d["r"], y0=d["y0"],
+                                  workspace=d["ws_lwe"], out=d["lwe_out"])
+            else:
+                ctx.he_conv2d(d["pl"], d["ct"], d["w"], x0=d["x0"], r=d["r"], out=d["out"], workspace=d["ws"],
+                              y0=d["y0"])
             comp_done[k] = torch.cuda.Event()
             comp_done[k].record(cs)
             ds.wait_event(comp_done[k])
             with torch.cuda.stream(ds):
-                h["out"].copy_(d["out"], non_blocking=True)
+                if lwe_keep:
+                    for hd, dd in zip(h["lwe_out"], d["lwe_out"]):
+                        hd.copy_(dd, non_blocking=True)
+                else:
+                    h["out"].copy_(d["out"], non_blocking=True)
                 h["y0"].copy_(d["y0"], non_blocking=True)
                 out_done[k] = torch.cuda.Event()
                 out_done[k].record(ds)
@@ -734,11 +757,17 @@ def run_e2e(ctx, st, K, dev, share_buf, world, runner):
     if world > 1:
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     # the host copies of the last step equal the device results (every step has the same inputs)
-    same = all(torch.equal(h["out"], d["out"].cpu()) and torch.equal(h["y0"], d["y0"].cpu()) for d, h in host)
+    outs = (lambda d, h: zip(h["lwe_out"], d["lwe_out"])) if lwe_keep else (lambda d, h: [(h["out"], d["out"])])
+    same = all(all(torch.equal(ho, do.cpu()) for ho, do in outs(d, h)) and torch.equal(h["y0"], d["y0"].cpu())
+               for d, h in host)
+    for d, _ in host:
+        d.pop("ws_lwe", None)
+        d.pop("lwe_out", None)
+    call = f"secn32_he_conv2d_lwe (keep {lwe_keep} limbs)" if lwe_keep else "secn_he_conv2d_ex"
     return {"value": round(float(ms.item()) / 1e3, 6), "unit": "s", "host_copies_match_device": same,
             "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h,
-            "path": "pinned host -> secn_he_conv2d_ex -> pinned host; H2D, calls and D2H on three streams (per-layer "
+            "path": f"pinned host -> {call} -> pinned host; H2D, calls and D2H on three streams (per-layer "
                     "events), so copies of one layer overlap the other layers' compute and each other"}
 
 

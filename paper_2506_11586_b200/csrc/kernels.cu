@@ -1290,7 +1290,7 @@ static cudaError_t ntt_fwd_t(const DevConsts& c, const void* in, void* out, size
                              cudaStream_t s) {
   const size_t n_polys = P / c.L;
   if constexpr (sizeof(typename A::W) == 4 && LOGN == 12)
-    if (n_polys % 2 == 0 && P >= 2 * 148 * 6) return ntt_fwd_np<A, LOGN, 2>(c, in, out, n_polys, x0, s);
+    if (n_polys % 2 == 0 && P >= (size_t)env_int("SECN_NTT_NP2_MIN", 2 * 148 * 6)) return ntt_fwd_np<A, LOGN, 2>(c, in, out, n_polys, x0, s);
   return ntt_fwd_np<A, LOGN, 1>(c, in, out, n_polys, x0, s);
 }
 
@@ -1298,7 +1298,7 @@ template <class A, int LOGN>
 static cudaError_t ntt_inv_t(const DevConsts& c, void* polys, size_t P, const uint64_t* r, cudaStream_t s) {
   const size_t n_polys = P / c.L;
   if constexpr (sizeof(typename A::W) == 4 && LOGN == 12)
-    if (n_polys % 2 == 0 && P >= 2 * 148 * 6) return ntt_inv_np<A, LOGN, 2>(c, polys, n_polys, r, s);
+    if (n_polys % 2 == 0 && P >= (size_t)env_int("SECN_NTT_NP2_MIN", 2 * 148 * 6)) return ntt_inv_np<A, LOGN, 2>(c, polys, n_polys, r, s);
   return ntt_inv_np<A, LOGN, 1>(c, polys, n_polys, r, s);
 }
 

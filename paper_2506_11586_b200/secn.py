@@ -285,11 +285,12 @@ class Context:
     # ---- extracted outputs (f2): modulus switch to `keep` limbs + designated coefficients ----
     def he_conv2d_lwe(self, plan: Plan, ct_in: torch.Tensor, w_ntt: torch.Tensor, keep: int,
                       x0: Optional[torch.Tensor] = None, r: Optional[torch.Tensor] = None,
-                      y0: Optional[torch.Tensor] = None, workspace: Optional[torch.Tensor] = None, stream=None):
-        """secn_he_conv2d_lwe -> (a' [M*S][keep][N], b' [M][OH][OW][keep]) in the residue dtype."""
+                      y0: Optional[torch.Tensor] = None, workspace: Optional[torch.Tensor] = None, stream=None,
+                      out: Optional[tuple] = None):
+        """secn_he_conv2d_lwe -> (a' [M*S][keep][N], b' [M][OH][OW][keep]) in the residue dtype
+        (written into `out` = (a', b') when given)."""
         L, n = self.L, self.n
-        a = self.empty(plan.M * plan.S, keep, n)
-        b = self.empty(plan.M, plan.OH, plan.OW, keep)
+        a, b = out if out is not None else (self.empty(plan.M * plan.S, keep, n), self.empty(plan.M, plan.OH, plan.OW, keep))
         if workspace is None:
             ws = int(lib().secn_he_conv2d_lwe_workspace(self._h, ctypes.byref(plan)))
             workspace = torch.empty((ws + 7) // 8, dtype=torch.int64, device=self.device)

@@ -35,6 +35,11 @@ def test_he_conv2d_lwe_matches_oracle(env, lay):
         assert (D.U(a) == ra).all(), keep
         assert (D.U(b) == rb).all(), keep
         assert (UP(y0) == packing.extract((P.t - r) % P.t, opl)).all()
+        # caller-owned output buffers (the bench's extracted-output e2e leg): same words
+        oa, ob = torch.full_like(a, -1), torch.full_like(b, -1)
+        a2, b2 = ctx.he_conv2d_lwe(plan, D.R(ct), w, keep, x0=TP(x0), r=TP(r), y0=y0, out=(oa, ob))
+        assert a2.data_ptr() == oa.data_ptr() and b2.data_ptr() == ob.data_ptr()
+        assert (D.U(oa) == ra).all() and (D.U(ob) == rb).all(), keep
 
 
 def test_he_conv2d_lwe_end_to_end_decrypt(env):
