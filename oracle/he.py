@@ -123,7 +123,16 @@ def server_mac(ct_in: np.ndarray, x0: Optional[np.ndarray], kp: np.ndarray, r: O
     """The server's linear-layer computation for any packing:
     out[m,s] = sum_{g<G} (in[g,s] + enc(x0[g,s]) on b) (*) lift(kp[m,g])  (+ enc(r[m,s]) on b),
     with kp [M][G][N] the raw plaintext polys (values < 2^t, centred-lifted per limb)."""
-    koff, kidx, kval = sparse(kp)
+    return server_mac_sparse(ct_in, x0, sparse(kp), r, G, S, M, P, sel, out)
+
+
+def server_mac_sparse(ct_in: np.ndarray, x0: Optional[np.ndarray], kp_sparse, r: Optional[np.ndarray],
+                      G: int, S: int, M: int, P: Params, sel: Optional[np.ndarray] = None,
+                      out: Optional[np.ndarray] = None) -> np.ndarray:
+    """server_mac with the plaintext polys already in sparse form (koff, kidx, kval) =
+    packing.sparse(kp): the weights are packed once per layer (the server's offline setup,
+    PAPER.md:427 §7 step 1) and every online call reuses them."""
+    koff, kidx, kval = kp_sparse
     ct_in = np.ascontiguousarray(ct_in, dtype=np.uint64)
     assert ct_in.shape == (G * S, 2, P.L, P.n), ct_in.shape
     if out is None:

@@ -100,13 +100,20 @@ def _geometry(C, H, W, kh, kw, stride, pad, poly=False):
     return OH, OW, decim, Hp, Wp, Ph, Pw
 
 
-def plan_conv(C, H, W, M, kh, kw, stride=1, pad=0, n=4096, L=2, Hw=None, Ww=None, poly=False) -> Plan:
-    """Reading R6: enumerate Hw in [khe, Hp], Ww in [kwe, Wp] with Hw*Ww <= N, take
+def plan_conv(C, H, W, M, kh, kw, stride=1, pad=0, n=4096, L=2, Hw=None, Ww=None, poly=False,
+              rule="bytes") -> Plan:
+    """Reading R6 (rule="bytes"): enumerate Hw in [khe, Hp], Ww in [kwe, Wp] with Hw*Ww <= N, take
     Cw = min(Ce, N // (Hw*Ww)), and minimise the algorithmic bytes
         8*L*N*(2*G*S + M*G + 2*M*S) + 8*N*M*S
     tie-breaking on fewer M*G*S products, then larger Hw, then larger Ww.
     An explicit (Hw, Ww) is validated and used instead. poly: the polyphase split of reading
-    R7b (strided kernels larger than 1x1)."""
+    R7b (strided kernels larger than 1x1). L is the number of 8-byte words per coefficient of one
+    ciphertext component (the limb count for 64-bit limbs, half of it for 32-bit limbs).
+    rule="time": reading R6b, see plan_conv_time (Hw, Ww, poly are then ignored)."""
+    if rule == "time":
+        return plan_conv_time(C, H, W, M, kh, kw, stride, pad, n, L)
+    if rule != "bytes":
+        raise ValueError(f"unknown plan rule {rule!r}")
     OH, OW, decim, Hp, Wp, Ph, Pw = _geometry(C, H, W, kh, kw, stride, pad, poly)
     if OH <= 0 or OW <= 0 or kh * kw > n:
         raise ValueError("unsupported shape")
@@ -131,6 +138,44 @@ def plan_conv(C, H, W, M, kh, kw, stride=1, pad=0, n=4096, L=2, Hw=None, Ww=None
     _, a, b, Cw, G, S, nbh, nbw = best
     O = (Cw - 1) * a * b + (khe - 1) * b + (kwe - 1)
     return Plan(C, H, W, M, kh, kw, stride, pad, OH, OW, decim, Hp, Wp, Cw, a, b, G, S, nbh, nbw, O)
+
+
+def plan_conv_time(C, H, W, M, kh, kw, stride=1, pad=0, n=4096, L=2) -> Plan:
+    """Reading R6b (the window rule the product library applies by default): among
+    every valid window -- plain and, for a strided kernel larger than 1x1, polyphase (reading R7b)
+    -- with G <= 30 (G <= 32 if no window has G <= 30), minimise the modelled device time in ns
+        t = 2 lp (13 M S + 1.3 M S G + 6 G S) + 0.3 bytes / 6450,   lp = 2 L N / 4096
+    (bytes = the R6 algorithmic bytes). Windows are scanned plain before polyphase, Hw then Ww
+    ascending; a window replaces the best so far if its t is smaller by a relative 1e-12, or
+    equal within 1e-12 and it has fewer bytes, or the same bytes and a larger Hw, then Ww. The
+    packing (and so every result) is exact for any window; the rule only picks a fast one."""
+    can_poly = stride > 1 and not (kh == 1 and kw == 1)
+    lp = 2.0 * L * n / 4096.0
+    for gmax in (30, 32):
+        best = None
+        best_t = best_cost = 0
+        for poly in ((False, True) if can_poly else (False,)):
+            OH, OW, decim, Hp, Wp, Ph, Pw = _geometry(C, H, W, kh, kw, stride, pad, poly)
+            ps = stride if decim == 2 else 1
+            khe, kwe = -(-kh // ps), -(-kw // ps)
+            for a in range(khe, Hp + 1):
+                for b in range(kwe, Wp + 1):
+                    if a * b > n:
+                        break
+                    p = plan_conv(C, H, W, M, kh, kw, stride, pad, n, L, Hw=a, Ww=b, poly=poly)
+                    if p.G > gmax:
+                        continue
+                    G, S = p.G, p.S
+                    cost = 8 * L * n * (2 * G * S + M * G + 2 * M * S) + 8 * n * M * S
+                    ms, gs = float(M * S), float(G * S)
+                    t = 2.0 * lp * (13.0 * ms + 1.3 * ms * float(G) + 6.0 * gs) + 0.3 * float(cost) / 6450.0
+                    if (best is None or t < best_t * (1 - 1e-12) or
+                            (t <= best_t * (1 + 1e-12) and
+                             (cost < best_cost or (cost == best_cost and (a > best.Hw or (a == best.Hw and b > best.Ww)))))):
+                        best, best_t, best_cost = p, t, cost
+        if best is not None:
+            return best
+    raise ValueError("unsupported shape: no window fits N")
 
 
 def effective_input(x: np.ndarray, p: Plan) -> np.ndarray:

@@ -67,44 +67,27 @@ def test_c_plan_other_ring_sizes_and_explicit_windows(secn):
     assert (c.Cw, c.G, c.S, c.nbh, c.nbw, c.O) == (o.Cw, o.G, o.S, o.nbh, o.nbw, o.O)
 
 
-def _time_rule(l, n, cw, gmax=30):
-    """Reading R6b restated: the window (plain or, for strided kernels larger than 1x1,
-    polyphase, reading R7b) minimising the modelled time (include/secn.h), among G <= 30, or
-    G <= 32 when no window has G <= 30."""
-    best = None
-    for poly in ([False, True] if l.stride > 1 and l.k > 1 else [False]):
-        OH, OW, decim, Hp, Wp, Ph, Pw = packing._geometry(l.C, l.H, l.W, l.k, l.k, l.stride, l.pad, poly)
-        ke = -(-l.k // l.stride) if poly else l.k
-        for a in range(ke, Hp + 1):
-            for b in range(ke, Wp + 1):
-                if a * b > n:
-                    break
-                o = packing.plan_conv(l.C, l.H, l.W, l.M, l.k, l.k, l.stride, l.pad, n, cw, Hw=a, Ww=b, poly=poly)
-                if o.G > gmax:
-                    continue
-                G, S, M = o.G, o.S, l.M
-                cost = 8 * cw * n * (2 * G * S + M * G + 2 * M * S) + 8 * n * M * S
-                lp = 2.0 * cw * n / 4096.0
-                t = 2.0 * lp * (13.0 * M * S + 1.3 * M * S * G + 6.0 * G * S) + 0.3 * cost / 6450.0
-                key = (t, cost, -a, -b)
-                if best is None or key[0] < best[0][0] * (1 - 1e-12) or (
-                        key[0] <= best[0][0] * (1 + 1e-12) and key[1:] < best[0][1:]):
-                    best = (key, o)
-    if best is None and gmax < 32:
-        return _time_rule(l, n, cw, 32)
-    return best[1]
-
-
 @pytest.mark.parametrize("net", ["tiny", "squeezenet1_1", "squeezenet1_0", "resnet50"])
-def test_c_time_plan_matches_python_rule(secn, net):
-    """The default plan (reading R6b): a valid window of the oracle's packing, G <= 32, equal to
-    the rule restated in Python, and never modelled slower than the byte-min plan."""
+def test_c_time_plan_matches_oracle_time_rule(secn, net):
+    """The default plan (reading R6b): the library's window equals the oracle's
+    plan_conv(rule="time") on every layer, G <= 32, and it is never modelled slower than the
+    byte-min plan. The tests, smoke() and bench.py take the window from the oracle and assert this
+    equality, so no oracle input depends on the product library."""
     fields = ("OH", "OW", "decim", "Hp", "Wp", "Cw", "Hw", "Ww", "G", "S", "nbh", "nbw", "O")
     for l in layers.network(net):
         c = secn.conv_plan(l.C, l.H, l.W, l.M, l.k, stride=l.stride, pad=l.pad)
-        o = _time_rule(l, 4096, 2)
+        o = packing.plan_conv(l.C, l.H, l.W, l.M, l.k, l.k, l.stride, l.pad, 4096, 2, rule="time")
         assert tuple(getattr(c, f) for f in fields) == tuple(getattr(o, f) for f in fields), l.name
         assert c.G <= 32
+
+
+@pytest.mark.parametrize("logn,cw", [(12, 1), (12, 4), (13, 2), (14, 2)])
+def test_c_time_plan_matches_oracle_other_rings(secn, logn, cw):
+    fields = ("decim", "Cw", "Hw", "Ww", "G", "S", "O")
+    for l in layers.squeezenet11()[:6] + [layers.ConvLayer("s2", 32, 30, 30, 40, 5, 2, 2)]:
+        c = secn.conv_plan(l.C, l.H, l.W, l.M, l.k, stride=l.stride, pad=l.pad, log_n=logn, n_limbs=cw)
+        o = packing.plan_conv(l.C, l.H, l.W, l.M, l.k, l.k, l.stride, l.pad, 1 << logn, cw, rule="time")
+        assert tuple(getattr(c, f) for f in fields) == tuple(getattr(o, f) for f in fields), (l.name, logn, cw)
 
 
 @pytest.mark.parametrize("n_i,n_o,logn,cw", [(2048, 1000, 12, 2), (512, 1000, 12, 2), (64, 16, 12, 2), (4096, 1, 12, 1),

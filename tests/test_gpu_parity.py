@@ -72,12 +72,24 @@ def env(request, secn):
     ctx.close()
 
 
-def oplan(P, ctx, lay):
-    """The oracle's plan for the packing window the library chose (the window is a performance
-    choice; the oracle computes the same packing for any valid window)."""
-    c = ctx.plan(lay.C, lay.H, lay.W, lay.M, lay.k, stride=lay.stride, pad=lay.pad)
-    return packing.plan_conv(lay.C, lay.H, lay.W, lay.M, lay.k, lay.k, lay.stride, lay.pad, P.n, ctx.coef_words64,
-                             Hw=c.Hw, Ww=c.Ww, poly=c.decim == 2)
+PLAN_FIELDS = ("OH", "OW", "decim", "Hp", "Wp", "Cw", "Hw", "Ww", "G", "S", "nbh", "nbw", "O")
+
+
+def same_plan(opl, plan):
+    """The oracle's plan and the library's agree field by field (the window is a performance
+    choice; the oracle's packing is exact for any valid window, so this is a plan-rule check)."""
+    assert tuple(getattr(opl, f) for f in PLAN_FIELDS) == tuple(getattr(plan, f) for f in PLAN_FIELDS), (opl, plan)
+
+
+def oplan(P, ctx, lay, rule="time"):
+    """The oracle's own plan (reading R6b time rule by default, or R6 byte-min), computed without
+    the product library and asserted equal to the window the library picks for this layer."""
+    opl = packing.plan_conv(lay.C, lay.H, lay.W, lay.M, lay.k, lay.k, lay.stride, lay.pad, P.n, ctx.coef_words64,
+                            rule=rule)
+    c = ctx.plan(lay.C, lay.H, lay.W, lay.M, lay.k, stride=lay.stride, pad=lay.pad,
+                 rule=secn_mod().PLAN_TIME if rule == "time" else secn_mod().PLAN_BYTES)
+    same_plan(opl, c)
+    return opl
 
 
 # ---------------------------------------------------------------------------------------------
@@ -594,8 +606,7 @@ def test_he_conv2d_ex_random_shapes_exact(env, lay, rule):
     ctx, P, D = env
     plan = ctx.plan(lay.C, lay.H, lay.W, lay.M, lay.k, stride=lay.stride, pad=lay.pad,
                     rule=secn_mod().PLAN_TIME if rule == "time" else secn_mod().PLAN_BYTES)
-    opl = packing.plan_conv(lay.C, lay.H, lay.W, lay.M, lay.k, lay.k, lay.stride, lay.pad, P.n, ctx.coef_words64,
-                            Hw=plan.Hw, Ww=plan.Ww, poly=plan.decim == 2)
+    opl = oplan(P, ctx, lay, rule)
     ct, x0, K, r = _layer_inputs(P, lay, 31, opl)
     w = ctx.preprocess_weights(plan, TP(K))
     y0 = torch.full((plan.M, plan.OH, plan.OW), -1, dtype=torch.int64, device=DEV)
