@@ -28,8 +28,14 @@
  *  - Thread safety: a context is immutable after creation; concurrent calls on different
  *    streams (and threads) are safe.
  *  - Range checks of input VALUES (residue < q_j, share < 2^t_bits) cost bandwidth and run
- *    only when the environment variable SECN_VALIDATE=1 is set (then the call synchronises
- *    its stream and returns SECN_ERANGE on a violation).
+ *    only when the environment variable SECN_VALIDATE=1 is set when the context is created
+ *    (then each call synchronises its stream and returns SECN_ERANGE on a violation; validated
+ *    calls on one context are serialised, and they cannot be captured into a CUDA graph).
+ *  - The other SECN_* environment variables are developer tuning knobs, also read once at
+ *    context creation; the defaults are the measured best.
+ *  - Ordering: a call may be scheduled, through programmatic dependent launch, while the
+ *    preceding kernel on `stream` finishes; it reads nothing that kernel may have written before
+ *    waiting for it, so inputs written by any earlier work on the stream are always seen.
  */
 #ifndef SECN_H_
 #define SECN_H_

@@ -101,15 +101,12 @@ struct DeviceGuard {
   }
 };
 
-bool validate_env() {
-  const char* v = std::getenv("SECN_VALIDATE");
-  return v && v[0] == '1';
-}
-
-// With SECN_VALIDATE=1: synchronously check that `n_words` words are in range
-// (kind 0: residues < q_j by limb, kind 1: < 2^t_bits).
+// With SECN_VALIDATE=1 (read at context creation): synchronously check that `n_words` words are
+// in range (kind 0: residues < q_j by limb, kind 1: < 2^t_bits). The context's one flag word is
+// shared by every validated call, so the whole check runs under the context's mutex.
 int check_range(secn_ctx* ctx, const void* v, size_t n_words, int kind, cudaStream_t s, const char* what) {
-  if (!validate_env() || v == nullptr || n_words == 0) return SECN_OK;
+  if (!ctx->dc.tune.validate || v == nullptr || n_words == 0) return SECN_OK;
+  std::lock_guard<std::mutex> lock(*ctx->flag_mutex);
   cudaError_t e = cudaMemsetAsync(ctx->d_flag, 0, sizeof(uint32_t), s);
   if (e == cudaSuccess) e = secn::launch_check_range(ctx->dc, v, n_words, kind, ctx->d_flag, s);
   uint32_t flag = 0;
@@ -215,6 +212,7 @@ static int ctx_create_impl(secn_ctx** out, int device, uint32_t log_n, uint32_t 
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
     return fail(SECN_ESTATE, "device %d not available", device);
   DeviceGuard guard(device);
+  if (cudaError_t e = secn::init_device(word_bits); e != cudaSuccess) return cuda_fail(e, "kernel attributes");
 
   secn_ctx* c = new secn_ctx();
   c->device = device, c->log_n = log_n, c->n = (uint32_t)n, c->L = n_limbs, c->t_bits = t_bits;
@@ -222,6 +220,7 @@ static int ctx_create_impl(secn_ctx** out, int device, uint32_t log_n, uint32_t 
   secn::DevConsts& dc = c->dc;
   std::memset(&dc, 0, sizeof dc);
   dc.t_bits = t_bits, dc.log_n = log_n, dc.L = n_limbs, dc.word_bits = word_bits;
+  secn::read_tune(device, &dc.tune);
   const uint64_t t = 1ull << t_bits, tmask = t - 1;
   // Q mod t = prod (q_j mod t) mod t (t a power of two)
   uint64_t qmt = 1;
@@ -313,9 +312,11 @@ static int ctx_create_impl(secn_ctx** out, int device, uint32_t log_n, uint32_t 
   if (e == cudaSuccess) e = cudaMemcpy(c->d_tables, tw.data(), tw_bytes, cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
     cudaFree(c->d_tables);
+    cudaFree(c->d_flag);
     delete c;
     return cuda_fail(e, "ctx tables");
   }
+  c->flag_mutex = new std::mutex();
   if (word_bits == 64) {
     dc.tw_fwd = static_cast<const ulonglong2*>(c->d_tables);
     dc.tw_inv = dc.tw_fwd + (size_t)n_limbs * n;
@@ -348,6 +349,7 @@ int secn_ctx_destroy(secn_ctx* ctx) {
   DeviceGuard guard(ctx->device);
   cudaFree(ctx->d_tables);
   cudaFree(ctx->d_flag);
+  delete ctx->flag_mutex;
   delete ctx;
   return SECN_OK;
 }
@@ -446,7 +448,7 @@ static int ntt_impl(secn_ctx* ctx, uint32_t bits, void* polys, size_t n_polys, v
   cudaStream_t s = (cudaStream_t)stream;
   const char* name = inverse ? "secn_ntt_inv" : "secn_ntt_fwd";
   if (int st = check_range(ctx, polys, n_polys * ctx->L * ctx->n, 0, s, name)) return st;
-  cudaError_t e = inverse ? secn::launch_ntt_inv(ctx->dc, polys, n_polys * ctx->L, nullptr, s)
+  cudaError_t e = inverse ? secn::launch_ntt_inv(ctx->dc, polys, n_polys * ctx->L, s)
                           : secn::launch_ntt_fwd(ctx->dc, polys, polys, n_polys * ctx->L, nullptr, s);
   return e == cudaSuccess ? SECN_OK : cuda_fail(e, name);
 }
@@ -518,9 +520,11 @@ size_t secn_he_conv2d_workspace(const secn_ctx* ctx, const secn_conv_plan_t* pla
   return (size_t)plan->G * plan->S * 2 * ctx->L * ctx->n * (ctx->word_bits / 8);
 }
 
+// stage -1 = the whole layer; 0 / 1 / 2 = one launch group. `chained`: the caller launched this
+// stage's predecessor stage itself just before (internal.h, "Pre-wait reads"); always true for -1.
 static int he_conv2d_impl(secn_ctx* ctx, uint32_t bits, const secn_conv_plan_t* plan, int stage, const void* ct_in,
                           const uint64_t* x0, const void* w_ntt, const uint64_t* r, void* ct_out, uint64_t* y0,
-                          void* workspace, size_t ws_bytes, void* stream) {
+                          void* workspace, size_t ws_bytes, void* stream, bool chained = false) {
   if (int st = check_ctx(ctx, bits)) return st;
   if (int st = check_plan(ctx, plan)) return st;
   if (stage < -1 || stage > 2) return fail(SECN_EINVAL, "stage %d not in {0,1,2}", stage);
@@ -544,9 +548,11 @@ static int he_conv2d_impl(secn_ctx* ctx, uint32_t bits, const secn_conv_plan_t* 
   cudaError_t e = cudaSuccess;
   if (stage == -1 || stage == 0) e = secn::launch_ntt_fwd(ctx->dc, ct_in, workspace, n_in * 2 * ctx->L, x0, s);  // A6+A1
   // A4 + A2 levels 0..7
-  if (e == cudaSuccess && (stage == -1 || stage == 1)) e = secn::launch_mac(ctx->dc, pd, workspace, w_ntt, ct_out, s);
+  const bool ch = chained || stage == -1;
+  if (e == cudaSuccess && (stage == -1 || stage == 1))
+    e = secn::launch_mac(ctx->dc, pd, workspace, w_ntt, ct_out, s, ch);
   if (e == cudaSuccess && (stage == -1 || stage == 2))
-    e = secn::launch_ntt_inv_tail(ctx->dc, ct_out, n_out * 2 * ctx->L, r, y0, pd, s);  // A2 (levels 8..) + A7 (+A8)
+    e = secn::launch_ntt_inv_tail(ctx->dc, ct_out, n_out * 2 * ctx->L, r, y0, pd, s, ch);  // A2 (levels 8..) + A7 (+A8)
   return e == cudaSuccess ? SECN_OK : cuda_fail(e, "secn_he_conv2d");
 }
 
@@ -686,8 +692,9 @@ static int he_fc_impl(secn_ctx* ctx, uint32_t bits, const secn_fc_plan_t* plan, 
   if (int st = check_range(ctx, r, (size_t)plan->M * N, 1, s, "secn_he_fc r")) return st;
   const secn::PlanDev pd = fc_plan_dev(plan);
   cudaError_t e = secn::launch_ntt_fwd(ctx->dc, ct_in, workspace, (size_t)plan->G * 2 * ctx->L, x0, s);
-  if (e == cudaSuccess) e = secn::launch_mac(ctx->dc, pd, workspace, w_ntt, ct_out, s);
-  if (e == cudaSuccess) e = secn::launch_ntt_inv_tail(ctx->dc, ct_out, (size_t)plan->M * 2 * ctx->L, r, y0, pd, s);
+  if (e == cudaSuccess) e = secn::launch_mac(ctx->dc, pd, workspace, w_ntt, ct_out, s, true);
+  if (e == cudaSuccess)
+    e = secn::launch_ntt_inv_tail(ctx->dc, ct_out, (size_t)plan->M * 2 * ctx->L, r, y0, pd, s, true);
   return e == cudaSuccess ? SECN_OK : cuda_fail(e, "secn_he_fc");
 }
 
@@ -763,11 +770,13 @@ static int he_conv2d_lwe_impl(secn_ctx* ctx, uint32_t bits, const secn_conv_plan
                               xhat_bytes_aligned(ctx, plan), stream))
     return st;
   if (int st = he_conv2d_impl(ctx, bits, plan, 1, ct_in, x0, w_ntt, r, yhat, nullptr, workspace,
-                              xhat_bytes_aligned(ctx, plan), stream))
+                              xhat_bytes_aligned(ctx, plan), stream, /*chained=*/true))
     return st;
   DeviceGuard guard(ctx->device);
+  if (int st = check_range(ctx, r, (size_t)plan->M * plan->S * ctx->n, 1, (cudaStream_t)stream, "secn_he_conv2d_lwe r"))
+    return st;
   cudaError_t e = secn::launch_ntt_inv_tail_lwe(ctx->dc, ms, yhat, (size_t)plan->M * plan->S, r, a_out, b_out, y0,
-                                                plan_dev(plan), (cudaStream_t)stream);
+                                                plan_dev(plan), (cudaStream_t)stream, true);
   return e == cudaSuccess ? SECN_OK : cuda_fail(e, "secn_he_conv2d_lwe");
 }
 
@@ -808,9 +817,12 @@ static int he_fc_lwe_impl(secn_ctx* ctx, uint32_t bits, const secn_fc_plan_t* pl
   const size_t xb = (secn_he_fc_workspace(ctx, plan) + 255) & ~(size_t)255;
   void* yhat = static_cast<unsigned char*>(workspace) + xb;
   const secn::PlanDev pd = fc_plan_dev(plan);
+  if (int st = check_range(ctx, ct_in, (size_t)plan->G * 2 * ctx->L * ctx->n, 0, s, "secn_he_fc_lwe ct_in")) return st;
+  if (int st = check_range(ctx, x0, (size_t)plan->G * ctx->n, 1, s, "secn_he_fc_lwe x0")) return st;
+  if (int st = check_range(ctx, r, (size_t)plan->M * ctx->n, 1, s, "secn_he_fc_lwe r")) return st;
   cudaError_t e = secn::launch_ntt_fwd(ctx->dc, ct_in, workspace, (size_t)plan->G * 2 * ctx->L, x0, s);
-  if (e == cudaSuccess) e = secn::launch_mac(ctx->dc, pd, workspace, w_ntt, yhat, s);
-  if (e == cudaSuccess) e = secn::launch_ntt_inv_tail_lwe(ctx->dc, ms, yhat, plan->M, r, a_out, b_out, y0, pd, s);
+  if (e == cudaSuccess) e = secn::launch_mac(ctx->dc, pd, workspace, w_ntt, yhat, s, true);
+  if (e == cudaSuccess) e = secn::launch_ntt_inv_tail_lwe(ctx->dc, ms, yhat, plan->M, r, a_out, b_out, y0, pd, s, true);
   return e == cudaSuccess ? SECN_OK : cuda_fail(e, "secn_he_fc_lwe");
 }
 

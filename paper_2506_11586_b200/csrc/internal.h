@@ -2,6 +2,7 @@
 #pragma once
 #include <cstddef>
 #include <cstdint>
+#include <mutex>
 
 #include <cuda_runtime.h>
 
@@ -14,6 +15,24 @@ namespace secn {
 // word_bits = 32: residues are uint32 (q < 2^30), twiddles in tw32_fwd/tw32_inv (w' over 2^32).
 // The 64-bit companions of delta / one_p are kept for both (encoding and reductions use 64-bit
 // arithmetic in either case).
+// Tuning knobs and device facts, read once at context creation (the SECN_* environment
+// variables are developer knobs for tools/; every default is the measured best).
+struct Tune {
+  int32_t no_pdl;       // SECN_NO_PDL=1: plain stream order instead of programmatic dependent launch
+  int32_t ntt_np2_min;  // SECN_NTT_NP2_MIN: limb-polys from which N = 4096 32-bit NTTs pair two polys per CTA
+  int32_t tail1;        // SECN_TAIL1=1: one-component INTT tail at N = 4096
+  int32_t mac_kb;       // SECN_MAC_KB: k_mac shared-memory budget per CTA (KiB)
+  int32_t mac_xamort;   // SECN_MAC_XAMORT=0: no X^-tile amortisation rule
+  int32_t mac_nmr;      // SECN_MAC_NMR: forced m-range count
+  int32_t mac_nohint;   // SECN_MAC_NOHINT=1: no L2 hint on the weight stream
+  int32_t mac_pre;      // SECN_MAC_PRE: weight stages issued before the dependency wait (chained calls)
+  int32_t mac_sg;       // SECN_MAC_SG / SECN_MAC_MT: forced k_mac register block
+  int32_t mac_mt;
+  int32_t fused;        // SECN_FUSED: 0 = never use the fused small-layer kernel, 1 = rule, 2 = always
+  int32_t validate;     // SECN_VALIDATE=1: range-check input values (synchronous)
+  int32_t num_sms;      // multiprocessor count of the context's device
+};
+
 struct DevConsts {
   uint64_t q[SECN_MAX_LIMBS];
   uint64_t ninv[SECN_MAX_LIMBS], ninv_p[SECN_MAX_LIMBS];    // N^-1 (Shoup, word-sized companion)
@@ -44,6 +63,7 @@ struct DevConsts {
   uint64_t wlast_mac[SECN_MAX_LIMBS], wlast_mac_p[SECN_MAX_LIMBS];
   uint64_t qneg_inv32[SECN_MAX_LIMBS];
   uint32_t mac_redc;  // 1: 32-bit limbs with every q < 2^27 (G q < 2^32 for G <= 32): k_mac uses REDC
+  Tune tune;          // host-side launch choices (never read by a kernel)
 };
 
 struct PlanDev {  // the subset of secn_conv_plan (kind 0) / secn_fc_plan (kind 1) the kernels use
@@ -65,23 +85,36 @@ struct MsConsts {
 };
 
 // ---- launchers (kernels.cu); all return cudaGetLastError() after the launch(es) ----
+// Reads the tuning knobs (environment) and the device's SM count into *t.
+void read_tune(int device, Tune* t);
+// Opts every shared-memory-hungry kernel of this word size into the full 227 KiB of dynamic shared
+// memory on the CURRENT device (function attributes are per device): called by secn_ctx_create.
+cudaError_t init_device(uint32_t word_bits);
+//
+// Pre-wait reads. Under programmatic dependent launch a kernel starts while its predecessor in the
+// stream finishes; it may read an input before griddepcontrol.wait only if that predecessor is
+// known not to produce it. `chained` = true says the predecessor is the preceding launch of the
+// same library call (which waits for its own predecessor before triggering and never writes the
+// weights or the mask), so k_mac may pre-issue weight loads and the tails may load the mask early;
+// a stage call on its own passes false.
 // Residue buffers are void* of the context's word size.
 cudaError_t launch_ntt_fwd(const DevConsts& c, const void* in, void* out, size_t n_limb_polys, const uint64_t* x0,
                            cudaStream_t s);
-cudaError_t launch_ntt_inv(const DevConsts& c, void* polys, size_t n_limb_polys, const uint64_t* r, cudaStream_t s);
+cudaError_t launch_ntt_inv(const DevConsts& c, void* polys, size_t n_limb_polys, cudaStream_t s);
 // levels 8.. of the inverse NTT (+N^-1, +mask) after launch_mac applied levels 0..7; if
 // y0 != NULL also the server share (A8) for plan pl
 cudaError_t launch_ntt_inv_tail(const DevConsts& c, void* polys, size_t n_limb_polys, const uint64_t* r, uint64_t* y0,
-                                const PlanDev& pl, cudaStream_t s);
+                                const PlanDev& pl, cudaStream_t s, bool chained);
 // NTT-domain MAC (A4) followed by inverse-NTT levels 0..7 of its outputs (lazy GS domain)
-cudaError_t launch_mac(const DevConsts& c, const PlanDev& p, const void* xhat, const void* w, void* y, cudaStream_t s);
+cudaError_t launch_mac(const DevConsts& c, const PlanDev& p, const void* xhat, const void* w, void* y, cudaStream_t s,
+                       bool chained);
 cudaError_t launch_pack_weights(const DevConsts& c, const PlanDev& p, const uint64_t* kernel, void* w, cudaStream_t s);
 // f2: levels 8.. of the inverse NTT + mask + modulus switch to ms.Lk limbs + extraction, N = 4096
 // only: polys [n_ct][2][L][N] (after launch_mac) -> a_out [n_ct][Lk][N], b_out [values][Lk] at the
 // designated coefficients of plan pl (conv or fc), and y0 (if not NULL) the server share.
 cudaError_t launch_ntt_inv_tail_lwe(const DevConsts& c, const MsConsts& ms, const void* polys, size_t n_ct,
                                     const uint64_t* r, void* a_out, void* b_out, uint64_t* y0, const PlanDev& pl,
-                                    cudaStream_t s);
+                                    cudaStream_t s, bool chained);
 // fc weights W [n_o][n_i] -> mirrored polys [M][G][L][N] (coefficient domain, zero-filled first)
 cudaError_t launch_pack_fc_weights(const DevConsts& c, const PlanDev& p, const uint64_t* W, void* w, cudaStream_t s);
 cudaError_t launch_enc_add(const DevConsts& c, void* ct, const uint64_t* v, size_t n, cudaStream_t s);
@@ -100,5 +133,6 @@ struct secn_ctx {
   uint64_t primes[SECN_MAX_LIMBS], psi[SECN_MAX_LIMBS];
   secn::DevConsts dc;
   void* d_tables;
-  uint32_t* d_flag;  // SECN_VALIDATE scratch
+  uint32_t* d_flag;        // SECN_VALIDATE scratch
+  std::mutex* flag_mutex;  // serialises the validated calls that share d_flag
 };

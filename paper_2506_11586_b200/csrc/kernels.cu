@@ -149,13 +149,12 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN, NP>(
   round_gstore<RL, W, NP>(x, dst);
 }
 
-// K3 (+A7 fused): inverse NTT of limb-polys in place; if r != NULL, on the b component of
-// ciphertexts [n][2][L][N]: b_j += enc_j(r[n]) after the transform. NP polys of
-// limb j per CTA as in K1. The last radix-16 round writes global memory directly (its tasks are
-// coalesced); the mask words are loaded at the start so their latency hides behind the transform.
+// K3: inverse NTT of limb-polys in place (the boundary call secn_ntt_inv; the hot path's inverse
+// transform runs in k_mac + the tails, which fuse the mask). NP polys of limb j per CTA as in K1.
+// The last radix-16 round writes global memory directly (its tasks are coalesced).
 template <class A, int LOGN, int NP>
 __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN, NP>())
-    k_ntt_inv(typename A::W* polys, const __grid_constant__ DevConsts c, const uint64_t* __restrict__ r) {
+    k_ntt_inv(typename A::W* polys, const __grid_constant__ DevConsts c) {
   using W = typename A::W;
   constexpr int N = 1 << LOGN, T = N / 16;
   constexpr int LL = GsLast<LOGN>::value;
@@ -172,24 +171,11 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN, NP>(
   // is (a, b) of one ciphertext, so at most one poly is masked). r is an input of the call, never
   // produced by the preceding kernel, so it is loaded and encoded before the dependency wait --
   // this work overlaps the previous kernel's tail -- and only the word-sized results are kept.
-  const EncK ek(c, j);
-  int mpp = -1;
-#pragma unroll
-  for (int pp = 0; pp < NP; ++pp)
-    if (r != nullptr && ((grp * NP + pp) & 1)) mpp = pp;
-  W em[16];
-  if (mpp >= 0) {
-    const uint64_t* rs = r + ((grp * NP + mpp) >> 1) * N;
-#pragma unroll
-    for (int k = 0; k < RL::NT; ++k)
-#pragma unroll
-      for (int i = 0; i < RL::GK; ++i) em[k * RL::GK + i] = enc_mod<A>(__ldg(&rs[RL::addr(k, i)]), ek);
-  }
   // round 0 (levels 0..3, contiguous tasks) straight from global memory
   using R0 = GsRound<LOGN, 0>;
   typename A::Tw tws[15];
   gs_twiddles<A, LOGN, 0>(tws, tw);
-  pdl_wait();  // the polys are produced by the preceding kernel (the MAC)
+  pdl_wait();  // the polys may come from the preceding kernel
   W x[NP][16];
   {
     const W* src[NP];
@@ -212,15 +198,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN, NP>(
 #pragma unroll
     for (int k = 0; k < RL::NT; ++k)
 #pragma unroll
-      for (int i = 0; i < RL::GK; ++i) {
-        const uint32_t e = RL::addr(k, i);
-        W v = A::canon_gs(x[pp][k * RL::GK + i], q);
-        if (pp == mpp) {
-          v += em[k * RL::GK + i];  // < 2q
-          v = v >= q ? v - q : v;
-        }
-        buf[e] = v;
-      }
+      for (int i = 0; i < RL::GK; ++i) buf[RL::addr(k, i)] = A::canon_gs(x[pp][k * RL::GK + i], q);
   }
 }
 
@@ -310,12 +288,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((1 << LOGH) / 16, 1)
 
 // Inverse: CTA h runs GS levels 0..13 on its half (level 13 with twiddle th[1] and no N^-1),
 // leaves the result in shared memory, and after a cluster barrier reads the partner's half
-// through DSMEM for the cross-half level 14 (with N^-1 folded in, as in k_ntt_inv); then the
-// mask on the b component. A second cluster barrier keeps each CTA's shared memory alive until
-// its partner has read it.
+// through DSMEM for the cross-half level 14 (with N^-1 folded in, as in k_ntt_inv). A second
+// cluster barrier keeps each CTA's shared memory alive until its partner has read it.
 template <class A, int LOGH>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((1 << LOGH) / 16, 1)
-    k_ntt_inv_cl(typename A::W* polys, const __grid_constant__ DevConsts c, const uint64_t* __restrict__ r) {
+    k_ntt_inv_cl(typename A::W* polys, const __grid_constant__ DevConsts c) {
   using W = typename A::W;
   constexpr int NH = 1 << LOGH, N = 2 * NH, T = NH / 16;
   constexpr int LL = GsLast<LOGH>::value;
@@ -326,27 +303,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((1 << LOGH) / 16, 1)
   const uint32_t h = cluster_rank();
   const size_t pl = blockIdx.x >> 1;
   const int j = (int)(pl % c.L);
-  const size_t pi = pl / c.L;
   const W q = (W)c.q[j], qb = A::bound(q);
   const typename A::Tw* th = Tab<A>::inv_half(c) + ((size_t)j * 2 + h) * NH;
   const typename A::Tw one = Tab<A>::pair(1, c.one_wp[j]);
   const typename A::Tw w13 = th[1];
   const typename A::Tw ninv = Tab<A>::pair(c.ninv[j], c.ninv_p[j]);
   const typename A::Tw wl = Tab<A>::pair(c.wlast[j], c.wlast_p[j]);
-  const EncK ek(c, j);
-  const bool mask = r != nullptr && (pi & 1);
-  const uint64_t* rs = mask ? r + (pi >> 1) * N + h * NH : nullptr;
-  // 32-bit words: the encoded mask is computed up front (16 registers); 64-bit words would need
-  // 32 more registers than the 64 a 1024-thread CTA has, so they encode at the store instead
-  constexpr bool early = sizeof(W) == 4;
-  W em[early ? 16 : 1];
-  if (early && mask) {
-#pragma unroll
-    for (int k = 0; k < 16; ++k) em[early ? k : 0] = enc_mod<A>(__ldg(&rs[threadIdx.x + k * T]), ek);
-  }
   typename A::Tw tws[15];
   gs_twiddles<A, LOGH, 0>(tws, th);
-  pdl_wait();
+  pdl_wait();  // the polys may come from the preceding kernel
   W* buf = polys + pl * N + h * NH;
   W x[1][16];
   {
@@ -371,16 +336,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((1 << LOGH) / 16, 1)
     const uint32_t e = threadIdx.x + k * T, pe = phys(e);
     const W mine = sm[pe], other = peer[pe];
     const W u = h ? other : mine, v = h ? mine : other;
-    W o = h ? A::mul4(u - v + qb, wl, q) : A::mul4(u + v, ninv, q);
-    o = A::canon_gs(o, q);
-    if (mask) {
-      if constexpr (early)
-        o += em[k];
-      else
-        o += enc_mod<A>(__ldg(&rs[e]), ek);
-      o = o >= q ? o - q : o;
-    }
-    buf[e] = o;
+    const W o = h ? A::mul4(u - v + qb, wl, q) : A::mul4(u + v, ninv, q);
+    buf[e] = A::canon_gs(o, q);
   }
   cluster_arrive();
   cluster_wait();  // the partner is done reading this CTA's shared memory
@@ -419,7 +376,7 @@ __device__ __forceinline__ void write_server_share_ct(const uint64_t* __restrict
 template <class A, int LOGN>
 __global__ void __launch_bounds__((1 << LOGN) / 16, sizeof(typename A::W) == 4 && LOGN == 12 ? 4 : ntt_min_blocks<A, LOGN, 1>())
     k_ntt_inv_tail(typename A::W* polys, const __grid_constant__ DevConsts c, const uint64_t* __restrict__ r,
-                   uint64_t* __restrict__ y0, const __grid_constant__ PlanDev pl, size_t ct0) {
+                   uint64_t* __restrict__ y0, const __grid_constant__ PlanDev pl, size_t ct0, int r_early) {
   using W = typename A::W;
   constexpr int N = 1 << LOGN;
   constexpr int LS = 8;
@@ -437,16 +394,20 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, sizeof(typename A::W) == 4 &
   const EncK ek(c, j);
   const bool mask = r != nullptr && (pi & 1);
   W em[16];
-  if (mask) {
+  // the mask is an input of the call: with r_early (the preceding kernel is this call's MAC, which
+  // never writes it) it is loaded and encoded before the dependency wait, overlapping the MAC's tail
+  const auto load_mask = [&] {
     const uint64_t* rs = r + (pi >> 1) * N;
 #pragma unroll
     for (int k = 0; k < RL::NT; ++k)
 #pragma unroll
       for (int i = 0; i < RL::GK; ++i) em[k * RL::GK + i] = enc_mod<A>(__ldg(&rs[RL::addr(k, i)]), ek);
-  }
+  };
+  if (mask && r_early) load_mask();
   typename A::Tw tws[15];
   gs_twiddles<A, LOGN, LS>(tws, tw);
   pdl_wait();  // the polys are produced by the preceding kernel (the MAC)
+  if (mask && !r_early) load_mask();
   W* buf = polys + (pi * c.L + j) * N;
   W x[1][16];
 #pragma unroll
@@ -483,7 +444,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, sizeof(typename A::W) == 4 &
 // The same tail at N = 4096 with both components of one (ciphertext, limb) per CTA: the pair
 // shares the twiddles and the index arithmetic and every thread keeps 32 independent words in
 // flight (the 16-word version is latency bound on small layers). Mask and A8 on component b.
-template <class A>
+template <class A, bool R_EARLY>
 __global__ void __launch_bounds__(256, 4)
     k_ntt_inv_tail2(typename A::W* polys, const __grid_constant__ DevConsts c, const uint64_t* __restrict__ r,
                     uint64_t* __restrict__ y0, const __grid_constant__ PlanDev pl, size_t ct0) {
@@ -501,16 +462,18 @@ __global__ void __launch_bounds__(256, 4)
   const bool mask = r != nullptr;
   const uint64_t* rs = mask ? r + ct * N : nullptr;
   W em[16];
-  if (mask) {
+  const auto load_mask = [&] {  // before the wait only when chained (see k_ntt_inv_tail)
     uint64_t rv[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) rv[i] = __ldg(&rs[RS::addr(0, i)]);
 #pragma unroll
     for (int i = 0; i < 16; ++i) em[i] = enc_mod<A>(rv[i], ek);
-  }
+  };
+  if (mask && R_EARLY) load_mask();
   typename A::Tw tws[15];
   gs_twiddles<A, LOGN, LS>(tws, tw);
   pdl_wait();  // the polys are produced by the preceding kernel (the MAC)
+  if (mask && !R_EARLY) load_mask();
   W* buf[2] = {polys + ((ct * 2) * c.L + j) * N, polys + ((ct * 2 + 1) * c.L + j) * N};
   W x[2][16];
 #pragma unroll
@@ -1013,7 +976,7 @@ template <class A, int ND>  // ND = L - Lk dropped limbs
 __global__ void __launch_bounds__(LWE_G * SECN_MAX_LIMBS)
     k_ntt_inv_tail_lwe(const typename A::W* __restrict__ polys, const __grid_constant__ DevConsts c,
                        const __grid_constant__ MsConsts ms, const uint64_t* __restrict__ r, typename A::W* a_out,
-                       typename A::W* b_out, uint64_t* y0, const __grid_constant__ PlanDev pl) {
+                       typename A::W* b_out, uint64_t* y0, const __grid_constant__ PlanDev pl, int r_early) {
   using W = typename A::W;
   constexpr int LOGN = 12, N = 1 << LOGN;
   using RS = GsRound<LOGN, 8>;
@@ -1046,11 +1009,15 @@ __global__ void __launch_bounds__(LWE_G * SECN_MAX_LIMBS)
   }
   const EncK ek(c, j);
   W em[16];
-  if (mask && work) {
+  if (mask && work && r_early) {
 #pragma unroll
     for (int i = 0; i < 16; ++i) em[i] = enc_mod<A>(__ldg(&rs[o + 256 * i]), ek);
   }
   pdl_wait();
+  if (mask && work && !r_early) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) em[i] = enc_mod<A>(__ldg(&rs[o + 256 * i]), ek);
+  }
   W x[1][16];
   if (work) {
     const W* buf = polys + (pi * L + j) * N;
@@ -1209,18 +1176,35 @@ __global__ void k_check_range(const W* __restrict__ v, size_t n_words, const __g
 // ------------------------------------------------------------------------------------------
 // launchers
 
-// Launch with programmatic stream serialization (PDL): the kernel may be scheduled while the
-// preceding kernel in the stream finishes; it synchronises with pdl_wait() before reading that
-// kernel's outputs. Captured into CUDA graphs as programmatic edges.
-// tuning knobs read at every launch (SECN_MAC_*, SECN_TAIL1): used by tools/variant_sweep.py
 static int env_int(const char* name, int dflt) {
   const char* v = getenv(name);
   return v && *v ? atoi(v) : dflt;
 }
 
+void read_tune(int device, Tune* t) {
+  int sms = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || sms <= 0) sms = 148;
+  t->num_sms = sms;
+  t->no_pdl = env_int("SECN_NO_PDL", 0);
+  t->ntt_np2_min = env_int("SECN_NTT_NP2_MIN", 2 * sms * 6);
+  t->tail1 = env_int("SECN_TAIL1", 0);
+  t->mac_kb = env_int("SECN_MAC_KB", 110);
+  t->mac_xamort = env_int("SECN_MAC_XAMORT", 1);
+  t->mac_nmr = env_int("SECN_MAC_NMR", 0);
+  t->mac_nohint = env_int("SECN_MAC_NOHINT", 0);
+  t->mac_pre = env_int("SECN_MAC_PRE", 2);
+  t->mac_sg = env_int("SECN_MAC_SG", 0);
+  t->mac_mt = env_int("SECN_MAC_MT", 0);
+  t->fused = env_int("SECN_FUSED", 1);
+  t->validate = env_int("SECN_VALIDATE", 0);
+}
+
+// Launch with programmatic stream serialization (PDL): the kernel may be scheduled while the
+// preceding kernel in the stream finishes; it synchronises with pdl_wait() before reading that
+// kernel's outputs. Captured into CUDA graphs as programmatic edges.
 template <typename... KArgs, typename... Args>
-static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
-                              Args&&... args) {
+static cudaError_t launch_pdl(const DevConsts& c, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t s, Args&&... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -1230,7 +1214,7 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = env_int("SECN_NO_PDL", 0) ? 0 : 1;  // SECN_NO_PDL=1: plain stream order (debugging)
+  cfg.numAttrs = c.tune.no_pdl ? 0 : 1;  // SECN_NO_PDL=1: plain stream order (debugging)
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
@@ -1242,12 +1226,7 @@ static cudaError_t ntt_fwd_np(const DevConsts& c, const void* in, void* out, siz
                               cudaStream_t s) {
   using W = typename A::W;
   constexpr int N = 1 << LOGN;
-  const size_t smem = (size_t)NP * smem_words<LOGN>() * sizeof(W);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_ntt_fwd<A, LOGN, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  const size_t smem = (size_t)NP * smem_words<LOGN>() * sizeof(W);  // opted in by init_device
   // groups per launch: an even number so that x0's ct index stays (poly index) / 2
   const size_t gmax = (0x7fffffffull / c.L) & ~(size_t)1;
   const size_t ngroups = n_polys / NP;
@@ -1257,29 +1236,23 @@ static cudaError_t ntt_fwd_np(const DevConsts& c, const void* in, void* out, siz
     const W* src = static_cast<const W*>(in) + off;
     W* dst = static_cast<W*>(out) + off;
     const uint64_t* xs = x0 ? x0 + g0 * NP / 2 * N : nullptr;
-    cudaError_t e = launch_pdl(k_ntt_fwd<A, LOGN, NP>, dim3((unsigned)(ng * c.L)), dim3(N / 16), smem, s, src, dst, c, xs);
+    cudaError_t e = launch_pdl(c, k_ntt_fwd<A, LOGN, NP>, dim3((unsigned)(ng * c.L)), dim3(N / 16), smem, s, src, dst, c, xs);
     if (e != cudaSuccess) return e;
   }
   return cudaGetLastError();
 }
 
 template <class A, int LOGN, int NP>
-static cudaError_t ntt_inv_np(const DevConsts& c, void* polys, size_t n_polys, const uint64_t* r, cudaStream_t s) {
+static cudaError_t ntt_inv_np(const DevConsts& c, void* polys, size_t n_polys, cudaStream_t s) {
   using W = typename A::W;
   constexpr int N = 1 << LOGN;
-  const size_t smem = (size_t)NP * smem_words<LOGN>() * sizeof(W);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_ntt_inv<A, LOGN, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  const size_t smem = (size_t)NP * smem_words<LOGN>() * sizeof(W);  // opted in by init_device
   const size_t gmax = (0x7fffffffull / c.L) & ~(size_t)1;
   const size_t ngroups = n_polys / NP;
   for (size_t g0 = 0; g0 < ngroups; g0 += gmax) {
     const size_t ng = ngroups - g0 < gmax ? ngroups - g0 : gmax;
     W* buf = static_cast<W*>(polys) + g0 * NP * c.L * N;
-    const uint64_t* rs = r ? r + g0 * NP / 2 * N : nullptr;
-    cudaError_t e = launch_pdl(k_ntt_inv<A, LOGN, NP>, dim3((unsigned)(ng * c.L)), dim3(N / 16), smem, s, buf, c, rs);
+    cudaError_t e = launch_pdl(c, k_ntt_inv<A, LOGN, NP>, dim3((unsigned)(ng * c.L)), dim3(N / 16), smem, s, buf, c);
     if (e != cudaSuccess) return e;
   }
   return cudaGetLastError();
@@ -1290,29 +1263,25 @@ static cudaError_t ntt_fwd_t(const DevConsts& c, const void* in, void* out, size
                              cudaStream_t s) {
   const size_t n_polys = P / c.L;
   if constexpr (sizeof(typename A::W) == 4 && LOGN == 12)
-    if (n_polys % 2 == 0 && P >= (size_t)env_int("SECN_NTT_NP2_MIN", 2 * 148 * 6)) return ntt_fwd_np<A, LOGN, 2>(c, in, out, n_polys, x0, s);
+    if (n_polys % 2 == 0 && P >= (size_t)c.tune.ntt_np2_min) return ntt_fwd_np<A, LOGN, 2>(c, in, out, n_polys, x0, s);
   return ntt_fwd_np<A, LOGN, 1>(c, in, out, n_polys, x0, s);
 }
 
 template <class A, int LOGN>
-static cudaError_t ntt_inv_t(const DevConsts& c, void* polys, size_t P, const uint64_t* r, cudaStream_t s) {
+static cudaError_t ntt_inv_t(const DevConsts& c, void* polys, size_t P, cudaStream_t s) {
   const size_t n_polys = P / c.L;
   if constexpr (sizeof(typename A::W) == 4 && LOGN == 12)
-    if (n_polys % 2 == 0 && P >= (size_t)env_int("SECN_NTT_NP2_MIN", 2 * 148 * 6)) return ntt_inv_np<A, LOGN, 2>(c, polys, n_polys, r, s);
-  return ntt_inv_np<A, LOGN, 1>(c, polys, n_polys, r, s);
+    if (n_polys % 2 == 0 && P >= (size_t)c.tune.ntt_np2_min) return ntt_inv_np<A, LOGN, 2>(c, polys, n_polys, s);
+  return ntt_inv_np<A, LOGN, 1>(c, polys, n_polys, s);
 }
 
 template <class A, int LOGN>
 static cudaError_t ntt_inv_tail_t(const DevConsts& c, void* polys, size_t P, const uint64_t* r, uint64_t* y0,
-                                  const PlanDev& pl, cudaStream_t s) {
+                                  const PlanDev& pl, cudaStream_t s, bool chained) {
   using W = typename A::W;
   constexpr int N = 1 << LOGN;
-  const size_t smem = LOGN > 12 ? smem_words<LOGN>() * sizeof(W) : 0;
-  static bool attr = false;
-  if (!attr && smem > 48 * 1024) {
-    cudaFuncSetAttribute(k_ntt_inv_tail<A, LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  const size_t smem = LOGN > 12 ? smem_words<LOGN>() * sizeof(W) : 0;  // opted in by init_device
+  const int r_early = chained ? 1 : 0;
   const size_t pmax = (0x7fffffffull / c.L / 2) * 2;  // polys per launch: even, so r's index is p/2
   const size_t n_polys = P / c.L;
   for (size_t p0 = 0; p0 < n_polys; p0 += pmax) {
@@ -1321,14 +1290,18 @@ static cudaError_t ntt_inv_tail_t(const DevConsts& c, void* polys, size_t P, con
     const uint64_t* rs = r ? r + p0 / 2 * N : nullptr;
     cudaError_t e;
     if constexpr (LOGN == 12 && sizeof(W) == 4) {
-      if (env_int("SECN_TAIL1", 0))
-        e = launch_pdl(k_ntt_inv_tail<A, LOGN>, dim3((unsigned)(np * c.L)), dim3(N / 16), smem, s, buf, c, rs, y0, pl,
-                       p0 / 2);
-      else  // both components of a (ciphertext, limb) per CTA
-        e = launch_pdl(k_ntt_inv_tail2<A>, dim3((unsigned)(np / 2 * c.L)), dim3(256), 0, s, buf, c, rs, y0, pl, p0 / 2);
+      if (c.tune.tail1)
+        e = launch_pdl(c, k_ntt_inv_tail<A, LOGN>, dim3((unsigned)(np * c.L)), dim3(N / 16), smem, s, buf, c, rs, y0,
+                       pl, p0 / 2, r_early);
+      else if (r_early)  // both components of a (ciphertext, limb) per CTA
+        e = launch_pdl(c, k_ntt_inv_tail2<A, true>, dim3((unsigned)(np / 2 * c.L)), dim3(256), 0, s, buf, c, rs, y0,
+                       pl, p0 / 2);
+      else
+        e = launch_pdl(c, k_ntt_inv_tail2<A, false>, dim3((unsigned)(np / 2 * c.L)), dim3(256), 0, s, buf, c, rs, y0,
+                       pl, p0 / 2);
     } else {
-      e = launch_pdl(k_ntt_inv_tail<A, LOGN>, dim3((unsigned)(np * c.L)), dim3(N / 16), smem, s, buf, c, rs, y0, pl,
-                     p0 / 2);
+      e = launch_pdl(c, k_ntt_inv_tail<A, LOGN>, dim3((unsigned)(np * c.L)), dim3(N / 16), smem, s, buf, c, rs, y0, pl,
+                     p0 / 2, r_early);
     }
     if (e != cudaSuccess) return e;
   }
@@ -1336,19 +1309,19 @@ static cudaError_t ntt_inv_tail_t(const DevConsts& c, void* polys, size_t P, con
 }
 
 cudaError_t launch_ntt_inv_tail(const DevConsts& c, void* polys, size_t P, const uint64_t* r, uint64_t* y0,
-                                const PlanDev& pl, cudaStream_t s) {
+                                const PlanDev& pl, cudaStream_t s, bool chained) {
   if (P == 0) return cudaSuccess;
   if (c.word_bits == 64) {
     switch (c.log_n) {
-      case 12: return ntt_inv_tail_t<Arith64, 12>(c, polys, P, r, y0, pl, s);
-      case 13: return ntt_inv_tail_t<Arith64, 13>(c, polys, P, r, y0, pl, s);
-      case 14: return ntt_inv_tail_t<Arith64, 14>(c, polys, P, r, y0, pl, s);
+      case 12: return ntt_inv_tail_t<Arith64, 12>(c, polys, P, r, y0, pl, s, chained);
+      case 13: return ntt_inv_tail_t<Arith64, 13>(c, polys, P, r, y0, pl, s, chained);
+      case 14: return ntt_inv_tail_t<Arith64, 14>(c, polys, P, r, y0, pl, s, chained);
     }
   } else {
     switch (c.log_n) {
-      case 12: return ntt_inv_tail_t<Arith32, 12>(c, polys, P, r, y0, pl, s);
-      case 13: return ntt_inv_tail_t<Arith32, 13>(c, polys, P, r, y0, pl, s);
-      case 14: return ntt_inv_tail_t<Arith32, 14>(c, polys, P, r, y0, pl, s);
+      case 12: return ntt_inv_tail_t<Arith32, 12>(c, polys, P, r, y0, pl, s, chained);
+      case 13: return ntt_inv_tail_t<Arith32, 13>(c, polys, P, r, y0, pl, s, chained);
+      case 14: return ntt_inv_tail_t<Arith32, 14>(c, polys, P, r, y0, pl, s, chained);
     }
   }
   return cudaErrorInvalidValue;
@@ -1356,29 +1329,21 @@ cudaError_t launch_ntt_inv_tail(const DevConsts& c, void* polys, size_t P, const
 
 // Cluster NTT: one cluster of two CTAs per limb-poly (launches of <= 2^30 polys)
 template <class A, int LOGH>
-static cudaError_t ntt_cl(const DevConsts& c, const void* in, void* out, size_t P, const uint64_t* x0,
-                          const uint64_t* r, bool inverse, cudaStream_t s) {
+static cudaError_t ntt_cl(const DevConsts& c, const void* in, void* out, size_t P, const uint64_t* x0, bool inverse,
+                          cudaStream_t s) {
   using W = typename A::W;
   constexpr int N = 2 << LOGH, T = (1 << LOGH) / 16;
-  const size_t smem = smem_words<LOGH>() * sizeof(W);
-  static bool attr[2] = {false, false};
-  if (!attr[inverse]) {
-    cudaError_t e = inverse ? cudaFuncSetAttribute(k_ntt_inv_cl<A, LOGH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
-                            : cudaFuncSetAttribute(k_ntt_fwd_cl<A, LOGH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr[inverse] = true;
-  }
-  // polys per launch: a multiple of 2L so that the ct index of x0 / r stays (poly / L) / 2
+  const size_t smem = smem_words<LOGH>() * sizeof(W);  // opted in by init_device
+  // polys per launch: a multiple of 2L so that the ct index of x0 stays (poly / L) / 2
   const size_t pmax = ((size_t)1 << 30) / (2 * c.L) * (2 * c.L);
   for (size_t p0 = 0; p0 < P; p0 += pmax) {
     const size_t np = P - p0 < pmax ? P - p0 : pmax;
     const size_t off = p0 * N;
     cudaError_t e;
     if (inverse)
-      e = launch_pdl(k_ntt_inv_cl<A, LOGH>, dim3((unsigned)(2 * np)), dim3(T), smem, s, static_cast<W*>(out) + off, c,
-                     r ? r + p0 / c.L / 2 * N : nullptr);
+      e = launch_pdl(c, k_ntt_inv_cl<A, LOGH>, dim3((unsigned)(2 * np)), dim3(T), smem, s, static_cast<W*>(out) + off, c);
     else
-      e = launch_pdl(k_ntt_fwd_cl<A, LOGH>, dim3((unsigned)(2 * np)), dim3(T), smem, s,
+      e = launch_pdl(c, k_ntt_fwd_cl<A, LOGH>, dim3((unsigned)(2 * np)), dim3(T), smem, s,
                      static_cast<const W*>(in) + off, static_cast<W*>(out) + off, c,
                      x0 ? x0 + p0 / c.L / 2 * N : nullptr);
     if (e != cudaSuccess) return e;
@@ -1390,14 +1355,13 @@ cudaError_t launch_ntt_fwd(const DevConsts& c, const void* in, void* out, size_t
                            cudaStream_t s) {
   if (P == 0) return cudaSuccess;
   if (c.log_n == 15)
-    return c.word_bits == 64 ? ntt_cl<Arith64, 14>(c, in, out, P, x0, nullptr, false, s)
-                             : ntt_cl<Arith32, 14>(c, in, out, P, x0, nullptr, false, s);
-  if (c.log_n == 14 && c.word_bits == 64) return ntt_cl<Arith64, 13>(c, in, out, P, x0, nullptr, false, s);
+    return c.word_bits == 64 ? ntt_cl<Arith64, 14>(c, in, out, P, x0, false, s)
+                             : ntt_cl<Arith32, 14>(c, in, out, P, x0, false, s);
+  if (c.log_n == 14 && c.word_bits == 64) return ntt_cl<Arith64, 13>(c, in, out, P, x0, false, s);
   if (c.word_bits == 64) {
     switch (c.log_n) {
       case 12: return ntt_fwd_t<Arith64, 12>(c, in, out, P, x0, s);
       case 13: return ntt_fwd_t<Arith64, 13>(c, in, out, P, x0, s);
-      case 14: return ntt_fwd_t<Arith64, 14>(c, in, out, P, x0, s);
     }
   } else {
     switch (c.log_n) {
@@ -1409,23 +1373,22 @@ cudaError_t launch_ntt_fwd(const DevConsts& c, const void* in, void* out, size_t
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_ntt_inv(const DevConsts& c, void* polys, size_t P, const uint64_t* r, cudaStream_t s) {
+cudaError_t launch_ntt_inv(const DevConsts& c, void* polys, size_t P, cudaStream_t s) {
   if (P == 0) return cudaSuccess;
   if (c.log_n == 15)
-    return c.word_bits == 64 ? ntt_cl<Arith64, 14>(c, nullptr, polys, P, nullptr, r, true, s)
-                             : ntt_cl<Arith32, 14>(c, nullptr, polys, P, nullptr, r, true, s);
-  if (c.log_n == 14 && c.word_bits == 64) return ntt_cl<Arith64, 13>(c, nullptr, polys, P, nullptr, r, true, s);
+    return c.word_bits == 64 ? ntt_cl<Arith64, 14>(c, nullptr, polys, P, nullptr, true, s)
+                             : ntt_cl<Arith32, 14>(c, nullptr, polys, P, nullptr, true, s);
+  if (c.log_n == 14 && c.word_bits == 64) return ntt_cl<Arith64, 13>(c, nullptr, polys, P, nullptr, true, s);
   if (c.word_bits == 64) {
     switch (c.log_n) {
-      case 12: return ntt_inv_t<Arith64, 12>(c, polys, P, r, s);
-      case 13: return ntt_inv_t<Arith64, 13>(c, polys, P, r, s);
-      case 14: return ntt_inv_t<Arith64, 14>(c, polys, P, r, s);
+      case 12: return ntt_inv_t<Arith64, 12>(c, polys, P, s);
+      case 13: return ntt_inv_t<Arith64, 13>(c, polys, P, s);
     }
   } else {
     switch (c.log_n) {
-      case 12: return ntt_inv_t<Arith32, 12>(c, polys, P, r, s);
-      case 13: return ntt_inv_t<Arith32, 13>(c, polys, P, r, s);
-      case 14: return ntt_inv_t<Arith32, 14>(c, polys, P, r, s);
+      case 12: return ntt_inv_t<Arith32, 12>(c, polys, P, s);
+      case 13: return ntt_inv_t<Arith32, 13>(c, polys, P, s);
+      case 14: return ntt_inv_t<Arith32, 14>(c, polys, P, s);
     }
   }
   return cudaErrorInvalidValue;
@@ -1458,32 +1421,25 @@ static bool encode_tmap(CUtensorMap* m, int wb, int rank, const void* base, cons
 
 template <class W, int SG, int MT>
 static cudaError_t mac_t(const DevConsts& c, const PlanDev& p, const void* xhat, const void* w, void* y,
-                         cudaStream_t s) {
+                         cudaStream_t s, bool chained) {
   const int N = 1 << c.log_n;
   const size_t xtile = (size_t)p.G * 2 * SG * MAC_THREADS * sizeof(W);
   const size_t stage = (size_t)MT * MAC_THREADS * sizeof(W);
   // ring depth: fill ~110 KiB per CTA (two CTAs per SM) after the X^ tile, 4..32 stages
   const size_t chunks = (size_t)MT * 2 * SG * MAC_CHS * sizeof(W) + MAC_THREADS * 2 * sizeof(W);
   const size_t fixed = xtile + chunks;
-  const size_t cta_budget = (size_t)env_int("SECN_MAC_KB", 110) * 1024;
+  const size_t cta_budget = (size_t)c.tune.mac_kb * 1024;
   const size_t budget = cta_budget > fixed + 4 * stage ? cta_budget - fixed : 4 * stage;
   int NS = (int)(budget / stage);
   NS = NS < 4 ? 4 : NS > 32 ? 32 : NS;
   const size_t smem = fixed + NS * stage + (2 * NS + 1) * sizeof(uint64_t);
-  if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  static size_t attr = 0;
-  if (smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_mac<W, SG, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)(smem > 48 * 1024 ? smem : 48 * 1024));
-    if (e != cudaSuccess) return e;
-    attr = smem;
-  }
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;  // opted in by init_device
   const int n_sg = (p.S + SG - 1) / SG;
   // m-range per CTA: the split of M into n_mr ranges (each >= MT channels, a multiple of MT)
   // whose CTA count fills whole waves of two CTAs per SM best; ties go to fewer, longer CTAs
   // (each CTA pays one X^ tile load and one pipeline fill).
   const long ctas_no_m = (long)(N / MAC_THREADS) * n_sg * c.L;
-  const long wave = 148 * 2;
+  const long wave = (long)c.tune.num_sms * 2;
   const int mblocks = (p.M + MT - 1) / MT;
   int best_nmr = 1;
   double best_eff = -1.0;
@@ -1500,11 +1456,11 @@ static cudaError_t mac_t(const DevConsts& c, const PlanDev& p, const void* xhat,
   // hide the INTT-level latency better; measured on the SqueezeNet fire layers)
   if (p.G <= 4 || p.M <= 48)
     best_nmr = mblocks;
-  else if (xtile >= (size_t)MT * p.G * MAC_THREADS * sizeof(W) && env_int("SECN_MAC_XAMORT", 1))
+  else if (xtile >= (size_t)MT * p.G * MAC_THREADS * sizeof(W) && c.tune.mac_xamort)
     // the X^ tile is at least one m-block of weights: a CTA takes >= 2 m-blocks so the tile load
     // is amortised (conv1 of SqueezeNet-1.1: 79 -> 69 us)
     best_nmr = best_nmr < (mblocks + 1) / 2 ? best_nmr : (mblocks + 1) / 2;
-  if (const int nmr_env = env_int("SECN_MAC_NMR", 0)) best_nmr = nmr_env < mblocks ? nmr_env : mblocks;
+  if (const int nmr_env = c.tune.mac_nmr) best_nmr = nmr_env < mblocks ? nmr_env : mblocks;
   const int m_range = ((mblocks + best_nmr - 1) / best_nmr) * MT;
   const int n_mr = (p.M + m_range - 1) / m_range;
   // tensor maps: X^ [G][S*2][L][N] viewed as (N, L, 2S, G); W [M][G][L][N] as (N, G*L, M)
@@ -1521,17 +1477,18 @@ static cudaError_t mac_t(const DevConsts& c, const PlanDev& p, const void* xhat,
   dim3 grid((N / MAC_THREADS) * n_sg, c.L, n_mr);
   W* yp = static_cast<W*>(y);
   DevConsts cc = c;  // debugging knobs ride in unused word_bits bits
-  if (env_int("SECN_MAC_NOHINT", 0)) cc.word_bits |= 0x400;
-  // ring stages issued before the X^ tile (SECN_MAC_PRE: tuning knob)
-  const int n_pre = env_int("SECN_MAC_PRE", 2);
-  cudaError_t e = launch_pdl(k_mac<W, SG, MT>, grid, dim3(MAC_THREADS + 32), smem, s, tmx, tmw, yp, cc, p, m_range,
+  if (c.tune.mac_nohint) cc.word_bits |= 0x400;
+  // ring stages issued before the dependency wait (and the X^ tile): only when the preceding
+  // launch is this call's forward NTT, which never writes the weights (internal.h, "Pre-wait reads")
+  const int n_pre = chained ? c.tune.mac_pre : 0;
+  cudaError_t e = launch_pdl(c, k_mac<W, SG, MT>, grid, dim3(MAC_THREADS + 32), smem, s, tmx, tmw, yp, cc, p, m_range,
                              n_sg, NS, n_pre);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
 cudaError_t launch_mac(const DevConsts& c, const PlanDev& p, const void* xhat, const void* w, void* y,
-                       cudaStream_t s) {
+                       cudaStream_t s, bool chained) {
   if (p.M == 0 || p.S == 0) return cudaSuccess;
   if (p.G > 32) return cudaErrorInvalidValue;
   // s-group: among the SG <= 4 whose X^ tile fits in 64 KiB, the one minimising
@@ -1546,7 +1503,7 @@ cudaError_t launch_mac(const DevConsts& c, const PlanDev& p, const void* xhat, c
     const int nc = (int)((p.S + cand - 1) / cand), nb = (int)((p.S + sg - 1) / sg);
     if (nc * (2 * cand + 1) < nb * (2 * sg + 1)) sg = cand;
   }
-  if (const int sg_env = env_int("SECN_MAC_SG", 0)) sg = sg_env;
+  if (const int sg_env = c.tune.mac_sg) sg = sg_env;
   if (c.word_bits == 32) {
     // output channels per m-block: the larger register block (more weight reuse) unless its
     // staged chunks plus a 4-stage ring would leave one CTA per SM; then the smaller one
@@ -1558,28 +1515,71 @@ cudaError_t launch_mac(const DevConsts& c, const PlanDev& p, const void* xhat, c
       return xtile + chunks + 4 * (size_t)mt * MAC_THREADS * wb <= 110 * 1024;
     };
     bool small = !fits2(mt_big[sg]) || (sg == 1 && xtile > 24 * 1024);
-    if (const int mt_env = env_int("SECN_MAC_MT", 0)) small = mt_env == mt_small[sg];
+    if (const int mt_env = c.tune.mac_mt) small = mt_env == mt_small[sg];
     if (small) {
       switch (sg) {
-        case 1: return mac_t<uint32_t, 1, 8>(c, p, xhat, w, y, s);
-        case 2: return mac_t<uint32_t, 2, 4>(c, p, xhat, w, y, s);
-        case 3: return mac_t<uint32_t, 3, 2>(c, p, xhat, w, y, s);
-        default: return mac_t<uint32_t, 4, 2>(c, p, xhat, w, y, s);
+        case 1: return mac_t<uint32_t, 1, 8>(c, p, xhat, w, y, s, chained);
+        case 2: return mac_t<uint32_t, 2, 4>(c, p, xhat, w, y, s, chained);
+        case 3: return mac_t<uint32_t, 3, 2>(c, p, xhat, w, y, s, chained);
+        default: return mac_t<uint32_t, 4, 2>(c, p, xhat, w, y, s, chained);
       }
     }
     switch (sg) {
-      case 1: return mac_t<uint32_t, 1, 16>(c, p, xhat, w, y, s);
-      case 2: return mac_t<uint32_t, 2, 8>(c, p, xhat, w, y, s);
-      case 3: return mac_t<uint32_t, 3, 5>(c, p, xhat, w, y, s);
-      default: return mac_t<uint32_t, 4, 3>(c, p, xhat, w, y, s);
+      case 1: return mac_t<uint32_t, 1, 16>(c, p, xhat, w, y, s, chained);
+      case 2: return mac_t<uint32_t, 2, 8>(c, p, xhat, w, y, s, chained);
+      case 3: return mac_t<uint32_t, 3, 5>(c, p, xhat, w, y, s, chained);
+      default: return mac_t<uint32_t, 4, 3>(c, p, xhat, w, y, s, chained);
     }
   }
   switch (sg) {
-    case 1: return mac_t<uint64_t, 1, 4>(c, p, xhat, w, y, s);
-    case 2: return mac_t<uint64_t, 2, 2>(c, p, xhat, w, y, s);
-    case 3: return mac_t<uint64_t, 3, 2>(c, p, xhat, w, y, s);
-    default: return mac_t<uint64_t, 4, 1>(c, p, xhat, w, y, s);
+    case 1: return mac_t<uint64_t, 1, 4>(c, p, xhat, w, y, s, chained);
+    case 2: return mac_t<uint64_t, 2, 2>(c, p, xhat, w, y, s, chained);
+    case 3: return mac_t<uint64_t, 3, 2>(c, p, xhat, w, y, s, chained);
+    default: return mac_t<uint64_t, 4, 1>(c, p, xhat, w, y, s, chained);
   }
+}
+
+// Per-device opt-in of the dynamic shared memory every launcher may request (function attributes
+// belong to the device that is current when they are set; secn_ctx_create runs this on its
+// device, so launches never set attributes and need no process-global state).
+template <class K>
+static cudaError_t optin(K* kern, int bytes) {
+  return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+cudaError_t init_device(uint32_t word_bits) {
+  int dev = 0, optin_max = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (e != cudaSuccess) return e;
+  const int b = optin_max;
+  cudaError_t r = cudaSuccess;
+  auto chk = [&](cudaError_t x) {
+    if (r == cudaSuccess) r = x;
+  };
+  if (word_bits == 64) {
+    using A = Arith64;
+    chk(optin(k_ntt_fwd<A, 12, 1>, b)), chk(optin(k_ntt_fwd<A, 13, 1>, b));
+    chk(optin(k_ntt_inv<A, 12, 1>, b)), chk(optin(k_ntt_inv<A, 13, 1>, b));
+    chk(optin(k_ntt_inv_tail<A, 12>, b)), chk(optin(k_ntt_inv_tail<A, 13>, b)), chk(optin(k_ntt_inv_tail<A, 14>, b));
+    chk(optin(k_ntt_fwd_cl<A, 13>, b)), chk(optin(k_ntt_inv_cl<A, 13>, b));
+    chk(optin(k_ntt_fwd_cl<A, 14>, b)), chk(optin(k_ntt_inv_cl<A, 14>, b));
+    chk(optin(k_mac<uint64_t, 1, 4>, b)), chk(optin(k_mac<uint64_t, 2, 2>, b));
+    chk(optin(k_mac<uint64_t, 3, 2>, b)), chk(optin(k_mac<uint64_t, 4, 1>, b));
+  } else {
+    using A = Arith32;
+    chk(optin(k_ntt_fwd<A, 12, 1>, b)), chk(optin(k_ntt_fwd<A, 12, 2>, b));
+    chk(optin(k_ntt_fwd<A, 13, 1>, b)), chk(optin(k_ntt_fwd<A, 14, 1>, b));
+    chk(optin(k_ntt_inv<A, 12, 1>, b)), chk(optin(k_ntt_inv<A, 12, 2>, b));
+    chk(optin(k_ntt_inv<A, 13, 1>, b)), chk(optin(k_ntt_inv<A, 14, 1>, b));
+    chk(optin(k_ntt_inv_tail<A, 12>, b)), chk(optin(k_ntt_inv_tail<A, 13>, b)), chk(optin(k_ntt_inv_tail<A, 14>, b));
+    chk(optin(k_ntt_fwd_cl<A, 14>, b)), chk(optin(k_ntt_inv_cl<A, 14>, b));
+    chk(optin(k_mac<uint32_t, 1, 16>, b)), chk(optin(k_mac<uint32_t, 2, 8>, b));
+    chk(optin(k_mac<uint32_t, 3, 5>, b)), chk(optin(k_mac<uint32_t, 4, 3>, b));
+    chk(optin(k_mac<uint32_t, 1, 8>, b)), chk(optin(k_mac<uint32_t, 2, 4>, b));
+    chk(optin(k_mac<uint32_t, 3, 2>, b)), chk(optin(k_mac<uint32_t, 4, 2>, b));
+  }
+  return r;
 }
 
 cudaError_t launch_pack_weights(const DevConsts& c, const PlanDev& p, const uint64_t* kernel, void* w,
@@ -1615,14 +1615,14 @@ cudaError_t launch_pack_fc_weights(const DevConsts& c, const PlanDev& p, const u
 
 cudaError_t launch_ntt_inv_tail_lwe(const DevConsts& c, const MsConsts& ms, const void* polys, size_t n_ct,
                                     const uint64_t* r, void* a_out, void* b_out, uint64_t* y0, const PlanDev& pl,
-                                    cudaStream_t s) {
+                                    cudaStream_t s, bool chained) {
   if (n_ct == 0) return cudaSuccess;
   if (c.log_n != 12 || 4 * n_ct > 0x7fffffffull) return cudaErrorInvalidValue;
   const dim3 grid((unsigned)(4 * n_ct)), block(LWE_G * c.L);  // (ct, component, half) x limbs
   const int nd = (int)(c.L - ms.Lk);
 #define SECN_LWE(AR, WT, ND)                                                                                   \
-  return launch_pdl(k_ntt_inv_tail_lwe<AR, ND>, grid, block, 0, s, static_cast<const WT*>(polys), c, ms, r,    \
-                    static_cast<WT*>(a_out), static_cast<WT*>(b_out), y0, pl)
+  return launch_pdl(c, k_ntt_inv_tail_lwe<AR, ND>, grid, block, 0, s, static_cast<const WT*>(polys), c, ms, r, \
+                    static_cast<WT*>(a_out), static_cast<WT*>(b_out), y0, pl, chained ? 1 : 0)
   if (c.word_bits == 64) {
     if (nd == 1) SECN_LWE(Arith64, uint64_t, 1);  // 64-bit limbs: one dropped prime (P < 2^62)
   } else {
@@ -1637,7 +1637,8 @@ cudaError_t launch_enc_add(const DevConsts& c, void* ct, const uint64_t* v, size
   if (n == 0) return cudaSuccess;
   const size_t total = n * c.L * (1ull << c.log_n);
   const size_t blocks = (total + 255) / 256;
-  const unsigned b = (unsigned)(blocks < 148 * 32 ? blocks : 148 * 32);
+  const size_t cap = (size_t)c.tune.num_sms * 32;
+  const unsigned b = (unsigned)(blocks < cap ? blocks : cap);
   if (c.word_bits == 64)
     k_enc_add<Arith64><<<b, 256, 0, s>>>(static_cast<uint64_t*>(ct), v, c, n);
   else
@@ -1649,7 +1650,7 @@ cudaError_t launch_extract_share(const DevConsts& c, const PlanDev& p, const uin
                                  cudaStream_t s) {
   const size_t total = (size_t)p.M * p.OH * p.OW;
   if (total) {
-    cudaError_t e = launch_pdl(k_extract_share, dim3((unsigned)((total + 255) / 256)), dim3(256), 0, s, r, y0, c, p);
+    cudaError_t e = launch_pdl(c, k_extract_share, dim3((unsigned)((total + 255) / 256)), dim3(256), 0, s, r, y0, c, p);
     if (e != cudaSuccess) return e;
   }
   return cudaGetLastError();
@@ -1659,7 +1660,8 @@ cudaError_t launch_check_range(const DevConsts& c, const void* v, size_t n_words
                                cudaStream_t s) {
   if (n_words == 0) return cudaSuccess;
   const size_t blocks = (n_words + 255) / 256;
-  const unsigned b = (unsigned)(blocks < 148 * 16 ? blocks : 148 * 16);
+  const size_t cap = (size_t)c.tune.num_sms * 16;
+  const unsigned b = (unsigned)(blocks < cap ? blocks : cap);
   if (kind == 0 && c.word_bits == 32)
     k_check_range<uint32_t><<<b, 256, 0, s>>>(static_cast<const uint32_t*>(v), n_words, c, kind, flag);
   else

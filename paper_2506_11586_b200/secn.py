@@ -168,6 +168,17 @@ def _ptr(t: Optional[torch.Tensor], shape=None, name="tensor", dtype=torch.int64
     return ctypes.c_void_p(t.data_ptr())
 
 
+def _ws(t: torch.Tensor, need: int, device) -> tuple:
+    """(pointer, bytes) of a caller's workspace tensor after checking it is a contiguous CUDA tensor
+    on the context's device with at least `need` bytes (the C ABI cannot see its size)."""
+    if not t.is_cuda or not t.is_contiguous() or t.device != device:
+        raise TypeError(f"workspace: expected a contiguous CUDA tensor on {device}, got {t.device}")
+    nb = t.numel() * t.element_size()
+    if nb < need:
+        raise ValueError(f"workspace: {nb} bytes < the {need} the call needs")
+    return ctypes.c_void_p(t.data_ptr()), nb
+
+
 class Context:
     """A libsecn context on one CUDA device (secn_ctx_create, or secn32_ctx_create with
     word_bits=32). Residue tensors are int64 (64-bit words) or int32 (32-bit words); plaintext
@@ -272,14 +283,14 @@ class Context:
         L, n = self.L, self.n
         if out is None:
             out = self.empty(plan.M, 2, L, n)
+        need = int(lib().secn_he_fc_workspace(self._h, ctypes.byref(plan)))
         if workspace is None:
-            ws = int(lib().secn_he_fc_workspace(self._h, ctypes.byref(plan)))
-            workspace = torch.empty((ws + 7) // 8, dtype=torch.int64, device=self.device)
+            workspace = torch.empty((need + 7) // 8, dtype=torch.int64, device=self.device)
+        wp, wn = _ws(workspace, need, self.device)
         _check(self._f("he_fc")(self._h, ctypes.byref(plan), self._rp(ct_in, (plan.G, 2, L, n), "ct_in"),
                                 _ptr(x0, (plan.G, n), "x0"), self._rp(w_ntt, (plan.M, plan.G, L, n), "w_ntt"),
                                 _ptr(r, (plan.M, n), "r"), self._rp(out, (plan.M, 2, L, n), "ct_out"),
-                                _ptr(y0, (plan.n_o,), "y0"), ctypes.c_void_p(workspace.data_ptr()),
-                                workspace.numel() * workspace.element_size(), self._stream(stream)))
+                                _ptr(y0, (plan.n_o,), "y0"), wp, wn, self._stream(stream)))
         return out
 
     # ---- extracted outputs (f2): modulus switch to `keep` limbs + designated coefficients ----
@@ -291,15 +302,16 @@ class Context:
         (written into `out` = (a', b') when given)."""
         L, n = self.L, self.n
         a, b = out if out is not None else (self.empty(plan.M * plan.S, keep, n), self.empty(plan.M, plan.OH, plan.OW, keep))
+        need = int(lib().secn_he_conv2d_lwe_workspace(self._h, ctypes.byref(plan)))
         if workspace is None:
-            ws = int(lib().secn_he_conv2d_lwe_workspace(self._h, ctypes.byref(plan)))
-            workspace = torch.empty((ws + 7) // 8, dtype=torch.int64, device=self.device)
+            workspace = torch.empty((need + 7) // 8, dtype=torch.int64, device=self.device)
+        wp, wn = _ws(workspace, need, self.device)
         _check(self._f("he_conv2d_lwe")(
             self._h, ctypes.byref(plan), self._rp(ct_in, (plan.G * plan.S, 2, L, n), "ct_in"),
             _ptr(x0, (plan.G * plan.S, n), "x0"), self._rp(w_ntt, (plan.M, plan.G, L, n), "w_ntt"),
-            _ptr(r, (plan.M * plan.S, n), "r"), keep, self._rp(a), self._rp(b),
-            _ptr(y0, (plan.M, plan.OH, plan.OW), "y0"), ctypes.c_void_p(workspace.data_ptr()),
-            workspace.numel() * workspace.element_size(), self._stream(stream)))
+            _ptr(r, (plan.M * plan.S, n), "r"), keep, self._rp(a, (plan.M * plan.S, keep, n), "a_out"),
+            self._rp(b, (plan.M, plan.OH, plan.OW, keep), "b_out"),
+            _ptr(y0, (plan.M, plan.OH, plan.OW), "y0"), wp, wn, self._stream(stream)))
         return a, b
 
     def he_fc_lwe(self, plan: FcPlan, ct_in: torch.Tensor, w_ntt: torch.Tensor, keep: int,
@@ -309,14 +321,15 @@ class Context:
         L, n = self.L, self.n
         a = self.empty(plan.M, keep, n)
         b = self.empty(plan.n_o, keep)
+        need = int(lib().secn_he_fc_lwe_workspace(self._h, ctypes.byref(plan)))
         if workspace is None:
-            ws = int(lib().secn_he_fc_lwe_workspace(self._h, ctypes.byref(plan)))
-            workspace = torch.empty((ws + 7) // 8, dtype=torch.int64, device=self.device)
+            workspace = torch.empty((need + 7) // 8, dtype=torch.int64, device=self.device)
+        wp, wn = _ws(workspace, need, self.device)
         _check(self._f("he_fc_lwe")(
             self._h, ctypes.byref(plan), self._rp(ct_in, (plan.G, 2, L, n), "ct_in"), _ptr(x0, (plan.G, n), "x0"),
-            self._rp(w_ntt, (plan.M, plan.G, L, n), "w_ntt"), _ptr(r, (plan.M, n), "r"), keep, self._rp(a),
-            self._rp(b), _ptr(y0, (plan.n_o,), "y0"), ctypes.c_void_p(workspace.data_ptr()),
-            workspace.numel() * workspace.element_size(), self._stream(stream)))
+            self._rp(w_ntt, (plan.M, plan.G, L, n), "w_ntt"), _ptr(r, (plan.M, n), "r"), keep,
+            self._rp(a, (plan.M, keep, n), "a_out"), self._rp(b, (plan.n_o, keep), "b_out"),
+            _ptr(y0, (plan.n_o,), "y0"), wp, wn, self._stream(stream)))
         return a, b
 
     def share_add(self, ct: torch.Tensor, x0: torch.Tensor, stream=None) -> torch.Tensor:
@@ -346,12 +359,11 @@ class Context:
             out = self.empty(n_out, 2, L, n)
         ws_bytes = self.workspace_bytes(plan)
         if workspace is None:
-            workspace = torch.empty(ws_bytes // 8, dtype=torch.int64, device=self.device)
+            workspace = torch.empty((ws_bytes + 7) // 8, dtype=torch.int64, device=self.device)
         args = [self._h, ctypes.byref(plan), self._rp(ct_in, (n_in, 2, L, n), "ct_in"),
                 _ptr(x0, (n_in, n), "x0"), self._rp(w_ntt, (plan.M, plan.G, L, n), "w_ntt"),
                 _ptr(r, (n_out, n), "r"), self._rp(out, (n_out, 2, L, n), "ct_out")]
-        tail = [ctypes.c_void_p(workspace.data_ptr()), workspace.numel() * workspace.element_size(),
-                self._stream(stream)]
+        tail = [*_ws(workspace, ws_bytes, self.device), self._stream(stream)]
         if y0 is None:
             _check(self._f("he_conv2d")(*args, *tail))
         else:
@@ -371,15 +383,15 @@ class Context:
         n_in, n_out = plan.G * plan.S, plan.M * plan.S
         if out is None:
             out = self.empty(n_out, 2, L, n)
+        need = self.online_workspace_bytes(plan)
         if workspace is None:
-            workspace = torch.empty((self.online_workspace_bytes(plan) + 7) // 8, dtype=torch.int64,
-                                    device=self.device)
+            workspace = torch.empty((need + 7) // 8, dtype=torch.int64, device=self.device)
+        wp, wn = _ws(workspace, need, self.device)
         _check(self._f("he_conv2d_online")(
             self._h, ctypes.byref(plan), self._rp(ct_in, (n_in, 2, L, n), "ct_in"), _ptr(x0, (n_in, n), "x0"),
             _ptr(kernel, (plan.M, plan.C, plan.kh, plan.kw), "kernel"), _ptr(r, (n_out, n), "r"),
             self._rp(out, (n_out, 2, L, n), "ct_out"),
-            _ptr(y0, (plan.M, plan.OH, plan.OW), "y0") if y0 is not None else None,
-            ctypes.c_void_p(workspace.data_ptr()), workspace.numel() * workspace.element_size(),
+            _ptr(y0, (plan.M, plan.OH, plan.OW), "y0") if y0 is not None else None, wp, wn,
             self._stream(stream)))
         return out
 
@@ -393,8 +405,8 @@ class Context:
                                           self._rp(ct_in, (n_in, 2, L, n), "ct_in"), _ptr(x0, (n_in, n), "x0"),
                                           self._rp(w_ntt, (plan.M, plan.G, L, n), "w_ntt"), _ptr(r, (n_out, n), "r"),
                                           self._rp(out, (n_out, 2, L, n), "ct_out"),
-                                          ctypes.c_void_p(workspace.data_ptr()),
-                                          workspace.numel() * workspace.element_size(), self._stream(stream)))
+                                          *_ws(workspace, self.workspace_bytes(plan), self.device),
+                                          self._stream(stream)))
         return out
 
     def he_conv2d_stage_ex(self, stage: int, plan: Plan, ct_in: torch.Tensor, w_ntt: torch.Tensor,
@@ -408,8 +420,8 @@ class Context:
                                              self._rp(w_ntt, (plan.M, plan.G, L, n), "w_ntt"), _ptr(r, (n_out, n), "r"),
                                              self._rp(out, (n_out, 2, L, n), "ct_out"),
                                              _ptr(y0, (plan.M, plan.OH, plan.OW), "y0") if y0 is not None else None,
-                                             ctypes.c_void_p(workspace.data_ptr()),
-                                             workspace.numel() * workspace.element_size(), self._stream(stream)))
+                                             *_ws(workspace, self.workspace_bytes(plan), self.device),
+                                             self._stream(stream)))
         return out
 
     def extract_share(self, plan: Plan, r: torch.Tensor, out: Optional[torch.Tensor] = None,

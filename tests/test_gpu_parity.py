@@ -336,6 +336,33 @@ def test_he_conv2d_tiny_exact(env, use_x0, use_r):
     assert (got == ref).all()
 
 
+@pytest.mark.parametrize("rep", range(3))
+def test_stage_calls_read_inputs_written_just_before(env, rep):
+    """A stage call whose weights (stage 1) or mask (stage 2) were written by the kernel right
+    before it on the stream: secn_preprocess_weights then stage 1, a device copy of r then
+    stage 2. Stage calls never read an input before the dependency wait (k_mac used to
+    pre-issue weight loads and the tails to load r before griddepcontrol.wait)."""
+    ctx, P, D = env
+    lay = layers.ConvLayer("pw", 64, 13, 13, 256, 3, 1, 1)  # many m-blocks: weights stream long after launch
+    opl = oplan(P, ctx, lay)
+    ct, x0, K, r = _layer_inputs(P, lay, 40 + rep, opl)
+    plan = ctx.plan(lay.C, lay.H, lay.W, lay.M, lay.k, stride=lay.stride, pad=lay.pad)
+    cti, x0t = D.R(ct), TP(x0)
+    out = ctx.empty(plan.M * plan.S, 2, ctx.L, ctx.n)
+    ws = torch.empty(ctx.workspace_bytes(plan) // 8, dtype=torch.int64, device=DEV)
+    w = ctx.empty(plan.M, plan.G, ctx.L, ctx.n)
+    w.fill_(-1)
+    rt = torch.full((plan.M * plan.S, ctx.n), -1, dtype=torch.int64, device=DEV)
+    rsrc = TP(r)
+    torch.cuda.synchronize()
+    ctx.he_conv2d_stage(0, plan, cti, w, x0t, rt, out, ws)
+    ctx.preprocess_weights(plan, TP(K), out=w)  # its last kernel writes w ...
+    ctx.he_conv2d_stage(1, plan, cti, w, x0t, rt, out, ws)  # ... and the MAC reads w
+    rt.copy_(rsrc)  # a plain kernel writes r ...
+    ctx.he_conv2d_stage(2, plan, cti, w, x0t, rt, out, ws)  # ... and the tail reads r
+    assert (D.U(out) == he.server_conv(ct, x0, K, r, opl, P)).all()
+
+
 def test_he_conv2d_stages_equal_fused_call(env):
     ctx, P, D = env
     lay = layers.ConvLayer("st", 20, 30, 30, 6, 3, 1, 1)
@@ -402,10 +429,13 @@ def test_mac_register_blocks_exact(env, sg, small, monkeypatch):
     opl = packing.plan_conv(lay.C, lay.H, lay.W, lay.M, 1, 1, 1, 0, P.n, ctx.coef_words64, Hw=11, Ww=28)
     ct, x0, K, r = _layer_inputs(P, lay, 21, opl)
     monkeypatch.setenv("SECN_MAC_SG", str(sg))
+    monkeypatch.setenv("SECN_FUSED", "0")  # the three-kernel path's k_mac
     if ctx.word_bits == 32:
         monkeypatch.setenv("SECN_MAC_MT", str(_MT32[sg][1 if small else 0]))
-    w = ctx.preprocess_weights(plan, TP(K))
-    got = D.U(ctx.he_conv2d(plan, D.R(ct), w, x0=TP(x0), r=TP(r)))
+    kctx = secn_mod().Context(0, word_bits=ctx.word_bits)  # knobs are read at context creation
+    w = kctx.preprocess_weights(plan, TP(K))
+    got = D.U(kctx.he_conv2d(plan, D.R(ct), w, x0=TP(x0), r=TP(r)))
+    kctx.close()
     assert (got == he.server_conv(ct, x0, K, r, opl, P)).all()
 
 
