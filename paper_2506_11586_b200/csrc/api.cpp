@@ -549,6 +549,10 @@ static int he_conv2d_impl(secn_ctx* ctx, uint32_t bits, const secn_conv_plan_t* 
   if (stage == -1 || stage == 0) e = secn::launch_ntt_fwd(ctx->dc, ct_in, workspace, n_in * 2 * ctx->L, x0, s);  // A6+A1
   // A4 + A2 levels 0..7
   const bool ch = chained || stage == -1;
+  if (e == cudaSuccess && stage == -1 && secn::fused_applies(ctx->dc, pd)) {  // MAC + INTT + mask in one kernel
+    e = secn::launch_layer_fused(ctx->dc, pd, workspace, w_ntt, ct_out, r, y0, s, true);
+    return e == cudaSuccess ? SECN_OK : cuda_fail(e, "secn_he_conv2d");
+  }
   if (e == cudaSuccess && (stage == -1 || stage == 1))
     e = secn::launch_mac(ctx->dc, pd, workspace, w_ntt, ct_out, s, ch);
   if (e == cudaSuccess && (stage == -1 || stage == 2))

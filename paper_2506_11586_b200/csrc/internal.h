@@ -28,7 +28,10 @@ struct Tune {
   int32_t mac_pre;      // SECN_MAC_PRE: weight stages issued before the dependency wait (chained calls)
   int32_t mac_sg;       // SECN_MAC_SG / SECN_MAC_MT: forced k_mac register block
   int32_t mac_mt;
-  int32_t fused;        // SECN_FUSED: 0 = never use the fused small-layer kernel, 1 = rule, 2 = always
+  int32_t fused;        // SECN_FUSED=2: the fused small-layer kernel for every layer it supports (default 0: off)
+  int32_t fused_sg;     // SECN_FUSED_SG / SECN_FUSED_MT: its register block (s-group, m-block)
+  int32_t fused_mt;
+  int32_t fused_kb;     // SECN_FUSED_KB: its shared-memory budget per CTA (KiB)
   int32_t validate;     // SECN_VALIDATE=1: range-check input values (synchronous)
   int32_t num_sms;      // multiprocessor count of the context's device
 };
@@ -105,6 +108,11 @@ cudaError_t launch_ntt_inv(const DevConsts& c, void* polys, size_t n_limb_polys,
 // y0 != NULL also the server share (A8) for plan pl
 cudaError_t launch_ntt_inv_tail(const DevConsts& c, void* polys, size_t n_limb_polys, const uint64_t* r, uint64_t* y0,
                                 const PlanDev& pl, cudaStream_t s, bool chained);
+// The whole layer after the forward NTT in one kernel (32-bit limbs, N = 4096): A4 MAC, the full
+// inverse NTT, A7 mask, A8 share. fused_applies says whether the layer takes this path.
+bool fused_applies(const DevConsts& c, const PlanDev& p);
+cudaError_t launch_layer_fused(const DevConsts& c, const PlanDev& p, const void* xhat, const void* w, void* y,
+                               const uint64_t* r, uint64_t* y0, cudaStream_t s, bool chained);
 // NTT-domain MAC (A4) followed by inverse-NTT levels 0..7 of its outputs (lazy GS domain)
 cudaError_t launch_mac(const DevConsts& c, const PlanDev& p, const void* xhat, const void* w, void* y, cudaStream_t s,
                        bool chained);

@@ -925,6 +925,208 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
 }
 
 // ------------------------------------------------------------------------------------------
+// The whole layer after the forward NTT in ONE kernel, for the small layers (32-bit limbs,
+// N = 4096): A4 MAC, all 12 inverse-NTT levels, N^-1, A7 mask and A8 server share. A CTA owns
+// whole output polys -- limb j of the MT x SG output ciphertexts (m, s) of an m-block and an
+// s-group, both components (NP = 2 MT SG polys, 17 KiB each in shared memory) -- so Y^ never
+// leaves the SM and there is no tail kernel. Phase A streams, per e-tile of 256 coefficients and
+// chunk of GC input groups, the X^ rows (G x 2SG, L2-resident) and the weight rows (MT x G, HBM,
+// read once) through a TMA ring (one elected producer thread, full/empty mbarriers), accumulates
+// the [MT x 2SG] block of lazy 64-bit sums per coefficient and reduces it (REDC) into the output
+// polys. Phase B runs the three radix-16 Gentleman-Sande rounds on the polys in shared memory
+// (every poly of the CTA has limb j, so one set of twiddles per task serves all of them); the
+// last round's tasks (coefficients tid + 256 i) are coalesced, so it adds the mask and stores
+// straight to global memory. The MAC's multiply-add work and weight bytes equal k_mac's; what
+// goes away is the Y^ round trip through HBM and the tail launch.
+constexpr int FUSED_THREADS = 256;  // consumers; +32 producer threads
+
+template <int SG, int MT>
+__global__ void __launch_bounds__(FUSED_THREADS + 32, 2)
+    k_layer_fused(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmw,
+                  uint32_t* __restrict__ y, const uint64_t* __restrict__ r, uint64_t* __restrict__ y0,
+                  const __grid_constant__ DevConsts c, const __grid_constant__ PlanDev pl, int n_sg, int NS, int GC,
+                  int n_pre) {
+  using AR = Arith32;
+  using W = uint32_t;
+  using Tw = uint2;
+  constexpr int LOGN = 12, N = 1 << LOGN, A2 = 2 * SG, NP = MT * A2, SW = smem_words<LOGN>();
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  const int L = (int)c.L, G = (int)pl.G, S = (int)pl.S;
+  const int j = blockIdx.y;
+  const int sgi = blockIdx.x % n_sg, mb = (blockIdx.x / n_sg) * MT;
+  const int s0 = sgi * SG, ns = min(SG, S - s0), rows = min(MT, (int)pl.M - mb);
+  const int n_gc = (G + GC - 1) / GC, total = (N / FUSED_THREADS) * n_gc;
+  const int stage_words = GC * (A2 + MT) * FUSED_THREADS;
+  // shared memory: [NP][SW] output polys (padded layout), [NS][stage] ring, 2 NS mbarriers
+  W* obuf = reinterpret_cast<W*>(smraw);
+  W* ring = obuf + NP * SW;
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)NS * stage_words);
+  uint64_t* empty = full + NS;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int st = 0; st < NS; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], FUSED_THREADS / 32);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (tid >= FUSED_THREADS) {  // ---- producer: stage k = (e-tile k / n_gc, group chunk k % n_gc) ----
+    if (tid == FUSED_THREADS) {
+      prefetch_tmap(&tmx);
+      prefetch_tmap(&tmw);
+      const uint64_t evict_first = policy_evict_first();  // weights are read once per query
+      const uint32_t bytes = (uint32_t)stage_words * sizeof(W);
+      const auto load_w = [&](int k, int st) {
+        W* dst = ring + (size_t)st * stage_words + GC * A2 * FUSED_THREADS;
+        tma_load_4d_hint(dst, &tmw, (k / n_gc) * FUSED_THREADS, j, (k % n_gc) * GC, mb, &full[st], evict_first);
+      };
+      const auto load_x = [&](int k, int st) {
+        tma_load_4d(ring + (size_t)st * stage_words, &tmx, (k / n_gc) * FUSED_THREADS, j, 2 * s0, (k % n_gc) * GC,
+                    &full[st]);
+      };
+      // the weights are never produced by the preceding kernel of a chained call: the first n_pre
+      // stages' weight rows go out before the dependency wait; X^ (the forward NTT's output) after
+      const int npre = min(n_pre, min(NS, total));
+      for (int k = 0; k < npre; ++k) {
+        mbar_arrive_expect_tx(&full[k], bytes);
+        load_w(k, k);
+      }
+      pdl_wait();
+      for (int k = 0; k < npre; ++k) load_x(k, k);
+      for (int k = npre; k < total; ++k) {
+        const int st = k % NS;
+        if (k >= NS) mbar_wait(&empty[st], ((k / NS) & 1) ^ 1);
+        mbar_arrive_expect_tx(&full[st], bytes);
+        load_w(k, st);
+        load_x(k, st);
+      }
+    }
+    return;
+  }
+
+  // ---- phase A: MAC, one coefficient of the e-tile per consumer thread ----
+  const uint32_t q = (uint32_t)c.q[j], qb = AR::bound(q);
+  const uint32_t qn = (uint32_t)c.qneg_inv32[j];
+  const uint32_t r32 = (uint32_t)c.r32[j], r32p = (uint32_t)c.r32_p[j], onep32 = (uint32_t)(c.one_p[j] >> 32);
+  int k = 0;
+  for (int et = 0; et < N / FUSED_THREADS; ++et) {
+    uint64_t acc[MT][A2];
+#pragma unroll
+    for (int rr = 0; rr < MT; ++rr)
+#pragma unroll
+      for (int a = 0; a < A2; ++a) acc[rr][a] = 0;
+    for (int gc = 0; gc < n_gc; ++gc, ++k) {
+      const int st = k % NS;
+      mbar_wait_sleep(&full[st], (k / NS) & 1);
+      const W* xs = ring + (size_t)st * stage_words + tid;
+      const W* wsg = xs + GC * A2 * FUSED_THREADS;
+      const int gn = min(GC, G - gc * GC);
+      for (int gg = 0; gg < gn; ++gg) {
+        uint32_t xv[A2];
+#pragma unroll
+        for (int a = 0; a < A2; ++a) xv[a] = xs[(gg * A2 + a) * FUSED_THREADS];
+#pragma unroll
+        for (int rr = 0; rr < MT; ++rr) {
+          const uint32_t wv = wsg[(rr * GC + gg) * FUSED_THREADS];
+#pragma unroll
+          for (int a = 0; a < A2; ++a) acc[rr][a] += (uint64_t)xv[a] * wv;  // G <= 32 terms < 2^54
+        }
+      }
+      consumer_release(&empty[st]);
+    }
+    const uint32_t pe = phys(et * FUSED_THREADS + tid);
+#pragma unroll
+    for (int rr = 0; rr < MT; ++rr)
+#pragma unroll
+      for (int a = 0; a < A2; ++a)
+        obuf[(rr * A2 + a) * SW + pe] = c.mac_redc ? redc32(acc[rr][a], q, qn)  // [0, 2q); 2^-32 undone by ninv_mac
+                                                   : reduce64(acc[rr][a], q, r32, r32p, onep32);
+  }
+
+  // ---- phase B: inverse NTT of the NP polys in shared memory ----
+  const Tw* tw = Tab<AR>::inv(c) + (size_t)j * N;
+  const Tw ninv = Tab<AR>::pair(c.ninv_mac[j], c.ninv_mac_p[j]), wl = Tab<AR>::pair(c.wlast_mac[j], c.wlast_mac_p[j]);
+  Tw tws[15];
+  const auto round_smem = [&](auto rtag) {
+    constexpr int L0 = decltype(rtag)::value;
+    using R = GsRound<LOGN, L0>;
+    gs_twiddles<AR, LOGN, L0>(tws, tw);
+    consumer_sync();  // the previous phase / round has written every poly
+#pragma unroll 1
+    for (int p = 0; p < NP; p += 2) {
+      W x[2][16];
+#pragma unroll
+      for (int pp = 0; pp < 2; ++pp)
+#pragma unroll
+        for (int i = 0; i < 16; ++i) x[pp][i] = obuf[(p + pp) * SW + R::pbase(0) + R::poff(i)];
+      gs_compute<AR, LOGN, L0, 2>(x, tws, q, qb, ninv, wl);
+#pragma unroll
+      for (int pp = 0; pp < 2; ++pp)
+#pragma unroll
+        for (int i = 0; i < 16; ++i) obuf[(p + pp) * SW + R::pbase(0) + R::poff(i)] = x[pp][i];
+    }
+  };
+  round_smem(std::integral_constant<int, 0>());
+  round_smem(std::integral_constant<int, 4>());
+  // last round (levels 8..11 with N^-1): tasks tid + 256 i are coalesced -> global memory, with the
+  // mask on the b component
+  using RL = GsRound<LOGN, 8>;
+  gs_twiddles<AR, LOGN, 8>(tws, tw);
+  consumer_sync();
+  const EncK ek(c, j);
+  const uint64_t tm = (1ull << c.t_bits) - 1;
+#pragma unroll 1
+  for (int p = 0; p < NP; p += 2) {  // p even: (a, b) of one output ciphertext
+    const int rr = p / A2, a = p % A2, sl = a >> 1;
+    const bool live = rr < rows && sl < ns;
+    const size_t ct = (size_t)(mb + rr) * S + s0 + sl;
+    W em[16];  // enc_j of the mask words (encoded before the polys are loaded: fewer live registers)
+    if (live && r != nullptr) {
+      uint64_t rv[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) rv[i] = __ldg(&r[ct * N + RL::addr(0, i)]);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) em[i] = enc_mod<AR>(rv[i], ek);
+    }
+    W x[2][16];
+#pragma unroll
+    for (int pp = 0; pp < 2; ++pp)
+#pragma unroll
+      for (int i = 0; i < 16; ++i) x[pp][i] = obuf[(p + pp) * SW + RL::pbase(0) + RL::poff(i)];
+    gs_compute<AR, LOGN, 8, 2>(x, tws, q, qb, ninv, wl);
+    if (live) {
+      W* ya = y + ((ct * 2) * L + j) * N;
+      W* yb = y + ((ct * 2 + 1) * L + j) * N;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        ya[RL::addr(0, i)] = AR::canon_gs(x[0][i], q);
+        W v = AR::canon_gs(x[1][i], q);
+        if (r != nullptr) {
+          v += em[i];
+          v = v >= q ? v - q : v;
+        }
+        yb[RL::addr(0, i)] = v;
+      }
+      // A8: the server's share y0 = -r mod t at the designated coefficients (limb 0's CTA)
+      if (y0 != nullptr && r != nullptr && j == 0) {
+        const uint32_t sidx = (uint32_t)(ct % S), bh = sidx / pl.nbw, bw = sidx % pl.nbw;
+        const uint32_t dh = pl.Hw - pl.kh + 1, dw = pl.Ww - pl.kw + 1;
+        for (uint32_t d = tid; d < dh * dw; d += FUSED_THREADS) {
+          const uint32_t i = d / dw, jj = d - i * dw;
+          const uint32_t py = bh * dh + i, px = bw * dw + jj;
+          const uint32_t oy = py / pl.sh, ox = px / pl.sh;
+          if (oy * pl.sh != py || ox * pl.sh != px || oy >= pl.OH || ox >= pl.OW) continue;
+          y0[((size_t)(mb + rr) * pl.OH + oy) * pl.OW + ox] = (tm + 1 - r[ct * N + pl.O + i * pl.Ww + jj]) & tm;
+        }
+      }
+    }
+  }
+  pdl_trigger();
+}
+
+// ------------------------------------------------------------------------------------------
 // f2 (reading R16): the INTT tail with the output switched to Lk limbs and
 // extracted. One CTA per (output ct, component), 256 threads, 16 coefficients o + 256 i per
 // thread (N = 4096). Modulus switching needs all L residues of a coefficient: the dropped limbs
@@ -1195,7 +1397,10 @@ void read_tune(int device, Tune* t) {
   t->mac_pre = env_int("SECN_MAC_PRE", 2);
   t->mac_sg = env_int("SECN_MAC_SG", 0);
   t->mac_mt = env_int("SECN_MAC_MT", 0);
-  t->fused = env_int("SECN_FUSED", 1);
+  t->fused = env_int("SECN_FUSED", 0);
+  t->fused_sg = env_int("SECN_FUSED_SG", 0);
+  t->fused_mt = env_int("SECN_FUSED_MT", 0);
+  t->fused_kb = env_int("SECN_FUSED_KB", 112);
   t->validate = env_int("SECN_VALIDATE", 0);
 }
 
@@ -1578,8 +1783,71 @@ cudaError_t init_device(uint32_t word_bits) {
     chk(optin(k_mac<uint32_t, 3, 5>, b)), chk(optin(k_mac<uint32_t, 4, 3>, b));
     chk(optin(k_mac<uint32_t, 1, 8>, b)), chk(optin(k_mac<uint32_t, 2, 4>, b));
     chk(optin(k_mac<uint32_t, 3, 2>, b)), chk(optin(k_mac<uint32_t, 4, 2>, b));
+    chk(optin(k_layer_fused<1, 1>, b)), chk(optin(k_layer_fused<1, 2>, b)), chk(optin(k_layer_fused<1, 4>, b));
+    chk(optin(k_layer_fused<2, 1>, b)), chk(optin(k_layer_fused<2, 2>, b));
   }
   return r;
+}
+
+// ---- the fused small-layer kernel (k_layer_fused) ----
+template <int SG, int MT>
+static size_t fused_smem(const DevConsts& c, int G, int* NS_out, int* GC_out) {
+  constexpr int A2 = 2 * SG, NP = MT * A2;
+  const size_t obuf = (size_t)NP * smem_words<12>() * sizeof(uint32_t);
+  const size_t per_g = (size_t)(A2 + MT) * FUSED_THREADS * sizeof(uint32_t);
+  const size_t budget = (size_t)c.tune.fused_kb * 1024;
+  const size_t ring = budget > obuf + 2 * per_g ? budget - obuf : 2 * per_g;
+  int GC = (int)(ring / (2 * per_g));
+  GC = GC < 1 ? 1 : GC > G ? G : GC;
+  int NS = (int)(ring / (GC * per_g));
+  NS = NS < 2 ? 2 : NS > 4 ? 4 : NS;
+  *NS_out = NS, *GC_out = GC;
+  return obuf + (size_t)NS * GC * per_g + 2 * NS * sizeof(uint64_t);
+}
+
+template <int SG, int MT>
+static cudaError_t fused_t(const DevConsts& c, const PlanDev& p, const void* xhat, const void* w, void* y,
+                           const uint64_t* r, uint64_t* y0, cudaStream_t s, bool chained) {
+  constexpr int N = 4096;
+  int NS = 0, GC = 0;
+  const size_t smem = fused_smem<SG, MT>(c, (int)p.G, &NS, &GC);
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;  // opted in by init_device
+  const int n_sg = (p.S + SG - 1) / SG, n_mb = (p.M + MT - 1) / MT;
+  // X^ [G][S*2][L][N] as (N, L, 2S, G); W [M][G][L][N] as (N, L, G, M)
+  const cuuint64_t wb = 4;
+  CUtensorMap tmx, tmw;
+  const cuuint64_t xd[4] = {(cuuint64_t)N, c.L, 2ull * p.S, p.G};
+  const cuuint64_t xs_[3] = {N * wb, (cuuint64_t)c.L * N * wb, 2ull * p.S * c.L * N * wb};
+  const cuuint32_t xb[4] = {FUSED_THREADS, 1, 2 * SG, (cuuint32_t)GC};
+  const cuuint64_t wd[4] = {(cuuint64_t)N, c.L, p.G, p.M};
+  const cuuint64_t ws_[3] = {N * wb, (cuuint64_t)c.L * N * wb, (cuuint64_t)p.G * c.L * N * wb};
+  const cuuint32_t wbx[4] = {FUSED_THREADS, 1, (cuuint32_t)GC, MT};
+  if (!encode_tmap(&tmx, 4, 4, xhat, xd, xs_, xb) || !encode_tmap(&tmw, 4, 4, w, wd, ws_, wbx))
+    return cudaErrorInvalidValue;
+  const int n_pre = chained ? c.tune.mac_pre : 0;
+  cudaError_t e = launch_pdl(c, k_layer_fused<SG, MT>, dim3((unsigned)(n_mb * n_sg), c.L), dim3(FUSED_THREADS + 32),
+                             smem, s, tmx, tmw, static_cast<uint32_t*>(y), r, y0, c, p, n_sg, NS, GC, n_pre);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+bool fused_applies(const DevConsts& c, const PlanDev& p) {
+  if (c.word_bits != 32 || c.log_n != 12 || p.G > 32 || p.M == 0 || p.S == 0 || c.tune.fused == 0) return false;
+  // SECN_FUSED=2: every layer it supports. Off by default: on every SqueezeNet-1.1 layer it measured
+  // slower than the three-kernel chain (profiles/r02_fused_ab.txt)
+  return c.tune.fused == 2;
+}
+
+cudaError_t launch_layer_fused(const DevConsts& c, const PlanDev& p, const void* xhat, const void* w, void* y,
+                               const uint64_t* r, uint64_t* y0, cudaStream_t s, bool chained) {
+  int sg = c.tune.fused_sg > 0 ? c.tune.fused_sg : 1;
+  int mt = c.tune.fused_mt > 0 ? c.tune.fused_mt : 2;
+  if (sg == 1 && mt == 1) return fused_t<1, 1>(c, p, xhat, w, y, r, y0, s, chained);
+  if (sg == 1 && mt == 2) return fused_t<1, 2>(c, p, xhat, w, y, r, y0, s, chained);
+  if (sg == 1 && mt == 4) return fused_t<1, 4>(c, p, xhat, w, y, r, y0, s, chained);
+  if (sg == 2 && mt == 1) return fused_t<2, 1>(c, p, xhat, w, y, r, y0, s, chained);
+  if (sg == 2 && mt == 2) return fused_t<2, 2>(c, p, xhat, w, y, r, y0, s, chained);
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_pack_weights(const DevConsts& c, const PlanDev& p, const uint64_t* kernel, void* w,

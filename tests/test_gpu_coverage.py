@@ -197,3 +197,34 @@ def test_sanitizer_conv1_layer(tool, wb):
     m-blocks per CTA) and a fire squeeze layer."""
     for name in ("conv1", "fire3.sq"):
         _sanitize(tool, _SAN_LAYER.format(root=str(ROOT), wb=wb, name=name), timeout=1500)
+
+
+@pytest.mark.parametrize("sgmt", ["1,1", "1,2", "1,4", "2,1", "2,2"])
+@pytest.mark.parametrize("name", ["fire9.e3", "conv1", "fire3.sq", "fire6.sq"])
+def test_fused_layer_kernel_exact(env, sgmt, name, monkeypatch):
+    """The fused small-layer kernel (k_layer_fused: MAC + all 12 inverse-NTT levels + mask + share
+    in one launch; SECN_FUSED=2, off by default) in every register block, exact against the
+    oracle on S > 1 (conv1: polyphase, ragged s-groups), large-G and many-m-block layers."""
+    ctx, P, D = env
+    if ctx.word_bits != 32:
+        pytest.skip("32-bit limbs only")
+    sg, mt = sgmt.split(",")
+    monkeypatch.setenv("SECN_FUSED", "2")
+    monkeypatch.setenv("SECN_FUSED_SG", sg)
+    monkeypatch.setenv("SECN_FUSED_MT", mt)
+    fctx = secn_mod().Context(0, word_bits=32)
+    lay = next(l for l in layers.squeezenet11() if l.name == name)
+    opl = oplan(P, fctx, lay)
+    ct, x0, K, r = _layer_inputs(P, lay, 77, opl)
+    plan = fctx.plan(lay.C, lay.H, lay.W, lay.M, lay.k, stride=lay.stride, pad=lay.pad)
+    w = fctx.preprocess_weights(plan, TP(K))
+    y0 = torch.full((plan.M, plan.OH, plan.OW), -1, dtype=torch.int64, device=DEV)
+    got = D.U(fctx.he_conv2d(plan, D.R(ct), w, x0=TP(x0), r=TP(r), y0=y0))
+    fctx.close()
+    n_out = opl.M * opl.S
+    pick = np.unique(np.array([0, 1, n_out // 2, n_out - 1]))
+    sel = np.zeros(n_out, np.uint8)
+    sel[pick] = 1
+    ref = he.server_conv(ct, x0, K, r, opl, P, sel=sel)
+    assert (got[pick] == ref[pick]).all()
+    assert (UP(y0) == packing.extract((P.t - r) % P.t, opl)).all()
