@@ -202,6 +202,36 @@ int secn_he_conv2d_online(secn_ctx* ctx, const secn_conv_plan_t* plan, const uin
 int secn_extract_share(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* r, uint64_t* y0, void* stream);
 
 /* ------------------------------------------------------------------------------------------
+ * Device-drawn mask (§7, "applies a random mask for security"; reading R17).
+ * The calls above take the server's mask r from the caller. These draw it on the device from the
+ * counter-based generator Philox4x32-10 (Salmon et al., SC'11), so the server's own randomness
+ * never crosses PCIe:
+ *   (w0, w1, w2, w3) = Philox4x32-10(counter = (e >> 1, ct0 + c, stream, 0),
+ *                                    key = (seed mod 2^32, seed >> 32))
+ *   r[c][e] = (w1 2^32 + w0) mod 2^t_bits for even e,  (w3 2^32 + w2) mod 2^t_bits for odd e,
+ * for output ciphertext c of the call (the layer's index m*S + s; ct0 lets a rank slice of the
+ * output channels draw exactly the rows of the whole layer it owns) and coefficient e. A fresh
+ * (seed, stream) per query and layer is the caller's responsibility.
+ * ------------------------------------------------------------------------------------------ */
+typedef struct {
+  uint64_t seed;   /* generator key                                                           */
+  uint32_t stream; /* e.g. (query, layer) id: distinct streams give independent masks          */
+  uint32_t ct0;    /* index of the call's first output ciphertext in the layer (0 = whole layer) */
+} secn_mask_gen_t;
+
+/* r [n_ct][N] (uint64 < 2^t_bits, device, 16-byte aligned) for output ciphertexts ct0 .. ct0+n_ct-1.
+ * SECN_EINVAL for a NULL generator or buffer. */
+int secn_mask_draw(secn_ctx* ctx, const secn_mask_gen_t* gen, size_t n_ct, uint64_t* r, void* stream);
+
+/* secn_he_conv2d_ex with r drawn by `gen` (the draw runs between the forward NTT and the MAC and
+ * lands in the workspace, >= secn_he_conv2d_gen_workspace bytes). y0 (may be NULL) receives the
+ * server's share -r mod t at the designated coefficients, as with a caller-supplied r. */
+size_t secn_he_conv2d_gen_workspace(const secn_ctx* ctx, const secn_conv_plan_t* plan);
+int secn_he_conv2d_gen(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* ct_in, const uint64_t* x0,
+                       const uint64_t* w_ntt, const secn_mask_gen_t* gen, uint64_t* ct_out, uint64_t* y0,
+                       void* workspace, size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------------------------------
  * HE fully-connected layer / matrix-vector product (§6
  * "fully-connected/matrix multiplication layers"; SPEC.md:612-619 fc_secure). The server's work
  * is the convolution's -- share add + NTT of the input cts, NTT-domain MAC over input blocks,
@@ -255,6 +285,12 @@ size_t secn_he_conv2d_lwe_workspace(const secn_ctx* ctx, const secn_conv_plan_t*
 int secn_he_conv2d_lwe(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* ct_in, const uint64_t* x0,
                        const uint64_t* w_ntt, const uint64_t* r, uint32_t keep_limbs, uint64_t* a_out,
                        uint64_t* b_out, uint64_t* y0, void* workspace, size_t ws_bytes, void* stream);
+/* secn_he_conv2d_lwe with the mask drawn by `gen` (reading R17; workspace >=
+ * secn_he_conv2d_lwe_gen_workspace bytes). */
+size_t secn_he_conv2d_lwe_gen_workspace(const secn_ctx* ctx, const secn_conv_plan_t* plan);
+int secn_he_conv2d_lwe_gen(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* ct_in, const uint64_t* x0,
+                           const uint64_t* w_ntt, const secn_mask_gen_t* gen, uint32_t keep_limbs, uint64_t* a_out,
+                           uint64_t* b_out, uint64_t* y0, void* workspace, size_t ws_bytes, void* stream);
 size_t secn_he_fc_lwe_workspace(const secn_ctx* ctx, const secn_fc_plan_t* plan);
 int secn_he_fc_lwe(secn_ctx* ctx, const secn_fc_plan_t* plan, const uint64_t* ct_in, const uint64_t* x0,
                    const uint64_t* w_ntt, const uint64_t* r, uint32_t keep_limbs, uint64_t* a_out, uint64_t* b_out,
@@ -298,6 +334,12 @@ int secn32_he_conv2d_lwe(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint
 int secn32_he_fc_lwe(secn_ctx* ctx, const secn_fc_plan_t* plan, const uint32_t* ct_in, const uint64_t* x0,
                      const uint32_t* w_ntt, const uint64_t* r, uint32_t keep_limbs, uint32_t* a_out, uint32_t* b_out,
                      uint64_t* y0, void* workspace, size_t ws_bytes, void* stream);
+int secn32_he_conv2d_gen(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint32_t* ct_in, const uint64_t* x0,
+                         const uint32_t* w_ntt, const secn_mask_gen_t* gen, uint32_t* ct_out, uint64_t* y0,
+                         void* workspace, size_t ws_bytes, void* stream);
+int secn32_he_conv2d_lwe_gen(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint32_t* ct_in, const uint64_t* x0,
+                             const uint32_t* w_ntt, const secn_mask_gen_t* gen, uint32_t keep_limbs, uint32_t* a_out,
+                             uint32_t* b_out, uint64_t* y0, void* workspace, size_t ws_bytes, void* stream);
 int secn32_he_conv2d_stage(secn_ctx* ctx, const secn_conv_plan_t* plan, int stage, const uint32_t* ct_in,
                            const uint64_t* x0, const uint32_t* w_ntt, const uint64_t* r, uint32_t* ct_out,
                            void* workspace, size_t ws_bytes, void* stream);

@@ -522,9 +522,12 @@ size_t secn_he_conv2d_workspace(const secn_ctx* ctx, const secn_conv_plan_t* pla
 
 // stage -1 = the whole layer; 0 / 1 / 2 = one launch group. `chained`: the caller launched this
 // stage's predecessor stage itself just before (internal.h, "Pre-wait reads"); always true for -1.
+// gen != NULL (stage -1 or 0 only): the mask is drawn on the device (reading R17) into gen_r, which
+// is then passed as r; the draw kernel runs between the forward NTT and the MAC.
 static int he_conv2d_impl(secn_ctx* ctx, uint32_t bits, const secn_conv_plan_t* plan, int stage, const void* ct_in,
                           const uint64_t* x0, const void* w_ntt, const uint64_t* r, void* ct_out, uint64_t* y0,
-                          void* workspace, size_t ws_bytes, void* stream, bool chained = false) {
+                          void* workspace, size_t ws_bytes, void* stream, bool chained = false,
+                          const secn::MaskGen* gen = nullptr, uint64_t* gen_r = nullptr) {
   if (int st = check_ctx(ctx, bits)) return st;
   if (int st = check_plan(ctx, plan)) return st;
   if (stage < -1 || stage > 2) return fail(SECN_EINVAL, "stage %d not in {0,1,2}", stage);
@@ -547,6 +550,7 @@ static int he_conv2d_impl(secn_ctx* ctx, uint32_t bits, const secn_conv_plan_t* 
   const secn::PlanDev pd = plan_dev(plan);
   cudaError_t e = cudaSuccess;
   if (stage == -1 || stage == 0) e = secn::launch_ntt_fwd(ctx->dc, ct_in, workspace, n_in * 2 * ctx->L, x0, s);  // A6+A1
+  if (e == cudaSuccess && gen != nullptr) e = secn::launch_mask_draw(ctx->dc, *gen, n_out, gen_r, s);  // R17
   // A4 + A2 levels 0..7
   const bool ch = chained || stage == -1;
   if (e == cudaSuccess && stage == -1 && secn::fused_applies(ctx->dc, pd)) {  // MAC + INTT + mask in one kernel
@@ -583,6 +587,53 @@ int secn32_he_conv2d_ex(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint3
 // after X^; then the same three launches as secn_he_conv2d_ex.
 static size_t xhat_bytes_aligned(const secn_ctx* ctx, const secn_conv_plan_t* plan) {
   return (secn_he_conv2d_workspace(ctx, plan) + 255) & ~(size_t)255;
+}
+
+static int check_gen(const secn_mask_gen_t* g, secn::MaskGen* out) {
+  if (!g) return fail(SECN_EINVAL, "NULL mask generator");
+  out->seed = g->seed, out->stream = g->stream, out->ct0 = g->ct0;
+  return SECN_OK;
+}
+
+size_t secn_he_conv2d_gen_workspace(const secn_ctx* ctx, const secn_conv_plan_t* plan) {
+  if (!ctx || !plan) return 0;
+  return xhat_bytes_aligned(ctx, plan) + (size_t)plan->M * plan->S * ctx->n * sizeof(uint64_t);
+}
+
+static int he_conv2d_gen_impl(secn_ctx* ctx, uint32_t bits, const secn_conv_plan_t* plan, const void* ct_in,
+                              const uint64_t* x0, const void* w_ntt, const secn_mask_gen_t* gen, void* ct_out,
+                              uint64_t* y0, void* workspace, size_t ws_bytes, void* stream) {
+  if (int st = check_ctx(ctx, bits)) return st;
+  if (int st = check_plan(ctx, plan)) return st;
+  secn::MaskGen g;
+  if (int st = check_gen(gen, &g)) return st;
+  if (!workspace) return fail(SECN_EINVAL, "NULL buffer");
+  if (ws_bytes < secn_he_conv2d_gen_workspace(ctx, plan)) return fail(SECN_EINVAL, "workspace too small");
+  uint64_t* r = reinterpret_cast<uint64_t*>(static_cast<unsigned char*>(workspace) + xhat_bytes_aligned(ctx, plan));
+  return he_conv2d_impl(ctx, bits, plan, -1, ct_in, x0, w_ntt, r, ct_out, y0, workspace, xhat_bytes_aligned(ctx, plan),
+                        stream, true, &g, r);
+}
+
+int secn_he_conv2d_gen(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* ct_in, const uint64_t* x0,
+                       const uint64_t* w_ntt, const secn_mask_gen_t* gen, uint64_t* ct_out, uint64_t* y0,
+                       void* workspace, size_t ws_bytes, void* stream) {
+  return he_conv2d_gen_impl(ctx, 64, plan, ct_in, x0, w_ntt, gen, ct_out, y0, workspace, ws_bytes, stream);
+}
+int secn32_he_conv2d_gen(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint32_t* ct_in, const uint64_t* x0,
+                         const uint32_t* w_ntt, const secn_mask_gen_t* gen, uint32_t* ct_out, uint64_t* y0,
+                         void* workspace, size_t ws_bytes, void* stream) {
+  return he_conv2d_gen_impl(ctx, 32, plan, ct_in, x0, w_ntt, gen, ct_out, y0, workspace, ws_bytes, stream);
+}
+
+int secn_mask_draw(secn_ctx* ctx, const secn_mask_gen_t* gen, size_t n_ct, uint64_t* r, void* stream) {
+  if (int st = check_ctx(ctx)) return st;
+  secn::MaskGen g;
+  if (int st = check_gen(gen, &g)) return st;
+  if (n_ct && !r) return fail(SECN_EINVAL, "NULL buffer");
+  if ((uintptr_t)r & 15) return fail(SECN_EINVAL, "r must be 16-byte aligned");
+  DeviceGuard guard(ctx->device);
+  cudaError_t e = secn::launch_mask_draw(ctx->dc, g, n_ct, r, (cudaStream_t)stream);
+  return e == cudaSuccess ? SECN_OK : cuda_fail(e, "secn_mask_draw");
 }
 
 size_t secn_he_conv2d_online_workspace(const secn_ctx* ctx, const secn_conv_plan_t* plan) {
@@ -760,7 +811,8 @@ size_t secn_he_conv2d_lwe_workspace(const secn_ctx* ctx, const secn_conv_plan_t*
 
 static int he_conv2d_lwe_impl(secn_ctx* ctx, uint32_t bits, const secn_conv_plan_t* plan, const void* ct_in,
                               const uint64_t* x0, const void* w_ntt, const uint64_t* r, uint32_t keep, void* a_out,
-                              void* b_out, uint64_t* y0, void* workspace, size_t ws_bytes, void* stream) {
+                              void* b_out, uint64_t* y0, void* workspace, size_t ws_bytes, void* stream,
+                              const secn::MaskGen* gen = nullptr) {
   if (int st = check_ctx(ctx, bits)) return st;
   if (int st = check_plan(ctx, plan)) return st;
   secn::MsConsts ms;
@@ -771,7 +823,7 @@ static int he_conv2d_lwe_impl(secn_ctx* ctx, uint32_t bits, const secn_conv_plan
   // X^ then Y^ (levels 0..7 applied) in the workspace; stages 0-1 of the full path
   void* yhat = static_cast<unsigned char*>(workspace) + xhat_bytes_aligned(ctx, plan);
   if (int st = he_conv2d_impl(ctx, bits, plan, 0, ct_in, x0, w_ntt, r, yhat, nullptr, workspace,
-                              xhat_bytes_aligned(ctx, plan), stream))
+                              xhat_bytes_aligned(ctx, plan), stream, false, gen, const_cast<uint64_t*>(r)))
     return st;
   if (int st = he_conv2d_impl(ctx, bits, plan, 1, ct_in, x0, w_ntt, r, yhat, nullptr, workspace,
                               xhat_bytes_aligned(ctx, plan), stream, /*chained=*/true))
@@ -782,6 +834,40 @@ static int he_conv2d_lwe_impl(secn_ctx* ctx, uint32_t bits, const secn_conv_plan
   cudaError_t e = secn::launch_ntt_inv_tail_lwe(ctx->dc, ms, yhat, (size_t)plan->M * plan->S, r, a_out, b_out, y0,
                                                 plan_dev(plan), (cudaStream_t)stream, true);
   return e == cudaSuccess ? SECN_OK : cuda_fail(e, "secn_he_conv2d_lwe");
+}
+
+size_t secn_he_conv2d_lwe_gen_workspace(const secn_ctx* ctx, const secn_conv_plan_t* plan) {
+  if (!ctx || !plan) return 0;
+  return ((secn_he_conv2d_lwe_workspace(ctx, plan) + 255) & ~(size_t)255) +
+         (size_t)plan->M * plan->S * ctx->n * sizeof(uint64_t);
+}
+
+static int he_conv2d_lwe_gen_impl(secn_ctx* ctx, uint32_t bits, const secn_conv_plan_t* plan, const void* ct_in,
+                                  const uint64_t* x0, const void* w_ntt, const secn_mask_gen_t* gen, uint32_t keep,
+                                  void* a_out, void* b_out, uint64_t* y0, void* workspace, size_t ws_bytes,
+                                  void* stream) {
+  if (int st = check_ctx(ctx, bits)) return st;
+  if (int st = check_plan(ctx, plan)) return st;
+  secn::MaskGen g;
+  if (int st = check_gen(gen, &g)) return st;
+  if (!workspace) return fail(SECN_EINVAL, "NULL buffer");
+  if (ws_bytes < secn_he_conv2d_lwe_gen_workspace(ctx, plan)) return fail(SECN_EINVAL, "workspace too small");
+  const size_t lw = (secn_he_conv2d_lwe_workspace(ctx, plan) + 255) & ~(size_t)255;
+  uint64_t* r = reinterpret_cast<uint64_t*>(static_cast<unsigned char*>(workspace) + lw);
+  return he_conv2d_lwe_impl(ctx, bits, plan, ct_in, x0, w_ntt, r, keep, a_out, b_out, y0, workspace, lw, stream, &g);
+}
+
+int secn_he_conv2d_lwe_gen(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* ct_in, const uint64_t* x0,
+                           const uint64_t* w_ntt, const secn_mask_gen_t* gen, uint32_t keep_limbs, uint64_t* a_out,
+                           uint64_t* b_out, uint64_t* y0, void* workspace, size_t ws_bytes, void* stream) {
+  return he_conv2d_lwe_gen_impl(ctx, 64, plan, ct_in, x0, w_ntt, gen, keep_limbs, a_out, b_out, y0, workspace,
+                                ws_bytes, stream);
+}
+int secn32_he_conv2d_lwe_gen(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint32_t* ct_in, const uint64_t* x0,
+                             const uint32_t* w_ntt, const secn_mask_gen_t* gen, uint32_t keep_limbs, uint32_t* a_out,
+                             uint32_t* b_out, uint64_t* y0, void* workspace, size_t ws_bytes, void* stream) {
+  return he_conv2d_lwe_gen_impl(ctx, 32, plan, ct_in, x0, w_ntt, gen, keep_limbs, a_out, b_out, y0, workspace,
+                                ws_bytes, stream);
 }
 
 int secn_he_conv2d_lwe(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* ct_in, const uint64_t* x0,

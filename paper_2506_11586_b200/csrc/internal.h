@@ -77,6 +77,13 @@ struct PlanDev {  // the subset of secn_conv_plan (kind 0) / secn_fc_plan (kind 
   uint32_t nib, nob, no; // fc: inputs per ct, output rows per ct, n_o (C holds n_i)
 };
 
+// Reading R17: the device-drawn mask (secn_mask_gen_t): Philox4x32-10 keyed by seed, counter
+// (coefficient pair, ct0 + output ct, stream, 0).
+struct MaskGen {
+  uint64_t seed;
+  uint32_t stream, ct0;
+};
+
 // Modulus switch Q -> Q' = q_0 .. q_{Lk-1} (reading R16): P = the product of the dropped primes
 // q_Lk .. q_{L-1}; for a dropped limb j: pq[j] = P / q_j and inv[j] = (P / q_j)^-1 mod q_j; for a
 // kept limb i: pinv[i] = P^-1 mod q_i (companions word-sized). Built per call on the host.
@@ -125,6 +132,8 @@ cudaError_t launch_ntt_inv_tail_lwe(const DevConsts& c, const MsConsts& ms, cons
                                     cudaStream_t s, bool chained);
 // fc weights W [n_o][n_i] -> mirrored polys [M][G][L][N] (coefficient domain, zero-filled first)
 cudaError_t launch_pack_fc_weights(const DevConsts& c, const PlanDev& p, const uint64_t* W, void* w, cudaStream_t s);
+// r [n_ct][N] from the generator (reading R17); launched with PDL, safe to chain (see k_mask_draw)
+cudaError_t launch_mask_draw(const DevConsts& c, const MaskGen& g, size_t n_ct, uint64_t* r, cudaStream_t s);
 cudaError_t launch_enc_add(const DevConsts& c, void* ct, const uint64_t* v, size_t n, cudaStream_t s);
 cudaError_t launch_extract_share(const DevConsts& c, const PlanDev& p, const uint64_t* r, uint64_t* y0,
                                  cudaStream_t s);

@@ -105,6 +105,9 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN, NP>(
   typename A::Tw tws[15];
   ct_twiddles<A, LOGN, 0>(tws, tw);
   pdl_wait();  // inputs may come from the preceding kernel
+  // dependents (the mask draw, the MAC) may launch now: none reads this kernel's output before its
+  // own dependency wait, and the MAC's pre-wait weight loads are never produced here
+  pdl_trigger();
   W x[NP][16];
 #pragma unroll
   for (int pp = 0; pp < NP; ++pp) {
@@ -138,7 +141,6 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN, NP>(
   __syncthreads();
   round_load<RL, W, NP, LOGN>(x, sm);
   ct_compute<A, LOGN, SL, NP>(x, tws, q, qb);
-  pdl_trigger();
 #pragma unroll
   for (int pp = 0; pp < NP; ++pp)
 #pragma unroll
@@ -1345,6 +1347,36 @@ __global__ void k_enc_add(typename A::W* __restrict__ ct, const uint64_t* __rest
   }
 }
 
+// Reading R17: the server's mask drawn on the device from Philox4x32-10 (Salmon et al., SC'11),
+// counter (e >> 1, ct0 + ct, stream, 0), key (seed lo, seed hi); one draw gives the mask words of
+// the coefficient pair (e, e + 1): r[e] = (w1 2^32 + w0) mod 2^t, r[e + 1] = (w3 2^32 + w2) mod 2^t.
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int rnd = 0; rnd < 10; ++rnd) {
+    if (rnd) k0 += 0x9E3779B9u, k1 += 0xBB67AE85u;
+    const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+    const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+    c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+  }
+  return c;
+}
+
+// r [n_ct][N]: one thread per coefficient pair, 16-byte stores. It reads nothing another kernel
+// writes, so it lets its dependents launch at once; it waits for its predecessor only at the end,
+// so that its own completion implies the predecessor's (the chain fwd NTT -> draw -> MAC relies on
+// this: the MAC's dependency wait then covers the forward NTT's output too).
+__global__ void k_mask_draw(uint64_t* __restrict__ r, MaskGen g, size_t n_pairs, uint32_t half_n, uint32_t t_bits) {
+  pdl_trigger();
+  const uint64_t tm = (1ull << t_bits) - 1;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n_pairs; i += (size_t)gridDim.x * blockDim.x) {
+    const uint32_t ct = (uint32_t)(i / half_n), pe = (uint32_t)(i % half_n);
+    const uint4 w = philox4x32_10(make_uint4(pe, g.ct0 + ct, g.stream, 0u), (uint32_t)g.seed, (uint32_t)(g.seed >> 32));
+    reinterpret_cast<ulonglong2*>(r)[i] =
+        make_ulonglong2((((uint64_t)w.y << 32) | w.x) & tm, (((uint64_t)w.w << 32) | w.z) & tm);
+  }
+  pdl_wait();
+}
+
 // Designated server share y0[m][oy][ox] = (t - r[m*S+s][O + i*Ww + j]) mod t.
 __global__ void k_extract_share(const uint64_t* __restrict__ r, uint64_t* __restrict__ y0,
                                 const __grid_constant__ DevConsts c, PlanDev pl) {
@@ -1922,6 +1954,14 @@ cudaError_t launch_extract_share(const DevConsts& c, const PlanDev& p, const uin
     if (e != cudaSuccess) return e;
   }
   return cudaGetLastError();
+}
+
+cudaError_t launch_mask_draw(const DevConsts& c, const MaskGen& g, size_t n_ct, uint64_t* r, cudaStream_t s) {
+  if (n_ct == 0) return cudaSuccess;
+  const size_t half = (size_t)1 << (c.log_n - 1), pairs = n_ct * half;
+  const size_t blocks = (pairs + 255) / 256, cap = (size_t)c.tune.num_sms * 16;
+  return launch_pdl(c, k_mask_draw, dim3((unsigned)(blocks < cap ? blocks : cap)), dim3(256), 0, s, r, g, pairs,
+                    (uint32_t)half, c.t_bits);
 }
 
 cudaError_t launch_check_range(const DevConsts& c, const void* v, size_t n_words, int kind, uint32_t* flag,

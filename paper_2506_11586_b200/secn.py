@@ -37,7 +37,8 @@ EXPORTS = ("secn_ctx_create", "secn_ctx_destroy", "secn_ctx_query", "secn_last_e
            "secn_he_conv2d_online", "secn32_he_conv2d_online", "secn_fc_plan", "secn_fc_preprocess_weights",
            "secn32_fc_preprocess_weights", "secn_he_fc_workspace", "secn_he_fc", "secn32_he_fc",
            "secn_he_conv2d_lwe_workspace", "secn_he_conv2d_lwe", "secn32_he_conv2d_lwe", "secn_he_fc_lwe_workspace",
-           "secn_he_fc_lwe", "secn32_he_fc_lwe")
+           "secn_he_fc_lwe", "secn32_he_fc_lwe", "secn_mask_draw", "secn_he_conv2d_gen_workspace", "secn_he_conv2d_gen",
+           "secn32_he_conv2d_gen", "secn_he_conv2d_lwe_gen_workspace", "secn_he_conv2d_lwe_gen", "secn32_he_conv2d_lwe_gen")
 
 
 class SecnError(RuntimeError):
@@ -51,6 +52,11 @@ class FcPlan(ctypes.Structure):
 
     def __repr__(self):
         return "FcPlan(" + ", ".join(f"{f}={getattr(self, f)}" for f, _ in self._fields_) + ")"
+
+
+class MaskGen(ctypes.Structure):
+    """secn_mask_gen_t (reading R17): Philox4x32-10 key `seed`, stream id, first output ct index."""
+    _fields_ = [("seed", ctypes.c_uint64), ("stream", ctypes.c_uint32), ("ct0", ctypes.c_uint32)]
 
 
 class Plan(ctypes.Structure):
@@ -121,10 +127,16 @@ def lib(path=None) -> ctypes.CDLL:
         "secn_he_conv2d_online": (i, [vp, P, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
         "secn_extract_share": (i, [vp, P, vp, vp, vp]),
         "secn32_ctx_create": (i, [ctypes.POINTER(vp), i, u32, u32, ctypes.POINTER(ctypes.c_uint32), u32]),
+        "secn_mask_draw": (i, [vp, ctypes.POINTER(MaskGen), sz, vp, vp]),
+        "secn_he_conv2d_gen_workspace": (sz, [vp, P]),
+        "secn_he_conv2d_gen": (i, [vp, P, vp, vp, vp, ctypes.POINTER(MaskGen), vp, vp, vp, sz, vp]),
+        "secn_he_conv2d_lwe_gen_workspace": (sz, [vp, P]),
+        "secn_he_conv2d_lwe_gen": (i, [vp, P, vp, vp, vp, ctypes.POINTER(MaskGen), u32, vp, vp, vp, vp, sz, vp]),
     }
     for f in ("ntt_fwd", "ntt_inv", "preprocess_weights", "share_add", "mask_add", "he_conv2d", "he_conv2d_stage",
               "he_conv2d_stage_ex", "he_conv2d_ex",
-              "he_conv2d_online", "fc_preprocess_weights", "he_fc", "he_conv2d_lwe", "he_fc_lwe"):
+              "he_conv2d_online", "fc_preprocess_weights", "he_fc", "he_conv2d_lwe", "he_fc_lwe", "he_conv2d_gen",
+              "he_conv2d_lwe_gen"):
         sig["secn32_" + f] = sig["secn_" + f]
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -423,6 +435,55 @@ class Context:
                                              *_ws(workspace, self.workspace_bytes(plan), self.device),
                                              self._stream(stream)))
         return out
+
+    # ---- device-drawn mask (reading R17) ----
+    def mask_draw(self, gen: MaskGen, n_ct: int, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+        """secn_mask_draw: r int64 [n_ct][N] from the generator."""
+        if out is None:
+            out = torch.empty((n_ct, self.n), dtype=torch.int64, device=self.device)
+        _check(lib().secn_mask_draw(self._h, ctypes.byref(gen), n_ct, _ptr(out, (n_ct, self.n), "r"),
+                                    self._stream(stream)))
+        return out
+
+    def gen_workspace_bytes(self, plan: Plan) -> int:
+        return int(lib().secn_he_conv2d_gen_workspace(self._h, ctypes.byref(plan)))
+
+    def he_conv2d_gen(self, plan: Plan, ct_in: torch.Tensor, w_ntt: torch.Tensor, gen: MaskGen,
+                      x0: Optional[torch.Tensor] = None, out: Optional[torch.Tensor] = None,
+                      y0: Optional[torch.Tensor] = None, workspace: Optional[torch.Tensor] = None,
+                      stream=None) -> torch.Tensor:
+        """secn_he_conv2d_gen: secn_he_conv2d_ex with the mask drawn on the device by `gen`."""
+        L, n = self.L, self.n
+        n_in, n_out = plan.G * plan.S, plan.M * plan.S
+        if out is None:
+            out = self.empty(n_out, 2, L, n)
+        need = self.gen_workspace_bytes(plan)
+        if workspace is None:
+            workspace = torch.empty((need + 7) // 8, dtype=torch.int64, device=self.device)
+        wp, wn = _ws(workspace, need, self.device)
+        _check(self._f("he_conv2d_gen")(
+            self._h, ctypes.byref(plan), self._rp(ct_in, (n_in, 2, L, n), "ct_in"), _ptr(x0, (n_in, n), "x0"),
+            self._rp(w_ntt, (plan.M, plan.G, L, n), "w_ntt"), ctypes.byref(gen),
+            self._rp(out, (n_out, 2, L, n), "ct_out"), _ptr(y0, (plan.M, plan.OH, plan.OW), "y0"), wp, wn,
+            self._stream(stream)))
+        return out
+
+    def he_conv2d_lwe_gen(self, plan: Plan, ct_in: torch.Tensor, w_ntt: torch.Tensor, keep: int, gen: MaskGen,
+                          x0: Optional[torch.Tensor] = None, y0: Optional[torch.Tensor] = None,
+                          workspace: Optional[torch.Tensor] = None, stream=None, out: Optional[tuple] = None):
+        """secn_he_conv2d_lwe_gen: extracted outputs with the mask drawn on the device."""
+        L, n = self.L, self.n
+        a, b = out if out is not None else (self.empty(plan.M * plan.S, keep, n), self.empty(plan.M, plan.OH, plan.OW, keep))
+        need = int(lib().secn_he_conv2d_lwe_gen_workspace(self._h, ctypes.byref(plan)))
+        if workspace is None:
+            workspace = torch.empty((need + 7) // 8, dtype=torch.int64, device=self.device)
+        wp, wn = _ws(workspace, need, self.device)
+        _check(self._f("he_conv2d_lwe_gen")(
+            self._h, ctypes.byref(plan), self._rp(ct_in, (plan.G * plan.S, 2, L, n), "ct_in"),
+            _ptr(x0, (plan.G * plan.S, n), "x0"), self._rp(w_ntt, (plan.M, plan.G, L, n), "w_ntt"), ctypes.byref(gen),
+            keep, self._rp(a, (plan.M * plan.S, keep, n), "a_out"), self._rp(b, (plan.M, plan.OH, plan.OW, keep), "b_out"),
+            _ptr(y0, (plan.M, plan.OH, plan.OW), "y0"), wp, wn, self._stream(stream)))
+        return a, b
 
     def extract_share(self, plan: Plan, r: torch.Tensor, out: Optional[torch.Tensor] = None,
                       stream=None) -> torch.Tensor:

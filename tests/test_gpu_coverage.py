@@ -179,6 +179,8 @@ def _sanitize(tool, code, timeout=900):
                           sys.executable, "-c", code], capture_output=True, text=True, timeout=timeout, cwd=ROOT,
                          env={**os.environ, "PYTHONPATH": str(ROOT)})
     tail = (res.stdout[-3000:] + res.stderr[-3000:])
+    if "compute-sanitizer is closed on this pool" in tail:  # the GPU pool's wrapper refuses it (leaves GPUs needing a reset)
+        pytest.skip("compute-sanitizer is disabled on this GPU pool: " + tail.strip().splitlines()[0][:200])
     assert res.returncode == 0, f"{tool}: rc={res.returncode}\n{tail}"
     assert "SANITIZED_RUN_OK" in res.stdout or "smoke OK" in res.stdout, tail
     assert "ERROR SUMMARY: 0 errors" in res.stdout + res.stderr or "RACECHECK SUMMARY: 0 hazards" in res.stdout + res.stderr, tail
