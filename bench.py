@@ -69,6 +69,9 @@ def parse():
     ap.add_argument("--cpu-frac", type=float, default=None,
                     help="fraction of every layer's output ciphertexts the oracle computes (default 1 = the whole "
                          "network, measured; ResNet-50 0.02, extrapolated)")
+    ap.add_argument("--mask", choices=["device", "host"], default="device",
+                    help="device (default): the server's mask r is drawn inside every layer call (secn32_he_conv2d_gen, "
+                         "Philox4x32-10, reading R17); host: r is a caller input (secn32_he_conv2d_ex)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-online", action="store_true", help="skip the online-NTT-preprocessing (f4) leg")
@@ -152,6 +155,11 @@ class ClockSampler:
 # ------------------------------------------------------------------------------------------
 # workload
 
+def mask_seed(seed):
+    """The bench's Philox key for the device-drawn mask (reading R17); the stream id is the layer index."""
+    return (0x5EC0_11D5_0000_0000 ^ (seed * 0x9E3779B97F4A7C15)) & (2**64 - 1)
+
+
 def layer_inputs(P_primes, n, t_bits, lay, opl_G, opl_S, M, seed):
     """Seeded synthetic inputs of one layer (identical on every rank and in the oracle)."""
     g = inputs.rng(seed)
@@ -162,10 +170,12 @@ def layer_inputs(P_primes, n, t_bits, lay, opl_G, opl_S, M, seed):
     return ct, x0, K, r
 
 
-def algorithmic_bytes(plan, L, n, wbytes=8):
-    """SURVEY.md §8d per-layer bytes: wb L N (2GS + MG + 2MS) + 8 N MS (+ 8 N GS for x0)."""
+def algorithmic_bytes(plan, L, n, wbytes=8, drawn_mask=False):
+    """SURVEY.md §8d per-layer bytes: wb L N (2GS + MG + 2MS) + 8 N MS (+ 8 N GS for x0; + 8 N MS
+    more when the mask is drawn on the device: the draw writes r, the tail reads it)."""
     G, S, M = plan.G, plan.S, plan.M
-    return wbytes * L * n * (2 * G * S + M * G + 2 * M * S) + 8 * n * M * S + 8 * n * G * S
+    return (wbytes * L * n * (2 * G * S + M * G + 2 * M * S) + 8 * n * M * S + 8 * n * G * S
+            + (8 * n * M * S if drawn_mask else 0))
 
 
 def stage_bytes(plan, L, n, wbytes=8):
@@ -286,11 +296,12 @@ def run_ntt_sweep_line(args, world, rank, local, dev):
 def run_secn(args, word_bits, world, rank, local, dev, full):
     """Builds the workload at one residue word size, times K graph replays of the step and (full)
     the per-stage, e2e and cpu_baseline legs. Returns the JSON dict on rank 0 (None elsewhere)."""
-    from paper_2506_11586_b200 import Context
+    from paper_2506_11586_b200 import Context, MaskGen
     from paper_2506_11586_b200 import dist as sdist
     from paper_2506_11586_b200.schedule import GroupRunner, StagedGroupRunner, concurrent_groups
 
     ctx = Context(local, word_bits=word_bits)
+    drawn = args.mask == "device"
     L, n, t_bits = ctx.L, ctx.n, ctx.t_bits
     wbytes = ctx.word_bits // 8
 
@@ -303,25 +314,32 @@ def run_secn(args, word_bits, world, rank, local, dev, full):
     st = []
     for li, lay in enumerate(net):
         plan = ctx.plan(lay.C, lay.H, lay.W, lay.M, lay.k, stride=lay.stride, pad=lay.pad)
-        m0, mc = sdist.m_slices(plan.M, world)[rank]
+        parts = sdist.partition(plan.M, plan.S, world)  # (channel x spatial-block) rectangle per rank
+        m0, mc = parts[rank].m0, parts[rank].mc
         ct, x0, K, r = layer_inputs(ctx.primes, n, t_bits, lay, plan.G, plan.S, plan.M, args.seed * 1000 + li)
         S = plan.S
         d = {"lay": lay, "plan": plan, "win": (plan.Hw, plan.Ww, plan.decim == 2), "m0": m0, "mc": mc, "ct_h": ct, "x0_h": x0,
-             "K_h": K, "r_h": r}
+             "K_h": K, "r_h": r, "parts": parts}
         if mc > 0:
-            pl = plan.copy(M=mc)
+            sl = parts[rank].sc < plan.S  # a spatial slice: only these blocks' output cts (include/secn.h)
+            pl = plan.copy(M=mc, s_begin=parts[rank].s0 if sl else 0, s_count=parts[rank].sc if sl else 0)
             d["pl"] = pl
             d["ct"] = R(ct)
             d["x0"] = torch.from_numpy(x0.view(np.int64)).to(dev)
             d["K"] = torch.from_numpy(np.ascontiguousarray(K[m0:m0 + mc]).view(np.int64)).to(dev)
-            d["r"] = torch.from_numpy(np.ascontiguousarray(r[m0 * S:(m0 + mc) * S]).view(np.int64)).to(dev)
+            if drawn:  # this rank's rows of the layer's mask (ct0 = m0 S); r itself only for the stage legs
+                d["gen"] = MaskGen(seed=mask_seed(args.seed), stream=li, ct0=m0 * S)
+                d["r"] = ctx.mask_draw(d["gen"], mc * S)
+                d["ws_gen"] = torch.empty((ctx.gen_workspace_bytes(pl) + 7) // 8, dtype=torch.int64, device=dev)
+            else:
+                d["r"] = torch.from_numpy(np.ascontiguousarray(r[m0 * S:(m0 + mc) * S]).view(np.int64)).to(dev)
             d["out"] = ctx.empty(mc * S, 2, L, n)
             d["ws"] = torch.empty(ctx.workspace_bytes(pl) // 8, dtype=torch.int64, device=dev)
         else:
             d["pl"] = None
         st.append(d)
     dims = [(d["plan"].M, d["plan"].OH, d["plan"].OW) for d in st]
-    layout = sdist.share_layout(dims, world)
+    layout = sdist.share_layout(dims, world, [d["parts"] for d in st])
     share_buf = torch.zeros(layout.chunk, dtype=torch.int64, device=dev)
     for d, off in zip(st, layout.offsets):
         if d["mc"] > 0:
@@ -345,7 +363,10 @@ def run_secn(args, word_bits, world, rank, local, dev, full):
 
     def layer_call(i):
         d = st[i]
-        if d["mc"] > 0:
+        if d["mc"] > 0 and drawn:
+            ctx.he_conv2d_gen(d["pl"], d["ct"], d["w"], d["gen"], x0=d["x0"], out=d["out"], workspace=d["ws_gen"],
+                              y0=d["y0"])
+        elif d["mc"] > 0:
             ctx.he_conv2d(d["pl"], d["ct"], d["w"], x0=d["x0"], r=d["r"], out=d["out"], workspace=d["ws"],
                           y0=d["y0"])
 
@@ -403,10 +424,11 @@ def run_secn(args, word_bits, world, rank, local, dev, full):
     ms_per_step = float(total_ms.item()) / K
 
     if world > 1 and rank == 0:
-        shares = sdist.reassemble(gathered, layout, dims, world)
+        shares = sdist.reassemble(gathered, layout, dims, world, [d["parts"] for d in st],
+                                  [sdist.block_of_output(d["plan"]) for d in st])
         assert all(f.shape[0] == M for f, (M, _, _) in zip(shares, dims))
     hbm_peak, peak_kind = peaks()
-    alg_bytes = sum(algorithmic_bytes(d["plan"], L, n, wbytes) for d in st)
+    alg_bytes = sum(algorithmic_bytes(d["plan"], L, n, wbytes, drawn) for d in st)
     step_s = ms_per_step / 1e3
     if not full:
         del graph
@@ -421,15 +443,15 @@ def run_secn(args, word_bits, world, rank, local, dev, full):
     stage_ms = stage_profile(ctx, st, K, dev)
 
     # ---- e2e: host buffers, H2D + public API + D2H every step ----
-    e2e = None if args.no_e2e else run_e2e(ctx, st, K, dev, share_buf, world, runner)
+    e2e = None if args.no_e2e else run_e2e(ctx, st, K, dev, share_buf, world, runner, drawn=drawn)
 
     # ---- f4: online NTT preprocessing (weights in coefficient form, transformed in each call) ----
     online = None if args.no_online else run_online(ctx, st, K, args.warmup, dev, world, runner)
 
     # ---- f2: extracted outputs (modulus switch + designated coefficients) ----
-    lwe = run_lwe(ctx, st, K, args.warmup, dev, world, runner)
+    lwe = run_lwe(ctx, st, K, args.warmup, dev, world, runner, drawn=drawn)
     if not args.no_e2e:  # the same step end to end, sending back only the extracted outputs
-        lwe["e2e"] = run_e2e(ctx, st, K, dev, share_buf, world, runner, lwe_keep=ctx.L // 2)
+        lwe["e2e"] = run_e2e(ctx, st, K, dev, share_buf, world, runner, lwe_keep=ctx.L // 2, drawn=drawn)
 
     # ---- f3: the ResNet-50 fully-connected layer through secn_he_fc ----
     fc_leg = run_fc(ctx, K, args.warmup, dev, world)
@@ -439,7 +461,8 @@ def run_secn(args, word_bits, world, rank, local, dev, full):
 
     # ---- derived numbers ----
     n_ntt = sum((d["plan"].G * d["plan"].S * world + d["plan"].M * d["plan"].S) * 2 * L for d in st)  # limb NTTs per step
-    launches_per_step = sum(3 for d in st if d["mc"] > 0)  # NTT, MAC(+INTT 0-7), INTT tail(+mask, share)
+    # NTT, (mask draw,) MAC(+INTT 0-7), INTT tail(+mask, share)
+    launches_per_step = sum(4 if drawn else 3 for d in st if d["mc"] > 0)
     sb = {s: sum(stage_bytes(d["pl"], L, n, wbytes)[s] for d in st if d["mc"] > 0) for s in range(3)}
     names = {0: "k_ntt_fwd (A6 share add + A1 NTT)", 1: "k_mac (A4 NTT-domain MAC + INTT levels 0-7)",
              2: "k_ntt_inv_tail (A2 INTT levels 8-11 + A7 mask)"}
@@ -471,7 +494,10 @@ def run_secn(args, word_bits, world, rank, local, dev, full):
         "He-normal 37-bit/scale-12 kernels)",
         "config": {"workload": net_info(args.net)[1],
                    "N": n, "limbs": L, "primes": [hex(q) for q in ctx.primes], "t_bits": t_bits,
-                   "parallelism": f"output-channel shards x{world}", "l2": (f"inputs {alg_bytes / 1e9:.2f} GB/step >> 126 MB L2 (no flush)" if alg_bytes > 5e8 else
+                   "parallelism": (f"(output channel x spatial block) rectangles over {world} ranks "
+                                   "(paper_2506_11586_b200/dist.partition)" if world > 1 else "1 GPU"),
+                   "mask": ("drawn on the device inside every layer call (secn32_he_conv2d_gen, Philox4x32-10, "
+                            "reading R17)" if drawn else "caller input r (secn32_he_conv2d_ex)"), "l2": (f"inputs {alg_bytes / 1e9:.2f} GB/step >> 126 MB L2 (no flush)" if alg_bytes > 5e8 else
                           "step footprint below 4x L2: timing includes L2 reuse across replays"),
                    "timing": "CUDA events around CUDA-graph replays of the whole step",
                    "layer_overlap": {"none": "none: every layer in network order on one stream",
@@ -480,7 +506,8 @@ def run_secn(args, word_bits, world, rank, local, dev, full):
                                      "free": "free: layers reading the same input tensor (fire e1/e3, ResNet "
                                              "c1/ds) on two streams; the rest in network order"}[args.overlap]},
         "throughput": {"ntt_per_s": round(n_ntt / step_s, 1), "alg_bytes_per_step": alg_bytes,
-                       "alg_GBps": round(alg_bytes / step_s / 1e9, 1), "hbm_frac": round(alg_bytes / step_s / 1e9 / hbm_peak, 4),
+                       "alg_GBps": round(alg_bytes / step_s / 1e9, 1),
+                       "hbm_frac": round(alg_bytes / step_s / 1e9 / (hbm_peak * world), 4),
                        "offline_preprocess_s": round(offline_s, 5), "wall_s_timed_region": round(wall, 4)},
         "roofline": roofline,
         "per_layer_stage_us": stage_profile.per_layer_us,
@@ -492,7 +519,7 @@ def run_secn(args, word_bits, world, rank, local, dev, full):
     }
     if not args.no_cpu_baseline and world == 1:
         frac = args.cpu_frac if args.cpu_frac is not None else default_cpu_frac(args.net)
-        out["cpu_baseline"] = cpu_baseline(st, ctx, frac, dev, wbytes, args.seed)
+        out["cpu_baseline"] = cpu_baseline(st, ctx, frac, dev, wbytes, args.seed, drawn)
     return out
 
 
@@ -608,7 +635,7 @@ def run_online(ctx, st, K, warmup, dev, world, runner):
             "layer_overlap": _leg_overlap(runner)}
 
 
-def run_lwe(ctx, st, K, warmup, dev, world, runner):
+def run_lwe(ctx, st, K, warmup, dev, world, runner, drawn=False):
     """the same step returning extracted outputs (secn32_he_conv2d_lwe: the
     INTT tail switches every output ct to half of its limbs and keeps the b component only at the
     designated coefficients), i.e. what Cheetah's server sends back."""
@@ -616,12 +643,15 @@ def run_lwe(ctx, st, K, warmup, dev, world, runner):
     for d in st:
         if d["mc"] > 0:
             pl = d["pl"]
-            d["ws_lwe"] = torch.empty((int(ctx_lib().secn_he_conv2d_lwe_workspace(ctx._h, ctypes.byref(pl))) + 7) // 8,
-                                      dtype=torch.int64, device=dev)
+            wsf = ctx_lib().secn_he_conv2d_lwe_gen_workspace if drawn else ctx_lib().secn_he_conv2d_lwe_workspace
+            d["ws_lwe"] = torch.empty((int(wsf(ctx._h, ctypes.byref(pl))) + 7) // 8, dtype=torch.int64, device=dev)
 
     def layer_lwe(i):
         d = st[i]
-        if d["mc"] > 0:
+        if d["mc"] > 0 and drawn:
+            d["lwe_out"] = ctx.he_conv2d_lwe_gen(d["pl"], d["ct"], d["w"], keep, d["gen"], x0=d["x0"], y0=d["y0"],
+                                                 workspace=d["ws_lwe"])
+        elif d["mc"] > 0:
             d["lwe_out"] = ctx.he_conv2d_lwe(d["pl"], d["ct"], d["w"], keep, x0=d["x0"], r=d["r"], y0=d["y0"],
                                              workspace=d["ws_lwe"])
 
@@ -635,7 +665,9 @@ def run_lwe(ctx, st, K, warmup, dev, world, runner):
     torch.cuda.empty_cache()
     return {"value": round(ms / 1e3, 7), "unit": "s", "ms_per_step": round(ms, 4), "keep_limbs": keep,
             "output_bytes_per_step": out_bytes, "full_ct_output_bytes_per_step": full_bytes,
-            "path": "secn32_he_conv2d_lwe: share add + NTT, MAC, INTT tail + mask + modulus switch + extraction",
+            "path": ("secn32_he_conv2d_lwe_gen: share add + NTT, mask draw, MAC, INTT tail + mask + modulus switch + "
+                     "extraction" if drawn else
+                     "secn32_he_conv2d_lwe: share add + NTT, MAC, INTT tail + mask + modulus switch + extraction"),
             "layer_overlap": _leg_overlap(runner)}
 
 
@@ -661,7 +693,7 @@ def run_fc(ctx, K, warmup, dev, world, n_i=2048, n_o=1000, seed=11):
             "hbm_frac": round(alg / (ms / 1e3) / 1e9 / peaks()[0], 4), "launches": 3}
 
 
-def run_e2e(ctx, st, K, dev, share_buf, world, runner, lwe_keep=None):
+def run_e2e(ctx, st, K, dev, share_buf, world, runner, lwe_keep=None, drawn=False):
     """Same metric end to end through the public API: every step copies that step's inputs
     (ct_in, x0, r) host->device from pinned memory, runs secn_he_conv2d_ex (ciphertexts and the
     server's shares) per layer, and copies the output ciphertexts and shares device->host.
@@ -674,15 +706,16 @@ def run_e2e(ctx, st, K, dev, share_buf, world, runner, lwe_keep=None):
             continue
         if lwe_keep:
             pl = d["plan"]
-            d["ws_lwe"] = torch.empty((int(ctx_lib().secn_he_conv2d_lwe_workspace(ctx._h, ctypes.byref(d["pl"]))) + 7)
-                                      // 8, dtype=torch.int64, device=dev)
+            wsf = ctx_lib().secn_he_conv2d_lwe_gen_workspace if drawn else ctx_lib().secn_he_conv2d_lwe_workspace
+            d["ws_lwe"] = torch.empty((int(wsf(ctx._h, ctypes.byref(d["pl"]))) + 7) // 8, dtype=torch.int64, device=dev)
             d["lwe_out"] = (ctx.empty(d["mc"] * pl.S, lwe_keep, ctx.n), ctx.empty(d["mc"], pl.OH, pl.OW, lwe_keep))
         ct = np.ascontiguousarray(d["ct_h"])
         ct = ct.view(np.int64) if d["ct"].dtype == torch.int64 else ct.astype(np.uint32).view(np.int32)
         h = {"ct": torch.from_numpy(ct).pin_memory(),
              "x0": torch.from_numpy(np.ascontiguousarray(d["x0_h"]).view(np.int64)).pin_memory()}
         S = d["plan"].S
-        h["r"] = torch.from_numpy(np.ascontiguousarray(d["r_h"][d["m0"] * S:(d["m0"] + d["mc"]) * S]).view(np.int64)).pin_memory()
+        if not drawn:  # a caller-supplied mask is an input that crosses PCIe every step
+            h["r"] = torch.from_numpy(np.ascontiguousarray(d["r_h"][d["m0"] * S:(d["m0"] + d["mc"]) * S]).view(np.int64)).pin_memory()
         if lwe_keep:
             h["lwe_out"] = tuple(torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in d["lwe_out"])
             h["out"] = torch.empty(0, dtype=d["out"].dtype)
@@ -691,7 +724,7 @@ def run_e2e(ctx, st, K, dev, share_buf, world, runner, lwe_keep=None):
             h["out"] = torch.empty(d["out"].shape, dtype=d["out"].dtype).pin_memory()
             d2h += h["out"].numel() * h["out"].element_size()
         h["y0"] = torch.empty(d["y0"].shape, dtype=torch.int64).pin_memory()
-        h2d += sum(h[k].numel() * h[k].element_size() for k in ("ct", "x0", "r"))
+        h2d += sum(h[k].numel() * h[k].element_size() for k in ("ct", "x0", "r") if k in h)
         d2h += h["y0"].numel() * 8
         host.append((d, h))
 
@@ -712,15 +745,22 @@ def run_e2e(ctx, st, K, dev, share_buf, world, runner, lwe_keep=None):
             with torch.cuda.stream(hs):
                 d["ct"].copy_(h["ct"], non_blocking=True)
                 d["x0"].copy_(h["x0"], non_blocking=True)
-                d["r"].copy_(h["r"], non_blocking=True)
+                if not drawn:
+                    d["r"].copy_(h["r"], non_blocking=True)
                 e_in = torch.cuda.Event()
                 e_in.record(hs)
             cs.wait_event(e_in)
             if k in out_done:
                 cs.wait_event(out_done[k])
-            if lwe_keep:
+            if lwe_keep and drawn:
+                ctx.he_conv2d_lwe_gen(d["pl"], d["ct"], d["w"], lwe_keep, d["gen"], x0=d["x0"], y0=d["y0"],
+                                      workspace=d["ws_lwe"], out=d["lwe_out"])
+            elif lwe_keep:
                 ctx.he_conv2d_lwe(d["pl"], d["ct"], d["w"], lwe_keep, x0=d["x0"], r=d["r"], y0=d["y0"],
                                   workspace=d["ws_lwe"], out=d["lwe_out"])
+            elif drawn:
+                ctx.he_conv2d_gen(d["pl"], d["ct"], d["w"], d["gen"], x0=d["x0"], out=d["out"], workspace=d["ws_gen"],
+                                  y0=d["y0"])
             else:
                 ctx.he_conv2d(d["pl"], d["ct"], d["w"], x0=d["x0"], r=d["r"], out=d["out"], workspace=d["ws"],
                               y0=d["y0"])
@@ -766,12 +806,14 @@ def run_e2e(ctx, st, K, dev, share_buf, world, runner, lwe_keep=None):
     for d, _ in host:
         d.pop("ws_lwe", None)
         d.pop("lwe_out", None)
-    call = f"secn32_he_conv2d_lwe (keep {lwe_keep} limbs)" if lwe_keep else "secn_he_conv2d_ex"
+    call = (f"secn32_he_conv2d_lwe{'_gen' if drawn else ''} (keep {lwe_keep} limbs)" if lwe_keep else
+            ("secn32_he_conv2d_gen" if drawn else "secn32_he_conv2d_ex"))
     return {"value": round(float(ms.item()) / 1e3, 6), "unit": "s", "host_copies_match_device": same,
             "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h,
             "path": f"pinned host -> {call} -> pinned host; H2D, calls and D2H on three streams (per-layer "
-                    "events), so copies of one layer overlap the other layers' compute and each other"}
+                    "events), so copies of one layer overlap the other layers' compute and each other"
+                    + ("; the mask is drawn on the device (no r crosses PCIe)" if drawn else "")}
 
 
 # ------------------------------------------------------------------------------------------
@@ -781,9 +823,10 @@ def run_e2e(ctx, st, K, dev, share_buf, world, runner, lwe_keep=None):
 # layer (the offline setup, untimed, as the GPU arm's weight preprocessing is); the timed part is
 # the online server computation over every output ciphertext of the network.
 
-def oracle_states(net, P, words64, seed):
+def oracle_states(net, P, words64, seed, drawn=True):
     """Per layer: the oracle's plan, the seeded inputs (identical to the GPU arm's) and the
-    sparse plaintext polys."""
+    sparse plaintext polys. With drawn, r is left to oracle_run, which draws it from the oracle's
+    Philox4x32-10 (oracle/philox.py) inside the timed region, as the GPU arm draws it in its step."""
     from oracle import packing
 
     states = []
@@ -792,7 +835,8 @@ def oracle_states(net, P, words64, seed):
                                 rule="time")
         ct, x0, K, r = layer_inputs(P.primes, P.n, P.t_bits, lay, opl.G, opl.S, opl.M, seed * 1000 + li)
         kp = packing.sparse(packing.kernel_polys(K, opl, P.n))
-        states.append({"lay": lay, "opl": opl, "ct_h": ct, "x0_h": x0, "K_h": K, "r_h": r, "kp": kp})
+        states.append({"lay": lay, "opl": opl, "ct_h": ct, "x0_h": x0, "K_h": K, "r_h": None if drawn else r,
+                       "kp": kp, "gen": (mask_seed(seed), li) if drawn else None})
     return states
 
 
@@ -822,7 +866,7 @@ def oracle_run(states, P, ranges, check=None):
     """Runs the oracle's server computation on the given (layer, lo, hi) output ranges.
     Returns (measured seconds, outputs, parity mismatches); `check(li, lo, hi)` returns the GPU's
     outputs [hi-lo][2][L][N] as uint64 (or None) to compare word for word (not timed)."""
-    from oracle import he
+    from oracle import he, philox
 
     dt, n, bad = 0.0, 0, 0
     for li, lo, hi in ranges:
@@ -831,7 +875,11 @@ def oracle_run(states, P, ranges, check=None):
         sel = np.zeros(o.M * o.S, np.uint8)
         sel[lo:hi] = 1
         t0 = time.perf_counter()
-        ref = he.server_mac_sparse(d["ct_h"], d["x0_h"], d["kp"], d["r_h"], o.G, o.S, o.M, P, sel=sel)
+        r = d["r_h"]
+        if d["gen"] is not None:  # the mask rows of these outputs, drawn as the GPU draws them
+            r = np.zeros((o.M * o.S, P.n), np.uint64)
+            r[lo:hi] = philox.mask(d["gen"][0], d["gen"][1], hi - lo, P.n, P.t_bits, ct0=lo)
+        ref = he.server_mac_sparse(d["ct_h"], d["x0_h"], d["kp"], r, o.G, o.S, o.M, P, sel=sel)
         dt += time.perf_counter() - t0
         n += hi - lo
         if check is not None:
@@ -848,7 +896,7 @@ def default_cpu_frac(net):
     return 0.02 if net == "resnet50" else 1.0
 
 
-def cpu_baseline(st, ctx, frac, dev, wbytes, seed):
+def cpu_baseline(st, ctx, frac, dev, wbytes, seed, drawn=True):
     """The oracle on this box's host cores over the whole network (frac = 1: every output
     ciphertext, measured, no extrapolation), on the GPU arm's seeded inputs; every output word is
     also compared with the GPU's (parity_mismatched_words)."""
@@ -856,7 +904,7 @@ def cpu_baseline(st, ctx, frac, dev, wbytes, seed):
     from oracle.params import Params
 
     P = Params(primes=ctx.primes)
-    states = oracle_states([d["lay"] for d in st], P, ctx.coef_words64, seed)
+    states = oracle_states([d["lay"] for d in st], P, ctx.coef_words64, seed, drawn)
     for d, o in zip(st, states):  # the oracle planned every layer itself: the library must agree
         assert (o["opl"].Hw, o["opl"].Ww, o["opl"].decim == 2, o["opl"].G, o["opl"].S) == \
             (d["plan"].Hw, d["plan"].Ww, d["plan"].decim == 2, d["plan"].G, d["plan"].S), d["lay"].name
@@ -899,7 +947,7 @@ def run_reference(args, world, rank):
     net = layers.network(args.net)
     P = Params(primes=oparams.DEFAULT_PRIMES if args.word_bits == 64 else oparams.PRIMES32)
     words64 = max(1, P.L * args.word_bits // 64)
-    states = oracle_states(net, P, words64, args.seed)
+    states = oracle_states(net, P, words64, args.seed, args.mask == "device")
     frac = args.cpu_frac if args.cpu_frac is not None else default_cpu_frac(args.net)
     small = min(range(len(states)), key=lambda i: states[i]["opl"].M * states[i]["opl"].S)
     for _ in range(args.warmup):  # one output ciphertext of the smallest layer

@@ -84,7 +84,15 @@ typedef struct {
   uint32_t Hw, Ww;                          /* 0 = choose (secn_conv_plan_ex rule); else validated */
   uint32_t OH, OW, decim, Hp, Wp;           /* filled (decim = 2 also an input, see above) */
   uint32_t Cw, G, S, nbh, nbw, O;           /* filled                                      */
+  uint32_t s_begin, s_count;                /* output spatial-block slice (caller; 0, 0 = all S) */
 } secn_conv_plan_t;
+/* Slices of one layer's output (the multi-GPU partition). M may be a slice of the
+ * output channels: pass a plan copy with M = the slice size and pointers offset to its weights,
+ * mask rows, output ciphertexts and share rows. s_begin, s_count select the spatial blocks
+ * [s_begin, s_begin + s_count) of S: the call computes only the output ciphertexts (m, s) with s in
+ * that range, at their usual positions m*S + s of ct_out / r (which keep all S rows; the other rows
+ * are neither read nor written), and writes y0 only at the outputs those blocks designate. The
+ * input ciphertexts are always all G*S. s_count = 0 means all of S (then s_begin must be 0). */
 
 typedef struct {
   uint32_t log_n, n, n_limbs, t_bits;

@@ -128,6 +128,7 @@ secn::PlanDev plan_dev(const secn_conv_plan_t* p) {
   d.kh0 = p->kh, d.kw0 = p->kw, d.ps = ps;                      // the caller's kernel tensor
   d.C = p->C, d.O = p->O, d.OH = p->OH, d.OW = p->OW, d.nbh = p->nbh, d.nbw = p->nbw;
   d.sh = p->decim ? 1 : p->stride;
+  d.s0 = p->s_count ? p->s_begin : 0, d.sn = p->s_count ? p->s_count : p->S;
   return d;
 }
 
@@ -181,6 +182,8 @@ int check_plan(const secn_ctx* ctx, const secn_conv_plan_t* p) {
   if (q.Cw != p->Cw || q.G != p->G || q.S != p->S || q.O != p->O || q.OH != p->OH || q.OW != p->OW ||
       q.decim != p->decim || q.nbh != p->nbh || q.nbw != p->nbw)
     return fail(SECN_EINVAL, "plan fields do not match secn_conv_plan() for this geometry and N");
+  if (p->s_count ? (uint64_t)p->s_begin + p->s_count > p->S : p->s_begin != 0)
+    return fail(SECN_EINVAL, "spatial slice [%u, %u + %u) not inside S = %u", p->s_begin, p->s_begin, p->s_count, p->S);
   return SECN_OK;
 }
 
@@ -540,7 +543,9 @@ static int he_conv2d_impl(secn_ctx* ctx, uint32_t bits, const secn_conv_plan_t* 
   if (plan->G > 32u) return fail(SECN_EUNSUPPORTED, "G=%u input channel groups too many", plan->G);
   DeviceGuard guard(ctx->device);
   cudaStream_t s = (cudaStream_t)stream;
+  // n_out: rows of r / ct_out; n_act: the output ciphertexts this call computes (its s-slice)
   const size_t n_in = (size_t)plan->G * plan->S, n_out = (size_t)plan->M * plan->S, N = ctx->n;
+  const size_t n_act = (size_t)plan->M * (plan->s_count ? plan->s_count : plan->S);
   if (stage <= 0) {
     if (int st = check_range(ctx, ct_in, n_in * 2 * ctx->L * N, 0, s, "secn_he_conv2d ct_in")) return st;
     if (int st = check_range(ctx, x0, n_in * N, 1, s, "secn_he_conv2d x0")) return st;
@@ -560,7 +565,7 @@ static int he_conv2d_impl(secn_ctx* ctx, uint32_t bits, const secn_conv_plan_t* 
   if (e == cudaSuccess && (stage == -1 || stage == 1))
     e = secn::launch_mac(ctx->dc, pd, workspace, w_ntt, ct_out, s, ch);
   if (e == cudaSuccess && (stage == -1 || stage == 2))
-    e = secn::launch_ntt_inv_tail(ctx->dc, ct_out, n_out * 2 * ctx->L, r, y0, pd, s, ch);  // A2 (levels 8..) + A7 (+A8)
+    e = secn::launch_ntt_inv_tail(ctx->dc, ct_out, n_act * 2 * ctx->L, r, y0, pd, s, ch);  // A2 (levels 8..) + A7 (+A8)
   return e == cudaSuccess ? SECN_OK : cuda_fail(e, "secn_he_conv2d");
 }
 
@@ -706,6 +711,7 @@ static int check_fc_plan(const secn_ctx* ctx, const secn_fc_plan_t* p) {
 static secn::PlanDev fc_plan_dev(const secn_fc_plan_t* p) {
   secn::PlanDev d{};
   d.kind = 1, d.M = p->M, d.G = p->G, d.S = 1, d.C = p->n_i, d.nib = p->nib, d.nob = p->nob, d.no = p->n_o;
+  d.s0 = 0, d.sn = 1;
   return d;
 }
 
@@ -831,8 +837,8 @@ static int he_conv2d_lwe_impl(secn_ctx* ctx, uint32_t bits, const secn_conv_plan
   DeviceGuard guard(ctx->device);
   if (int st = check_range(ctx, r, (size_t)plan->M * plan->S * ctx->n, 1, (cudaStream_t)stream, "secn_he_conv2d_lwe r"))
     return st;
-  cudaError_t e = secn::launch_ntt_inv_tail_lwe(ctx->dc, ms, yhat, (size_t)plan->M * plan->S, r, a_out, b_out, y0,
-                                                plan_dev(plan), (cudaStream_t)stream, true);
+  cudaError_t e = secn::launch_ntt_inv_tail_lwe(ctx->dc, ms, yhat, (size_t)plan->M * plan_dev(plan).sn, r, a_out,
+                                                b_out, y0, plan_dev(plan), (cudaStream_t)stream, true);
   return e == cudaSuccess ? SECN_OK : cuda_fail(e, "secn_he_conv2d_lwe");
 }
 

@@ -69,11 +69,16 @@ struct DevConsts {
   Tune tune;          // host-side launch choices (never read by a kernel)
 };
 
+struct PlanDev;
+// the index m*S + s of the i-th output ciphertext of a call with an s-slice (i = m * sn + s - s0)
+__host__ __device__ inline uint32_t slice_ct(const PlanDev& p, uint32_t i);
+
 struct PlanDev {  // the subset of secn_conv_plan (kind 0) / secn_fc_plan (kind 1) the kernels use
   uint32_t M, G, S, Cw, Hw, Ww, kh, kw, C, O, OH, OW, nbh, nbw, sh;
   uint32_t kh0, kw0, ps;  // the caller's kernel extent and the polyphase factor (reading R7b; kh, kw
                           // above are the window's extent ceil(kh0/ps) x ceil(kw0/ps))
   uint32_t kind;         // 0: convolution, 1: fully connected (S = 1)
+  uint32_t s0, sn;       // output spatial-block slice [s0, s0 + sn) of S (sn = S: all)
   uint32_t nib, nob, no; // fc: inputs per ct, output rows per ct, n_o (C holds n_i)
 };
 
@@ -83,6 +88,10 @@ struct MaskGen {
   uint64_t seed;
   uint32_t stream, ct0;
 };
+
+__host__ __device__ inline uint32_t slice_ct(const PlanDev& p, uint32_t i) {
+  return p.sn == p.S ? i : (i / p.sn) * p.S + p.s0 + i % p.sn;
+}
 
 // Modulus switch Q -> Q' = q_0 .. q_{Lk-1} (reading R16): P = the product of the dropped primes
 // q_Lk .. q_{L-1}; for a dropped limb j: pq[j] = P / q_j and inv[j] = (P / q_j)^-1 mod q_j; for a

@@ -388,7 +388,8 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, sizeof(typename A::W) == 4 &
   extern __shared__ __align__(16) unsigned char smraw[];
   W* sm = reinterpret_cast<W*>(smraw);
   const int j = (int)(blockIdx.x % c.L);
-  const size_t pi = blockIdx.x / c.L;
+  const size_t pa = blockIdx.x / c.L;  // (active ct, component); the ct's row is slice_ct (s-slice)
+  const size_t pi = 2 * (size_t)slice_ct(pl, (uint32_t)(ct0 + (pa >> 1))) + (pa & 1) - 2 * ct0;
   const W q = (W)c.q[j], qb = A::bound(q);
   const typename A::Tw* tw = Tab<A>::inv(c) + (size_t)j * N;
   const typename A::Tw ninv = Tab<A>::pair(c.ninv_mac[j], c.ninv_mac_p[j]);  // inputs are k_mac outputs
@@ -455,7 +456,7 @@ __global__ void __launch_bounds__(256, 4)
   using RS = GsRound<LOGN, LS>;
   static_assert(GsLast<LOGN>::value == LS, "one round");
   const int j = (int)(blockIdx.x % c.L);
-  const size_t ct = blockIdx.x / c.L;
+  const size_t ct = slice_ct(pl, (uint32_t)(ct0 + blockIdx.x / c.L)) - ct0;  // row of this ct (s-slice aware)
   const W q = (W)c.q[j], qb = A::bound(q);
   const typename A::Tw* tw = Tab<A>::inv(c) + (size_t)j * N;
   const typename A::Tw ninv = Tab<A>::pair(c.ninv_mac[j], c.ninv_mac_p[j]);  // inputs are k_mac outputs
@@ -744,8 +745,8 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
   const int j = blockIdx.y;
   const int sgi = blockIdx.x % n_sg, et = blockIdx.x / n_sg;
   const uint32_t e0 = et * MAC_THREADS;
-  const int s0 = sgi * SG;
-  const int ns = min(SG, S - s0);
+  const int s0 = (int)pl.s0 + sgi * SG;  // s-groups tile the call's spatial slice
+  const int ns = min(SG, (int)(pl.s0 + pl.sn) - s0);
   const int m_begin = blockIdx.z * m_range, m_end = min((int)pl.M, m_begin + m_range);
   const uint32_t row_bytes = MAC_THREADS * sizeof(W);
   using AR = typename ArithOf<W>::A;
@@ -956,7 +957,7 @@ __global__ void __launch_bounds__(FUSED_THREADS + 32, 2)
   const int L = (int)c.L, G = (int)pl.G, S = (int)pl.S;
   const int j = blockIdx.y;
   const int sgi = blockIdx.x % n_sg, mb = (blockIdx.x / n_sg) * MT;
-  const int s0 = sgi * SG, ns = min(SG, S - s0), rows = min(MT, (int)pl.M - mb);
+  const int s0 = (int)pl.s0 + sgi * SG, ns = min(SG, (int)(pl.s0 + pl.sn) - s0), rows = min(MT, (int)pl.M - mb);
   const int n_gc = (G + GC - 1) / GC, total = (N / FUSED_THREADS) * n_gc;
   const int stage_words = GC * (A2 + MT) * FUSED_THREADS;
   // shared memory: [NP][SW] output polys (padded layout), [NS][stage] ring, 2 NS mbarriers
@@ -1186,7 +1187,7 @@ __global__ void __launch_bounds__(LWE_G * SECN_MAX_LIMBS)
   using RS = GsRound<LOGN, 8>;
   static_assert(RS::NT == 1 && RS::GK == 16, "one radix-16 task per thread");
   __shared__ W ys[ND][16][LWE_G];
-  const size_t pi = blockIdx.x >> 1, ct = pi >> 1;
+  const size_t ct = slice_ct(pl, (uint32_t)(blockIdx.x >> 2)), pi = 2 * ct + ((blockIdx.x >> 1) & 1);
   const uint32_t o = (blockIdx.x & 1) * LWE_G + threadIdx.x % LWE_G;  // radix-16 task: coefficients o + 256 i
   const int j = threadIdx.x / LWE_G;                                   // this group's limb
   const bool isb = pi & 1, mask = isb && r != nullptr;
@@ -1390,6 +1391,7 @@ __global__ void k_extract_share(const uint64_t* __restrict__ r, uint64_t* __rest
   const uint32_t bh = py / (pl.Hw - pl.kh + 1), i = py % (pl.Hw - pl.kh + 1);
   const uint32_t bw = px / (pl.Ww - pl.kw + 1), jj = px % (pl.Ww - pl.kw + 1);
   const uint32_t s = bh * pl.nbw + bw;
+  if (s < pl.s0 || s >= pl.s0 + pl.sn) return;  // another call's spatial slice
   const size_t N = 1ull << c.log_n;
   const uint64_t t = 1ull << c.t_bits;
   y0[idx] = (t - r[((size_t)m * pl.S + s) * N + pl.O + i * pl.Ww + jj]) & (t - 1);
@@ -1671,7 +1673,7 @@ static cudaError_t mac_t(const DevConsts& c, const PlanDev& p, const void* xhat,
   NS = NS < 4 ? 4 : NS > 32 ? 32 : NS;
   const size_t smem = fixed + NS * stage + (2 * NS + 1) * sizeof(uint64_t);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;  // opted in by init_device
-  const int n_sg = (p.S + SG - 1) / SG;
+  const int n_sg = (p.sn + SG - 1) / SG;
   // m-range per CTA: the split of M into n_mr ranges (each >= MT channels, a multiple of MT)
   // whose CTA count fills whole waves of two CTAs per SM best; ties go to fewer, longer CTAs
   // (each CTA pays one X^ tile load and one pipeline fill).
@@ -1735,9 +1737,9 @@ cudaError_t launch_mac(const DevConsts& c, const PlanDev& p, const void* xhat, c
   // (64-bit limbs), spill-free at the 96 registers two 288-thread CTAs per SM allow.
   const size_t wb = c.word_bits / 8;
   int sg = 1;
-  for (int cand = 2; cand <= 4 && cand <= (int)p.S; ++cand) {
+  for (int cand = 2; cand <= 4 && cand <= (int)p.sn; ++cand) {
     if ((size_t)p.G * 2 * cand * MAC_THREADS * wb > 64 * 1024) break;
-    const int nc = (int)((p.S + cand - 1) / cand), nb = (int)((p.S + sg - 1) / sg);
+    const int nc = (int)((p.sn + cand - 1) / cand), nb = (int)((p.sn + sg - 1) / sg);
     if (nc * (2 * cand + 1) < nb * (2 * sg + 1)) sg = cand;
   }
   if (const int sg_env = c.tune.mac_sg) sg = sg_env;
@@ -1844,7 +1846,7 @@ static cudaError_t fused_t(const DevConsts& c, const PlanDev& p, const void* xha
   int NS = 0, GC = 0;
   const size_t smem = fused_smem<SG, MT>(c, (int)p.G, &NS, &GC);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;  // opted in by init_device
-  const int n_sg = (p.S + SG - 1) / SG, n_mb = (p.M + MT - 1) / MT;
+  const int n_sg = (p.sn + SG - 1) / SG, n_mb = (p.M + MT - 1) / MT;
   // X^ [G][S*2][L][N] as (N, L, 2S, G); W [M][G][L][N] as (N, L, G, M)
   const cuuint64_t wb = 4;
   CUtensorMap tmx, tmw;

@@ -62,7 +62,7 @@ class MaskGen(ctypes.Structure):
 class Plan(ctypes.Structure):
     _fields_ = [(f, ctypes.c_uint32) for f in
                 ("C", "H", "W", "M", "kh", "kw", "stride", "pad", "Hw", "Ww", "OH", "OW", "decim", "Hp", "Wp",
-                 "Cw", "G", "S", "nbh", "nbw", "O")]
+                 "Cw", "G", "S", "nbh", "nbw", "O", "s_begin", "s_count")]
 
     def copy(self, **kw) -> "Plan":
         p = Plan()

@@ -16,7 +16,7 @@ import numpy as np
 import pytest
 import torch
 
-from oracle import he, packing
+from oracle import he, packing, philox
 from test_gpu_parity import DEV, TP, UP, Dev, _layer_inputs, env, oplan, secn, secn_mod  # noqa: F401  (fixtures)
 from workloads import layers
 
@@ -105,38 +105,57 @@ def test_mac_worst_case_accumulator_g32(env, m):
 
 
 @pytest.mark.parametrize("world", [2, 4, 8])
-@pytest.mark.parametrize("name", ["fire9.e3", "conv1", "fire2.sq"])
-def test_rank_sliced_calls_reassemble(env, world, name):
-    """Each rank's call of the multi-GPU path (bench.py: plan.copy(M=mc), the rank's weights,
-    mask rows and share block), run one after another on this GPU, then reassembled with
-    dist.reassemble exactly as after the NCCL all-gather: the ciphertexts (concatenated over
-    ranks) and the server shares equal the oracle's single-GPU result."""
+@pytest.mark.parametrize("name", ["fire9.e3", "conv1", "fire2.sq", "fire3.sq"])
+@pytest.mark.parametrize("drawn", [False, True], ids=["r_in", "r_drawn"])
+def test_rank_partition_calls_reassemble(env, world, name, drawn):
+    """Each rank's call of the multi-GPU path (bench.py: dist.partition's (channel x spatial
+    block) rectangle -> plan.copy(M=mc, s_begin, s_count), the rank's weights, mask rows -- given,
+    or drawn with ct0 = m0 S -- and share block), run one after another on this GPU, then
+    reassembled with dist.reassemble exactly as after the NCCL all-gather: every output ciphertext
+    (from the rank that owns it) and every server share equal the oracle's single-GPU result.
+    fire2.sq / fire3.sq at 4 and 8 ranks take spatial slices (Ps > 1)."""
     from paper_2506_11586_b200 import dist as sdist
 
     ctx, P, D = env
     lay = next(l for l in layers.squeezenet11() if l.name == name)
     opl = oplan(P, ctx, lay)
     ct, x0, K, r = _layer_inputs(P, lay, 900 + world, opl)
+    seed, stream = 31337, 4
+    if drawn:
+        r = philox.mask(seed, stream, opl.M * opl.S, P.n, P.t_bits)
     plan = ctx.plan(lay.C, lay.H, lay.W, lay.M, lay.k, stride=lay.stride, pad=lay.pad)
     S = plan.S
+    parts = sdist.partition(plan.M, S, world)
     dims = [(plan.M, plan.OH, plan.OW)]
-    layout = sdist.share_layout(dims, world)
-    chunks, outs = [], []
+    layout = sdist.share_layout(dims, world, [parts])
+    chunks = []
+    got = np.zeros((plan.M * S, 2, ctx.L, ctx.n), np.uint64)
+    owned = np.zeros(plan.M * S, bool)
     cti, x0t = D.R(ct), TP(x0)
-    for rank, (m0, mc) in enumerate(sdist.m_slices(plan.M, world)):
-        chunk = torch.zeros(layout.chunk, dtype=torch.int64, device=DEV)
-        if mc > 0:
-            pl = plan.copy(M=mc)
-            w = ctx.preprocess_weights(pl, TP(np.ascontiguousarray(K[m0:m0 + mc])))
-            y0 = chunk[layout.offsets[0]:layout.offsets[0] + mc * plan.OH * plan.OW].view(mc, plan.OH, plan.OW)
-            o = ctx.he_conv2d(pl, cti, w, x0=x0t, r=TP(np.ascontiguousarray(r[m0 * S:(m0 + mc) * S])), y0=y0)
-            outs.append(D.U(o))
+    for p in parts:
+        chunk = torch.full((layout.chunk,), -5, dtype=torch.int64, device=DEV)
+        if p.mc > 0:
+            sl = p.sc < S
+            pl = plan.copy(M=p.mc, s_begin=p.s0 if sl else 0, s_count=p.sc if sl else 0)
+            w = ctx.preprocess_weights(pl, TP(np.ascontiguousarray(K[p.m0:p.m0 + p.mc])))
+            y0 = chunk[layout.offsets[0]:layout.offsets[0] + p.mc * plan.OH * plan.OW].view(p.mc, plan.OH, plan.OW)
+            if drawn:
+                g = secn_mod().MaskGen(seed=seed, stream=stream, ct0=p.m0 * S)
+                o = D.U(ctx.he_conv2d_gen(pl, cti, w, g, x0=x0t, y0=y0))
+            else:
+                o = D.U(ctx.he_conv2d(pl, cti, w, x0=x0t, r=TP(np.ascontiguousarray(r[p.m0 * S:(p.m0 + p.mc) * S])),
+                                      y0=y0))
+            for m in range(p.mc):
+                for s_ in range(p.s0, p.s0 + p.sc):
+                    row = (p.m0 + m) * S + s_
+                    assert not owned[row]
+                    owned[row] = True
+                    got[row] = o[m * S + s_]
         chunks.append(chunk)
-    full = sdist.reassemble(torch.cat(chunks), layout, dims, world)[0]
+    assert owned.all()
+    full = sdist.reassemble(torch.cat(chunks), layout, dims, world, [parts], [sdist.block_of_output(plan)])[0]
     n_out = opl.M * opl.S
-    got = np.concatenate(outs)
-    assert got.shape[0] == n_out
-    pick = np.unique(np.array([0, n_out // 3, n_out // 2, n_out - 1]))
+    pick = np.unique(np.array([0, n_out // 3, n_out // 2, n_out - 1, min(n_out - 1, S)]))
     sel = np.zeros(n_out, np.uint8)
     sel[pick] = 1
     ref = he.server_conv(ct, x0, K, r, opl, P, sel=sel)
