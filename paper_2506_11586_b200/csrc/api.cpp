@@ -518,27 +518,43 @@ int secn32_mask_add(secn_ctx* ctx, uint32_t* ct, const uint64_t* r, size_t n, vo
   return enc_add_impl(ctx, 32, ct, r, n, stream, "secn32_mask_add");
 }
 
+// Workspace of one layer call: the NTT-domain inputs X^ [G*S][2][L][N], then (full calls with a
+// mask) the encoded mask em [M*S][L][N] (k_mask_encode), both in the context's word size.
+static size_t xhat_bytes(const secn_ctx* ctx, const secn_conv_plan_t* plan) {
+  return (size_t)plan->G * plan->S * 2 * ctx->L * ctx->n * (ctx->word_bits / 8);
+}
+static size_t xhat_bytes_aligned(const secn_ctx* ctx, const secn_conv_plan_t* plan) {
+  return (xhat_bytes(ctx, plan) + 255) & ~(size_t)255;
+}
+static size_t em_bytes(const secn_ctx* ctx, const secn_conv_plan_t* plan) {
+  return (size_t)plan->M * plan->S * ctx->L * ctx->n * (ctx->word_bits / 8);
+}
+
 size_t secn_he_conv2d_workspace(const secn_ctx* ctx, const secn_conv_plan_t* plan) {
   if (!ctx || !plan) return 0;
-  return (size_t)plan->G * plan->S * 2 * ctx->L * ctx->n * (ctx->word_bits / 8);
+  return xhat_bytes_aligned(ctx, plan) + em_bytes(ctx, plan);
 }
 
 // stage -1 = the whole layer; 0 / 1 / 2 = one launch group. `chained`: the caller launched this
 // stage's predecessor stage itself just before (internal.h, "Pre-wait reads"); always true for -1.
-// gen != NULL (stage -1 or 0 only): the mask is drawn on the device (reading R17) into gen_r, which
-// is then passed as r; the draw kernel runs between the forward NTT and the MAC.
+// Full calls (stage -1) with a mask encode it once, right after the forward NTT (k_mask_encode:
+// em in the workspace, y0 written there), and the tail adds em; gen != NULL draws r on the device
+// (reading R17) instead of reading it. Stage calls (0, 1, 2) need only X^ in the workspace and
+// encode r in the tail.
 static int he_conv2d_impl(secn_ctx* ctx, uint32_t bits, const secn_conv_plan_t* plan, int stage, const void* ct_in,
                           const uint64_t* x0, const void* w_ntt, const uint64_t* r, void* ct_out, uint64_t* y0,
                           void* workspace, size_t ws_bytes, void* stream, bool chained = false,
-                          const secn::MaskGen* gen = nullptr, uint64_t* gen_r = nullptr) {
+                          const secn::MaskGen* gen = nullptr) {
   if (int st = check_ctx(ctx, bits)) return st;
   if (int st = check_plan(ctx, plan)) return st;
   if (stage < -1 || stage > 2) return fail(SECN_EINVAL, "stage %d not in {0,1,2}", stage);
   if (!ct_in || !w_ntt || !ct_out || !workspace) return fail(SECN_EINVAL, "NULL buffer");
   if (ctx->log_n > 14) return fail(SECN_EUNSUPPORTED, "convolutions need log_n <= 14 (N = 2^15 is NTT-only)");
-  if (y0 && !r) return fail(SECN_EINVAL, "y0 needs the mask r");
-  if (ws_bytes < secn_he_conv2d_workspace(ctx, plan)) return fail(SECN_EINVAL, "workspace too small");
-  if (((uintptr_t)workspace | (uintptr_t)ct_in | (uintptr_t)ct_out | (uintptr_t)w_ntt) & 15)
+  if (y0 && !r && !gen) return fail(SECN_EINVAL, "y0 needs the mask r");
+  const bool encode = stage == -1 && (r != nullptr || gen != nullptr);
+  if (ws_bytes < (encode ? secn_he_conv2d_workspace(ctx, plan) : xhat_bytes(ctx, plan)))
+    return fail(SECN_EINVAL, "workspace too small");
+  if (((uintptr_t)workspace | (uintptr_t)ct_in | (uintptr_t)ct_out | (uintptr_t)w_ntt | (uintptr_t)r) & 15)
     return fail(SECN_EINVAL, "buffers must be 16-byte aligned");
   if (plan->G > 32u) return fail(SECN_EUNSUPPORTED, "G=%u input channel groups too many", plan->G);
   DeviceGuard guard(ctx->device);
@@ -555,17 +571,24 @@ static int he_conv2d_impl(secn_ctx* ctx, uint32_t bits, const secn_conv_plan_t* 
   const secn::PlanDev pd = plan_dev(plan);
   cudaError_t e = cudaSuccess;
   if (stage == -1 || stage == 0) e = secn::launch_ntt_fwd(ctx->dc, ct_in, workspace, n_in * 2 * ctx->L, x0, s);  // A6+A1
-  if (e == cudaSuccess && gen != nullptr) e = secn::launch_mask_draw(ctx->dc, *gen, n_out, gen_r, s);  // R17
+  void* em = nullptr;
+  if (e == cudaSuccess && encode) {  // A7 (+A8) prepared on the SMs the forward NTT leaves idle
+    em = static_cast<unsigned char*>(workspace) + xhat_bytes_aligned(ctx, plan);
+    const secn::MaskGen g = gen ? *gen : secn::MaskGen{0, 0, 0};
+    e = secn::launch_mask_encode(ctx->dc, pd, n_act, gen ? nullptr : r, g, em, y0, s);
+  }
   // A4 + A2 levels 0..7
   const bool ch = chained || stage == -1;
   if (e == cudaSuccess && stage == -1 && secn::fused_applies(ctx->dc, pd)) {  // MAC + INTT + mask in one kernel
-    e = secn::launch_layer_fused(ctx->dc, pd, workspace, w_ntt, ct_out, r, y0, s, true);
+    e = secn::launch_layer_fused(ctx->dc, pd, workspace, w_ntt, ct_out, em ? nullptr : r, em ? nullptr : y0, s, true,
+                                 em);
     return e == cudaSuccess ? SECN_OK : cuda_fail(e, "secn_he_conv2d");
   }
   if (e == cudaSuccess && (stage == -1 || stage == 1))
     e = secn::launch_mac(ctx->dc, pd, workspace, w_ntt, ct_out, s, ch);
-  if (e == cudaSuccess && (stage == -1 || stage == 2))
-    e = secn::launch_ntt_inv_tail(ctx->dc, ct_out, n_act * 2 * ctx->L, r, y0, pd, s, ch);  // A2 (levels 8..) + A7 (+A8)
+  if (e == cudaSuccess && (stage == -1 || stage == 2))  // A2 (levels 8..) + A7 (+A8)
+    e = secn::launch_ntt_inv_tail(ctx->dc, ct_out, n_act * 2 * ctx->L, em ? nullptr : r, em ? nullptr : y0, pd, s, ch,
+                                  em);
   return e == cudaSuccess ? SECN_OK : cuda_fail(e, "secn_he_conv2d");
 }
 
@@ -590,10 +613,6 @@ int secn32_he_conv2d_ex(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint3
 // f4 ("online/offline/no NTT preprocessing"): the weights arrive in
 // coefficient form and are packed + transformed inside the online call, into workspace scratch
 // after X^; then the same three launches as secn_he_conv2d_ex.
-static size_t xhat_bytes_aligned(const secn_ctx* ctx, const secn_conv_plan_t* plan) {
-  return (secn_he_conv2d_workspace(ctx, plan) + 255) & ~(size_t)255;
-}
-
 static int check_gen(const secn_mask_gen_t* g, secn::MaskGen* out) {
   if (!g) return fail(SECN_EINVAL, "NULL mask generator");
   out->seed = g->seed, out->stream = g->stream, out->ct0 = g->ct0;
@@ -601,8 +620,7 @@ static int check_gen(const secn_mask_gen_t* g, secn::MaskGen* out) {
 }
 
 size_t secn_he_conv2d_gen_workspace(const secn_ctx* ctx, const secn_conv_plan_t* plan) {
-  if (!ctx || !plan) return 0;
-  return xhat_bytes_aligned(ctx, plan) + (size_t)plan->M * plan->S * ctx->n * sizeof(uint64_t);
+  return secn_he_conv2d_workspace(ctx, plan);  // the drawn mask goes straight into the encoded-mask buffer
 }
 
 static int he_conv2d_gen_impl(secn_ctx* ctx, uint32_t bits, const secn_conv_plan_t* plan, const void* ct_in,
@@ -612,11 +630,8 @@ static int he_conv2d_gen_impl(secn_ctx* ctx, uint32_t bits, const secn_conv_plan
   if (int st = check_plan(ctx, plan)) return st;
   secn::MaskGen g;
   if (int st = check_gen(gen, &g)) return st;
-  if (!workspace) return fail(SECN_EINVAL, "NULL buffer");
-  if (ws_bytes < secn_he_conv2d_gen_workspace(ctx, plan)) return fail(SECN_EINVAL, "workspace too small");
-  uint64_t* r = reinterpret_cast<uint64_t*>(static_cast<unsigned char*>(workspace) + xhat_bytes_aligned(ctx, plan));
-  return he_conv2d_impl(ctx, bits, plan, -1, ct_in, x0, w_ntt, r, ct_out, y0, workspace, xhat_bytes_aligned(ctx, plan),
-                        stream, true, &g, r);
+  return he_conv2d_impl(ctx, bits, plan, -1, ct_in, x0, w_ntt, nullptr, ct_out, y0, workspace, ws_bytes, stream, true,
+                        &g);
 }
 
 int secn_he_conv2d_gen(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* ct_in, const uint64_t* x0,
@@ -641,9 +656,13 @@ int secn_mask_draw(secn_ctx* ctx, const secn_mask_gen_t* gen, size_t n_ct, uint6
   return e == cudaSuccess ? SECN_OK : cuda_fail(e, "secn_mask_draw");
 }
 
+static size_t conv_ws_aligned(const secn_ctx* ctx, const secn_conv_plan_t* plan) {
+  return (secn_he_conv2d_workspace(ctx, plan) + 255) & ~(size_t)255;
+}
+
 size_t secn_he_conv2d_online_workspace(const secn_ctx* ctx, const secn_conv_plan_t* plan) {
   if (!ctx || !plan) return 0;
-  return xhat_bytes_aligned(ctx, plan) + (size_t)plan->M * plan->G * ctx->L * ctx->n * (ctx->word_bits / 8);
+  return conv_ws_aligned(ctx, plan) + (size_t)plan->M * plan->G * ctx->L * ctx->n * (ctx->word_bits / 8);
 }
 
 static int he_conv2d_online_impl(secn_ctx* ctx, uint32_t bits, const secn_conv_plan_t* plan, const void* ct_in,
@@ -653,9 +672,9 @@ static int he_conv2d_online_impl(secn_ctx* ctx, uint32_t bits, const secn_conv_p
   if (int st = check_plan(ctx, plan)) return st;
   if (!workspace || !kernel) return fail(SECN_EINVAL, "NULL buffer");
   if (ws_bytes < secn_he_conv2d_online_workspace(ctx, plan)) return fail(SECN_EINVAL, "workspace too small");
-  void* w_ntt = static_cast<unsigned char*>(workspace) + xhat_bytes_aligned(ctx, plan);
+  void* w_ntt = static_cast<unsigned char*>(workspace) + conv_ws_aligned(ctx, plan);
   if (int st = preprocess_impl(ctx, bits, plan, kernel, w_ntt, stream)) return st;
-  return he_conv2d_impl(ctx, bits, plan, -1, ct_in, x0, w_ntt, r, ct_out, y0, workspace, xhat_bytes_aligned(ctx, plan),
+  return he_conv2d_impl(ctx, bits, plan, -1, ct_in, x0, w_ntt, r, ct_out, y0, workspace, conv_ws_aligned(ctx, plan),
                         stream);
 }
 
@@ -809,10 +828,11 @@ static int make_ms(const secn_ctx* ctx, uint32_t keep, secn::MsConsts* ms) {
   return SECN_OK;
 }
 
+// X^ [G*S][2][L][N], Y^ [M*S][2][L][N] (the MAC's output, levels 0..7 applied), em [M*S][L][N]
 size_t secn_he_conv2d_lwe_workspace(const secn_ctx* ctx, const secn_conv_plan_t* plan) {
   if (!ctx || !plan) return 0;
   const size_t wb = ctx->word_bits / 8;
-  return xhat_bytes_aligned(ctx, plan) + (size_t)plan->M * plan->S * 2 * ctx->L * ctx->n * wb;
+  return xhat_bytes_aligned(ctx, plan) + (size_t)plan->M * plan->S * 2 * ctx->L * ctx->n * wb + em_bytes(ctx, plan);
 }
 
 static int he_conv2d_lwe_impl(secn_ctx* ctx, uint32_t bits, const secn_conv_plan_t* plan, const void* ct_in,
@@ -823,44 +843,47 @@ static int he_conv2d_lwe_impl(secn_ctx* ctx, uint32_t bits, const secn_conv_plan
   if (int st = check_plan(ctx, plan)) return st;
   secn::MsConsts ms;
   if (int st = make_ms(ctx, keep, &ms)) return st;
-  if (!a_out || !b_out || !workspace) return fail(SECN_EINVAL, "NULL buffer");
+  if (!ct_in || !w_ntt || !a_out || !b_out || !workspace) return fail(SECN_EINVAL, "NULL buffer");
   if (ws_bytes < secn_he_conv2d_lwe_workspace(ctx, plan)) return fail(SECN_EINVAL, "workspace too small");
-  if (y0 && !r) return fail(SECN_EINVAL, "y0 needs the mask r");
-  // X^ then Y^ (levels 0..7 applied) in the workspace; stages 0-1 of the full path
-  void* yhat = static_cast<unsigned char*>(workspace) + xhat_bytes_aligned(ctx, plan);
-  if (int st = he_conv2d_impl(ctx, bits, plan, 0, ct_in, x0, w_ntt, r, yhat, nullptr, workspace,
-                              xhat_bytes_aligned(ctx, plan), stream, false, gen, const_cast<uint64_t*>(r)))
-    return st;
-  if (int st = he_conv2d_impl(ctx, bits, plan, 1, ct_in, x0, w_ntt, r, yhat, nullptr, workspace,
-                              xhat_bytes_aligned(ctx, plan), stream, /*chained=*/true))
-    return st;
+  if (y0 && !r && !gen) return fail(SECN_EINVAL, "y0 needs the mask r");
+  if (((uintptr_t)workspace | (uintptr_t)ct_in | (uintptr_t)w_ntt | (uintptr_t)r) & 15)
+    return fail(SECN_EINVAL, "buffers must be 16-byte aligned");
+  if (plan->G > 32u) return fail(SECN_EUNSUPPORTED, "G=%u input channel groups too many", plan->G);
   DeviceGuard guard(ctx->device);
-  if (int st = check_range(ctx, r, (size_t)plan->M * plan->S * ctx->n, 1, (cudaStream_t)stream, "secn_he_conv2d_lwe r"))
-    return st;
-  cudaError_t e = secn::launch_ntt_inv_tail_lwe(ctx->dc, ms, yhat, (size_t)plan->M * plan_dev(plan).sn, r, a_out,
-                                                b_out, y0, plan_dev(plan), (cudaStream_t)stream, true);
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t n_in = (size_t)plan->G * plan->S, n_out = (size_t)plan->M * plan->S, N = ctx->n;
+  const secn::PlanDev pd = plan_dev(plan);
+  const size_t n_act = (size_t)plan->M * pd.sn;
+  if (int st = check_range(ctx, ct_in, n_in * 2 * ctx->L * N, 0, s, "secn_he_conv2d_lwe ct_in")) return st;
+  if (int st = check_range(ctx, x0, n_in * N, 1, s, "secn_he_conv2d_lwe x0")) return st;
+  if (int st = check_range(ctx, r, n_out * N, 1, s, "secn_he_conv2d_lwe r")) return st;
+  // workspace: X^, then Y^ (levels 0..7 applied), then the encoded mask
+  unsigned char* ws = static_cast<unsigned char*>(workspace);
+  void* yhat = ws + xhat_bytes_aligned(ctx, plan);
+  void* em = (r || gen) ? ws + xhat_bytes_aligned(ctx, plan) + n_out * 2 * ctx->L * N * (ctx->word_bits / 8) : nullptr;
+  cudaError_t e = secn::launch_ntt_fwd(ctx->dc, ct_in, workspace, n_in * 2 * ctx->L, x0, s);  // A6 + A1
+  if (e == cudaSuccess && em) {
+    const secn::MaskGen g = gen ? *gen : secn::MaskGen{0, 0, 0};
+    e = secn::launch_mask_encode(ctx->dc, pd, n_act, gen ? nullptr : r, g, em, y0, s);  // A7 (+A8)
+  }
+  if (e == cudaSuccess) e = secn::launch_mac(ctx->dc, pd, workspace, w_ntt, yhat, s, true);  // A4 + INTT 0..7
+  if (e == cudaSuccess)  // INTT 8.. + mask + modulus switch + extraction
+    e = secn::launch_ntt_inv_tail_lwe(ctx->dc, ms, yhat, n_act, nullptr, a_out, b_out, nullptr, pd, s, true, em);
   return e == cudaSuccess ? SECN_OK : cuda_fail(e, "secn_he_conv2d_lwe");
 }
 
 size_t secn_he_conv2d_lwe_gen_workspace(const secn_ctx* ctx, const secn_conv_plan_t* plan) {
-  if (!ctx || !plan) return 0;
-  return ((secn_he_conv2d_lwe_workspace(ctx, plan) + 255) & ~(size_t)255) +
-         (size_t)plan->M * plan->S * ctx->n * sizeof(uint64_t);
+  return secn_he_conv2d_lwe_workspace(ctx, plan);  // the drawn mask goes straight into the encoded-mask buffer
 }
 
 static int he_conv2d_lwe_gen_impl(secn_ctx* ctx, uint32_t bits, const secn_conv_plan_t* plan, const void* ct_in,
                                   const uint64_t* x0, const void* w_ntt, const secn_mask_gen_t* gen, uint32_t keep,
                                   void* a_out, void* b_out, uint64_t* y0, void* workspace, size_t ws_bytes,
                                   void* stream) {
-  if (int st = check_ctx(ctx, bits)) return st;
-  if (int st = check_plan(ctx, plan)) return st;
   secn::MaskGen g;
   if (int st = check_gen(gen, &g)) return st;
-  if (!workspace) return fail(SECN_EINVAL, "NULL buffer");
-  if (ws_bytes < secn_he_conv2d_lwe_gen_workspace(ctx, plan)) return fail(SECN_EINVAL, "workspace too small");
-  const size_t lw = (secn_he_conv2d_lwe_workspace(ctx, plan) + 255) & ~(size_t)255;
-  uint64_t* r = reinterpret_cast<uint64_t*>(static_cast<unsigned char*>(workspace) + lw);
-  return he_conv2d_lwe_impl(ctx, bits, plan, ct_in, x0, w_ntt, r, keep, a_out, b_out, y0, workspace, lw, stream, &g);
+  return he_conv2d_lwe_impl(ctx, bits, plan, ct_in, x0, w_ntt, nullptr, keep, a_out, b_out, y0, workspace, ws_bytes,
+                            stream, &g);
 }
 
 int secn_he_conv2d_lwe_gen(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* ct_in, const uint64_t* x0,

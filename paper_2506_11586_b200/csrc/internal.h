@@ -122,13 +122,14 @@ cudaError_t launch_ntt_fwd(const DevConsts& c, const void* in, void* out, size_t
 cudaError_t launch_ntt_inv(const DevConsts& c, void* polys, size_t n_limb_polys, cudaStream_t s);
 // levels 8.. of the inverse NTT (+N^-1, +mask) after launch_mac applied levels 0..7; if
 // y0 != NULL also the server share (A8) for plan pl
+// em != NULL: the mask arrives encoded (k_mask_encode's em [rows][L][N]); r and y0 are then unused
 cudaError_t launch_ntt_inv_tail(const DevConsts& c, void* polys, size_t n_limb_polys, const uint64_t* r, uint64_t* y0,
-                                const PlanDev& pl, cudaStream_t s, bool chained);
+                                const PlanDev& pl, cudaStream_t s, bool chained, const void* em = nullptr);
 // The whole layer after the forward NTT in one kernel (32-bit limbs, N = 4096): A4 MAC, the full
 // inverse NTT, A7 mask, A8 share. fused_applies says whether the layer takes this path.
 bool fused_applies(const DevConsts& c, const PlanDev& p);
 cudaError_t launch_layer_fused(const DevConsts& c, const PlanDev& p, const void* xhat, const void* w, void* y,
-                               const uint64_t* r, uint64_t* y0, cudaStream_t s, bool chained);
+                               const uint64_t* r, uint64_t* y0, cudaStream_t s, bool chained, const void* em);
 // NTT-domain MAC (A4) followed by inverse-NTT levels 0..7 of its outputs (lazy GS domain)
 cudaError_t launch_mac(const DevConsts& c, const PlanDev& p, const void* xhat, const void* w, void* y, cudaStream_t s,
                        bool chained);
@@ -138,11 +139,16 @@ cudaError_t launch_pack_weights(const DevConsts& c, const PlanDev& p, const uint
 // designated coefficients of plan pl (conv or fc), and y0 (if not NULL) the server share.
 cudaError_t launch_ntt_inv_tail_lwe(const DevConsts& c, const MsConsts& ms, const void* polys, size_t n_ct,
                                     const uint64_t* r, void* a_out, void* b_out, uint64_t* y0, const PlanDev& pl,
-                                    cudaStream_t s, bool chained);
+                                    cudaStream_t s, bool chained, const void* em = nullptr);
 // fc weights W [n_o][n_i] -> mirrored polys [M][G][L][N] (coefficient domain, zero-filled first)
 cudaError_t launch_pack_fc_weights(const DevConsts& c, const PlanDev& p, const uint64_t* W, void* w, cudaStream_t s);
 // r [n_ct][N] from the generator (reading R17); launched with PDL, safe to chain (see k_mask_draw)
 cudaError_t launch_mask_draw(const DevConsts& c, const MaskGen& g, size_t n_ct, uint64_t* r, cudaStream_t s);
+// em [rows][L][N] (word size) = enc_j(r) of the call's n_act output ciphertexts (rows slice_ct),
+// r from `r` (device) or, if r == NULL, drawn by g; y0 (may be NULL) = -r mod t at the designated
+// outputs. Chains like launch_mask_draw (run it right after the forward NTT).
+cudaError_t launch_mask_encode(const DevConsts& c, const PlanDev& p, size_t n_act, const uint64_t* r, const MaskGen& g,
+                               void* em, uint64_t* y0, cudaStream_t s);
 cudaError_t launch_enc_add(const DevConsts& c, void* ct, const uint64_t* v, size_t n, cudaStream_t s);
 cudaError_t launch_extract_share(const DevConsts& c, const PlanDev& p, const uint64_t* r, uint64_t* y0,
                                  cudaStream_t s);

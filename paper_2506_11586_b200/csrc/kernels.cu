@@ -55,10 +55,9 @@ struct EncK {
         tinv_hi_p(c.tinv_hi_p[j]), tbits(c.t_bits) {}
 };
 
+// the limb-dependent half of enc_j(v), from rho = (Q mod t) v mod t and up = [rho >= t/2]
 template <class A>
-__device__ __forceinline__ typename A::W enc_mod(uint64_t v, const EncK& k) {
-  const uint64_t rho = (k.qmt * v) & ((1ull << k.tbits) - 1);
-  const uint32_t up = rho >= (1ull << (k.tbits - 1));
+__device__ __forceinline__ typename A::W enc_limb(uint64_t rho, uint32_t up, const EncK& k) {
   if constexpr (sizeof(typename A::W) == 8) {
     const uint64_t a = shoup(rho, k.tinv, k.tinv_p, k.q);  // [0, 2q)
     const uint64_t e = 2 * k.q - a + up;                     // [1, 2q + 1]
@@ -71,6 +70,12 @@ __device__ __forceinline__ typename A::W enc_mod(uint64_t v, const EncK& k) {
     e = csub32(e, 2 * q);
     return csub32(csub32(e, q), q);
   }
+}
+
+template <class A>
+__device__ __forceinline__ typename A::W enc_mod(uint64_t v, const EncK& k) {
+  const uint64_t rho = (k.qmt * v) & ((1ull << k.tbits) - 1);
+  return enc_limb<A>(rho, rho >= (1ull << (k.tbits - 1)), k);
 }
 
 // CTAs per SM the NTT kernels are compiled for (register cap 65536 / (N/16 threads * this)). N =
@@ -378,7 +383,8 @@ __device__ __forceinline__ void write_server_share_ct(const uint64_t* __restrict
 template <class A, int LOGN>
 __global__ void __launch_bounds__((1 << LOGN) / 16, sizeof(typename A::W) == 4 && LOGN == 12 ? 4 : ntt_min_blocks<A, LOGN, 1>())
     k_ntt_inv_tail(typename A::W* polys, const __grid_constant__ DevConsts c, const uint64_t* __restrict__ r,
-                   uint64_t* __restrict__ y0, const __grid_constant__ PlanDev pl, size_t ct0, int r_early) {
+                   uint64_t* __restrict__ y0, const __grid_constant__ PlanDev pl, size_t ct0, int r_early,
+                   const typename A::W* __restrict__ emb) {
   using W = typename A::W;
   constexpr int N = 1 << LOGN;
   constexpr int LS = 8;
@@ -395,11 +401,20 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, sizeof(typename A::W) == 4 &
   const typename A::Tw ninv = Tab<A>::pair(c.ninv_mac[j], c.ninv_mac_p[j]);  // inputs are k_mac outputs
   const typename A::Tw wl = Tab<A>::pair(c.wlast_mac[j], c.wlast_mac_p[j]);
   const EncK ek(c, j);
-  const bool mask = r != nullptr && (pi & 1);
+  const bool mask = (r != nullptr || emb != nullptr) && (pi & 1);
   W em[16];
   // the mask is an input of the call: with r_early (the preceding kernel is this call's MAC, which
-  // never writes it) it is loaded and encoded before the dependency wait, overlapping the MAC's tail
+  // never writes it) it is loaded and encoded before the dependency wait, overlapping the MAC's tail.
+  // emb != NULL: the call's k_mask_encode already encoded it (em[ct][j][e]; chained, so early too)
   const auto load_mask = [&] {
+    if (emb != nullptr) {
+      const W* es = emb + (((pi >> 1) + ct0) * c.L + j) * N;
+#pragma unroll
+      for (int k = 0; k < RL::NT; ++k)
+#pragma unroll
+        for (int i = 0; i < RL::GK; ++i) em[k * RL::GK + i] = es[RL::addr(k, i)];
+      return;
+    }
     const uint64_t* rs = r + (pi >> 1) * N;
 #pragma unroll
     for (int k = 0; k < RL::NT; ++k)
@@ -441,16 +456,20 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, sizeof(typename A::W) == 4 &
   // A8 fused (secn_he_conv2d_ex): the server's output share y0 = -r mod t at the designated
   // coefficients of this ciphertext (one CTA per ciphertext does it: limb 0, b component). It
   // depends on r only, so it never waits on the transform; it saves a launch per layer.
-  if (y0 != nullptr && mask && j == 0) write_server_share_ct(r + (pi >> 1) * N, y0, pl, (uint32_t)(ct0 + (pi >> 1)), c.t_bits);
+  if (y0 != nullptr && r != nullptr && mask && j == 0)
+    write_server_share_ct(r + (pi >> 1) * N, y0, pl, (uint32_t)(ct0 + (pi >> 1)), c.t_bits);
 }
 
 // The same tail at N = 4096 with both components of one (ciphertext, limb) per CTA: the pair
 // shares the twiddles and the index arithmetic and every thread keeps 32 independent words in
 // flight (the 16-word version is latency bound on small layers). Mask and A8 on component b.
-template <class A, bool R_EARLY>
+// MS: how the mask arrives -- 0: r, loaded and encoded after the dependency wait (stage calls);
+// 1: r, before the wait (chained); 2: already encoded by k_mask_encode, em[ct][j][e] (chained full calls).
+template <class A, int MS>
 __global__ void __launch_bounds__(256, 4)
     k_ntt_inv_tail2(typename A::W* polys, const __grid_constant__ DevConsts c, const uint64_t* __restrict__ r,
-                    uint64_t* __restrict__ y0, const __grid_constant__ PlanDev pl, size_t ct0) {
+                    uint64_t* __restrict__ y0, const __grid_constant__ PlanDev pl, size_t ct0,
+                    const typename A::W* __restrict__ emb) {
   using W = typename A::W;
   constexpr int LOGN = 12, N = 1 << LOGN, LS = 8;
   using RS = GsRound<LOGN, LS>;
@@ -462,21 +481,27 @@ __global__ void __launch_bounds__(256, 4)
   const typename A::Tw ninv = Tab<A>::pair(c.ninv_mac[j], c.ninv_mac_p[j]);  // inputs are k_mac outputs
   const typename A::Tw wl = Tab<A>::pair(c.wlast_mac[j], c.wlast_mac_p[j]);
   const EncK ek(c, j);
-  const bool mask = r != nullptr;
-  const uint64_t* rs = mask ? r + ct * N : nullptr;
+  const bool mask = MS == 2 ? emb != nullptr : r != nullptr;
+  const uint64_t* rs = r != nullptr ? r + ct * N : nullptr;
   W em[16];
   const auto load_mask = [&] {  // before the wait only when chained (see k_ntt_inv_tail)
-    uint64_t rv[16];
+    if constexpr (MS == 2) {
+      const W* es = emb + ((ct + ct0) * c.L + j) * N;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) rv[i] = __ldg(&rs[RS::addr(0, i)]);
+      for (int i = 0; i < 16; ++i) em[i] = es[RS::addr(0, i)];
+    } else {
+      uint64_t rv[16];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) em[i] = enc_mod<A>(rv[i], ek);
+      for (int i = 0; i < 16; ++i) rv[i] = __ldg(&rs[RS::addr(0, i)]);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) em[i] = enc_mod<A>(rv[i], ek);
+    }
   };
-  if (mask && R_EARLY) load_mask();
+  if (mask && MS == 1) load_mask();
   typename A::Tw tws[15];
   gs_twiddles<A, LOGN, LS>(tws, tw);
   pdl_wait();  // the polys are produced by the preceding kernel (the MAC)
-  if (mask && !R_EARLY) load_mask();
+  if (mask && MS == 0) load_mask();
   W* buf[2] = {polys + ((ct * 2) * c.L + j) * N, polys + ((ct * 2 + 1) * c.L + j) * N};
   W x[2][16];
 #pragma unroll
@@ -485,6 +510,7 @@ __global__ void __launch_bounds__(256, 4)
     for (int i = 0; i < 16; ++i) x[pp][i] = buf[pp][RS::addr(0, i)];
   gs_compute<A, LOGN, LS, 2>(x, tws, q, qb, ninv, wl);
   pdl_trigger();
+  if (mask && MS == 2) load_mask();  // 4-byte words: loaded here, their latency overlaps the a stores
 #pragma unroll
   for (int i = 0; i < 16; ++i) buf[0][RS::addr(0, i)] = A::canon_gs(x[0][i], q);
 #pragma unroll
@@ -496,7 +522,7 @@ __global__ void __launch_bounds__(256, 4)
     }
     buf[1][RS::addr(0, i)] = v;
   }
-  if (y0 != nullptr && mask && j == 0) write_server_share_ct(rs, y0, pl, (uint32_t)(ct0 + ct), c.t_bits);
+  if (MS != 2 && y0 != nullptr && mask && j == 0) write_server_share_ct(rs, y0, pl, (uint32_t)(ct0 + ct), c.t_bits);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -948,7 +974,7 @@ __global__ void __launch_bounds__(FUSED_THREADS + 32, 2)
     k_layer_fused(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmw,
                   uint32_t* __restrict__ y, const uint64_t* __restrict__ r, uint64_t* __restrict__ y0,
                   const __grid_constant__ DevConsts c, const __grid_constant__ PlanDev pl, int n_sg, int NS, int GC,
-                  int n_pre) {
+                  int n_pre, const uint32_t* __restrict__ emb) {
   using AR = Arith32;
   using W = uint32_t;
   using Tw = uint2;
@@ -1086,7 +1112,11 @@ __global__ void __launch_bounds__(FUSED_THREADS + 32, 2)
     const bool live = rr < rows && sl < ns;
     const size_t ct = (size_t)(mb + rr) * S + s0 + sl;
     W em[16];  // enc_j of the mask words (encoded before the polys are loaded: fewer live registers)
-    if (live && r != nullptr) {
+    const bool masked = r != nullptr || emb != nullptr;
+    if (live && emb != nullptr) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) em[i] = emb[(ct * L + j) * N + RL::addr(0, i)];
+    } else if (live && r != nullptr) {
       uint64_t rv[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i) rv[i] = __ldg(&r[ct * N + RL::addr(0, i)]);
@@ -1106,14 +1136,15 @@ __global__ void __launch_bounds__(FUSED_THREADS + 32, 2)
       for (int i = 0; i < 16; ++i) {
         ya[RL::addr(0, i)] = AR::canon_gs(x[0][i], q);
         W v = AR::canon_gs(x[1][i], q);
-        if (r != nullptr) {
+        if (masked) {
           v += em[i];
           v = v >= q ? v - q : v;
         }
         yb[RL::addr(0, i)] = v;
       }
-      // A8: the server's share y0 = -r mod t at the designated coefficients (limb 0's CTA)
-      if (y0 != nullptr && r != nullptr && j == 0) {
+      // A8: the server's share y0 = -r mod t at the designated coefficients (limb 0's CTA; with em,
+      // k_mask_encode wrote it)
+      if (y0 != nullptr && r != nullptr && emb == nullptr && j == 0) {
         const uint32_t sidx = (uint32_t)(ct % S), bh = sidx / pl.nbw, bw = sidx % pl.nbw;
         const uint32_t dh = pl.Hw - pl.kh + 1, dw = pl.Ww - pl.kw + 1;
         for (uint32_t d = tid; d < dh * dw; d += FUSED_THREADS) {
@@ -1181,7 +1212,8 @@ template <class A, int ND>  // ND = L - Lk dropped limbs
 __global__ void __launch_bounds__(LWE_G * SECN_MAX_LIMBS)
     k_ntt_inv_tail_lwe(const typename A::W* __restrict__ polys, const __grid_constant__ DevConsts c,
                        const __grid_constant__ MsConsts ms, const uint64_t* __restrict__ r, typename A::W* a_out,
-                       typename A::W* b_out, uint64_t* y0, const __grid_constant__ PlanDev pl, int r_early) {
+                       typename A::W* b_out, uint64_t* y0, const __grid_constant__ PlanDev pl, int r_early,
+                       const typename A::W* __restrict__ emb) {
   using W = typename A::W;
   constexpr int LOGN = 12, N = 1 << LOGN;
   using RS = GsRound<LOGN, 8>;
@@ -1190,8 +1222,8 @@ __global__ void __launch_bounds__(LWE_G * SECN_MAX_LIMBS)
   const size_t ct = slice_ct(pl, (uint32_t)(blockIdx.x >> 2)), pi = 2 * ct + ((blockIdx.x >> 1) & 1);
   const uint32_t o = (blockIdx.x & 1) * LWE_G + threadIdx.x % LWE_G;  // radix-16 task: coefficients o + 256 i
   const int j = threadIdx.x / LWE_G;                                   // this group's limb
-  const bool isb = pi & 1, mask = isb && r != nullptr;
-  const uint64_t* rs = mask ? r + ct * N : nullptr;
+  const bool isb = pi & 1, mask = isb && (r != nullptr || emb != nullptr);
+  const uint64_t* rs = isb && r != nullptr ? r + ct * N : nullptr;
   const int L = (int)c.L, Lk = L - ND;
   const W q = (W)c.q[j], qb = A::bound(q);
   typename A::Tw tws[15];
@@ -1214,12 +1246,15 @@ __global__ void __launch_bounds__(LWE_G * SECN_MAX_LIMBS)
   }
   const EncK ek(c, j);
   W em[16];
-  if (mask && work && r_early) {
+  if (mask && work && emb != nullptr) {  // encoded by the call's k_mask_encode
+#pragma unroll
+    for (int i = 0; i < 16; ++i) em[i] = emb[(ct * L + j) * N + o + 256 * i];
+  } else if (mask && work && r_early) {
 #pragma unroll
     for (int i = 0; i < 16; ++i) em[i] = enc_mod<A>(__ldg(&rs[o + 256 * i]), ek);
   }
   pdl_wait();
-  if (mask && work && !r_early) {
+  if (mask && work && emb == nullptr && !r_early) {
 #pragma unroll
     for (int i = 0; i < 16; ++i) em[i] = enc_mod<A>(__ldg(&rs[o + 256 * i]), ek);
   }
@@ -1271,7 +1306,7 @@ __global__ void __launch_bounds__(LWE_G * SECN_MAX_LIMBS)
       a_out[(ct * Lk + j) * N + e] = out;
     } else {
       b_out[(size_t)oi * Lk + j] = out;
-      if (j == 0 && y0 != nullptr && mask) {
+      if (j == 0 && y0 != nullptr && rs != nullptr) {  // (with em, k_mask_encode wrote y0)
         const uint64_t tm = (1ull << c.t_bits) - 1;
         y0[oi] = (tm + 1 - rs[e]) & tm;
       }
@@ -1374,6 +1409,72 @@ __global__ void k_mask_draw(uint64_t* __restrict__ r, MaskGen g, size_t n_pairs,
     const uint4 w = philox4x32_10(make_uint4(pe, g.ct0 + ct, g.stream, 0u), (uint32_t)g.seed, (uint32_t)(g.seed >> 32));
     reinterpret_cast<ulonglong2*>(r)[i] =
         make_ulonglong2((((uint64_t)w.y << 32) | w.x) & tm, (((uint64_t)w.w << 32) | w.z) & tm);
+  }
+  pdl_wait();
+}
+
+// A7 prepared once per layer call (the full calls; the stage calls encode r in the tail): the
+// encoded mask em[ct][j][e] = enc_j(r[ct][e]) of every output ciphertext the call computes, for
+// every limb, with r read from the caller's buffer or drawn from the generator (reading R17); and
+// the server's share y0 = -r mod t at the designated outputs (A8). The limb-independent half of
+// enc (rho, up) is computed once per coefficient. Launched right after the forward NTT with the
+// same chaining as k_mask_draw (it reads nothing the NTT writes; it waits for it at the end), so
+// it runs on the SMs the forward NTT leaves idle, and the INTT tails only add em_j (4 or 8 bytes
+// per limb-coefficient) instead of reading and encoding r (8 bytes per coefficient, per limb).
+template <class A>
+__global__ void __launch_bounds__(256) k_mask_encode(typename A::W* __restrict__ em, uint64_t* __restrict__ y0,
+                                                     const uint64_t* __restrict__ r, MaskGen g,
+                                                     const __grid_constant__ DevConsts c,
+                                                     const __grid_constant__ PlanDev pl, uint32_t n_act) {
+  using W = typename A::W;
+  pdl_trigger();
+  const uint32_t N = 1u << c.log_n, half = N >> 1, L = c.L;
+  const uint64_t tm = (1ull << c.t_bits) - 1, thalf = 1ull << (c.t_bits - 1);
+  const size_t n_pairs = (size_t)n_act * half, stride = (size_t)gridDim.x * blockDim.x;
+  const auto mask_pair = [&](uint32_t ct, uint32_t pe, uint64_t& v0, uint64_t& v1) {
+    if (r != nullptr) {
+      const ulonglong2 rr = reinterpret_cast<const ulonglong2*>(r + (size_t)ct * N)[pe];
+      v0 = rr.x, v1 = rr.y;
+    } else {
+      const uint4 w = philox4x32_10(make_uint4(pe, g.ct0 + ct, g.stream, 0u), (uint32_t)g.seed, (uint32_t)(g.seed >> 32));
+      v0 = (((uint64_t)w.y << 32) | w.x) & tm, v1 = (((uint64_t)w.w << 32) | w.z) & tm;
+    }
+  };
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n_pairs; i += stride) {
+    const uint32_t ct = slice_ct(pl, (uint32_t)(i / half)), pe = (uint32_t)(i % half);
+    uint64_t v0, v1;
+    mask_pair(ct, pe, v0, v1);
+    const uint64_t rho0 = (c.qmt * v0) & tm, rho1 = (c.qmt * v1) & tm;
+    const uint32_t up0 = rho0 >= thalf, up1 = rho1 >= thalf;
+    for (uint32_t j = 0; j < L; ++j) {
+      const EncK ek(c, (int)j);
+      W* dst = em + ((size_t)ct * L + j) * N + 2 * pe;
+      const W e0 = enc_limb<A>(rho0, up0, ek), e1 = enc_limb<A>(rho1, up1, ek);
+      if constexpr (sizeof(W) == 4)
+        *reinterpret_cast<uint2*>(dst) = make_uint2(e0, e1);
+      else
+        *reinterpret_cast<ulonglong2*>(dst) = make_ulonglong2(e0, e1);
+    }
+  }
+  if (y0 != nullptr) {  // A8 at the designated outputs of the call's output ciphertexts
+    const size_t total = pl.kind == 1 ? (size_t)pl.no : (size_t)pl.M * pl.OH * pl.OW;
+    for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total; idx += stride) {
+      uint32_t ct, e;
+      if (pl.kind == 1) {  // fc: y[m nob + d] at coefficient d nib + nib - 1 of output ct m
+        ct = (uint32_t)(idx / pl.nob), e = (uint32_t)(idx % pl.nob) * pl.nib + pl.nib - 1;
+      } else {
+        const uint32_t ox = idx % pl.OW, oy = (idx / pl.OW) % pl.OH, m = (uint32_t)(idx / ((size_t)pl.OW * pl.OH));
+        const uint32_t py = oy * pl.sh, px = ox * pl.sh;
+        const uint32_t bh = py / (pl.Hw - pl.kh + 1), ii = py % (pl.Hw - pl.kh + 1);
+        const uint32_t bw = px / (pl.Ww - pl.kw + 1), jj = px % (pl.Ww - pl.kw + 1);
+        const uint32_t s = bh * pl.nbw + bw;
+        if (s < pl.s0 || s >= pl.s0 + pl.sn) continue;  // another call's spatial slice
+        ct = m * pl.S + s, e = pl.O + ii * pl.Ww + jj;
+      }
+      uint64_t v0, v1;
+      mask_pair(ct, e >> 1, v0, v1);
+      y0[idx] = (tm + 1 - ((e & 1) ? v1 : v0)) & tm;
+    }
   }
   pdl_wait();
 }
@@ -1516,7 +1617,7 @@ static cudaError_t ntt_inv_t(const DevConsts& c, void* polys, size_t P, cudaStre
 
 template <class A, int LOGN>
 static cudaError_t ntt_inv_tail_t(const DevConsts& c, void* polys, size_t P, const uint64_t* r, uint64_t* y0,
-                                  const PlanDev& pl, cudaStream_t s, bool chained) {
+                                  const PlanDev& pl, cudaStream_t s, bool chained, const void* emv) {
   using W = typename A::W;
   constexpr int N = 1 << LOGN;
   const size_t smem = LOGN > 12 ? smem_words<LOGN>() * sizeof(W) : 0;  // opted in by init_device
@@ -1525,22 +1626,27 @@ static cudaError_t ntt_inv_tail_t(const DevConsts& c, void* polys, size_t P, con
   const size_t n_polys = P / c.L;
   for (size_t p0 = 0; p0 < n_polys; p0 += pmax) {
     const size_t np = n_polys - p0 < pmax ? n_polys - p0 : pmax;
+    // with an s-slice the chunk's rows start at row p0 / 2 (rows >= active index, see slice_ct)
     W* buf = static_cast<W*>(polys) + p0 * c.L * N;
     const uint64_t* rs = r ? r + p0 / 2 * N : nullptr;
+    const W* em = static_cast<const W*>(emv);  // indexed by the global row in the kernels
     cudaError_t e;
     if constexpr (LOGN == 12 && sizeof(W) == 4) {
       if (c.tune.tail1)
         e = launch_pdl(c, k_ntt_inv_tail<A, LOGN>, dim3((unsigned)(np * c.L)), dim3(N / 16), smem, s, buf, c, rs, y0,
-                       pl, p0 / 2, r_early);
-      else if (r_early)  // both components of a (ciphertext, limb) per CTA
-        e = launch_pdl(c, k_ntt_inv_tail2<A, true>, dim3((unsigned)(np / 2 * c.L)), dim3(256), 0, s, buf, c, rs, y0,
-                       pl, p0 / 2);
+                       pl, p0 / 2, r_early, em);
+      else if (em != nullptr)  // both components of a (ciphertext, limb) per CTA
+        e = launch_pdl(c, k_ntt_inv_tail2<A, 2>, dim3((unsigned)(np / 2 * c.L)), dim3(256), 0, s, buf, c, rs, y0, pl,
+                       p0 / 2, em);
+      else if (r_early)
+        e = launch_pdl(c, k_ntt_inv_tail2<A, 1>, dim3((unsigned)(np / 2 * c.L)), dim3(256), 0, s, buf, c, rs, y0, pl,
+                       p0 / 2, em);
       else
-        e = launch_pdl(c, k_ntt_inv_tail2<A, false>, dim3((unsigned)(np / 2 * c.L)), dim3(256), 0, s, buf, c, rs, y0,
-                       pl, p0 / 2);
+        e = launch_pdl(c, k_ntt_inv_tail2<A, 0>, dim3((unsigned)(np / 2 * c.L)), dim3(256), 0, s, buf, c, rs, y0, pl,
+                       p0 / 2, em);
     } else {
       e = launch_pdl(c, k_ntt_inv_tail<A, LOGN>, dim3((unsigned)(np * c.L)), dim3(N / 16), smem, s, buf, c, rs, y0, pl,
-                     p0 / 2, r_early);
+                     p0 / 2, r_early || em != nullptr ? 1 : 0, em);
     }
     if (e != cudaSuccess) return e;
   }
@@ -1548,19 +1654,19 @@ static cudaError_t ntt_inv_tail_t(const DevConsts& c, void* polys, size_t P, con
 }
 
 cudaError_t launch_ntt_inv_tail(const DevConsts& c, void* polys, size_t P, const uint64_t* r, uint64_t* y0,
-                                const PlanDev& pl, cudaStream_t s, bool chained) {
+                                const PlanDev& pl, cudaStream_t s, bool chained, const void* em) {
   if (P == 0) return cudaSuccess;
   if (c.word_bits == 64) {
     switch (c.log_n) {
-      case 12: return ntt_inv_tail_t<Arith64, 12>(c, polys, P, r, y0, pl, s, chained);
-      case 13: return ntt_inv_tail_t<Arith64, 13>(c, polys, P, r, y0, pl, s, chained);
-      case 14: return ntt_inv_tail_t<Arith64, 14>(c, polys, P, r, y0, pl, s, chained);
+      case 12: return ntt_inv_tail_t<Arith64, 12>(c, polys, P, r, y0, pl, s, chained, em);
+      case 13: return ntt_inv_tail_t<Arith64, 13>(c, polys, P, r, y0, pl, s, chained, em);
+      case 14: return ntt_inv_tail_t<Arith64, 14>(c, polys, P, r, y0, pl, s, chained, em);
     }
   } else {
     switch (c.log_n) {
-      case 12: return ntt_inv_tail_t<Arith32, 12>(c, polys, P, r, y0, pl, s, chained);
-      case 13: return ntt_inv_tail_t<Arith32, 13>(c, polys, P, r, y0, pl, s, chained);
-      case 14: return ntt_inv_tail_t<Arith32, 14>(c, polys, P, r, y0, pl, s, chained);
+      case 12: return ntt_inv_tail_t<Arith32, 12>(c, polys, P, r, y0, pl, s, chained, em);
+      case 13: return ntt_inv_tail_t<Arith32, 13>(c, polys, P, r, y0, pl, s, chained, em);
+      case 14: return ntt_inv_tail_t<Arith32, 14>(c, polys, P, r, y0, pl, s, chained, em);
     }
   }
   return cudaErrorInvalidValue;
@@ -1841,7 +1947,7 @@ static size_t fused_smem(const DevConsts& c, int G, int* NS_out, int* GC_out) {
 
 template <int SG, int MT>
 static cudaError_t fused_t(const DevConsts& c, const PlanDev& p, const void* xhat, const void* w, void* y,
-                           const uint64_t* r, uint64_t* y0, cudaStream_t s, bool chained) {
+                           const uint64_t* r, uint64_t* y0, cudaStream_t s, bool chained, const void* em) {
   constexpr int N = 4096;
   int NS = 0, GC = 0;
   const size_t smem = fused_smem<SG, MT>(c, (int)p.G, &NS, &GC);
@@ -1860,7 +1966,8 @@ static cudaError_t fused_t(const DevConsts& c, const PlanDev& p, const void* xha
     return cudaErrorInvalidValue;
   const int n_pre = chained ? c.tune.mac_pre : 0;
   cudaError_t e = launch_pdl(c, k_layer_fused<SG, MT>, dim3((unsigned)(n_mb * n_sg), c.L), dim3(FUSED_THREADS + 32),
-                             smem, s, tmx, tmw, static_cast<uint32_t*>(y), r, y0, c, p, n_sg, NS, GC, n_pre);
+                             smem, s, tmx, tmw, static_cast<uint32_t*>(y), r, y0, c, p, n_sg, NS, GC, n_pre,
+                             static_cast<const uint32_t*>(em));
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
@@ -1873,14 +1980,14 @@ bool fused_applies(const DevConsts& c, const PlanDev& p) {
 }
 
 cudaError_t launch_layer_fused(const DevConsts& c, const PlanDev& p, const void* xhat, const void* w, void* y,
-                               const uint64_t* r, uint64_t* y0, cudaStream_t s, bool chained) {
+                               const uint64_t* r, uint64_t* y0, cudaStream_t s, bool chained, const void* em) {
   int sg = c.tune.fused_sg > 0 ? c.tune.fused_sg : 1;
   int mt = c.tune.fused_mt > 0 ? c.tune.fused_mt : 2;
-  if (sg == 1 && mt == 1) return fused_t<1, 1>(c, p, xhat, w, y, r, y0, s, chained);
-  if (sg == 1 && mt == 2) return fused_t<1, 2>(c, p, xhat, w, y, r, y0, s, chained);
-  if (sg == 1 && mt == 4) return fused_t<1, 4>(c, p, xhat, w, y, r, y0, s, chained);
-  if (sg == 2 && mt == 1) return fused_t<2, 1>(c, p, xhat, w, y, r, y0, s, chained);
-  if (sg == 2 && mt == 2) return fused_t<2, 2>(c, p, xhat, w, y, r, y0, s, chained);
+  if (sg == 1 && mt == 1) return fused_t<1, 1>(c, p, xhat, w, y, r, y0, s, chained, em);
+  if (sg == 1 && mt == 2) return fused_t<1, 2>(c, p, xhat, w, y, r, y0, s, chained, em);
+  if (sg == 1 && mt == 4) return fused_t<1, 4>(c, p, xhat, w, y, r, y0, s, chained, em);
+  if (sg == 2 && mt == 1) return fused_t<2, 1>(c, p, xhat, w, y, r, y0, s, chained, em);
+  if (sg == 2 && mt == 2) return fused_t<2, 2>(c, p, xhat, w, y, r, y0, s, chained, em);
   return cudaErrorInvalidValue;
 }
 
@@ -1917,14 +2024,14 @@ cudaError_t launch_pack_fc_weights(const DevConsts& c, const PlanDev& p, const u
 
 cudaError_t launch_ntt_inv_tail_lwe(const DevConsts& c, const MsConsts& ms, const void* polys, size_t n_ct,
                                     const uint64_t* r, void* a_out, void* b_out, uint64_t* y0, const PlanDev& pl,
-                                    cudaStream_t s, bool chained) {
+                                    cudaStream_t s, bool chained, const void* em) {
   if (n_ct == 0) return cudaSuccess;
   if (c.log_n != 12 || 4 * n_ct > 0x7fffffffull) return cudaErrorInvalidValue;
   const dim3 grid((unsigned)(4 * n_ct)), block(LWE_G * c.L);  // (ct, component, half) x limbs
   const int nd = (int)(c.L - ms.Lk);
 #define SECN_LWE(AR, WT, ND)                                                                                   \
   return launch_pdl(c, k_ntt_inv_tail_lwe<AR, ND>, grid, block, 0, s, static_cast<const WT*>(polys), c, ms, r, \
-                    static_cast<WT*>(a_out), static_cast<WT*>(b_out), y0, pl, chained ? 1 : 0)
+                    static_cast<WT*>(a_out), static_cast<WT*>(b_out), y0, pl, chained ? 1 : 0, static_cast<const WT*>(em))
   if (c.word_bits == 64) {
     if (nd == 1) SECN_LWE(Arith64, uint64_t, 1);  // 64-bit limbs: one dropped prime (P < 2^62)
   } else {
@@ -1964,6 +2071,19 @@ cudaError_t launch_mask_draw(const DevConsts& c, const MaskGen& g, size_t n_ct, 
   const size_t blocks = (pairs + 255) / 256, cap = (size_t)c.tune.num_sms * 16;
   return launch_pdl(c, k_mask_draw, dim3((unsigned)(blocks < cap ? blocks : cap)), dim3(256), 0, s, r, g, pairs,
                     (uint32_t)half, c.t_bits);
+}
+
+cudaError_t launch_mask_encode(const DevConsts& c, const PlanDev& p, size_t n_act, const uint64_t* r, const MaskGen& g,
+                               void* em, uint64_t* y0, cudaStream_t s) {
+  if (n_act == 0) return cudaSuccess;
+  const size_t pairs = n_act << (c.log_n - 1);
+  const size_t blocks = (pairs + 255) / 256, cap = (size_t)c.tune.num_sms * 8;
+  const dim3 grid((unsigned)(blocks < cap ? blocks : cap));
+  if (c.word_bits == 64)
+    return launch_pdl(c, k_mask_encode<Arith64>, grid, dim3(256), 0, s, static_cast<uint64_t*>(em), y0, r, g, c, p,
+                      (uint32_t)n_act);
+  return launch_pdl(c, k_mask_encode<Arith32>, grid, dim3(256), 0, s, static_cast<uint32_t*>(em), y0, r, g, c, p,
+                    (uint32_t)n_act);
 }
 
 cudaError_t launch_check_range(const DevConsts& c, const void* v, size_t n_words, int kind, uint32_t* flag,
