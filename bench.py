@@ -72,6 +72,11 @@ def parse():
     ap.add_argument("--mask", choices=["device", "host"], default="device",
                     help="device (default): the server's mask r is drawn inside every layer call (secn32_he_conv2d_gen, "
                          "Philox4x32-10, reading R17); host: r is a caller input (secn32_he_conv2d_ex)")
+    ap.add_argument("--mask-schedule", choices=["ahead", "lookahead", "inline"], default="ahead",
+                    help="device mask: when each layer's mask is drawn + encoded (secn_mask_encode) -- ahead "
+                         "(default): every layer's at the start of the step, on a side stream beside the layer chain "
+                         "(1.209 ms, profiles/r02h_*); lookahead: the next group's while a group runs (1.253 ms); "
+                         "inline: inside the layer call, secn32_he_conv2d_gen (1.232 ms)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-online", action="store_true", help="skip the online-NTT-preprocessing (f4) leg")
@@ -331,6 +336,7 @@ def run_secn(args, word_bits, world, rank, local, dev, full):
                 d["gen"] = MaskGen(seed=mask_seed(args.seed), stream=li, ct0=m0 * S)
                 d["r"] = ctx.mask_draw(d["gen"], mc * S)
                 d["ws_gen"] = torch.empty((ctx.gen_workspace_bytes(pl) + 7) // 8, dtype=torch.int64, device=dev)
+                d["em"] = ctx.empty(mc * S, L, n)  # the encoded mask (secn_mask_encode), for the side-stream schedules
             else:
                 d["r"] = torch.from_numpy(np.ascontiguousarray(r[m0 * S:(m0 + mc) * S]).view(np.int64)).to(dev)
             d["out"] = ctx.empty(mc * S, 2, L, n)
@@ -361,9 +367,25 @@ def run_secn(args, word_bits, world, rank, local, dev, full):
     groups = concurrent_groups(names) if args.overlap != "none" else [[i] for i in range(len(st))]
     runner = StagedGroupRunner(groups, dev) if args.overlap == "staged" else GroupRunner(groups, dev)
 
+    # device mask drawn + encoded apart from the layer call (it is input-independent): on a side
+    # stream, ahead of the layer that adds it; the layer's stream waits for its event
+    msched = args.mask_schedule if drawn and args.overlap != "staged" else "inline"
+    mstream = torch.cuda.Stream(dev)
+    mev = [torch.cuda.Event() for _ in st]
+
+    def encode_mask(i):
+        d = st[i]
+        if d["mc"] > 0:
+            with torch.cuda.stream(mstream):
+                ctx.mask_encode(d["pl"], gen=d["gen"], out=d["em"], y0=d["y0"])
+                mev[i].record(mstream)
+
     def layer_call(i):
         d = st[i]
-        if d["mc"] > 0 and drawn:
+        if d["mc"] > 0 and drawn and msched != "inline":
+            torch.cuda.current_stream().wait_event(mev[i])  # recorded before this layer was issued
+            ctx.he_conv2d_em(d["pl"], d["ct"], d["w"], d["em"], x0=d["x0"], out=d["out"], workspace=d["ws"])
+        elif d["mc"] > 0 and drawn:
             ctx.he_conv2d_gen(d["pl"], d["ct"], d["w"], d["gen"], x0=d["x0"], out=d["out"], workspace=d["ws_gen"],
                               y0=d["y0"])
         elif d["mc"] > 0:
@@ -375,11 +397,24 @@ def run_secn(args, word_bits, world, rank, local, dev, full):
         if d["mc"] > 0:
             ctx.he_conv2d_stage_ex(k, d["pl"], d["ct"], d["w"], d["x0"], d["r"], d["out"], d["y0"], d["ws"])
 
+    def before_group(k):  # lookahead: group k+1's masks on the side stream while group k runs
+        if k + 1 < len(runner.groups):
+            mstream.wait_stream(torch.cuda.current_stream())
+            for i in runner.groups[k + 1]:
+                encode_mask(i)
+
     def step_public():
+        ahead = drawn and msched != "inline"
+        if ahead:
+            mstream.wait_stream(torch.cuda.current_stream())
+            for i in (range(len(st)) if msched == "ahead" else runner.groups[0]):
+                encode_mask(i)
         if args.overlap == "staged":
             runner(layer_call, stage_call)
         else:
-            runner(layer_call)
+            runner(layer_call, before_group if ahead and msched == "lookahead" else None)
+        if ahead:
+            torch.cuda.current_stream().wait_stream(mstream)
 
     # ---- warmup (eager), then capture the step in a CUDA graph ----
     for _ in range(max(args.warmup, 3)):
@@ -496,8 +531,14 @@ def run_secn(args, word_bits, world, rank, local, dev, full):
                    "N": n, "limbs": L, "primes": [hex(q) for q in ctx.primes], "t_bits": t_bits,
                    "parallelism": (f"(output channel x spatial block) rectangles over {world} ranks "
                                    "(paper_2506_11586_b200/dist.partition)" if world > 1 else "1 GPU"),
-                   "mask": ("drawn on the device inside every layer call (secn32_he_conv2d_gen, Philox4x32-10, "
-                            "reading R17)" if drawn else "caller input r (secn32_he_conv2d_ex)"), "l2": (f"inputs {alg_bytes / 1e9:.2f} GB/step >> 126 MB L2 (no flush)" if alg_bytes > 5e8 else
+                   "mask": ({"inline": "drawn + encoded on the device inside every layer call (secn32_he_conv2d_gen, "
+                                       "Philox4x32-10, reading R17)",
+                             "lookahead": "drawn + encoded on the device (secn_mask_encode, Philox4x32-10, reading R17) "
+                                          "on a side stream one layer ahead of the chain, added by secn32_he_conv2d_em",
+                             "ahead": "drawn + encoded on the device (secn_mask_encode, Philox4x32-10, reading R17) for "
+                                      "every layer at the start of the step on a side stream, added by "
+                                      "secn32_he_conv2d_em"}[msched]
+                            if drawn else "caller input r (secn32_he_conv2d_ex)"), "l2": (f"inputs {alg_bytes / 1e9:.2f} GB/step >> 126 MB L2 (no flush)" if alg_bytes > 5e8 else
                           "step footprint below 4x L2: timing includes L2 reuse across replays"),
                    "timing": "CUDA events around CUDA-graph replays of the whole step",
                    "layer_overlap": {"none": "none: every layer in network order on one stream",

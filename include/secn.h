@@ -154,8 +154,9 @@ int secn_share_add(secn_ctx* ctx, uint64_t* ct, const uint64_t* x0, size_t n, vo
  * (coefficient domain), r [n][N] < 2^t_bits. The server's share is (t - r) mod t. */
 int secn_mask_add(secn_ctx* ctx, uint64_t* ct, const uint64_t* r, size_t n, void* stream);
 
-/* Bytes of device workspace secn_he_conv2d needs for `plan` (the NTT-domain inputs
- * X^ = G*S*2*L*N words of the context's word size). */
+/* Bytes of device workspace the secn_he_conv2d family needs for `plan`: the NTT-domain inputs
+ * X^ = G*S*2*L*N words of the context's word size (all a call with a caller mask r or a
+ * pre-encoded mask needs), then the encoded mask (M*S*L*N words) for the *_gen calls. */
 size_t secn_he_conv2d_workspace(const secn_ctx* ctx, const secn_conv_plan_t* plan);
 
 /* The hot path (PAPER.md:380 §6.2, :431 §7), one layer:
@@ -239,6 +240,22 @@ int secn_he_conv2d_gen(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64
                        const uint64_t* w_ntt, const secn_mask_gen_t* gen, uint64_t* ct_out, uint64_t* y0,
                        void* workspace, size_t ws_bytes, void* stream);
 
+/* The encoded mask, prepared apart from the layer call. The mask is input-independent, so a server
+ * can draw and encode it ahead of (or concurrently with) the computation that needs it, e.g. on a
+ * low-priority stream while earlier layers run (bench.py does). secn_mask_encode writes
+ * em [M*S][L][N] (words of the context's size, secn_mask_encoded_bytes bytes, 16-byte aligned):
+ * em[m*S + s][j][e] = enc_j(r[m*S + s][e]) for the plan's output ciphertexts (its spatial slice;
+ * M may be a channel slice as elsewhere) with r from the caller (r [M*S][N] < 2^t_bits) or drawn
+ * by `gen` (exactly one of r, gen), and y0 (may be NULL) = -r mod t at the designated outputs.
+ * secn_he_conv2d_em / secn32_he_conv2d_em then run the layer adding em (A7) -- the result of
+ * secn_he_conv2d_ex with that r. The LWE form is secn[32]_he_conv2d_lwe_em. */
+size_t secn_mask_encoded_bytes(const secn_ctx* ctx, const secn_conv_plan_t* plan);
+int secn_mask_encode(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* r, const secn_mask_gen_t* gen,
+                     void* em, uint64_t* y0, void* stream);
+int secn_he_conv2d_em(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* ct_in, const uint64_t* x0,
+                      const uint64_t* w_ntt, const uint64_t* em, uint64_t* ct_out, void* workspace, size_t ws_bytes,
+                      void* stream);
+
 /* ------------------------------------------------------------------------------------------
  * HE fully-connected layer / matrix-vector product (§6
  * "fully-connected/matrix multiplication layers"; SPEC.md:612-619 fc_secure). The server's work
@@ -299,6 +316,9 @@ size_t secn_he_conv2d_lwe_gen_workspace(const secn_ctx* ctx, const secn_conv_pla
 int secn_he_conv2d_lwe_gen(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* ct_in, const uint64_t* x0,
                            const uint64_t* w_ntt, const secn_mask_gen_t* gen, uint32_t keep_limbs, uint64_t* a_out,
                            uint64_t* b_out, uint64_t* y0, void* workspace, size_t ws_bytes, void* stream);
+int secn_he_conv2d_lwe_em(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* ct_in, const uint64_t* x0,
+                          const uint64_t* w_ntt, const uint64_t* em, uint32_t keep_limbs, uint64_t* a_out,
+                          uint64_t* b_out, void* workspace, size_t ws_bytes, void* stream);
 size_t secn_he_fc_lwe_workspace(const secn_ctx* ctx, const secn_fc_plan_t* plan);
 int secn_he_fc_lwe(secn_ctx* ctx, const secn_fc_plan_t* plan, const uint64_t* ct_in, const uint64_t* x0,
                    const uint64_t* w_ntt, const uint64_t* r, uint32_t keep_limbs, uint64_t* a_out, uint64_t* b_out,
@@ -348,6 +368,12 @@ int secn32_he_conv2d_gen(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint
 int secn32_he_conv2d_lwe_gen(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint32_t* ct_in, const uint64_t* x0,
                              const uint32_t* w_ntt, const secn_mask_gen_t* gen, uint32_t keep_limbs, uint32_t* a_out,
                              uint32_t* b_out, uint64_t* y0, void* workspace, size_t ws_bytes, void* stream);
+int secn32_he_conv2d_em(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint32_t* ct_in, const uint64_t* x0,
+                        const uint32_t* w_ntt, const uint32_t* em, uint32_t* ct_out, void* workspace, size_t ws_bytes,
+                        void* stream);
+int secn32_he_conv2d_lwe_em(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint32_t* ct_in, const uint64_t* x0,
+                            const uint32_t* w_ntt, const uint32_t* em, uint32_t keep_limbs, uint32_t* a_out,
+                            uint32_t* b_out, void* workspace, size_t ws_bytes, void* stream);
 int secn32_he_conv2d_stage(secn_ctx* ctx, const secn_conv_plan_t* plan, int stage, const uint32_t* ct_in,
                            const uint64_t* x0, const uint32_t* w_ntt, const uint64_t* r, uint32_t* ct_out,
                            void* workspace, size_t ws_bytes, void* stream);

@@ -537,24 +537,26 @@ size_t secn_he_conv2d_workspace(const secn_ctx* ctx, const secn_conv_plan_t* pla
 
 // stage -1 = the whole layer; 0 / 1 / 2 = one launch group. `chained`: the caller launched this
 // stage's predecessor stage itself just before (internal.h, "Pre-wait reads"); always true for -1.
-// Full calls (stage -1) with a mask encode it once, right after the forward NTT (k_mask_encode:
-// em in the workspace, y0 written there), and the tail adds em; gen != NULL draws r on the device
-// (reading R17) instead of reading it. Stage calls (0, 1, 2) need only X^ in the workspace and
-// encode r in the tail.
+// The mask (A7) arrives one of three ways: r (the tail loads and encodes it per limb, and writes
+// y0); gen != NULL (full calls: drawn on the device, reading R17 -- k_mask_encode, launched right
+// after the forward NTT, writes the encoded words em into the workspace and y0, and the tail adds
+// em); or em_in != NULL (full calls: encoded beforehand by secn_mask_encode, the tail adds it).
+// Stage calls (0, 1, 2) need only X^ in the workspace.
 static int he_conv2d_impl(secn_ctx* ctx, uint32_t bits, const secn_conv_plan_t* plan, int stage, const void* ct_in,
                           const uint64_t* x0, const void* w_ntt, const uint64_t* r, void* ct_out, uint64_t* y0,
                           void* workspace, size_t ws_bytes, void* stream, bool chained = false,
-                          const secn::MaskGen* gen = nullptr) {
+                          const secn::MaskGen* gen = nullptr, const void* em_in = nullptr) {
   if (int st = check_ctx(ctx, bits)) return st;
   if (int st = check_plan(ctx, plan)) return st;
   if (stage < -1 || stage > 2) return fail(SECN_EINVAL, "stage %d not in {0,1,2}", stage);
   if (!ct_in || !w_ntt || !ct_out || !workspace) return fail(SECN_EINVAL, "NULL buffer");
   if (ctx->log_n > 14) return fail(SECN_EUNSUPPORTED, "convolutions need log_n <= 14 (N = 2^15 is NTT-only)");
   if (y0 && !r && !gen) return fail(SECN_EINVAL, "y0 needs the mask r");
-  const bool encode = stage == -1 && (r != nullptr || gen != nullptr);
+  const bool encode = stage == -1 && gen != nullptr;
   if (ws_bytes < (encode ? secn_he_conv2d_workspace(ctx, plan) : xhat_bytes(ctx, plan)))
     return fail(SECN_EINVAL, "workspace too small");
-  if (((uintptr_t)workspace | (uintptr_t)ct_in | (uintptr_t)ct_out | (uintptr_t)w_ntt | (uintptr_t)r) & 15)
+  if (((uintptr_t)workspace | (uintptr_t)ct_in | (uintptr_t)ct_out | (uintptr_t)w_ntt | (uintptr_t)r |
+       (uintptr_t)em_in) & 15)
     return fail(SECN_EINVAL, "buffers must be 16-byte aligned");
   if (plan->G > 32u) return fail(SECN_EUNSUPPORTED, "G=%u input channel groups too many", plan->G);
   DeviceGuard guard(ctx->device);
@@ -571,17 +573,17 @@ static int he_conv2d_impl(secn_ctx* ctx, uint32_t bits, const secn_conv_plan_t* 
   const secn::PlanDev pd = plan_dev(plan);
   cudaError_t e = cudaSuccess;
   if (stage == -1 || stage == 0) e = secn::launch_ntt_fwd(ctx->dc, ct_in, workspace, n_in * 2 * ctx->L, x0, s);  // A6+A1
-  void* em = nullptr;
-  if (e == cudaSuccess && encode) {  // A7 (+A8) prepared on the SMs the forward NTT leaves idle
-    em = static_cast<unsigned char*>(workspace) + xhat_bytes_aligned(ctx, plan);
-    const secn::MaskGen g = gen ? *gen : secn::MaskGen{0, 0, 0};
-    e = secn::launch_mask_encode(ctx->dc, pd, n_act, gen ? nullptr : r, g, em, y0, s);
+  const void* em = em_in;
+  if (e == cudaSuccess && encode) {  // A7 (+A8) drawn and encoded on the SMs the forward NTT leaves idle
+    void* emw = static_cast<unsigned char*>(workspace) + xhat_bytes_aligned(ctx, plan);
+    e = secn::launch_mask_encode(ctx->dc, pd, n_act, nullptr, *gen, emw, y0, s, true);
+    em = emw;
   }
   // A4 + A2 levels 0..7
   const bool ch = chained || stage == -1;
   if (e == cudaSuccess && stage == -1 && secn::fused_applies(ctx->dc, pd)) {  // MAC + INTT + mask in one kernel
     e = secn::launch_layer_fused(ctx->dc, pd, workspace, w_ntt, ct_out, em ? nullptr : r, em ? nullptr : y0, s, true,
-                                 em);
+                                 const_cast<void*>(em));
     return e == cudaSuccess ? SECN_OK : cuda_fail(e, "secn_he_conv2d");
   }
   if (e == cudaSuccess && (stage == -1 || stage == 1))
@@ -643,6 +645,46 @@ int secn32_he_conv2d_gen(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint
                          const uint32_t* w_ntt, const secn_mask_gen_t* gen, uint32_t* ct_out, uint64_t* y0,
                          void* workspace, size_t ws_bytes, void* stream) {
   return he_conv2d_gen_impl(ctx, 32, plan, ct_in, x0, w_ntt, gen, ct_out, y0, workspace, ws_bytes, stream);
+}
+
+size_t secn_mask_encoded_bytes(const secn_ctx* ctx, const secn_conv_plan_t* plan) {
+  if (!ctx || !plan) return 0;
+  return em_bytes(ctx, plan);
+}
+
+int secn_mask_encode(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* r, const secn_mask_gen_t* gen,
+                     void* em, uint64_t* y0, void* stream) {
+  if (int st = check_ctx(ctx)) return st;
+  if (int st = check_plan(ctx, plan)) return st;
+  if (!em || (!r && !gen) || (r && gen)) return fail(SECN_EINVAL, "need em and exactly one of r, gen");
+  if (((uintptr_t)em | (uintptr_t)r) & 15) return fail(SECN_EINVAL, "buffers must be 16-byte aligned");
+  secn::MaskGen g{0, 0, 0};
+  if (gen)
+    if (int st = check_gen(gen, &g)) return st;
+  DeviceGuard guard(ctx->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (int st = check_range(ctx, r, (size_t)plan->M * plan->S * ctx->n, 1, s, "secn_mask_encode r")) return st;
+  const secn::PlanDev pd = plan_dev(plan);
+  cudaError_t e = secn::launch_mask_encode(ctx->dc, pd, (size_t)plan->M * pd.sn, r, g, em, y0, s, false);
+  return e == cudaSuccess ? SECN_OK : cuda_fail(e, "secn_mask_encode");
+}
+
+static int he_conv2d_em_impl(secn_ctx* ctx, uint32_t bits, const secn_conv_plan_t* plan, const void* ct_in,
+                             const uint64_t* x0, const void* w_ntt, const void* em, void* ct_out, void* workspace,
+                             size_t ws_bytes, void* stream) {
+  if (!em) return fail(SECN_EINVAL, "NULL encoded mask");
+  return he_conv2d_impl(ctx, bits, plan, -1, ct_in, x0, w_ntt, nullptr, ct_out, nullptr, workspace, ws_bytes, stream,
+                        true, nullptr, em);
+}
+int secn_he_conv2d_em(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* ct_in, const uint64_t* x0,
+                      const uint64_t* w_ntt, const uint64_t* em, uint64_t* ct_out, void* workspace, size_t ws_bytes,
+                      void* stream) {
+  return he_conv2d_em_impl(ctx, 64, plan, ct_in, x0, w_ntt, em, ct_out, workspace, ws_bytes, stream);
+}
+int secn32_he_conv2d_em(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint32_t* ct_in, const uint64_t* x0,
+                        const uint32_t* w_ntt, const uint32_t* em, uint32_t* ct_out, void* workspace, size_t ws_bytes,
+                        void* stream) {
+  return he_conv2d_em_impl(ctx, 32, plan, ct_in, x0, w_ntt, em, ct_out, workspace, ws_bytes, stream);
 }
 
 int secn_mask_draw(secn_ctx* ctx, const secn_mask_gen_t* gen, size_t n_ct, uint64_t* r, void* stream) {
@@ -838,7 +880,7 @@ size_t secn_he_conv2d_lwe_workspace(const secn_ctx* ctx, const secn_conv_plan_t*
 static int he_conv2d_lwe_impl(secn_ctx* ctx, uint32_t bits, const secn_conv_plan_t* plan, const void* ct_in,
                               const uint64_t* x0, const void* w_ntt, const uint64_t* r, uint32_t keep, void* a_out,
                               void* b_out, uint64_t* y0, void* workspace, size_t ws_bytes, void* stream,
-                              const secn::MaskGen* gen = nullptr) {
+                              const secn::MaskGen* gen = nullptr, const void* em_in = nullptr) {
   if (int st = check_ctx(ctx, bits)) return st;
   if (int st = check_plan(ctx, plan)) return st;
   secn::MsConsts ms;
@@ -846,7 +888,7 @@ static int he_conv2d_lwe_impl(secn_ctx* ctx, uint32_t bits, const secn_conv_plan
   if (!ct_in || !w_ntt || !a_out || !b_out || !workspace) return fail(SECN_EINVAL, "NULL buffer");
   if (ws_bytes < secn_he_conv2d_lwe_workspace(ctx, plan)) return fail(SECN_EINVAL, "workspace too small");
   if (y0 && !r && !gen) return fail(SECN_EINVAL, "y0 needs the mask r");
-  if (((uintptr_t)workspace | (uintptr_t)ct_in | (uintptr_t)w_ntt | (uintptr_t)r) & 15)
+  if (((uintptr_t)workspace | (uintptr_t)ct_in | (uintptr_t)w_ntt | (uintptr_t)r | (uintptr_t)em_in) & 15)
     return fail(SECN_EINVAL, "buffers must be 16-byte aligned");
   if (plan->G > 32u) return fail(SECN_EUNSUPPORTED, "G=%u input channel groups too many", plan->G);
   DeviceGuard guard(ctx->device);
@@ -860,15 +902,19 @@ static int he_conv2d_lwe_impl(secn_ctx* ctx, uint32_t bits, const secn_conv_plan
   // workspace: X^, then Y^ (levels 0..7 applied), then the encoded mask
   unsigned char* ws = static_cast<unsigned char*>(workspace);
   void* yhat = ws + xhat_bytes_aligned(ctx, plan);
-  void* em = (r || gen) ? ws + xhat_bytes_aligned(ctx, plan) + n_out * 2 * ctx->L * N * (ctx->word_bits / 8) : nullptr;
+  // the mask: r (encoded in the tail), drawn (gen: encoded into the workspace right after the
+  // forward NTT), or encoded beforehand (em_in)
+  const void* em = em_in;
+  void* emw = gen ? ws + xhat_bytes_aligned(ctx, plan) + n_out * 2 * ctx->L * N * (ctx->word_bits / 8) : nullptr;
   cudaError_t e = secn::launch_ntt_fwd(ctx->dc, ct_in, workspace, n_in * 2 * ctx->L, x0, s);  // A6 + A1
-  if (e == cudaSuccess && em) {
-    const secn::MaskGen g = gen ? *gen : secn::MaskGen{0, 0, 0};
-    e = secn::launch_mask_encode(ctx->dc, pd, n_act, gen ? nullptr : r, g, em, y0, s);  // A7 (+A8)
+  if (e == cudaSuccess && gen) {
+    e = secn::launch_mask_encode(ctx->dc, pd, n_act, nullptr, *gen, emw, y0, s, true);  // A7 (+A8)
+    em = emw;
   }
   if (e == cudaSuccess) e = secn::launch_mac(ctx->dc, pd, workspace, w_ntt, yhat, s, true);  // A4 + INTT 0..7
   if (e == cudaSuccess)  // INTT 8.. + mask + modulus switch + extraction
-    e = secn::launch_ntt_inv_tail_lwe(ctx->dc, ms, yhat, n_act, nullptr, a_out, b_out, nullptr, pd, s, true, em);
+    e = secn::launch_ntt_inv_tail_lwe(ctx->dc, ms, yhat, n_act, em ? nullptr : r, a_out, b_out, em ? nullptr : y0, pd,
+                                      s, true, em);
   return e == cudaSuccess ? SECN_OK : cuda_fail(e, "secn_he_conv2d_lwe");
 }
 
@@ -884,6 +930,26 @@ static int he_conv2d_lwe_gen_impl(secn_ctx* ctx, uint32_t bits, const secn_conv_
   if (int st = check_gen(gen, &g)) return st;
   return he_conv2d_lwe_impl(ctx, bits, plan, ct_in, x0, w_ntt, nullptr, keep, a_out, b_out, y0, workspace, ws_bytes,
                             stream, &g);
+}
+
+static int he_conv2d_lwe_em_impl(secn_ctx* ctx, uint32_t bits, const secn_conv_plan_t* plan, const void* ct_in,
+                                 const uint64_t* x0, const void* w_ntt, const void* em, uint32_t keep, void* a_out,
+                                 void* b_out, void* workspace, size_t ws_bytes, void* stream) {
+  if (!em) return fail(SECN_EINVAL, "NULL encoded mask");
+  return he_conv2d_lwe_impl(ctx, bits, plan, ct_in, x0, w_ntt, nullptr, keep, a_out, b_out, nullptr, workspace,
+                            ws_bytes, stream, nullptr, em);
+}
+int secn_he_conv2d_lwe_em(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* ct_in, const uint64_t* x0,
+                          const uint64_t* w_ntt, const uint64_t* em, uint32_t keep_limbs, uint64_t* a_out,
+                          uint64_t* b_out, void* workspace, size_t ws_bytes, void* stream) {
+  return he_conv2d_lwe_em_impl(ctx, 64, plan, ct_in, x0, w_ntt, em, keep_limbs, a_out, b_out, workspace, ws_bytes,
+                               stream);
+}
+int secn32_he_conv2d_lwe_em(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint32_t* ct_in, const uint64_t* x0,
+                            const uint32_t* w_ntt, const uint32_t* em, uint32_t keep_limbs, uint32_t* a_out,
+                            uint32_t* b_out, void* workspace, size_t ws_bytes, void* stream) {
+  return he_conv2d_lwe_em_impl(ctx, 32, plan, ct_in, x0, w_ntt, em, keep_limbs, a_out, b_out, workspace, ws_bytes,
+                               stream);
 }
 
 int secn_he_conv2d_lwe_gen(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* ct_in, const uint64_t* x0,

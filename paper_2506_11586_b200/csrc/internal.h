@@ -146,9 +146,10 @@ cudaError_t launch_pack_fc_weights(const DevConsts& c, const PlanDev& p, const u
 cudaError_t launch_mask_draw(const DevConsts& c, const MaskGen& g, size_t n_ct, uint64_t* r, cudaStream_t s);
 // em [rows][L][N] (word size) = enc_j(r) of the call's n_act output ciphertexts (rows slice_ct),
 // r from `r` (device) or, if r == NULL, drawn by g; y0 (may be NULL) = -r mod t at the designated
-// outputs. Chains like launch_mask_draw (run it right after the forward NTT).
+// outputs. chained: launched right after the forward NTT of the same call (waits for it only at the
+// end, so that the MAC's dependency wait covers both); else a standalone call (waits first).
 cudaError_t launch_mask_encode(const DevConsts& c, const PlanDev& p, size_t n_act, const uint64_t* r, const MaskGen& g,
-                               void* em, uint64_t* y0, cudaStream_t s);
+                               void* em, uint64_t* y0, cudaStream_t s, bool chained);
 cudaError_t launch_enc_add(const DevConsts& c, void* ct, const uint64_t* v, size_t n, cudaStream_t s);
 cudaError_t launch_extract_share(const DevConsts& c, const PlanDev& p, const uint64_t* r, uint64_t* y0,
                                  cudaStream_t s);

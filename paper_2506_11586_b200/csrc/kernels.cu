@@ -1421,13 +1421,17 @@ __global__ void k_mask_draw(uint64_t* __restrict__ r, MaskGen g, size_t n_pairs,
 // same chaining as k_mask_draw (it reads nothing the NTT writes; it waits for it at the end), so
 // it runs on the SMs the forward NTT leaves idle, and the INTT tails only add em_j (4 or 8 bytes
 // per limb-coefficient) instead of reading and encoding r (8 bytes per coefficient, per limb).
+// wait_first: a standalone call (secn_mask_encode), whose r may come from the preceding kernel,
+// waits for it before reading; chained after the forward NTT it waits only at the end.
 template <class A>
 __global__ void __launch_bounds__(256) k_mask_encode(typename A::W* __restrict__ em, uint64_t* __restrict__ y0,
                                                      const uint64_t* __restrict__ r, MaskGen g,
                                                      const __grid_constant__ DevConsts c,
-                                                     const __grid_constant__ PlanDev pl, uint32_t n_act) {
+                                                     const __grid_constant__ PlanDev pl, uint32_t n_act,
+                                                     int wait_first) {
   using W = typename A::W;
   pdl_trigger();
+  if (wait_first) pdl_wait();
   const uint32_t N = 1u << c.log_n, half = N >> 1, L = c.L;
   const uint64_t tm = (1ull << c.t_bits) - 1, thalf = 1ull << (c.t_bits - 1);
   const size_t n_pairs = (size_t)n_act * half, stride = (size_t)gridDim.x * blockDim.x;
@@ -1476,7 +1480,7 @@ __global__ void __launch_bounds__(256) k_mask_encode(typename A::W* __restrict__
       y0[idx] = (tm + 1 - ((e & 1) ? v1 : v0)) & tm;
     }
   }
-  pdl_wait();
+  if (!wait_first) pdl_wait();
 }
 
 // Designated server share y0[m][oy][ox] = (t - r[m*S+s][O + i*Ww + j]) mod t.
@@ -2074,16 +2078,16 @@ cudaError_t launch_mask_draw(const DevConsts& c, const MaskGen& g, size_t n_ct, 
 }
 
 cudaError_t launch_mask_encode(const DevConsts& c, const PlanDev& p, size_t n_act, const uint64_t* r, const MaskGen& g,
-                               void* em, uint64_t* y0, cudaStream_t s) {
+                               void* em, uint64_t* y0, cudaStream_t s, bool chained) {
   if (n_act == 0) return cudaSuccess;
   const size_t pairs = n_act << (c.log_n - 1);
   const size_t blocks = (pairs + 255) / 256, cap = (size_t)c.tune.num_sms * 8;
   const dim3 grid((unsigned)(blocks < cap ? blocks : cap));
   if (c.word_bits == 64)
     return launch_pdl(c, k_mask_encode<Arith64>, grid, dim3(256), 0, s, static_cast<uint64_t*>(em), y0, r, g, c, p,
-                      (uint32_t)n_act);
+                      (uint32_t)n_act, chained ? 0 : 1);
   return launch_pdl(c, k_mask_encode<Arith32>, grid, dim3(256), 0, s, static_cast<uint32_t*>(em), y0, r, g, c, p,
-                    (uint32_t)n_act);
+                    (uint32_t)n_act, chained ? 0 : 1);
 }
 
 cudaError_t launch_check_range(const DevConsts& c, const void* v, size_t n_words, int kind, uint32_t* flag,

@@ -49,20 +49,27 @@ class GroupRunner:
         width = max((len(g) for g in groups), default=1)
         self.side = [torch.cuda.Stream(device) for _ in range(width - 1)]
 
-    def __call__(self, fn: Callable[[int], None]) -> None:
+    def __call__(self, fn: Callable[[int], None], before_group: Optional[Callable[[int], None]] = None) -> None:
+        """before_group(k), if given, runs on the host before group k is issued (e.g. to issue side
+        work the group's layers wait for)."""
+        for k, g in enumerate(self.groups):
+            if before_group is not None:
+                before_group(k)
+            self.run_group(g, fn)
+
+    def run_group(self, g: List[int], fn: Callable[[int], None]) -> None:
         main = torch.cuda.current_stream()
-        for g in self.groups:
-            if len(g) == 1:
-                fn(g[0])
-                continue
-            for s in self.side[:len(g) - 1]:
-                s.wait_stream(main)
-            for s, i in zip(self.side, g[1:]):
-                with torch.cuda.stream(s):
-                    fn(i)
+        if len(g) == 1:
             fn(g[0])
-            for s in self.side[:len(g) - 1]:
-                main.wait_stream(s)
+            return
+        for s in self.side[:len(g) - 1]:
+            s.wait_stream(main)
+        for s, i in zip(self.side, g[1:]):
+            with torch.cuda.stream(s):
+                fn(i)
+        fn(g[0])
+        for s in self.side[:len(g) - 1]:
+            main.wait_stream(s)
 
 
 class StagedGroupRunner:

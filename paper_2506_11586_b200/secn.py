@@ -38,7 +38,9 @@ EXPORTS = ("secn_ctx_create", "secn_ctx_destroy", "secn_ctx_query", "secn_last_e
            "secn32_fc_preprocess_weights", "secn_he_fc_workspace", "secn_he_fc", "secn32_he_fc",
            "secn_he_conv2d_lwe_workspace", "secn_he_conv2d_lwe", "secn32_he_conv2d_lwe", "secn_he_fc_lwe_workspace",
            "secn_he_fc_lwe", "secn32_he_fc_lwe", "secn_mask_draw", "secn_he_conv2d_gen_workspace", "secn_he_conv2d_gen",
-           "secn32_he_conv2d_gen", "secn_he_conv2d_lwe_gen_workspace", "secn_he_conv2d_lwe_gen", "secn32_he_conv2d_lwe_gen")
+           "secn32_he_conv2d_gen", "secn_he_conv2d_lwe_gen_workspace", "secn_he_conv2d_lwe_gen", "secn32_he_conv2d_lwe_gen",
+           "secn_mask_encoded_bytes", "secn_mask_encode", "secn_he_conv2d_em", "secn32_he_conv2d_em",
+           "secn_he_conv2d_lwe_em", "secn32_he_conv2d_lwe_em")
 
 
 class SecnError(RuntimeError):
@@ -132,11 +134,15 @@ def lib(path=None) -> ctypes.CDLL:
         "secn_he_conv2d_gen": (i, [vp, P, vp, vp, vp, ctypes.POINTER(MaskGen), vp, vp, vp, sz, vp]),
         "secn_he_conv2d_lwe_gen_workspace": (sz, [vp, P]),
         "secn_he_conv2d_lwe_gen": (i, [vp, P, vp, vp, vp, ctypes.POINTER(MaskGen), u32, vp, vp, vp, vp, sz, vp]),
+        "secn_mask_encoded_bytes": (sz, [vp, P]),
+        "secn_mask_encode": (i, [vp, P, vp, ctypes.POINTER(MaskGen), vp, vp, vp]),
+        "secn_he_conv2d_em": (i, [vp, P, vp, vp, vp, vp, vp, vp, sz, vp]),
+        "secn_he_conv2d_lwe_em": (i, [vp, P, vp, vp, vp, vp, u32, vp, vp, vp, sz, vp]),
     }
     for f in ("ntt_fwd", "ntt_inv", "preprocess_weights", "share_add", "mask_add", "he_conv2d", "he_conv2d_stage",
               "he_conv2d_stage_ex", "he_conv2d_ex",
               "he_conv2d_online", "fc_preprocess_weights", "he_fc", "he_conv2d_lwe", "he_fc_lwe", "he_conv2d_gen",
-              "he_conv2d_lwe_gen"):
+              "he_conv2d_lwe_gen", "he_conv2d_em", "he_conv2d_lwe_em"):
         sig["secn32_" + f] = sig["secn_" + f]
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -444,6 +450,53 @@ class Context:
         _check(lib().secn_mask_draw(self._h, ctypes.byref(gen), n_ct, _ptr(out, (n_ct, self.n), "r"),
                                     self._stream(stream)))
         return out
+
+    def mask_encode(self, plan: Plan, r: Optional[torch.Tensor] = None, gen: Optional[MaskGen] = None,
+                    out: Optional[torch.Tensor] = None, y0: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+        """secn_mask_encode: the encoded mask em [M*S][L][N] (residue dtype) from r or the generator,
+        and y0 (int64 [M][OH][OW], optional) = -r mod t at the designated outputs."""
+        shape = (plan.M * plan.S, self.L, self.n)
+        if out is None:
+            out = self.empty(*shape)
+        _check(lib().secn_mask_encode(self._h, ctypes.byref(plan), _ptr(r, (plan.M * plan.S, self.n), "r"),
+                                      ctypes.byref(gen) if gen is not None else None, self._rp(out, shape, "em"),
+                                      _ptr(y0, (plan.M, plan.OH, plan.OW), "y0"), self._stream(stream)))
+        return out
+
+    def he_conv2d_em(self, plan: Plan, ct_in: torch.Tensor, w_ntt: torch.Tensor, em: torch.Tensor,
+                     x0: Optional[torch.Tensor] = None, out: Optional[torch.Tensor] = None,
+                     workspace: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+        """secn_he_conv2d_em: the layer with a mask encoded beforehand by mask_encode."""
+        L, n = self.L, self.n
+        n_in, n_out = plan.G * plan.S, plan.M * plan.S
+        if out is None:
+            out = self.empty(n_out, 2, L, n)
+        need = self.workspace_bytes(plan)
+        if workspace is None:
+            workspace = torch.empty((need + 7) // 8, dtype=torch.int64, device=self.device)
+        wp, wn = _ws(workspace, need, self.device)
+        _check(self._f("he_conv2d_em")(
+            self._h, ctypes.byref(plan), self._rp(ct_in, (n_in, 2, L, n), "ct_in"), _ptr(x0, (n_in, n), "x0"),
+            self._rp(w_ntt, (plan.M, plan.G, L, n), "w_ntt"), self._rp(em, (n_out, L, n), "em"),
+            self._rp(out, (n_out, 2, L, n), "ct_out"), wp, wn, self._stream(stream)))
+        return out
+
+    def he_conv2d_lwe_em(self, plan: Plan, ct_in: torch.Tensor, w_ntt: torch.Tensor, keep: int, em: torch.Tensor,
+                         x0: Optional[torch.Tensor] = None, workspace: Optional[torch.Tensor] = None, stream=None,
+                         out: Optional[tuple] = None):
+        """secn_he_conv2d_lwe_em: extracted outputs with a mask encoded beforehand."""
+        L, n = self.L, self.n
+        a, b = out if out is not None else (self.empty(plan.M * plan.S, keep, n), self.empty(plan.M, plan.OH, plan.OW, keep))
+        need = int(lib().secn_he_conv2d_lwe_workspace(self._h, ctypes.byref(plan)))
+        if workspace is None:
+            workspace = torch.empty((need + 7) // 8, dtype=torch.int64, device=self.device)
+        wp, wn = _ws(workspace, need, self.device)
+        _check(self._f("he_conv2d_lwe_em")(
+            self._h, ctypes.byref(plan), self._rp(ct_in, (plan.G * plan.S, 2, L, n), "ct_in"),
+            _ptr(x0, (plan.G * plan.S, n), "x0"), self._rp(w_ntt, (plan.M, plan.G, L, n), "w_ntt"),
+            self._rp(em, (plan.M * plan.S, L, n), "em"), keep, self._rp(a, (plan.M * plan.S, keep, n), "a_out"),
+            self._rp(b, (plan.M, plan.OH, plan.OW, keep), "b_out"), wp, wn, self._stream(stream)))
+        return a, b
 
     def gen_workspace_bytes(self, plan: Plan) -> int:
         return int(lib().secn_he_conv2d_gen_workspace(self._h, ctypes.byref(plan)))

@@ -103,3 +103,45 @@ def test_he_conv2d_lwe_gen_equals_lwe_with_drawn_mask(env):
     a2, b2 = ctx.he_conv2d_lwe_gen(plan, D.R(ct), w, keep, g, x0=TP(x0), y0=y0b)
     assert torch.equal(a1, a2) and torch.equal(b1, b2) and torch.equal(y0a, y0b)
     assert (UP(y0b) == packing.extract((P.t - r) % P.t, opl)).all()
+
+
+@pytest.mark.parametrize("name", ["fire9.e3", "conv1", "fire2.sq"])
+@pytest.mark.parametrize("src", ["r", "gen"])
+def test_mask_encode_then_he_conv2d_em(env, name, src):
+    """secn_mask_encode (from r or the generator) + secn_he_conv2d_em equals secn_he_conv2d_ex with
+    that r, word for word, and the encoded words are enc_j(r) (the oracle's encoding); also with a
+    spatial slice of the outputs and through the LWE form."""
+    ctx, P, D = env
+    lay = next(l for l in layers.squeezenet11() if l.name == name)
+    opl = oplan(P, ctx, lay)
+    ct, x0, K, r = _layer_inputs(P, lay, 64, opl)
+    seed, stream = 2024, 3
+    g = secn_mod().MaskGen(seed=seed, stream=stream, ct0=0)
+    if src == "gen":
+        r = philox.mask(seed, stream, opl.M * opl.S, P.n, P.t_bits)
+    plan = ctx.plan(lay.C, lay.H, lay.W, lay.M, lay.k, stride=lay.stride, pad=lay.pad)
+    w = ctx.preprocess_weights(plan, TP(K))
+    y0 = torch.full((plan.M, plan.OH, plan.OW), -1, dtype=torch.int64, device=DEV)
+    em = ctx.mask_encode(plan, r=TP(r) if src == "r" else None, gen=g if src == "gen" else None, y0=y0)
+    emh = D.U(em)
+    for j in range(P.L):
+        for row in (0, opl.M * opl.S - 1):
+            assert (emh[row, j] == he.enc(r[row], P, j)).all()
+    assert (UP(y0) == packing.extract((P.t - r) % P.t, opl)).all()
+    got = D.U(ctx.he_conv2d_em(plan, D.R(ct), w, em, x0=TP(x0)))
+    ref = D.U(ctx.he_conv2d(plan, D.R(ct), w, x0=TP(x0), r=TP(r)))
+    assert (got == ref).all()
+    keep = 1 if ctx.L == 2 else 2
+    a1, b1 = ctx.he_conv2d_lwe(plan, D.R(ct), w, keep, x0=TP(x0), r=TP(r))
+    a2, b2 = ctx.he_conv2d_lwe_em(plan, D.R(ct), w, keep, em, x0=TP(x0))
+    assert torch.equal(a1, a2) and torch.equal(b1, b2)
+    if plan.S > 1:  # a spatial slice: only its blocks' rows are computed (the rest keep their old words)
+        pl = plan.copy(s_begin=1, s_count=plan.S - 1)
+        em2 = ctx.mask_encode(pl, r=TP(r))
+        out = ctx.empty(plan.M * plan.S, 2, ctx.L, ctx.n)
+        out.fill_(-1)
+        o = D.U(ctx.he_conv2d_em(pl, D.R(ct), w, em2, x0=TP(x0), out=out))
+        rows = [m * plan.S + s for m in range(plan.M) for s in range(1, plan.S)]
+        assert (o[rows] == ref[rows]).all()
+        other = [m * plan.S for m in range(plan.M)]
+        assert (o[other] == np.uint64(2**64 - 1) if ctx.word_bits == 64 else o[other] == 2**32 - 1).all()
