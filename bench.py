@@ -522,6 +522,24 @@ def run_secn(args, word_bits, world, rank, local, dev, full):
                 "avg_launch_us": round(stage_ms[dom] / n_layers_active * 1e3, 2),
                 "stage_ms": {names[s]: round(stage_ms[s], 4) for s in range(3)},
                 "stage_GBps": {names[s]: round(sb[s] / (stage_ms[s] / 1e3) / 1e9, 1) for s in range(3)}}
+    # the whole step against its byte floors, and every kernel's pipes and stalls, from the committed
+    # ncu capture of one step (tools/gpu_step_ncu.sh -> profiles/*_step_ncu.json)
+    bytemin = sum(algorithmic_bytes(ctx.plan(d["lay"].C, d["lay"].H, d["lay"].W, d["lay"].M, d["lay"].k,
+                                             stride=d["lay"].stride, pad=d["lay"].pad, rule=0), L, n, wbytes, drawn)
+                  for d in st)
+    roofline["step"] = {"alg_bytes_executed_plans": alg_bytes, "alg_bytes_byte_min_plans": bytemin,
+                        "hbm_frac_executed_plans": round(alg_bytes / step_s / 1e9 / (hbm_peak * world), 4),
+                        "hbm_frac_byte_min_plans": round(bytemin / step_s / 1e9 / (hbm_peak * world), 4)}
+    snc = sorted((ROOT / "profiles").glob("*_step_ncu.json"))
+    if snc and world == 1:
+        sj = json.loads(snc[-1].read_text())
+        roofline["step"].update({
+            "dram_traffic_ncu": sj["step_dram_bytes"],
+            "traffic_over_alg_bytes": round(sj["step_dram_bytes"] / alg_bytes, 3),
+            "ncu_source": f"profiles/{snc[-1].name} (one eager step, kernels serialised by ncu)",
+            "kernels": {k: {f: v for f, v in kv.items() if f in ("issue_active_pct", "pipe_alu_pct", "pipe_fma_pct",
+                                                                 "warps_active_pct", "dram_bytes", "top_stalls_per_issue")}
+                        for k, kv in sj["kernels"].items()}})
     out = {
         "metric": net_info(args.net)[0], "value": round(step_s, 7), "unit": "s", "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": False,

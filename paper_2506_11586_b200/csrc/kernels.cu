@@ -1432,9 +1432,8 @@ __global__ void __launch_bounds__(256) k_mask_encode(typename A::W* __restrict__
   using W = typename A::W;
   pdl_trigger();
   if (wait_first) pdl_wait();
-  const uint32_t N = 1u << c.log_n, half = N >> 1, L = c.L;
+  const uint32_t N = 1u << c.log_n, L = c.L;
   const uint64_t tm = (1ull << c.t_bits) - 1, thalf = 1ull << (c.t_bits - 1);
-  const size_t n_pairs = (size_t)n_act * half, stride = (size_t)gridDim.x * blockDim.x;
   const auto mask_pair = [&](uint32_t ct, uint32_t pe, uint64_t& v0, uint64_t& v1) {
     if (r != nullptr) {
       const ulonglong2 rr = reinterpret_cast<const ulonglong2*>(r + (size_t)ct * N)[pe];
@@ -1444,13 +1443,17 @@ __global__ void __launch_bounds__(256) k_mask_encode(typename A::W* __restrict__
       v0 = (((uint64_t)w.y << 32) | w.x) & tm, v1 = (((uint64_t)w.w << 32) | w.z) & tm;
     }
   };
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n_pairs; i += stride) {
-    const uint32_t ct = slice_ct(pl, (uint32_t)(i / half)), pe = (uint32_t)(i % half);
+  // grid (pairs / 256, active cts): one coefficient pair per thread, the ct uniform per CTA
+  const uint32_t pe = blockIdx.x * blockDim.x + threadIdx.x;
+  if (blockIdx.y < n_act && pe < (N >> 1)) {
+    const uint32_t ct = slice_ct(pl, blockIdx.y);
     uint64_t v0, v1;
     mask_pair(ct, pe, v0, v1);
     const uint64_t rho0 = (c.qmt * v0) & tm, rho1 = (c.qmt * v1) & tm;
     const uint32_t up0 = rho0 >= thalf, up1 = rho1 >= thalf;
-    for (uint32_t j = 0; j < L; ++j) {
+#pragma unroll
+    for (uint32_t j = 0; j < SECN_MAX_LIMBS; ++j) {
+      if (j >= L) break;
       const EncK ek(c, (int)j);
       W* dst = em + ((size_t)ct * L + j) * N + 2 * pe;
       const W e0 = enc_limb<A>(rho0, up0, ek), e1 = enc_limb<A>(rho1, up1, ek);
@@ -1462,7 +1465,9 @@ __global__ void __launch_bounds__(256) k_mask_encode(typename A::W* __restrict__
   }
   if (y0 != nullptr) {  // A8 at the designated outputs of the call's output ciphertexts
     const size_t total = pl.kind == 1 ? (size_t)pl.no : (size_t)pl.M * pl.OH * pl.OW;
-    for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total; idx += stride) {
+    const size_t stride = (size_t)gridDim.x * gridDim.y * blockDim.x;
+    for (size_t idx = ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
+         idx += stride) {
       uint32_t ct, e;
       if (pl.kind == 1) {  // fc: y[m nob + d] at coefficient d nib + nib - 1 of output ct m
         ct = (uint32_t)(idx / pl.nob), e = (uint32_t)(idx % pl.nob) * pl.nib + pl.nib - 1;
@@ -2080,9 +2085,8 @@ cudaError_t launch_mask_draw(const DevConsts& c, const MaskGen& g, size_t n_ct, 
 cudaError_t launch_mask_encode(const DevConsts& c, const PlanDev& p, size_t n_act, const uint64_t* r, const MaskGen& g,
                                void* em, uint64_t* y0, cudaStream_t s, bool chained) {
   if (n_act == 0) return cudaSuccess;
-  const size_t pairs = n_act << (c.log_n - 1);
-  const size_t blocks = (pairs + 255) / 256, cap = (size_t)c.tune.num_sms * 8;
-  const dim3 grid((unsigned)(blocks < cap ? blocks : cap));
+  if (n_act > 65535) return cudaErrorInvalidValue;  // grid.y
+  const dim3 grid((unsigned)(((1u << (c.log_n - 1)) + 255) / 256), (unsigned)n_act);
   if (c.word_bits == 64)
     return launch_pdl(c, k_mask_encode<Arith64>, grid, dim3(256), 0, s, static_cast<uint64_t*>(em), y0, r, g, c, p,
                       (uint32_t)n_act, chained ? 0 : 1);
