@@ -28,6 +28,7 @@ struct Tune {
   int32_t mac_pre;      // SECN_MAC_PRE: weight stages issued before the dependency wait (chained calls)
   int32_t mac_sg;       // SECN_MAC_SG / SECN_MAC_MT: forced k_mac register block
   int32_t mac_mt;
+  int32_t mac_ws;       // SECN_MAC_WS: the warp-specialised k_mac_ws (32-bit limbs): 0 never, 1 rule, 2 always
   int32_t fused;        // SECN_FUSED=2: the fused small-layer kernel for every layer it supports (default 0: off)
   int32_t fused_sg;     // SECN_FUSED_SG / SECN_FUSED_MT: its register block (s-group, m-block)
   int32_t fused_mt;

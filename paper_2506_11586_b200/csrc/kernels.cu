@@ -646,13 +646,21 @@ __device__ __forceinline__ void twe_row(Tw* out, const Tw* twe, int b) {
 // stores to global memory): every task is loaded before a barrier and written after it, so the
 // in-place change of layout cannot overwrite words another task has not read (needs
 // nch <= 2 MAC_THREADS / 16 = 32 chunks).
-template <class A, bool kDense = false>
+// NT threads (local index lt) run the levels and synchronise among themselves with named barrier BAR
+// (the default: k_mac's 256 consumers on barrier 1).
+template <int BAR, int NT>
+__device__ __forceinline__ void named_sync() {
+  asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(NT) : "memory");
+}
+
+template <class A, bool kDense = false, int NT = MAC_THREADS, int BAR = 1>
 __device__ __forceinline__ void mac_intt_levels_0_7(typename A::W* cbuf, const typename A::Tw* twe, int nch,
-                                                    typename A::W q, typename A::W qb) {
+                                                    typename A::W q, typename A::W qb, int lt = -1) {
   using W = typename A::W;
+  if (lt < 0) lt = threadIdx.x;
   const int ntask = nch * 16;
   // round A: levels 0..3, task = 16 consecutive coefficients 16b .. 16b+15 (phys: 17b + i)
-  for (int tau = threadIdx.x; tau < ntask; tau += MAC_THREADS) {
+  for (int tau = lt; tau < ntask; tau += NT) {
     W* base = cbuf + (tau >> 4) * MAC_CHS + 17 * (tau & 15);
     const int b = tau & 15;
     W x[16];
@@ -688,10 +696,10 @@ __device__ __forceinline__ void mac_intt_levels_0_7(typename A::W* cbuf, const t
 #pragma unroll
     for (int i = 0; i < 16; ++i) base[i] = x[i];
   }
-  consumer_sync();
+  named_sync<BAR, NT>();
   if constexpr (kDense) {
     W x[2][16];
-    const int t0 = threadIdx.x, t1 = threadIdx.x + MAC_THREADS;
+    const int t0 = lt, t1 = lt + NT;
     if (t0 < ntask) {  // fewer than 16 chunks (MT x 2SG = 12 for SG = 3, MT = 2): not every thread has a task
 #pragma unroll
       for (int i = 0; i < 16; ++i) x[0][i] = cbuf[(t0 >> 4) * MAC_CHS + (t0 & 15) + 17 * i];
@@ -700,7 +708,7 @@ __device__ __forceinline__ void mac_intt_levels_0_7(typename A::W* cbuf, const t
 #pragma unroll
       for (int i = 0; i < 16; ++i) x[1][i] = cbuf[(t1 >> 4) * MAC_CHS + (t1 & 15) + 17 * i];
     }
-    consumer_sync();  // every task's words are in registers: the chunks may change layout
+    named_sync<BAR, NT>();  // every task's words are in registers: the chunks may change layout
     if (t0 < ntask) {
 #pragma unroll
       for (int p = 0; p < 4; ++p) {
@@ -728,12 +736,12 @@ __device__ __forceinline__ void mac_intt_levels_0_7(typename A::W* cbuf, const t
       for (int i = 0; i < 16; ++i) cbuf[(t1 >> 4) * MAC_CHS + (t1 & 15) + 16 * i] = x[1][i];
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the bulk stores read these words
-    consumer_sync();
+    named_sync<BAR, NT>();
     return;
   }
   // round B: levels 4..7, task = coefficients 16i + o (phys: 17i + o); the twiddles do not
   // depend on the task
-  for (int tau = threadIdx.x; tau < ntask; tau += MAC_THREADS) {
+  for (int tau = lt; tau < ntask; tau += NT) {
     W* base = cbuf + (tau >> 4) * MAC_CHS + (tau & 15);
     W x[16];
 #pragma unroll
@@ -751,7 +759,7 @@ __device__ __forceinline__ void mac_intt_levels_0_7(typename A::W* cbuf, const t
 #pragma unroll
     for (int i = 0; i < 16; ++i) base[17 * i] = x[i];
   }
-  consumer_sync();
+  named_sync<BAR, NT>();
 }
 
 // Register blocking: each consumer thread accumulates an [MT][2*SG] block of outputs (MT output
@@ -950,6 +958,173 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
   if (sizeof(W) == 4 && tid < 32) bulk_wait_read0();  // shared memory stays valid until the stores have read it
   PROBE0(5);
   PROBE_CTA(1);
+  pdl_trigger();
+}
+
+// ------------------------------------------------------------------------------------------
+// k_mac_ws: the same computation as k_mac<uint32_t, SG, MT> (32-bit limbs), warp-specialised so that
+// a CTA's MAC and its inverse-NTT epilogue overlap across m-blocks. Warps 0-3 (128 threads, two
+// coefficients of the e-tile each) accumulate m-block i+1 while warps 4-7 run levels 0..7 of m-block
+// i on the other of two output-chunk buffers and bulk-store it; warp 8 streams the weights as in
+// k_mac. Hand-offs: cfull[b] (the 4 MAC warps arrive after writing buffer b's reduced sums) and
+// cempty[b] (the INTT store thread arrives once the bulk stores of b have read it). k_mac runs the
+// two phases back to back on all 8 warps, so within a CTA the weight ring sits idle during the
+// INTT and the integer pipes during the MAC's waits; here each m-block's phases hide the other's.
+constexpr int WS_HALF = MAC_THREADS / 2;  // threads per role (MAC, INTT)
+
+template <int SG, int MT>
+__global__ void __launch_bounds__(MAC_THREADS + 32, 2)
+    k_mac_ws(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmw, uint32_t* __restrict__ y,
+             const __grid_constant__ DevConsts c, PlanDev pl, int m_range, int n_sg, int NS, int n_pre) {
+  using W = uint32_t;
+  using AR = Arith32;
+  using Tw = uint2;
+  constexpr int A2 = 2 * SG, NCH = MT * A2;
+  static_assert(NCH <= 2 * WS_HALF / 16, "the dense round B keeps <= 2 tasks per INTT thread");
+  extern __shared__ __align__(128) unsigned char smraw[];
+  const int N = 1 << c.log_n, L = c.L, G = pl.G, S = pl.S;
+  const int j = blockIdx.y;
+  const int sgi = blockIdx.x % n_sg, et = blockIdx.x / n_sg;
+  const uint32_t e0 = et * MAC_THREADS;
+  const int s0 = (int)pl.s0 + sgi * SG;
+  const int ns = min(SG, (int)(pl.s0 + pl.sn) - s0);
+  const int m_begin = blockIdx.z * m_range, m_end = min((int)pl.M, m_begin + m_range);
+  const uint32_t row_bytes = MAC_THREADS * sizeof(W);
+  // shared memory: [G][2SG][256] X^ tile, [NS][MT][256] weight ring, [2][NCH][MAC_CHS] output
+  // chunks, [256] e-tile twiddles, 2 NS + 1 + 4 mbarriers
+  W* xs = reinterpret_cast<W*>(smraw);
+  W* ring = xs + (size_t)G * A2 * MAC_THREADS;
+  W* cbuf0 = ring + (size_t)NS * MT * MAC_THREADS;
+  Tw* twe = reinterpret_cast<Tw*>(cbuf0 + 2 * (size_t)NCH * MAC_CHS);
+  uint64_t* full = reinterpret_cast<uint64_t*>(twe + MAC_THREADS);
+  uint64_t* empty = full + NS;
+  uint64_t* xbar = empty + NS;
+  uint64_t* cfull = xbar + 1;
+  uint64_t* cempty = cfull + 2;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int st = 0; st < NS; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], WS_HALF / 32);
+    }
+    mbar_init(xbar, 1);
+    for (int b = 0; b < 2; ++b) mbar_init(&cfull[b], WS_HALF / 32), mbar_init(&cempty[b], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (tid >= MAC_THREADS) {  // ---- producer warp: as in k_mac ----
+    if (tid == MAC_THREADS) {
+      prefetch_tmap(&tmx);
+      prefetch_tmap(&tmw);
+      const uint64_t evict_first = policy_evict_first();
+      int st = 0, issued = 0;
+      uint32_t ph = 0, first = 1;
+      bool waited = false;
+      for (int mb = m_begin; mb < m_end; mb += MT) {
+        for (int g = 0; g < G; ++g) {
+          if (!waited && (!first || issued == n_pre)) {
+            pdl_wait();
+            waited = true;
+            mbar_arrive_expect_tx(xbar, G * A2 * row_bytes);
+            tma_load_4d(xs, &tmx, e0, j, 2 * s0, 0, xbar);
+          }
+          if (!first) mbar_wait(&empty[st], ph ^ 1);
+          mbar_arrive_expect_tx(&full[st], MT * row_bytes);
+          tma_load_3d_hint(ring + (size_t)st * MT * MAC_THREADS, &tmw, e0, g * L + j, mb, &full[st], evict_first);
+          ++issued;
+          if (++st == NS) st = 0, ph ^= 1, first = 0;
+        }
+      }
+      if (!waited) {
+        pdl_wait();
+        mbar_arrive_expect_tx(xbar, G * A2 * row_bytes);
+        tma_load_4d(xs, &tmx, e0, j, 2 * s0, 0, xbar);
+      }
+    }
+    return;
+  }
+
+  const uint32_t q = (uint32_t)c.q[j];
+  if (tid < WS_HALF) {  // ---- MAC warps: coefficients e0 + tid and e0 + tid + 128 ----
+    const uint32_t qn = (uint32_t)c.qneg_inv32[j];
+    const uint32_t r32 = (uint32_t)c.r32[j], r32p = (uint32_t)c.r32_p[j], onep32 = (uint32_t)(c.one_p[j] >> 32);
+    mbar_wait(xbar, 0);
+    int st = 0;
+    uint32_t ph = 0;
+    int nb = 0;
+    for (int mb = m_begin; mb < m_end; mb += MT, ++nb) {
+      uint64_t acc[MT][A2][2];
+#pragma unroll
+      for (int r = 0; r < MT; ++r)
+#pragma unroll
+        for (int a = 0; a < A2; ++a) acc[r][a][0] = acc[r][a][1] = 0;
+      for (int g = 0; g < G; ++g) {
+        uint32_t xv[A2][2];
+#pragma unroll
+        for (int a = 0; a < A2; ++a)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) xv[a][h] = xs[(g * A2 + a) * MAC_THREADS + tid + h * WS_HALF];
+        mbar_wait_sleep(&full[st], ph);
+        const W* wst = ring + (size_t)st * MT * MAC_THREADS + tid;
+#pragma unroll
+        for (int r = 0; r < MT; ++r)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t wv = wst[r * MAC_THREADS + h * WS_HALF];
+#pragma unroll
+            for (int a = 0; a < A2; ++a) acc[r][a][h] += (uint64_t)xv[a][h] * wv;  // < 2^56 each, G <= 32
+          }
+        consumer_release(&empty[st]);
+        if (++st == NS) st = 0, ph ^= 1;
+      }
+      const int b = nb & 1;
+      if (nb >= 2) mbar_wait(&cempty[b], ((nb >> 1) - 1) & 1);  // the INTT warps are done with buffer b
+      W* cb = cbuf0 + (size_t)b * NCH * MAC_CHS;
+#pragma unroll
+      for (int r = 0; r < MT; ++r)
+#pragma unroll
+        for (int a = 0; a < A2; ++a)
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            cb[(r * A2 + a) * MAC_CHS + phys(tid + h * WS_HALF)] =
+                c.mac_redc ? redc32(acc[r][a][h], q, qn) : reduce64(acc[r][a][h], q, r32, r32p, onep32);
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(&cfull[b]);  // release: the chunk writes precede it
+    }
+  } else {  // ---- INTT warps: levels 0..7 of each m-block's chunks, then the bulk stores ----
+    const int lt = tid - WS_HALF;
+    {  // the e-tile's inverse-NTT twiddles for levels 0..7
+      const Tw* tinv = Tab<AR>::inv(c) + (size_t)j * N;
+      for (int k = lt; k < 255; k += WS_HALF) {
+        int l = 0;
+        while (k >= 256 - (256 >> (l + 1))) ++l;
+        const int g = k - (256 - (256 >> l));
+        twe[twe_pos<Tw>(l, g)] = tinv[(N >> (l + 1)) + (e0 >> (l + 1)) + g];
+      }
+    }
+    named_sync<2, WS_HALF>();
+    int nb = 0;
+    for (int mb = m_begin; mb < m_end; mb += MT, ++nb) {
+      const int b = nb & 1, rows = min(MT, m_end - mb);
+      W* cb = cbuf0 + (size_t)b * NCH * MAC_CHS;
+      mbar_wait(&cfull[b], (nb >> 1) & 1);
+      mac_intt_levels_0_7<AR, true, WS_HALF, 2>(cb, twe, NCH, q, AR::bound(q), lt);  // dense chunks, proxy fence
+      if (lt < 32) {  // INTT warp 0: lane ch stores chunk ch (one 1 KiB row segment per output limb-poly)
+        const int r = lt / A2, a = lt % A2;
+        if (lt < NCH && r < rows && a < 2 * ns)
+          bulk_store_s2g(y + ((((size_t)(mb + r) * S + s0 + (a >> 1)) * 2 + (a & 1)) * L + j) * N + e0,
+                         cb + lt * MAC_CHS, MAC_THREADS * sizeof(W));
+        bulk_commit();
+        // the previous m-block's stores (the other buffer) have read their chunks: hand it back
+        if (nb >= 1) {
+          asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          if (lt == 0) mbar_arrive(&cempty[b ^ 1]);
+        }
+      }
+    }
+    if (lt < 32) bulk_wait_read0();  // shared memory stays valid until the stores have read it
+  }
   pdl_trigger();
 }
 
@@ -1542,6 +1717,7 @@ void read_tune(int device, Tune* t) {
   t->mac_sg = env_int("SECN_MAC_SG", 0);
   t->mac_mt = env_int("SECN_MAC_MT", 0);
   t->fused = env_int("SECN_FUSED", 0);
+  t->mac_ws = env_int("SECN_MAC_WS", 1);
   t->fused_sg = env_int("SECN_FUSED_SG", 0);
   t->fused_mt = env_int("SECN_FUSED_MT", 0);
   t->fused_kb = env_int("SECN_FUSED_KB", 112);
@@ -1773,15 +1949,16 @@ static bool encode_tmap(CUtensorMap* m, int wb, int rank, const void* base, cons
 }
 
 
-template <class W, int SG, int MT>
+// WS: the warp-specialised k_mac_ws (32-bit limbs, two output-chunk buffers) instead of k_mac
+template <class W, int SG, int MT, bool WS = false>
 static cudaError_t mac_t(const DevConsts& c, const PlanDev& p, const void* xhat, const void* w, void* y,
                          cudaStream_t s, bool chained) {
   const int N = 1 << c.log_n;
   const size_t xtile = (size_t)p.G * 2 * SG * MAC_THREADS * sizeof(W);
   const size_t stage = (size_t)MT * MAC_THREADS * sizeof(W);
   // ring depth: fill ~110 KiB per CTA (two CTAs per SM) after the X^ tile, 4..32 stages
-  const size_t chunks = (size_t)MT * 2 * SG * MAC_CHS * sizeof(W) + MAC_THREADS * 2 * sizeof(W);
-  const size_t fixed = xtile + chunks;
+  const size_t chunks = (size_t)MT * 2 * SG * MAC_CHS * sizeof(W) * (WS ? 2 : 1) + MAC_THREADS * 2 * sizeof(W);
+  const size_t fixed = xtile + chunks + (WS ? 4 * sizeof(uint64_t) : 0);
   const size_t cta_budget = (size_t)c.tune.mac_kb * 1024;
   const size_t budget = cta_budget > fixed + 4 * stage ? cta_budget - fixed : 4 * stage;
   int NS = (int)(budget / stage);
@@ -1808,7 +1985,9 @@ static cudaError_t mac_t(const DevConsts& c, const PlanDev& p, const void* xhat,
   }
   // layers with few input groups or few output channels: one m-block per CTA (more, shorter CTAs
   // hide the INTT-level latency better; measured on the SqueezeNet fire layers)
-  if (p.G <= 4 || p.M <= 48)
+  if (WS)  // the pipeline needs >= 2 m-blocks per CTA (its MAC of one overlaps the INTT of the last)
+    best_nmr = best_nmr < (mblocks + 1) / 2 ? best_nmr : (mblocks + 1) / 2;
+  else if (p.G <= 4 || p.M <= 48)
     best_nmr = mblocks;
   else if (xtile >= (size_t)MT * p.G * MAC_THREADS * sizeof(W) && c.tune.mac_xamort)
     // the X^ tile is at least one m-block of weights: a CTA takes >= 2 m-blocks so the tile load
@@ -1835,8 +2014,13 @@ static cudaError_t mac_t(const DevConsts& c, const PlanDev& p, const void* xhat,
   // ring stages issued before the dependency wait (and the X^ tile): only when the preceding
   // launch is this call's forward NTT, which never writes the weights (internal.h, "Pre-wait reads")
   const int n_pre = chained ? c.tune.mac_pre : 0;
-  cudaError_t e = launch_pdl(c, k_mac<W, SG, MT>, grid, dim3(MAC_THREADS + 32), smem, s, tmx, tmw, yp, cc, p, m_range,
-                             n_sg, NS, n_pre);
+  cudaError_t e;
+  if constexpr (WS)
+    e = launch_pdl(c, k_mac_ws<SG, MT>, grid, dim3(MAC_THREADS + 32), smem, s, tmx, tmw, yp, cc, p, m_range, n_sg, NS,
+                   n_pre);
+  else
+    e = launch_pdl(c, k_mac<W, SG, MT>, grid, dim3(MAC_THREADS + 32), smem, s, tmx, tmw, yp, cc, p, m_range, n_sg, NS,
+                   n_pre);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
@@ -1870,6 +2054,19 @@ cudaError_t launch_mac(const DevConsts& c, const PlanDev& p, const void* xhat, c
     };
     bool small = !fits2(mt_big[sg]) || (sg == 1 && xtile > 24 * 1024);
     if (const int mt_env = c.tune.mac_mt) small = mt_env == mt_small[sg];
+    // the warp-specialised pipeline (k_mac_ws) where its two phases balance: measured per layer on
+    // SqueezeNet-1.1 and ResNet-50 (profiles/r02_mac_ws_ab_*.txt): faster for one s-group, 5..22
+    // input groups and >= 48 channels (a tiny MAC phase, G <= 4 with M >= 256, leaves half its warps
+    // idle; a long one, G >= 25 or several s-groups, needs all eight); SECN_MAC_WS=0/2: never/always
+    const bool ws_rule = sg == 1 && p.G <= 22 && p.M >= 48 && !(p.G <= 4 && p.M >= 256);
+    if ((c.tune.mac_ws == 2 || (c.tune.mac_ws == 1 && ws_rule)) && (size_t)p.M > (size_t)mt_small[sg]) {
+      switch (sg) {
+        case 1: return mac_t<uint32_t, 1, 8, true>(c, p, xhat, w, y, s, chained);
+        case 2: return mac_t<uint32_t, 2, 4, true>(c, p, xhat, w, y, s, chained);
+        case 3: return mac_t<uint32_t, 3, 2, true>(c, p, xhat, w, y, s, chained);
+        default: return mac_t<uint32_t, 4, 2, true>(c, p, xhat, w, y, s, chained);
+      }
+    }
     if (small) {
       switch (sg) {
         case 1: return mac_t<uint32_t, 1, 8>(c, p, xhat, w, y, s, chained);
@@ -1932,6 +2129,8 @@ cudaError_t init_device(uint32_t word_bits) {
     chk(optin(k_mac<uint32_t, 3, 5>, b)), chk(optin(k_mac<uint32_t, 4, 3>, b));
     chk(optin(k_mac<uint32_t, 1, 8>, b)), chk(optin(k_mac<uint32_t, 2, 4>, b));
     chk(optin(k_mac<uint32_t, 3, 2>, b)), chk(optin(k_mac<uint32_t, 4, 2>, b));
+    chk(optin(k_mac_ws<1, 8>, b)), chk(optin(k_mac_ws<2, 4>, b)), chk(optin(k_mac_ws<3, 2>, b));
+    chk(optin(k_mac_ws<4, 2>, b));
     chk(optin(k_layer_fused<1, 1>, b)), chk(optin(k_layer_fused<1, 2>, b)), chk(optin(k_layer_fused<1, 4>, b));
     chk(optin(k_layer_fused<2, 1>, b)), chk(optin(k_layer_fused<2, 2>, b));
   }
