@@ -20,7 +20,7 @@ want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "smsp__inst_executed.sum", "sm__warps_active.avg.pct_of_peak_sustained_active",
         "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
         "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smsp__thread_inst_executed_per_inst_executed.ratio"]
-stall = [h for h in hdr if h.startswith("smsp__average_warp_latency_issue_stalled") and h.endswith(".ratio")]
+stall = [h for h in hdr if h.startswith("smsp__average_warps_issue_stalled_") and h.endswith("_per_issue_active.ratio")]
 for row in rows[2:]:
     print("=" * 100)
     print(row[ki][:110])
@@ -34,5 +34,5 @@ for row in rows[2:]:
         except ValueError:
             continue
         if v > 0.05:
-            st.append((v, h.replace("smsp__average_warp_latency_issue_stalled_", "").replace(".ratio", "")))
+            st.append((v, h.replace("smsp__average_warps_issue_stalled_", "").replace("_per_issue_active.ratio", "")))
     print("  stalls (cycles per issued instr):", ", ".join(f"{n}={v:.2f}" for v, n in sorted(st, reverse=True)[:8]))
