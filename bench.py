@@ -77,6 +77,12 @@ def parse():
                          "(default): every layer's at the start of the step, on a side stream beside the layer chain "
                          "(1.209 ms, profiles/r02h_*); lookahead: the next group's while a group runs (1.253 ms); "
                          "inline: inside the layer call, secn32_he_conv2d_gen (1.232 ms)")
+    ap.add_argument("--queries", type=int, default=1,
+                    help="B > 1: the batched-queries line instead -- B independent inferences per step (the "
+                         "north star's ciphertext batches), each on its own stream, weights shared; metric = "
+                         "inferences/s over all ranks (weak scaling: every rank runs its own B)")
+    ap.add_argument("--batched-leg", type=int, default=8,
+                    help="queries of the batched leg reported under 'batched_queries' in the default run (0: skip)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-online", action="store_true", help="skip the online-NTT-preprocessing (f4) leg")
@@ -213,7 +219,14 @@ def main():
         dist.barrier()
     if args.net == "ntt_sweep":
         return run_ntt_sweep_line(args, world, rank, local, dev)
+    if args.queries > 1:
+        return run_batched_line(args, world, rank, local, dev)
     out = run_secn(args, args.word_bits, world, rank, local, dev, full=True)
+    if args.batched_leg > 1:
+        torch.cuda.empty_cache()
+        bq = run_batched(args, args.batched_leg, world, rank, local, dev)
+        if rank == 0:
+            out["batched_queries"] = bq
     if not args.no_sweep:
         torch.cuda.empty_cache()
         sw = ntt_sweep(args, world, local, dev, word_bits=(args.word_bits,), steps=10)
@@ -226,6 +239,79 @@ def main():
         if rank == 0:
             out["companion"] = comp
     if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_batched(args, B, world, rank, local, dev):
+    """B independent inferences of the network per step (the ciphertext-batch axis): query b has
+    its own seeded inputs, device-drawn masks (stream id 1000 b + layer) and outputs and runs the
+    whole layer chain on its own stream; the weights are preprocessed once and shared. Captured as
+    one CUDA graph; device time with CUDA events (max over ranks; every rank runs its own B)."""
+    from paper_2506_11586_b200 import Context, MaskGen
+
+    ctx = Context(local, word_bits=args.word_bits)
+    L, n = ctx.L, ctx.n
+    net = layers.network(args.net)
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int64)).to(dev)  # noqa: E731
+    R = ((lambda a: T(a)) if ctx.word_bits == 64 else
+         (lambda a: torch.from_numpy(np.ascontiguousarray(a).astype(np.uint32).view(np.int32)).to(dev)))
+    lay_state = []
+    for li, lay in enumerate(net):
+        plan = ctx.plan(lay.C, lay.H, lay.W, lay.M, lay.k, stride=lay.stride, pad=lay.pad)
+        g = inputs.rng(args.seed * 1000 + li)
+        w = ctx.preprocess_weights(plan, T(inputs.quantized_kernel(g, plan.M, lay.C, lay.k, lay.k, ctx.t_bits)))
+        qs = []
+        for b in range(B):
+            gq = inputs.rng(10_000_000 + 1000 * (rank * B + b) + li)
+            qs.append({"ct": R(inputs.uniform_residues(gq, (plan.G * plan.S, 2), ctx.primes, n)),
+                       "x0": T(inputs.uniform_below(gq, (plan.G * plan.S, n), 1 << ctx.t_bits)),
+                       "gen": MaskGen(seed=mask_seed(args.seed), stream=1000 * (rank * B + b) + li, ct0=0),
+                       "em": ctx.empty(plan.M * plan.S, L, n), "out": ctx.empty(plan.M * plan.S, 2, L, n),
+                       "y0": torch.empty((plan.M, plan.OH, plan.OW), dtype=torch.int64, device=dev),
+                       "ws": torch.empty(ctx.workspace_bytes(plan) // 8 + 1, dtype=torch.int64, device=dev)})
+        lay_state.append((plan, w, qs))
+    streams = [torch.cuda.Stream(dev) for _ in range(B)]
+
+    def step():
+        main = torch.cuda.current_stream(dev)
+        for b, s in enumerate(streams):
+            s.wait_stream(main)
+            with torch.cuda.stream(s):
+                for plan, w, qs in lay_state:
+                    q = qs[b]
+                    ctx.mask_encode(plan, gen=q["gen"], out=q["em"], y0=q["y0"])
+                for plan, w, qs in lay_state:
+                    q = qs[b]
+                    ctx.he_conv2d_em(plan, q["ct"], w, q["em"], x0=q["x0"], out=q["out"], workspace=q["ws"])
+        for s in streams:
+            main.wait_stream(s)
+
+    ms = graph_ms(step, args.steps, max(args.warmup, 3), dev, world)
+    total = B * world
+    alg = sum(algorithmic_bytes(plan, L, n, ctx.word_bits // 8, True) for plan, _, _ in lay_state) * B
+    ctx.close()
+    return {"queries_per_gpu": B, "value": round(total / (ms / 1e3), 1), "unit": "inferences/s",
+            "ms_per_step": round(ms, 4), "latency_per_query_ms_upper": round(ms, 4),
+            "hbm_frac": round(alg / (ms / 1e3) / 1e9 / peaks()[0], 4),
+            "path": "per query: secn_mask_encode (drawn masks) then secn32_he_conv2d_em for every layer, on the "
+                    "query's own stream; B streams concurrently, weights shared"}
+
+
+def run_batched_line(args, world, rank, local, dev):
+    with ClockSampler(local) as clk:
+        bq = run_batched(args, args.queries, world, rank, local, dev)
+    if rank == 0:
+        out = {"metric": f"{args.net} HE-linear-layer throughput (inferences/s)", "value": bq["value"],
+               "unit": "inferences/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+               "ms_per_step": bq["ms_per_step"], "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+               "dtype": f"u{args.word_bits}", "data": "synthetic",
+               "config": {"workload": net_info(args.net)[1] + f", {args.queries} independent queries per GPU",
+                          "parallelism": f"query batches: {args.queries} per rank, no collective",
+                          "timing": "CUDA events around CUDA-graph replays (max over ranks)"},
+               "batched_queries": bq, "gpu_launches": None, "clocks": clk.summary()}
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.barrier()
