@@ -111,8 +111,9 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN, NP>(
   ct_twiddles<A, LOGN, 0>(tws, tw);
   pdl_wait();  // inputs may come from the preceding kernel
   // dependents (the mask draw, the MAC) may launch now: none reads this kernel's output before its
-  // own dependency wait, and the MAC's pre-wait weight loads are never produced here
-  pdl_trigger();
+  // own dependency wait, and the MAC's pre-wait weight loads are never produced here (the two-poly
+  // variant of the large batches triggers at its end: the early trigger costs it registers)
+  if constexpr (NP == 1) pdl_trigger();
   W x[NP][16];
 #pragma unroll
   for (int pp = 0; pp < NP; ++pp) {
@@ -146,6 +147,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN, NP>(
   __syncthreads();
   round_load<RL, W, NP, LOGN>(x, sm);
   ct_compute<A, LOGN, SL, NP>(x, tws, q, qb);
+  if constexpr (NP != 1) pdl_trigger();
 #pragma unroll
   for (int pp = 0; pp < NP; ++pp)
 #pragma unroll
