@@ -9,11 +9,21 @@
 
 #include "internal.h"
 
+#include <nvtx3/nvToolsExt.h>
+
 typedef unsigned __int128 u128;
 
 namespace {
 
 thread_local std::string g_err;
+
+// An NVTX range named after the entry point around every call that launches work (nsys/ncu
+// --nvtx timelines group the call's kernels under it; without a tool attached, a no-op).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+#define SECN_NVTX() NvtxRange secn_nvtx_range_(__func__)
 
 int fail(int status, const char* fmt, ...) {
   char buf[512];
@@ -336,11 +346,13 @@ static int ctx_create_impl(secn_ctx** out, int device, uint32_t log_n, uint32_t 
 
 int secn_ctx_create(secn_ctx** out, int device, uint32_t log_n, uint32_t n_limbs, const uint64_t* primes,
                     uint32_t t_bits) {
+  SECN_NVTX();
   return ctx_create_impl(out, device, log_n, n_limbs, primes, t_bits, 64);
 }
 
 int secn32_ctx_create(secn_ctx** out, int device, uint32_t log_n, uint32_t n_limbs, const uint32_t* primes,
                       uint32_t t_bits) {
+  SECN_NVTX();
   if (!primes) return fail(SECN_EINVAL, "NULL argument");
   uint64_t p64[SECN_MAX_LIMBS] = {0, 0, 0, 0};
   for (uint32_t j = 0; j < n_limbs && j < SECN_MAX_LIMBS; ++j) p64[j] = primes[j];
@@ -484,37 +496,47 @@ static int enc_add_impl(secn_ctx* ctx, uint32_t bits, void* ct, const uint64_t* 
 }
 
 int secn_ntt_fwd(secn_ctx* ctx, uint64_t* polys, size_t n_polys, void* stream) {
+  SECN_NVTX();
   return ntt_impl(ctx, 64, polys, n_polys, stream, false);
 }
 int secn_ntt_inv(secn_ctx* ctx, uint64_t* polys, size_t n_polys, void* stream) {
+  SECN_NVTX();
   return ntt_impl(ctx, 64, polys, n_polys, stream, true);
 }
 int secn32_ntt_fwd(secn_ctx* ctx, uint32_t* polys, size_t n_polys, void* stream) {
+  SECN_NVTX();
   return ntt_impl(ctx, 32, polys, n_polys, stream, false);
 }
 int secn32_ntt_inv(secn_ctx* ctx, uint32_t* polys, size_t n_polys, void* stream) {
+  SECN_NVTX();
   return ntt_impl(ctx, 32, polys, n_polys, stream, true);
 }
 
 int secn_preprocess_weights(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* kernel, uint64_t* w_ntt,
                             void* stream) {
+  SECN_NVTX();
   return preprocess_impl(ctx, 64, plan, kernel, w_ntt, stream);
 }
 int secn32_preprocess_weights(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* kernel, uint32_t* w_ntt,
                               void* stream) {
+  SECN_NVTX();
   return preprocess_impl(ctx, 32, plan, kernel, w_ntt, stream);
 }
 
 int secn_share_add(secn_ctx* ctx, uint64_t* ct, const uint64_t* x0, size_t n, void* stream) {
+  SECN_NVTX();
   return enc_add_impl(ctx, 64, ct, x0, n, stream, "secn_share_add");
 }
 int secn_mask_add(secn_ctx* ctx, uint64_t* ct, const uint64_t* r, size_t n, void* stream) {
+  SECN_NVTX();
   return enc_add_impl(ctx, 64, ct, r, n, stream, "secn_mask_add");
 }
 int secn32_share_add(secn_ctx* ctx, uint32_t* ct, const uint64_t* x0, size_t n, void* stream) {
+  SECN_NVTX();
   return enc_add_impl(ctx, 32, ct, x0, n, stream, "secn32_share_add");
 }
 int secn32_mask_add(secn_ctx* ctx, uint32_t* ct, const uint64_t* r, size_t n, void* stream) {
+  SECN_NVTX();
   return enc_add_impl(ctx, 32, ct, r, n, stream, "secn32_mask_add");
 }
 
@@ -597,18 +619,21 @@ static int he_conv2d_impl(secn_ctx* ctx, uint32_t bits, const secn_conv_plan_t* 
 int secn_he_conv2d(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* ct_in, const uint64_t* x0,
                    const uint64_t* w_ntt, const uint64_t* r, uint64_t* ct_out, void* workspace, size_t ws_bytes,
                    void* stream) {
+  SECN_NVTX();
   return he_conv2d_impl(ctx, 64, plan, -1, ct_in, x0, w_ntt, r, ct_out, nullptr, workspace, ws_bytes, stream);
 }
 
 int secn_he_conv2d_ex(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* ct_in, const uint64_t* x0,
                       const uint64_t* w_ntt, const uint64_t* r, uint64_t* ct_out, uint64_t* y0, void* workspace,
                       size_t ws_bytes, void* stream) {
+  SECN_NVTX();
   return he_conv2d_impl(ctx, 64, plan, -1, ct_in, x0, w_ntt, r, ct_out, y0, workspace, ws_bytes, stream);
 }
 
 int secn32_he_conv2d_ex(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint32_t* ct_in, const uint64_t* x0,
                         const uint32_t* w_ntt, const uint64_t* r, uint32_t* ct_out, uint64_t* y0, void* workspace,
                         size_t ws_bytes, void* stream) {
+  SECN_NVTX();
   return he_conv2d_impl(ctx, 32, plan, -1, ct_in, x0, w_ntt, r, ct_out, y0, workspace, ws_bytes, stream);
 }
 
@@ -639,11 +664,13 @@ static int he_conv2d_gen_impl(secn_ctx* ctx, uint32_t bits, const secn_conv_plan
 int secn_he_conv2d_gen(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* ct_in, const uint64_t* x0,
                        const uint64_t* w_ntt, const secn_mask_gen_t* gen, uint64_t* ct_out, uint64_t* y0,
                        void* workspace, size_t ws_bytes, void* stream) {
+  SECN_NVTX();
   return he_conv2d_gen_impl(ctx, 64, plan, ct_in, x0, w_ntt, gen, ct_out, y0, workspace, ws_bytes, stream);
 }
 int secn32_he_conv2d_gen(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint32_t* ct_in, const uint64_t* x0,
                          const uint32_t* w_ntt, const secn_mask_gen_t* gen, uint32_t* ct_out, uint64_t* y0,
                          void* workspace, size_t ws_bytes, void* stream) {
+  SECN_NVTX();
   return he_conv2d_gen_impl(ctx, 32, plan, ct_in, x0, w_ntt, gen, ct_out, y0, workspace, ws_bytes, stream);
 }
 
@@ -654,6 +681,7 @@ size_t secn_mask_encoded_bytes(const secn_ctx* ctx, const secn_conv_plan_t* plan
 
 int secn_mask_encode(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* r, const secn_mask_gen_t* gen,
                      void* em, uint64_t* y0, void* stream) {
+  SECN_NVTX();
   if (int st = check_ctx(ctx)) return st;
   if (int st = check_plan(ctx, plan)) return st;
   if (!em || (!r && !gen) || (r && gen)) return fail(SECN_EINVAL, "need em and exactly one of r, gen");
@@ -679,15 +707,18 @@ static int he_conv2d_em_impl(secn_ctx* ctx, uint32_t bits, const secn_conv_plan_
 int secn_he_conv2d_em(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* ct_in, const uint64_t* x0,
                       const uint64_t* w_ntt, const uint64_t* em, uint64_t* ct_out, void* workspace, size_t ws_bytes,
                       void* stream) {
+  SECN_NVTX();
   return he_conv2d_em_impl(ctx, 64, plan, ct_in, x0, w_ntt, em, ct_out, workspace, ws_bytes, stream);
 }
 int secn32_he_conv2d_em(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint32_t* ct_in, const uint64_t* x0,
                         const uint32_t* w_ntt, const uint32_t* em, uint32_t* ct_out, void* workspace, size_t ws_bytes,
                         void* stream) {
+  SECN_NVTX();
   return he_conv2d_em_impl(ctx, 32, plan, ct_in, x0, w_ntt, em, ct_out, workspace, ws_bytes, stream);
 }
 
 int secn_mask_draw(secn_ctx* ctx, const secn_mask_gen_t* gen, size_t n_ct, uint64_t* r, void* stream) {
+  SECN_NVTX();
   if (int st = check_ctx(ctx)) return st;
   secn::MaskGen g;
   if (int st = check_gen(gen, &g)) return st;
@@ -723,12 +754,14 @@ static int he_conv2d_online_impl(secn_ctx* ctx, uint32_t bits, const secn_conv_p
 int secn_he_conv2d_online(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* ct_in, const uint64_t* x0,
                           const uint64_t* kernel, const uint64_t* r, uint64_t* ct_out, uint64_t* y0, void* workspace,
                           size_t ws_bytes, void* stream) {
+  SECN_NVTX();
   return he_conv2d_online_impl(ctx, 64, plan, ct_in, x0, kernel, r, ct_out, y0, workspace, ws_bytes, stream);
 }
 
 int secn32_he_conv2d_online(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint32_t* ct_in, const uint64_t* x0,
                             const uint64_t* kernel, const uint64_t* r, uint32_t* ct_out, uint64_t* y0,
                             void* workspace, size_t ws_bytes, void* stream) {
+  SECN_NVTX();
   return he_conv2d_online_impl(ctx, 32, plan, ct_in, x0, kernel, r, ct_out, y0, workspace, ws_bytes, stream);
 }
 
@@ -822,20 +855,24 @@ static int he_fc_impl(secn_ctx* ctx, uint32_t bits, const secn_fc_plan_t* plan, 
 
 int secn_fc_preprocess_weights(secn_ctx* ctx, const secn_fc_plan_t* plan, const uint64_t* W, uint64_t* w_ntt,
                                void* stream) {
+  SECN_NVTX();
   return fc_preprocess_impl(ctx, 64, plan, W, w_ntt, stream);
 }
 int secn32_fc_preprocess_weights(secn_ctx* ctx, const secn_fc_plan_t* plan, const uint64_t* W, uint32_t* w_ntt,
                                  void* stream) {
+  SECN_NVTX();
   return fc_preprocess_impl(ctx, 32, plan, W, w_ntt, stream);
 }
 int secn_he_fc(secn_ctx* ctx, const secn_fc_plan_t* plan, const uint64_t* ct_in, const uint64_t* x0,
                const uint64_t* w_ntt, const uint64_t* r, uint64_t* ct_out, uint64_t* y0, void* workspace,
                size_t ws_bytes, void* stream) {
+  SECN_NVTX();
   return he_fc_impl(ctx, 64, plan, ct_in, x0, w_ntt, r, ct_out, y0, workspace, ws_bytes, stream);
 }
 int secn32_he_fc(secn_ctx* ctx, const secn_fc_plan_t* plan, const uint32_t* ct_in, const uint64_t* x0,
                  const uint32_t* w_ntt, const uint64_t* r, uint32_t* ct_out, uint64_t* y0, void* workspace,
                  size_t ws_bytes, void* stream) {
+  SECN_NVTX();
   return he_fc_impl(ctx, 32, plan, ct_in, x0, w_ntt, r, ct_out, y0, workspace, ws_bytes, stream);
 }
 
@@ -942,12 +979,14 @@ static int he_conv2d_lwe_em_impl(secn_ctx* ctx, uint32_t bits, const secn_conv_p
 int secn_he_conv2d_lwe_em(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* ct_in, const uint64_t* x0,
                           const uint64_t* w_ntt, const uint64_t* em, uint32_t keep_limbs, uint64_t* a_out,
                           uint64_t* b_out, void* workspace, size_t ws_bytes, void* stream) {
+  SECN_NVTX();
   return he_conv2d_lwe_em_impl(ctx, 64, plan, ct_in, x0, w_ntt, em, keep_limbs, a_out, b_out, workspace, ws_bytes,
                                stream);
 }
 int secn32_he_conv2d_lwe_em(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint32_t* ct_in, const uint64_t* x0,
                             const uint32_t* w_ntt, const uint32_t* em, uint32_t keep_limbs, uint32_t* a_out,
                             uint32_t* b_out, void* workspace, size_t ws_bytes, void* stream) {
+  SECN_NVTX();
   return he_conv2d_lwe_em_impl(ctx, 32, plan, ct_in, x0, w_ntt, em, keep_limbs, a_out, b_out, workspace, ws_bytes,
                                stream);
 }
@@ -955,12 +994,14 @@ int secn32_he_conv2d_lwe_em(secn_ctx* ctx, const secn_conv_plan_t* plan, const u
 int secn_he_conv2d_lwe_gen(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* ct_in, const uint64_t* x0,
                            const uint64_t* w_ntt, const secn_mask_gen_t* gen, uint32_t keep_limbs, uint64_t* a_out,
                            uint64_t* b_out, uint64_t* y0, void* workspace, size_t ws_bytes, void* stream) {
+  SECN_NVTX();
   return he_conv2d_lwe_gen_impl(ctx, 64, plan, ct_in, x0, w_ntt, gen, keep_limbs, a_out, b_out, y0, workspace,
                                 ws_bytes, stream);
 }
 int secn32_he_conv2d_lwe_gen(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint32_t* ct_in, const uint64_t* x0,
                              const uint32_t* w_ntt, const secn_mask_gen_t* gen, uint32_t keep_limbs, uint32_t* a_out,
                              uint32_t* b_out, uint64_t* y0, void* workspace, size_t ws_bytes, void* stream) {
+  SECN_NVTX();
   return he_conv2d_lwe_gen_impl(ctx, 32, plan, ct_in, x0, w_ntt, gen, keep_limbs, a_out, b_out, y0, workspace,
                                 ws_bytes, stream);
 }
@@ -968,12 +1009,14 @@ int secn32_he_conv2d_lwe_gen(secn_ctx* ctx, const secn_conv_plan_t* plan, const 
 int secn_he_conv2d_lwe(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* ct_in, const uint64_t* x0,
                        const uint64_t* w_ntt, const uint64_t* r, uint32_t keep_limbs, uint64_t* a_out,
                        uint64_t* b_out, uint64_t* y0, void* workspace, size_t ws_bytes, void* stream) {
+  SECN_NVTX();
   return he_conv2d_lwe_impl(ctx, 64, plan, ct_in, x0, w_ntt, r, keep_limbs, a_out, b_out, y0, workspace, ws_bytes,
                             stream);
 }
 int secn32_he_conv2d_lwe(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint32_t* ct_in, const uint64_t* x0,
                          const uint32_t* w_ntt, const uint64_t* r, uint32_t keep_limbs, uint32_t* a_out,
                          uint32_t* b_out, uint64_t* y0, void* workspace, size_t ws_bytes, void* stream) {
+  SECN_NVTX();
   return he_conv2d_lwe_impl(ctx, 32, plan, ct_in, x0, w_ntt, r, keep_limbs, a_out, b_out, y0, workspace, ws_bytes,
                             stream);
 }
@@ -1014,17 +1057,20 @@ static int he_fc_lwe_impl(secn_ctx* ctx, uint32_t bits, const secn_fc_plan_t* pl
 int secn_he_fc_lwe(secn_ctx* ctx, const secn_fc_plan_t* plan, const uint64_t* ct_in, const uint64_t* x0,
                    const uint64_t* w_ntt, const uint64_t* r, uint32_t keep_limbs, uint64_t* a_out, uint64_t* b_out,
                    uint64_t* y0, void* workspace, size_t ws_bytes, void* stream) {
+  SECN_NVTX();
   return he_fc_lwe_impl(ctx, 64, plan, ct_in, x0, w_ntt, r, keep_limbs, a_out, b_out, y0, workspace, ws_bytes, stream);
 }
 int secn32_he_fc_lwe(secn_ctx* ctx, const secn_fc_plan_t* plan, const uint32_t* ct_in, const uint64_t* x0,
                      const uint32_t* w_ntt, const uint64_t* r, uint32_t keep_limbs, uint32_t* a_out, uint32_t* b_out,
                      uint64_t* y0, void* workspace, size_t ws_bytes, void* stream) {
+  SECN_NVTX();
   return he_fc_lwe_impl(ctx, 32, plan, ct_in, x0, w_ntt, r, keep_limbs, a_out, b_out, y0, workspace, ws_bytes, stream);
 }
 
 int secn_he_conv2d_stage(secn_ctx* ctx, const secn_conv_plan_t* plan, int stage, const uint64_t* ct_in,
                          const uint64_t* x0, const uint64_t* w_ntt, const uint64_t* r, uint64_t* ct_out,
                          void* workspace, size_t ws_bytes, void* stream) {
+  SECN_NVTX();
   if (stage < 0 || stage > 2) return fail(SECN_EINVAL, "stage %d not in {0,1,2}", stage);
   return he_conv2d_impl(ctx, 64, plan, stage, ct_in, x0, w_ntt, r, ct_out, nullptr, workspace, ws_bytes, stream);
 }
@@ -1032,12 +1078,14 @@ int secn_he_conv2d_stage(secn_ctx* ctx, const secn_conv_plan_t* plan, int stage,
 int secn32_he_conv2d(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint32_t* ct_in, const uint64_t* x0,
                      const uint32_t* w_ntt, const uint64_t* r, uint32_t* ct_out, void* workspace, size_t ws_bytes,
                      void* stream) {
+  SECN_NVTX();
   return he_conv2d_impl(ctx, 32, plan, -1, ct_in, x0, w_ntt, r, ct_out, nullptr, workspace, ws_bytes, stream);
 }
 
 int secn32_he_conv2d_stage(secn_ctx* ctx, const secn_conv_plan_t* plan, int stage, const uint32_t* ct_in,
                            const uint64_t* x0, const uint32_t* w_ntt, const uint64_t* r, uint32_t* ct_out,
                            void* workspace, size_t ws_bytes, void* stream) {
+  SECN_NVTX();
   if (stage < 0 || stage > 2) return fail(SECN_EINVAL, "stage %d not in {0,1,2}", stage);
   return he_conv2d_impl(ctx, 32, plan, stage, ct_in, x0, w_ntt, r, ct_out, nullptr, workspace, ws_bytes, stream);
 }
@@ -1045,6 +1093,7 @@ int secn32_he_conv2d_stage(secn_ctx* ctx, const secn_conv_plan_t* plan, int stag
 int secn_he_conv2d_stage_ex(secn_ctx* ctx, const secn_conv_plan_t* plan, int stage, const uint64_t* ct_in,
                             const uint64_t* x0, const uint64_t* w_ntt, const uint64_t* r, uint64_t* ct_out, uint64_t* y0,
                             void* workspace, size_t ws_bytes, void* stream) {
+  SECN_NVTX();
   if (stage < 0 || stage > 2) return fail(SECN_EINVAL, "stage %d not in {0,1,2}", stage);
   return he_conv2d_impl(ctx, 64, plan, stage, ct_in, x0, w_ntt, r, ct_out, y0, workspace, ws_bytes, stream);
 }
@@ -1052,11 +1101,13 @@ int secn_he_conv2d_stage_ex(secn_ctx* ctx, const secn_conv_plan_t* plan, int sta
 int secn32_he_conv2d_stage_ex(secn_ctx* ctx, const secn_conv_plan_t* plan, int stage, const uint32_t* ct_in,
                               const uint64_t* x0, const uint32_t* w_ntt, const uint64_t* r, uint32_t* ct_out,
                               uint64_t* y0, void* workspace, size_t ws_bytes, void* stream) {
+  SECN_NVTX();
   if (stage < 0 || stage > 2) return fail(SECN_EINVAL, "stage %d not in {0,1,2}", stage);
   return he_conv2d_impl(ctx, 32, plan, stage, ct_in, x0, w_ntt, r, ct_out, y0, workspace, ws_bytes, stream);
 }
 
 int secn_extract_share(secn_ctx* ctx, const secn_conv_plan_t* plan, const uint64_t* r, uint64_t* y0, void* stream) {
+  SECN_NVTX();
   if (int st = check_ctx(ctx)) return st;
   if (int st = check_plan(ctx, plan)) return st;
   if (!r || !y0) return fail(SECN_EINVAL, "NULL buffer");

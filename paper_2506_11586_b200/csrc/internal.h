@@ -20,6 +20,8 @@ namespace secn {
 struct Tune {
   int32_t no_pdl;       // SECN_NO_PDL=1: plain stream order instead of programmatic dependent launch
   int32_t ntt_np2_min;  // SECN_NTT_NP2_MIN: limb-polys from which N = 4096 32-bit NTTs pair two polys per CTA
+  int32_t ntt_tma;      // SECN_NTT_TMA: plain calls on the TMA-staged engine -- 0 never, 1 measured rule, 2 always
+  int32_t ntt_tma_min;  // SECN_NTT_TMA_MIN: limb-polys from which the plain calls use the TMA-staged engine
   int32_t tail1;        // SECN_TAIL1=1: one-component INTT tail at N = 4096
   int32_t mac_kb;       // SECN_MAC_KB: k_mac shared-memory budget per CTA (KiB)
   int32_t mac_xamort;   // SECN_MAC_XAMORT=0: no X^-tile amortisation rule

@@ -99,7 +99,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN, NP>(
               const uint64_t* __restrict__ x0) {
   using W = typename A::W;
   using R0 = CtRound<LOGN, 0>;
-  constexpr int N = 1 << LOGN, T = N / 16;
+  constexpr int N = 1 << LOGN;
   extern __shared__ __align__(16) unsigned char smraw[];
   W* sm = reinterpret_cast<W*>(smraw);
   const int j = (int)(blockIdx.x % c.L);
@@ -165,7 +165,7 @@ template <class A, int LOGN, int NP>
 __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN, NP>())
     k_ntt_inv(typename A::W* polys, const __grid_constant__ DevConsts c) {
   using W = typename A::W;
-  constexpr int N = 1 << LOGN, T = N / 16;
+  constexpr int N = 1 << LOGN;
   constexpr int LL = GsLast<LOGN>::value;
   using RL = GsRound<LOGN, LL>;
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -209,6 +209,237 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN, NP>(
 #pragma unroll
       for (int i = 0; i < RL::GK; ++i) buf[RL::addr(k, i)] = A::canon_gs(x[pp][k * RL::GK + i], q);
   }
+}
+
+// ------------------------------------------------------------------------------------------
+// C5 NTT engine for the plain batched calls (secn_ntt_fwd / secn_ntt_inv, weight preprocessing):
+// persistent CTAs, each bound to one limb j, loop over items of NP limb-polys of that limb. Items
+// arrive by TMA (cp.async.bulk.tensor through a 4-D map: 128-byte rows x rows x limb x poly,
+// 128-byte swizzle) in two alternating buffers, and every radix-16 round works IN PLACE in the
+// buffer the item landed in. The TMA of item i+1 (into the other buffer) is issued at item i's
+// first barrier -- by then every thread has finished item i-1, the other buffer's last user --
+// so the load overlaps item i's rounds, no global load sits on the critical path (the
+// one-CTA-per-poly kernels above stall on their loads: profiles/r02s_ntt_full_summary.txt) and
+// no barrier is added. The buffers keep TMA's swizzled layout: word e of a poly sits at
+// stage_swz(e) (the 16-byte chunk index XOR the 128-byte row index mod 8), under which the
+// rounds with contiguous tasks move whole 16-byte chunks conflict-free (LDS.128 / STS.128), the
+// rounds with task stride >= 256 words are conflict-free word by word, and the stride-16 round
+// has 2-way conflicts on 32-bit words (bank-conflict model: tools/ntt_bank_model.py).
+template <class W>
+__host__ __device__ __forceinline__ constexpr uint32_t stage_swz(uint32_t e) {
+  constexpr int lw = sizeof(W) == 4 ? 2 : 3;  // log2 of the word size
+  return e ^ (((e >> (7 - lw)) & 7) << (4 - lw));
+}
+
+#ifndef SECN_TMA_NP12
+#define SECN_TMA_NP12 1
+#endif
+#ifndef SECN_TMA_MINB12
+#define SECN_TMA_MINB12 3
+#endif
+// polys per item and CTAs per SM (two buffers of NP polys per CTA: 64 KiB for 32-bit words at
+// N = 4096 with NP = 2 -> 3 per SM; the register cap is 65536 / (N/16 x CTAs per SM))
+template <class A, int LOGN>
+__host__ __device__ constexpr int ntt_tma_np() { return SECN_TMA_NP12 && sizeof(typename A::W) == 4 && LOGN == 12 ? 2 : 1; }
+template <class A, int LOGN>
+__host__ __device__ constexpr int ntt_tma_minb() { return LOGN == 12 ? (sizeof(typename A::W) == 4 ? SECN_TMA_MINB12 : 2) : LOGN == 13 && sizeof(typename A::W) == 4 ? 2 : 1; }
+template <class A, int LOGN>
+constexpr size_t ntt_tma_smem() {
+  return 1024 + 2 * (size_t)ntt_tma_np<A, LOGN>() * (1 << LOGN) * sizeof(typename A::W) + 16;
+}
+
+// round R's words of NP polys (poly pp at buf + pp N) <-> registers, in the swizzled layout
+template <class R, class W, int NP, int N>
+__device__ __forceinline__ void sw_load(W (&x)[NP][16], const W* buf) {
+  constexpr int VW = 16 / (int)sizeof(W);
+  if constexpr (R::logD == 0 && R::GK >= VW) {  // contiguous tasks: whole 16-byte chunks
+#pragma unroll
+    for (int k = 0; k < R::NT; ++k)
+#pragma unroll
+      for (int pp = 0; pp < NP; ++pp)
+#pragma unroll
+        for (int v = 0; v < R::GK / VW; ++v) {
+          const uint4 t = *reinterpret_cast<const uint4*>(buf + pp * N + stage_swz<W>(R::addr(k, v * VW)));
+          const W* tv = reinterpret_cast<const W*>(&t);
+#pragma unroll
+          for (int u = 0; u < VW; ++u) x[pp][k * R::GK + v * VW + u] = tv[u];
+        }
+  } else {
+#pragma unroll
+    for (int k = 0; k < R::NT; ++k)
+#pragma unroll
+      for (int pp = 0; pp < NP; ++pp)
+#pragma unroll
+        for (int i = 0; i < R::GK; ++i) x[pp][k * R::GK + i] = buf[pp * N + stage_swz<W>(R::addr(k, i))];
+  }
+}
+
+template <class R, class W, int NP, int N>
+__device__ __forceinline__ void sw_store(const W (&x)[NP][16], W* buf) {
+  constexpr int VW = 16 / (int)sizeof(W);
+  if constexpr (R::logD == 0 && R::GK >= VW) {
+#pragma unroll
+    for (int k = 0; k < R::NT; ++k)
+#pragma unroll
+      for (int pp = 0; pp < NP; ++pp)
+#pragma unroll
+        for (int v = 0; v < R::GK / VW; ++v) {
+          uint4 t;
+          W* tv = reinterpret_cast<W*>(&t);
+#pragma unroll
+          for (int u = 0; u < VW; ++u) tv[u] = x[pp][k * R::GK + v * VW + u];
+          *reinterpret_cast<uint4*>(buf + pp * N + stage_swz<W>(R::addr(k, v * VW))) = t;
+        }
+  } else {
+#pragma unroll
+    for (int k = 0; k < R::NT; ++k)
+#pragma unroll
+      for (int pp = 0; pp < NP; ++pp)
+#pragma unroll
+        for (int i = 0; i < R::GK; ++i) buf[pp * N + stage_swz<W>(R::addr(k, i))] = x[pp][k * R::GK + i];
+  }
+}
+
+// CT rounds S0.. (in place, swizzled) up to but not including the last one; the first of them
+// (S0 = 4) is preceded by the item's first barrier, where `at_first_barrier` runs
+template <class A, int LOGN, int S0, int NP, class F>
+__device__ __forceinline__ void ct_rounds_sw(typename A::W* buf, const typename A::Tw* __restrict__ tw,
+                                             typename A::W q, typename A::W qb, F&& at_first_barrier) {
+  using R = CtRound<LOGN, S0>;
+  if constexpr (S0 + R::K < LOGN) {
+    typename A::Tw tws[15];
+    ct_twiddles<A, LOGN, S0>(tws, tw);
+    if constexpr (S0 == 4) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if constexpr (S0 == 4) at_first_barrier();
+    typename A::W x[NP][16];
+    sw_load<R, typename A::W, NP, 1 << LOGN>(x, buf);
+    ct_compute<A, LOGN, S0, NP>(x, tws, q, qb);
+    sw_store<R, typename A::W, NP, 1 << LOGN>(x, buf);
+    ct_rounds_sw<A, LOGN, S0 + R::K, NP>(buf, tw, q, qb, at_first_barrier);
+  }
+}
+
+template <class A, int LOGN, int L0, int NP, class F>
+__device__ __forceinline__ void gs_rounds_sw(typename A::W* buf, const typename A::Tw* __restrict__ tw,
+                                             typename A::W q, typename A::W qb, typename A::Tw ninv,
+                                             typename A::Tw wlast, F&& at_first_barrier) {
+  using R = GsRound<LOGN, L0>;
+  if constexpr (L0 + R::K < LOGN) {
+    typename A::Tw tws[15];
+    gs_twiddles<A, LOGN, L0>(tws, tw);
+    if constexpr (L0 == 4) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if constexpr (L0 == 4) at_first_barrier();
+    typename A::W x[NP][16];
+    sw_load<R, typename A::W, NP, 1 << LOGN>(x, buf);
+    gs_compute<A, LOGN, L0, NP>(x, tws, q, qb, ninv, wlast);
+    sw_store<R, typename A::W, NP, 1 << LOGN>(x, buf);
+    gs_rounds_sw<A, LOGN, L0 + R::K, NP>(buf, tw, q, qb, ninv, wlast, at_first_barrier);
+  }
+}
+
+template <class A, int LOGN, bool INV>
+__global__ void __launch_bounds__((1 << LOGN) / 16, ntt_tma_minb<A, LOGN>())
+    k_ntt_tma(const __grid_constant__ CUtensorMap tm, typename A::W* out, const __grid_constant__ DevConsts c,
+              uint32_t n_polys) {
+  using W = typename A::W;
+  using Tw = typename A::Tw;
+  constexpr int N = 1 << LOGN, NP = ntt_tma_np<A, LOGN>();
+  constexpr int RW = 128 / (int)sizeof(W), ROWS = N / RW, BR = ROWS < 256 ? ROWS : 256;
+  static_assert(LOGN >= 12, "the first internal barrier is the one before round S0 = 4, and a later round exists");
+  extern __shared__ __align__(1024) unsigned char smraw_tma[];
+  W* bufs = reinterpret_cast<W*>(smraw_tma + ((1024 - (smem_u32(smraw_tma) & 1023)) & 1023));  // swizzle atoms
+  uint64_t* bar = reinterpret_cast<uint64_t*>(bufs + 2 * NP * N);
+  const uint32_t L = c.L, j = blockIdx.x % L, per_limb = gridDim.x / L;
+  const uint32_t n_items = (n_polys + NP - 1) / NP;
+  const W q = (W)c.q[j], qb = A::bound(q);
+  const Tw* tw = (INV ? Tab<A>::inv(c) : Tab<A>::fwd(c)) + (size_t)j * N;
+  const Tw ninv = Tab<A>::pair(c.ninv[j], c.ninv_p[j]), wl = Tab<A>::pair(c.wlast[j], c.wlast_p[j]);
+  const auto issue = [&](uint32_t item, int b) {  // one thread: the item's NP polys (zero-filled past n_polys)
+    mbar_arrive_expect_tx(&bar[b], (uint32_t)(NP * N * sizeof(W)));
+#pragma unroll
+    for (int pp = 0; pp < NP; ++pp)
+#pragma unroll
+      for (int k = 0; k < ROWS / BR; ++k)
+        tma_load_4d(bufs + (b * NP + pp) * N + k * BR * RW, &tm, 0, k * BR, (int)j, (int)(item * NP + pp), &bar[b]);
+  };
+  if (threadIdx.x == 0) {
+    prefetch_tmap(&tm);
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  pdl_wait();  // the polys may come from the preceding kernel
+  uint32_t it = blockIdx.x / L;
+  if (threadIdx.x == 0 && it < n_items) issue(it, 0);
+  for (uint32_t k = 0; it < n_items; it += per_limb, ++k) {
+    const int b = (int)(k & 1);
+    W* buf = bufs + b * NP * N;
+    const uint32_t nxt = it + per_limb;
+    const auto at_first_barrier = [&] {
+      if (threadIdx.x == 0 && nxt < n_items) issue(nxt, b ^ 1);
+    };
+    const uint32_t p0 = it * NP;
+    W x[NP][16];
+    Tw tws[15];
+    if constexpr (!INV) {
+      using R0 = CtRound<LOGN, 0>;
+      constexpr int SL = CtLast<LOGN>::value;
+      using RL = CtRound<LOGN, SL>;
+      ct_twiddles<A, LOGN, 0>(tws, tw);
+      mbar_wait(&bar[b], (k >> 1) & 1);
+      sw_load<R0, W, NP, N>(x, buf);
+      ct_compute<A, LOGN, 0, NP>(x, tws, q, qb);
+      sw_store<R0, W, NP, N>(x, buf);
+      ct_rounds_sw<A, LOGN, R0::K, NP>(buf, tw, q, qb, at_first_barrier);
+      ct_twiddles<A, LOGN, SL>(tws, tw);
+      __syncthreads();
+      sw_load<RL, W, NP, N>(x, buf);
+      ct_compute<A, LOGN, SL, NP>(x, tws, q, qb);
+#pragma unroll
+      for (int pp = 0; pp < NP; ++pp)
+#pragma unroll
+        for (int i = 0; i < 16; ++i) x[pp][i] = A::canon_ct(x[pp][i], q);
+      W* dst[NP];
+#pragma unroll
+      for (int pp = 0; pp < NP; ++pp) dst[pp] = out + ((size_t)(p0 + pp) * L + j) * N;
+      if (NP == 1 || p0 + NP <= n_polys) {
+        round_gstore<RL, W, NP>(x, dst);
+      } else {  // odd tail: the item's second poly does not exist
+        W y[1][16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) y[0][i] = x[0][i];
+        W* d1[1] = {dst[0]};
+        round_gstore<RL, W, 1>(y, d1);
+      }
+    } else {
+      using R0 = GsRound<LOGN, 0>;
+      constexpr int LL = GsLast<LOGN>::value;
+      using RL = GsRound<LOGN, LL>;
+      gs_twiddles<A, LOGN, 0>(tws, tw);
+      mbar_wait(&bar[b], (k >> 1) & 1);
+      sw_load<R0, W, NP, N>(x, buf);
+      gs_compute<A, LOGN, 0, NP>(x, tws, q, qb, ninv, wl);
+      sw_store<R0, W, NP, N>(x, buf);
+      gs_rounds_sw<A, LOGN, R0::K, NP>(buf, tw, q, qb, ninv, wl, at_first_barrier);
+      gs_twiddles<A, LOGN, LL>(tws, tw);
+      __syncthreads();
+      sw_load<RL, W, NP, N>(x, buf);
+      gs_compute<A, LOGN, LL, NP>(x, tws, q, qb, ninv, wl);
+#pragma unroll
+      for (int pp = 0; pp < NP; ++pp) {
+        if (pp > 0 && p0 + pp >= n_polys) break;
+        W* o = out + ((size_t)(p0 + pp) * L + j) * N;
+#pragma unroll
+        for (int kk = 0; kk < RL::NT; ++kk)
+#pragma unroll
+          for (int i = 0; i < RL::GK; ++i) o[RL::addr(kk, i)] = A::canon_gs(x[pp][kk * RL::GK + i], q);
+      }
+    }
+  }
+  pdl_trigger();
 }
 
 // ------------------------------------------------------------------------------------------
@@ -773,7 +1004,7 @@ template <class W, int SG, int MT>
 __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
     k_mac(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmw, W* __restrict__ y,
           const __grid_constant__ DevConsts c, PlanDev pl, int m_range, int n_sg, int NS, int n_pre) {
-  extern __shared__ __align__(128) unsigned char smraw[];
+  extern __shared__ __align__(128) unsigned char smraw_mac[];
   PROBE_CTA(0);
   PROBE0(0);
   constexpr int A2 = 2 * SG;
@@ -789,7 +1020,7 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
   using Tw = typename AR::Tw;
   // shared memory: [G][2SG][256] X^ tile, [NS][MT][256] weight ring, [MT*2SG][MAC_CHS] output
   // chunks, [256] e-tile twiddles, 2*NS + 1 mbarriers
-  W* xs = reinterpret_cast<W*>(smraw);
+  W* xs = reinterpret_cast<W*>(smraw_mac);
   W* ring = xs + (size_t)G * A2 * MAC_THREADS;
   W* cbuf = ring + (size_t)NS * MT * MAC_THREADS;
   Tw* twe = reinterpret_cast<Tw*>(cbuf + (size_t)MT * A2 * MAC_CHS);
@@ -983,7 +1214,7 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
   using Tw = uint2;
   constexpr int A2 = 2 * SG, NCH = MT * A2;
   static_assert(NCH <= 2 * WS_HALF / 16, "the dense round B keeps <= 2 tasks per INTT thread");
-  extern __shared__ __align__(128) unsigned char smraw[];
+  extern __shared__ __align__(128) unsigned char smraw_ws[];
   const int N = 1 << c.log_n, L = c.L, G = pl.G, S = pl.S;
   const int j = blockIdx.y;
   const int sgi = blockIdx.x % n_sg, et = blockIdx.x / n_sg;
@@ -994,7 +1225,7 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
   const uint32_t row_bytes = MAC_THREADS * sizeof(W);
   // shared memory: [G][2SG][256] X^ tile, [NS][MT][256] weight ring, [2][NCH][MAC_CHS] output
   // chunks, [256] e-tile twiddles, 2 NS + 1 + 4 mbarriers
-  W* xs = reinterpret_cast<W*>(smraw);
+  W* xs = reinterpret_cast<W*>(smraw_ws);
   W* ring = xs + (size_t)G * A2 * MAC_THREADS;
   W* cbuf0 = ring + (size_t)NS * MT * MAC_THREADS;
   Tw* twe = reinterpret_cast<Tw*>(cbuf0 + 2 * (size_t)NCH * MAC_CHS);
@@ -1156,7 +1387,7 @@ __global__ void __launch_bounds__(FUSED_THREADS + 32, 2)
   using W = uint32_t;
   using Tw = uint2;
   constexpr int LOGN = 12, N = 1 << LOGN, A2 = 2 * SG, NP = MT * A2, SW = smem_words<LOGN>();
-  extern __shared__ __align__(1024) unsigned char smraw[];
+  extern __shared__ __align__(1024) unsigned char smraw_fused[];
   const int L = (int)c.L, G = (int)pl.G, S = (int)pl.S;
   const int j = blockIdx.y;
   const int sgi = blockIdx.x % n_sg, mb = (blockIdx.x / n_sg) * MT;
@@ -1164,7 +1395,7 @@ __global__ void __launch_bounds__(FUSED_THREADS + 32, 2)
   const int n_gc = (G + GC - 1) / GC, total = (N / FUSED_THREADS) * n_gc;
   const int stage_words = GC * (A2 + MT) * FUSED_THREADS;
   // shared memory: [NP][SW] output polys (padded layout), [NS][stage] ring, 2 NS mbarriers
-  W* obuf = reinterpret_cast<W*>(smraw);
+  W* obuf = reinterpret_cast<W*>(smraw_fused);
   W* ring = obuf + NP * SW;
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)NS * stage_words);
   uint64_t* empty = full + NS;
@@ -1710,6 +1941,8 @@ void read_tune(int device, Tune* t) {
   t->num_sms = sms;
   t->no_pdl = env_int("SECN_NO_PDL", 0);
   t->ntt_np2_min = env_int("SECN_NTT_NP2_MIN", 2 * sms * 6);
+  t->ntt_tma = env_int("SECN_NTT_TMA", 1);
+  t->ntt_tma_min = env_int("SECN_NTT_TMA_MIN", 0);
   t->tail1 = env_int("SECN_TAIL1", 0);
   t->mac_kb = env_int("SECN_MAC_KB", 110);
   t->mac_xamort = env_int("SECN_MAC_XAMORT", 1);
@@ -1785,10 +2018,58 @@ static cudaError_t ntt_inv_np(const DevConsts& c, void* polys, size_t n_polys, c
   return cudaGetLastError();
 }
 
+static bool encode_tmap(CUtensorMap* m, int wb, int rank, const void* base, const cuuint64_t* dims,
+                        const cuuint64_t* strides_bytes, const cuuint32_t* box, bool swizzle128 = false);
+
+// the TMA-staged engine (k_ntt_tma): polys [n_polys][L][N] viewed as (128-byte row, row, limb,
+// poly); persistent grid of L x per_limb CTAs (ntt_tma_minb per SM)
+template <class A, int LOGN, bool INV>
+static cudaError_t ntt_tma(const DevConsts& c, const void* in, void* out, size_t n_polys, cudaStream_t s) {
+  using W = typename A::W;
+  constexpr int N = 1 << LOGN, NP = ntt_tma_np<A, LOGN>();
+  constexpr int RW = 128 / (int)sizeof(W), ROWS = N / RW, BR = ROWS < 256 ? ROWS : 256;
+  const size_t pmax = (size_t)1 << 30;  // polys per launch (32-bit TMA coordinates)
+  for (size_t p0 = 0; p0 < n_polys; p0 += pmax) {
+    const size_t np = n_polys - p0 < pmax ? n_polys - p0 : pmax;
+    const size_t off = p0 * c.L * N;
+    CUtensorMap tm;
+    const cuuint64_t d[4] = {(cuuint64_t)RW, (cuuint64_t)ROWS, c.L, np};
+    const cuuint64_t st[3] = {128, (cuuint64_t)N * sizeof(W), (cuuint64_t)c.L * N * sizeof(W)};
+    const cuuint32_t box[4] = {(cuuint32_t)RW, (cuuint32_t)BR, 1, 1};
+    if (!encode_tmap(&tm, (int)sizeof(W), 4, static_cast<const W*>(in) + off, d, st, box, true))
+      return cudaErrorInvalidValue;
+    const size_t items = (np + NP - 1) / NP;
+    size_t per_limb = (size_t)ntt_tma_minb<A, LOGN>() * c.tune.num_sms / c.L;
+    per_limb = per_limb < 1 ? 1 : per_limb > items ? items : per_limb;
+    cudaError_t e = launch_pdl(c, k_ntt_tma<A, LOGN, INV>, dim3((unsigned)(per_limb * c.L)), dim3(N / 16),
+                               ntt_tma_smem<A, LOGN>(), s, tm, static_cast<W*>(out) + off, c, (uint32_t)np);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaGetLastError();
+}
+
+// Which plain calls take the TMA-staged engine (SECN_NTT_TMA: 0 never, 1 this rule, 2 always):
+// the shapes where it measured faster on the C5 sweep (profiles/r02t_*): every inverse except
+// 32-bit N = 4096 with an even poly count (the two-poly one-CTA-per-poly kernel runs at 4 CTAs
+// per SM there and is 2% faster), 32-bit N = 4096 with an odd count (where the old kernels fall
+// back to one poly per CTA: 0.33 -> 0.42 of HBM forward), and both directions at 32-bit
+// N = 2^14 and 64-bit N = 2^13.
+template <class A, int LOGN, bool INV>
+static bool use_ntt_tma(const DevConsts& c, size_t n_polys, size_t P) {
+  if (c.tune.ntt_tma == 0 || P < (size_t)c.tune.ntt_tma_min) return false;
+  if (c.tune.ntt_tma == 2) return true;
+  constexpr bool w32 = sizeof(typename A::W) == 4;
+  if (w32 && LOGN == 12) return n_polys % 2 == 1;
+  if (w32 && LOGN == 14) return true;
+  if (!w32 && LOGN == 13) return true;
+  return INV;
+}
+
 template <class A, int LOGN>
 static cudaError_t ntt_fwd_t(const DevConsts& c, const void* in, void* out, size_t P, const uint64_t* x0,
                              cudaStream_t s) {
   const size_t n_polys = P / c.L;
+  if (x0 == nullptr && use_ntt_tma<A, LOGN, false>(c, n_polys, P)) return ntt_tma<A, LOGN, false>(c, in, out, n_polys, s);
   if constexpr (sizeof(typename A::W) == 4 && LOGN == 12)
     if (n_polys % 2 == 0 && P >= (size_t)c.tune.ntt_np2_min) return ntt_fwd_np<A, LOGN, 2>(c, in, out, n_polys, x0, s);
   return ntt_fwd_np<A, LOGN, 1>(c, in, out, n_polys, x0, s);
@@ -1797,6 +2078,7 @@ static cudaError_t ntt_fwd_t(const DevConsts& c, const void* in, void* out, size
 template <class A, int LOGN>
 static cudaError_t ntt_inv_t(const DevConsts& c, void* polys, size_t P, cudaStream_t s) {
   const size_t n_polys = P / c.L;
+  if (use_ntt_tma<A, LOGN, true>(c, n_polys, P)) return ntt_tma<A, LOGN, true>(c, polys, polys, n_polys, s);
   if constexpr (sizeof(typename A::W) == 4 && LOGN == 12)
     if (n_polys % 2 == 0 && P >= (size_t)c.tune.ntt_np2_min) return ntt_inv_np<A, LOGN, 2>(c, polys, n_polys, s);
   return ntt_inv_np<A, LOGN, 1>(c, polys, n_polys, s);
@@ -1940,13 +2222,13 @@ static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
 }
 
 static bool encode_tmap(CUtensorMap* m, int wb, int rank, const void* base, const cuuint64_t* dims,
-                        const cuuint64_t* strides_bytes, const cuuint32_t* box) {
+                        const cuuint64_t* strides_bytes, const cuuint32_t* box, bool swizzle128) {
   auto enc = tmap_encoder();
   if (!enc) return false;
   const cuuint32_t estr[4] = {1, 1, 1, 1};
   return enc(m, wb == 4 ? CU_TENSOR_MAP_DATA_TYPE_UINT32 : CU_TENSOR_MAP_DATA_TYPE_UINT64, rank,
              const_cast<void*>(base), dims, strides_bytes, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -2115,6 +2397,8 @@ cudaError_t init_device(uint32_t word_bits) {
     chk(optin(k_ntt_fwd<A, 12, 1>, b)), chk(optin(k_ntt_fwd<A, 13, 1>, b));
     chk(optin(k_ntt_inv<A, 12, 1>, b)), chk(optin(k_ntt_inv<A, 13, 1>, b));
     chk(optin(k_ntt_inv_tail<A, 12>, b)), chk(optin(k_ntt_inv_tail<A, 13>, b)), chk(optin(k_ntt_inv_tail<A, 14>, b));
+    chk(optin(k_ntt_tma<A, 12, false>, b)), chk(optin(k_ntt_tma<A, 12, true>, b));
+    chk(optin(k_ntt_tma<A, 13, false>, b)), chk(optin(k_ntt_tma<A, 13, true>, b));
     chk(optin(k_ntt_fwd_cl<A, 13>, b)), chk(optin(k_ntt_inv_cl<A, 13>, b));
     chk(optin(k_ntt_fwd_cl<A, 14>, b)), chk(optin(k_ntt_inv_cl<A, 14>, b));
     chk(optin(k_mac<uint64_t, 1, 4>, b)), chk(optin(k_mac<uint64_t, 2, 2>, b));
@@ -2126,6 +2410,9 @@ cudaError_t init_device(uint32_t word_bits) {
     chk(optin(k_ntt_inv<A, 12, 1>, b)), chk(optin(k_ntt_inv<A, 12, 2>, b));
     chk(optin(k_ntt_inv<A, 13, 1>, b)), chk(optin(k_ntt_inv<A, 14, 1>, b));
     chk(optin(k_ntt_inv_tail<A, 12>, b)), chk(optin(k_ntt_inv_tail<A, 13>, b)), chk(optin(k_ntt_inv_tail<A, 14>, b));
+    chk(optin(k_ntt_tma<A, 12, false>, b)), chk(optin(k_ntt_tma<A, 12, true>, b));
+    chk(optin(k_ntt_tma<A, 13, false>, b)), chk(optin(k_ntt_tma<A, 13, true>, b));
+    chk(optin(k_ntt_tma<A, 14, false>, b)), chk(optin(k_ntt_tma<A, 14, true>, b));
     chk(optin(k_ntt_fwd_cl<A, 14>, b)), chk(optin(k_ntt_inv_cl<A, 14>, b));
     chk(optin(k_mac<uint32_t, 1, 16>, b)), chk(optin(k_mac<uint32_t, 2, 8>, b));
     chk(optin(k_mac<uint32_t, 3, 5>, b)), chk(optin(k_mac<uint32_t, 4, 3>, b));

@@ -1,6 +1,6 @@
 """One forward and one inverse NTT call per ring degree of the C5 sweep (32-bit limbs, 4 sweep
 primes, ~256 MiB per call) between cudaProfilerStart/Stop, for an ncu capture of the NTT engine.
-Usage: python tools/sweep_profile.py [word_bits] [MiB]"""
+Usage: python tools/sweep_profile.py [word_bits] [MiB] [log_n,...]"""
 import sys
 from pathlib import Path
 
@@ -18,7 +18,8 @@ P = {64: (0xFFFFFFFFFFC0001, 0xFFFFFFFFF840001, 0xFFFFFFFFF6A0001, 0xFFFFFFFFF5A
      32: (0x7E90001, 0x7E00001, 0x7DD0001, 0x7D70001)}[wb]
 L = 4 if wb == 32 else 2
 jobs = []
-for logn in (12, 13, 14, 15):
+logns = tuple(int(v) for v in sys.argv[3].split(",")) if len(sys.argv) > 3 else (12, 13, 14, 15)
+for logn in logns:
     ctx = Context(0, log_n=logn, primes=P[:L], word_bits=wb)
     n_polys = (mib << 20) // ((1 << logn) * (wb // 8) * L)
     t = ctx.empty(n_polys, L, 1 << logn)
