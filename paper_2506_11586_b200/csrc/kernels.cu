@@ -1831,6 +1831,15 @@ __global__ void k_mask_draw(uint64_t* __restrict__ r, MaskGen g, size_t n_pairs,
 // per limb-coefficient) instead of reading and encoding r (8 bytes per coefficient, per limb).
 // wait_first: a standalone call (secn_mask_encode), whose r may come from the preceding kernel,
 // waits for it before reading; chained after the forward NTT it waits only at the end.
+// A thread owns MASK_COEFS consecutive coefficients of one output ciphertext (two Philox draws):
+// the per-limb constants are loaded once per 4 coefficients and each limb is one 16-byte
+// (32-bit words) store. y0 is written by the thread that holds the designated coefficient, from
+// the value it already drew (the designation inverted: d = e - O = ii Ww + jj, ii < dh, jj < dw;
+// the division by Ww by a multiply-shift that is exact for d < 2^12 <= 2^24 / Ww).
+constexpr int MASK_COEFS = 4;
+
+__device__ __forceinline__ uint32_t div_small(uint32_t d, uint32_t magic) { return (uint32_t)(((uint64_t)d * magic) >> 24); }
+
 template <class A>
 __global__ void __launch_bounds__(256) k_mask_encode(typename A::W* __restrict__ em, uint64_t* __restrict__ y0,
                                                      const uint64_t* __restrict__ r, MaskGen g,
@@ -1842,55 +1851,67 @@ __global__ void __launch_bounds__(256) k_mask_encode(typename A::W* __restrict__
   if (wait_first) pdl_wait();
   const uint32_t N = 1u << c.log_n, L = c.L;
   const uint64_t tm = (1ull << c.t_bits) - 1, thalf = 1ull << (c.t_bits - 1);
-  const auto mask_pair = [&](uint32_t ct, uint32_t pe, uint64_t& v0, uint64_t& v1) {
-    if (r != nullptr) {
-      const ulonglong2 rr = reinterpret_cast<const ulonglong2*>(r + (size_t)ct * N)[pe];
-      v0 = rr.x, v1 = rr.y;
-    } else {
-      const uint4 w = philox4x32_10(make_uint4(pe, g.ct0 + ct, g.stream, 0u), (uint32_t)g.seed, (uint32_t)(g.seed >> 32));
-      v0 = (((uint64_t)w.y << 32) | w.x) & tm, v1 = (((uint64_t)w.w << 32) | w.z) & tm;
-    }
-  };
-  // grid (pairs / 256, active cts): one coefficient pair per thread, the ct uniform per CTA
-  const uint32_t pe = blockIdx.x * blockDim.x + threadIdx.x;
-  if (blockIdx.y < n_act && pe < (N >> 1)) {
+  // grid (coefficients / (256 MASK_COEFS), active cts): the ct uniform per CTA
+  const uint32_t e0 = (blockIdx.x * blockDim.x + threadIdx.x) * MASK_COEFS;
+  if (blockIdx.y < n_act && e0 < N) {
     const uint32_t ct = slice_ct(pl, blockIdx.y);
-    uint64_t v0, v1;
-    mask_pair(ct, pe, v0, v1);
-    const uint64_t rho0 = (c.qmt * v0) & tm, rho1 = (c.qmt * v1) & tm;
-    const uint32_t up0 = rho0 >= thalf, up1 = rho1 >= thalf;
+    uint64_t v[MASK_COEFS];
+    if (r != nullptr) {
+#pragma unroll
+      for (int h = 0; h < MASK_COEFS / 2; ++h) {
+        const ulonglong2 rr = reinterpret_cast<const ulonglong2*>(r + (size_t)ct * N + e0)[h];
+        v[2 * h] = rr.x, v[2 * h + 1] = rr.y;
+      }
+    } else {
+#pragma unroll
+      for (int h = 0; h < MASK_COEFS / 2; ++h) {
+        const uint4 w = philox4x32_10(make_uint4((e0 >> 1) + h, g.ct0 + ct, g.stream, 0u), (uint32_t)g.seed,
+                                      (uint32_t)(g.seed >> 32));
+        v[2 * h] = (((uint64_t)w.y << 32) | w.x) & tm, v[2 * h + 1] = (((uint64_t)w.w << 32) | w.z) & tm;
+      }
+    }
+    uint64_t rho[MASK_COEFS];
+    uint32_t up[MASK_COEFS];
+#pragma unroll
+    for (int i = 0; i < MASK_COEFS; ++i) rho[i] = (c.qmt * v[i]) & tm, up[i] = rho[i] >= thalf;
 #pragma unroll
     for (uint32_t j = 0; j < SECN_MAX_LIMBS; ++j) {
       if (j >= L) break;
       const EncK ek(c, (int)j);
-      W* dst = em + ((size_t)ct * L + j) * N + 2 * pe;
-      const W e0 = enc_limb<A>(rho0, up0, ek), e1 = enc_limb<A>(rho1, up1, ek);
-      if constexpr (sizeof(W) == 4)
-        *reinterpret_cast<uint2*>(dst) = make_uint2(e0, e1);
-      else
-        *reinterpret_cast<ulonglong2*>(dst) = make_ulonglong2(e0, e1);
-    }
-  }
-  if (y0 != nullptr) {  // A8 at the designated outputs of the call's output ciphertexts
-    const size_t total = pl.kind == 1 ? (size_t)pl.no : (size_t)pl.M * pl.OH * pl.OW;
-    const size_t stride = (size_t)gridDim.x * gridDim.y * blockDim.x;
-    for (size_t idx = ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
-         idx += stride) {
-      uint32_t ct, e;
-      if (pl.kind == 1) {  // fc: y[m nob + d] at coefficient d nib + nib - 1 of output ct m
-        ct = (uint32_t)(idx / pl.nob), e = (uint32_t)(idx % pl.nob) * pl.nib + pl.nib - 1;
+      W* dst = em + ((size_t)ct * L + j) * N + e0;
+      W e[MASK_COEFS];
+#pragma unroll
+      for (int i = 0; i < MASK_COEFS; ++i) e[i] = enc_limb<A>(rho[i], up[i], ek);
+      if constexpr (sizeof(W) == 4) {
+        *reinterpret_cast<uint4*>(dst) = make_uint4(e[0], e[1], e[2], e[3]);
       } else {
-        const uint32_t ox = idx % pl.OW, oy = (idx / pl.OW) % pl.OH, m = (uint32_t)(idx / ((size_t)pl.OW * pl.OH));
-        const uint32_t py = oy * pl.sh, px = ox * pl.sh;
-        const uint32_t bh = py / (pl.Hw - pl.kh + 1), ii = py % (pl.Hw - pl.kh + 1);
-        const uint32_t bw = px / (pl.Ww - pl.kw + 1), jj = px % (pl.Ww - pl.kw + 1);
-        const uint32_t s = bh * pl.nbw + bw;
-        if (s < pl.s0 || s >= pl.s0 + pl.sn) continue;  // another call's spatial slice
-        ct = m * pl.S + s, e = pl.O + ii * pl.Ww + jj;
+        reinterpret_cast<ulonglong2*>(dst)[0] = make_ulonglong2(e[0], e[1]);
+        reinterpret_cast<ulonglong2*>(dst)[1] = make_ulonglong2(e[2], e[3]);
       }
-      uint64_t v0, v1;
-      mask_pair(ct, e >> 1, v0, v1);
-      y0[idx] = (tm + 1 - ((e & 1) ? v1 : v0)) & tm;
+    }
+    if (y0 != nullptr) {  // A8: this thread's designated coefficients (at most MASK_COEFS)
+      if (pl.kind == 1) {  // fc: output row m nob + d at coefficient d nib + nib - 1 of output ct m
+#pragma unroll
+        for (int i = 0; i < MASK_COEFS; ++i) {
+          const uint32_t e = e0 + i, d = (e + 1) / pl.nib - 1;
+          if ((e + 1) % pl.nib == 0 && d < pl.nob && ct * pl.nob + d < pl.no)
+            y0[(size_t)ct * pl.nob + d] = (tm + 1 - v[i]) & tm;
+        }
+      } else if (e0 + MASK_COEFS > pl.O) {
+        const uint32_t dh = pl.Hw - pl.kh + 1, dw = pl.Ww - pl.kw + 1;
+        const uint32_t m = ct / pl.S, sidx = ct % pl.S, bh = sidx / pl.nbw, bw = sidx - bh * pl.nbw;
+        const uint32_t magic = ((1u << 24) + pl.Ww - 1) / pl.Ww;
+#pragma unroll
+        for (int i = 0; i < MASK_COEFS; ++i) {
+          const uint32_t e = e0 + i;
+          if (e < pl.O) continue;
+          const uint32_t d = e - pl.O, ii = div_small(d, magic), jj = d - ii * pl.Ww;
+          if (ii >= dh || jj >= dw) continue;
+          const uint32_t py = bh * dh + ii, px = bw * dw + jj, oy = py / pl.sh, ox = px / pl.sh;
+          if (oy * pl.sh != py || ox * pl.sh != px || oy >= pl.OH || ox >= pl.OW) continue;
+          y0[((size_t)m * pl.OH + oy) * pl.OW + ox] = (tm + 1 - v[i]) & tm;
+        }
+      }
     }
   }
   if (!wait_first) pdl_wait();
@@ -2574,7 +2595,7 @@ cudaError_t launch_mask_encode(const DevConsts& c, const PlanDev& p, size_t n_ac
                                void* em, uint64_t* y0, cudaStream_t s, bool chained) {
   if (n_act == 0) return cudaSuccess;
   if (n_act > 65535) return cudaErrorInvalidValue;  // grid.y
-  const dim3 grid((unsigned)(((1u << (c.log_n - 1)) + 255) / 256), (unsigned)n_act);
+  const dim3 grid((unsigned)(((1u << c.log_n) / MASK_COEFS + 255) / 256), (unsigned)n_act);
   if (c.word_bits == 64)
     return launch_pdl(c, k_mask_encode<Arith64>, grid, dim3(256), 0, s, static_cast<uint64_t*>(em), y0, r, g, c, p,
                       (uint32_t)n_act, chained ? 0 : 1);

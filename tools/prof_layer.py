@@ -1,5 +1,6 @@
 """Runs one layer of the hot path a few times (for ncu captures of single kernels).
-Usage: python tools/prof_layer.py [layer_name] [net] [reps] [word_bits] [mode: full|lwe]"""
+Usage: python tools/prof_layer.py [layer_name] [net] [reps] [word_bits] [mode: full|lwe|em]
+(em: the bench step's path -- secn_mask_encode from the generator, then secn[32]_he_conv2d_em)"""
 import sys
 from pathlib import Path
 
@@ -9,7 +10,7 @@ import numpy as np
 import torch
 
 import __graft_entry__
-from paper_2506_11586_b200 import Context
+from paper_2506_11586_b200 import Context, MaskGen
 from workloads import inputs, layers
 
 name = sys.argv[1] if len(sys.argv) > 1 else "conv10"
@@ -35,8 +36,14 @@ ws = torch.empty(ctx.workspace_bytes(plan) // 8, dtype=torch.int64, device=dev)
 y0 = torch.empty((plan.M, plan.OH, plan.OW), dtype=torch.int64, device=dev)
 
 
+em = ctx.empty(plan.M * plan.S, ctx.L, ctx.n)
+
+
 def call():
-    if mode == "lwe":
+    if mode == "em":
+        ctx.mask_encode(plan, gen=MaskGen(seed=77, stream=1, ct0=0), out=em, y0=y0)
+        ctx.he_conv2d_em(plan, ct, w, em, x0=x0, out=out, workspace=ws)
+    elif mode == "lwe":
         ctx.he_conv2d_lwe(plan, ct, w, ctx.L // 2, x0=x0, r=r, y0=y0)
     else:
         ctx.he_conv2d(plan, ct, w, x0=x0, r=r, out=out, workspace=ws, y0=y0)
