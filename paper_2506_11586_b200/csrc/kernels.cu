@@ -549,8 +549,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((1 << LOGH) / 16, 1)
   const typename A::Tw w13 = th[1];
   const typename A::Tw ninv = Tab<A>::pair(c.ninv[j], c.ninv_p[j]);
   const typename A::Tw wl = Tab<A>::pair(c.wlast[j], c.wlast_p[j]);
+  // twiddles loaded at their use would avoid the 24-byte spill of 64-bit words at 2 x 2^14 points,
+  // but measured slower there (0.145 -> 0.142 of HBM): gathered in registers for every word size
+  constexpr bool tight = false;
   typename A::Tw tws[15];
-  gs_twiddles<A, LOGH, 0>(tws, th);
+  if constexpr (!tight) gs_twiddles<A, LOGH, 0>(tws, th);
   pdl_wait();  // the polys may come from the preceding kernel
   W* buf = polys + pl * N + h * NH;
   W x[1][16];
@@ -558,13 +561,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((1 << LOGH) / 16, 1)
     const W* src[1] = {buf};
     round_gload<R0, W, 1>(x, src);
   }
-  gs_compute<A, LOGH, 0, 1>(x, tws, q, qb, one, w13);
-  round_store<R0, W, 1, LOGH>(x, sm);
-  gs_rounds_smem_but_last<A, LOGH, R0::K, 1>(sm, th, q, qb, one, w13);
-  gs_twiddles<A, LOGH, LL>(tws, th);
-  __syncthreads();
-  round_load<RL, W, 1, LOGH>(x, sm);
-  gs_compute<A, LOGH, LL, 1>(x, tws, q, qb, one, w13);
+  if constexpr (tight) {
+    gs_compute_ld<A, LOGH, 0, 1>(x, th, q, qb, one, w13);
+    round_store<R0, W, 1, LOGH>(x, sm);
+    gs_rounds_smem_but_last_ld<A, LOGH, R0::K, 1>(sm, th, q, qb, one, w13);
+    __syncthreads();
+    round_load<RL, W, 1, LOGH>(x, sm);
+    gs_compute_ld<A, LOGH, LL, 1>(x, th, q, qb, one, w13);
+  } else {
+    gs_compute<A, LOGH, 0, 1>(x, tws, q, qb, one, w13);
+    round_store<R0, W, 1, LOGH>(x, sm);
+    gs_rounds_smem_but_last<A, LOGH, R0::K, 1>(sm, th, q, qb, one, w13);
+    gs_twiddles<A, LOGH, LL>(tws, th);
+    __syncthreads();
+    round_load<RL, W, 1, LOGH>(x, sm);
+    gs_compute<A, LOGH, LL, 1>(x, tws, q, qb, one, w13);
+  }
   __syncthreads();  // every thread has read its last-round inputs before they are overwritten
   round_store<RL, W, 1, LOGH>(x, sm);
   cluster_arrive();
@@ -654,25 +666,37 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, sizeof(typename A::W) == 4 &
 #pragma unroll
       for (int i = 0; i < RL::GK; ++i) em[k * RL::GK + i] = enc_mod<A>(__ldg(&rs[RL::addr(k, i)]), ek);
   };
-  if (mask && r_early) load_mask();
+  // 64-bit words at N = 2^14 (1024 threads, 64 registers): twiddles loaded at their use and the
+  // mask after the transform, so the 16 words per thread are the only long-lived registers
+  constexpr bool tight = sizeof(W) == 8 && LOGN >= 14;
+  if (mask && r_early && !tight) load_mask();
   typename A::Tw tws[15];
-  gs_twiddles<A, LOGN, LS>(tws, tw);
+  if constexpr (!tight) gs_twiddles<A, LOGN, LS>(tws, tw);
   pdl_wait();  // the polys are produced by the preceding kernel (the MAC)
-  if (mask && !r_early) load_mask();
+  if (mask && !r_early && !tight) load_mask();
   W* buf = polys + (pi * c.L + j) * N;
   W x[1][16];
 #pragma unroll
   for (int k = 0; k < RS::NT; ++k)
 #pragma unroll
     for (int i = 0; i < RS::GK; ++i) x[0][k * RS::GK + i] = buf[RS::addr(k, i)];
-  gs_compute<A, LOGN, LS, 1>(x, tws, q, qb, ninv, wl);
-  if constexpr (LL != LS) {  // N > 4096: the remaining levels go through shared memory
+  if constexpr (tight) {
+    gs_compute_ld<A, LOGN, LS, 1>(x, tw, q, qb, ninv, wl);
     round_store<RS, W, 1, LOGN>(x, sm);
-    gs_rounds_smem_but_last<A, LOGN, LS + RS::K, 1>(sm, tw, q, qb, ninv, wl);
-    gs_twiddles<A, LOGN, LL>(tws, tw);
+    gs_rounds_smem_but_last_ld<A, LOGN, LS + RS::K, 1>(sm, tw, q, qb, ninv, wl);
     __syncthreads();
     round_load<RL, W, 1, LOGN>(x, sm);
-    gs_compute<A, LOGN, LL, 1>(x, tws, q, qb, ninv, wl);
+    gs_compute_ld<A, LOGN, LL, 1>(x, tw, q, qb, ninv, wl);
+  } else {
+    gs_compute<A, LOGN, LS, 1>(x, tws, q, qb, ninv, wl);
+    if constexpr (LL != LS) {  // N > 4096: the remaining levels go through shared memory
+      round_store<RS, W, 1, LOGN>(x, sm);
+      gs_rounds_smem_but_last<A, LOGN, LS + RS::K, 1>(sm, tw, q, qb, ninv, wl);
+      gs_twiddles<A, LOGN, LL>(tws, tw);
+      __syncthreads();
+      round_load<RL, W, 1, LOGN>(x, sm);
+      gs_compute<A, LOGN, LL, 1>(x, tws, q, qb, ninv, wl);
+    }
   }
   pdl_trigger();
 #pragma unroll
@@ -681,7 +705,11 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, sizeof(typename A::W) == 4 &
     for (int i = 0; i < RL::GK; ++i) {
       W v = A::canon_gs(x[0][k * RL::GK + i], q);
       if (mask) {
-        v += em[k * RL::GK + i];
+        if constexpr (tight)  // the mask word loaded (and encoded) at its use
+          v += emb != nullptr ? emb[(((pi >> 1) + ct0) * c.L + j) * N + RL::addr(k, i)]
+                              : enc_mod<A>(__ldg(&r[(pi >> 1) * N + RL::addr(k, i)]), EncK(c, j));
+        else
+          v += em[k * RL::GK + i];
         v = v >= q ? v - q : v;
       }
       buf[RL::addr(k, i)] = v;
@@ -1060,7 +1088,7 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
             mbar_arrive_expect_tx(xbar, G * A2 * row_bytes);
             tma_load_4d(xs, &tmx, e0, j, 2 * s0, 0, xbar);
           }
-          if (!first) mbar_wait(&empty[st], ph ^ 1);
+          if (!first) mbar_wait_sleep(&empty[st], ph ^ 1);
           // weights: box (256 coefficients, row g*L + j, MT output channels from mb)
           mbar_arrive_expect_tx(&full[st], MT * row_bytes);
           if (c.word_bits & 0x400)  // debug: no L2 cache hint on the weight stream
@@ -1095,7 +1123,7 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
   const uint32_t qn = (uint32_t)c.qneg_inv32[j];
   const uint32_t r32 = (uint32_t)c.r32[j], r32p = (uint32_t)c.r32_p[j], onep32 = (uint32_t)(onep >> 32);
   PROBE0(1);
-  mbar_wait(xbar, 0);
+  mbar_wait_sleep(xbar, 0);
   PROBE0(2);
   int st = 0;
   uint32_t ph = 0;
@@ -1262,7 +1290,7 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
             mbar_arrive_expect_tx(xbar, G * A2 * row_bytes);
             tma_load_4d(xs, &tmx, e0, j, 2 * s0, 0, xbar);
           }
-          if (!first) mbar_wait(&empty[st], ph ^ 1);
+          if (!first) mbar_wait_sleep(&empty[st], ph ^ 1);
           mbar_arrive_expect_tx(&full[st], MT * row_bytes);
           tma_load_3d_hint(ring + (size_t)st * MT * MAC_THREADS, &tmw, e0, g * L + j, mb, &full[st], evict_first);
           ++issued;
@@ -1282,7 +1310,7 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
   if (tid < WS_HALF) {  // ---- MAC warps: coefficients e0 + tid and e0 + tid + 128 ----
     const uint32_t qn = (uint32_t)c.qneg_inv32[j];
     const uint32_t r32 = (uint32_t)c.r32[j], r32p = (uint32_t)c.r32_p[j], onep32 = (uint32_t)(c.one_p[j] >> 32);
-    mbar_wait(xbar, 0);
+    mbar_wait_sleep(xbar, 0);
     int st = 0;
     uint32_t ph = 0;
     int nb = 0;
@@ -1312,7 +1340,7 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
         if (++st == NS) st = 0, ph ^= 1;
       }
       const int b = nb & 1;
-      if (nb >= 2) mbar_wait(&cempty[b], ((nb >> 1) - 1) & 1);  // the INTT warps are done with buffer b
+      if (nb >= 2) mbar_wait_sleep(&cempty[b], ((nb >> 1) - 1) & 1);  // the INTT warps are done with buffer b
       W* cb = cbuf0 + (size_t)b * NCH * MAC_CHS;
 #pragma unroll
       for (int r = 0; r < MT; ++r)
@@ -1341,7 +1369,7 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
     for (int mb = m_begin; mb < m_end; mb += MT, ++nb) {
       const int b = nb & 1, rows = min(MT, m_end - mb);
       W* cb = cbuf0 + (size_t)b * NCH * MAC_CHS;
-      mbar_wait(&cfull[b], (nb >> 1) & 1);
+      mbar_wait_sleep(&cfull[b], (nb >> 1) & 1);
       mac_intt_levels_0_7<AR, true, WS_HALF, 2>(cb, twe, NCH, q, AR::bound(q), lt);  // dense chunks, proxy fence
       if (lt < 32) {  // INTT warp 0: lane ch stores chunk ch (one 1 KiB row segment per output limb-poly)
         const int r = lt / A2, a = lt % A2;
@@ -1434,7 +1462,7 @@ __global__ void __launch_bounds__(FUSED_THREADS + 32, 2)
       for (int k = 0; k < npre; ++k) load_x(k, k);
       for (int k = npre; k < total; ++k) {
         const int st = k % NS;
-        if (k >= NS) mbar_wait(&empty[st], ((k / NS) & 1) ^ 1);
+        if (k >= NS) mbar_wait_sleep(&empty[st], ((k / NS) & 1) ^ 1);
         mbar_arrive_expect_tx(&full[st], bytes);
         load_w(k, st);
         load_x(k, st);

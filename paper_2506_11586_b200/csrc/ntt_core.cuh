@@ -291,6 +291,68 @@ __device__ __forceinline__ void gs_rounds_smem_but_last(typename A::W* sm, const
   }
 }
 
+// The same levels with each butterfly group's twiddle loaded at its use instead of gathered into
+// registers first (15 pairs = 60 registers for 64-bit words): for kernels whose register budget
+// cannot hold them (64-bit words at N = 2^14, 1024 threads per CTA).
+template <class A, int LOGN, int L0, int NP>
+__device__ __forceinline__ void gs_compute_ld(typename A::W (&x)[NP][16], const typename A::Tw* __restrict__ tw,
+                                              typename A::W q, typename A::W qb, typename A::Tw ninv,
+                                              typename A::Tw wlast) {
+  using R = GsRound<LOGN, L0>;
+#pragma unroll
+  for (int p = 0; p < R::K; ++p) {
+    const int dist = 1 << p;
+    if (L0 + p == LOGN - 1) {
+#pragma unroll
+      for (int k = 0; k < R::NT; ++k)
+#pragma unroll
+        for (int i = 0; i < R::GK; ++i) {
+          if (i & dist) continue;
+#pragma unroll
+          for (int pp = 0; pp < NP; ++pp) {
+            const typename A::W u = x[pp][k * R::GK + i], v = x[pp][k * R::GK + i + dist];
+            x[pp][k * R::GK + i] = A::mul4(u + v, ninv, q);
+            x[pp][k * R::GK + i + dist] = A::mul4(u - v + qb, wlast, q);
+          }
+        }
+    } else {
+      const uint32_t h = (1u << LOGN) >> (L0 + p + 1);
+#pragma unroll
+      for (int k = 0; k < R::NT; ++k) {
+#pragma unroll
+        for (int gi = 0; gi < 8; ++gi) {
+          if (gi < (R::GK >> (p + 1))) {
+            const typename A::Tw w = tw[h + (R::blk(k) << (R::K - p - 1)) + gi];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              if (i < dist) {
+                const int a = k * R::GK + gi * (2 * dist) + i;
+#pragma unroll
+                for (int pp = 0; pp < NP; ++pp) A::gs(x[pp][a], x[pp][a + dist], w, q, qb);
+              }
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
+template <class A, int LOGN, int L0, int NP>
+__device__ __forceinline__ void gs_rounds_smem_but_last_ld(typename A::W* sm, const typename A::Tw* __restrict__ tw,
+                                                           typename A::W q, typename A::W qb, typename A::Tw ninv,
+                                                           typename A::Tw wlast) {
+  using R = GsRound<LOGN, L0>;
+  if constexpr (L0 + R::K < LOGN) {
+    __syncthreads();
+    typename A::W x[NP][16];
+    round_load<R, typename A::W, NP, LOGN>(x, sm);
+    gs_compute_ld<A, LOGN, L0, NP>(x, tw, q, qb, ninv, wlast);
+    round_store<R, typename A::W, NP, LOGN>(x, sm);
+    gs_rounds_smem_but_last_ld<A, LOGN, L0 + R::K, NP>(sm, tw, q, qb, ninv, wlast);
+  }
+}
+
 template <int LOGN, int L0 = 0>
 struct GsLast {
   static constexpr int value =
