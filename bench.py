@@ -553,12 +553,15 @@ def run_secn(args, word_bits, world, rank, local, dev, full):
     step_s = ms_per_step / 1e3
     if not full:
         del graph
+        stage_ms = stage_profile(ctx, st, K, dev)  # every rank runs the eager stage calls together
         if rank != 0:
             return None
         return {"dtype": f"u{ctx.word_bits}", "primes": [hex(q) for q in ctx.primes], "limbs": L,
                 "value": round(step_s, 7), "unit": "s", "ms_per_step": round(ms_per_step, 4),
                 "alg_bytes_per_step": alg_bytes, "hbm_frac": round(alg_bytes / step_s / 1e9 / hbm_peak, 4),
-                "clocks": clk.summary(), "timing": "CUDA events around CUDA-graph replays of the whole step"}
+                "clocks": clk.summary(), "timing": "CUDA events around CUDA-graph replays of the whole step",
+                "alu_roof": alu_roof(ctx, st, stage_ms, clk.summary()),
+                "stage_ms_eager": {k: round(v, 4) for k, v in zip(("fwd", "mac", "tail"), stage_ms)}}
 
     # ---- per-stage live timing (eager stage calls, launches pre-queued behind a sleep) ----
     stage_ms = stage_profile(ctx, st, K, dev)
@@ -608,6 +611,7 @@ def run_secn(args, word_bits, world, rank, local, dev, full):
                 "avg_launch_us": round(stage_ms[dom] / n_layers_active * 1e3, 2),
                 "stage_ms": {names[s]: round(stage_ms[s], 4) for s in range(3)},
                 "stage_GBps": {names[s]: round(sb[s] / (stage_ms[s] / 1e3) / 1e9, 1) for s in range(3)}}
+    roofline["alu_roof"] = alu_roof(ctx, st, stage_ms, clk.summary())
     # the whole step against its byte floors, and every kernel's pipes and stalls, from the committed
     # ncu capture of one step (tools/gpu_step_ncu.sh -> profiles/*_step_ncu.json)
     bytemin = sum(algorithmic_bytes(ctx.plan(d["lay"].C, d["lay"].H, d["lay"].W, d["lay"].M, d["lay"].k,
@@ -666,6 +670,35 @@ def run_secn(args, word_bits, world, rank, local, dev, full):
         frac = args.cpu_frac if args.cpu_frac is not None else default_cpu_frac(args.net)
         out["cpu_baseline"] = cpu_baseline(st, ctx, frac, dev, wbytes, args.seed, drawn)
     return out
+
+
+# Calibrated integer throughputs (ops per clock per SM; profiles/r01_calib_intpipe.txt, tools/calib):
+# a lazy modular butterfly and a 64x64 -> 128-bit multiply-accumulate for 64-bit words, an exact
+# 32-bit Shoup product for 32-bit words (one butterfly), IMAD.WIDE for a 32-bit MAC.
+CALIB = {64: {"bfly": 2.97, "mac": 3.69}, 32: {"bfly": 15.86, "mac": 27.95}}
+
+
+def alu_roof(ctx, st, stage_ms, clocks):
+    """Each stage's integer-ALU floor -- its modular butterflies and multiply-accumulates at the
+    calibrated rates on every SM at the sampled SM clock -- against its eager device time."""
+    L, n = ctx.L, ctx.n
+    logn = n.bit_length() - 1
+    rate = CALIB[ctx.word_bits]
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    hz = (clocks.get("sm_mhz") or clocks.get("sm_max_mhz") or 1965.0) * 1e6
+    bf = n // 2
+    fwd_b = sum(2 * d["pl"].G * d["pl"].S * L * bf * logn for d in st if d["mc"] > 0)
+    out_polys = sum(2 * d["pl"].M * d["pl"].S * L for d in st if d["mc"] > 0)
+    macs = sum(2 * d["pl"].M * d["pl"].G * d["pl"].S * L * n for d in st if d["mc"] > 0)
+    floor_ms = [fwd_b / (rate["bfly"] * sms * hz) * 1e3,
+                (macs / rate["mac"] + out_polys * bf * 8 / rate["bfly"]) / (sms * hz) * 1e3,
+                out_polys * bf * (logn - 8) / (rate["bfly"] * sms * hz) * 1e3]
+    return {"rates_per_clk_per_sm": rate, "source": "profiles/r01_calib_intpipe.txt (tools/calib/intbench.cu)",
+            "sm_clock_mhz": hz / 1e6, "sms": sms,
+            "stages": {k: {"floor_ms": round(f, 4), "measured_ms": round(m, 4), "frac": round(f / m, 3) if m else None}
+                       for k, f, m in zip(("fwd (A6 + A1 NTT)", "mac (A4 MAC + INTT levels 0-7)",
+                                           "tail (INTT levels 8.. + mask)"), floor_ms, stage_ms)},
+            "step_floor_ms": round(sum(floor_ms), 4)}
 
 
 def stage_profile(ctx, st, K, dev):

@@ -15,4 +15,4 @@ for s in wait long_scoreboard short_scoreboard math_pipe_throttle barrier membar
 done
 timeout 1200 ncu --profile-from-start off --clock-control none --metrics $M -f -o $O/step_$TAG python tools/step_profile.py squeezenet1_1 64 > $O/step_ncu_$TAG.log 2>&1
 echo "ncu rc=$?"
-python tools/ncu_step_summary.py $O/step_$TAG.ncu-rep > $O/step_summary_$TAG.txt 2>&1; cat $O/step_summary_$TAG.txt
+python tools/ncu_step_summary.py $O/step_$TAG.ncu-rep $O/${TAG}_step_ncu_w64.json > $O/step_summary_$TAG.txt 2>&1; cat $O/step_summary_$TAG.txt
