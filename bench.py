@@ -77,6 +77,9 @@ def parse():
                          "(default): every layer's at the start of the step, on a side stream beside the layer chain "
                          "(1.209 ms, profiles/r02h_*); lookahead: the next group's while a group runs (1.253 ms); "
                          "inline: inside the layer call, secn32_he_conv2d_gen (1.232 ms)")
+    ap.add_argument("--priority", choices=["chain", "same"], default="chain",
+                    help="chain: the layer chain's streams at high priority, the mask side stream at the "
+                         "default (the scheduler prefers the latency-bound chain's CTAs); same: all default")
     ap.add_argument("--queries", type=int, default=1,
                     help="B > 1: the batched-queries line instead -- B independent inferences per step (the "
                          "north star's ciphertext batches), each on its own stream, weights shared; metric = "
@@ -451,7 +454,8 @@ def run_secn(args, word_bits, world, rank, local, dev, full):
     # everything else keeps network order (paper_2506_11586_b200/schedule.py)
     names = [d["lay"].name for d in st]
     groups = concurrent_groups(names) if args.overlap != "none" else [[i] for i in range(len(st))]
-    runner = StagedGroupRunner(groups, dev) if args.overlap == "staged" else GroupRunner(groups, dev)
+    hi = -1 if args.priority == "chain" else 0  # torch maps it to the device's highest priority
+    runner = StagedGroupRunner(groups, dev) if args.overlap == "staged" else GroupRunner(groups, dev, priority=hi)
 
     # device mask drawn + encoded apart from the layer call (it is input-independent): on a side
     # stream, ahead of the layer that adds it; the layer's stream waits for its event
@@ -507,7 +511,7 @@ def run_secn(args, word_bits, world, rank, local, dev, full):
         step_public()
     torch.cuda.synchronize()
     graph = torch.cuda.CUDAGraph()
-    cap = torch.cuda.Stream(dev)
+    cap = torch.cuda.Stream(dev, priority=hi)
     cap.wait_stream(torch.cuda.current_stream(dev))
     with torch.cuda.stream(cap):
         step_public()

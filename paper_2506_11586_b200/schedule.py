@@ -44,10 +44,10 @@ class GroupRunner:
     stream, the others on side streams forked from it and joined back before the next group.
     Works eagerly and under CUDA-graph capture (the fork/join become graph edges)."""
 
-    def __init__(self, groups: List[List[int]], device):
+    def __init__(self, groups: List[List[int]], device, priority: int = 0):
         self.groups = groups
         width = max((len(g) for g in groups), default=1)
-        self.side = [torch.cuda.Stream(device) for _ in range(width - 1)]
+        self.side = [torch.cuda.Stream(device, priority=priority) for _ in range(width - 1)]
 
     def __call__(self, fn: Callable[[int], None], before_group: Optional[Callable[[int], None]] = None) -> None:
         """before_group(k), if given, runs on the host before group k is issued (e.g. to issue side
