@@ -36,6 +36,8 @@
  *  - Ordering: a call may be scheduled, through programmatic dependent launch, while the
  *    preceding kernel on `stream` finishes; it reads nothing that kernel may have written before
  *    waiting for it, so inputs written by any earlier work on the stream are always seen.
+ *  - Tracing: every call that enqueues work opens an NVTX range named after the entry point
+ *    (nsys / ncu --nvtx group its kernels under it; a no-op when no tool is attached).
  */
 #ifndef SECN_H_
 #define SECN_H_
