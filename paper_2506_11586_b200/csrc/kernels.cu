@@ -243,9 +243,16 @@ template <class A, int LOGN>
 __host__ __device__ constexpr int ntt_tma_np() { return SECN_TMA_NP12 && sizeof(typename A::W) == 4 && LOGN == 12 ? 2 : 1; }
 template <class A, int LOGN>
 __host__ __device__ constexpr int ntt_tma_minb() { return LOGN == 12 ? (sizeof(typename A::W) == 4 ? SECN_TMA_MINB12 : 2) : LOGN == 13 && sizeof(typename A::W) == 4 ? 2 : 1; }
+#ifndef SECN_TMA_NBUF12
+#define SECN_TMA_NBUF12 2
+#endif
+// staging buffers: 2 (the next item lands while this one is transformed), or 1 (it is issued after
+// the last round has read the buffer, overlapping that round and the stores; more CTAs per SM)
+template <class A, int LOGN>
+__host__ __device__ constexpr int ntt_tma_nbuf() { return sizeof(typename A::W) == 4 && LOGN == 12 ? SECN_TMA_NBUF12 : 2; }
 template <class A, int LOGN>
 constexpr size_t ntt_tma_smem() {
-  return 1024 + 2 * (size_t)ntt_tma_np<A, LOGN>() * (1 << LOGN) * sizeof(typename A::W) + 16;
+  return 1024 + (size_t)ntt_tma_nbuf<A, LOGN>() * ntt_tma_np<A, LOGN>() * (1 << LOGN) * sizeof(typename A::W) + 16;
 }
 
 // round R's words of NP polys (poly pp at buf + pp N) <-> registers, in the swizzled layout
@@ -345,12 +352,12 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_tma_minb<A, LOGN>())
               uint32_t n_polys) {
   using W = typename A::W;
   using Tw = typename A::Tw;
-  constexpr int N = 1 << LOGN, NP = ntt_tma_np<A, LOGN>();
+  constexpr int N = 1 << LOGN, NP = ntt_tma_np<A, LOGN>(), NBUF = ntt_tma_nbuf<A, LOGN>();
   constexpr int RW = 128 / (int)sizeof(W), ROWS = N / RW, BR = ROWS < 256 ? ROWS : 256;
   static_assert(LOGN >= 12, "the first internal barrier is the one before round S0 = 4, and a later round exists");
   extern __shared__ __align__(1024) unsigned char smraw_tma[];
   W* bufs = reinterpret_cast<W*>(smraw_tma + ((1024 - (smem_u32(smraw_tma) & 1023)) & 1023));  // swizzle atoms
-  uint64_t* bar = reinterpret_cast<uint64_t*>(bufs + 2 * NP * N);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(bufs + NBUF * NP * N);
   const uint32_t L = c.L, j = blockIdx.x % L, per_limb = gridDim.x / L;
   const uint32_t n_items = (n_polys + NP - 1) / NP;
   const W q = (W)c.q[j], qb = A::bound(q);
@@ -375,11 +382,19 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_tma_minb<A, LOGN>())
   uint32_t it = blockIdx.x / L;
   if (threadIdx.x == 0 && it < n_items) issue(it, 0);
   for (uint32_t k = 0; it < n_items; it += per_limb, ++k) {
-    const int b = (int)(k & 1);
+    const int b = NBUF == 2 ? (int)(k & 1) : 0;
+    const uint32_t par = NBUF == 2 ? (k >> 1) & 1 : k & 1;
     W* buf = bufs + b * NP * N;
     const uint32_t nxt = it + per_limb;
     const auto at_first_barrier = [&] {
-      if (threadIdx.x == 0 && nxt < n_items) issue(nxt, b ^ 1);
+      if (NBUF == 2 && threadIdx.x == 0 && nxt < n_items) issue(nxt, b ^ 1);
+    };
+    const auto after_last_read = [&] {  // one buffer: every thread has read this item's words
+      if constexpr (NBUF == 1) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (threadIdx.x == 0 && nxt < n_items) issue(nxt, 0);
+      }
     };
     const uint32_t p0 = it * NP;
     W x[NP][16];
@@ -389,7 +404,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_tma_minb<A, LOGN>())
       constexpr int SL = CtLast<LOGN>::value;
       using RL = CtRound<LOGN, SL>;
       ct_twiddles<A, LOGN, 0>(tws, tw);
-      mbar_wait(&bar[b], (k >> 1) & 1);
+      mbar_wait(&bar[b], par);
       sw_load<R0, W, NP, N>(x, buf);
       ct_compute<A, LOGN, 0, NP>(x, tws, q, qb);
       sw_store<R0, W, NP, N>(x, buf);
@@ -397,6 +412,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_tma_minb<A, LOGN>())
       ct_twiddles<A, LOGN, SL>(tws, tw);
       __syncthreads();
       sw_load<RL, W, NP, N>(x, buf);
+      after_last_read();
       ct_compute<A, LOGN, SL, NP>(x, tws, q, qb);
 #pragma unroll
       for (int pp = 0; pp < NP; ++pp)
@@ -419,7 +435,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_tma_minb<A, LOGN>())
       constexpr int LL = GsLast<LOGN>::value;
       using RL = GsRound<LOGN, LL>;
       gs_twiddles<A, LOGN, 0>(tws, tw);
-      mbar_wait(&bar[b], (k >> 1) & 1);
+      mbar_wait(&bar[b], par);
       sw_load<R0, W, NP, N>(x, buf);
       gs_compute<A, LOGN, 0, NP>(x, tws, q, qb, ninv, wl);
       sw_store<R0, W, NP, N>(x, buf);
@@ -427,6 +443,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_tma_minb<A, LOGN>())
       gs_twiddles<A, LOGN, LL>(tws, tw);
       __syncthreads();
       sw_load<RL, W, NP, N>(x, buf);
+      after_last_read();
       gs_compute<A, LOGN, LL, NP>(x, tws, q, qb, ninv, wl);
 #pragma unroll
       for (int pp = 0; pp < NP; ++pp) {

@@ -7,6 +7,6 @@ cp paper_2506_11586_b200/libsecn.so /tmp/libsecn_default.so
 for v in variants/*.so; do
   n=$(basename $v .so)
   cp $v paper_2506_11586_b200/libsecn.so; touch paper_2506_11586_b200/libsecn.so
-  timeout 600 python bench.py --net ntt_sweep --steps 10 > gpurun_out/sweep_$n.json 2> gpurun_out/sweep_$n.err
+  timeout 600 env ${VARIANT_ENV:-} python bench.py --net ntt_sweep --steps 10 > gpurun_out/sweep_$n.json 2> gpurun_out/sweep_$n.err
 done
 cp /tmp/libsecn_default.so paper_2506_11586_b200/libsecn.so
