@@ -348,8 +348,8 @@ __device__ __forceinline__ void gs_rounds_sw(typename A::W* buf, const typename 
 
 template <class A, int LOGN, bool INV>
 __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_tma_minb<A, LOGN>())
-    k_ntt_tma(const __grid_constant__ CUtensorMap tm, typename A::W* out, const __grid_constant__ DevConsts c,
-              uint32_t n_polys) {
+    k_ntt_tma(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmo, typename A::W* out,
+              const __grid_constant__ DevConsts c, uint32_t n_polys) {
   using W = typename A::W;
   using Tw = typename A::Tw;
   constexpr int N = 1 << LOGN, NP = ntt_tma_np<A, LOGN>(), NBUF = ntt_tma_nbuf<A, LOGN>();
@@ -363,7 +363,11 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_tma_minb<A, LOGN>())
   const W q = (W)c.q[j], qb = A::bound(q);
   const Tw* tw = (INV ? Tab<A>::inv(c) : Tab<A>::fwd(c)) + (size_t)j * N;
   const Tw ninv = Tab<A>::pair(c.ninv[j], c.ninv_p[j]), wl = Tab<A>::pair(c.wlast[j], c.wlast_p[j]);
+  // forward: the last round's words go back in place and leave by TMA store (whole 128-byte rows;
+  // plain 16-byte stores of a thread's 16 contiguous words half-fill 32-byte sectors per instruction)
+  constexpr bool tstore = !INV && LOGN == 12;  // measured: the inverse's coalesced word stores are faster
   const auto issue = [&](uint32_t item, int b) {  // one thread: the item's NP polys (zero-filled past n_polys)
+    if constexpr (tstore) bulk_wait_read0();  // this buffer's TMA store (two items back) has read it
     mbar_arrive_expect_tx(&bar[b], (uint32_t)(NP * N * sizeof(W)));
 #pragma unroll
     for (int pp = 0; pp < NP; ++pp)
@@ -373,6 +377,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_tma_minb<A, LOGN>())
   };
   if (threadIdx.x == 0) {
     prefetch_tmap(&tm);
+    if constexpr (tstore) prefetch_tmap(&tmo);
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
     fence_mbar_init();
@@ -390,13 +395,28 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_tma_minb<A, LOGN>())
       if (NBUF == 2 && threadIdx.x == 0 && nxt < n_items) issue(nxt, b ^ 1);
     };
     const auto after_last_read = [&] {  // one buffer: every thread has read this item's words
-      if constexpr (NBUF == 1) {
+      if constexpr (NBUF == 1 && !tstore) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncthreads();
         if (threadIdx.x == 0 && nxt < n_items) issue(nxt, 0);
       }
     };
     const uint32_t p0 = it * NP;
+    const auto store_item = [&] {  // the item's words are back in place: one thread TMA-stores them
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+      if (threadIdx.x == 0) {  // rows past n_polys (the odd tail's missing poly) are clipped
+#pragma unroll
+        for (int pp = 0; pp < NP; ++pp)
+#pragma unroll
+          for (int kk = 0; kk < ROWS / BR; ++kk)
+            tma_store_4d(&tmo, buf + pp * N + kk * BR * RW, 0, kk * BR, (int)j, (int)(p0 + pp));
+        bulk_commit();
+        if constexpr (NBUF == 1) {
+          if (nxt < n_items) issue(nxt, 0);
+        }
+      }
+    };
     W x[NP][16];
     Tw tws[15];
     if constexpr (!INV) {
@@ -418,17 +438,22 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_tma_minb<A, LOGN>())
       for (int pp = 0; pp < NP; ++pp)
 #pragma unroll
         for (int i = 0; i < 16; ++i) x[pp][i] = A::canon_ct(x[pp][i], q);
-      W* dst[NP];
+      if constexpr (tstore) {
+        sw_store<RL, W, NP, N>(x, buf);  // each thread rewrites the words it read: no hazard
+        store_item();
+      } else {
+        W* dst[NP];
 #pragma unroll
-      for (int pp = 0; pp < NP; ++pp) dst[pp] = out + ((size_t)(p0 + pp) * L + j) * N;
-      if (NP == 1 || p0 + NP <= n_polys) {
-        round_gstore<RL, W, NP>(x, dst);
-      } else {  // odd tail: the item's second poly does not exist
-        W y[1][16];
+        for (int pp = 0; pp < NP; ++pp) dst[pp] = out + ((size_t)(p0 + pp) * L + j) * N;
+        if (NP == 1 || p0 + NP <= n_polys) {
+          round_gstore<RL, W, NP>(x, dst);
+        } else {  // odd tail: the item's second poly does not exist
+          W y[1][16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) y[0][i] = x[0][i];
-        W* d1[1] = {dst[0]};
-        round_gstore<RL, W, 1>(y, d1);
+          for (int i = 0; i < 16; ++i) y[0][i] = x[0][i];
+          W* d1[1] = {dst[0]};
+          round_gstore<RL, W, 1>(y, d1);
+        }
       }
     } else {
       using R0 = GsRound<LOGN, 0>;
@@ -445,17 +470,27 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_tma_minb<A, LOGN>())
       sw_load<RL, W, NP, N>(x, buf);
       after_last_read();
       gs_compute<A, LOGN, LL, NP>(x, tws, q, qb, ninv, wl);
+      if constexpr (tstore) {
 #pragma unroll
-      for (int pp = 0; pp < NP; ++pp) {
-        if (pp > 0 && p0 + pp >= n_polys) break;
-        W* o = out + ((size_t)(p0 + pp) * L + j) * N;
+        for (int pp = 0; pp < NP; ++pp)
 #pragma unroll
-        for (int kk = 0; kk < RL::NT; ++kk)
+          for (int i = 0; i < 16; ++i) x[pp][i] = A::canon_gs(x[pp][i], q);
+        sw_store<RL, W, NP, N>(x, buf);
+        store_item();
+      } else {
 #pragma unroll
-          for (int i = 0; i < RL::GK; ++i) o[RL::addr(kk, i)] = A::canon_gs(x[pp][kk * RL::GK + i], q);
+        for (int pp = 0; pp < NP; ++pp) {
+          if (pp > 0 && p0 + pp >= n_polys) break;
+          W* o = out + ((size_t)(p0 + pp) * L + j) * N;
+#pragma unroll
+          for (int kk = 0; kk < RL::NT; ++kk)
+#pragma unroll
+            for (int i = 0; i < RL::GK; ++i) o[RL::addr(kk, i)] = A::canon_gs(x[pp][kk * RL::GK + i], q);
+        }
       }
     }
   }
+  if (tstore && threadIdx.x == 0) bulk_wait0();  // the stores are performed before the grid completes
   pdl_trigger();
 }
 
@@ -2102,30 +2137,32 @@ static cudaError_t ntt_tma(const DevConsts& c, const void* in, void* out, size_t
     const cuuint64_t d[4] = {(cuuint64_t)RW, (cuuint64_t)ROWS, c.L, np};
     const cuuint64_t st[3] = {128, (cuuint64_t)N * sizeof(W), (cuuint64_t)c.L * N * sizeof(W)};
     const cuuint32_t box[4] = {(cuuint32_t)RW, (cuuint32_t)BR, 1, 1};
-    if (!encode_tmap(&tm, (int)sizeof(W), 4, static_cast<const W*>(in) + off, d, st, box, true))
+    CUtensorMap tmo;  // the output (in place: the same tensor)
+    if (!encode_tmap(&tm, (int)sizeof(W), 4, static_cast<const W*>(in) + off, d, st, box, true) ||
+        !encode_tmap(&tmo, (int)sizeof(W), 4, static_cast<W*>(out) + off, d, st, box, true))
       return cudaErrorInvalidValue;
     const size_t items = (np + NP - 1) / NP;
     size_t per_limb = (size_t)ntt_tma_minb<A, LOGN>() * c.tune.num_sms / c.L;
     per_limb = per_limb < 1 ? 1 : per_limb > items ? items : per_limb;
     cudaError_t e = launch_pdl(c, k_ntt_tma<A, LOGN, INV>, dim3((unsigned)(per_limb * c.L)), dim3(N / 16),
-                               ntt_tma_smem<A, LOGN>(), s, tm, static_cast<W*>(out) + off, c, (uint32_t)np);
+                               ntt_tma_smem<A, LOGN>(), s, tm, tmo, static_cast<W*>(out) + off, c, (uint32_t)np);
     if (e != cudaSuccess) return e;
   }
   return cudaGetLastError();
 }
 
 // Which plain calls take the TMA-staged engine (SECN_NTT_TMA: 0 never, 1 this rule, 2 always):
-// the shapes where it measured faster on the C5 sweep (profiles/r02t_*): every inverse except
-// 32-bit N = 4096 with an even poly count (the two-poly one-CTA-per-poly kernel runs at 4 CTAs
-// per SM there and is 2% faster), 32-bit N = 4096 with an odd count (where the old kernels fall
-// back to one poly per CTA: 0.33 -> 0.42 of HBM forward), and both directions at 32-bit
-// N = 2^14 and 64-bit N = 2^13.
+// the shapes where it measured faster on the C5 sweep (profiles/r02t_*, r02z_*): the 32-bit
+// N = 4096 forward (with its TMA store: 0.50 of HBM against 0.485), every inverse except 32-bit
+// N = 4096 with an even poly count (the two-poly one-CTA-per-poly kernel at 4 CTAs per SM is 2%
+// faster there), the 32-bit N = 4096 inverse with an odd count (where the old kernels fall back
+// to one poly per CTA: 0.38 -> 0.49), and both directions at 32-bit N = 2^14 and 64-bit 2^13.
 template <class A, int LOGN, bool INV>
 static bool use_ntt_tma(const DevConsts& c, size_t n_polys, size_t P) {
   if (c.tune.ntt_tma == 0 || P < (size_t)c.tune.ntt_tma_min) return false;
   if (c.tune.ntt_tma == 2) return true;
   constexpr bool w32 = sizeof(typename A::W) == 4;
-  if (w32 && LOGN == 12) return n_polys % 2 == 1;
+  if (w32 && LOGN == 12) return !INV || n_polys % 2 == 1;
   if (w32 && LOGN == 14) return true;
   if (!w32 && LOGN == 13) return true;
   return INV;

@@ -87,6 +87,15 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
+// Tiled TMA store through a tensor map (cp.async.bulk.tensor shared -> global, bulk async-group
+// completion): the box is read from shared memory in box order; out-of-bounds elements are not
+// written. Commit / wait with bulk_commit / bulk_wait_read0 / bulk_wait0.
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void* src, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(map),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+               : "memory");
+}
+
 // Same as tma_load_3d with an L2 cache-policy hint (e.g. evict_first for a stream read once).
 __device__ __forceinline__ void tma_load_3d_hint(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
                                                  uint64_t* bar, uint64_t policy) {
