@@ -134,6 +134,45 @@ __device__ __forceinline__ void round_gstore(const W (&x)[NP][16], W* const (&ds
   }
 }
 
+// The dense swizzled layout of TMA's 128-byte swizzle: word e of a poly at stage_swz(e) (the
+// 16-byte chunk index XOR the 128-byte row index mod 8, relative to a 1024-byte-aligned base;
+// with a 16-byte-aligned base the bank pattern is the same up to a rotation).
+template <class W>
+__host__ __device__ __forceinline__ constexpr uint32_t stage_swz(uint32_t e) {
+  constexpr int lw = sizeof(W) == 4 ? 2 : 3;  // log2 of the word size
+  return e ^ (((e >> (7 - lw)) & 7) << (4 - lw));
+}
+
+// The last CT round's words (contiguous tasks) to global memory through shared memory, so that
+// each warp store instruction covers 512 contiguous bytes instead of 16 bytes every 64 (which
+// half-fills every 32-byte sector per instruction). sm holds >= NP * N words and every thread
+// has finished reading it (the caller's barrier).
+template <class R, class W, int NP, int LOGN>
+__device__ __forceinline__ void round_gstore_coalesced(const W (&x)[NP][16], W* sm, W* const (&dst)[NP]) {
+  constexpr int N = 1 << LOGN, VW = 16 / (int)sizeof(W);
+  static_assert(R::logD == 0 && R::GK >= VW, "contiguous tasks of whole 16-byte chunks");
+#pragma unroll
+  for (int k = 0; k < R::NT; ++k)
+#pragma unroll
+    for (int pp = 0; pp < NP; ++pp)
+#pragma unroll
+      for (int v = 0; v < R::GK / VW; ++v) {
+        uint4 t;
+        W* tv = reinterpret_cast<W*>(&t);
+#pragma unroll
+        for (int u = 0; u < VW; ++u) tv[u] = x[pp][k * R::GK + v * VW + u];
+        *reinterpret_cast<uint4*>(sm + pp * N + stage_swz<W>(R::addr(k, v * VW))) = t;
+      }
+  __syncthreads();
+#pragma unroll
+  for (int pp = 0; pp < NP; ++pp)
+#pragma unroll
+    for (int v = 0; v < 16 / VW; ++v) {
+      const uint32_t ch = threadIdx.x + v * R::T;  // 16-byte chunk: 16 per thread per poly
+      *reinterpret_cast<uint4*>(dst[pp] + ch * VW) = *reinterpret_cast<const uint4*>(sm + pp * N + stage_swz<W>(ch * VW));
+    }
+}
+
 // ------------------------------------------------------------------------------------------
 // Cooley-Tukey: stages S0 .. S0+K-1 (stage s: 2^s groups, group i uses psi^brv(2^s + i)).
 // Twiddles of one round are gathered into registers before the round's barrier so their load
