@@ -10,6 +10,8 @@ M="gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,smsp__inst_
 M="$M,smsp__issue_active.avg.pct_of_peak_sustained_active,sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"
 M="$M,sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active,sm__warps_active.avg.pct_of_peak_sustained_active"
 M="$M,dram__throughput.avg.pct_of_peak_sustained_elapsed"
+M="$M,smsp__sass_average_data_bytes_per_sector_mem_global_op_ld.pct,smsp__sass_average_data_bytes_per_sector_mem_global_op_st.pct"
+M="$M,l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum,l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum"
 for s in wait long_scoreboard short_scoreboard math_pipe_throttle barrier membar not_selected selected dispatch_stall no_instruction mio_throttle lg_throttle sleeping branch_resolving drain tex_throttle imc_miss misc; do
   M="$M,smsp__average_warps_issue_stalled_${s}_per_issue_active.ratio"
 done

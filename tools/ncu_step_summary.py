@@ -55,8 +55,12 @@ for r in data:
     f["inst"] += num(r, "smsp__inst_executed.sum")
     for m in ("smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
               "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
-              "dram__throughput.avg.pct_of_peak_sustained_elapsed"):
+              "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+              "smsp__sass_average_data_bytes_per_sector_mem_global_op_ld.pct",
+              "smsp__sass_average_data_bytes_per_sector_mem_global_op_st.pct"):
         f[m] += num(r, m) * t
+    for m in ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum"):
+        f[m] += num(r, m)
     for h in stall_cols:
         f[h] += num(r, h) * t
     f["t"] += t
@@ -77,6 +81,14 @@ for k, f in fam.items():
           f"{f['sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active'] / t:6.1f} "
           f"{f['sm__warps_active.avg.pct_of_peak_sustained_active'] / t:7.1f} "
           f"{f['dram__throughput.avg.pct_of_peak_sustained_elapsed'] / t:6.1f}  {sts}")
+if any(f["smsp__sass_average_data_bytes_per_sector_mem_global_op_ld.pct"] for f in fam.values()):
+    print("global-access sector efficiency (bytes used per sector fetched / stored, %) and shared-memory bank conflicts:")
+    for k, f in fam.items():
+        t = f["t"] or 1
+        print(f"  {k[:40]:40s} ld {f['smsp__sass_average_data_bytes_per_sector_mem_global_op_ld.pct'] / t:6.1f}  "
+              f"st {f['smsp__sass_average_data_bytes_per_sector_mem_global_op_st.pct'] / t:6.1f}  "
+              f"conflicts ld {f['l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum'] / 1e6:7.2f} M  "
+              f"st {f['l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum'] / 1e6:7.2f} M")
 print(f"step DRAM traffic (read + write, all kernels): {tot_dram / 1e9:.3f} GB"
       + (f"; algorithmic bytes {alg / 1e9:.3f} GB; traffic / algorithmic = {tot_dram / alg:.3f}" if alg else ""))
 
