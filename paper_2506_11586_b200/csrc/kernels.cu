@@ -107,6 +107,18 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN, NP>(
   const W q = (W)c.q[j], qb = A::bound(q);
   const typename A::Tw* tw = Tab<A>::fwd(c) + (size_t)j * N;
   const EncK ek(c, j);
+  {  // the CTA's input polys (and share words) to L2 while the preceding kernel finishes: a prefetch
+     // never reads stale data (L2 is the point of coherence), and the loads after the wait hit L2
+     // (step -0.5%, profiles/r02zc_*)
+    constexpr int LW = 128 / (int)sizeof(W);  // words per 128-byte line
+#pragma unroll
+    for (int pp = 0; pp < NP; ++pp) {
+      const size_t pi = grp * NP + pp;
+      if (threadIdx.x < N / LW) prefetch_l2(in + (pi * c.L + j) * N + threadIdx.x * LW);
+      if (x0 != nullptr && (pi & 1) && threadIdx.x < N / 16)
+        for (int u = threadIdx.x; u < N / 16; u += N / 16) prefetch_l2(x0 + (pi >> 1) * N + u * 16);
+    }
+  }
   typename A::Tw tws[15];
   ct_twiddles<A, LOGN, 0>(tws, tw);
   pdl_wait();  // inputs may come from the preceding kernel
@@ -814,6 +826,10 @@ __global__ void __launch_bounds__(256, 4)
     }
   };
   if (mask && MS == 1) load_mask();
+  // the encoded mask to L2 now (an input of the call, never written by the MAC), loaded after the
+  // transform: step -0.75% (profiles/r02zc_*)
+  if (MS == 2 && mask && (threadIdx.x & 31) < 16)
+    prefetch_l2(emb + ((ct + ct0) * c.L + j) * N + (threadIdx.x & ~31u) + RS::T * (threadIdx.x & 31));
   typename A::Tw tws[15];
   gs_twiddles<A, LOGN, LS>(tws, tw);
   pdl_wait();  // the polys are produced by the preceding kernel (the MAC)
