@@ -841,7 +841,7 @@ __global__ void __launch_bounds__(256, 4)
 #pragma unroll
     for (int i = 0; i < 16; ++i) x[pp][i] = buf[pp][RS::addr(0, i)];
   gs_compute<A, LOGN, LS, 2>(x, tws, q, qb, ninv, wl);
-  pdl_trigger();
+  pdl_trigger();  // (right after the wait instead: the next layer's forward NTT CTAs take the SMs early, +3.6%)
   if (mask && MS == 2) load_mask();  // 4-byte words: loaded here, their latency overlaps the a stores
 #pragma unroll
   for (int i = 0; i < 16; ++i) buf[0][RS::addr(0, i)] = A::canon_gs(x[0][i], q);
