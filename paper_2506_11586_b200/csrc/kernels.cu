@@ -125,7 +125,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN, NP>(
   // dependents (the mask draw, the MAC) may launch now: none reads this kernel's output before its
   // own dependency wait, and the MAC's pre-wait weight loads are never produced here (the two-poly
   // variant of the large batches triggers at its end: the early trigger costs it registers)
-  if constexpr (NP == 1) pdl_trigger();
+  if constexpr (NP == 1) pdl_trigger();  // (at the end instead: 1.171 -> 1.197 ms, profiles/r02zd_*)
   W x[NP][16];
 #pragma unroll
   for (int pp = 0; pp < NP; ++pp) {
