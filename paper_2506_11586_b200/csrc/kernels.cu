@@ -1268,11 +1268,12 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
       // output limb-poly), asynchronous to the next m-block's MAC
       mac_intt_levels_0_7<AR, true>(cbuf, twe, MT * A2, (W)q, AR::bound((W)q));
       PROBE0(4);
-      if (tid < 32) {  // warp 0: lane ch issues chunk ch's store (MT x 2SG <= 32)
+      if (tid < 32) {  // warp 0: lane ch issues chunk ch's store (MT x 2SG <= 32); L2 evict_last: the
+                       // tail reads Y^ right back (step 1.1724 -> 1.1612 ms, profiles/r02zh_*)
         const int r = tid / A2, a = tid % A2;
         if (tid < MT * A2 && r < rows && a < 2 * ns)
-          bulk_store_s2g(y + ((((size_t)(mb + r) * S + s0 + (a >> 1)) * 2 + (a & 1)) * L + j) * N + e0,
-                         cbuf + tid * MAC_CHS, MAC_THREADS * sizeof(W));
+          bulk_store_s2g_hint(y + ((((size_t)(mb + r) * S + s0 + (a >> 1)) * 2 + (a & 1)) * L + j) * N + e0,
+                              cbuf + tid * MAC_CHS, MAC_THREADS * sizeof(W), policy_evict_last());
         bulk_commit();
       }
     } else {
@@ -1445,8 +1446,8 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
       if (lt < 32) {  // INTT warp 0: lane ch stores chunk ch (one 1 KiB row segment per output limb-poly)
         const int r = lt / A2, a = lt % A2;
         if (lt < NCH && r < rows && a < 2 * ns)
-          bulk_store_s2g(y + ((((size_t)(mb + r) * S + s0 + (a >> 1)) * 2 + (a & 1)) * L + j) * N + e0,
-                         cb + lt * MAC_CHS, MAC_THREADS * sizeof(W));
+          bulk_store_s2g_hint(y + ((((size_t)(mb + r) * S + s0 + (a >> 1)) * 2 + (a & 1)) * L + j) * N + e0,
+                              cb + lt * MAC_CHS, MAC_THREADS * sizeof(W), policy_evict_last());
         bulk_commit();
         // the previous m-block's stores (the other buffer) have read their chunks: hand it back
         if (nb >= 1) {
