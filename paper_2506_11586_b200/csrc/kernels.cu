@@ -1279,13 +1279,14 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, 2)
     } else {
       mac_intt_levels_0_7<AR>(cbuf, twe, MT * A2, (W)q, AR::bound((W)q));
       PROBE0(4);
+      const uint64_t evl = policy_evict_last();  // the tail reads Y^ right back
 #pragma unroll
       for (int r = 0; r < MT; ++r)
 #pragma unroll
         for (int a = 0; a < A2; ++a)
           if (r < rows && a < 2 * ns)
-            y[((((size_t)(mb + r) * S + s0 + (a >> 1)) * 2 + (a & 1)) * L + j) * N + e] =
-                cbuf[(r * A2 + a) * MAC_CHS + phys(tid)];
+            st_hint(&y[((((size_t)(mb + r) * S + s0 + (a >> 1)) * 2 + (a & 1)) * L + j) * N + e],
+                    cbuf[(r * A2 + a) * MAC_CHS + phys(tid)], evl);
     }
   }
   if (sizeof(W) == 4 && tid < 32) bulk_wait_read0();  // shared memory stays valid until the stores have read it
