@@ -577,7 +577,7 @@ def run_secn(args, word_bits, world, rank, local, dev, full):
     online = None if args.no_online else run_online(ctx, st, K, args.warmup, dev, world, runner)
 
     # ---- f2: extracted outputs (modulus switch + designated coefficients) ----
-    lwe = run_lwe(ctx, st, K, args.warmup, dev, world, runner, drawn=drawn)
+    lwe = run_lwe(ctx, st, K, args.warmup, dev, world, runner, drawn=drawn, priority=hi)
     if not args.no_e2e:  # the same step end to end, sending back only the extracted outputs
         lwe["e2e"] = run_e2e(ctx, st, K, dev, share_buf, world, runner, lwe_keep=ctx.L // 2, drawn=drawn)
 
@@ -753,13 +753,13 @@ def ctx_lib():
     return secn.lib()
 
 
-def graph_ms(fn, K, warmup, dev, world):
+def graph_ms(fn, K, warmup, dev, world, priority=0):
     """Captures fn() in a CUDA graph and returns the device ms per replay (max over ranks)."""
     for _ in range(max(warmup, 3)):
         fn()
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
-    cap = torch.cuda.Stream(dev)
+    cap = torch.cuda.Stream(dev, priority=priority)
     cap.wait_stream(torch.cuda.current_stream(dev))
     with torch.cuda.graph(g, stream=cap):
         fn()
@@ -817,27 +817,45 @@ def run_online(ctx, st, K, warmup, dev, world, runner):
             "layer_overlap": _leg_overlap(runner)}
 
 
-def run_lwe(ctx, st, K, warmup, dev, world, runner, drawn=False):
+def run_lwe(ctx, st, K, warmup, dev, world, runner, drawn=False, priority=0):
     """the same step returning extracted outputs (secn32_he_conv2d_lwe: the
     INTT tail switches every output ct to half of its limbs and keeps the b component only at the
-    designated coefficients), i.e. what Cheetah's server sends back."""
+    designated coefficients), i.e. what Cheetah's server sends back. With the drawn mask, the same
+    schedule as the main step: every layer's mask encoded at the start on a side stream, each layer
+    through secn32_he_conv2d_lwe_em after its mask's event."""
     keep = ctx.L // 2
     for d in st:
         if d["mc"] > 0:
             pl = d["pl"]
-            wsf = ctx_lib().secn_he_conv2d_lwe_gen_workspace if drawn else ctx_lib().secn_he_conv2d_lwe_workspace
-            d["ws_lwe"] = torch.empty((int(wsf(ctx._h, ctypes.byref(pl))) + 7) // 8, dtype=torch.int64, device=dev)
+            d["ws_lwe"] = torch.empty((int(ctx_lib().secn_he_conv2d_lwe_workspace(ctx._h, ctypes.byref(pl))) + 7) // 8,
+                                      dtype=torch.int64, device=dev)
+            d["lwe_out"] = (ctx.empty(d["mc"] * pl.S, keep, ctx.n), ctx.empty(d["mc"], pl.OH, pl.OW, keep))
+    mstream = torch.cuda.Stream(dev)
+    mev = [torch.cuda.Event() for _ in st]
 
     def layer_lwe(i):
         d = st[i]
         if d["mc"] > 0 and drawn:
-            d["lwe_out"] = ctx.he_conv2d_lwe_gen(d["pl"], d["ct"], d["w"], keep, d["gen"], x0=d["x0"], y0=d["y0"],
-                                                 workspace=d["ws_lwe"])
+            torch.cuda.current_stream().wait_event(mev[i])
+            ctx.he_conv2d_lwe_em(d["pl"], d["ct"], d["w"], keep, d["em"], x0=d["x0"], workspace=d["ws_lwe"],
+                                 out=d["lwe_out"])
         elif d["mc"] > 0:
-            d["lwe_out"] = ctx.he_conv2d_lwe(d["pl"], d["ct"], d["w"], keep, x0=d["x0"], r=d["r"], y0=d["y0"],
-                                             workspace=d["ws_lwe"])
+            ctx.he_conv2d_lwe(d["pl"], d["ct"], d["w"], keep, x0=d["x0"], r=d["r"], y0=d["y0"],
+                              workspace=d["ws_lwe"], out=d["lwe_out"])
 
-    ms = graph_ms(lambda: runner(layer_lwe), K, warmup, dev, world)
+    def step():
+        if drawn:
+            mstream.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(mstream):
+                for i, d in enumerate(st):
+                    if d["mc"] > 0:
+                        ctx.mask_encode(d["pl"], gen=d["gen"], out=d["em"], y0=d["y0"])
+                        mev[i].record(mstream)
+        runner(layer_lwe)
+        if drawn:
+            torch.cuda.current_stream().wait_stream(mstream)
+
+    ms = graph_ms(step, K, warmup, dev, world, priority=priority)
     out_bytes = sum(a.numel() * a.element_size() + b.numel() * b.element_size()
                     for a, b in (d["lwe_out"] for d in st if d["mc"] > 0))
     full_bytes = sum(d["out"].numel() * d["out"].element_size() for d in st if d["mc"] > 0)
@@ -847,8 +865,8 @@ def run_lwe(ctx, st, K, warmup, dev, world, runner, drawn=False):
     torch.cuda.empty_cache()
     return {"value": round(ms / 1e3, 7), "unit": "s", "ms_per_step": round(ms, 4), "keep_limbs": keep,
             "output_bytes_per_step": out_bytes, "full_ct_output_bytes_per_step": full_bytes,
-            "path": ("secn32_he_conv2d_lwe_gen: share add + NTT, mask draw, MAC, INTT tail + mask + modulus switch + "
-                     "extraction" if drawn else
+            "path": ("secn_mask_encode ahead (drawn mask) + secn32_he_conv2d_lwe_em: share add + NTT, MAC, INTT tail + "
+                     "mask + modulus switch + extraction" if drawn else
                      "secn32_he_conv2d_lwe: share add + NTT, MAC, INTT tail + mask + modulus switch + extraction"),
             "layer_overlap": _leg_overlap(runner)}
 
