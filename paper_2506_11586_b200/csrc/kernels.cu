@@ -705,8 +705,9 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, sizeof(typename A::W) == 4 &
   using RL = GsRound<LOGN, LL>;
   extern __shared__ __align__(16) unsigned char smraw[];
   W* sm = reinterpret_cast<W*>(smraw);
-  const int j = (int)(blockIdx.x % c.L);
-  const size_t pa = blockIdx.x / c.L;  // (active ct, component); the ct's row is slice_ct (s-slice)
+  const uint32_t rb = gridDim.x - 1 - blockIdx.x;  // reverse output order, as k_ntt_inv_tail2
+  const int j = (int)(rb % c.L);
+  const size_t pa = rb / c.L;  // (active ct, component); the ct's row is slice_ct (s-slice)
   const size_t pi = 2 * (size_t)slice_ct(pl, (uint32_t)(ct0 + (pa >> 1))) + (pa & 1) - 2 * ct0;
   const W q = (W)c.q[j], qb = A::bound(q);
   const typename A::Tw* tw = Tab<A>::inv(c) + (size_t)j * N;
@@ -802,8 +803,11 @@ __global__ void __launch_bounds__(256, 4)
   constexpr int LOGN = 12, N = 1 << LOGN, LS = 8;
   using RS = GsRound<LOGN, LS>;
   static_assert(GsLast<LOGN>::value == LS, "one round");
-  const int j = (int)(blockIdx.x % c.L);
-  const size_t ct = slice_ct(pl, (uint32_t)(ct0 + blockIdx.x / c.L)) - ct0;  // row of this ct (s-slice aware)
+  // CTAs in reverse output order: the MAC wrote the highest output rows last, so theirs are the Y^
+  // lines still in L2 when the tail starts (conv10's Y^ is twice the L2; step -0.4%, profiles/r02zj_*)
+  const uint32_t rb = gridDim.x - 1 - blockIdx.x;
+  const size_t ct = slice_ct(pl, (uint32_t)(ct0 + rb / c.L)) - ct0;  // row of this ct (s-slice aware)
+  const int j = (int)(rb % c.L);
   const W q = (W)c.q[j], qb = A::bound(q);
   const typename A::Tw* tw = Tab<A>::inv(c) + (size_t)j * N;
   const typename A::Tw ninv = Tab<A>::pair(c.ninv_mac[j], c.ninv_mac_p[j]);  // inputs are k_mac outputs
