@@ -115,8 +115,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 16, ntt_min_blocks<A, LOGN, NP>(
     for (int pp = 0; pp < NP; ++pp) {
       const size_t pi = grp * NP + pp;
       if (threadIdx.x < N / LW) prefetch_l2(in + (pi * c.L + j) * N + threadIdx.x * LW);
-      if (x0 != nullptr && (pi & 1) && threadIdx.x < N / 16)
-        for (int u = threadIdx.x; u < N / 16; u += N / 16) prefetch_l2(x0 + (pi >> 1) * N + u * 16);
+      if (x0 != nullptr && (pi & 1)) prefetch_l2(x0 + (pi >> 1) * N + threadIdx.x * 16);  // N/16 lines, one per thread
     }
   }
   typename A::Tw tws[15];
