@@ -2398,8 +2398,8 @@ static cudaError_t mac_t(const DevConsts& c, const PlanDev& p, const void* xhat,
   // hide the INTT-level latency better; measured on the SqueezeNet fire layers)
   if (WS)  // the pipeline needs >= 2 m-blocks per CTA (its MAC of one overlaps the INTT of the last)
     best_nmr = best_nmr < (mblocks + 1) / 2 ? best_nmr : (mblocks + 1) / 2;
-  else if (p.G <= 4 || p.M <= 48)
-    best_nmr = mblocks;
+  else if ((p.G <= 4 && p.M < 256) || p.M <= 48)  // (G <= 4 with M >= 256: the wave-fill split,
+    best_nmr = mblocks;                               //  several m-blocks per CTA; profiles/r02zq_*)
   else if (xtile >= (size_t)MT * p.G * MAC_THREADS * sizeof(W) && c.tune.mac_xamort)
     // the X^ tile is at least one m-block of weights: a CTA takes >= 2 m-blocks so the tile load
     // is amortised (conv1 of SqueezeNet-1.1: 79 -> 69 us)
