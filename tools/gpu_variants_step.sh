@@ -7,7 +7,7 @@ cp paper_2506_11586_b200/libsecn.so /tmp/libsecn_default.so
 for v in variants/*.so; do
   n=$(basename $v .so)
   cp $v paper_2506_11586_b200/libsecn.so; touch paper_2506_11586_b200/libsecn.so
-  timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -k "ntt or tiny or shapes" > gpurun_out/pt_$n.log 2>&1
+  timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_mask.py -q -x -k "ntt or tiny or shapes or mask or gen" > gpurun_out/pt_$n.log 2>&1
   for i in 1 2; do
     timeout 600 python bench.py --no-sweep --no-cpu-baseline --no-online --no-e2e --batched-leg 0 > gpurun_out/step_${n}_$i.json 2> /dev/null
   done
