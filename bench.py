@@ -293,12 +293,27 @@ def run_batched(args, B, world, rank, local, dev):
             main.wait_stream(s)
 
     ms = graph_ms(step, args.steps, max(args.warmup, 3), dev, world)
+    # the B concurrent streams against one query at a time: queries 0 and B-1 re-run eagerly on
+    # one stream into fresh buffers must give the graph's words (ciphertexts and shares) exactly
+    torch.cuda.synchronize()
+    compared = mismatched = 0
+    for b in sorted({0, B - 1}):
+        for plan, w, qs in lay_state:
+            q = qs[b]
+            em, y0 = ctx.empty(plan.M * plan.S, L, n), torch.empty_like(q["y0"])
+            ctx.mask_encode(plan, gen=q["gen"], out=em, y0=y0)
+            out = ctx.he_conv2d_em(plan, q["ct"], w, em, x0=q["x0"], workspace=q["ws"])
+            torch.cuda.synchronize()
+            mismatched += int((out != q["out"]).sum().item()) + int((y0 != q["y0"]).sum().item())
+            compared += out.numel() + y0.numel()
     total = B * world
     alg = sum(algorithmic_bytes(plan, L, n, ctx.word_bits // 8, True) for plan, _, _ in lay_state) * B
     ctx.close()
     return {"queries_per_gpu": B, "value": round(total / (ms / 1e3), 1), "unit": "inferences/s",
             "ms_per_step": round(ms, 4), "latency_per_query_ms_upper": round(ms, 4),
             "hbm_frac": round(alg / (ms / 1e3) / 1e9 / peaks()[0], 4),
+            "graph_vs_eager": {"queries_checked": sorted({0, B - 1}), "words_compared": compared,
+                               "words_mismatched": mismatched},
             "path": "per query: secn_mask_encode (drawn masks) then secn32_he_conv2d_em for every layer, on the "
                     "query's own stream; B streams concurrently, weights shared"}
 
