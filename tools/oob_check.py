@@ -1,5 +1,8 @@
-"""Out-of-bounds write check: every layer's output and workspace live inside a larger buffer
-with canary guards; one network step (all 26 layers, serial) must leave every guard intact."""
+"""Out-of-bounds write check (compute-sanitizer is closed on this GPU pool): every layer's outputs,
+workspace, encoded mask and share live inside larger buffers with canary guards; one network step
+(all layers, serial) through secn32_he_conv2d (caller mask) and through secn_mask_encode +
+secn32_he_conv2d_em (drawn mask, the bench path), and the plain NTT / INTT calls on odd batches
+(the TMA-staged engine), must leave every guard intact."""
 import sys
 from pathlib import Path
 
@@ -9,7 +12,7 @@ import numpy as np
 import torch
 
 import __graft_entry__
-from paper_2506_11586_b200 import Context
+from paper_2506_11586_b200 import Context, MaskGen
 from workloads import inputs, layers
 
 __graft_entry__.build()
@@ -52,5 +55,33 @@ for lay in layers.network(sys.argv[1] if len(sys.argv) > 1 else "squeezenet1_1")
     lo = int((y0b[:GUARD] != CANARY).sum()); hi = int((y0b[GUARD + plan.M * plan.OH * plan.OW:] != CANARY).sum())
     if lo or hi:
         bad.append((lay.name, "y0", lo, hi))
+    # the bench path: drawn mask encoded into a guarded buffer, then the _em call
+    n_em = plan.M * plan.S * ctx.L * ctx.n
+    eb, em = guarded(n_em)
+    ob.fill_(CANARY)
+    wb.fill_(CANARY)
+    y0b.fill_(CANARY)
+    ctx.mask_encode(plan, gen=MaskGen(seed=5, stream=1, ct0=0), out=em.view(plan.M * plan.S, ctx.L, ctx.n), y0=y0)
+    ctx.he_conv2d_em(plan, ct, w, em.view(plan.M * plan.S, ctx.L, ctx.n), x0=x0,
+                     out=out.view(plan.M * plan.S, 2, ctx.L, ctx.n), workspace=ws.view(torch.int64))
+    torch.cuda.synchronize()
+    for name, b, n in (("out_em", ob, n_out), ("ws_em", wb, wsw), ("em", eb, n_em)):
+        lo = int((b[:GUARD] != CANARY).sum())
+        hi = int((b[GUARD + n:] != CANARY).sum())
+        if lo or hi:
+            bad.append((lay.name, name, lo, hi))
+    lo = int((y0b[:GUARD] != CANARY).sum()); hi = int((y0b[GUARD + plan.M * plan.OH * plan.OW:] != CANARY).sum())
+    if lo or hi:
+        bad.append((lay.name, "y0_em", lo, hi))
     print(lay.name, "ok" if not bad or bad[-1][0] != lay.name else bad[-1], flush=True)
+for n_polys in (1, 7, 301, 1777):  # plain NTT / INTT calls (odd batches take the TMA-staged engine)
+    nb, polys = guarded(n_polys * ctx.L * ctx.n)
+    polys.random_(0, min(ctx.primes))
+    ctx.ntt_fwd(polys.view(n_polys, ctx.L, ctx.n))
+    ctx.ntt_inv(polys.view(n_polys, ctx.L, ctx.n))
+    torch.cuda.synchronize()
+    lo = int((nb[:GUARD] != CANARY).sum()); hi = int((nb[GUARD + n_polys * ctx.L * ctx.n:] != CANARY).sum())
+    if lo or hi:
+        bad.append(("ntt", n_polys, lo, hi))
+    print("ntt", n_polys, "ok" if not (lo or hi) else (lo, hi), flush=True)
 print("guard violations:", bad)
