@@ -1794,8 +1794,10 @@ __global__ void __launch_bounds__(LWE_G * SECN_MAX_LIMBS)
   using RS = GsRound<LOGN, 8>;
   static_assert(RS::NT == 1 && RS::GK == 16, "one radix-16 task per thread");
   __shared__ W ys[ND][16][LWE_G];
-  const size_t ct = slice_ct(pl, (uint32_t)(blockIdx.x >> 2)), pi = 2 * ct + ((blockIdx.x >> 1) & 1);
-  const uint32_t o = (blockIdx.x & 1) * LWE_G + threadIdx.x % LWE_G;  // radix-16 task: coefficients o + 256 i
+  // CTAs in reverse output order, as the full-ciphertext tails: the Y^ rows the MAC wrote last are read first
+  const uint32_t rb = gridDim.x - 1 - blockIdx.x;
+  const size_t ct = slice_ct(pl, rb >> 2), pi = 2 * ct + ((rb >> 1) & 1);
+  const uint32_t o = (rb & 1) * LWE_G + threadIdx.x % LWE_G;  // radix-16 task: coefficients o + 256 i
   const int j = threadIdx.x / LWE_G;                                   // this group's limb
   const bool isb = pi & 1, mask = isb && (r != nullptr || emb != nullptr);
   const uint64_t* rs = isb && r != nullptr ? r + ct * N : nullptr;
